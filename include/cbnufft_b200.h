@@ -1,0 +1,155 @@
+/*
+ * cbnufft_b200 -- C ABI of the B200-native NUFFT cone-beam projector.
+ *
+ * The reference (`cbnufft`, /root/reference/pkg/src/cbnufft) is a pure-Python
+ * package with no FFI; its operator API is the set of module functions
+ * listed in SURVEY.md 8(b).  Each entry point below replaces one of them and
+ * cites the reference function it stands in for.  The Python package
+ * `paper_1605_05231_b200` binds these with ctypes (`_lib.py`) and re-exports
+ * the reference names and signatures; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Plain C types only.  Array arguments marked [device] are CUDA device
+ *    pointers (the Python layer passes torch tensor storage); [host] are host
+ *    pointers.  Complex arrays are interleaved float32 pairs (complex64).
+ *  - `stream` is a cudaStream_t passed as void*; every compute call is
+ *    stream-ordered and asynchronous unless documented otherwise.
+ *  - Return value: CBN_OK or an error status; cbn_last_error() gives a
+ *    thread-local message.  CBN_EINVAL maps to ValueError and CBN_ENONFINITE
+ *    to FloatingPointError in the Python layer (pipeline.py:144-145).
+ *  - Caller owns all input/output buffers; plan objects own their scratch
+ *    (cuFFT plans + workspace, tables, grids).  A plan must not be used from
+ *    two streams at once.
+ */
+#ifndef CBNUFFT_B200_H
+#define CBNUFFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBN_OK 0
+#define CBN_EINVAL 1
+#define CBN_ECUDA 2
+#define CBN_ENOMEM 3
+#define CBN_ENONFINITE 4
+#define CBN_ENCCL 5
+#define CBN_EUNSUPPORTED 6
+
+const char* cbn_last_error(void);
+int cbn_version(void);
+
+/* Kaiser-Bessel shape parameter of the reference (nufft.py:53-56). */
+double cbn_beatty_beta(int j, double alpha);
+
+/* ------------------------------------------------------------------ NUFFT
+ * Replaces plan_nufft / nufft_forward / nufft_adjoint (nufft.py:137-247).
+ */
+typedef struct cbn_nufft_s cbn_nufft;
+
+/* plan_nufft(dims, nodes, oversample_factor, j)  (nufft.py:137-218)
+ * nodes [host] m x ndim float64 row-major, any range (wrapped here);
+ * taps [host] ndim tap counts; ls_rows [host] the scaling-fit subsample rows
+ * (numpy default_rng(0).choice(m, 8192, replace=False) sorted, or 0..m-1),
+ * nufft.py:163-168. */
+int cbn_nufft_create(cbn_nufft** plan, int ndim, const int64_t* dims, const int32_t* taps,
+                     double oversample_factor, const double* nodes, int64_t m,
+                     const int64_t* ls_rows, int64_t n_ls, void* stream);
+int cbn_nufft_destroy(cbn_nufft* plan);
+/* per-axis float64 LS scaling vectors, concatenated (sum(dims) values) [host] */
+int cbn_nufft_scaling(const cbn_nufft* plan, double* out);
+/* wrapped nodes (m x ndim float64) and first-tap indices mod K (m x ndim int32) [host] */
+int cbn_nufft_wrapped_nodes(const cbn_nufft* plan, double* out);
+int cbn_nufft_first_indices(const cbn_nufft* plan, int32_t* out, void* stream);
+/* nufft_forward (nufft.py:221-233): x [device] complex64 dims -> y [device] complex64 m */
+int cbn_nufft_type2(cbn_nufft* plan, const void* x, void* y, void* stream);
+/* nufft_adjoint (nufft.py:236-247): y [device] complex64 m -> x [device] complex64 dims */
+int cbn_nufft_type1(cbn_nufft* plan, const void* y, void* x, void* stream);
+
+/* -------------------------------------------------------------- projector
+ * Replaces ConeGeometry / ProjectorConfig / nufft_forward_project /
+ * nufft_backproject (geometry.py:21-64, pipeline.py:31-212).
+ */
+typedef struct {
+    double so_mm, sd_mm, det_width_mm, det_height_mm;
+    int32_t nu, nv, n_views;
+    double object_extent_mm;
+} cbn_geometry;
+
+typedef struct {
+    int32_t n_rho, n_theta, n_phi;
+    double rho_max;
+} cbn_radial_spec;
+
+typedef struct {
+    int32_t method;            /* 0 = 'a' (only method implemented on device) */
+    cbn_radial_spec spec;
+    int32_t n_mu, n_t;
+    double t_pitch_mm;         /* <= 0 : None (virtual pixel pitch) */
+    int32_t t_taper;           /* 0 = none, 1 = hann */
+    int32_t spectrum_j;
+    int32_t resample_j[3];
+    int32_t side_lobes;
+    double oversample_factor;
+    int32_t rho_pad;           /* < 0 : None (n_rho / 2) */
+    int32_t basis;             /* 0 = trilinear, 1 = dirac */
+    double normalization, bp_normalization, den_tol;
+    int64_t target_batch;      /* pipeline._TARGET_BATCH */
+    int64_t plan_chunk;        /* nufft._PLAN_CHUNK */
+} cbn_projector_config;
+
+typedef struct cbn_projector_s cbn_projector;
+
+/* direction: 1 = forward, 2 = backprojector, 3 = both.
+ * n_vol / voxel_mm: volume edge and pitch (forward: the input volume; back:
+ * out_size, voxel_mm of nufft_backproject). */
+int cbn_projector_create(cbn_projector** proj, const cbn_geometry* geom,
+                         const cbn_projector_config* cfg, int32_t n_vol, double voxel_mm,
+                         int32_t direction);
+int cbn_projector_destroy(cbn_projector* proj);
+/* node-set sizes m whose scaling-fit rows the host must supply */
+int cbn_projector_ls_sizes(const cbn_projector* proj, int64_t* sizes, int32_t* count);
+int cbn_projector_set_ls_rows(cbn_projector* proj, int64_t m, const int64_t* rows, int64_t n);
+/* bytes of device scratch the plan will hold once built */
+int cbn_projector_scratch_bytes(const cbn_projector* proj, int64_t* bytes);
+
+/* nufft_forward_project (pipeline.py:122-147): vol [device] float32 N^3 [ix,iy,iz]
+ * -> frames [device] float32 (view_hi - view_lo) x nu x nv, views [view_lo, view_hi).
+ * Batches keep the reference's boundaries.  Returns CBN_ENONFINITE if any
+ * projection value is non-finite (checked on device, synchronises). */
+int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
+                        int32_t view_lo, int32_t view_hi, void* stream);
+/* nufft_backproject (pipeline.py:150-212): frames [device] float32 V x nu x nv
+ * -> vol [device] float32 N^3 */
+int cbn_backproject(cbn_projector* proj, const float* frames, float* vol, void* stream);
+
+/* Stage entry points (for stage parity and the mirrored module API). */
+/* _radial_lattice (pipeline.py:113-119): complex64 lattice, layout
+ * (n_phi, n_theta, n_rho) -- rho fastest, i.e. node order. */
+int cbn_projector_radial_lattice(cbn_projector* proj, const float* vol, void* lattice,
+                                 void* stream);
+/* resample_apply of method A for the umbrella targets of views [lo, hi) with the
+ * reference's per-batch plans (resampling.py:136-148, pipeline.py:130-137):
+ * lattice [device] as above -> values [device] float32 (hi-lo) x n_mu x n_t */
+int cbn_projector_resample_views(cbn_projector* proj, const void* lattice, float* values,
+                                 int32_t view_lo, int32_t view_hi, void* stream);
+/* reverse_grangeat_view for a block of views (grangeat.py:149-170):
+ * values float32 (nv_blk x n_mu x n_t) -> frames float32 (nv_blk x nu x nv) */
+int cbn_projector_grangeat_reverse(cbn_projector* proj, const float* values, float* frames,
+                                   int32_t n_views_blk, void* stream);
+/* forward_grangeat_view for a block of views (grangeat.py:131-146) with the
+ * backprojector's t grid: frames -> values float32 (nv_blk x n_mu x 2 nu) */
+int cbn_projector_grangeat_forward(cbn_projector* proj, const float* frames, float* values,
+                                   int32_t n_views_blk, void* stream);
+
+/* Stage timing of the last operator call, milliseconds (CUDA events). */
+int cbn_projector_stage_times(const cbn_projector* proj, double* ms, int32_t* count,
+                              char* names, int32_t names_len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CBNUFFT_B200_H */

@@ -1,0 +1,131 @@
+// Common device helpers for the B200 NUFFT cone-beam projector.
+//
+// * Bit-exact float64 index math of the reference plan (nufft.py:104-108,
+//   171-179): every operation on that path is an explicit round-to-nearest
+//   intrinsic so nvcc can never contract it into an FMA, which would change
+//   the last bit and with it the integer first-tap index.
+// * Kaiser-Bessel weights (nufft.py:36-41) evaluated in fp32 as a positive-
+//   coefficient polynomial in t = 1 - (2x/J)^2, normalised by I0(beta); the
+//   per-axis deapodisation absorbs the I0(beta) factor.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CBN_HD __host__ __device__ __forceinline__
+#define CBN_D __device__ __forceinline__
+
+namespace cbn {
+
+// numpy's float64 pi and 2*pi (exact doubles)
+constexpr double kPi = 3.141592653589793115997963468544185161590576171875;
+constexpr double kTwoPi = 6.28318530717958623199592693708837032318115234375;
+
+constexpr int kMaxPoly = 48;   // KB polynomial degree cap
+constexpr int kMaxDim = 3;
+
+// ---------------------------------------------------------------- complex
+CBN_HD float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+CBN_HD float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+CBN_HD float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+CBN_HD float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+
+// --------------------------------------------------- exact float64 helpers
+CBN_D double dadd(double a, double b) { return __dadd_rn(a, b); }
+CBN_D double dsub(double a, double b) { return __dsub_rn(a, b); }
+CBN_D double dmul(double a, double b) { return __dmul_rn(a, b); }
+CBN_D double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// numpy.remainder for float64 (npy_divmod): fmod, then move to the divisor's sign.
+CBN_D double np_mod(double a, double b) {
+    double m = fmod(a, b);
+    if (m != 0.0) {
+        if ((b < 0.0) != (m < 0.0)) m = dadd(m, b);
+    } else {
+        m = copysign(0.0, b);
+    }
+    return m;
+}
+
+// mod(x + pi, 2 pi) - pi   (nufft.py:104-108)
+CBN_D double wrap_pi(double x) { return dsub(np_mod(dadd(x, kPi), kTwoPi), kPi); }
+
+// u = mod(w, 2 pi) * K / (2 pi); snap |u - rint(u)| < 1e-9; first = ceil(u - J/2)
+// (nufft.py:173-176).  Returns u; first through the reference.
+CBN_D double axis_coord(double w, int K, double half_j, int& first) {
+    double u = ddiv(dmul(np_mod(w, kTwoPi), (double)K), kTwoPi);
+    double r = rint(u);
+    if (fabs(dsub(u, r)) < 1e-9) u = r;
+    first = (int)ceil(dsub(u, half_j));
+    return u;
+}
+
+CBN_HD int wrap_index(int c, int K) {
+    c %= K;
+    return c < 0 ? c + K : c;
+}
+
+// ------------------------------------------------------------ KB kernel
+struct KBAxis {
+    int J;          // taps
+    int K;          // oversampled length
+    int deg;        // polynomial degree
+    float poly[kMaxPoly + 1];   // I0(beta sqrt(t)) / I0(beta) = sum poly[k] t^k
+};
+
+// Exact support decision of the reference: arg = 1 - ((2x)/J)^2 > 0.
+// |2x| < J - margin is certainly inside, |2x| >= J certainly outside;
+// the thin band between uses the reference's exact float64 sequence.
+CBN_D bool kb_inside(double x, int J) {
+    double ax2 = fabs(dmul(2.0, x));
+    double jj = (double)J;
+    if (ax2 < jj * (1.0 - 1e-12)) return true;
+    if (ax2 >= jj) return false;
+    double q = ddiv(dmul(2.0, x), jj);
+    return dsub(1.0, dmul(q, q)) > 0.0;
+}
+
+CBN_D float kb_poly(const KBAxis& kb, float t) {
+    float acc = kb.poly[kb.deg];
+#pragma unroll 4
+    for (int k = kb.deg - 1; k >= 0; --k) acc = fmaf(acc, t, kb.poly[k]);
+    return acc;
+}
+
+// Weights of the J taps first..first+J-1 for grid coordinate u (fp64).
+template <int J>
+CBN_D void kb_weights(const KBAxis& kb, double u, int first, float (&w)[J]) {
+#pragma unroll
+    for (int p = 0; p < J; ++p) {
+        double x = dsub(u, (double)(first + p));
+        if (kb_inside(x, J)) {
+            float q = (float)x * (2.0f / (float)J);
+            float t = (1.0f - q) * (1.0f + q);
+            w[p] = kb_poly(kb, fmaxf(t, 0.0f));
+        } else {
+            w[p] = 0.0f;
+        }
+    }
+}
+
+// float64 I0 by its (all-positive) power series; |z| <= ~25 here.
+CBN_HD double i0_series(double z) {
+    double y = 0.25 * z * z;
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 200; ++k) {
+        term *= y / ((double)k * (double)k);
+        sum += term;
+        if (term < 1e-17 * sum) break;
+    }
+    return sum;
+}
+
+// float64 KB value exactly as the reference decides its support (nufft.py:36-41)
+CBN_D double kb_value_f64(double x, int J, double beta) {
+    double q = ddiv(dmul(2.0, x), (double)J);
+    double arg = dsub(1.0, dmul(q, q));
+    if (!(arg > 0.0)) return 0.0;
+    return i0_series(beta * sqrt(arg));
+}
+
+}  // namespace cbn

@@ -1,0 +1,104 @@
+// Non-template kernels shared by the plans: scaling fit and remap tables.
+#include "cbn_kernels.cuh"
+
+namespace cbn {
+
+__global__ void k_ls_fit(const double* __restrict__ frac, const double* __restrict__ wts, int n,
+                         LSParams p, double* __restrict__ s_raw, int s_stride) {
+    const int d = blockIdx.y;
+    const int k = blockIdx.x;
+    if (k >= p.N[d]) return;
+    const int N = p.N[d], K = p.K[d], J = p.J[d];
+    // nu = (k - N//2) / K cycles per oversampled sample (nufft.py:122)
+    const double nu = (double)(k - N / 2) / (double)K;
+    double er[kLSMaxJ], ei[kLSMaxJ];
+    for (int q = 0; q < J; ++q) sincospi(-2.0 * q * nu, &ei[q], &er[q]);
+    double num = 0.0, den = 0.0;
+    for (int s = threadIdx.x; s < n; s += blockDim.x) {
+        const double* ws = wts + ((size_t)d * n + s) * kLSMaxJ;
+        double rr = 0.0, ri = 0.0;
+        for (int q = 0; q < J; ++q) {
+            rr += ws[q] * er[q];
+            ri += ws[q] * ei[q];
+        }
+        den += rr * rr + ri * ri;
+        double sn, cs;
+        sincospi(2.0 * frac[(size_t)d * n + s] * nu, &sn, &cs);
+        // sum_p w_p cos(2 pi (frac - p) nu) = Re(e^{2 pi i frac nu} * resp)
+        num += cs * rr - sn * ri;
+    }
+    __shared__ double sh_num[32], sh_den[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        sh_num[warp] = num;
+        sh_den[warp] = den;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += sh_num[w];
+            b += sh_den[w];
+        }
+        s_raw[(size_t)d * s_stride + k] = a / fmax(b, 1e-300);
+    }
+}
+
+__global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, const double* i0beta,
+                            float* s32, int s32_stride) {
+    const int d = blockIdx.x;
+    const int N = p.N[d];
+    double* s = s_raw + (size_t)d * s_stride;
+    double mx = -1e308;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) mx = fmax(mx, s[k]);
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = sh[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+        sh[0] = m;
+    }
+    __syncthreads();
+    const double floor_v = 1e-8 * sh[0];
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        double v = fmax(s[k], floor_v);
+        s[k] = v;
+        s32[(size_t)d * s32_stride + k] = (float)(v * i0beta[d]);
+    }
+}
+
+__global__ void k_build_table(int mode, int N, int K, const float* __restrict__ s32, int* idx,
+                              float* scale) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int h = N / 2;
+    if (mode == kTabPad || mode == kTabPadShift) {
+        if (e >= K) return;
+        int n = -1;
+        if (e < N - h) n = e + h;
+        else if (e >= K - h) n = e - K + h;
+        if (n < 0) {
+            idx[e] = -1;
+            scale[e] = 0.f;
+            return;
+        }
+        int src = n;
+        if (mode == kTabPadShift) src = ((n - h) % N + N) % N;
+        idx[e] = src;
+        scale[e] = s32 ? s32[n] : 1.f;
+    } else {
+        if (e >= N) return;
+        int n = e;
+        if (mode == kTabCropShift) n = (e + h) % N;
+        int g = ((n - h) % K + K) % K;
+        idx[e] = g;
+        scale[e] = s32 ? s32[n] : 1.f;
+    }
+}
+
+}  // namespace cbn

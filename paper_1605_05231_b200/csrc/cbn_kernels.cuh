@@ -1,0 +1,284 @@
+// Templated NUFFT kernels shared by the generic plan and the projector.
+//
+// Node sources (`Src`) generate the wrapped float64 node of row i on the fly
+// (explicit arrays, radial-line tables, umbrella planes), so the reference's
+// dense (m, J^d) interpolation matrix (nufft.py:188-213) is never formed:
+// only the integer first tap and the fp32 KB weights are computed per point.
+//
+// Src concept:
+//   struct Aux;                                     // per-row side data
+//   __device__ void node(int64_t i, double (&w)[D], Aux&) const;   // wrapped node
+// Gather epilogue:  __device__ void put(int64_t i, float2 v, const double (&w)[D], const Aux&) const;
+// Spread values:    __device__ float2 value(int64_t i, const double (&w)[D], const Aux&) const;
+#pragma once
+
+#include "cbn_common.cuh"
+
+namespace cbn {
+
+struct KBSet {
+    KBAxis ax[kMaxDim];
+};
+
+template <int D>
+struct TapIndex {
+    int first[D];
+    double u[D];
+};
+
+template <int D, int J>
+CBN_D void tap_setup(const KBSet& kb, const double (&w)[D], int (&first)[D], float (&wt)[D][J]) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        double u = axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, first[d]);
+        kb_weights<J>(kb.ax[d], u, first[d], wt[d]);
+    }
+}
+
+CBN_D int wrapc(int c, int K) {
+    c = c < 0 ? c + K : c;
+    return c >= K ? c - K : c;
+}
+
+// ------------------------------------------------------------------ gather
+// y_i = sum_taps w0 w1 w2 G[c0, c1, c2]  (SparseInterpolator.apply, nufft.py:68-74)
+template <int D, int J, class Src, class Epi>
+__global__ void __launch_bounds__(256)
+k_gather(const float2* __restrict__ grid, KBSet kb, Src src, Epi epi, int64_t m) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double w[D];
+    typename Src::Aux aux;
+    src.node(i, w, aux);
+    int first[D];
+    float wt[D][J];
+    tap_setup<D, J>(kb, w, first, wt);
+    float2 acc = make_float2(0.f, 0.f);
+    if constexpr (D == 1) {
+        const int K0 = kb.ax[0].K;
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            float2 g = __ldg(grid + wrapc(first[0] + a, K0));
+            acc.x = fmaf(wt[0][a], g.x, acc.x);
+            acc.y = fmaf(wt[0][a], g.y, acc.y);
+        }
+    } else if constexpr (D == 2) {
+        const int K0 = kb.ax[0].K, K1 = kb.ax[1].K;
+        int c1[J];
+#pragma unroll
+        for (int b = 0; b < J; ++b) c1[b] = wrapc(first[1] + b, K1);
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            const float2* row = grid + (size_t)wrapc(first[0] + a, K0) * K1;
+            float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int b = 0; b < J; ++b) {
+                float2 g = __ldg(row + c1[b]);
+                r.x = fmaf(wt[1][b], g.x, r.x);
+                r.y = fmaf(wt[1][b], g.y, r.y);
+            }
+            acc.x = fmaf(wt[0][a], r.x, acc.x);
+            acc.y = fmaf(wt[0][a], r.y, acc.y);
+        }
+    } else {
+        const int K0 = kb.ax[0].K, K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+        int c2[J];
+#pragma unroll
+        for (int c = 0; c < J; ++c) c2[c] = wrapc(first[2] + c, K2);
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            const float2* plane = grid + (size_t)wrapc(first[0] + a, K0) * K1 * K2;
+            float2 pa = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int b = 0; b < J; ++b) {
+                const float2* row = plane + (size_t)wrapc(first[1] + b, K1) * K2;
+                float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < J; ++c) {
+                    float2 g = __ldg(row + c2[c]);
+                    r.x = fmaf(wt[2][c], g.x, r.x);
+                    r.y = fmaf(wt[2][c], g.y, r.y);
+                }
+                pa.x = fmaf(wt[1][b], r.x, pa.x);
+                pa.y = fmaf(wt[1][b], r.y, pa.y);
+            }
+            acc.x = fmaf(wt[0][a], pa.x, acc.x);
+            acc.y = fmaf(wt[0][a], pa.y, acc.y);
+        }
+    }
+    epi.put(i, acc, w, aux);
+}
+
+// ------------------------------------------------------------------ spread
+// G[c] += w0 w1 w2 y_i   (SparseInterpolator.apply_adjoint, nufft.py:76-85)
+template <int D, int J, class Src>
+__global__ void __launch_bounds__(256)
+k_spread(float2* __restrict__ grid, KBSet kb, Src src, int64_t m) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double w[D];
+    typename Src::Aux aux;
+    src.node(i, w, aux);
+    float2 v = src.value(i, w, aux);
+    if (v.x == 0.f && v.y == 0.f) return;
+    int first[D];
+    float wt[D][J];
+    tap_setup<D, J>(kb, w, first, wt);
+    if constexpr (D == 1) {
+        const int K0 = kb.ax[0].K;
+#pragma unroll
+        for (int a = 0; a < J; ++a)
+            atomicAdd(grid + wrapc(first[0] + a, K0), cscale(v, wt[0][a]));
+    } else if constexpr (D == 2) {
+        const int K0 = kb.ax[0].K, K1 = kb.ax[1].K;
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            float2* row = grid + (size_t)wrapc(first[0] + a, K0) * K1;
+            float2 va = cscale(v, wt[0][a]);
+#pragma unroll
+            for (int b = 0; b < J; ++b) atomicAdd(row + wrapc(first[1] + b, K1), cscale(va, wt[1][b]));
+        }
+    } else {
+        const int K0 = kb.ax[0].K, K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+        int c2[J];
+#pragma unroll
+        for (int c = 0; c < J; ++c) c2[c] = wrapc(first[2] + c, K2);
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            float2* plane = grid + (size_t)wrapc(first[0] + a, K0) * K1 * K2;
+            float2 va = cscale(v, wt[0][a]);
+#pragma unroll
+            for (int b = 0; b < J; ++b) {
+                float2* row = plane + (size_t)wrapc(first[1] + b, K1) * K2;
+                float2 vb = cscale(va, wt[1][b]);
+#pragma unroll
+                for (int c = 0; c < J; ++c) atomicAdd(row + c2[c], cscale(vb, wt[2][c]));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------ least-squares scaling
+// _ls_scaling (nufft.py:111-134) on the plan's sampled rows (nufft.py:163-168).
+constexpr int kLSMaxJ = 16;
+
+struct LSParams {
+    int ndim;
+    int N[kMaxDim];
+    int K[kMaxDim];
+    int J[kMaxDim];
+    double beta[kMaxDim];
+};
+
+// per sampled row and axis: frac = u - first and the float64 KB weights
+template <int D, class Src>
+__global__ void k_ls_samples(Src src, const int64_t* __restrict__ rows, int n, LSParams p,
+                             double* __restrict__ frac, double* __restrict__ wts) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    double w[D];
+    typename Src::Aux aux;
+    src.node(rows[s], w, aux);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        int first;
+        double u = axis_coord(w[d], p.K[d], 0.5 * (double)p.J[d], first);
+        frac[d * n + s] = dsub(u, (double)first);
+        for (int q = 0; q < p.J[d]; ++q)
+            wts[((size_t)d * n + s) * kLSMaxJ + q] =
+                kb_value_f64(dsub(u, (double)(first + q)), p.J[d], p.beta[d]);
+    }
+}
+
+// one block per (frequency n, axis): num / den reductions over the samples
+__global__ void k_ls_fit(const double* __restrict__ frac, const double* __restrict__ wts, int n,
+                         LSParams p, double* __restrict__ s_raw, int s_stride);
+
+// one block per axis: clip at 1e-8 max, write float64 and scaled float32 copies
+__global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, const double* i0beta,
+                            float* s32, int s32_stride);
+
+// ----------------------------------------------------------- separable remap
+// dst[e] = gain * prod_d scale_d[e_d] * src[sum_d idx_d[e_d] * sstride_d]
+// (zero when any idx is negative).  Implements deapodise+pad (nufft.py:226-230),
+// crop+deapodise (nufft.py:245-247) and the resampler's fftshift/ifftshift
+// index maps (resampling.py:146,175) as one table-driven pass.
+struct RemapAxis {
+    const int* idx;
+    const float* scale;
+    int n;            // destination extent
+    int64_t sstride;  // source stride (elements)
+};
+
+enum RemapMode { kStoreC = 0, kAccumC = 1, kStoreRe = 2 };
+
+template <int D, class SrcT, int MODE>
+__global__ void k_remap(const SrcT* __restrict__ src, void* __restrict__ dst, RemapAxis a0,
+                        RemapAxis a1, RemapAxis a2, float gain) {
+    // D == 3: (x: a2 fastest, y: a1, z: a0); D == 2: (x: a1, y: a0); D == 1: x: a0
+    int e_last = blockIdx.x * blockDim.x + threadIdx.x;
+    RemapAxis ax[3] = {a0, a1, a2};
+    const RemapAxis& fast = ax[D - 1];
+    if (e_last >= fast.n) return;
+    int e[3] = {0, 0, 0};
+    e[D - 1] = e_last;
+    if (D >= 2) e[D - 2] = blockIdx.y;
+    if (D >= 3) e[0] = blockIdx.z;
+    float sc = gain;
+    int64_t so = 0;
+    bool zero = false;
+    size_t doff = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        int id = ax[d].idx[e[d]];
+        zero |= id < 0;
+        so += (int64_t)id * ax[d].sstride;
+        sc *= ax[d].scale[e[d]];
+        doff = doff * (size_t)ax[d].n + (size_t)e[d];
+    }
+    float2 v = make_float2(0.f, 0.f);
+    if (!zero) {
+        if constexpr (sizeof(SrcT) == sizeof(float)) {
+            v.x = sc * (float)src[so];
+        } else {
+            float2 g = src[so];
+            v = make_float2(g.x * sc, g.y * sc);
+        }
+    }
+    if constexpr (MODE == kStoreC) {
+        static_cast<float2*>(dst)[doff] = v;
+    } else if constexpr (MODE == kAccumC) {
+        float2* p = static_cast<float2*>(dst) + doff;
+        float2 o = *p;
+        *p = make_float2(o.x + v.x, o.y + v.y);
+    } else {
+        static_cast<float*>(dst)[doff] = v.x;
+    }
+}
+
+// Table modes for k_build_table.
+enum TableMode {
+    kTabPad = 0,      // g in [0,K): source n of the rolled placement (n - N//2) mod K, scale s[n]
+    kTabCrop = 1,     // n in [0,N): source g = (n - N//2) mod K, scale s[n]
+    kTabPadShift = 2, // as kTabPad, but the source is the unshifted FFT: f = (n - N//2) mod N
+    kTabCropShift = 3 // k in [0,N): n = (k + N//2) mod N, source g = (n - N//2) mod K, scale s[n]
+};
+
+__global__ void k_build_table(int mode, int N, int K, const float* __restrict__ s32, int* idx,
+                              float* scale);
+
+// Host-side launch helper for k_remap.
+template <class SrcT, int MODE>
+void launch_remap(int D, const SrcT* src, void* dst, const RemapAxis* ax, float gain,
+                  cudaStream_t s) {
+    RemapAxis z{nullptr, nullptr, 1, 0};
+    RemapAxis a0 = ax[0], a1 = D > 1 ? ax[1] : z, a2 = D > 2 ? ax[2] : z;
+    int fastn = ax[D - 1].n;
+    dim3 block(256);
+    dim3 grid((fastn + 255) / 256, D >= 2 ? ax[D - 2].n : 1, D >= 3 ? ax[0].n : 1);
+    if (D == 1) k_remap<1, SrcT, MODE><<<grid, block, 0, s>>>(src, dst, a0, a1, a2, gain);
+    else if (D == 2) k_remap<2, SrcT, MODE><<<grid, block, 0, s>>>(src, dst, a0, a1, a2, gain);
+    else k_remap<3, SrcT, MODE><<<grid, block, 0, s>>>(src, dst, a0, a1, a2, gain);
+}
+
+}  // namespace cbn

@@ -1,0 +1,330 @@
+// Generic NUFFT plan over explicit nodes: the device replacement of
+// plan_nufft / nufft_forward / nufft_adjoint (nufft.py:137-247).
+//
+// Plan state is O(m*d) wrapped float64 nodes plus per-axis scalings and remap
+// tables; interpolation weights are recomputed inside the gather/spread
+// kernels instead of being stored (the reference stores J^d per node).
+#include <cstring>
+#include <vector>
+
+#include "cbn_plan.h"
+
+namespace cbn {
+
+template <int D>
+struct ExplicitSrc {
+    const double* nodes;  // wrapped, m x D
+    struct Aux {};
+    CBN_D void node(int64_t i, double (&w)[D], Aux&) const {
+#pragma unroll
+        for (int d = 0; d < D; ++d) w[d] = nodes[i * D + d];
+    }
+};
+
+// plan.phase = exp(-i w . (N//2))  (nufft.py:215-216), angle in float64
+template <int D>
+struct PhaseOut {
+    float2* y;
+    double c[kMaxDim];
+    CBN_D void put(int64_t i, float2 v, const double (&w)[D], const typename ExplicitSrc<D>::Aux&) const {
+        double a = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) a += w[d] * c[d];
+        double sn, cs;
+        sincos(-a, &sn, &cs);
+        y[i] = cmul(v, make_float2((float)cs, (float)sn));
+    }
+};
+
+template <int D>
+struct PhaseIn : ExplicitSrc<D> {
+    const float2* yin;
+    double c[kMaxDim];
+    CBN_D float2 value(int64_t i, const double (&w)[D], const typename ExplicitSrc<D>::Aux&) const {
+        double a = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) a += w[d] * c[d];
+        double sn, cs;
+        sincos(a, &sn, &cs);   // conj(phase)
+        return cmul(yin[i], make_float2((float)cs, (float)sn));
+    }
+};
+
+__global__ void k_wrap_nodes(const double* __restrict__ in, double* __restrict__ out, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = wrap_pi(in[i]);
+}
+
+template <int D>
+__global__ void k_first(const double* __restrict__ nodes, KBSet kb, int64_t m, int32_t* out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        int f;
+        axis_coord(nodes[i * D + d], kb.ax[d].K, 0.5 * (double)kb.ax[d].J, f);
+        out[i * D + d] = wrapc(f, kb.ax[d].K);
+    }
+}
+
+}  // namespace cbn
+
+using namespace cbn;
+
+struct cbn_nufft_s {
+    int D = 0;
+    int J = 0;
+    int64_t m = 0;
+    AxisPlan ax[kMaxDim];
+    KBSet kb{};
+    DevBuf<double> nodes;
+    DevBuf<float> s32;         // D x smax
+    DevBuf<int> pad_idx, crop_idx;
+    DevBuf<float> pad_sc, crop_sc;
+    DevBuf<float2> grid;
+    std::vector<double> s64_host;
+    int smax = 0;
+    int64_t ktot = 1, ntot = 1;
+    FFTCache fft;
+    double centre[kMaxDim] = {0, 0, 0};
+};
+
+namespace {
+
+template <int D>
+void run_type2(cbn_nufft* p, const float2* x, float2* y, cudaStream_t s) {
+    RemapAxis ax[kMaxDim];
+    int64_t stride = 1;
+    int koff = 0;
+    for (int d = D - 1; d >= 0; --d) {
+        ax[d].n = p->ax[d].K;
+        ax[d].sstride = stride;
+        stride *= p->ax[d].N;
+    }
+    for (int d = 0; d < D; ++d) {
+        ax[d].idx = p->pad_idx.p + koff;
+        ax[d].scale = p->pad_sc.p + koff;
+        koff += p->ax[d].K;
+    }
+    launch_remap<float2, kStoreC>(D, x, p->grid.p, ax, 1.0f, s);
+    CBN_LAUNCH_CHECK();
+    long long kd[3];
+    for (int d = 0; d < D; ++d) kd[d] = p->ax[d].K;
+    p->fft.exec(p->fft.get(D, kd, 1), p->grid.p, p->grid.p, CUFFT_FORWARD, s);
+    PhaseOut<D> epi;
+    epi.y = y;
+    for (int d = 0; d < D; ++d) epi.c[d] = p->centre[d];
+    ExplicitSrc<D> src{p->nodes.p};
+    dispatch_j(p->J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        k_gather<D, J><<<blocks_for(p->m, 256), 256, 0, s>>>(p->grid.p, p->kb, src, epi, p->m);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
+}
+
+template <int D>
+void run_type1(cbn_nufft* p, const float2* y, float2* x, cudaStream_t s) {
+    CBN_CUDA(cudaMemsetAsync(p->grid.p, 0, p->grid.bytes(), s));
+    PhaseIn<D> src;
+    src.nodes = p->nodes.p;
+    src.yin = y;
+    for (int d = 0; d < D; ++d) src.c[d] = p->centre[d];
+    dispatch_j(p->J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        k_spread<D, J><<<blocks_for(p->m, 256), 256, 0, s>>>(p->grid.p, p->kb, src, p->m);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
+    long long kd[3];
+    for (int d = 0; d < D; ++d) kd[d] = p->ax[d].K;
+    p->fft.exec(p->fft.get(D, kd, 1), p->grid.p, p->grid.p, CUFFT_INVERSE, s);
+    RemapAxis ax[kMaxDim];
+    int64_t stride = 1;
+    int noff = 0;
+    for (int d = D - 1; d >= 0; --d) {
+        ax[d].n = p->ax[d].N;
+        ax[d].sstride = stride;
+        stride *= p->ax[d].K;
+    }
+    for (int d = 0; d < D; ++d) {
+        ax[d].idx = p->crop_idx.p + noff;
+        ax[d].scale = p->crop_sc.p + noff;
+        noff += p->ax[d].N;
+    }
+    launch_remap<float2, kStoreC>(D, p->grid.p, x, ax, 1.0f, s);
+    CBN_LAUNCH_CHECK();
+}
+
+template <int D>
+void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t s) {
+    DevBuf<int64_t> rows;
+    rows.upload(rows_host, (size_t)n_ls, s);
+    LSScratch sc;
+    ExplicitSrc<D> src{p->nodes.p};
+    ls_fit<D>(src, rows.p, (int)n_ls, p->ax, sc, p->s32.p, p->smax, s);
+    p->s64_host.assign((size_t)D * p->smax, 0.0);
+    CBN_CUDA(cudaMemcpyAsync(p->s64_host.data(), sc.s64.p, sizeof(double) * D * p->smax,
+                             cudaMemcpyDeviceToHost, s));
+    int koff = 0, noff = 0;
+    for (int d = 0; d < D; ++d) {
+        build_table(kTabPad, p->ax[d].N, p->ax[d].K, p->s32.p + (size_t)d * p->smax,
+                    p->pad_idx.p + koff, p->pad_sc.p + koff, s);
+        build_table(kTabCrop, p->ax[d].N, p->ax[d].K, p->s32.p + (size_t)d * p->smax,
+                    p->crop_idx.p + noff, p->crop_sc.p + noff, s);
+        koff += p->ax[d].K;
+        noff += p->ax[d].N;
+    }
+    CBN_CUDA(cudaStreamSynchronize(s));   // rows / host scaling copy must outlive the launch
+}
+
+template <class F>
+auto dispatch_d(int D, F&& f) {
+    switch (D) {
+        case 1: return f(std::integral_constant<int, 1>{});
+        case 2: return f(std::integral_constant<int, 2>{});
+        case 3: return f(std::integral_constant<int, 3>{});
+        default: throw Error(CBN_EINVAL, "ndim must be 1..3");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cbn_last_error(void);
+
+int cbn_version(void) { return 1; }
+
+double cbn_beatty_beta(int j, double alpha) { return cbn::beatty_beta(j, alpha); }
+
+int cbn_nufft_create(cbn_nufft** out, int ndim, const int64_t* dims, const int32_t* taps,
+                     double oversample_factor, const double* nodes, int64_t m,
+                     const int64_t* ls_rows, int64_t n_ls, void* stream) {
+    try {
+        CBN_REQUIRE(out && dims && taps, "null argument");
+        CBN_REQUIRE(ndim >= 1 && ndim <= 3, "ndim must be 1..3");
+        CBN_REQUIRE(oversample_factor >= 1.0, "oversample_factor must be >= 1");
+        CBN_REQUIRE(m >= 1 && nodes, "need at least one node");
+        CBN_REQUIRE(n_ls >= 1 && n_ls <= kMaxLS && ls_rows, "scaling-fit rows must number 1..8192");
+        for (int d = 0; d < ndim; ++d) {
+            CBN_REQUIRE(dims[d] >= 1, "dims must be >= 1");
+            CBN_REQUIRE(taps[d] >= 1, "tap counts must be >= 1");
+            CBN_REQUIRE(taps[d] == taps[0], "per-axis tap counts must be equal on the device path");
+        }
+        for (int64_t r = 0; r < n_ls; ++r) CBN_REQUIRE(ls_rows[r] >= 0 && ls_rows[r] < m, "bad scaling-fit row");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto p = std::make_unique<cbn_nufft_s>();
+        p->D = ndim;
+        p->J = taps[0];
+        p->m = m;
+        for (int d = 0; d < ndim; ++d) {
+            p->ax[d] = make_axis((int)dims[d], taps[d], oversample_factor);
+            p->kb.ax[d] = p->ax[d].kb;
+            p->smax = std::max(p->smax, p->ax[d].N);
+            p->ktot *= p->ax[d].K;
+            p->ntot *= p->ax[d].N;
+            p->centre[d] = (double)(dims[d] / 2);
+        }
+        DevBuf<double> raw;
+        raw.upload(nodes, (size_t)m * ndim, s);
+        p->nodes.alloc((size_t)m * ndim);
+        k_wrap_nodes<<<blocks_for(m * ndim, 256), 256, 0, s>>>(raw.p, p->nodes.p, m * ndim);
+        CBN_LAUNCH_CHECK();
+        size_t ksum = 0, nsum = 0;
+        for (int d = 0; d < ndim; ++d) {
+            ksum += p->ax[d].K;
+            nsum += p->ax[d].N;
+        }
+        p->s32.alloc((size_t)ndim * p->smax);
+        p->pad_idx.alloc(ksum);
+        p->pad_sc.alloc(ksum);
+        p->crop_idx.alloc(nsum);
+        p->crop_sc.alloc(nsum);
+        p->grid.alloc((size_t)p->ktot);
+        dispatch_d(ndim, [&](auto dc) {
+            fit_plan<decltype(dc)::value>(p.get(), ls_rows, n_ls, s);
+            return 0;
+        });
+        *out = p.release();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_destroy(cbn_nufft* plan) {
+    delete plan;
+    return CBN_OK;
+}
+
+int cbn_nufft_scaling(const cbn_nufft* p, double* out) {
+    try {
+        CBN_REQUIRE(p && out, "null argument");
+        size_t k = 0;
+        for (int d = 0; d < p->D; ++d)
+            for (int n = 0; n < p->ax[d].N; ++n) out[k++] = p->s64_host[(size_t)d * p->smax + n];
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_wrapped_nodes(const cbn_nufft* p, double* out) {
+    try {
+        CBN_REQUIRE(p && out, "null argument");
+        CBN_CUDA(cudaMemcpy(out, p->nodes.p, sizeof(double) * p->m * p->D, cudaMemcpyDeviceToHost));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_first_indices(const cbn_nufft* p, int32_t* out, void* stream) {
+    try {
+        CBN_REQUIRE(p && out, "null argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevBuf<int32_t> dev((size_t)p->m * p->D);
+        dispatch_d(p->D, [&](auto dc) {
+            constexpr int D = decltype(dc)::value;
+            k_first<D><<<blocks_for(p->m, 256), 256, 0, s>>>(p->nodes.p, p->kb, p->m, dev.p);
+            return 0;
+        });
+        CBN_LAUNCH_CHECK();
+        CBN_CUDA(cudaMemcpyAsync(out, dev.p, sizeof(int32_t) * p->m * p->D, cudaMemcpyDeviceToHost, s));
+        CBN_CUDA(cudaStreamSynchronize(s));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_type2(cbn_nufft* p, const void* x, void* y, void* stream) {
+    try {
+        CBN_REQUIRE(p && x && y, "null argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        dispatch_d(p->D, [&](auto dc) {
+            run_type2<decltype(dc)::value>(p, static_cast<const float2*>(x), static_cast<float2*>(y), s);
+            return 0;
+        });
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_type1(cbn_nufft* p, const void* y, void* x, void* stream) {
+    try {
+        CBN_REQUIRE(p && x && y, "null argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        dispatch_d(p->D, [&](auto dc) {
+            run_type1<decltype(dc)::value>(p, static_cast<const float2*>(y), static_cast<float2*>(x), s);
+            return 0;
+        });
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"

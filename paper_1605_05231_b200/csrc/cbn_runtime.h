@@ -1,0 +1,103 @@
+// Host-side runtime for the C-ABI library: status codes, exceptions mapped to
+// codes at the boundary, device buffers, and a cuFFT plan cache whose plans
+// share one workspace (plans on one stream run back to back).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/cbnufft_b200.h"
+
+namespace cbn {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+int fail(const std::exception& e);
+
+#define CBN_REQUIRE(cond, msg)                                                   \
+    do {                                                                         \
+        if (!(cond)) throw ::cbn::Error(CBN_EINVAL, (msg));                      \
+    } while (0)
+
+#define CBN_CUDA(expr)                                                           \
+    do {                                                                         \
+        cudaError_t e_ = (expr);                                                 \
+        if (e_ != cudaSuccess) {                                                 \
+            int code_ = e_ == cudaErrorMemoryAllocation ? CBN_ENOMEM : CBN_ECUDA; \
+            throw ::cbn::Error(code_, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+        }                                                                        \
+    } while (0)
+
+#define CBN_CUFFT(expr)                                                          \
+    do {                                                                         \
+        cufftResult r_ = (expr);                                                 \
+        if (r_ != CUFFT_SUCCESS) {                                               \
+            int code_ = r_ == CUFFT_ALLOC_FAILED ? CBN_ENOMEM : CBN_ECUDA;       \
+            throw ::cbn::Error(code_, std::string(#expr ": cufft error ") + std::to_string((int)r_)); \
+        }                                                                        \
+    } while (0)
+
+#define CBN_LAUNCH_CHECK() CBN_CUDA(cudaGetLastError())
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        release();
+        if (count) CBN_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void upload(const T* host, size_t count, cudaStream_t s) {
+        ensure(count);
+        CBN_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// C2C float FFT plans keyed by geometry; one shared workspace per cache.
+class FFTCache {
+public:
+    ~FFTCache();
+    // rank-r transform of `batch` contiguous arrays of shape n[0..r-1] (row-major)
+    cufftHandle get(int rank, const long long* n, long long batch);
+    // 1D transforms of length n over `batch` lines with element stride / distance
+    cufftHandle get_strided(long long n, long long batch, long long stride, long long dist);
+    void exec(cufftHandle h, void* in, void* out, int direction, cudaStream_t s);
+    void clear();
+
+private:
+    using Key = std::tuple<int, long long, long long, long long, long long, long long, long long>;
+    std::map<Key, cufftHandle> plans_;
+    DevBuf<char> work_;
+    cufftHandle make(int rank, long long* n, long long batch, long long stride, long long dist);
+};
+
+}  // namespace cbn

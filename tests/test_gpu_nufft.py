@@ -1,0 +1,72 @@
+"""Device NUFFT (C ABI) against the reference's golden vectors: bit-exact
+first-tap (bin) indices, scalings, type-2 / type-1 outputs, dot tests."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["r3_j6", "r3_j3_odd", "r2_j5", "r1_j6", "r3_j8", "r3_big",
+         "edge_j6", "edge_j3", "edge_j5_2d"]
+
+
+@pytest.fixture(scope="module")
+def nf():
+    from paper_1605_05231_b200 import nufft
+    return nufft
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_first_indices_bit_exact(nf, nufft_cases, name):
+    c = nufft_cases[name]
+    dims = tuple(int(v) for v in c["dims"])
+    plan = nf.plan_nufft(dims, c["nodes"], 2.0, tuple(int(v) for v in c["j"]))
+    assert np.array_equal(plan.nodes, c["wrapped"])
+    assert np.array_equal(plan.first_indices().astype(np.int64), c["first"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_scaling_matches_reference(nf, nufft_cases, name):
+    c = nufft_cases[name]
+    dims = tuple(int(v) for v in c["dims"])
+    plan = nf.plan_nufft(dims, c["nodes"], 2.0, tuple(int(v) for v in c["j"]))
+    assert rel_l2(plan.scaling, c["scaling"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_type2_type1_match_reference(nf, nufft_cases, name):
+    c = nufft_cases[name]
+    dims = tuple(int(v) for v in c["dims"])
+    plan = nf.plan_nufft(dims, c["nodes"], 2.0, tuple(int(v) for v in c["j"]))
+    assert rel_l2(nf.nufft_forward(plan, c["x"]), c["fwd"]) < 1e-5
+    assert rel_l2(nf.nufft_adjoint(plan, c["y"]), c["adj"]) < 1e-5
+
+
+@pytest.mark.parametrize("dims", [(32,), (16, 16), (8, 8, 8), (20, 18, 16)])
+def test_dot_test_fp32(nf, dims):
+    rng = np.random.default_rng(9)
+    nodes = rng.uniform(-np.pi, np.pi, (3000, len(dims)))
+    plan = nf.plan_nufft(dims, nodes, 2.0, 6)
+    x = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
+    y = rng.standard_normal(3000) + 1j * rng.standard_normal(3000)
+    lhs = np.vdot(y, nf.nufft_forward(plan, x))
+    rhs = np.vdot(nf.nufft_adjoint(plan, y), x)
+    assert abs(lhs - rhs) / abs(lhs) < 1e-5
+
+
+def test_validation_errors(nf):
+    with pytest.raises(ValueError):
+        nf.plan_nufft((8,), np.zeros((4, 2)), 2.0, 6)
+    with pytest.raises(ValueError):
+        nf.plan_nufft((8,), np.zeros((4, 1)), 0.5, 6)
+    with pytest.raises(ValueError):
+        nf.plan_nufft((8,), np.zeros((4, 1)), 2.0, 0)
+    with pytest.raises(ValueError):
+        nf.plan_nufft((8,), np.full((4, 1), np.nan), 2.0, 6)
+    plan = nf.plan_nufft((8,), np.zeros((4, 1)), 2.0, 6)
+    with pytest.raises(ValueError):
+        nf.nufft_forward(plan, np.zeros(7))
+    with pytest.raises(ValueError):
+        nf.nufft_adjoint(plan, np.zeros(5))
