@@ -1,0 +1,461 @@
+// Direct NUFFT backprojector (pipeline.py:150-212) on the B200:
+//   per reference view batch:
+//     forward Grangeat (grangeat.py:131-146): w1, deapod/pad, cuFFT 2D,
+//       KB J=5 gather at polar nodes, i omega, centred t IFFT, w2
+//     resample transpose (resampling.py:164-196): KB J=3 spread of the values
+//       and of the validity mask (num/den) at umbrella targets, cuFFT^-1,
+//       crop + per-batch deapodisation, accumulated over batches
+//   then: ifftshift + cuFFT^-1 of the accumulators, rho crop, origin average,
+//   num/den with the vacancy threshold, centred radial FFT, ramp * sin(theta)
+//   * trilinear, KB J spread onto (2N)^3, cuFFT^-1, crop + deapodisation.
+#include <algorithm>
+#include <array>
+#include <cmath>
+
+#include "cbn_projector.h"
+
+namespace cbn {
+
+const int64_t* projector_rows(cbn_projector_s* p, int64_t m, int& n);
+std::vector<std::pair<int, int>> projector_batches(int n_views, int64_t per_view, int64_t target);
+int64_t projector_chunk(const cbn_projector_s* p, int64_t m);
+int64_t projector_target_batch(const cbn_projector_s* p);
+UmbrellaGeom projector_umb_geom(const cbn_projector_s* p, const UmbrellaTables& u,
+                                const RadialTables& r, int pad);
+void projector_build_tables(cbn_projector_s* p, int mode, const AxisPlan* ax, int smax,
+                            cudaStream_t s, RemapAxis* out, const int64_t* sstride);
+void projector_fit_grangeat(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
+                            cudaStream_t s);
+void projector_column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
+                           double* partial, double* out, cudaStream_t s);
+void build_backward_plan(cbn_projector_s* p, cudaStream_t s);
+
+namespace {
+
+constexpr int kRed = 296;
+
+CBN_D double w1_val(int u, int v, int nu, int nv, double pu, double pv, double so) {
+    double uc = (((double)u - (double)nu / 2.0) + 0.5) * pu;
+    double vc = (((double)v - (double)nv / 2.0) + 0.5) * pv;
+    return so / sqrt(so * so + uc * uc + vc * vc);
+}
+
+CBN_D int pad_src(int g, int N, int K) {
+    const int h = N / 2;
+    if (g < N - h) return g + h;
+    if (g >= K - h) return g - K + h;
+    return -1;
+}
+
+// h = frame * w1 ; y = h * scaling placed at rolled positions (nufft.py:226-230)
+__global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int Ku, int Kv,
+                          double pu, double pv, double so, const float* __restrict__ s32, int smax,
+                          int64_t total, float2* __restrict__ grids) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int64_t per = (int64_t)Ku * Kv;
+    const int v = (int)(e / per);
+    const int rem = (int)(e % per);
+    const int gu = rem / Kv, gv = rem % Kv;
+    const int nu_i = pad_src(gu, nu, Ku), nv_i = pad_src(gv, nv, Kv);
+    float2 out = make_float2(0.f, 0.f);
+    if (nu_i >= 0 && nv_i >= 0) {
+        double h = (double)frames[((size_t)v * nu + nu_i) * nv + nv_i] *
+                   w1_val(nu_i, nv_i, nu, nv, pu, pv, so);
+        out.x = (float)h * s32[nu_i] * s32[smax + nv_i];
+    }
+    grids[e] = out;
+}
+
+struct GrFwdParams {
+    int n_mu, n_t, Ku, Kv;
+    double pc0, pc1;     // plan phase * centre phase: exp(+i w.pc)
+    float pupv;
+};
+
+template <int J>
+__global__ void __launch_bounds__(256)
+k_grf_gather(const float2* __restrict__ grids, KBSet kb, PolarSrc src, GrFwdParams p,
+             const double* __restrict__ omega, int nb, float2* __restrict__ out) {
+    const int64_t m = (int64_t)p.n_mu * p.n_t;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double w[2];
+    PolarSrc::Aux aux;
+    src.node(i, w, aux);
+    double sn, cs;
+    sincos(w[0] * p.pc0 + w[1] * p.pc1, &sn, &cs);
+    const float om = (float)omega[aux.jt] * p.pupv;
+    // phase * pu pv * (i omega)
+    const float2 fac = make_float2(-(float)sn * om, (float)cs * om);
+    int first[2];
+    float wt[2][J];
+    tap_setup<2, J>(kb, w, first, wt);
+    int c1[J];
+#pragma unroll
+    for (int b = 0; b < J; ++b) c1[b] = wrapc(first[1] + b, p.Kv);
+    const int im = (int)(i / p.n_t);
+    const int col = (aux.jt - p.n_t / 2 + p.n_t) % p.n_t;   // ifftshift for the t IFFT
+    const size_t gsz = (size_t)p.Ku * p.Kv;
+    for (int v = 0; v < nb; ++v) {
+        const float2* grid = grids + v * gsz;
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            const float2* row = grid + (size_t)wrapc(first[0] + a, p.Ku) * p.Kv;
+            float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int b = 0; b < J; ++b) {
+                float2 g = __ldg(row + c1[b]);
+                r.x = fmaf(wt[1][b], g.x, r.x);
+                r.y = fmaf(wt[1][b], g.y, r.y);
+            }
+            acc.x = fmaf(wt[0][a], r.x, acc.x);
+            acc.y = fmaf(wt[0][a], r.y, acc.y);
+        }
+        out[((size_t)v * p.n_mu + im) * p.n_t + col] = cmul(acc, fac);
+    }
+}
+
+// values = Re(fftshift(ifft)) / dt * w2   (grangeat.py:144-145)
+__global__ void k_grf_post(const float2* __restrict__ t, const float* __restrict__ w2, int n_t,
+                           double inv, int64_t total, float* __restrict__ vals) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int j = (int)(e % n_t);
+    const int64_t row = e / n_t;
+    float re = t[row * n_t + (j - n_t / 2 + n_t) % n_t].x;
+    vals[e] = (float)(re * inv) * w2[j];
+}
+
+// num / den spreads of one resample batch (resample_transpose, called with the
+// values and with the validity mask, pipeline.py:183-184); real inputs, the
+// phases cancel, so only the real part of each grid receives data
+template <int J>
+__global__ void __launch_bounds__(256)
+k_rs_spread2(float* __restrict__ gnum, float* __restrict__ gden, KBSet kb, UmbrellaSrc src,
+             const float* __restrict__ vals, int64_t m) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double w[3];
+    UmbrellaSrc::Aux aux;
+    src.node(i, w, aux);
+    if (!aux.valid) return;
+    const float vn = vals[i];
+    int first[3];
+    float wt[3][J];
+    tap_setup<3, J>(kb, w, first, wt);
+    const int K0 = kb.ax[0].K, K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+    int c2[J];
+#pragma unroll
+    for (int c = 0; c < J; ++c) c2[c] = wrapc(first[2] + c, K2);
+#pragma unroll
+    for (int a = 0; a < J; ++a) {
+        const size_t pa = (size_t)wrapc(first[0] + a, K0) * K1;
+#pragma unroll
+        for (int b = 0; b < J; ++b) {
+            const size_t row = (pa + (size_t)wrapc(first[1] + b, K1)) * K2;
+            const float wab = wt[0][a] * wt[1][b];
+#pragma unroll
+            for (int c = 0; c < J; ++c) {
+                const float wk = wab * wt[2][c];
+                const size_t idx = 2 * (row + c2[c]);
+                if (vn != 0.f) atomicAdd(gnum + idx, wk * vn);
+                atomicAdd(gden + idx, wk);
+            }
+        }
+    }
+}
+
+// den after origin average, maxima partials
+__global__ void k_den_max(const float2* __restrict__ acc_den, int64_t lines, int dr, int pad, int n,
+                          double inv, const double* __restrict__ means, double* __restrict__ partial) {
+    double mx = -1e308;
+    const int64_t total = lines * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(e % n);
+        const int64_t line = e / n;
+        double d = (j == n / 2) ? means[2] : (double)acc_den[line * dr + pad + j].x * inv;
+        mx = fmax(mx, d);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = sh[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+        partial[blockIdx.x] = m;
+    }
+}
+
+__global__ void k_max_final(const double* __restrict__ partial, int n, double* __restrict__ out) {
+    if (threadIdx.x) return;
+    double m = -1e308;
+    for (int i = 0; i < n; ++i) m = fmax(m, partial[i]);
+    out[0] = m;
+}
+
+// lattice = num / den where den > tol * max (pipeline.py:187-188), written at
+// the ifftshifted rho position for the centred radial FFT (radon_fourier.py:117-130)
+__global__ void k_bp_div(const float2* __restrict__ acc_num, const float2* __restrict__ acc_den,
+                         int64_t lines, int dr, int pad, int n, double inv,
+                         const double* __restrict__ means, const double* __restrict__ dmax,
+                         double tol, float2* __restrict__ out) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= lines * n) return;
+    const int j = (int)(e % n);
+    const int64_t line = e / n;
+    double nr, ni, d;
+    if (j == n / 2) {
+        nr = means[0];
+        ni = means[1];
+        d = means[2];
+    } else {
+        float2 a = acc_num[line * dr + pad + j];
+        nr = a.x * inv;
+        ni = a.y * inv;
+        d = (double)acc_den[line * dr + pad + j].x * inv;
+    }
+    float2 v = make_float2(0.f, 0.f);
+    if (d > tol * dmax[0]) v = make_float2((float)(nr / d), (float)(ni / d));
+    out[line * n + (j - n / 2 + n) % n] = v;
+}
+
+// y for the 3D adjoint: fftshift(FFT) * d_rho * (-i omega apod c3) * sin(theta)
+// * trilinear * conj(centre phase) * conj(plan phase)   (pipeline.py:189-210)
+struct BpSrc : RadialSrc {
+    const float2* X;
+    const float* q;        // per rho bin: omega * apod * c3 * d_rho
+    const float* sin_th;
+    double pc[3];
+    int tri;
+    CBN_D float2 value(int64_t i, const double (&w)[3], const RadialSrc::Aux& a) const {
+        const int64_t line = i / n_rho;
+        float2 x = X[line * n_rho + (a.ir - n_rho / 2 + n_rho) % n_rho];
+        const float qq = q[a.ir] * sin_th[a.it];
+        float2 v = make_float2(x.y * qq, -x.x * qq);
+        if (tri) {
+            float t = 1.f;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                float xx = (float)(a.raw[d] * (1.0 / kTwoPi));
+                float sc = xx == 0.f ? 1.f : sinpif(xx) / (3.14159265358979f * xx);
+                t *= sc * sc;
+            }
+            v = cscale(v, t);
+        }
+        double sn, cs;
+        sincos(-(w[0] * pc[0] + w[1] * pc[1] + w[2] * pc[2]), &sn, &cs);
+        return cmul(v, make_float2((float)cs, (float)sn));
+    }
+};
+
+}  // namespace
+
+void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s) {
+    build_backward_plan(p, s);
+    const cbn_projector_config& c = p->c;
+    const RadialTables& r = p->brad;
+    const UmbrellaTables& u = p->bumb;
+    GrangeatPlan& gp = p->bgr;
+    if (!gp.built) projector_fit_grangeat(p, gp, u, s);
+    const AxisPlan* rax = p->bres;
+    const int dr = r.n_rho + 2 * p->bpad;
+    const int64_t dsize = (int64_t)dr * r.n_theta * r.n_phi;
+    const int64_t kres = (int64_t)rax[0].K * rax[1].K * rax[2].K;
+    const int64_t k3 = (int64_t)p->bspec[0].K * p->bspec[1].K * p->bspec[2].K;
+    p->big.ensure((size_t)std::max(2 * kres, k3));
+    p->padded.ensure(2 * (size_t)dsize);
+    float2* acc_num = p->padded.p;
+    float2* acc_den = p->padded.p + dsize;
+    CBN_CUDA(cudaMemsetAsync(p->padded.p, 0, sizeof(float2) * 2 * dsize, s));
+    const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+    const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
+    const int nu = p->g.nu, nv = p->g.nv;
+    const int smax_r = std::max(rax[0].N, std::max(rax[1].N, rax[2].N));
+    p->s32.ensure(3 * (size_t)std::max(smax_r, p->n_vol));
+    KBSet kbr;
+    for (int d = 0; d < 3; ++d) kbr.ax[d] = rax[d].kb;
+
+    for (auto& b : projector_batches(p->g.n_views, per_view, projector_target_batch(p))) {
+        const int nbv = b.second - b.first;
+        const int64_t mb = per_view * nbv;
+        p->values.ensure((size_t)mb);
+        // ---- forward Grangeat of the batch's frames, in blocks of views
+        for (int v0 = 0; v0 < nbv; v0 += 32) {
+            const int nb = std::min(32, nbv - v0);
+            p->gr_grid.ensure((size_t)nb * Ku * Kv);
+            p->gr_t.ensure((size_t)nb * per_view);
+            const int64_t gtot = (int64_t)nb * Ku * Kv;
+            k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(
+                frames + (size_t)(b.first + v0) * nu * nv, nu, nv, Ku, Kv, gp.pu, gp.pv,
+                p->g.so_mm, gp.s32.p, gp.smax, gtot, p->gr_grid.p);
+            CBN_LAUNCH_CHECK();
+            long long kd[2] = {Ku, Kv};
+            p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_FORWARD, s);
+            GrFwdParams fp;
+            fp.n_mu = u.n_mu;
+            fp.n_t = u.n_t;
+            fp.Ku = Ku;
+            fp.Kv = Kv;
+            fp.pc0 = (double)nu / 2.0 - 0.5 - (double)(nu / 2);
+            fp.pc1 = (double)nv / 2.0 - 0.5 - (double)(nv / 2);
+            fp.pupv = (float)(gp.pu * gp.pv);
+            PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+            k_grf_gather<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, fp,
+                                                                 u.omega_t.p, nb, p->gr_t.p);
+            CBN_LAUNCH_CHECK();
+            long long nt[1] = {u.n_t};
+            p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p,
+                        CUFFT_INVERSE, s);
+            const int64_t vt = (int64_t)nb * per_view;
+            k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(p->gr_t.p, gp.w2.p, u.n_t,
+                                                          1.0 / ((double)u.n_t * u.dt), vt,
+                                                          p->values.p + (size_t)v0 * per_view);
+            CBN_LAUNCH_CHECK();
+        }
+        // ---- resample transpose of the batch (num and den)
+        UmbrellaSrc src{projector_umb_geom(p, u, r, p->bpad), b.first};
+        int nrows;
+        const int64_t* rows = projector_rows(p, mb, nrows);
+        ls_fit<3>(src, rows, nrows, rax, p->ls, p->s32.p, smax_r, s);
+        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * 2 * kres, s));
+        dispatch_j(rax[0].J, [&](auto jc) {
+            constexpr int J = decltype(jc)::value;
+            k_rs_spread2<J><<<blocks_for(mb, 256), 256, 0, s>>>(
+                reinterpret_cast<float*>(p->big.p), reinterpret_cast<float*>(p->big.p + kres), kbr,
+                src, p->values.p, mb);
+            return 0;
+        });
+        CBN_LAUNCH_CHECK();
+        long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
+        p->fft.exec(p->fft.get(3, kd3, 2), p->big.p, p->big.p, CUFFT_INVERSE, s);
+        RemapAxis ax[3];
+        const int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
+        projector_build_tables(p, kTabCropShift, rax, smax_r, s, ax, sstr);
+        launch_remap<float2, kAccumC>(3, p->big.p, acc_num, ax, 1.0f, s);
+        CBN_LAUNCH_CHECK();
+        launch_remap<float2, kAccumC>(3, p->big.p + kres, acc_den, ax, 1.0f, s);
+        CBN_LAUNCH_CHECK();
+    }
+    // ---- ifftn of the accumulated ifftshifted grids, rho crop, origin average
+    long long dd[3] = {r.n_phi, r.n_theta, dr};
+    p->fft.exec(p->fft.get(3, dd, 2), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
+    const double inv = 1.0 / (double)dsize;
+    p->red.ensure(2 * kRed + 64);
+    double* means = p->red.p + 2 * kRed;        // num re, num im, den re, den im
+    projector_column_mean(acc_num, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p, means, s);
+    projector_column_mean(acc_den, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p, means + 2, s);
+    double* dmax = means + 4;
+    k_den_max<<<kRed, 256, 0, s>>>(acc_den, r.lines(), dr, p->bpad, r.n_rho, inv, means, p->red.p);
+    CBN_LAUNCH_CHECK();
+    k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, dmax);
+    CBN_LAUNCH_CHECK();
+    const int64_t M = r.nodes();
+    p->lattice.ensure((size_t)M);
+    k_bp_div<<<blocks_for(M, 256), 256, 0, s>>>(acc_num, acc_den, r.lines(), dr, p->bpad, r.n_rho,
+                                                 inv, means, dmax, c.den_tol, p->lattice.p);
+    CBN_LAUNCH_CHECK();
+    long long nr1[1] = {r.n_rho};
+    p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_FORWARD, s);
+    // ---- ramp filter weights (pipeline.py:190-200), per rho bin incl. d_rho
+    {
+        std::vector<float> q(r.n_rho);
+        const double c3 = 1.0 / (4.0 * r.n_theta * r.n_phi * r.n_rho * r.d_rho);
+        const double corner = kPi * std::sqrt(3.0) / p->voxel;
+        for (int k = 0; k < r.n_rho; ++k) {
+            double om = (kTwoPi * (double)(k - r.n_rho / 2)) / ((double)r.n_rho * r.d_rho);
+            double ap = std::cos(kPi * std::min(std::fabs(om) / corner, 1.0) / 2.0);
+            q[k] = (float)(om * ap * ap * c3 * r.d_rho);
+        }
+        p->values.ensure((size_t)r.n_rho);
+        CBN_CUDA(cudaMemcpyAsync(p->values.p, q.data(), sizeof(float) * r.n_rho,
+                                 cudaMemcpyHostToDevice, s));
+        CBN_CUDA(cudaStreamSynchronize(s));
+    }
+    // ---- 3D type-1 NUFFT onto (2N)^3 (nufft_adjoint_chunked, nufft.py:268-282)
+    const AxisPlan* sax = p->bspec;
+    const int n = p->n_vol;
+    int nrows;
+    const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
+    ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->s32.p, n, s);
+    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
+    BpSrc bsrc;
+    static_cast<RadialSrc&>(bsrc) = r.src();
+    bsrc.X = p->lattice.p;
+    bsrc.q = p->values.p;
+    bsrc.sin_th = r.sin_theta.p;
+    for (int d = 0; d < 3; ++d) bsrc.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
+    bsrc.tri = c.basis == 0;
+    KBSet kbs;
+    for (int d = 0; d < 3; ++d) kbs.ax[d] = sax[d].kb;
+    dispatch_j(sax[0].J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        k_spread<3, J><<<blocks_for(M, 256), 256, 0, s>>>(p->big.p, kbs, bsrc, M);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
+    long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
+    p->fft.exec(p->fft.get(3, k3d, 1), p->big.p, p->big.p, CUFFT_INVERSE, s);
+    RemapAxis cax[3];
+    const int64_t cstr[3] = {(int64_t)sax[1].K * sax[2].K, sax[2].K, 1};
+    projector_build_tables(p, kTabCrop, sax, n, s, cax, cstr);
+    launch_remap<float2, kStoreRe>(3, p->big.p, vol, cax, (float)c.bp_normalization, s);
+    CBN_LAUNCH_CHECK();
+}
+
+}  // namespace cbn
+
+extern "C" int cbn_projector_grangeat_forward(cbn_projector* p, const float* frames, float* values,
+                                              int32_t nb, void* stream) {
+    using namespace cbn;
+    try {
+        CBN_REQUIRE(p && frames && values && nb >= 1, "bad argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_backward_plan(p, s);
+        GrangeatPlan& gp = p->bgr;
+        if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
+        const UmbrellaTables& u = p->bumb;
+        const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
+        const int nu = p->g.nu, nv = p->g.nv;
+        const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+        for (int v0 = 0; v0 < nb; v0 += 32) {
+            const int k = std::min(32, nb - v0);
+            p->gr_grid.ensure((size_t)k * Ku * Kv);
+            p->gr_t.ensure((size_t)k * per_view);
+            const int64_t gtot = (int64_t)k * Ku * Kv;
+            k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames + (size_t)v0 * nu * nv, nu, nv,
+                                                            Ku, Kv, gp.pu, gp.pv, p->g.so_mm,
+                                                            gp.s32.p, gp.smax, gtot, p->gr_grid.p);
+            CBN_LAUNCH_CHECK();
+            long long kd[2] = {Ku, Kv};
+            p->fft.exec(p->fft.get(2, kd, k), p->gr_grid.p, p->gr_grid.p, CUFFT_FORWARD, s);
+            GrFwdParams fp;
+            fp.n_mu = u.n_mu;
+            fp.n_t = u.n_t;
+            fp.Ku = Ku;
+            fp.Kv = Kv;
+            fp.pc0 = (double)nu / 2.0 - 0.5 - (double)(nu / 2);
+            fp.pc1 = (double)nv / 2.0 - 0.5 - (double)(nv / 2);
+            fp.pupv = (float)(gp.pu * gp.pv);
+            PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+            k_grf_gather<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, fp,
+                                                                 u.omega_t.p, k, p->gr_t.p);
+            CBN_LAUNCH_CHECK();
+            long long nt[1] = {u.n_t};
+            p->fft.exec(p->fft.get(1, nt, (long long)k * u.n_mu), p->gr_t.p, p->gr_t.p,
+                        CUFFT_INVERSE, s);
+            const int64_t vt = (int64_t)k * per_view;
+            k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(p->gr_t.p, gp.w2.p, u.n_t,
+                                                          1.0 / ((double)u.n_t * u.dt), vt,
+                                                          values + (size_t)v0 * per_view);
+            CBN_LAUNCH_CHECK();
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}

@@ -1,0 +1,914 @@
+// NUFFT cone-beam forward projector and direct backprojector on the B200.
+//
+// Forward  (pipeline.py:122-147):
+//   volume --[deapod/pad, cuFFT (2N)^3, KB J gather at radial nodes, phase *
+//   trilinear * i omega]--> radial lines --[cuFFT along rho]--> derivative
+//   Radon lattice --[origin average, rho pad, cuFFT]--> lattice spectrum;
+//   per reference view batch: [LS fit, deapod/pad, cuFFT 2x, KB J=3 gather at
+//   umbrella targets] --> umbrella values; per view: [t cuFFT, filter, 2D KB
+//   spread, cuFFT, crop/deapod/w1, ring mean] --> detector frames.
+// Backprojector (pipeline.py:150-212): the transposed chain.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "cbn_projector.h"
+
+using namespace cbn;
+
+namespace cbn {
+
+// ----------------------------------------------------------------- tables
+void RadialTables::build(int nr, int nt, int np_, double rmax, double vox, cudaStream_t s) {
+    n_rho = nr;
+    n_theta = nt;
+    n_phi = np_;
+    rho_max = rmax;
+    d_rho = 2.0 * rmax / nr;                  // RadialGridSpec.delta_rho
+    std::vector<double> h_om(nr), h_cp(np_), h_sp(np_), h_ct(nt), h_st(nt);
+    std::vector<float> h_omp(nr), h_stf(nt);
+    for (int k = 0; k < nr; ++k) {
+        // radial_omega (radon_fourier.py:46-49), then * voxel (radon_fourier.py:61)
+        double omega = (kTwoPi * (double)(k - nr / 2)) / ((double)nr * d_rho);
+        h_om[k] = omega * vox;
+        h_omp[k] = (float)omega;
+    }
+    for (int j = 0; j < nt; ++j) {
+        double th = ((double)j * kPi) / (double)nt;
+        h_ct[j] = std::cos(th);
+        h_st[j] = std::sin(th);
+        h_stf[j] = (float)h_st[j];
+    }
+    for (int k = 0; k < np_; ++k) {
+        double ph = (((double)k * 2.0) * kPi) / (double)np_;
+        h_cp[k] = std::cos(ph);
+        h_sp[k] = std::sin(ph);
+    }
+    om.upload(h_om.data(), nr, s);
+    cphi.upload(h_cp.data(), np_, s);
+    sphi.upload(h_sp.data(), np_, s);
+    cth.upload(h_ct.data(), nt, s);
+    sth.upload(h_st.data(), nt, s);
+    om_phys.upload(h_omp.data(), nr, s);
+    sin_theta.upload(h_stf.data(), nt, s);
+    CBN_CUDA(cudaStreamSynchronize(s));
+}
+
+void UmbrellaTables::build(const cbn_geometry& g, int nmu, int nt, double pitch, cudaStream_t s) {
+    n_mu = nmu;
+    n_t = nt;
+    dt = pitch;
+    std::vector<double> ca(g.n_views), sa(g.n_views), cm(nmu), sm(nmu), om(nt);
+    for (int k = 0; k < g.n_views; ++k) {
+        double a = (kTwoPi * (double)k) / (double)g.n_views;   // ConeGeometry.view_angle
+        ca[k] = std::cos(a);
+        sa[k] = std::sin(a);
+    }
+    for (int i = 0; i < nmu; ++i) {
+        double mu = ((double)i * kPi) / (double)nmu;             // umbrella_line_grid
+        cm[i] = std::cos(mu);
+        sm[i] = std::sin(mu);
+    }
+    for (int j = 0; j < nt; ++j)
+        om[j] = (kTwoPi * (double)(j - nt / 2)) / ((double)nt * pitch);   // grangeat.py:109
+    cos_a.upload(ca.data(), ca.size(), s);
+    sin_a.upload(sa.data(), sa.size(), s);
+    cos_mu.upload(cm.data(), cm.size(), s);
+    sin_mu.upload(sm.data(), sm.size(), s);
+    omega_t.upload(om.data(), om.size(), s);
+    CBN_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------- epilogues
+
+// radial spectrum -> i omega * trilinear * phase, written at the ifftshifted
+// rho position of its line (image_to_radial_spectrum + trilinear_transfer +
+// spectral_rho_derivative + the input shift of _centered_ifft).
+struct SpecOut {
+    float2* out;
+    const float* om_phys;
+    double pc[3];          // N/2 - 1/2 - N//2 per axis (centre phase * plan phase)
+    int n_rho;
+    int tri;
+    CBN_D void put(int64_t i, float2 v, const double (&w)[3], const RadialSrc::Aux& a) const {
+        double ang = w[0] * pc[0] + w[1] * pc[1] + w[2] * pc[2];
+        double sn, cs;
+        sincos(ang, &sn, &cs);
+        float2 r = cmul(v, make_float2((float)cs, (float)sn));
+        if (tri) {
+            float t = 1.f;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                float x = (float)(a.raw[d] * (1.0 / kTwoPi));
+                float sc = x == 0.f ? 1.f : sinpif(x) / (3.14159265358979f * x);
+                t *= sc * sc;
+            }
+            r = cscale(r, t);
+        }
+        const float o = om_phys[a.ir];
+        const int64_t line = i / n_rho;
+        const int k = (a.ir + n_rho - n_rho / 2) % n_rho;
+        out[line * n_rho + k] = make_float2(-r.y * o, r.x * o);
+    }
+};
+
+struct UmbOut {
+    float* vals;
+    CBN_D void put(int64_t i, float2 v, const double (&)[3], const UmbrellaSrc::Aux& a) const {
+        vals[i] = a.valid ? v.x : 0.f;   // Re(resample_apply), invalid -> 0 (pipeline.py:136-137)
+    }
+};
+
+// ----------------------------------------------------------------- kernels
+
+// lattice[line][j] = raw[line][(j - n//2) mod n] * scale   (fftshift of the IFFT)
+__global__ void k_lattice_final(const float2* __restrict__ raw, float2* __restrict__ out, int n,
+                                int64_t total, float scale) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    int j = (int)(e % n);
+    int64_t line = e / n;
+    float2 v = raw[line * n + (j - n / 2 + n) % n];
+    out[e] = make_float2(v.x * scale, v.y * scale);
+}
+
+// partial sums of src[line][col] over lines (complex, float64)
+__global__ void k_col_partial(const float2* __restrict__ src, int64_t lines, int64_t ld, int col,
+                              double* __restrict__ partial) {
+    double re = 0.0, im = 0.0;
+    for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < lines;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        float2 v = src[l * ld + col];
+        re += v.x;
+        im += v.y;
+    }
+    __shared__ double sr[32], si[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sr[threadIdx.x >> 5] = re;
+        si[threadIdx.x >> 5] = im;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += sr[w];
+            b += si[w];
+        }
+        partial[2 * blockIdx.x] = a;
+        partial[2 * blockIdx.x + 1] = b;
+    }
+}
+
+__global__ void k_partial_final(const double* __restrict__ partial, int nblk, double mul,
+                                double* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double a = 0, b = 0;
+    for (int i = 0; i < nblk; ++i) {
+        a += partial[2 * i];
+        b += partial[2 * i + 1];
+    }
+    out[0] = a * mul;
+    out[1] = b * mul;
+}
+
+constexpr int kRedBlocks = 296;
+
+// mean over lines of src[line][col] * scale -> out[0..1]
+static void column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
+                        double* partial, double* out, cudaStream_t s) {
+    k_col_partial<<<kRedBlocks, 256, 0, s>>>(src, lines, ld, col, partial);
+    CBN_LAUNCH_CHECK();
+    k_partial_final<<<1, 32, 0, s>>>(partial, kRedBlocks, scale / (double)lines, out);
+    CBN_LAUNCH_CHECK();
+}
+
+// x = pad_rho(origin_average(lattice)) (resampling.py:106-117, 144-145) in the
+// device layout [line][rho_padded]; src[line][(j + shift) % n] * scale is the
+// lattice value at rho index j.
+__global__ void k_pad_lattice(const float2* __restrict__ src, int shift, float scale, int n,
+                              int pad, int dr, int64_t total, const double* __restrict__ mean,
+                              float2* __restrict__ out) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    int r = (int)(e % dr);
+    int64_t line = e / dr;
+    int j = r - pad;
+    float2 v = make_float2(0.f, 0.f);
+    if (j >= 0 && j < n) {
+        if (j == n / 2) {
+            v = make_float2((float)mean[0], (float)mean[1]);
+        } else {
+            float2 g = src[line * n + (j + shift) % n];
+            v = make_float2(g.x * scale, g.y * scale);
+        }
+    }
+    out[e] = v;
+}
+
+// ---- reverse Grangeat (grangeat.py:149-170)
+struct GrRevParams {
+    int n_mu, n_t;
+    int nu, nv, Ku, Kv;
+    double pc0, pc1;       // conj(centre phase) * conj(plan phase): exp(-i w.pc)
+    const float* q;        // per t: -sign(omega) taper dt c2  (y = S * i q)
+};
+
+__global__ void k_gr_pre(const float* __restrict__ vals, const float* __restrict__ w2, int n_t,
+                         int64_t total, float2* __restrict__ out) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    int j = (int)(e % n_t);
+    int64_t row = e / n_t;
+    out[row * n_t + (j - n_t / 2 + n_t) % n_t] = make_float2(vals[e] / w2[j], 0.f);
+}
+
+template <int J>
+__global__ void __launch_bounds__(256)
+k_gr_spread(float2* __restrict__ grids, KBSet kb, PolarSrc src, const float2* __restrict__ tf,
+            GrRevParams p, int nb) {
+    const int64_t m = (int64_t)p.n_mu * p.n_t;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double w[2];
+    PolarSrc::Aux aux;
+    src.node(i, w, aux);
+    const float q = p.q[aux.jt];
+    if (q == 0.f) return;
+    double sn, cs;
+    sincos(-(w[0] * p.pc0 + w[1] * p.pc1), &sn, &cs);
+    // factor = phase * (i q)
+    const float2 fac = make_float2(-(float)sn * q, (float)cs * q);
+    int first[2];
+    float wt[2][J];
+    tap_setup<2, J>(kb, w, first, wt);
+    int c1[J];
+#pragma unroll
+    for (int b = 0; b < J; ++b) c1[b] = wrapc(first[1] + b, p.Kv);
+    const int im = (int)(i / p.n_t);
+    const int col = (aux.jt - p.n_t / 2 + p.n_t) % p.n_t;   // fftshift of the t FFT
+    const size_t gsz = (size_t)p.Ku * p.Kv;
+    for (int v = 0; v < nb; ++v) {
+        float2 val = cmul(tf[((size_t)v * p.n_mu + im) * p.n_t + col], fac);
+        float2* grid = grids + v * gsz;
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            float2* row = grid + (size_t)wrapc(first[0] + a, p.Ku) * p.Kv;
+            float2 va = cscale(val, wt[0][a]);
+#pragma unroll
+            for (int b = 0; b < J; ++b) atomicAdd(row + c1[b], cscale(va, wt[1][b]));
+        }
+    }
+}
+
+CBN_D double w1_at(int u, int v, int nu, int nv, double pu, double pv, double so) {
+    double uc = (((double)u - (double)nu / 2.0) + 0.5) * pu;
+    double vc = (((double)v - (double)nv / 2.0) + 0.5) * pv;
+    return so / sqrt(so * so + uc * uc + vc * vc);
+}
+
+struct GrPost {
+    int nu, nv, Ku, Kv, smax;
+    double pu, pv, so;
+    const float* s32;   // 2 x smax
+};
+
+CBN_D float gr_value(const float2* grid, const GrPost& p, int u, int v) {
+    int gu = (u - p.nu / 2 + p.Ku) % p.Ku;
+    int gv = (v - p.nv / 2 + p.Kv) % p.Kv;
+    float re = grid[(size_t)gu * p.Kv + gv].x * p.s32[u] * p.s32[p.smax + v];
+    return (float)((double)re / w1_at(u, v, p.nu, p.nv, p.pu, p.pv, p.so));
+}
+
+// mean of the outermost detector ring per view (grangeat.py:167-169)
+__global__ void k_gr_ring(const float2* __restrict__ grids, GrPost p, double* __restrict__ mean) {
+    const int v = blockIdx.x;
+    const float2* grid = grids + (size_t)v * p.Ku * p.Kv;
+    const int nring = p.nu == 1 || p.nv == 1 ? p.nu * p.nv : 2 * p.nu + 2 * p.nv - 4;
+    double acc = 0.0;
+    for (int r = threadIdx.x; r < nring; r += blockDim.x) {
+        int u, w;
+        if (p.nu == 1 || p.nv == 1) {
+            u = r / p.nv;
+            w = r % p.nv;
+        } else if (r < p.nv) {
+            u = 0;
+            w = r;
+        } else if (r < 2 * p.nv) {
+            u = p.nu - 1;
+            w = r - p.nv;
+        } else {
+            int k = r - 2 * p.nv;   // columns 0 and nv-1 of rows 1..nu-2
+            u = 1 + k / 2;
+            w = (k & 1) ? p.nv - 1 : 0;
+        }
+        acc += gr_value(grid, p, u, w);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        mean[v] = t / nring;
+    }
+}
+
+__global__ void k_gr_frame(const float2* __restrict__ grids, GrPost p,
+                           const double* __restrict__ mean, float norm, float* __restrict__ frames,
+                           int64_t total, int* __restrict__ flag) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int64_t per = (int64_t)p.nu * p.nv;
+    const int v = (int)(e / per);
+    const int rem = (int)(e % per);
+    const int u = rem / p.nv, w = rem % p.nv;
+    float g = gr_value(grids + (size_t)v * p.Ku * p.Kv, p, u, w);
+    float out = (float)((double)g - mean[v]) * norm;
+    if (!isfinite(out)) atomicOr(flag, 1);
+    frames[e] = out;
+}
+
+}  // namespace cbn
+
+// =================================================================== plan
+
+namespace {
+
+using P = cbn_projector_s;
+
+int64_t spectrum_chunk(const P* p, int64_t m) {
+    int64_t ch = p->c.plan_chunk > 0 ? p->c.plan_chunk : (int64_t)1 << 21;
+    return std::min(m, ch);
+}
+
+std::vector<std::pair<int, int>> view_batches(int n_views, int64_t per_view, int64_t target) {
+    int64_t step = std::max<int64_t>(1, target / per_view);
+    std::vector<std::pair<int, int>> out;
+    for (int64_t lo = 0; lo < n_views; lo += step)
+        out.emplace_back((int)lo, (int)std::min<int64_t>(lo + step, n_views));
+    return out;
+}
+
+int64_t target_batch(const P* p) { return p->c.target_batch > 0 ? p->c.target_batch : (int64_t)1 << 20; }
+
+const int64_t* rows_for(P* p, int64_t m, int& n) {
+    auto it = p->ls_rows.find(m);
+    if (it == p->ls_rows.end())
+        throw Error(CBN_EINVAL, "scaling-fit rows for a " + std::to_string(m) +
+                                    "-node plan were not supplied (cbn_projector_set_ls_rows)");
+    n = (int)it->second->n;
+    return it->second->p;
+}
+
+void add_needed(P* p, int64_t m) {
+    if (std::find(p->ls_needed.begin(), p->ls_needed.end(), m) == p->ls_needed.end())
+        p->ls_needed.push_back(m);
+}
+
+int rho_pad_of(int cfg_pad, int n_rho) { return cfg_pad < 0 ? n_rho / 2 : cfg_pad; }
+
+void require_uniform(const int32_t* j, const char* what) {
+    if (!(j[0] == j[1] && j[1] == j[2]))
+        throw Error(CBN_EUNSUPPORTED, std::string(what) + ": per-axis tap counts must be equal");
+}
+
+UmbrellaGeom umb_geom(const P* p, const UmbrellaTables& u, const RadialTables& r, int pad) {
+    UmbrellaGeom g;
+    g.cos_a = u.cos_a.p;
+    g.sin_a = u.sin_a.p;
+    g.cos_mu = u.cos_mu.p;
+    g.sin_mu = u.sin_mu.p;
+    g.so = p->g.so_mm;
+    g.dt = u.dt;
+    g.n_mu = u.n_mu;
+    g.n_t = u.n_t;
+    g.rho_max = r.rho_max;
+    g.d_rho = r.d_rho;
+    g.n_rho = r.n_rho;
+    g.n_theta = r.n_theta;
+    g.n_phi = r.n_phi;
+    g.pad = pad;
+    g.padded[0] = (double)(r.n_rho + 2 * pad);
+    g.padded[1] = (double)r.n_theta;
+    g.padded[2] = (double)r.n_phi;
+    return g;
+}
+
+void build_grangeat(P* p, GrangeatPlan& gp, const UmbrellaTables& u, int taper, cudaStream_t s) {
+    gp.ax[0] = make_axis(p->g.nu, 5, 2.0);    // plan_grangeat j=(5,5), oversample 2 (grangeat.py:93-118)
+    gp.ax[1] = make_axis(p->g.nv, 5, 2.0);
+    gp.kb.ax[0] = gp.ax[0].kb;
+    gp.kb.ax[1] = gp.ax[1].kb;
+    gp.smax = std::max(p->g.nu, p->g.nv);
+    gp.pu = p->pu;
+    gp.pv = p->pv;
+    gp.m = (int64_t)u.n_mu * u.n_t;
+    gp.s32.alloc(2 * (size_t)gp.smax);
+    std::vector<double> om(u.n_t);
+    CBN_CUDA(cudaMemcpy(om.data(), u.omega_t.p, sizeof(double) * u.n_t, cudaMemcpyDeviceToHost));
+    double amax = 0;
+    for (double o : om) amax = std::max(amax, std::fabs(o));
+    const double c2 = 1.0 / (2.0 * u.n_mu * u.n_t * u.dt);
+    std::vector<float> w2(u.n_t), q(u.n_t);
+    const double so = p->g.so_mm;
+    for (int j = 0; j < u.n_t; ++j) {
+        double t = (double)(j - u.n_t / 2) * u.dt;
+        w2[j] = (float)((so * so + t * t) / (so * so));
+        double tp = 1.0;
+        if (taper == 1) {
+            double cv = std::cos(kPi * om[j] / (2.0 * amax));
+            tp = cv * cv;
+        }
+        double sg = om[j] > 0 ? 1.0 : (om[j] < 0 ? -1.0 : 0.0);
+        q[j] = (float)(-sg * tp * u.dt * c2);
+    }
+    gp.w2.upload(w2.data(), w2.size(), s);
+    gp.fac_im.upload(q.data(), q.size(), s);
+    CBN_CUDA(cudaStreamSynchronize(s));
+}
+
+void fit_grangeat(P* p, GrangeatPlan& gp, const UmbrellaTables& u, cudaStream_t s) {
+    int n;
+    const int64_t* rows = rows_for(p, gp.m, n);
+    PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+    ls_fit<2>(src, rows, n, gp.ax, p->ls, gp.s32.p, gp.smax, s);
+    gp.built = true;
+}
+
+void build_forward(P* p, cudaStream_t s) {
+    if (p->fw_built) return;
+    const cbn_projector_config& c = p->c;
+    CBN_REQUIRE(c.method == 0, "only method 'a' runs on the device");
+    CBN_REQUIRE(c.spectrum_j >= 2 && c.spectrum_j <= 8, "spectrum_j must be 2..8");
+    require_uniform(c.resample_j, "resample_j");
+    p->frad.build(c.spec.n_rho, c.spec.n_theta, c.spec.n_phi, c.spec.rho_max, p->voxel, s);
+    const double dt = c.t_pitch_mm > 0 ? c.t_pitch_mm : p->pu;
+    p->fumb.build(p->g, c.n_mu, c.n_t, dt, s);
+    for (int d = 0; d < 3; ++d) p->fspec[d] = make_axis(p->n_vol, c.spectrum_j, c.oversample_factor);
+    p->fpad = rho_pad_of(c.rho_pad, c.spec.n_rho);
+    const int dr = c.spec.n_rho + 2 * p->fpad;
+    p->fres[0] = make_axis(c.spec.n_phi, c.resample_j[2], c.oversample_factor);
+    p->fres[1] = make_axis(c.spec.n_theta, c.resample_j[1], c.oversample_factor);
+    p->fres[2] = make_axis(dr, c.resample_j[0], c.oversample_factor);
+    build_grangeat(p, p->fgr, p->fumb, c.t_taper, s);
+    p->fw_built = true;
+}
+
+void build_backward(P* p, cudaStream_t s) {
+    if (p->bw_built) return;
+    const cbn_projector_config& c = p->c;
+    CBN_REQUIRE(c.method == 0, "only method 'a' runs on the device");
+    require_uniform(c.resample_j, "resample_j");
+    const int out = p->n_vol;
+    const double extent = out * p->voxel;
+    const int n_rho = 2 * (int)std::ceil(1.5 * out / 2.0);                 // pipeline.py:165
+    p->brad.build(n_rho, c.spec.n_theta, c.spec.n_phi, extent * std::sqrt(3.0) / 2.0, p->voxel, s);
+    p->bumb.build(p->g, c.n_mu, 2 * p->g.nu, p->pu, s);                    // pipeline.py:168
+    for (int d = 0; d < 3; ++d) p->bspec[d] = make_axis(out, c.spectrum_j, c.oversample_factor);
+    p->bpad = std::min(n_rho / 8, 32);                                       // pipeline.py:169
+    const int dr = n_rho + 2 * p->bpad;
+    p->bres[0] = make_axis(c.spec.n_phi, c.resample_j[2], c.oversample_factor);
+    p->bres[1] = make_axis(c.spec.n_theta, c.resample_j[1], c.oversample_factor);
+    p->bres[2] = make_axis(dr, c.resample_j[0], c.oversample_factor);
+    build_grangeat(p, p->bgr, p->bumb, 0, s);
+    p->bw_built = true;
+}
+
+void compute_needed(P* p) {
+    const cbn_projector_config& c = p->c;
+    p->ls_needed.clear();
+    if (p->direction & 1) {
+        int64_t M = (int64_t)c.spec.n_rho * c.spec.n_theta * c.spec.n_phi;
+        add_needed(p, spectrum_chunk(p, M));
+        int64_t per_view = (int64_t)c.n_mu * c.n_t;
+        for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p)))
+            add_needed(p, per_view * (b.second - b.first));
+        add_needed(p, per_view);
+    }
+    if (p->direction & 2) {
+        const int n_rho = 2 * (int)std::ceil(1.5 * p->n_vol / 2.0);
+        int64_t M = (int64_t)n_rho * c.spec.n_theta * c.spec.n_phi;
+        add_needed(p, spectrum_chunk(p, M));
+        int64_t per_view = (int64_t)c.n_mu * 2 * p->g.nu;
+        for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p)))
+            add_needed(p, per_view * (b.second - b.first));
+        add_needed(p, per_view);
+    }
+}
+
+// per-axis tables from the scalings in p->s32 (stride smax) for one mode
+void build_tables(P* p, int mode, const AxisPlan* ax, int smax, cudaStream_t s, RemapAxis* out,
+                  const int64_t* sstride) {
+    size_t need = 0;
+    for (int d = 0; d < 3; ++d) need += (mode == kTabPad || mode == kTabPadShift) ? ax[d].K : ax[d].N;
+    p->tab_idx.ensure(need);
+    p->tab_sc.ensure(need);
+    size_t off = 0;
+    for (int d = 0; d < 3; ++d) {
+        int n = (mode == kTabPad || mode == kTabPadShift) ? ax[d].K : ax[d].N;
+        build_table(mode, ax[d].N, ax[d].K, p->s32.p + (size_t)d * smax, p->tab_idx.p + off,
+                    p->tab_sc.p + off, s);
+        out[d].idx = p->tab_idx.p + off;
+        out[d].scale = p->tab_sc.p + off;
+        out[d].n = n;
+        out[d].sstride = sstride[d];
+        off += n;
+    }
+}
+
+int smax_of(const AxisPlan* ax) { return std::max(ax[0].N, std::max(ax[1].N, ax[2].N)); }
+
+int64_t ktot(const AxisPlan* ax) { return (int64_t)ax[0].K * ax[1].K * ax[2].K; }
+
+// ---------------------------------------------------------------- forward
+
+// radial lattice in raw layout (IFFT output, ifftshifted rho) into p->lattice
+void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
+    const RadialTables& r = p->frad;
+    const AxisPlan* ax = p->fspec;
+    const int64_t M = r.nodes();
+    const int n = p->n_vol;
+    const int64_t K3 = ktot(ax);
+    p->big.ensure((size_t)K3);
+    p->lattice.ensure((size_t)M);
+    const int smax = n;
+    p->s32.ensure(3 * (size_t)smax);
+    // scaling fit on the first sub-plan of nufft_forward_chunked (nufft.py:250-265)
+    int nrows;
+    const int64_t* rows = rows_for(p, spectrum_chunk(p, M), nrows);
+    ls_fit<3>(r.src(), rows, nrows, ax, p->ls, p->s32.p, smax, s);
+    RemapAxis rax[3];
+    const int64_t sstr[3] = {(int64_t)n * n, n, 1};
+    build_tables(p, kTabPad, ax, smax, s, rax, sstr);
+    launch_remap<float, kStoreC>(3, vol, p->big.p, rax, 1.0f, s);
+    CBN_LAUNCH_CHECK();
+    long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    SpecOut epi;
+    epi.out = p->lattice.p;
+    epi.om_phys = r.om_phys.p;
+    for (int d = 0; d < 3; ++d) epi.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
+    epi.n_rho = r.n_rho;
+    epi.tri = p->c.basis == 0;
+    KBSet kb;
+    for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
+    dispatch_j(ax[0].J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        k_gather<3, J><<<blocks_for(M, 256), 256, 0, s>>>(p->big.p, kb, r.src(), epi, M);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
+    // centred IFFT along rho (radon_fourier.py:122-124,133-135); 1/(n d_rho) applied by consumers
+    long long nr1[1] = {r.n_rho};
+    p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_INVERSE, s);
+}
+
+// lattice spectrum for resampling: fftn(pad(origin_avg(lattice))) into p->padded
+// (src/shift/scale describe how to read the lattice value at rho index j)
+void lattice_spectrum(P* p, const float2* src, int shift, float scale, cudaStream_t s) {
+    const RadialTables& r = p->frad;
+    const int dr = r.n_rho + 2 * p->fpad;
+    const int64_t total = r.lines() * dr;
+    p->padded.ensure((size_t)total);
+    p->red.ensure(2 * kRedBlocks + 64);
+    double* mean = p->red.p + 2 * kRedBlocks;
+    column_mean(src, r.lines(), r.n_rho, (r.n_rho / 2 + shift) % r.n_rho, scale, p->red.p, mean, s);
+    k_pad_lattice<<<blocks_for(total, 256), 256, 0, s>>>(src, shift, scale, r.n_rho, p->fpad, dr,
+                                                         total, mean, p->padded.p);
+    CBN_LAUNCH_CHECK();
+    long long dims[3] = {r.n_phi, r.n_theta, dr};
+    p->fft.exec(p->fft.get(3, dims, 1), p->padded.p, p->padded.p, CUFFT_FORWARD, s);
+}
+
+// Re(resample_apply) for views [lo, hi) of reference batch [blo, bhi) -> vals
+void resample_batch(P* p, int blo, int bhi, int lo, int hi, float* vals, cudaStream_t s) {
+    const RadialTables& r = p->frad;
+    const AxisPlan* ax = p->fres;
+    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+    const int64_t mb = per_view * (bhi - blo);
+    const int smax = smax_of(ax);
+    p->s32.ensure(3 * (size_t)smax);
+    UmbrellaSrc fit_src{umb_geom(p, p->fumb, r, p->fpad), blo};
+    int nrows;
+    const int64_t* rows = rows_for(p, mb, nrows);
+    ls_fit<3>(fit_src, rows, nrows, ax, p->ls, p->s32.p, smax, s);
+    const int dr = r.n_rho + 2 * p->fpad;
+    RemapAxis rax[3];
+    const int64_t sstr[3] = {(int64_t)r.n_theta * dr, dr, 1};
+    build_tables(p, kTabPadShift, ax, smax, s, rax, sstr);
+    const int64_t kt = ktot(ax);
+    p->big.ensure((size_t)kt);
+    const double size = (double)dr * r.n_theta * r.n_phi;
+    launch_remap<float2, kStoreC>(3, p->padded.p, p->big.p, rax, (float)(1.0 / size), s);
+    CBN_LAUNCH_CHECK();
+    long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    UmbrellaSrc src{umb_geom(p, p->fumb, r, p->fpad), lo};
+    const int64_t m = per_view * (hi - lo);
+    KBSet kb;
+    for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
+    dispatch_j(ax[0].J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        k_gather<3, J><<<blocks_for(m, 256), 256, 0, s>>>(p->big.p, kb, src, UmbOut{vals}, m);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
+}
+
+GrPost gr_post(const P* p, const GrangeatPlan& gp) {
+    GrPost q;
+    q.nu = p->g.nu;
+    q.nv = p->g.nv;
+    q.Ku = gp.ax[0].K;
+    q.Kv = gp.ax[1].K;
+    q.smax = gp.smax;
+    q.pu = gp.pu;
+    q.pv = gp.pv;
+    q.so = p->g.so_mm;
+    q.s32 = gp.s32.p;
+    return q;
+}
+
+// reverse_grangeat_view for nb views: vals (nb x n_mu x n_t) -> frames (nb x nu x nv)
+void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s) {
+    GrangeatPlan& gp = p->fgr;
+    if (!gp.built) fit_grangeat(p, gp, p->fumb, s);
+    const UmbrellaTables& u = p->fumb;
+    const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
+    const int64_t tl = (int64_t)nb * u.n_mu * u.n_t;
+    p->gr_t.ensure((size_t)tl);
+    p->gr_grid.ensure((size_t)nb * Ku * Kv);
+    k_gr_pre<<<blocks_for(tl, 256), 256, 0, s>>>(vals, gp.w2.p, u.n_t, tl, p->gr_t.p);
+    CBN_LAUNCH_CHECK();
+    long long nt[1] = {u.n_t};
+    p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_FORWARD, s);
+    CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
+    GrRevParams rp;
+    rp.n_mu = u.n_mu;
+    rp.n_t = u.n_t;
+    rp.nu = p->g.nu;
+    rp.nv = p->g.nv;
+    rp.Ku = Ku;
+    rp.Kv = Kv;
+    rp.pc0 = (double)p->g.nu / 2.0 - 0.5 - (double)(p->g.nu / 2);
+    rp.pc1 = (double)p->g.nv / 2.0 - 0.5 - (double)(p->g.nv / 2);
+    rp.q = gp.fac_im.p;
+    PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+    k_gr_spread<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, p->gr_t.p, rp, nb);
+    CBN_LAUNCH_CHECK();
+    long long kd[2] = {Ku, Kv};
+    p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_INVERSE, s);
+    GrPost q = gr_post(p, gp);
+    p->red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
+    double* mean = p->red.p + 2 * kRedBlocks + 64;
+    k_gr_ring<<<nb, 256, 0, s>>>(p->gr_grid.p, q, mean);
+    CBN_LAUNCH_CHECK();
+    const int64_t total = (int64_t)nb * p->g.nu * p->g.nv;
+    k_gr_frame<<<blocks_for(total, 256), 256, 0, s>>>(p->gr_grid.p, q, mean,
+                                                      (float)p->c.normalization, frames, total,
+                                                      p->flag.p);
+    CBN_LAUNCH_CHECK();
+}
+
+void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s) {
+    build_forward(p, s);
+    p->flag.ensure(1);
+    CBN_CUDA(cudaMemsetAsync(p->flag.p, 0, sizeof(int), s));
+    radial_lattice_raw(p, vol, s);
+    const RadialTables& r = p->frad;
+    lattice_spectrum(p, p->lattice.p, r.n_rho - r.n_rho / 2, (float)(1.0 / (r.n_rho * r.d_rho)), s);
+    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+    const size_t frame_sz = (size_t)p->g.nu * p->g.nv;
+    for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p))) {
+        int vlo = std::max(lo, b.first), vhi = std::min(hi, b.second);
+        if (vlo >= vhi) continue;
+        p->values.ensure((size_t)per_view * (vhi - vlo));
+        resample_batch(p, b.first, b.second, vlo, vhi, p->values.p, s);
+        const int blk = 32;
+        for (int v = vlo; v < vhi; v += blk) {
+            int nb = std::min(blk, vhi - v);
+            grangeat_reverse(p, p->values.p + (size_t)(v - vlo) * per_view,
+                             frames + (size_t)(v - lo) * frame_sz, nb, s);
+        }
+    }
+    int flag = 0;
+    CBN_CUDA(cudaMemcpyAsync(&flag, p->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    if (flag) throw Error(CBN_ENONFINITE, "non-finite projection values");
+}
+
+}  // namespace
+
+// backprojector lives in cbn_backproject.cu
+namespace cbn {
+void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s);
+void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
+const int64_t* projector_rows(cbn_projector_s* p, int64_t m, int& n) { return rows_for(p, m, n); }
+std::vector<std::pair<int, int>> projector_batches(int n_views, int64_t per_view, int64_t target) {
+    return view_batches(n_views, per_view, target);
+}
+int64_t projector_chunk(const cbn_projector_s* p, int64_t m) { return spectrum_chunk(p, m); }
+int64_t projector_target_batch(const cbn_projector_s* p) { return target_batch(p); }
+UmbrellaGeom projector_umb_geom(const cbn_projector_s* p, const UmbrellaTables& u,
+                                const RadialTables& r, int pad) {
+    return umb_geom(p, u, r, pad);
+}
+void projector_build_tables(cbn_projector_s* p, int mode, const AxisPlan* ax, int smax,
+                            cudaStream_t s, RemapAxis* out, const int64_t* sstride) {
+    build_tables(p, mode, ax, smax, s, out, sstride);
+}
+void projector_fit_grangeat(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
+                            cudaStream_t s) {
+    fit_grangeat(p, gp, u, s);
+}
+void projector_column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
+                           double* partial, double* out, cudaStream_t s) {
+    column_mean(src, lines, ld, col, scale, partial, out, s);
+}
+}  // namespace cbn
+
+// =================================================================== C ABI
+extern "C" {
+
+int cbn_projector_create(cbn_projector** out, const cbn_geometry* geom,
+                         const cbn_projector_config* cfg, int32_t n_vol, double voxel_mm,
+                         int32_t direction) {
+    try {
+        CBN_REQUIRE(out && geom && cfg, "null argument");
+        CBN_REQUIRE(geom->so_mm > 0 && geom->sd_mm > geom->so_mm, "invalid geometry");
+        CBN_REQUIRE(geom->nu >= 1 && geom->nv >= 1 && geom->n_views >= 1, "invalid detector");
+        CBN_REQUIRE(cfg->spec.n_rho >= 2 && cfg->spec.n_rho % 2 == 0, "n_rho must be even and >= 2");
+        CBN_REQUIRE(cfg->spec.n_theta >= 1 && cfg->spec.n_phi >= 1, "n_theta, n_phi must be >= 1");
+        CBN_REQUIRE(cfg->spec.rho_max > 0, "rho_max must be positive");
+        CBN_REQUIRE(cfg->n_mu >= 1 && cfg->n_t >= 1, "n_mu and n_t must be >= 1");
+        CBN_REQUIRE(n_vol >= 1 && voxel_mm > 0, "invalid volume size");
+        CBN_REQUIRE(direction >= 1 && direction <= 3, "direction must be 1..3");
+        CBN_REQUIRE(cfg->oversample_factor >= 1.0, "oversample_factor must be >= 1");
+        auto p = std::make_unique<cbn_projector_s>();
+        p->g = *geom;
+        p->c = *cfg;
+        p->n_vol = n_vol;
+        p->voxel = voxel_mm;
+        p->direction = direction;
+        const double mag = geom->sd_mm / geom->so_mm;
+        p->pu = (geom->det_width_mm / geom->nu) / mag;
+        p->pv = (geom->det_height_mm / geom->nv) / mag;
+        compute_needed(p.get());
+        *out = p.release();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_destroy(cbn_projector* proj) {
+    delete proj;
+    return CBN_OK;
+}
+
+int cbn_projector_ls_sizes(const cbn_projector* p, int64_t* sizes, int32_t* count) {
+    try {
+        CBN_REQUIRE(p && count, "null argument");
+        int cap = *count;
+        *count = (int32_t)p->ls_needed.size();
+        if (sizes)
+            for (int i = 0; i < std::min<int>(cap, *count); ++i) sizes[i] = p->ls_needed[i];
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_set_ls_rows(cbn_projector* p, int64_t m, const int64_t* rows, int64_t n) {
+    try {
+        CBN_REQUIRE(p && rows, "null argument");
+        CBN_REQUIRE(n >= 1 && n <= kMaxLS && n <= m, "row count must be 1..min(m, 8192)");
+        for (int64_t i = 0; i < n; ++i) CBN_REQUIRE(rows[i] >= 0 && rows[i] < m, "row out of range");
+        auto* buf = new DevBuf<int64_t>();
+        buf->alloc((size_t)n);
+        CBN_CUDA(cudaMemcpy(buf->p, rows, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+        auto it = p->ls_rows.find(m);
+        if (it != p->ls_rows.end()) delete it->second;
+        p->ls_rows[m] = buf;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_scratch_bytes(const cbn_projector* p, int64_t* bytes) {
+    try {
+        CBN_REQUIRE(p && bytes, "null argument");
+        *bytes = (int64_t)(p->big.bytes() + p->lattice.bytes() + p->padded.bytes() +
+                           p->gr_t.bytes() + p->gr_grid.bytes() + p->values.bytes());
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_project(cbn_projector* p, const float* vol, float* frames, int32_t lo, int32_t hi,
+                        void* stream) {
+    try {
+        CBN_REQUIRE(p && vol && frames, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        forward_project(p, vol, frames, lo, hi, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject(cbn_projector* p, const float* frames, float* vol, void* stream) {
+    try {
+        CBN_REQUIRE(p && vol && frames, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        backproject_impl(p, frames, vol, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_radial_lattice(cbn_projector* p, const float* vol, void* lattice, void* stream) {
+    try {
+        CBN_REQUIRE(p && vol && lattice, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        radial_lattice_raw(p, vol, s);
+        const RadialTables& r = p->frad;
+        const int64_t M = r.nodes();
+        k_lattice_final<<<blocks_for(M, 256), 256, 0, s>>>(p->lattice.p, static_cast<float2*>(lattice),
+                                                           r.n_rho, M,
+                                                           (float)(1.0 / (r.n_rho * r.d_rho)));
+        CBN_LAUNCH_CHECK();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_resample_views(cbn_projector* p, const void* lattice, float* values, int32_t lo,
+                                 int32_t hi, void* stream) {
+    try {
+        CBN_REQUIRE(p && lattice && values, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        lattice_spectrum(p, static_cast<const float2*>(lattice), 0, 1.0f, s);
+        const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+        for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p))) {
+            int vlo = std::max<int>(lo, b.first), vhi = std::min<int>(hi, b.second);
+            if (vlo >= vhi) continue;
+            resample_batch(p, b.first, b.second, vlo, vhi, values + (size_t)(vlo - lo) * per_view, s);
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_grangeat_reverse(cbn_projector* p, const float* values, float* frames,
+                                   int32_t nb, void* stream) {
+    try {
+        CBN_REQUIRE(p && values && frames && nb >= 1, "bad argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        p->flag.ensure(1);
+        CBN_CUDA(cudaMemsetAsync(p->flag.p, 0, sizeof(int), s));
+        const size_t per_view = (size_t)p->fumb.n_mu * p->fumb.n_t;
+        const size_t fsz = (size_t)p->g.nu * p->g.nv;
+        for (int v = 0; v < nb; v += 32) {
+            int k = std::min(32, nb - v);
+            grangeat_reverse(p, values + v * per_view, frames + v * fsz, k, s);
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_stage_times(const cbn_projector* p, double* ms, int32_t* count, char* names,
+                              int32_t names_len) {
+    try {
+        CBN_REQUIRE(p && count, "null argument");
+        *count = 0;
+        if (names && names_len > 0) names[0] = 0;
+        (void)ms;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"

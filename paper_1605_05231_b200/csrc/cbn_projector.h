@@ -1,0 +1,99 @@
+// Projector plan: device state of nufft_forward_project / nufft_backproject
+// (pipeline.py:122-212).  See DESIGN.md for the data layout.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "cbn_plan.h"
+#include "cbn_sources.cuh"
+
+namespace cbn {
+
+// Radial lattice spec + the node tables of its 3D NUFFT (radon_fourier.py:46-67).
+struct RadialTables {
+    int n_rho = 0, n_theta = 0, n_phi = 0;
+    double rho_max = 0, d_rho = 0;
+    DevBuf<double> om, cphi, sphi, cth, sth;   // float64 node tables
+    DevBuf<float> om_phys;                      // radial_omega (rad / mm)
+    DevBuf<float> sin_theta;                    // sin(theta) as float
+    int64_t lines() const { return (int64_t)n_theta * n_phi; }
+    int64_t nodes() const { return lines() * n_rho; }
+    void build(int n_rho, int n_theta, int n_phi, double rho_max, double voxel, cudaStream_t s);
+    RadialSrc src() const { return RadialSrc{om.p, cphi.p, sphi.p, cth.p, sth.p, n_rho, n_theta}; }
+};
+
+// Umbrella line grid of one direction (forward: cfg t grid; back: detector grid).
+struct UmbrellaTables {
+    int n_mu = 0, n_t = 0;
+    double dt = 0;
+    DevBuf<double> cos_a, sin_a, cos_mu, sin_mu, omega_t;
+    void build(const cbn_geometry& g, int n_mu, int n_t, double dt, cudaStream_t s);
+};
+
+// 2D NUFFT of the per-view Grangeat step (grangeat.py:93-128).
+struct GrangeatPlan {
+    AxisPlan ax[2];
+    KBSet kb{};
+    DevBuf<float> s32;     // 2 x smax
+    int smax = 0;
+    double pu = 0, pv = 0;
+    int64_t m = 0;
+    DevBuf<float> w2, fac_re, fac_im;   // per t: post-weight, reverse filter (complex)
+    bool built = false;
+};
+
+struct cbn_projector_impl;
+
+}  // namespace cbn
+
+struct cbn_projector_s {
+    cbn_geometry g{};
+    cbn_projector_config c{};
+    int n_vol = 0;
+    double voxel = 0;
+    int direction = 0;
+    double pu = 0, pv = 0;   // virtual pixel pitch
+
+    std::map<int64_t, cbn::DevBuf<int64_t>*> ls_rows;
+    std::vector<int64_t> ls_needed;
+
+    cbn::FFTCache fft;
+    cbn::LSScratch ls;
+
+    // ---- forward
+    cbn::RadialTables frad;
+    cbn::UmbrellaTables fumb;
+    cbn::GrangeatPlan fgr;
+    cbn::AxisPlan fspec[3];     // spectrum NUFFT axes (N = n_vol)
+    cbn::AxisPlan fres[3];      // resample NUFFT axes, device order (phi, theta, rho_padded)
+    int fpad = 0;
+    bool fw_built = false;
+
+    // ---- back
+    cbn::RadialTables brad;
+    cbn::UmbrellaTables bumb;
+    cbn::GrangeatPlan bgr;
+    cbn::AxisPlan bspec[3];
+    cbn::AxisPlan bres[3];
+    int bpad = 0;
+    bool bw_built = false;
+
+    // ---- scratch (shared by both directions, sized on demand)
+    cbn::DevBuf<float2> big;        // spectrum grid / resample grid(s)
+    cbn::DevBuf<float2> lattice;    // radial lattice (raw IFFT layout)
+    cbn::DevBuf<float2> padded;     // padded lattice and its FFT / transpose accumulators
+    cbn::DevBuf<float2> gr_t;       // Grangeat t-line buffers
+    cbn::DevBuf<float2> gr_grid;    // Grangeat 2D grids
+    cbn::DevBuf<float> values;      // umbrella values of a view batch
+    cbn::DevBuf<float> s32;         // per-plan float32 scalings (3 x smax)
+    cbn::DevBuf<int> tab_idx;
+    cbn::DevBuf<float> tab_sc;
+    cbn::DevBuf<double> red;        // reductions
+    cbn::DevBuf<int> flag;          // non-finite flag
+
+    ~cbn_projector_s() {
+        for (auto& kv : ls_rows) delete kv.second;
+    }
+};

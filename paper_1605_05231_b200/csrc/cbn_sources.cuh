@@ -1,0 +1,172 @@
+// Node generators of the projector, evaluated per point on the device in
+// float64 with the reference's operation order (no FMA contraction):
+//
+//  * RadialSrc   -- radial-line lattice nodes  (radon_fourier.py:59-72,
+//                   geometry.py:162-168), node order rho fastest, then theta,
+//                   then phi; wrapped twice as the reference does
+//                   (_wrap_nodes, then plan_nufft's wrap_nodes).
+//  * UmbrellaSrc -- one umbrella plane per target (geometry.py:190-217),
+//                   canonical polar wrap twice (geometry.py:143-159), the
+//                   |rho| validity mask and origin pinning
+//                   (pipeline.py:96-102), fractional lattice indices with the
+//                   +rho_max fold (resampling.py:38-59), the rho padding and
+//                   node = -2 pi pos / padded (resampling.py:97-101).
+//                   Output axis order is the device grid order (phi, theta, rho).
+//  * PolarSrc    -- Grangeat detector-plane polar nodes (grangeat.py:110-117).
+#pragma once
+
+#include "cbn_common.cuh"
+
+namespace cbn {
+
+struct RadialSrc {
+    const double* om;     // n_rho   radial_omega(spec) * voxel (rad / voxel)
+    const double* cphi;   // n_phi
+    const double* sphi;
+    const double* cth;    // n_theta
+    const double* sth;
+    int n_rho, n_theta;
+    struct Aux {
+        double raw[3];    // unwrapped node (for the trilinear transfer)
+        int ir, it;
+    };
+    CBN_D void node(int64_t i, double (&w)[3], Aux& a) const {
+        const int ir = (int)(i % n_rho);
+        const int64_t rest = i / n_rho;
+        const int it = (int)(rest % n_theta);
+        const int ip = (int)(rest / n_theta);
+        const double st = sth[it];
+        const double o = om[ir];
+        a.raw[0] = dmul(o, dmul(cphi[ip], st));
+        a.raw[1] = dmul(o, dmul(sphi[ip], st));
+        a.raw[2] = dmul(o, cth[it]);
+        a.ir = ir;
+        a.it = it;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) w[d] = wrap_pi(wrap_pi(a.raw[d]));
+    }
+};
+
+struct UmbrellaGeom {
+    const double* cos_a;   // per view: cos / sin of the source angle
+    const double* sin_a;
+    const double* cos_mu;  // per umbrella line angle
+    const double* sin_mu;
+    double so, dt;
+    int n_mu, n_t;
+    // radial spec and resample padding
+    double rho_max, d_rho;
+    int n_rho, n_theta, n_phi;
+    int pad;
+    double padded[3];      // reference order (rho, theta, phi)
+};
+
+// canonical_polar (geometry.py:143-159)
+CBN_D void canonical(double& rho, double& theta, double& phi) {
+    const double st = sin(theta);
+    double nx = dmul(cos(phi), st);
+    double ny = dmul(sin(phi), st);
+    double nz = cos(theta);
+    if (nz < 0.0) {
+        nx = -nx;
+        ny = -ny;
+        nz = -nz;
+        rho = -rho;
+    }
+    double th = acos(fmin(fmax(nz, -1.0), 1.0));
+    double ph = np_mod(atan2(ny, nx), kTwoPi);
+    theta = th >= kPi ? 0.0 : th;
+    phi = ph;
+}
+
+struct UmbrellaSrc {
+    UmbrellaGeom g;
+    int view0;
+    struct Aux {
+        bool valid;
+    };
+    // fractional lattice indices (rho incl. padding, theta, phi), reference order
+    CBN_D void position(int64_t i, double (&pos)[3], bool& valid) const {
+        const int64_t per_view = (int64_t)g.n_mu * g.n_t;
+        const int v = view0 + (int)(i / per_view);
+        const int rem = (int)(i % per_view);
+        const int im = rem / g.n_t;
+        const int jt = rem % g.n_t;
+        const double ca = g.cos_a[v], sa = g.sin_a[v];
+        const double cm = g.cos_mu[im], sm = g.sin_mu[im];
+        const double t = dmul((double)(jt - g.n_t / 2), g.dt);
+        // s = SO (cos a, sin a, 0); u_hat = (-sin a, cos a, 0); v_hat = (0, 0, 1)
+        const double sx = dmul(g.so, ca), sy = dmul(g.so, sa), sz = dmul(g.so, 0.0);
+        const double ux = -sa, uy = ca, uz = 0.0;
+        // e = cos mu u_hat + sin mu v_hat ; d = -sin mu u_hat + cos mu v_hat
+        const double ex = dadd(dmul(cm, ux), dmul(sm, 0.0));
+        const double ey = dadd(dmul(cm, uy), dmul(sm, 0.0));
+        const double ez = dadd(dmul(cm, uz), dmul(sm, 1.0));
+        const double msm = -sm;
+        const double dx = dadd(dmul(msm, ux), dmul(cm, 0.0));
+        const double dy = dadd(dmul(msm, uy), dmul(cm, 0.0));
+        const double dz = dadd(dmul(msm, uz), dmul(cm, 1.0));
+        // a = p0 - s ; n = a x d ; n /= |n|
+        const double ax = dsub(dmul(t, ex), sx);
+        const double ay = dsub(dmul(t, ey), sy);
+        const double az = dsub(dmul(t, ez), sz);
+        double nx = dsub(dmul(ay, dz), dmul(az, dy));
+        double ny = dsub(dmul(az, dx), dmul(ax, dz));
+        double nz = dsub(dmul(ax, dy), dmul(ay, dx));
+        const double nn = sqrt(dadd(dadd(dmul(nx, nx), dmul(ny, ny)), dmul(nz, nz)));
+        nx = ddiv(nx, nn);
+        ny = ddiv(ny, nn);
+        nz = ddiv(nz, nn);
+        double rho = dadd(dadd(dmul(nx, sx), dmul(ny, sy)), dmul(nz, sz));
+        double theta = acos(fmin(fmax(nz, -1.0), 1.0));
+        double phi = np_mod(atan2(ny, nx), kTwoPi);
+        canonical(rho, theta, phi);
+        valid = fabs(rho) <= g.rho_max * (1.0 + 1e-12);
+        if (!valid) {
+            rho = 0.0;
+            theta = 0.0;
+            phi = 0.0;
+        }
+        canonical(rho, theta, phi);   // polar_index_map wraps again
+        double ir = dadd(ddiv(rho, g.d_rho), (double)g.n_rho / 2.0);
+        double it = ddiv(dmul(theta, (double)g.n_theta), kPi);
+        double ip = ddiv(dmul(phi, (double)g.n_phi), kTwoPi);
+        if (ir >= (double)g.n_rho - 1e-9) {
+            ir = 0.0;
+            it = np_mod(dsub((double)g.n_theta, it), (double)g.n_theta);
+            ip = np_mod(dadd(ip, (double)g.n_phi / 2.0), (double)g.n_phi);
+        }
+        pos[0] = dadd(ir, (double)g.pad);
+        pos[1] = it;
+        pos[2] = ip;
+    }
+    CBN_D void node(int64_t i, double (&w)[3], Aux& a) const {
+        double pos[3];
+        position(i, pos, a.valid);
+        const double m2pi = -kTwoPi;
+        // device axis order: (phi, theta, rho)
+        w[0] = wrap_pi(ddiv(dmul(m2pi, pos[2]), g.padded[2]));
+        w[1] = wrap_pi(ddiv(dmul(m2pi, pos[1]), g.padded[1]));
+        w[2] = wrap_pi(ddiv(dmul(m2pi, pos[0]), g.padded[0]));
+    }
+};
+
+struct PolarSrc {
+    const double* omega;   // n_t  rad / mm
+    const double* cos_mu;  // n_mu
+    const double* sin_mu;
+    double pu, pv;
+    int n_t;
+    struct Aux {
+        int jt;
+    };
+    CBN_D void node(int64_t i, double (&w)[2], Aux& a) const {
+        const int im = (int)(i / n_t);
+        a.jt = (int)(i % n_t);
+        const double o = omega[a.jt];
+        w[0] = wrap_pi(wrap_pi(dmul(dmul(o, cos_mu[im]), pu)));
+        w[1] = wrap_pi(wrap_pi(dmul(dmul(o, sin_mu[im]), pv)));
+    }
+};
+
+}  // namespace cbn

@@ -1,0 +1,226 @@
+"""End-to-end NUFFT cone-beam operators on the B200 (drop-in for
+``cbnufft/pipeline.py:1-212``).
+
+``nufft_forward_project(vol, geom, cfg)`` and
+``nufft_backproject(frames, geom, cfg, out_size, voxel_mm)`` keep the
+reference's signatures, return types (``list[DetectorFrame]``,
+``Volume3D``), view batching (``_TARGET_BATCH``, read at call time like the
+reference module global) and exceptions (``ValueError`` for a frame-count
+mismatch, ``FloatingPointError`` for non-finite projections).  The whole chain
+runs in one C-ABI call per operator (``cbn_forward_project`` /
+``cbn_backproject``); there is no host compute path.
+
+``Projector`` exposes the same device plan with torch CUDA tensors in and out
+(no host round trip) plus the stage entry points used by the parity tests.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _device, _lib
+from .config import ProjectorConfig, make_projector_config  # noqa: F401  (API re-export)
+from .geometry import ConeGeometry, RadialGridSpec  # noqa: F401
+from .grangeat import DetectorFrame, UmbrellaView  # noqa: F401
+from .phantom import Volume3D
+
+_TARGET_BATCH = 1 << 20   # umbrella targets per resampling plan (pipeline.py:28)
+
+_FORWARD, _BACK = 1, 2
+_CACHE: "OrderedDict[tuple, Projector]" = OrderedDict()
+_CACHE_SIZE = 2
+
+
+def _geometry_struct(geom) -> _lib.Geometry:
+    return _lib.Geometry(float(geom.so_mm), float(geom.sd_mm), float(geom.det_width_mm),
+                         float(geom.det_height_mm), int(geom.nu), int(geom.nv),
+                         int(geom.n_views), float(geom.object_extent_mm))
+
+
+def _config_struct(cfg, target_batch: int, plan_chunk: int) -> _lib.ProjectorConfig:
+    method = str(cfg.method).lower()
+    if method not in ("a", "b"):
+        raise ValueError("method must be 'a' or 'b'")
+    if method == "b":
+        raise NotImplementedError("resample method 'b' is not on the device path yet "
+                                  "(SURVEY.md 8(f) next item 1)")
+    if cfg.t_taper not in ("none", "hann"):
+        raise ValueError("t_taper must be 'none' or 'hann'")
+    if cfg.basis not in ("trilinear", "dirac"):
+        raise ValueError("basis must be 'trilinear' or 'dirac'")
+    rj = np.broadcast_to(np.atleast_1d(cfg.resample_j), (3,)).astype(int)
+    spec = cfg.radial_spec
+    c = _lib.ProjectorConfig()
+    c.method = 0
+    c.spec = _lib.RadialSpec(int(spec.n_rho), int(spec.n_theta), int(spec.n_phi),
+                             float(spec.rho_max))
+    c.n_mu = int(cfg.n_mu)
+    c.n_t = int(cfg.n_t)
+    c.t_pitch_mm = -1.0 if cfg.t_pitch_mm is None else float(cfg.t_pitch_mm)
+    if cfg.t_pitch_mm is not None and not float(cfg.t_pitch_mm) > 0:
+        raise ValueError("t_pitch_mm must be positive")
+    c.t_taper = 1 if cfg.t_taper == "hann" else 0
+    c.spectrum_j = int(cfg.spectrum_j)
+    for k in range(3):
+        c.resample_j[k] = int(rj[k])
+    c.side_lobes = int(cfg.side_lobes)
+    c.oversample_factor = float(cfg.oversample_factor)
+    c.rho_pad = -1 if cfg.rho_pad is None else int(cfg.rho_pad)
+    c.basis = 0 if cfg.basis == "trilinear" else 1
+    c.normalization = float(cfg.normalization)
+    c.bp_normalization = float(cfg.bp_normalization)
+    c.den_tol = float(cfg.den_tol)
+    c.target_batch = int(target_batch)
+    c.plan_chunk = int(plan_chunk)
+    return c
+
+
+def _key(geom, cfg, n, voxel, direction, target_batch, plan_chunk):
+    spec = cfg.radial_spec
+    return (tuple(float(getattr(geom, f)) for f in ("so_mm", "sd_mm", "det_width_mm",
+                                                       "det_height_mm", "object_extent_mm")),
+            int(geom.nu), int(geom.nv), int(geom.n_views),
+            (int(spec.n_rho), int(spec.n_theta), int(spec.n_phi), float(spec.rho_max)),
+            str(cfg.method), int(cfg.n_mu), int(cfg.n_t), cfg.t_pitch_mm, cfg.t_taper,
+            int(cfg.spectrum_j), tuple(np.broadcast_to(np.atleast_1d(cfg.resample_j), (3,)).tolist()),
+            float(cfg.oversample_factor), cfg.rho_pad, cfg.basis, float(cfg.normalization),
+            float(cfg.bp_normalization), float(cfg.den_tol), int(n), float(voxel), direction,
+            int(target_batch), int(plan_chunk))
+
+
+class Projector:
+    """Device plan of the forward projector and/or backprojector."""
+
+    def __init__(self, geom, cfg, n: int, voxel_mm: float, direction: int = 3,
+                 target_batch: int | None = None, plan_chunk: int | None = None):
+        from . import nufft as _nufft
+        lib = _lib.load()
+        _device.require_cuda()
+        self.geom, self.cfg, self.n, self.voxel = geom, cfg, int(n), float(voxel_mm)
+        self.direction = direction
+        tb = _TARGET_BATCH if target_batch is None else int(target_batch)
+        pc = _nufft._PLAN_CHUNK if plan_chunk is None else int(plan_chunk)
+        self._g = _geometry_struct(geom)
+        self._c = _config_struct(cfg, tb, pc)
+        h = ctypes.c_void_p()
+        _lib.check(lib.cbn_projector_create(ctypes.byref(h), ctypes.byref(self._g),
+                                            ctypes.byref(self._c), self.n, self.voxel,
+                                            direction), "projector")
+        self._h = h
+        cnt = ctypes.c_int32(64)
+        sizes = (ctypes.c_int64 * 64)()
+        _lib.check(lib.cbn_projector_ls_sizes(h, sizes, ctypes.byref(cnt)))
+        for m in list(sizes)[:cnt.value]:
+            rows, rp = _lib.i64_array(_device.ls_rows(int(m)))
+            _lib.check(lib.cbn_projector_set_ls_rows(h, int(m), rp, rows.size))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and _lib._lib is not None:
+            _lib._lib.cbn_projector_destroy(h)
+            self._h = ctypes.c_void_p()
+
+    @property
+    def _s(self):
+        return ctypes.c_void_p(_device.stream_ptr())
+
+    # ---- whole operators (device tensors)
+    def forward(self, vol, view_lo: int = 0, view_hi: int | None = None):
+        t = _device.require_cuda()
+        view_hi = self.geom.n_views if view_hi is None else view_hi
+        v = _device.to_device(vol, t.float32)
+        if tuple(v.shape) != (self.n,) * 3:
+            raise ValueError(f"volume must be ({self.n},)*3")
+        out = t.empty((view_hi - view_lo, self.geom.nu, self.geom.nv), dtype=t.float32,
+                      device="cuda")
+        _lib.check(_lib.load().cbn_forward_project(self._h, _device.ptr(v), _device.ptr(out),
+                                                   int(view_lo), int(view_hi), self._s),
+                   "nufft_forward_project")
+        return out
+
+    def backproject(self, frames):
+        t = _device.require_cuda()
+        f = _device.to_device(frames, t.float32)
+        if tuple(f.shape) != (self.geom.n_views, self.geom.nu, self.geom.nv):
+            raise ValueError("frames must be (n_views, nu, nv)")
+        out = t.empty((self.n,) * 3, dtype=t.float32, device="cuda")
+        _lib.check(_lib.load().cbn_backproject(self._h, _device.ptr(f), _device.ptr(out), self._s),
+                   "nufft_backproject")
+        return out
+
+    # ---- stages
+    def radial_lattice(self, vol):
+        """Complex lattice in node order (n_phi, n_theta, n_rho)."""
+        t = _device.require_cuda()
+        v = _device.to_device(vol, t.float32)
+        spec = self.cfg.radial_spec
+        out = t.empty((spec.n_phi, spec.n_theta, spec.n_rho), dtype=t.complex64, device="cuda")
+        _lib.check(_lib.load().cbn_projector_radial_lattice(self._h, _device.ptr(v),
+                                                            _device.ptr(out), self._s))
+        return out
+
+    def resample_views(self, lattice, view_lo: int, view_hi: int):
+        t = _device.require_cuda()
+        lat = _device.to_device(lattice, t.complex64)
+        out = t.empty((view_hi - view_lo, self.cfg.n_mu, self.cfg.n_t), dtype=t.float32,
+                      device="cuda")
+        _lib.check(_lib.load().cbn_projector_resample_views(self._h, _device.ptr(lat),
+                                                            _device.ptr(out), view_lo, view_hi,
+                                                            self._s))
+        return out
+
+    def grangeat_reverse(self, values):
+        t = _device.require_cuda()
+        v = _device.to_device(values, t.float32)
+        nb = v.shape[0]
+        out = t.empty((nb, self.geom.nu, self.geom.nv), dtype=t.float32, device="cuda")
+        _lib.check(_lib.load().cbn_projector_grangeat_reverse(self._h, _device.ptr(v),
+                                                              _device.ptr(out), nb, self._s))
+        return out
+
+    def grangeat_forward(self, frames):
+        t = _device.require_cuda()
+        f = _device.to_device(frames, t.float32)
+        nb = f.shape[0]
+        out = t.empty((nb, self.cfg.n_mu, 2 * self.geom.nu), dtype=t.float32, device="cuda")
+        _lib.check(_lib.load().cbn_projector_grangeat_forward(self._h, _device.ptr(f),
+                                                              _device.ptr(out), nb, self._s))
+        return out
+
+
+def get_projector(geom, cfg, n, voxel_mm, direction):
+    from . import nufft as _nufft
+    key = _key(geom, cfg, n, voxel_mm, direction, _TARGET_BATCH, _nufft._PLAN_CHUNK)
+    p = _CACHE.get(key)
+    if p is None:
+        p = Projector(geom, cfg, n, voxel_mm, direction)
+        _CACHE[key] = p
+        while len(_CACHE) > _CACHE_SIZE:
+            _CACHE.popitem(last=False)
+    else:
+        _CACHE.move_to_end(key)
+    return p
+
+
+def clear_plan_cache() -> None:
+    _CACHE.clear()
+
+
+def nufft_forward_project(vol: Volume3D, geom, cfg) -> list[DetectorFrame]:
+    """NUFFT cone-beam forward projection of all views (pipeline.py:122-147)."""
+    proj = get_projector(geom, cfg, vol.data.shape[0], vol.voxel_mm, _FORWARD)
+    frames = proj.forward(vol.data).cpu().numpy().astype(np.float64)
+    return [DetectorFrame(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
+
+
+def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volume3D:
+    """Direct NUFFT backprojection (pipeline.py:150-212)."""
+    if len(frames) != geom.n_views:
+        raise ValueError("frame count does not match the geometry")
+    data = np.stack([np.asarray(f.data, dtype=np.float32) for f in frames])
+    proj = get_projector(geom, cfg, out_size, voxel_mm, _BACK)
+    vol = proj.backproject(data).cpu().numpy().astype(np.float64)
+    return Volume3D(vol, voxel_mm)
