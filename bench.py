@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: NUFFT cone-beam forward projector, BASELINE.json config 2.
+
+One step = one full forward projection (``nufft_forward_project``) of the
+seeded 256^3 30-ellipsoid phantom onto 360 cone-beam views (256^2 detector),
+with the reference's view batching and per-batch resample scalings.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 2] [--direction forward|back]
+
+Under torchrun (N > 1) the views are sharded across ranks (strong scaling:
+360 views in total); every rank computes the radial lattice itself.
+``--impl reference`` times the CPU oracle port (oracle/cbn_oracle.py, the
+reference algorithm in numpy/scipy) on a bounded, extrapolated sample.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--direction", choices=["forward", "back"], default="forward")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------- roofline helpers
+def stage_bytes(stage: str, w, per_step_views: int) -> float | None:
+    """Algorithmic (compulsory) HBM bytes of one step's stage."""
+    spec, cfg = w.spec, w.cfg
+    n = w.n
+    K3 = (2 * n) ** 3
+    M = spec.n_rho * spec.n_theta * spec.n_phi
+    pad = cfg.rho_pad
+    dr = spec.n_rho + 2 * pad
+    D = dr * spec.n_theta * spec.n_phi
+    Kr = 8 * D
+    targets = cfg.n_mu * cfg.n_t
+    if stage == "spectrum_gather":        # read K^3 grid once, write M lattice values
+        return 8.0 * K3 + 8.0 * M
+    if stage == "spectrum_pad":           # read N^3 f32, write K^3 c64
+        return 4.0 * n ** 3 + 8.0 * K3
+    if stage == "resample_pad":           # per batch: read D c64, write K_r c64
+        return per_step_views * (8.0 * D + 8.0 * Kr)
+    if stage == "resample_gather":        # per batch: read K_r grid, write targets f32
+        return per_step_views * (8.0 * Kr + 4.0 * targets)
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1605_05231_b200 import _lib
+    from paper_1605_05231_b200.pipeline import Projector
+    from paper_1605_05231_b200.workloads import workload
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args.config)
+    V = w.geom.n_views
+    lo, hi = rank * V // world, (rank + 1) * V // world
+    vol_host = w.volume()
+    lib = _lib.load()
+    direction = 1 if args.direction == "forward" else 2
+    proj = Projector(w.geom, w.cfg, w.n, w.voxel, direction)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    if direction == 1:
+        x_dev = torch.from_numpy(vol_host).cuda()
+
+        def step():
+            return proj.forward(x_dev, lo, hi)
+    else:
+        frames_dev = Projector(w.geom, w.cfg, w.n, w.voxel, 1).forward(torch.from_numpy(vol_host).cuda())
+        x_dev = frames_dev
+
+        def step():
+            return proj.backproject(x_dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    lib.cbn_projector_set_timing(proj._h, 1)
+    n0 = lib.cbn_launch_count()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = lib.cbn_launch_count() - n0
+    ms = t0.elapsed_time(t1)
+    clk = clocks.stop()
+    import ctypes
+    cnt = ctypes.c_int32(64)
+    stage_ms = (ctypes.c_double * 64)()
+    names = ctypes.create_string_buffer(4096)
+    lib.cbn_projector_stage_times(proj._h, stage_ms, ctypes.byref(cnt), names, 4096, 1)
+    lib.cbn_projector_set_timing(proj._h, 0)
+    stages = {nm: stage_ms[i] / args.steps
+              for i, nm in enumerate(names.value.decode().split(";")[:cnt.value])}
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    units = V if direction == 1 else V        # views per step across all ranks
+    value = units * args.steps / (ms_max / 1e3)
+
+    # ---- end to end through the public API path: pinned host in, host out
+    e2e = None
+    if not args.no_e2e:
+        if direction == 1:
+            host_in = torch.from_numpy(vol_host).pin_memory()
+            host_out = torch.empty((hi - lo, w.geom.nu, w.geom.nv), dtype=torch.float32).pin_memory()
+        else:
+            host_in = x_dev.cpu().pin_memory()
+            host_out = torch.empty((w.n,) * 3, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            dev = host_in.to("cuda", non_blocking=True)
+            out = proj.forward(dev, lo, hi) if direction == 1 else proj.backproject(dev)
+            host_out.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        wall0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        barrier()
+        et = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        e2e = {"value": units * args.steps / (e_ms / 1e3), "unit": "views/s",
+               "h2d_bytes_per_step": int(host_in.numel() * 4),
+               "d2h_bytes_per_step": int(host_out.numel() * 4),
+               "wall_s": wall, "api": "Projector.forward/backproject with pinned host tensors"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = hbm_peak()
+    # dominant stage among our kernels with an algorithmic byte count
+    ranked = sorted(((t, s) for s, t in stages.items() if stage_bytes(s, w, hi - lo) is not None),
+                    reverse=True)
+    roofline = None
+    if ranked:
+        t_ms, st = ranked[0]
+        b = stage_bytes(st, w, hi - lo)
+        ach = b / (t_ms / 1e3) / 1e9
+        roofline = {"kernel": st, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
+                    "traffic": None, "algorithmic_bytes_per_step": b, "ms_per_step": t_ms}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(w, direction, n_samples=1)
+    out = {
+        "metric": "cone-beam views/s (NUFFT forward projector)" if direction == 1
+        else "cone-beam views/s (NUFFT backprojector)",
+        "value": round(value, 3),
+        "unit": "views/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "c64/f32 (fp64 index math)",
+        "data": "synthetic: seeded 30-ellipsoid phantom (BASELINE config 2)",
+        "config": {"workload": f"{w.name} {args.direction}: {w.n}^3 volume, "
+                               f"{w.spec.n_rho}x{w.spec.n_theta}x{w.spec.n_phi} radial lattice, "
+                               f"{V} views of {w.geom.nu}^2, KB J=6 sigma=2, resample J=3",
+                   "views": V, "views_per_rank": hi - lo, "parallelism": f"views sharded x{world}",
+                   "l2": "working set > L2 (resample grid 2.4 GB per view batch)"},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": int(launches) // max(args.steps, 1),
+        "clocks": clk,
+        "roofline": roofline,
+        "stages_ms_per_step": {k: round(v, 3) for k, v in stages.items()},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------- CPU (oracle) leg
+def cpu_sample(w, direction: int, n_samples: int = 1):
+    """Time the oracle port on a bounded sample and extrapolate to the full
+    workload: one 2^21-node spectrum sub-plan (of ceil(M / 2^21)) and the
+    resample + reverse Grangeat of one view (of V)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import cbn_oracle as orc
+    cores = os.cpu_count() or 1
+    orc.WORKERS = cores
+    spec, cfg, geom = w.spec, w.cfg, w.geom
+    M = spec.n_rho * spec.n_theta * spec.n_phi
+    n_chunks = -(-M // orc.PLAN_CHUNK)
+    vol = w.volume(np.float64)
+    nodes_all = None
+    t_chunk, t_view = [], []
+    rng = np.random.default_rng(0)
+    for s in range(n_samples):
+        if direction != 1:
+            break
+        # spectrum sub-plan sample
+        t = time.perf_counter()
+        if nodes_all is None:
+            nodes_all = orc.wrap(orc.radial_direction_nodes(spec, w.voxel))
+        lo = (s % n_chunks) * orc.PLAN_CHUNK
+        hi = min(lo + orc.PLAN_CHUNK, M)
+        plan = orc.make_plan((w.n,) * 3, nodes_all[lo:hi], 2.0, 6)
+        orc.type2(plan, vol.astype(np.complex128))
+        t_chunk.append(time.perf_counter() - t)
+        del plan
+        # one view: umbrella targets, per-batch resample plan + apply, reverse Grangeat
+        t = time.perf_counter()
+        lattice = (rng.standard_normal((spec.n_rho, spec.n_theta, spec.n_phi))
+                   + 1j * rng.standard_normal((spec.n_rho, spec.n_theta, spec.n_phi)))
+        t_lat = time.perf_counter() - t
+        t = time.perf_counter()
+        per_view = cfg.n_mu * cfg.n_t
+        batch = orc.view_batches(geom.n_views, per_view)[s % geom.n_views]
+        targets, valid = orc.umbrella_targets(geom, spec, batch, cfg.n_mu, cfg.n_t, cfg.t_pitch_mm)
+        rs = orc.make_resampler(spec, targets, cfg.rho_pad, cfg.resample_j)
+        vals = np.real(orc.resample_forward(rs, lattice))
+        gp = orc.make_grangeat(geom, cfg.n_mu, cfg.n_t, t_pitch_mm=cfg.t_pitch_mm,
+                               t_taper=cfg.t_taper)
+        for i in range(len(batch)):
+            orc.grangeat_reverse(vals[i * per_view:(i + 1) * per_view].reshape(cfg.n_mu, cfg.n_t), gp)
+        t_view.append((time.perf_counter() - t) / len(batch))
+        del lattice, rs
+    if direction != 1:
+        return None
+    tc, tv = float(np.mean(t_chunk)), float(np.mean(t_view))
+    total = n_chunks * tc + geom.n_views * tv
+    return {"value": round(geom.n_views / total, 6), "unit": "views/s", "cores": cores,
+            "kind": "port",
+            "sample": f"oracle port: {len(t_chunk)} of {n_chunks} spectrum sub-plans (2^21 nodes) "
+                      f"+ {len(t_view)} view(s) of {geom.n_views} (resample plan+apply, reverse "
+                      f"Grangeat); extrapolated linearly; sub-plan {tc:.2f}s, view {tv:.2f}s; "
+                      "scipy.fft uses all cores, the numpy gather/bincount one",
+            "extrapolated": True}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1605_05231_b200.workloads import workload
+    w = workload(args.config)
+    direction = 1 if args.direction == "forward" else 2
+    t0 = time.perf_counter()
+    vals = []
+    for _ in range(max(args.warmup, 0) + args.steps):
+        r = cpu_sample(w, direction, 1)
+        vals.append(r)
+    timed = [v for v in vals[max(args.warmup, 0):] if v is not None]
+    wall = time.perf_counter() - t0
+    if not timed:
+        print(json.dumps({"impl": "reference", "unavailable": "backprojector CPU sample not implemented"}))
+        return
+    value = float(np.mean([v["value"] for v in timed]))
+    cpu = dict(timed[-1])
+    cpu["value"] = round(value, 6)
+    out = {"impl": "reference",
+           "metric": "cone-beam views/s (NUFFT forward projector)",
+           "value": round(value, 6), "unit": "views/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * w.geom.n_views / value, 1),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f64/c128", "data": "synthetic: seeded 30-ellipsoid phantom (BASELINE config 2)",
+           "config": {"workload": f"{w.name} {args.direction} (CPU oracle port, extrapolated)"},
+           "cpu_baseline": cpu,
+           "e2e": {"value": round(value, 6), "unit": "views/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "wall_s": round(wall, 1)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -144,9 +144,17 @@ int cbn_projector_grangeat_reverse(cbn_projector* proj, const float* values, flo
 int cbn_projector_grangeat_forward(cbn_projector* proj, const float* frames, float* values,
                                    int32_t n_views_blk, void* stream);
 
-/* Stage timing of the last operator call, milliseconds (CUDA events). */
-int cbn_projector_stage_times(const cbn_projector* proj, double* ms, int32_t* count,
-                              char* names, int32_t names_len);
+/* Per-stage CUDA-event timing: enable (1) / disable (0); when enabled every
+ * operator call records events per stage.  stage_times synchronises and
+ * returns the accumulated milliseconds per stage since the last reset
+ * (names: ';'-separated), then resets if `reset` is non-zero. */
+int cbn_projector_set_timing(cbn_projector* proj, int32_t on);
+int cbn_projector_stage_times(cbn_projector* proj, double* ms, int32_t* count,
+                              char* names, int32_t names_len, int32_t reset);
+
+/* Number of kernels this library has launched in the process (cuFFT's own
+ * kernels are not counted). */
+long long cbn_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -71,7 +71,10 @@ _SIGS = {
     "cbn_projector_resample_views": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_projector_grangeat_reverse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
     "cbn_projector_grangeat_forward": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),
-    "cbn_projector_stage_times": (ctypes.c_int, [c_vp, P_f64, P_i32, ctypes.c_char_p, c_i32]),
+    "cbn_projector_set_timing": (ctypes.c_int, [c_vp, c_i32]),
+    "cbn_projector_stage_times": (ctypes.c_int, [c_vp, P_f64, P_i32, ctypes.c_char_p, c_i32,
+                                                 c_i32]),
+    "cbn_launch_count": (ctypes.c_longlong, []),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -285,6 +285,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         p->values.ensure((size_t)mb);
         // ---- forward Grangeat of the batch's frames, in blocks of views
         for (int v0 = 0; v0 < nbv; v0 += 32) {
+            StageScope st(p->timer, "grangeat_forward", s);
             const int nb = std::min(32, nbv - v0);
             p->gr_grid.ensure((size_t)nb * Ku * Kv);
             p->gr_t.ensure((size_t)nb * per_view);
@@ -320,7 +321,11 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         UmbrellaSrc src{projector_umb_geom(p, u, r, p->bpad), b.first};
         int nrows;
         const int64_t* rows = projector_rows(p, mb, nrows);
-        ls_fit<3>(src, rows, nrows, rax, p->ls, p->s32.p, smax_r, s);
+        {
+            StageScope st(p->timer, "transpose_fit", s);
+            ls_fit<3>(src, rows, nrows, rax, p->ls, p->s32.p, smax_r, s);
+        }
+        StageScope st_sp(p->timer, "transpose_spread", s);
         CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * 2 * kres, s));
         dispatch_j(rax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
@@ -331,7 +336,11 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         });
         CBN_LAUNCH_CHECK();
         long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
-        p->fft.exec(p->fft.get(3, kd3, 2), p->big.p, p->big.p, CUFFT_INVERSE, s);
+        {
+            StageScope st(p->timer, "transpose_ifft", s);
+            p->fft.exec(p->fft.get(3, kd3, 2), p->big.p, p->big.p, CUFFT_INVERSE, s);
+        }
+        StageScope st_cr(p->timer, "transpose_crop", s);
         RemapAxis ax[3];
         const int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
         projector_build_tables(p, kTabCropShift, rax, smax_r, s, ax, sstr);
@@ -341,6 +350,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         CBN_LAUNCH_CHECK();
     }
     // ---- ifftn of the accumulated ifftshifted grids, rho crop, origin average
+    StageScope st_lat(p->timer, "bp_lattice", s);
     long long dd[3] = {r.n_phi, r.n_theta, dr};
     p->fft.exec(p->fft.get(3, dd, 2), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
     const double inv = 1.0 / (double)dsize;
@@ -381,6 +391,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     int nrows;
     const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
     ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->s32.p, n, s);
+    StageScope st_sp(p->timer, "bp_spread", s);
     CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
     BpSrc bsrc;
     static_cast<RadialSrc&>(bsrc) = r.src();
@@ -398,6 +409,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     });
     CBN_LAUNCH_CHECK();
     long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
+    StageScope st_ff(p->timer, "bp_ifft_crop", s);
     p->fft.exec(p->fft.get(3, k3d, 1), p->big.p, p->big.p, CUFFT_INVERSE, s);
     RemapAxis cax[3];
     const int64_t cstr[3] = {(int64_t)sax[1].K * sax[2].K, sax[2].K, 1};

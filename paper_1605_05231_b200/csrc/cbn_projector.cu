@@ -542,14 +542,23 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
     // scaling fit on the first sub-plan of nufft_forward_chunked (nufft.py:250-265)
     int nrows;
     const int64_t* rows = rows_for(p, spectrum_chunk(p, M), nrows);
-    ls_fit<3>(r.src(), rows, nrows, ax, p->ls, p->s32.p, smax, s);
     RemapAxis rax[3];
-    const int64_t sstr[3] = {(int64_t)n * n, n, 1};
-    build_tables(p, kTabPad, ax, smax, s, rax, sstr);
-    launch_remap<float, kStoreC>(3, vol, p->big.p, rax, 1.0f, s);
-    CBN_LAUNCH_CHECK();
+    {
+        StageScope st(p->timer, "spectrum_fit", s);
+        ls_fit<3>(r.src(), rows, nrows, ax, p->ls, p->s32.p, smax, s);
+        const int64_t sstr[3] = {(int64_t)n * n, n, 1};
+        build_tables(p, kTabPad, ax, smax, s, rax, sstr);
+    }
+    {
+        StageScope st(p->timer, "spectrum_pad", s);
+        launch_remap<float, kStoreC>(3, vol, p->big.p, rax, 1.0f, s);
+        CBN_LAUNCH_CHECK();
+    }
     long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
-    p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    {
+        StageScope st(p->timer, "spectrum_fft", s);
+        p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    }
     SpecOut epi;
     epi.out = p->lattice.p;
     epi.om_phys = r.om_phys.p;
@@ -558,14 +567,18 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
     epi.tri = p->c.basis == 0;
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
-    dispatch_j(ax[0].J, [&](auto jc) {
-        constexpr int J = decltype(jc)::value;
-        k_gather<3, J><<<blocks_for(M, 256), 256, 0, s>>>(p->big.p, kb, r.src(), epi, M);
-        return 0;
-    });
-    CBN_LAUNCH_CHECK();
+    {
+        StageScope st(p->timer, "spectrum_gather", s);
+        dispatch_j(ax[0].J, [&](auto jc) {
+            constexpr int J = decltype(jc)::value;
+            k_gather<3, J><<<blocks_for(M, 256), 256, 0, s>>>(p->big.p, kb, r.src(), epi, M);
+            return 0;
+        });
+        CBN_LAUNCH_CHECK();
+    }
     // centred IFFT along rho (radon_fourier.py:122-124,133-135); 1/(n d_rho) applied by consumers
     long long nr1[1] = {r.n_rho};
+    StageScope st(p->timer, "radial_ifft", s);
     p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_INVERSE, s);
 }
 
@@ -576,6 +589,7 @@ void lattice_spectrum(P* p, const float2* src, int shift, float scale, cudaStrea
     const int dr = r.n_rho + 2 * p->fpad;
     const int64_t total = r.lines() * dr;
     p->padded.ensure((size_t)total);
+    StageScope st(p->timer, "lattice_spectrum", s);
     p->red.ensure(2 * kRedBlocks + 64);
     double* mean = p->red.p + 2 * kRedBlocks;
     column_mean(src, r.lines(), r.n_rho, (r.n_rho / 2 + shift) % r.n_rho, scale, p->red.p, mean, s);
@@ -597,22 +611,32 @@ void resample_batch(P* p, int blo, int bhi, int lo, int hi, float* vals, cudaStr
     UmbrellaSrc fit_src{umb_geom(p, p->fumb, r, p->fpad), blo};
     int nrows;
     const int64_t* rows = rows_for(p, mb, nrows);
-    ls_fit<3>(fit_src, rows, nrows, ax, p->ls, p->s32.p, smax, s);
     const int dr = r.n_rho + 2 * p->fpad;
     RemapAxis rax[3];
-    const int64_t sstr[3] = {(int64_t)r.n_theta * dr, dr, 1};
-    build_tables(p, kTabPadShift, ax, smax, s, rax, sstr);
+    {
+        StageScope st(p->timer, "resample_fit", s);
+        ls_fit<3>(fit_src, rows, nrows, ax, p->ls, p->s32.p, smax, s);
+        const int64_t sstr[3] = {(int64_t)r.n_theta * dr, dr, 1};
+        build_tables(p, kTabPadShift, ax, smax, s, rax, sstr);
+    }
     const int64_t kt = ktot(ax);
     p->big.ensure((size_t)kt);
     const double size = (double)dr * r.n_theta * r.n_phi;
-    launch_remap<float2, kStoreC>(3, p->padded.p, p->big.p, rax, (float)(1.0 / size), s);
-    CBN_LAUNCH_CHECK();
+    {
+        StageScope st(p->timer, "resample_pad", s);
+        launch_remap<float2, kStoreC>(3, p->padded.p, p->big.p, rax, (float)(1.0 / size), s);
+        CBN_LAUNCH_CHECK();
+    }
     long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
-    p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    {
+        StageScope st(p->timer, "resample_fft", s);
+        p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    }
     UmbrellaSrc src{umb_geom(p, p->fumb, r, p->fpad), lo};
     const int64_t m = per_view * (hi - lo);
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
+    StageScope st(p->timer, "resample_gather", s);
     dispatch_j(ax[0].J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         k_gather<3, J><<<blocks_for(m, 256), 256, 0, s>>>(p->big.p, kb, src, UmbOut{vals}, m);
@@ -644,6 +668,7 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     const int64_t tl = (int64_t)nb * u.n_mu * u.n_t;
     p->gr_t.ensure((size_t)tl);
     p->gr_grid.ensure((size_t)nb * Ku * Kv);
+    StageScope st(p->timer, "grangeat_reverse", s);
     k_gr_pre<<<blocks_for(tl, 256), 256, 0, s>>>(vals, gp.w2.p, u.n_t, tl, p->gr_t.p);
     CBN_LAUNCH_CHECK();
     long long nt[1] = {u.n_t};
@@ -898,13 +923,35 @@ int cbn_projector_grangeat_reverse(cbn_projector* p, const float* values, float*
     }
 }
 
-int cbn_projector_stage_times(const cbn_projector* p, double* ms, int32_t* count, char* names,
-                              int32_t names_len) {
+int cbn_projector_set_timing(cbn_projector* p, int32_t on) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        p->timer.reset();
+        p->timer.on = on != 0;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_stage_times(cbn_projector* p, double* ms, int32_t* count, char* names,
+                              int32_t names_len, int32_t reset) {
     try {
         CBN_REQUIRE(p && count, "null argument");
-        *count = 0;
-        if (names && names_len > 0) names[0] = 0;
-        (void)ms;
+        p->timer.collect();
+        const int cap = *count;
+        *count = (int32_t)p->timer.totals.size();
+        std::string joined;
+        for (int i = 0; i < *count; ++i) {
+            if (ms && i < cap) ms[i] = p->timer.totals[i].second;
+            if (i) joined += ";";
+            joined += p->timer.totals[i].first;
+        }
+        if (names && names_len > 0) {
+            std::strncpy(names, joined.c_str(), (size_t)names_len - 1);
+            names[names_len - 1] = 0;
+        }
+        if (reset) p->timer.totals.clear();
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

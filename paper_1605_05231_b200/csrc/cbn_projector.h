@@ -61,6 +61,7 @@ struct cbn_projector_s {
 
     cbn::FFTCache fft;
     cbn::LSScratch ls;
+    cbn::StageTimer timer;
 
     // ---- forward
     cbn::RadialTables frad;

@@ -5,6 +5,7 @@
 namespace cbn {
 
 static thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
@@ -81,6 +82,67 @@ void FFTCache::exec(cufftHandle h, void* in, void* out, int direction, cudaStrea
                            direction));
 }
 
+StageTimer::~StageTimer() {
+    for (auto& r : recs_) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : pool_) cudaEventDestroy(e);
+}
+
+cudaEvent_t StageTimer::get() {
+    if (!pool_.empty()) {
+        cudaEvent_t e = pool_.back();
+        pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    CBN_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void StageTimer::begin(const char* name, cudaStream_t s) {
+    Rec r{name, get(), nullptr};
+    CBN_CUDA(cudaEventRecord(r.a, s));
+    recs_.push_back(r);
+}
+
+void StageTimer::end(cudaStream_t s) {
+    for (auto it = recs_.rbegin(); it != recs_.rend(); ++it) {
+        if (!it->b) {
+            it->b = get();
+            CBN_CUDA(cudaEventRecord(it->b, s));
+            return;
+        }
+    }
+}
+
+void StageTimer::collect() {
+    for (auto& r : recs_) {
+        if (!r.b) continue;
+        CBN_CUDA(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        CBN_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        bool found = false;
+        for (auto& kv : totals)
+            if (kv.first == r.name) {
+                kv.second += ms;
+                found = true;
+            }
+        if (!found) totals.emplace_back(r.name, (double)ms);
+        pool_.push_back(r.a);
+        pool_.push_back(r.b);
+    }
+    recs_.clear();
+}
+
+void StageTimer::reset() {
+    collect();
+    totals.clear();
+}
+
 }  // namespace cbn
+
+extern "C" long long cbn_launch_count(void) { return cbn::g_launches.load(); }
 
 extern "C" const char* cbn_last_error(void) { return cbn::g_last_error.c_str(); }

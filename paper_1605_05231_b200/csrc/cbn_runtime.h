@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <map>
@@ -50,7 +51,12 @@ int fail(const std::exception& e);
         }                                                                        \
     } while (0)
 
-#define CBN_LAUNCH_CHECK() CBN_CUDA(cudaGetLastError())
+extern std::atomic<long long> g_launches;
+#define CBN_LAUNCH_CHECK()                                                       \
+    do {                                                                         \
+        ::cbn::g_launches.fetch_add(1, std::memory_order_relaxed);               \
+        CBN_CUDA(cudaGetLastError());                                            \
+    } while (0)
 
 template <class T>
 struct DevBuf {
@@ -98,6 +104,35 @@ private:
     std::map<Key, cufftHandle> plans_;
     DevBuf<char> work_;
     cufftHandle make(int rank, long long* n, long long batch, long long stride, long long dist);
+};
+
+// Per-stage CUDA-event timing (enabled per plan; off by default).
+class StageTimer {
+public:
+    ~StageTimer();
+    bool on = false;
+    void begin(const char* name, cudaStream_t s);
+    void end(cudaStream_t s);
+    // synchronises, folds recorded pairs into per-name totals
+    void collect();
+    void reset();
+    std::vector<std::pair<std::string, double>> totals;   // name -> ms
+private:
+    struct Rec { std::string name; cudaEvent_t a, b; };
+    std::vector<Rec> recs_;
+    std::vector<cudaEvent_t> pool_;
+    cudaEvent_t get();
+};
+
+struct StageScope {
+    StageTimer& t;
+    cudaStream_t s;
+    StageScope(StageTimer& t_, const char* name, cudaStream_t s_) : t(t_), s(s_) {
+        if (t.on) t.begin(name, s);
+    }
+    ~StageScope() {
+        if (t.on) t.end(s);
+    }
 };
 
 }  // namespace cbn

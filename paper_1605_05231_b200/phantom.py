@@ -78,15 +78,22 @@ def random_ellipsoid_phantom(n: int, n_ellipsoids: int, seed: int,
     # process x-slabs to bound the temporaries at large n
     slab = max(1, (1 << 22) // (n * n))
     for centre, axes, rot, density in random_ellipsoids(n_ellipsoids, seed):
-        for x0 in range(0, n, slab):
-            xs = c[x0:x0 + slab]
+        # voxels farther than the largest semi-axis from the centre are outside
+        # (q >= |p - c|^2 / a_max^2), so only a bounding box is evaluated
+        r = float(np.max(axes))
+        sl = [np.nonzero(np.abs(c - centre[k]) <= r * (1.0 + 1e-9))[0] for k in range(3)]
+        if any(s.size == 0 for s in sl):
+            continue
+        (i0, i1), (j0, j1), (k0, k1) = ((s[0], s[-1] + 1) for s in sl)
+        py = c[None, j0:j1, None] - centre[1]
+        pz = c[None, None, k0:k1] - centre[2]
+        for x0 in range(i0, i1, slab):
+            xs = c[x0:min(x0 + slab, i1)]
             px = xs[:, None, None] - centre[0]
-            py = c[None, :, None] - centre[1]
-            pz = c[None, None, :] - centre[2]
             # body coordinates: R^T (p - centre)
             q = 0.0
             for k in range(3):
                 bk = (rot[0, k] * px + rot[1, k] * py + rot[2, k] * pz) / axes[k]
                 q = q + bk * bk
-            vol[x0:x0 + slab] += density * (q <= 1.0)
+            vol[x0:x0 + xs.size, j0:j1, k0:k1] += density * (q <= 1.0)
     return vol.astype(dtype)

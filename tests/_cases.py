@@ -14,13 +14,7 @@ def small_setup(n=16, views=12, basis="trilinear"):
 
 
 def config_setup(idx):
-    """BASELINE.json configs 0-3."""
-    n, views, polar, azim, n_rho = {0: (64, 90, 64, 128, 128), 1: (64, 90, 64, 128, 128),
-                                    2: (256, 360, 180, 360, 512),
-                                    3: (512, 720, 360, 720, 1024)}[idx]
-    geom = ConeGeometry(3.0, 6.0, 2.0, 2.0, n, n, views, 2.0)
-    voxel = 2.0 / n
-    spec = RadialGridSpec(n_rho, polar, azim, n_rho * voxel / 2.0)
-    cfg = make_projector_config(geom, n, "a", radial_spec=spec, spectrum_j=6,
-                                rho_pad=min(n_rho // 8, 32))
-    return geom, voxel, spec, cfg
+    """BASELINE.json configs 0-3; see workloads.py."""
+    from paper_1605_05231_b200.workloads import workload
+    w = workload(idx)
+    return w.geom, w.voxel, w.spec, w.cfg
