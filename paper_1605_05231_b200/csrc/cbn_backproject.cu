@@ -29,6 +29,8 @@ void projector_fit_grangeat(cbn_projector_s* p, GrangeatPlan& gp, const Umbrella
 void projector_column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
                            double* partial, double* out, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s);
+void projector_batch_plan(cbn_projector_s* p, BatchPlan& bp, const UmbrellaTables& u,
+                          const RadialTables& r, int pad, const AxisPlan* ax, cudaStream_t s);
 
 namespace {
 
@@ -142,6 +144,7 @@ k_rs_spread2(float* __restrict__ gnum, float* __restrict__ gden, KBSet kb, Umbre
     src.node(i, w, aux);
     if (!aux.valid) return;
     const float vn = vals[i];
+    if (vn == 0.f && !gden) return;
     int first[3];
     float wt[3][J];
     tap_setup<3, J>(kb, w, first, wt);
@@ -161,24 +164,28 @@ k_rs_spread2(float* __restrict__ gnum, float* __restrict__ gden, KBSet kb, Umbre
                 const float wk = wab * wt[2][c];
                 const size_t idx = 2 * (row + c2[c]);
                 if (vn != 0.f) atomicAdd(gnum + idx, wk * vn);
-                atomicAdd(gden + idx, wk);
+                if (gden) atomicAdd(gden + idx, wk);
             }
         }
     }
 }
 
-// den after origin average, maxima partials
-__global__ void k_den_max(const float2* __restrict__ acc_den, int64_t lines, int dr, int pad, int n,
-                          double inv, const double* __restrict__ means, double* __restrict__ partial) {
+// final den lattice (origin average and 1/size applied), node order
+__global__ void k_den_final(const float2* __restrict__ acc_den, int64_t lines, int dr, int pad,
+                            int n, double inv, const double* __restrict__ means,
+                            float* __restrict__ den) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= lines * n) return;
+    const int j = (int)(e % n);
+    const int64_t line = e / n;
+    den[e] = (j == n / 2) ? (float)means[0] : (float)((double)acc_den[line * dr + pad + j].x * inv);
+}
+
+__global__ void k_max_partial(const float* __restrict__ x, int64_t total, double* __restrict__ partial) {
     double mx = -1e308;
-    const int64_t total = lines * n;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int j = (int)(e % n);
-        const int64_t line = e / n;
-        double d = (j == n / 2) ? means[2] : (double)acc_den[line * dr + pad + j].x * inv;
-        mx = fmax(mx, d);
-    }
+         e += (int64_t)gridDim.x * blockDim.x)
+        mx = fmax(mx, (double)x[e]);
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     __shared__ double sh[32];
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
@@ -199,7 +206,7 @@ __global__ void k_max_final(const double* __restrict__ partial, int n, double* _
 
 // lattice = num / den where den > tol * max (pipeline.py:187-188), written at
 // the ifftshifted rho position for the centred radial FFT (radon_fourier.py:117-130)
-__global__ void k_bp_div(const float2* __restrict__ acc_num, const float2* __restrict__ acc_den,
+__global__ void k_bp_div(const float2* __restrict__ acc_num, const float* __restrict__ den,
                          int64_t lines, int dr, int pad, int n, double inv,
                          const double* __restrict__ means, const double* __restrict__ dmax,
                          double tol, float2* __restrict__ out) {
@@ -207,17 +214,16 @@ __global__ void k_bp_div(const float2* __restrict__ acc_num, const float2* __res
     if (e >= lines * n) return;
     const int j = (int)(e % n);
     const int64_t line = e / n;
-    double nr, ni, d;
+    double nr, ni;
     if (j == n / 2) {
         nr = means[0];
         ni = means[1];
-        d = means[2];
     } else {
         float2 a = acc_num[line * dr + pad + j];
         nr = a.x * inv;
         ni = a.y * inv;
-        d = (double)acc_den[line * dr + pad + j].x * inv;
     }
+    const double d = den[e];
     float2 v = make_float2(0.f, 0.f);
     if (d > tol * dmax[0]) v = make_float2((float)(nr / d), (float)(ni / d));
     out[line * n + (j - n / 2 + n) % n] = v;
@@ -262,24 +268,65 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     GrangeatPlan& gp = p->bgr;
     if (!gp.built) projector_fit_grangeat(p, gp, u, s);
     const AxisPlan* rax = p->bres;
+    BatchPlan& bp = p->bbatch;
+    projector_batch_plan(p, bp, u, r, p->bpad, rax, s);
     const int dr = r.n_rho + 2 * p->bpad;
     const int64_t dsize = (int64_t)dr * r.n_theta * r.n_phi;
     const int64_t kres = (int64_t)rax[0].K * rax[1].K * rax[2].K;
     const int64_t k3 = (int64_t)p->bspec[0].K * p->bspec[1].K * p->bspec[2].K;
-    p->big.ensure((size_t)std::max(2 * kres, k3));
-    p->padded.ensure(2 * (size_t)dsize);
+    // den (the transposed validity mask) depends on the geometry only: the first
+    // call computes and caches it, later calls spread the values alone
+    const bool need_den = !p->den_cached;
+    const int nch = need_den ? 2 : 1;
+    p->big.ensure((size_t)std::max(nch * kres, k3));
+    p->padded.ensure((size_t)nch * dsize);
     float2* acc_num = p->padded.p;
-    float2* acc_den = p->padded.p + dsize;
-    CBN_CUDA(cudaMemsetAsync(p->padded.p, 0, sizeof(float2) * 2 * dsize, s));
+    float2* acc_den = need_den ? p->padded.p + dsize : nullptr;
+    CBN_CUDA(cudaMemsetAsync(p->padded.p, 0, sizeof(float2) * nch * dsize, s));
+    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
     const int64_t per_view = (int64_t)u.n_mu * u.n_t;
     const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
     const int nu = p->g.nu, nv = p->g.nv;
-    const int smax_r = std::max(rax[0].N, std::max(rax[1].N, rax[2].N));
-    p->s32.ensure(3 * (size_t)std::max(smax_r, p->n_vol));
+    p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
     KBSet kbr;
     for (int d = 0; d < 3; ++d) kbr.ax[d] = rax[d].kb;
+    long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
+    const int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
 
-    for (auto& b : projector_batches(p->g.n_views, per_view, projector_target_batch(p))) {
+    // transposed resample of one group of batches sharing a scaling: one
+    // inverse FFT of the summed spreads, crop * scaling, accumulate
+    auto flush = [&](int g) {
+        {
+            StageScope st(p->timer, "transpose_ifft", s);
+            p->fft.exec(p->fft.get(3, kd3, nch), p->big.p, p->big.p, CUFFT_INVERSE, s);
+        }
+        StageScope st(p->timer, "transpose_crop", s);
+        size_t need = (size_t)rax[0].N + rax[1].N + rax[2].N;
+        p->tab_idx.ensure(need);
+        p->tab_sc.ensure(need);
+        RemapAxis ax[3];
+        size_t off = 0;
+        for (int d = 0; d < 3; ++d) {
+            build_table(kTabCropShift, rax[d].N, rax[d].K, bp.s32.p + ((size_t)g * 3 + d) * bp.smax,
+                        p->tab_idx.p + off, p->tab_sc.p + off, s);
+            ax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, rax[d].N, sstr[d]};
+            off += rax[d].N;
+        }
+        launch_remap<float2, kAccumC>(3, p->big.p, acc_num, ax, 1.0f, s);
+        CBN_LAUNCH_CHECK();
+        if (need_den) {
+            launch_remap<float2, kAccumC>(3, p->big.p + kres, acc_den, ax, 1.0f, s);
+            CBN_LAUNCH_CHECK();
+        }
+        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
+    };
+
+    int cur = -1;
+    for (size_t bi = 0; bi < bp.batches.size(); ++bi) {
+        const auto& b = bp.batches[bi];
+        const int g = bp.group[bi];
+        if (cur >= 0 && g != cur) flush(cur);
+        cur = g;
         const int nbv = b.second - b.first;
         const int64_t mb = per_view * nbv;
         p->values.ensure((size_t)mb);
@@ -317,61 +364,58 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
                                                           p->values.p + (size_t)v0 * per_view);
             CBN_LAUNCH_CHECK();
         }
-        // ---- resample transpose of the batch (num and den)
+        // ---- spread of the batch's values (and mask) at its umbrella targets
         UmbrellaSrc src{projector_umb_geom(p, u, r, p->bpad), b.first};
-        int nrows;
-        const int64_t* rows = projector_rows(p, mb, nrows);
-        {
-            StageScope st(p->timer, "transpose_fit", s);
-            ls_fit<3>(src, rows, nrows, rax, p->ls, p->s32.p, smax_r, s);
-        }
         StageScope st_sp(p->timer, "transpose_spread", s);
-        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * 2 * kres, s));
         dispatch_j(rax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             k_rs_spread2<J><<<blocks_for(mb, 256), 256, 0, s>>>(
-                reinterpret_cast<float*>(p->big.p), reinterpret_cast<float*>(p->big.p + kres), kbr,
-                src, p->values.p, mb);
+                reinterpret_cast<float*>(p->big.p),
+                need_den ? reinterpret_cast<float*>(p->big.p + kres) : nullptr, kbr, src,
+                p->values.p, mb);
             return 0;
         });
         CBN_LAUNCH_CHECK();
-        long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
-        {
-            StageScope st(p->timer, "transpose_ifft", s);
-            p->fft.exec(p->fft.get(3, kd3, 2), p->big.p, p->big.p, CUFFT_INVERSE, s);
-        }
-        StageScope st_cr(p->timer, "transpose_crop", s);
-        RemapAxis ax[3];
-        const int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
-        projector_build_tables(p, kTabCropShift, rax, smax_r, s, ax, sstr);
-        launch_remap<float2, kAccumC>(3, p->big.p, acc_num, ax, 1.0f, s);
-        CBN_LAUNCH_CHECK();
-        launch_remap<float2, kAccumC>(3, p->big.p + kres, acc_den, ax, 1.0f, s);
-        CBN_LAUNCH_CHECK();
     }
+    if (cur >= 0) flush(cur);
     // ---- ifftn of the accumulated ifftshifted grids, rho crop, origin average
     StageScope st_lat(p->timer, "bp_lattice", s);
     long long dd[3] = {r.n_phi, r.n_theta, dr};
-    p->fft.exec(p->fft.get(3, dd, 2), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
+    p->fft.exec(p->fft.get(3, dd, nch), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
     const double inv = 1.0 / (double)dsize;
     p->red.ensure(2 * kRed + 64);
     double* means = p->red.p + 2 * kRed;        // num re, num im, den re, den im
     projector_column_mean(acc_num, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p, means, s);
-    projector_column_mean(acc_den, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p, means + 2, s);
-    double* dmax = means + 4;
-    k_den_max<<<kRed, 256, 0, s>>>(acc_den, r.lines(), dr, p->bpad, r.n_rho, inv, means, p->red.p);
-    CBN_LAUNCH_CHECK();
-    k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, dmax);
-    CBN_LAUNCH_CHECK();
     const int64_t M = r.nodes();
+    if (need_den) {
+        projector_column_mean(acc_den, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p,
+                              means + 2, s);
+        p->den_cache.alloc((size_t)M);
+        p->den_max.alloc(1);
+        k_den_final<<<blocks_for(M, 256), 256, 0, s>>>(acc_den, r.lines(), dr, p->bpad, r.n_rho,
+                                                        inv, means + 2, p->den_cache.p);
+        CBN_LAUNCH_CHECK();
+        k_max_partial<<<kRed, 256, 0, s>>>(p->den_cache.p, M, p->red.p);
+        CBN_LAUNCH_CHECK();
+        k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, p->den_max.p);
+        CBN_LAUNCH_CHECK();
+        p->den_cached = true;
+    }
     p->lattice.ensure((size_t)M);
-    k_bp_div<<<blocks_for(M, 256), 256, 0, s>>>(acc_num, acc_den, r.lines(), dr, p->bpad, r.n_rho,
-                                                 inv, means, dmax, c.den_tol, p->lattice.p);
+    k_bp_div<<<blocks_for(M, 256), 256, 0, s>>>(acc_num, p->den_cache.p, r.lines(), dr, p->bpad,
+                                                 r.n_rho, inv, means, p->den_max.p, c.den_tol,
+                                                 p->lattice.p);
     CBN_LAUNCH_CHECK();
     long long nr1[1] = {r.n_rho};
     p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_FORWARD, s);
-    // ---- ramp filter weights (pipeline.py:190-200), per rho bin incl. d_rho
-    {
+    // ---- 3D type-1 NUFFT onto (2N)^3 (nufft_adjoint_chunked, nufft.py:268-282)
+    const AxisPlan* sax = p->bspec;
+    const int n = p->n_vol;
+    int nrows;
+    const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
+    ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->s32.p, n, s);
+    if (!p->ramp_q.p) {
+        // ramp filter weights (pipeline.py:190-200), per rho bin incl. d_rho
         std::vector<float> q(r.n_rho);
         const double c3 = 1.0 / (4.0 * r.n_theta * r.n_phi * r.n_rho * r.d_rho);
         const double corner = kPi * std::sqrt(3.0) / p->voxel;
@@ -380,23 +424,15 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
             double ap = std::cos(kPi * std::min(std::fabs(om) / corner, 1.0) / 2.0);
             q[k] = (float)(om * ap * ap * c3 * r.d_rho);
         }
-        p->values.ensure((size_t)r.n_rho);
-        CBN_CUDA(cudaMemcpyAsync(p->values.p, q.data(), sizeof(float) * r.n_rho,
-                                 cudaMemcpyHostToDevice, s));
+        p->ramp_q.upload(q.data(), q.size(), s);
         CBN_CUDA(cudaStreamSynchronize(s));
     }
-    // ---- 3D type-1 NUFFT onto (2N)^3 (nufft_adjoint_chunked, nufft.py:268-282)
-    const AxisPlan* sax = p->bspec;
-    const int n = p->n_vol;
-    int nrows;
-    const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
-    ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->s32.p, n, s);
     StageScope st_sp(p->timer, "bp_spread", s);
     CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
     BpSrc bsrc;
     static_cast<RadialSrc&>(bsrc) = r.src();
     bsrc.X = p->lattice.p;
-    bsrc.q = p->values.p;
+    bsrc.q = p->ramp_q.p;
     bsrc.sin_th = r.sin_theta.p;
     for (int d = 0; d < 3; ++d) bsrc.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
     bsrc.tri = c.basis == 0;

@@ -48,8 +48,7 @@ __global__ void k_ls_fit(const double* __restrict__ frac, const double* __restri
     }
 }
 
-__global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, const double* i0beta,
-                            float* s32, int s32_stride) {
+__global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, float* s32, int s32_stride) {
     const int d = blockIdx.x;
     const int N = p.N[d];
     double* s = s_raw + (size_t)d * s_stride;
@@ -69,7 +68,7 @@ __global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, const doubl
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         double v = fmax(s[k], floor_v);
         s[k] = v;
-        s32[(size_t)d * s32_stride + k] = (float)(v * i0beta[d]);
+        s32[(size_t)d * s32_stride + k] = (float)(v * p.i0beta[d]);
     }
 }
 

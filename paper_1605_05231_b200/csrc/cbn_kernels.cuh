@@ -168,6 +168,7 @@ struct LSParams {
     int K[kMaxDim];
     int J[kMaxDim];
     double beta[kMaxDim];
+    double i0beta[kMaxDim];
 };
 
 // per sampled row and axis: frac = u - first and the float64 KB weights
@@ -195,8 +196,7 @@ __global__ void k_ls_fit(const double* __restrict__ frac, const double* __restri
                          LSParams p, double* __restrict__ s_raw, int s_stride);
 
 // one block per axis: clip at 1e-8 max, write float64 and scaled float32 copies
-__global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, const double* i0beta,
-                            float* s32, int s32_stride);
+__global__ void k_ls_finish(double* s_raw, int s_stride, LSParams p, float* s32, int s32_stride);
 
 // ----------------------------------------------------------- separable remap
 // dst[e] = gain * prod_d scale_d[e_d] * src[sum_d idx_d[e_d] * sstride_d]

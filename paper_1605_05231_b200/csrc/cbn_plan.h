@@ -23,12 +23,10 @@ int oversample_mult(double sigma);
 constexpr int kMaxLS = 8192;
 struct LSScratch {
     DevBuf<double> frac, wts, s64;
-    DevBuf<double> i0b;
     void ensure(int nrows, int ndim, int stride) {
         frac.ensure((size_t)ndim * nrows);
         wts.ensure((size_t)ndim * nrows * kLSMaxJ);
         s64.ensure((size_t)ndim * stride);
-        i0b.ensure(kMaxDim);
     }
 };
 
@@ -40,6 +38,7 @@ inline LSParams ls_params(int D, const AxisPlan* ax) {
         p.K[d] = ax[d].K;
         p.J[d] = ax[d].J;
         p.beta[d] = ax[d].beta;
+        p.i0beta[d] = ax[d].i0beta;
     }
     return p;
 }
@@ -53,9 +52,6 @@ void ls_fit(const Src& src, const int64_t* rows_dev, int nrows, const AxisPlan* 
     CBN_REQUIRE(nrows > 0 && nrows <= kMaxLS, "scaling fit needs 1..8192 rows");
     sc.ensure(nrows, D, stride);
     LSParams p = ls_params(D, ax);
-    double i0b[kMaxDim] = {1.0, 1.0, 1.0};
-    for (int d = 0; d < D; ++d) i0b[d] = ax[d].i0beta;
-    CBN_CUDA(cudaMemcpyAsync(sc.i0b.p, i0b, sizeof(i0b), cudaMemcpyHostToDevice, s));
     k_ls_samples<D, Src><<<(nrows + 127) / 128, 128, 0, s>>>(src, rows_dev, nrows, p, sc.frac.p,
                                                              sc.wts.p);
     CBN_LAUNCH_CHECK();
@@ -63,7 +59,7 @@ void ls_fit(const Src& src, const int64_t* rows_dev, int nrows, const AxisPlan* 
     for (int d = 0; d < D; ++d) maxN = ax[d].N > maxN ? ax[d].N : maxN;
     k_ls_fit<<<dim3(maxN, D), 256, 0, s>>>(sc.frac.p, sc.wts.p, nrows, p, sc.s64.p, stride);
     CBN_LAUNCH_CHECK();
-    k_ls_finish<<<D, 256, 0, s>>>(sc.s64.p, stride, p, sc.i0b.p, s32, stride);
+    k_ls_finish<<<D, 256, 0, s>>>(sc.s64.p, stride, p, s32, stride);
     CBN_LAUNCH_CHECK();
 }
 

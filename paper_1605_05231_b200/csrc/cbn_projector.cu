@@ -600,27 +600,75 @@ void lattice_spectrum(P* p, const float2* src, int shift, float scale, cudaStrea
     p->fft.exec(p->fft.get(3, dims, 1), p->padded.p, p->padded.p, CUFFT_FORWARD, s);
 }
 
-// Re(resample_apply) for views [lo, hi) of reference batch [blo, bhi) -> vals
-void resample_batch(P* p, int blo, int bhi, int lo, int hi, float* vals, cudaStream_t s) {
+// Fit the resample scalings of every view batch once (plan_resample's
+// plan_nufft, resampling.py:102) and group batches with equal scalings.
+void ensure_batch_plan(P* p, BatchPlan& bp, const UmbrellaTables& u, const RadialTables& r,
+                       int pad, const AxisPlan* ax, cudaStream_t s) {
+    if (bp.ready) return;
+    StageScope st(p->timer, "batch_scalings", s);
+    const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+    bp.batches = view_batches(p->g.n_views, per_view, target_batch(p));
+    const int B = (int)bp.batches.size();
+    bp.smax = smax_of(ax);
+    const size_t per = 3 * (size_t)bp.smax;
+    bp.s32.alloc(per * B);
+    DevBuf<double> s64((size_t)per * B);
+    CBN_CUDA(cudaMemsetAsync(s64.p, 0, sizeof(double) * per * B, s));
+    for (int b = 0; b < B; ++b) {
+        UmbrellaSrc src{umb_geom(p, u, r, pad), bp.batches[b].first};
+        int nrows;
+        const int64_t* rows =
+            rows_for(p, per_view * (bp.batches[b].second - bp.batches[b].first), nrows);
+        ls_fit<3>(src, rows, nrows, ax, p->ls, bp.s32.p + per * b, bp.smax, s);
+        CBN_CUDA(cudaMemcpyAsync(s64.p + per * b, p->ls.s64.p, sizeof(double) * per,
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    std::vector<double> h(per * B);
+    CBN_CUDA(cudaMemcpyAsync(h.data(), s64.p, sizeof(double) * per * B, cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    bp.group.assign(B, -1);
+    std::vector<int> reps;
+    for (int b = 0; b < B; ++b) {
+        for (int rep : reps) {
+            double worst = 0.0;
+            for (int d = 0; d < 3; ++d)
+                for (int k = 0; k < ax[d].N; ++k) {
+                    double x = h[per * b + (size_t)d * bp.smax + k];
+                    double y = h[per * rep + (size_t)d * bp.smax + k];
+                    worst = std::max(worst, std::fabs(x - y) / std::fabs(y));
+                }
+            if (worst <= 1e-9) {
+                bp.group[b] = rep;
+                break;
+            }
+        }
+        if (bp.group[b] < 0) {
+            bp.group[b] = b;
+            reps.push_back(b);
+        }
+    }
+    bp.ready = true;
+}
+
+// G = FFT_2x(pad(fftshift(F) / size * scaling)) for a batch's scalings
+// (resample_apply + nufft_forward, resampling.py:146-147, nufft.py:226-231)
+void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fres;
-    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
-    const int64_t mb = per_view * (bhi - blo);
-    const int smax = smax_of(ax);
-    p->s32.ensure(3 * (size_t)smax);
-    UmbrellaSrc fit_src{umb_geom(p, p->fumb, r, p->fpad), blo};
-    int nrows;
-    const int64_t* rows = rows_for(p, mb, nrows);
     const int dr = r.n_rho + 2 * p->fpad;
     RemapAxis rax[3];
-    {
-        StageScope st(p->timer, "resample_fit", s);
-        ls_fit<3>(fit_src, rows, nrows, ax, p->ls, p->s32.p, smax, s);
-        const int64_t sstr[3] = {(int64_t)r.n_theta * dr, dr, 1};
-        build_tables(p, kTabPadShift, ax, smax, s, rax, sstr);
+    const int64_t sstr[3] = {(int64_t)r.n_theta * dr, dr, 1};
+    size_t need = (size_t)ax[0].K + ax[1].K + ax[2].K;
+    p->tab_idx.ensure(need);
+    p->tab_sc.ensure(need);
+    size_t off = 0;
+    for (int d = 0; d < 3; ++d) {
+        build_table(kTabPadShift, ax[d].N, ax[d].K, s32b + (size_t)d * smax, p->tab_idx.p + off,
+                    p->tab_sc.p + off, s);
+        rax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, ax[d].K, sstr[d]};
+        off += ax[d].K;
     }
-    const int64_t kt = ktot(ax);
-    p->big.ensure((size_t)kt);
+    p->big.ensure((size_t)ktot(ax));
     const double size = (double)dr * r.n_theta * r.n_phi;
     {
         StageScope st(p->timer, "resample_pad", s);
@@ -628,10 +676,15 @@ void resample_batch(P* p, int blo, int bhi, int lo, int hi, float* vals, cudaStr
         CBN_LAUNCH_CHECK();
     }
     long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
-    {
-        StageScope st(p->timer, "resample_fft", s);
-        p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
-    }
+    StageScope st(p->timer, "resample_fft", s);
+    p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+}
+
+// Re(resample_apply) at the umbrella targets of views [lo, hi) from the current grid
+void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s) {
+    const RadialTables& r = p->frad;
+    const AxisPlan* ax = p->fres;
+    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
     UmbrellaSrc src{umb_geom(p, p->fumb, r, p->fpad), lo};
     const int64_t m = per_view * (hi - lo);
     KBSet kb;
@@ -701,6 +754,49 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     CBN_LAUNCH_CHECK();
 }
 
+constexpr int kViewBlock = 32;
+
+// Views [lo, hi): one resample grid per run of batches with equal scalings,
+// gather at the umbrella targets, then reverse Grangeat in blocks of up to
+// kViewBlock consecutive views.  With `values_out` only the umbrella values
+// are produced (stage API).
+void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
+                          float* values_out = nullptr) {
+    BatchPlan& bp = p->fbatch;
+    ensure_batch_plan(p, bp, p->fumb, p->frad, p->fpad, p->fres, s);
+    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+    const size_t frame_sz = (size_t)p->g.nu * p->g.nv;
+    if (!values_out) p->values.ensure((size_t)per_view * kViewBlock);
+    int cur = -1, blk_lo = lo, blk_n = 0;
+    auto flush = [&]() {
+        if (!blk_n) return;
+        grangeat_reverse(p, p->values.p, frames + (size_t)(blk_lo - lo) * frame_sz, blk_n, s);
+        blk_lo += blk_n;
+        blk_n = 0;
+    };
+    for (size_t b = 0; b < bp.batches.size(); ++b) {
+        const int vlo = std::max(lo, bp.batches[b].first), vhi = std::min(hi, bp.batches[b].second);
+        if (vlo >= vhi) continue;
+        const int g = bp.group[b];
+        if (g != cur) {
+            build_resample_grid(p, bp.s32.p + (size_t)g * 3 * bp.smax, bp.smax, s);
+            cur = g;
+        }
+        if (values_out) {
+            gather_views(p, vlo, vhi, values_out + (size_t)(vlo - lo) * per_view, s);
+            continue;
+        }
+        for (int v = vlo; v < vhi;) {
+            const int take = std::min(vhi - v, kViewBlock - blk_n);
+            gather_views(p, v, v + take, p->values.p + (size_t)blk_n * per_view, s);
+            blk_n += take;
+            v += take;
+            if (blk_n == kViewBlock) flush();
+        }
+    }
+    flush();
+}
+
 void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s) {
     build_forward(p, s);
     p->flag.ensure(1);
@@ -708,20 +804,7 @@ void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cuda
     radial_lattice_raw(p, vol, s);
     const RadialTables& r = p->frad;
     lattice_spectrum(p, p->lattice.p, r.n_rho - r.n_rho / 2, (float)(1.0 / (r.n_rho * r.d_rho)), s);
-    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
-    const size_t frame_sz = (size_t)p->g.nu * p->g.nv;
-    for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p))) {
-        int vlo = std::max(lo, b.first), vhi = std::min(hi, b.second);
-        if (vlo >= vhi) continue;
-        p->values.ensure((size_t)per_view * (vhi - vlo));
-        resample_batch(p, b.first, b.second, vlo, vhi, p->values.p, s);
-        const int blk = 32;
-        for (int v = vlo; v < vhi; v += blk) {
-            int nb = std::min(blk, vhi - v);
-            grangeat_reverse(p, p->values.p + (size_t)(v - vlo) * per_view,
-                             frames + (size_t)(v - lo) * frame_sz, nb, s);
-        }
-    }
+    resample_and_reverse(p, lo, hi, frames, s);
     int flag = 0;
     CBN_CUDA(cudaMemcpyAsync(&flag, p->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CBN_CUDA(cudaStreamSynchronize(s));
@@ -734,6 +817,10 @@ void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cuda
 namespace cbn {
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
+void projector_batch_plan(cbn_projector_s* p, BatchPlan& bp, const UmbrellaTables& u,
+                          const RadialTables& r, int pad, const AxisPlan* ax, cudaStream_t s) {
+    ensure_batch_plan(p, bp, u, r, pad, ax, s);
+}
 const int64_t* projector_rows(cbn_projector_s* p, int64_t m, int& n) { return rows_for(p, m, n); }
 std::vector<std::pair<int, int>> projector_batches(int n_views, int64_t per_view, int64_t target) {
     return view_batches(n_views, per_view, target);
@@ -890,12 +977,7 @@ int cbn_projector_resample_views(cbn_projector* p, const void* lattice, float* v
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         build_forward(p, s);
         lattice_spectrum(p, static_cast<const float2*>(lattice), 0, 1.0f, s);
-        const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
-        for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p))) {
-            int vlo = std::max<int>(lo, b.first), vhi = std::min<int>(hi, b.second);
-            if (vlo >= vhi) continue;
-            resample_batch(p, b.first, b.second, vlo, vhi, values + (size_t)(vlo - lo) * per_view, s);
-        }
+        resample_and_reverse(p, lo, hi, nullptr, s, values);
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

@@ -44,7 +44,22 @@ struct GrangeatPlan {
     bool built = false;
 };
 
-struct cbn_projector_impl;
+// Per-batch resample scalings of one direction (plan data: they depend only on
+// the geometry), fitted once on the device and cached.  Batches whose
+// scalings agree to 1e-9 relative on every axis share a representative
+// (`group`), so they can share one resample grid / one transpose FFT.
+struct BatchPlan {
+    bool ready = false;
+    std::vector<std::pair<int, int>> batches;
+    std::vector<int> group;
+    int smax = 0;
+    DevBuf<float> s32;     // batches x 3 x smax
+    int groups() const {
+        int g = 0;
+        for (size_t b = 0; b < group.size(); ++b) g += group[b] == (int)b;
+        return g;
+    }
+};
 
 }  // namespace cbn
 
@@ -71,6 +86,7 @@ struct cbn_projector_s {
     cbn::AxisPlan fres[3];      // resample NUFFT axes, device order (phi, theta, rho_padded)
     int fpad = 0;
     bool fw_built = false;
+    cbn::BatchPlan fbatch;
 
     // ---- back
     cbn::RadialTables brad;
@@ -80,6 +96,11 @@ struct cbn_projector_s {
     cbn::AxisPlan bres[3];
     int bpad = 0;
     bool bw_built = false;
+    cbn::BatchPlan bbatch;
+    bool den_cached = false;
+    cbn::DevBuf<float> den_cache;   // final den lattice (incl. origin average), node order
+    cbn::DevBuf<double> den_max;
+    cbn::DevBuf<float> ramp_q;      // backprojector ramp per rho bin
 
     // ---- scratch (shared by both directions, sized on demand)
     cbn::DevBuf<float2> big;        // spectrum grid / resample grid(s)

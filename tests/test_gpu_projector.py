@@ -129,3 +129,29 @@ def test_frame_count_mismatch(pl):
     geom, voxel, spec, cfg = small_setup()
     with pytest.raises(ValueError):
         pl.nufft_backproject([], geom, cfg, 16, voxel)
+
+
+def test_repeated_calls_use_cached_plan_data(pl, golden_n16):
+    """Second call reuses the cached batch scalings and den lattice."""
+    from paper_1605_05231_b200.grangeat import DetectorFrame
+    from paper_1605_05231_b200.phantom import Volume3D
+    g = golden_n16
+    geom, voxel, spec, cfg = small_setup()
+    vol = Volume3D(g["vol"], voxel)
+    f1 = np.stack([f.data for f in pl.nufft_forward_project(vol, geom, cfg)])
+    f2 = np.stack([f.data for f in pl.nufft_forward_project(vol, geom, cfg)])
+    assert rel_l2(f2, f1) < 1e-6
+    frames = [DetectorFrame(k, g["frames"][k], geom.pixel_mm) for k in range(12)]
+    b1 = pl.nufft_backproject(frames, geom, cfg, 16, voxel).data
+    b2 = pl.nufft_backproject(frames, geom, cfg, 16, voxel).data
+    assert rel_l2(b2, b1) < 1e-6 and rel_l2(b2, g["bp"]) < TOL
+
+
+def test_view_range_matches_full(pl, golden_n16):
+    """Sharded view ranges (multi-GPU path) reproduce the full projection."""
+    g = golden_n16
+    geom, voxel, spec, cfg = small_setup()
+    proj = pl.Projector(geom, cfg, 16, voxel, 1, target_batch=cfg.n_mu * cfg.n_t * 5)
+    full = proj.forward(g["vol"]).cpu().numpy()
+    parts = [proj.forward(g["vol"], lo, hi).cpu().numpy() for lo, hi in ((0, 3), (3, 7), (7, 12))]
+    assert rel_l2(np.concatenate(parts), full) < 1e-6
