@@ -1,0 +1,43 @@
+#!/usr/bin/env python
+"""Run one steady-state projector step between cudaProfilerStart/Stop so
+`ncu --profile-from-start off` sees exactly one step's kernels.
+
+  python tools/profile_step.py [--config 2] [--direction forward|back]
+"""
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--direction", choices=["forward", "back"], default="forward")
+    args = ap.parse_args()
+    import torch
+    from paper_1605_05231_b200.pipeline import Projector
+    from paper_1605_05231_b200.workloads import workload
+    w = workload(args.config)
+    vol = torch.from_numpy(w.volume()).cuda()
+    if args.direction == "forward":
+        proj = Projector(w.geom, w.cfg, w.n, w.voxel, 1)
+        step = lambda: proj.forward(vol)          # noqa: E731
+    else:
+        frames = Projector(w.geom, w.cfg, w.n, w.voxel, 1).forward(vol)
+        proj = Projector(w.geom, w.cfg, w.n, w.voxel, 2)
+        step = lambda: proj.backproject(frames)   # noqa: E731
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    step()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print("profiled one step", flush=True)
+
+
+if __name__ == "__main__":
+    main()
