@@ -29,6 +29,8 @@ void projector_fit_grangeat(cbn_projector_s* p, GrangeatPlan& gp, const Umbrella
 void projector_column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
                            double* partial, double* out, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s);
+UmbrellaSrc projector_cached_umbrella(cbn_projector_s* p, UmbrellaTables& u, const RadialTables& r,
+                                      int pad, int view0, cudaStream_t s);
 void projector_batch_plan(cbn_projector_s* p, BatchPlan& bp, const UmbrellaTables& u,
                           const RadialTables& r, int pad, const AxisPlan* ax, cudaStream_t s);
 
@@ -365,7 +367,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
             CBN_LAUNCH_CHECK();
         }
         // ---- spread of the batch's values (and mask) at its umbrella targets
-        UmbrellaSrc src{projector_umb_geom(p, u, r, p->bpad), b.first};
+        UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, b.first, s);
         StageScope st_sp(p->timer, "transpose_spread", s);
         dispatch_j(rax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;

@@ -397,7 +397,33 @@ UmbrellaGeom umb_geom(const P* p, const UmbrellaTables& u, const RadialTables& r
     g.padded[0] = (double)(r.n_rho + 2 * pad);
     g.padded[1] = (double)r.n_theta;
     g.padded[2] = (double)r.n_phi;
+    g.n_views = p->g.n_views;
     return g;
+}
+
+__global__ void k_umb_cache(UmbrellaSrc src, int64_t n, double4* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double pos[3];
+    bool valid;
+    src.position(i, pos, valid);
+    out[i] = make_double4(pos[0], pos[1], pos[2], valid ? 1.0 : 0.0);
+}
+
+// umbrella source for the gathers / spreads: base-view cache + phi rotation
+UmbrellaSrc cached_umbrella(P* p, UmbrellaTables& u, const RadialTables& r, int pad, int view0,
+                            cudaStream_t s) {
+    UmbrellaSrc src{umb_geom(p, u, r, pad), 0};
+    if (!u.base_ready) {
+        const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+        u.base.alloc((size_t)per_view);
+        k_umb_cache<<<blocks_for(per_view, 256), 256, 0, s>>>(src, per_view, u.base.p);
+        CBN_LAUNCH_CHECK();
+        u.base_ready = true;
+    }
+    src.view0 = view0;
+    src.cache = u.base.p;
+    return src;
 }
 
 void build_grangeat(P* p, GrangeatPlan& gp, const UmbrellaTables& u, int taper, cudaStream_t s) {
@@ -685,7 +711,7 @@ void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
-    UmbrellaSrc src{umb_geom(p, p->fumb, r, p->fpad), lo};
+    UmbrellaSrc src = cached_umbrella(p, p->fumb, r, p->fpad, lo, s);
     const int64_t m = per_view * (hi - lo);
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
@@ -817,6 +843,10 @@ void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cuda
 namespace cbn {
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
+UmbrellaSrc projector_cached_umbrella(cbn_projector_s* p, UmbrellaTables& u, const RadialTables& r,
+                                      int pad, int view0, cudaStream_t s) {
+    return cached_umbrella(p, u, r, pad, view0, s);
+}
 void projector_batch_plan(cbn_projector_s* p, BatchPlan& bp, const UmbrellaTables& u,
                           const RadialTables& r, int pad, const AxisPlan* ax, cudaStream_t s) {
     ensure_batch_plan(p, bp, u, r, pad, ax, s);

@@ -29,6 +29,8 @@ struct UmbrellaTables {
     int n_mu = 0, n_t = 0;
     double dt = 0;
     DevBuf<double> cos_a, sin_a, cos_mu, sin_mu, omega_t;
+    DevBuf<double4> base;   // view-0 target positions (see UmbrellaSrc::cache)
+    bool base_ready = false;
     void build(const cbn_geometry& g, int n_mu, int n_t, double dt, cudaStream_t s);
 };
 

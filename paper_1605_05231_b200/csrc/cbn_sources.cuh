@@ -59,6 +59,7 @@ struct UmbrellaGeom {
     int n_rho, n_theta, n_phi;
     int pad;
     double padded[3];      // reference order (rho, theta, phi)
+    int n_views;
 };
 
 // canonical_polar (geometry.py:143-159)
@@ -82,11 +83,31 @@ CBN_D void canonical(double& rho, double& theta, double& phi) {
 struct UmbrellaSrc {
     UmbrellaGeom g;
     int view0;
+    // Optional base-view cache: positions (rho, theta, phi, valid) of view 0's
+    // targets.  Rotating the source by 2 pi k / V rotates every umbrella
+    // plane normal about z, leaving rho and theta unchanged and adding
+    // k n_phi / V to the phi index (mod n_phi), so view k's targets follow
+    // from view 0's without the per-target trigonometry.
+    const double4* cache = nullptr;
     struct Aux {
         bool valid;
     };
+    CBN_D void cached_position(int64_t i, double (&pos)[3], bool& valid) const {
+        const int64_t per_view = (int64_t)g.n_mu * g.n_t;
+        const int v = view0 + (int)(i / per_view);
+        const double4 c = cache[i % per_view];
+        valid = c.w != 0.0;
+        pos[0] = c.x;
+        pos[1] = c.y;
+        const double shift = ddiv(dmul((double)v, (double)g.n_phi), (double)g.n_views);
+        pos[2] = valid ? np_mod(dadd(c.z, shift), (double)g.n_phi) : c.z;
+    }
     // fractional lattice indices (rho incl. padding, theta, phi), reference order
     CBN_D void position(int64_t i, double (&pos)[3], bool& valid) const {
+        if (cache) {
+            cached_position(i, pos, valid);
+            return;
+        }
         const int64_t per_view = (int64_t)g.n_mu * g.n_t;
         const int v = view0 + (int)(i / per_view);
         const int rem = (int)(i % per_view);

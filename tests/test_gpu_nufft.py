@@ -56,6 +56,24 @@ def test_dot_test_fp32(nf, dims):
     assert abs(lhs - rhs) / abs(lhs) < 1e-5
 
 
+def test_wrap_is_bitwise_numpy(nf):
+    """Device remainder (fma-based fmod) == numpy's mod(x + pi, 2 pi) - pi, bit for bit."""
+    rng = np.random.default_rng(3)
+    k = rng.integers(-40, 40, 60000)
+    vals = np.concatenate([
+        rng.uniform(-20 * np.pi, 20 * np.pi, 100000),
+        2 * np.pi * k / 64.0,                                   # grid-aligned
+        np.nextafter(2 * np.pi * k / 64.0, np.inf),
+        np.pi * rng.integers(-9, 9, 20000),                     # odd multiples of pi
+        np.nextafter(np.pi * rng.integers(-9, 9, 20000), -np.inf),
+        [0.0, -0.0, 1e-300, -1e-300, np.pi, -np.pi, 2 * np.pi, -2 * np.pi]])
+    nodes = vals[: (vals.size // 3) * 3].reshape(-1, 3)
+    plan = nf.plan_nufft((8, 8, 8), nodes, 2.0, 6)
+    ref = np.mod(nodes + np.pi, 2.0 * np.pi) - np.pi
+    got = plan.nodes
+    assert np.array_equal(got.view(np.int64), ref.view(np.int64))
+
+
 def test_validation_errors(nf):
     with pytest.raises(ValueError):
         nf.plan_nufft((8,), np.zeros((4, 2)), 2.0, 6)
