@@ -381,7 +381,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     }
     if (cur >= 0) flush(cur);
     // ---- ifftn of the accumulated ifftshifted grids, rho crop, origin average
-    StageScope st_lat(p->timer, "bp_lattice", s);
+    if (p->timer.on) p->timer.begin("bp_lattice", s);
     long long dd[3] = {r.n_phi, r.n_theta, dr};
     p->fft.exec(p->fft.get(3, dd, nch), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
     const double inv = 1.0 / (double)dsize;
@@ -410,12 +410,25 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     CBN_LAUNCH_CHECK();
     long long nr1[1] = {r.n_rho};
     p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_FORWARD, s);
+    if (p->timer.on) p->timer.end(s);
     // ---- 3D type-1 NUFFT onto (2N)^3 (nufft_adjoint_chunked, nufft.py:268-282)
     const AxisPlan* sax = p->bspec;
     const int n = p->n_vol;
-    int nrows;
-    const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
-    ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->s32.p, n, s);
+    KBSet kbs;
+    for (int d = 0; d < 3; ++d) kbs.ax[d] = sax[d].kb;
+    if (!p->bspec_fit) {
+        // scaling of the first sub-plan, cached with the sorted node order
+        int nrows;
+        const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
+        p->bspec_s32.alloc(3 * (size_t)n);
+        ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->bspec_s32.p, n, s);
+        const int tile[3] = {kTile3, kTile3, kTile3};
+        dispatch_j(sax[0].J, [&](auto jc) {
+            build_bins<3, decltype(jc)::value>(p->bspec_bins, r.src(), kbs, M, tile, kMaxSub, s);
+            return 0;
+        });
+        p->bspec_fit = true;
+    }
     if (!p->ramp_q.p) {
         // ramp filter weights (pipeline.py:190-200), per rho bin incl. d_rho
         std::vector<float> q(r.n_rho);
@@ -429,8 +442,6 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         p->ramp_q.upload(q.data(), q.size(), s);
         CBN_CUDA(cudaStreamSynchronize(s));
     }
-    StageScope st_sp(p->timer, "bp_spread", s);
-    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
     BpSrc bsrc;
     static_cast<RadialSrc&>(bsrc) = r.src();
     bsrc.X = p->lattice.p;
@@ -438,19 +449,30 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     bsrc.sin_th = r.sin_theta.p;
     for (int d = 0; d < 3; ++d) bsrc.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
     bsrc.tri = c.basis == 0;
-    KBSet kbs;
-    for (int d = 0; d < 3; ++d) kbs.ax[d] = sax[d].kb;
-    dispatch_j(sax[0].J, [&](auto jc) {
-        constexpr int J = decltype(jc)::value;
-        k_spread<3, J><<<blocks_for(M, 256), 256, 0, s>>>(p->big.p, kbs, bsrc, M);
-        return 0;
-    });
-    CBN_LAUNCH_CHECK();
+    {
+        StageScope st_sp(p->timer, "bp_spread", s);
+        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
+        const BinPlan& bb = p->bspec_bins;
+        dispatch_j(sax[0].J, [&](auto jc) {
+            constexpr int J = decltype(jc)::value;
+            constexpr int W = 4;
+            const size_t smem = spread_smem_bytes<3, J, W>(bb.nreg);
+            CBN_CUDA(cudaFuncSetAttribute(k_spread_binned<3, J, W, BpSrc>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_spread_binned<3, J, W><<<bb.nsubs, W * 32, smem, s>>>(p->big.p, kbs, bb.geom<3>(), bsrc,
+                                                                   bb.perm.p, bb.subs.p);
+            return 0;
+        });
+        CBN_LAUNCH_CHECK();
+    }
     long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
     StageScope st_ff(p->timer, "bp_ifft_crop", s);
     p->fft.exec(p->fft.get(3, k3d, 1), p->big.p, p->big.p, CUFFT_INVERSE, s);
     RemapAxis cax[3];
     const int64_t cstr[3] = {(int64_t)sax[1].K * sax[2].K, sax[2].K, 1};
+    p->s32.ensure(3 * (size_t)n);
+    CBN_CUDA(cudaMemcpyAsync(p->s32.p, p->bspec_s32.p, sizeof(float) * 3 * n,
+                             cudaMemcpyDeviceToDevice, s));
     projector_build_tables(p, kTabCrop, sax, n, s, cax, cstr);
     launch_remap<float2, kStoreRe>(3, p->big.p, vol, cax, (float)c.bp_normalization, s);
     CBN_LAUNCH_CHECK();

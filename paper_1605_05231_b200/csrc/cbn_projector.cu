@@ -593,11 +593,21 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
     epi.tri = p->c.basis == 0;
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
+    if (!p->fspec_bins.ready) {
+        StageScope st(p->timer, "spectrum_bins", s);
+        const int tile[3] = {kTile3, kTile3, kTile3};
+        dispatch_j(ax[0].J, [&](auto jc) {
+            build_bins<3, decltype(jc)::value>(p->fspec_bins, r.src(), kb, M, tile, kMaxSub, s);
+            return 0;
+        });
+    }
     {
         StageScope st(p->timer, "spectrum_gather", s);
+        const BinPlan& bp = p->fspec_bins;
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
-            k_gather<3, J><<<blocks_for(M, 256), 256, 0, s>>>(p->big.p, kb, r.src(), epi, M);
+            k_gather_binned<3, J><<<bp.nsubs, 256, sizeof(float2) * bp.nreg, s>>>(
+                p->big.p, kb, bp.geom<3>(), r.src(), epi, bp.perm.p, bp.subs.p);
             return 0;
         });
         CBN_LAUNCH_CHECK();

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "cbn_binned.cuh"
 #include "cbn_plan.h"
 #include "cbn_sources.cuh"
 
@@ -45,6 +46,9 @@ struct GrangeatPlan {
     DevBuf<float> w2, fac_re, fac_im;   // per t: post-weight, reverse filter (complex)
     bool built = false;
 };
+
+constexpr int kTile3 = 8;      // 3D bin edge (oversampled cells)
+constexpr int kMaxSub = 1024;  // points per subproblem
 
 // Per-batch resample scalings of one direction (plan data: they depend only on
 // the geometry), fitted once on the device and cached.  Batches whose
@@ -89,6 +93,7 @@ struct cbn_projector_s {
     int fpad = 0;
     bool fw_built = false;
     cbn::BatchPlan fbatch;
+    cbn::BinPlan fspec_bins;     // radial nodes sorted by spectrum-grid tile
 
     // ---- back
     cbn::RadialTables brad;
@@ -99,6 +104,9 @@ struct cbn_projector_s {
     int bpad = 0;
     bool bw_built = false;
     cbn::BatchPlan bbatch;
+    cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
+    bool bspec_fit = false;
+    cbn::DevBuf<float> bspec_s32;   // cached first-sub-plan scaling of the 3D adjoint
     bool den_cached = false;
     cbn::DevBuf<float> den_cache;   // final den lattice (incl. origin average), node order
     cbn::DevBuf<double> den_max;
