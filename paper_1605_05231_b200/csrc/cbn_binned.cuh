@@ -89,8 +89,13 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
                 wrapc(o[2] + r2, tg.K[2]);
         else
             g = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
-        tile[e] = __ldg(grid + g);
+        // asynchronous 8-byte copy global -> shared (LDGSTS): all of a thread's
+        // halo loads are in flight at once
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(tile + e)),
+                     "l"(grid + g));
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
         const int64_t i = perm[sp.start + k];

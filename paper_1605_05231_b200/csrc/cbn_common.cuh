@@ -90,11 +90,16 @@ CBN_HD int wrap_index(int c, int K) {
 }
 
 // ------------------------------------------------------------ KB kernel
+constexpr int kMaxJ = 8;
+constexpr int kPPDeg = 15;     // piecewise-polynomial degree (fitted to < 2e-8 of the peak)
+
 struct KBAxis {
     int J;          // taps
     int K;          // oversampled length
-    int deg;        // polynomial degree
-    float poly[kMaxPoly + 1];   // I0(beta sqrt(t)) / I0(beta) = sum poly[k] t^k
+    // Tap p's weight I0(beta sqrt(1 - (2x/J)^2)) / I0(beta) at x = frac - p,
+    // frac = u - first in (J/2 - 1, J/2], as a polynomial in
+    // y = 2 (frac - J/2 + 1) - 1 in (-1, 1]: pp[p][k] y^k.
+    float pp[kMaxJ][kPPDeg + 1];
 };
 
 // Exact support decision of the reference: arg = 1 - ((2x)/J)^2 > 0.
@@ -109,27 +114,22 @@ CBN_D bool kb_inside(double x, int J) {
     return dsub(1.0, dmul(q, q)) > 0.0;
 }
 
-CBN_D float kb_poly(const KBAxis& kb, float t) {
-    float acc = kb.poly[kb.deg];
-#pragma unroll 4
-    for (int k = kb.deg - 1; k >= 0; --k) acc = fmaf(acc, t, kb.poly[k]);
-    return acc;
-}
-
 // Weights of the J taps first..first+J-1 for grid coordinate u (fp64).
+// All taps share one Horner sweep (J independent FMA chains, coefficients are
+// compile-time offsets into the kernel-parameter bank).  Only tap 0 can reach
+// the support edge (x = J/2 when u - J/2 is an integer); there the reference's
+// exact float64 support test decides (nufft.py:39-41).
 template <int J>
 CBN_D void kb_weights(const KBAxis& kb, double u, int first, float (&w)[J]) {
+    const double fr = dsub(u, (double)first);
+    const float y = (float)(2.0 * (fr - (0.5 * J - 1.0)) - 1.0);
 #pragma unroll
-    for (int p = 0; p < J; ++p) {
-        double x = dsub(u, (double)(first + p));
-        if (kb_inside(x, J)) {
-            float q = (float)x * (2.0f / (float)J);
-            float t = (1.0f - q) * (1.0f + q);
-            w[p] = kb_poly(kb, fmaxf(t, 0.0f));
-        } else {
-            w[p] = 0.0f;
-        }
-    }
+    for (int p = 0; p < J; ++p) w[p] = kb.pp[p][kPPDeg];
+#pragma unroll
+    for (int k = kPPDeg - 1; k >= 0; --k)
+#pragma unroll
+        for (int p = 0; p < J; ++p) w[p] = fmaf(w[p], y, kb.pp[p][k]);
+    if (fr >= 0.5 * J * (1.0 - 1e-12) && !kb_inside(fr, J)) w[0] = 0.0f;
 }
 
 // float64 I0 by its (all-positive) power series; |z| <= ~25 here.

@@ -17,6 +17,7 @@ struct AxisPlan {
 double beatty_beta(int j, double alpha);
 // K = N * ceil(sigma - 1e-12) (nufft.py:159); beta from K/N; KB polynomial.
 AxisPlan make_axis(int N, int J, double sigma);
+void fit_kb_pieces(KBAxis& kb, int J, double beta, double i0beta);
 int oversample_mult(double sigma);
 
 // Scratch for one scaling fit of up to kMaxLS rows.
