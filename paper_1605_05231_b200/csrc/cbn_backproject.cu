@@ -262,6 +262,43 @@ struct BpSrc : RadialSrc {
 
 }  // namespace
 
+void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
+                                 bool reverse, cudaStream_t s);
+
+// forward_grangeat_view for nb (<= 32) views: frames (nb x nu x nv) -> values
+// (nb x n_mu x n_t), grangeat.py:131-146
+void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, float* values,
+                            cudaStream_t s) {
+    GrangeatPlan& gp = p->bgr;
+    if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
+    projector_prepare_gr_points(p, gp, p->bumb, false, s);
+    const UmbrellaTables& u = p->bumb;
+    const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
+    const int nu = p->g.nu, nv = p->g.nv;
+    const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+    p->gr_grid.ensure((size_t)nb * Ku * Kv);
+    p->gr_t.ensure((size_t)nb * per_view);
+    const int64_t gtot = (int64_t)nb * Ku * Kv;
+    k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames, nu, nv, Ku, Kv, gp.pu, gp.pv,
+                                                    p->g.so_mm, gp.s32.p, gp.smax, gtot,
+                                                    p->gr_grid.p);
+    CBN_LAUNCH_CHECK();
+    long long kd[2] = {Ku, Kv};
+    p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_FORWARD, s);
+    const BinPlan& bb = gp.bins;
+    dim3 grid(bb.nsubs, (nb + kGrVG - 1) / kGrVG);
+    k_gr_gather_binned<kGrJ, kGrVG><<<grid, 256, sizeof(float2) * kGrVG * bb.nreg, s>>>(
+        p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(), reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p),
+        bb.subs.p, p->gr_t.p, (size_t)per_view, nb);
+    CBN_LAUNCH_CHECK();
+    long long nt[1] = {u.n_t};
+    p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_INVERSE, s);
+    const int64_t vt = (int64_t)nb * per_view;
+    k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(p->gr_t.p, gp.w2.p, u.n_t,
+                                                  1.0 / ((double)u.n_t * u.dt), vt, values);
+    CBN_LAUNCH_CHECK();
+}
+
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s) {
     build_backward_plan(p, s);
     const cbn_projector_config& c = p->c;
@@ -287,7 +324,6 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     CBN_CUDA(cudaMemsetAsync(p->padded.p, 0, sizeof(float2) * nch * dsize, s));
     CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
     const int64_t per_view = (int64_t)u.n_mu * u.n_t;
-    const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
     const int nu = p->g.nu, nv = p->g.nv;
     p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
     KBSet kbr;
@@ -336,35 +372,8 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         for (int v0 = 0; v0 < nbv; v0 += 32) {
             StageScope st(p->timer, "grangeat_forward", s);
             const int nb = std::min(32, nbv - v0);
-            p->gr_grid.ensure((size_t)nb * Ku * Kv);
-            p->gr_t.ensure((size_t)nb * per_view);
-            const int64_t gtot = (int64_t)nb * Ku * Kv;
-            k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(
-                frames + (size_t)(b.first + v0) * nu * nv, nu, nv, Ku, Kv, gp.pu, gp.pv,
-                p->g.so_mm, gp.s32.p, gp.smax, gtot, p->gr_grid.p);
-            CBN_LAUNCH_CHECK();
-            long long kd[2] = {Ku, Kv};
-            p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_FORWARD, s);
-            GrFwdParams fp;
-            fp.n_mu = u.n_mu;
-            fp.n_t = u.n_t;
-            fp.Ku = Ku;
-            fp.Kv = Kv;
-            fp.pc0 = (double)nu / 2.0 - 0.5 - (double)(nu / 2);
-            fp.pc1 = (double)nv / 2.0 - 0.5 - (double)(nv / 2);
-            fp.pupv = (float)(gp.pu * gp.pv);
-            PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
-            k_grf_gather<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, fp,
-                                                                 u.omega_t.p, nb, p->gr_t.p);
-            CBN_LAUNCH_CHECK();
-            long long nt[1] = {u.n_t};
-            p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p,
-                        CUFFT_INVERSE, s);
-            const int64_t vt = (int64_t)nb * per_view;
-            k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(p->gr_t.p, gp.w2.p, u.n_t,
-                                                          1.0 / ((double)u.n_t * u.dt), vt,
-                                                          p->values.p + (size_t)v0 * per_view);
-            CBN_LAUNCH_CHECK();
+            grangeat_forward_block(p, frames + (size_t)(b.first + v0) * nu * nv, nb,
+                                   p->values.p + (size_t)v0 * per_view, s);
         }
         // ---- spread of the batch's values (and mask) at its umbrella targets
         UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, b.first, s);
@@ -488,43 +497,11 @@ extern "C" int cbn_projector_grangeat_forward(cbn_projector* p, const float* fra
         CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         build_backward_plan(p, s);
-        GrangeatPlan& gp = p->bgr;
-        if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
-        const UmbrellaTables& u = p->bumb;
-        const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
-        const int nu = p->g.nu, nv = p->g.nv;
-        const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+        const int64_t per_view = (int64_t)p->bumb.n_mu * p->bumb.n_t;
         for (int v0 = 0; v0 < nb; v0 += 32) {
             const int k = std::min(32, nb - v0);
-            p->gr_grid.ensure((size_t)k * Ku * Kv);
-            p->gr_t.ensure((size_t)k * per_view);
-            const int64_t gtot = (int64_t)k * Ku * Kv;
-            k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames + (size_t)v0 * nu * nv, nu, nv,
-                                                            Ku, Kv, gp.pu, gp.pv, p->g.so_mm,
-                                                            gp.s32.p, gp.smax, gtot, p->gr_grid.p);
-            CBN_LAUNCH_CHECK();
-            long long kd[2] = {Ku, Kv};
-            p->fft.exec(p->fft.get(2, kd, k), p->gr_grid.p, p->gr_grid.p, CUFFT_FORWARD, s);
-            GrFwdParams fp;
-            fp.n_mu = u.n_mu;
-            fp.n_t = u.n_t;
-            fp.Ku = Ku;
-            fp.Kv = Kv;
-            fp.pc0 = (double)nu / 2.0 - 0.5 - (double)(nu / 2);
-            fp.pc1 = (double)nv / 2.0 - 0.5 - (double)(nv / 2);
-            fp.pupv = (float)(gp.pu * gp.pv);
-            PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
-            k_grf_gather<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, fp,
-                                                                 u.omega_t.p, k, p->gr_t.p);
-            CBN_LAUNCH_CHECK();
-            long long nt[1] = {u.n_t};
-            p->fft.exec(p->fft.get(1, nt, (long long)k * u.n_mu), p->gr_t.p, p->gr_t.p,
-                        CUFFT_INVERSE, s);
-            const int64_t vt = (int64_t)k * per_view;
-            k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(p->gr_t.p, gp.w2.p, u.n_t,
-                                                          1.0 / ((double)u.n_t * u.dt), vt,
-                                                          values + (size_t)v0 * per_view);
-            CBN_LAUNCH_CHECK();
+            grangeat_forward_block(p, frames + (size_t)v0 * p->g.nu * p->g.nv, k,
+                                   values + (size_t)v0 * per_view, s);
         }
         return CBN_OK;
     } catch (const std::exception& e) {

@@ -1,0 +1,181 @@
+// Binned 2D KB spread / gather of the per-view Grangeat step over blocks of
+// views (grangeat.py:131-170).  The polar detector-plane nodes are shared by
+// all views (plan_grangeat), so per plan each node is sorted into a 2D tile,
+// and its local first tap, the J + J KB weights and its complex factor
+// (filter * phase) are precomputed once.  Per (subproblem, view group) a CTA
+// then only streams the per-view values:
+//   reverse: warp-private shared tiles, one view group of VG views per CTA,
+//            lanes = taps, plain load/add/store, one RED per non-zero cell;
+//   forward: the VG view tiles are staged in shared memory, one thread per
+//            node reads its taps for each view.
+#pragma once
+
+#include "cbn_binned.cuh"
+#include "cbn_sources.cuh"
+
+namespace cbn {
+
+template <int J>
+struct GrPoint {
+    short lu, lv;      // first tap relative to the bin origin
+    int col;           // mu * n_t + (rolled t index) into the per-view t buffer
+    float2 fac;        // complex factor (filter * phase), zero if the node is inert
+    float w[2 * J];    // u weights, then v weights
+};
+
+struct GrFactor {
+    int n_t;
+    int reverse;               // 1: conj phases * (i q_t); 0: phases * pu pv * (i omega_t)
+    double pc0, pc1;           // N/2 - 1/2 - N//2 per axis
+    const float* q;            // reverse: -sign(omega) taper dt c2 per t
+    const double* omega;       // forward: omega_t
+    float pupv;
+};
+
+template <int J>
+__global__ void k_gr_points(KBSet kb, TileGeom<2> tg, PolarSrc src, GrFactor f,
+                            const int* __restrict__ perm, const SubProblem* __restrict__ subs,
+                            GrPoint<J>* __restrict__ out) {
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<2>(tg, sp.bin, o);
+    for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
+        const int i = perm[sp.start + k];
+        double w[2];
+        PolarSrc::Aux aux;
+        src.node(i, w, aux);
+        int first[2];
+        float wt[2][J];
+        tap_setup<2, J>(kb, w, first, wt);
+        GrPoint<J> g;
+        g.lu = (short)(wrapc(first[0], tg.K[0]) - o[0]);
+        g.lv = (short)(wrapc(first[1], tg.K[1]) - o[1]);
+        const int im = i / f.n_t;
+        g.col = im * f.n_t + (aux.jt - f.n_t / 2 + f.n_t) % f.n_t;
+        double sn, cs;
+        if (f.reverse) {
+            sincos(-(w[0] * f.pc0 + w[1] * f.pc1), &sn, &cs);
+            const float q = f.q[aux.jt];
+            g.fac = make_float2(-(float)sn * q, (float)cs * q);
+        } else {
+            sincos(w[0] * f.pc0 + w[1] * f.pc1, &sn, &cs);
+            const float om = (float)f.omega[aux.jt] * f.pupv;
+            g.fac = make_float2(-(float)sn * om, (float)cs * om);
+        }
+#pragma unroll
+        for (int p = 0; p < J; ++p) {
+            g.w[p] = wt[0][p];
+            g.w[J + p] = wt[1][p];
+        }
+        out[sp.start + k] = g;
+    }
+}
+
+// reverse: grids[v] += sum_points w * (t[v][col] * fac)  for views [v0, v0 + nv)
+template <int J, int VG, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+k_gr_spread_binned(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
+                   const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
+                   const float2* __restrict__ tf, size_t tf_stride, int nviews) {
+    extern __shared__ float2 smem[];
+    const SubProblem sp = subs[blockIdx.x];
+    const int v0 = blockIdx.y * VG;
+    const int nv = min(VG, nviews - v0);
+    int o[3];
+    bin_origin<2>(tg, sp.bin, o);
+    const int R1 = tg.R[1];
+    const int nreg = tg.R[0] * R1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float2* copy = smem + (size_t)warp * VG * nreg;
+    for (int e = threadIdx.x; e < WARPS * VG * nreg; e += blockDim.x) smem[e] = make_float2(0.f, 0.f);
+    __syncthreads();
+    const int a = lane / J, b = lane % J;
+    const bool active = lane < J * J;
+    const float2* tfv = tf + (size_t)v0 * tf_stride;
+    for (int k = warp; k < sp.count; k += WARPS) {
+        const GrPoint<J>& g = pts[sp.start + k];
+        const float2 fac = g.fac;
+        if (fac.x == 0.f && fac.y == 0.f) continue;
+        const float wk = active ? g.w[a] * g.w[J + b] : 0.f;
+        const int cell = (g.lu + a) * R1 + g.lv + b;
+        float2 val[VG];
+#pragma unroll
+        for (int v = 0; v < VG; ++v)
+            val[v] = v < nv ? __ldg(tfv + v * tf_stride + g.col) : make_float2(0.f, 0.f);
+        if (active) {
+#pragma unroll
+            for (int v = 0; v < VG; ++v) {
+                const float2 y = cmul(val[v], fac);
+                float2 cur = copy[v * nreg + cell];
+                cur.x = fmaf(wk, y.x, cur.x);
+                cur.y = fmaf(wk, y.y, cur.y);
+                copy[v * nreg + cell] = cur;
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
+        float2 s = smem[e];
+#pragma unroll
+        for (int wi = 1; wi < WARPS; ++wi) {
+            const float2 x = smem[(size_t)wi * VG * nreg + e];
+            s.x += x.x;
+            s.y += x.y;
+        }
+        if (s.x == 0.f && s.y == 0.f) continue;
+        const int v = e / nreg, c = e % nreg;
+        const int r0 = c / R1, r1 = c % R1;
+        const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
+        atomicAdd(grids + (size_t)(v0 + v) * grid_stride + gi, s);
+    }
+}
+
+// forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv)
+template <int J, int VG>
+__global__ void __launch_bounds__(256)
+k_gr_gather_binned(const float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
+                   const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
+                   float2* __restrict__ out, size_t out_stride, int nviews) {
+    extern __shared__ float2 tile[];
+    const SubProblem sp = subs[blockIdx.x];
+    const int v0 = blockIdx.y * VG;
+    const int nv = min(VG, nviews - v0);
+    int o[3];
+    bin_origin<2>(tg, sp.bin, o);
+    const int R1 = tg.R[1];
+    const int nreg = tg.R[0] * R1;
+    for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
+        const int v = e / nreg, c = e % nreg;
+        const int r0 = c / R1, r1 = c % R1;
+        const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(tile + e)),
+                     "l"(grids + (size_t)(v0 + v) * grid_stride + gi));
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
+        const GrPoint<J> g = pts[sp.start + k];
+        for (int v = 0; v < nv; ++v) {
+            const float2* t = tile + v * nreg;
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int a = 0; a < J; ++a) {
+                const float2* row = t + (g.lu + a) * R1 + g.lv;
+                float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int b = 0; b < J; ++b) {
+                    const float2 x = row[b];
+                    r.x = fmaf(g.w[J + b], x.x, r.x);
+                    r.y = fmaf(g.w[J + b], x.y, r.y);
+                }
+                acc.x = fmaf(g.w[a], r.x, acc.x);
+                acc.y = fmaf(g.w[a], r.y, acc.y);
+            }
+            out[(size_t)(v0 + v) * out_stride + g.col] = cmul(acc, g.fac);
+        }
+    }
+}
+
+}  // namespace cbn

@@ -734,6 +734,29 @@ void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s) {
     CBN_LAUNCH_CHECK();
 }
 
+// sorted polar nodes with their precomputed taps and factors (plan data)
+void prepare_gr_points(P* p, GrangeatPlan& gp, const UmbrellaTables& u, bool reverse,
+                       cudaStream_t s) {
+    if (gp.pts_ready) return;
+    PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+    const int tile[2] = {kGrTile, kGrTile};
+    build_bins<2, kGrJ>(gp.bins, src, gp.kb, gp.m, tile, kMaxSub, s);
+    gp.pts.alloc((size_t)gp.m * sizeof(GrPoint<kGrJ>));
+    GrFactor f;
+    f.n_t = u.n_t;
+    f.reverse = reverse ? 1 : 0;
+    f.pc0 = (double)p->g.nu / 2.0 - 0.5 - (double)(p->g.nu / 2);
+    f.pc1 = (double)p->g.nv / 2.0 - 0.5 - (double)(p->g.nv / 2);
+    f.q = gp.fac_im.p;
+    f.omega = u.omega_t.p;
+    f.pupv = (float)(gp.pu * gp.pv);
+    k_gr_points<kGrJ><<<gp.bins.nsubs, 256, 0, s>>>(gp.kb, gp.bins.geom<2>(), src, f,
+                                                    gp.bins.perm.p, gp.bins.subs.p,
+                                                    reinterpret_cast<GrPoint<kGrJ>*>(gp.pts.p));
+    CBN_LAUNCH_CHECK();
+    gp.pts_ready = true;
+}
+
 GrPost gr_post(const P* p, const GrangeatPlan& gp) {
     GrPost q;
     q.nu = p->g.nu;
@@ -763,19 +786,19 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     long long nt[1] = {u.n_t};
     p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_FORWARD, s);
     CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
-    GrRevParams rp;
-    rp.n_mu = u.n_mu;
-    rp.n_t = u.n_t;
-    rp.nu = p->g.nu;
-    rp.nv = p->g.nv;
-    rp.Ku = Ku;
-    rp.Kv = Kv;
-    rp.pc0 = (double)p->g.nu / 2.0 - 0.5 - (double)(p->g.nu / 2);
-    rp.pc1 = (double)p->g.nv / 2.0 - 0.5 - (double)(p->g.nv / 2);
-    rp.q = gp.fac_im.p;
-    PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
-    k_gr_spread<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, p->gr_t.p, rp, nb);
-    CBN_LAUNCH_CHECK();
+    prepare_gr_points(p, gp, u, true, s);
+    {
+        const BinPlan& bb = gp.bins;
+        const size_t smem = sizeof(float2) * kGrWarps * kGrVG * bb.nreg;
+        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_binned<kGrJ, kGrVG, kGrWarps>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid(bb.nsubs, (nb + kGrVG - 1) / kGrVG);
+        k_gr_spread_binned<kGrJ, kGrVG, kGrWarps><<<grid, kGrWarps * 32, smem, s>>>(
+            p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(),
+            reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p), bb.subs.p, p->gr_t.p,
+            (size_t)u.n_mu * u.n_t, nb);
+        CBN_LAUNCH_CHECK();
+    }
     long long kd[2] = {Ku, Kv};
     p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_INVERSE, s);
     GrPost q = gr_post(p, gp);
@@ -853,6 +876,10 @@ void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cuda
 namespace cbn {
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
+void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
+                                 bool reverse, cudaStream_t s) {
+    prepare_gr_points(p, gp, u, reverse, s);
+}
 UmbrellaSrc projector_cached_umbrella(cbn_projector_s* p, UmbrellaTables& u, const RadialTables& r,
                                       int pad, int view0, cudaStream_t s) {
     return cached_umbrella(p, u, r, pad, view0, s);

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "cbn_binned.cuh"
+#include "cbn_grangeat.cuh"
 #include "cbn_plan.h"
 #include "cbn_sources.cuh"
 
@@ -45,7 +46,15 @@ struct GrangeatPlan {
     int64_t m = 0;
     DevBuf<float> w2, fac_re, fac_im;   // per t: post-weight, reverse filter (complex)
     bool built = false;
+    BinPlan bins;                       // polar nodes sorted by 2D tile
+    DevBuf<char> pts;                   // GrPoint<5> per sorted node
+    bool pts_ready = false;
 };
+
+constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)
+constexpr int kGrTile = 16;
+constexpr int kGrVG = 8;       // views per CTA in the binned Grangeat kernels
+constexpr int kGrWarps = 4;
 
 constexpr int kTile3 = 8;      // 3D bin edge (oversampled cells)
 constexpr int kMaxSub = 1024;  // points per subproblem
