@@ -92,27 +92,34 @@ k_gr_spread_binned(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> t
     const int a = lane / J, b = lane % J;
     const bool active = lane < J * J;
     const float2* tfv = tf + (size_t)v0 * tf_stride;
-    for (int k = warp; k < sp.count; k += WARPS) {
-        const GrPoint<J>& g = pts[sp.start + k];
-        const float2 fac = g.fac;
-        if (fac.x == 0.f && fac.y == 0.f) continue;
-        const float wk = active ? g.w[a] * g.w[J + b] : 0.f;
-        const int cell = (g.lu + a) * R1 + g.lv + b;
-        float2 val[VG];
-#pragma unroll
-        for (int v = 0; v < VG; ++v)
-            val[v] = v < nv ? __ldg(tfv + v * tf_stride + g.col) : make_float2(0.f, 0.f);
-        if (active) {
+    // PG points x VG views per step: one independent value load per lane, then
+    // the warp walks the PG points with lanes = taps and shuffles the values in
+    constexpr int PG = 32 / VG;
+    for (int base = warp * PG; base < sp.count; base += WARPS * PG) {
+        const int kl = base + lane / VG, vl = lane % VG;
+        float2 y = make_float2(0.f, 0.f);
+        if (kl < sp.count && vl < nv) {
+            const GrPoint<J>& gl = pts[sp.start + kl];
+            y = cmul(__ldg(tfv + vl * tf_stride + gl.col), gl.fac);
+        }
+        const int npg = min(PG, sp.count - base);
+        for (int j = 0; j < npg; ++j) {
+            const GrPoint<J>& g = pts[sp.start + base + j];
+            const float wk = active ? g.w[a] * g.w[J + b] : 0.f;
+            const int cell = (g.lu + a) * R1 + g.lv + b;
 #pragma unroll
             for (int v = 0; v < VG; ++v) {
-                const float2 y = cmul(val[v], fac);
-                float2 cur = copy[v * nreg + cell];
-                cur.x = fmaf(wk, y.x, cur.x);
-                cur.y = fmaf(wk, y.y, cur.y);
-                copy[v * nreg + cell] = cur;
+                const float yx = __shfl_sync(0xffffffffu, y.x, j * VG + v);
+                const float yy = __shfl_sync(0xffffffffu, y.y, j * VG + v);
+                if (active && (yx != 0.f || yy != 0.f)) {
+                    float2 cur = copy[v * nreg + cell];
+                    cur.x = fmaf(wk, yx, cur.x);
+                    cur.y = fmaf(wk, yy, cur.y);
+                    copy[v * nreg + cell] = cur;
+                }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
