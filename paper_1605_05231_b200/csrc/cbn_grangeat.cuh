@@ -138,6 +138,63 @@ k_gr_spread_binned(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> t
     }
 }
 
+// reverse, lanes = views: each warp walks its points, every lane adds its own
+// view's value to a private [cell][32 views] shared tile (consecutive lanes,
+// consecutive words: conflict-free, no shuffles); one RED per non-zero
+// (cell, view) at the end.  nviews <= 32.
+template <int J, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+k_gr_spread_views(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
+                  const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
+                  const float2* __restrict__ tf, size_t tf_stride, int nviews) {
+    extern __shared__ float2 smem[];
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<2>(tg, sp.bin, o);
+    const int R1 = tg.R[1];
+    const int nreg = tg.R[0] * R1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float2* copy = smem + (size_t)warp * nreg * 32;
+    for (int e = threadIdx.x; e < WARPS * nreg * 32; e += blockDim.x) smem[e] = make_float2(0.f, 0.f);
+    __syncthreads();
+    const bool live = lane < nviews;
+    const float2* tfl = tf + (size_t)lane * tf_stride;
+    for (int k = warp; k < sp.count; k += WARPS) {
+        const GrPoint<J> g = pts[sp.start + k];
+        if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
+        const float2 y = live ? cmul(__ldg(tfl + g.col), g.fac) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int a = 0; a < J; ++a) {
+            float2* row = copy + ((g.lu + a) * R1 + g.lv) * 32 + lane;
+            const float wa = g.w[a];
+#pragma unroll
+            for (int b = 0; b < J; ++b) {
+                const float wk = wa * g.w[J + b];
+                float2 cur = row[b * 32];
+                cur.x = fmaf(wk, y.x, cur.x);
+                cur.y = fmaf(wk, y.y, cur.y);
+                row[b * 32] = cur;
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nreg * 32; e += blockDim.x) {
+        const int v = e & 31, c = e >> 5;
+        if (v >= nviews) continue;
+        float2 s = smem[e];
+#pragma unroll
+        for (int wi = 1; wi < WARPS; ++wi) {
+            const float2 x = smem[(size_t)wi * nreg * 32 + e];
+            s.x += x.x;
+            s.y += x.y;
+        }
+        if (s.x == 0.f && s.y == 0.f) continue;
+        const int r0 = c / R1, r1 = c % R1;
+        const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
+        atomicAdd(grids + (size_t)v * grid_stride + gi, s);
+    }
+}
+
 // forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv)
 template <int J, int VG>
 __global__ void __launch_bounds__(256)

@@ -739,7 +739,8 @@ void prepare_gr_points(P* p, GrangeatPlan& gp, const UmbrellaTables& u, bool rev
                        cudaStream_t s) {
     if (gp.pts_ready) return;
     PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
-    const int tile[2] = {kGrTile, kGrTile};
+    const int edge = reverse ? kGrTileRev : kGrTile;
+    const int tile[2] = {edge, edge};
     build_bins<2, kGrJ>(gp.bins, src, gp.kb, gp.m, tile, kMaxSub, s);
     gp.pts.alloc((size_t)gp.m * sizeof(GrPoint<kGrJ>));
     GrFactor f;
@@ -789,11 +790,10 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     prepare_gr_points(p, gp, u, true, s);
     {
         const BinPlan& bb = gp.bins;
-        const size_t smem = sizeof(float2) * kGrWarps * kGrVG * bb.nreg;
-        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_binned<kGrJ, kGrVG, kGrWarps>,
+        const size_t smem = sizeof(float2) * kGrWarps * 32 * bb.nreg;
+        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_views<kGrJ, kGrWarps>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dim3 grid(bb.nsubs, (nb + kGrVG - 1) / kGrVG);
-        k_gr_spread_binned<kGrJ, kGrVG, kGrWarps><<<grid, kGrWarps * 32, smem, s>>>(
+        k_gr_spread_views<kGrJ, kGrWarps><<<bb.nsubs, kGrWarps * 32, smem, s>>>(
             p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(),
             reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p), bb.subs.p, p->gr_t.p,
             (size_t)u.n_mu * u.n_t, nb);

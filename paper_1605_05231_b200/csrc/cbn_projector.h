@@ -52,7 +52,8 @@ struct GrangeatPlan {
 };
 
 constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)
-constexpr int kGrTile = 16;
+constexpr int kGrTile = 16;    // forward (gather) tile edge
+constexpr int kGrTileRev = 8;  // reverse (views-in-lanes spread) tile edge
 constexpr int kGrVG = 8;       // views per CTA in the binned Grangeat kernels
 constexpr int kGrWarps = 4;
 
