@@ -142,7 +142,7 @@ k_gr_spread_binned(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> t
 // view's value to a private [cell][32 views] shared tile (consecutive lanes,
 // consecutive words: conflict-free, no shuffles); one RED per non-zero
 // (cell, view) at the end.  nviews <= 32.
-template <int J, int WARPS>
+template <int J, int WARPS, int TILE>
 __global__ void __launch_bounds__(WARPS * 32)
 k_gr_spread_views(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
                   const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
@@ -151,8 +151,8 @@ k_gr_spread_views(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<2>(tg, sp.bin, o);
-    const int R1 = tg.R[1];
-    const int nreg = tg.R[0] * R1;
+    constexpr int R1 = TILE + J - 1;
+    constexpr int nreg = R1 * R1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2* copy = smem + (size_t)warp * nreg * 32;
     for (int e = threadIdx.x; e < WARPS * nreg * 32; e += blockDim.x) smem[e] = make_float2(0.f, 0.f);
@@ -163,19 +163,25 @@ k_gr_spread_views(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg
         const GrPoint<J> g = pts[sp.start + k];
         if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
         const float2 y = live ? cmul(__ldg(tfl + g.col), g.fac) : make_float2(0.f, 0.f);
+        // the J x J cells are distinct: load all, update, store all
+        float2* base = copy + (g.lu * R1 + g.lv) * 32 + lane;
+        float2 cur[J][J];
 #pragma unroll
-        for (int a = 0; a < J; ++a) {
-            float2* row = copy + ((g.lu + a) * R1 + g.lv) * 32 + lane;
-            const float wa = g.w[a];
+        for (int a = 0; a < J; ++a)
+#pragma unroll
+            for (int b = 0; b < J; ++b) cur[a][b] = base[(a * R1 + b) * 32];
+#pragma unroll
+        for (int a = 0; a < J; ++a)
 #pragma unroll
             for (int b = 0; b < J; ++b) {
-                const float wk = wa * g.w[J + b];
-                float2 cur = row[b * 32];
-                cur.x = fmaf(wk, y.x, cur.x);
-                cur.y = fmaf(wk, y.y, cur.y);
-                row[b * 32] = cur;
+                const float wk = g.w[a] * g.w[J + b];
+                cur[a][b].x = fmaf(wk, y.x, cur[a][b].x);
+                cur[a][b].y = fmaf(wk, y.y, cur[a][b].y);
             }
-        }
+#pragma unroll
+        for (int a = 0; a < J; ++a)
+#pragma unroll
+            for (int b = 0; b < J; ++b) base[(a * R1 + b) * 32] = cur[a][b];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nreg * 32; e += blockDim.x) {

@@ -791,9 +791,9 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     {
         const BinPlan& bb = gp.bins;
         const size_t smem = sizeof(float2) * kGrWarps * 32 * bb.nreg;
-        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_views<kGrJ, kGrWarps>,
+        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_views<kGrJ, kGrWarps, kGrTileRev>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_gr_spread_views<kGrJ, kGrWarps><<<bb.nsubs, kGrWarps * 32, smem, s>>>(
+        k_gr_spread_views<kGrJ, kGrWarps, kGrTileRev><<<bb.nsubs, kGrWarps * 32, smem, s>>>(
             p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(),
             reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p), bb.subs.p, p->gr_t.p,
             (size_t)u.n_mu * u.n_t, nb);
