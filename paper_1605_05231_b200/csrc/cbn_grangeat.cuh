@@ -159,29 +159,58 @@ k_gr_spread_views(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg
     __syncthreads();
     const bool live = lane < nviews;
     const float2* tfl = tf + (size_t)lane * tf_stride;
-    for (int k = warp; k < sp.count; k += WARPS) {
-        const GrPoint<J> g = pts[sp.start + k];
-        if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
-        const float2 y = live ? cmul(__ldg(tfl + g.col), g.fac) : make_float2(0.f, 0.f);
-        // the J x J cells are distinct: load all, update, store all
-        float2* base = copy + (g.lu * R1 + g.lv) * 32 + lane;
-        float2 cur[J][J];
+    // CH points per step: lanes < CH fetch one point record each; then every
+    // lane issues its CH view-value loads back to back (deep memory-level
+    // parallelism at 4 warps / SM), and the CH points are applied from registers
+    constexpr int CH = 16;
+    for (int base0 = warp * CH; base0 < sp.count; base0 += WARPS * CH) {
+        const int npts = min(CH, sp.count - base0);
+        GrPoint<J> mine;
+        if (lane < npts) mine = pts[sp.start + base0 + lane];
+        else {
+            mine.lu = mine.lv = 0;
+            mine.col = 0;
+            mine.fac = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int a = 0; a < J; ++a)
+            for (int q = 0; q < 2 * J; ++q) mine.w[q] = 0.f;
+        }
+        float2 yv[CH];
 #pragma unroll
-            for (int b = 0; b < J; ++b) cur[a][b] = base[(a * R1 + b) * 32];
+        for (int j = 0; j < CH; ++j) {
+            const int col = __shfl_sync(0xffffffffu, mine.col, j);
+            yv[j] = (live && j < npts) ? __ldg(tfl + col) : make_float2(0.f, 0.f);
+        }
 #pragma unroll
-        for (int a = 0; a < J; ++a)
+        for (int j = 0; j < CH; ++j) {
+            const float fx = __shfl_sync(0xffffffffu, mine.fac.x, j);
+            const float fy = __shfl_sync(0xffffffffu, mine.fac.y, j);
+            if (fx == 0.f && fy == 0.f) continue;   // warp-uniform (also past npts)
+            const int lu = __shfl_sync(0xffffffffu, (int)mine.lu, j);
+            const int lv = __shfl_sync(0xffffffffu, (int)mine.lv, j);
+            float w[2 * J];
 #pragma unroll
-            for (int b = 0; b < J; ++b) {
-                const float wk = g.w[a] * g.w[J + b];
-                cur[a][b].x = fmaf(wk, y.x, cur[a][b].x);
-                cur[a][b].y = fmaf(wk, y.y, cur[a][b].y);
-            }
+            for (int q = 0; q < 2 * J; ++q) w[q] = __shfl_sync(0xffffffffu, mine.w[q], j);
+            const float2 y = cmul(yv[j], make_float2(fx, fy));
+            // the J x J cells are distinct: load all, update, store all
+            float2* base = copy + (lu * R1 + lv) * 32 + lane;
+            float2 cur[J][J];
 #pragma unroll
-        for (int a = 0; a < J; ++a)
+            for (int a = 0; a < J; ++a)
 #pragma unroll
-            for (int b = 0; b < J; ++b) base[(a * R1 + b) * 32] = cur[a][b];
+                for (int b = 0; b < J; ++b) cur[a][b] = base[(a * R1 + b) * 32];
+#pragma unroll
+            for (int a = 0; a < J; ++a)
+#pragma unroll
+                for (int b = 0; b < J; ++b) {
+                    const float wk = w[a] * w[J + b];
+                    cur[a][b].x = fmaf(wk, y.x, cur[a][b].x);
+                    cur[a][b].y = fmaf(wk, y.y, cur[a][b].y);
+                }
+#pragma unroll
+            for (int a = 0; a < J; ++a)
+#pragma unroll
+                for (int b = 0; b < J; ++b) base[(a * R1 + b) * 32] = cur[a][b];
+        }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nreg * 32; e += blockDim.x) {
