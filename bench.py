@@ -32,6 +32,9 @@ sys.path.insert(0, REPO)
 
 PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
+# dram__bytes_read.sum + dram__bytes_write.sum per step from the committed ncu
+# captures (profiles/README.md), keyed by stage; None where not captured
+TRAFFIC: dict = {}
 
 
 def parse_args():
@@ -109,25 +112,30 @@ class ClockSampler:
 
 
 # ------------------------------------------------------- roofline helpers
-def stage_bytes(stage: str, w, per_step_views: int) -> float | None:
-    """Algorithmic (compulsory) HBM bytes of one step's stage."""
+def stage_bytes(stage: str, w, views: int):
+    """Algorithmic bytes of one step's stage: (compulsory HBM bytes, on-chip tap
+    bytes).  DESIGN.md section 4 derives each; nodes/targets generated from
+    index tables stream no coordinates (c = 0 in SURVEY 8(d))."""
     spec, cfg = w.spec, w.cfg
     n = w.n
     K3 = (2 * n) ** 3
     M = spec.n_rho * spec.n_theta * spec.n_phi
-    pad = cfg.rho_pad
-    dr = spec.n_rho + 2 * pad
+    dr = spec.n_rho + 2 * cfg.rho_pad
     D = dr * spec.n_theta * spec.n_phi
     Kr = 8 * D
-    targets = cfg.n_mu * cfg.n_t
-    if stage == "spectrum_gather":        # read K^3 grid once, write M lattice values
-        return 8.0 * K3 + 8.0 * M
-    if stage == "spectrum_pad":           # read N^3 f32, write K^3 c64
-        return 4.0 * n ** 3 + 8.0 * K3
-    if stage == "resample_pad":           # per batch: read D c64, write K_r c64
-        return per_step_views * (8.0 * D + 8.0 * Kr)
-    if stage == "resample_gather":        # per batch: read K_r grid, write targets f32
-        return per_step_views * (8.0 * Kr + 4.0 * targets)
+    tpv = cfg.n_mu * cfg.n_t                  # umbrella targets per view
+    grid2 = 4 * w.geom.nu * w.geom.nv          # oversampled detector cells per view
+    J, Jr, Jg = 6, 3, 5
+    if stage == "spectrum_gather":             # read K^3 grid once, write M lattice values
+        return 8.0 * K3 + 8.0 * M, 8.0 * J ** 3 * M
+    if stage == "resample_gather":             # read the resample grid once, write f32 values
+        return 8.0 * Kr + 4.0 * tpv * views + 32.0 * tpv, 8.0 * Jr ** 3 * tpv * views
+    if stage == "grangeat_spread":             # read t-spectra, RED the 2D grids once
+        return 8.0 * tpv * views + 8.0 * grid2 * views + 56.0 * tpv, 16.0 * Jg ** 2 * tpv * views
+    if stage == "spectrum_pad":
+        return 4.0 * n ** 3 + 8.0 * K3, 0.0
+    if stage == "resample_pad":
+        return 8.0 * D + 8.0 * Kr, 0.0
     return None
 
 
@@ -248,17 +256,28 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     peak, peak_kind = hbm_peak()
-    # dominant stage among our kernels with an algorithmic byte count
-    ranked = sorted(((t, s) for s, t in stages.items() if stage_bytes(s, w, hi - lo) is not None),
-                    reverse=True)
+    # per-kernel rooflines for the stages that are a single kernel of ours
+    kernels = {}
+    for st, t_ms in stages.items():
+        sb = stage_bytes(st, w, hi - lo)
+        if sb is None or t_ms <= 0:
+            continue
+        hbm_b, chip_b = sb
+        ach = hbm_b / (t_ms / 1e3) / 1e9
+        kernels[st] = {"ms_per_step": round(t_ms, 3), "hbm_bytes": hbm_b,
+                       "achieved_gbs": round(ach, 1), "hbm_frac": round(ach / peak, 4),
+                       "onchip_tap_bytes": chip_b,
+                       "onchip_tbs": round(chip_b / (t_ms / 1e3) / 1e12, 2)}
     roofline = None
-    if ranked:
-        t_ms, st = ranked[0]
-        b = stage_bytes(st, w, hi - lo)
-        ach = b / (t_ms / 1e3) / 1e9
-        roofline = {"kernel": st, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
-                    "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-                    "traffic": None, "algorithmic_bytes_per_step": b, "ms_per_step": t_ms}
+    if kernels:
+        st = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+        kk = kernels[st]
+        roofline = {"kernel": st, "bound": "hbm", "achieved": kk["achieved_gbs"], "peak": peak,
+                    "unit": "GB/s", "frac": kk["hbm_frac"], "traffic": TRAFFIC.get(st),
+                    "peak_kind": peak_kind,
+                    "note": "achieved = compulsory bytes / CUDA-event stage time; these "
+                            "gathers/spreads are bound on chip (tap traffic, onchip_tbs)",
+                    "onchip_tbs": kk["onchip_tbs"]}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample(w, direction, n_samples=1)
@@ -286,6 +305,7 @@ def run_ours(args):
         "gpu_launches_per_step": int(launches) // max(args.steps, 1),
         "clocks": clk,
         "roofline": roofline,
+        "kernels": kernels,
         "stages_ms_per_step": {k: round(v, 3) for k, v in stages.items()},
         "cpu_baseline": cpu,
     }

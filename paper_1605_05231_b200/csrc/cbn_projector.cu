@@ -781,14 +781,16 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     const int64_t tl = (int64_t)nb * u.n_mu * u.n_t;
     p->gr_t.ensure((size_t)tl);
     p->gr_grid.ensure((size_t)nb * Ku * Kv);
-    StageScope st(p->timer, "grangeat_reverse", s);
+    prepare_gr_points(p, gp, u, true, s);
+    if (p->timer.on) p->timer.begin("grangeat_tfft", s);
     k_gr_pre<<<blocks_for(tl, 256), 256, 0, s>>>(vals, gp.w2.p, u.n_t, tl, p->gr_t.p);
     CBN_LAUNCH_CHECK();
     long long nt[1] = {u.n_t};
     p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_FORWARD, s);
     CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
-    prepare_gr_points(p, gp, u, true, s);
+    if (p->timer.on) p->timer.end(s);
     {
+        StageScope st(p->timer, "grangeat_spread", s);
         const BinPlan& bb = gp.bins;
         const size_t smem = sizeof(float2) * kGrWarps * 32 * bb.nreg;
         CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_views<kGrJ, kGrWarps, kGrTileRev>,
@@ -800,6 +802,7 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         CBN_LAUNCH_CHECK();
     }
     long long kd[2] = {Ku, Kv};
+    StageScope st(p->timer, "grangeat_ifft_post", s);
     p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_INVERSE, s);
     GrPost q = gr_post(p, gp);
     p->red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
