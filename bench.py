@@ -32,9 +32,11 @@ sys.path.insert(0, REPO)
 
 PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
-# dram__bytes_read.sum + dram__bytes_write.sum per step from the committed ncu
-# captures (profiles/README.md), keyed by stage; None where not captured
-TRAFFIC: dict = {}
+# dram__bytes_read.sum + dram__bytes_write.sum per config-2 step, summed over
+# the stage's launches, from the committed ncu launch list
+# (profiles/r1a_launches_fwd.txt); stages not captured there report null
+TRAFFIC: dict = {"resample_gather": 14.581e9, "grangeat_spread": 4.195e9,
+                 "spectrum_gather": 1.027e9}
 
 
 def parse_args():
@@ -152,9 +154,13 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1605_05231_b200 import pipeline as _pl
+    from paper_1605_05231_b200 import sharding
     w = workload(args.config)
     V = w.geom.n_views
-    lo, hi = rank * V // world, (rank + 1) * V // world
+    per_view = w.cfg.n_mu * w.cfg.n_t
+    lo, hi = sharding.view_shard(V, world, rank,
+                                 sharding.view_batches(V, per_view, _pl._TARGET_BATCH))
     vol_host = w.volume()
     lib = _lib.load()
     direction = 1 if args.direction == "forward" else 2
