@@ -67,6 +67,31 @@ int cbn_nufft_first_indices(const cbn_nufft* plan, int32_t* out, void* stream);
 int cbn_nufft_type2(cbn_nufft* plan, const void* x, void* y, void* stream);
 /* nufft_adjoint (nufft.py:236-247): y [device] complex64 m -> x [device] complex64 dims */
 int cbn_nufft_type1(cbn_nufft* plan, const void* y, void* x, void* stream);
+/* apply (1, default) or omit (0) the per-node centring phase exp(-i w.(N//2))
+ * (nufft.py:215-216) -- omitted where the caller's own phase cancels it
+ * exactly (resampling.py:147-148, SURVEY finding 9) */
+int cbn_nufft_set_phase(cbn_nufft* plan, int32_t on);
+
+/* ------------------------------------------------------------ resampling
+ * plan_resample / resample_apply / resample_transpose, method A
+ * (resampling.py:79-103,136-148,164-196).  targets [host] m x 3 float64
+ * fractional lattice indices (rho, theta, phi); lattice arrays [device]
+ * complex64 in the reference layout (n_rho, n_theta, n_phi).
+ */
+typedef struct cbn_resample_s cbn_resample;
+int cbn_resample_create(cbn_resample** plan, int32_t n_rho, int32_t n_theta, int32_t n_phi,
+                        int32_t rho_pad, const int32_t* taps, double oversample_factor,
+                        const double* targets, int64_t m, const int64_t* ls_rows, int64_t n_ls,
+                        void* stream);
+int cbn_resample_destroy(cbn_resample* plan);
+int cbn_resample_apply(cbn_resample* plan, const void* lattice, void* values, void* stream);
+int cbn_resample_transpose(cbn_resample* plan, const void* values, void* lattice, void* stream);
+
+/* radial_fft / radial_ifft (radon_fourier.py:117-135): centred FFT (inverse=0)
+ * or IFFT (inverse=1, includes 1/n) of `lines` contiguous complex64 lines of
+ * length n [device], in place, times `scale` */
+int cbn_radial_fft(void* data, int64_t n, int64_t lines, int32_t inverse, double scale,
+                   void* stream);
 
 /* -------------------------------------------------------------- projector
  * Replaces ConeGeometry / ProjectorConfig / nufft_forward_project /
@@ -98,6 +123,8 @@ typedef struct {
     double normalization, bp_normalization, den_tol;
     int64_t target_batch;      /* pipeline._TARGET_BATCH */
     int64_t plan_chunk;        /* nufft._PLAN_CHUNK */
+    int32_t bp_n_t;            /* <= 0 : 2 nu (pipeline.py:168); else the t grid of */
+    double bp_t_pitch_mm;      /* <= 0 : virtual pixel; the back-direction Grangeat */
 } cbn_projector_config;
 
 typedef struct cbn_projector_s cbn_projector;
@@ -126,6 +153,10 @@ int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
 int cbn_backproject(cbn_projector* proj, const float* frames, float* vol, void* stream);
 
 /* Stage entry points (for stage parity and the mirrored module API). */
+/* image_to_radial_spectrum (radon_fourier.py:89-108): complex64 node-order
+ * values (n_phi, n_theta, n_rho), centre phase applied, no basis transfer */
+int cbn_projector_radial_spectrum(cbn_projector* proj, const float* vol, void* spectrum,
+                                  void* stream);
 /* _radial_lattice (pipeline.py:113-119): complex64 lattice, layout
  * (n_phi, n_theta, n_rho) -- rho fastest, i.e. node order. */
 int cbn_projector_radial_lattice(cbn_projector* proj, const float* vol, void* lattice,

@@ -44,7 +44,7 @@ class ProjectorConfig(ctypes.Structure):
                 ("resample_j", c_i32 * 3), ("side_lobes", c_i32), ("oversample_factor", c_f64),
                 ("rho_pad", c_i32), ("basis", c_i32), ("normalization", c_f64),
                 ("bp_normalization", c_f64), ("den_tol", c_f64), ("target_batch", c_i64),
-                ("plan_chunk", c_i64)]
+                ("plan_chunk", c_i64), ("bp_n_t", c_i32), ("bp_t_pitch_mm", c_f64)]
 
 
 _SIGS = {
@@ -59,6 +59,14 @@ _SIGS = {
     "cbn_nufft_first_indices": (ctypes.c_int, [c_vp, P_i32, c_vp]),
     "cbn_nufft_type2": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_nufft_type1": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cbn_nufft_set_phase": (ctypes.c_int, [c_vp, c_i32]),
+    "cbn_resample_create": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, c_i32, P_i32,
+                                           c_f64, P_f64, c_i64, P_i64, c_i64, c_vp]),
+    "cbn_resample_destroy": (ctypes.c_int, [c_vp]),
+    "cbn_resample_apply": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cbn_resample_transpose": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cbn_radial_fft": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i32, c_f64, c_vp]),
+    "cbn_projector_radial_spectrum": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_projector_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(Geometry),
                                             ctypes.POINTER(ProjectorConfig), c_i32, c_f64, c_i32]),
     "cbn_projector_destroy": (ctypes.c_int, [c_vp]),

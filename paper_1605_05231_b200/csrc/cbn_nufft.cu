@@ -258,6 +258,16 @@ int cbn_nufft_destroy(cbn_nufft* plan) {
     return CBN_OK;
 }
 
+int cbn_nufft_set_phase(cbn_nufft* p, int32_t on) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        for (int d = 0; d < p->D; ++d) p->centre[d] = on ? (double)(p->ax[d].N / 2) : 0.0;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int cbn_nufft_scaling(const cbn_nufft* p, double* out) {
     try {
         CBN_REQUIRE(p && out, "null argument");

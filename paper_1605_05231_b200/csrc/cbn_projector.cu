@@ -91,11 +91,16 @@ struct SpecOut {
     double pc[3];          // N/2 - 1/2 - N//2 per axis (centre phase * plan phase)
     int n_rho;
     int tri;
+    int spectrum_only;     // 1: image_to_radial_spectrum values in node order
     CBN_D void put(int64_t i, float2 v, const double (&w)[3], const RadialSrc::Aux& a) const {
         double ang = w[0] * pc[0] + w[1] * pc[1] + w[2] * pc[2];
         double sn, cs;
         sincos(ang, &sn, &cs);
         float2 r = cmul(v, make_float2((float)cs, (float)sn));
+        if (spectrum_only) {
+            out[i] = r;
+            return;
+        }
         if (tri) {
             float t = 1.f;
 #pragma unroll
@@ -495,7 +500,8 @@ void build_backward(P* p, cudaStream_t s) {
     const double extent = out * p->voxel;
     const int n_rho = 2 * (int)std::ceil(1.5 * out / 2.0);                 // pipeline.py:165
     p->brad.build(n_rho, c.spec.n_theta, c.spec.n_phi, extent * std::sqrt(3.0) / 2.0, p->voxel, s);
-    p->bumb.build(p->g, c.n_mu, 2 * p->g.nu, p->pu, s);                    // pipeline.py:168
+    p->bumb.build(p->g, c.n_mu, c.bp_n_t > 0 ? c.bp_n_t : 2 * p->g.nu,     // pipeline.py:168
+                  c.bp_t_pitch_mm > 0 ? c.bp_t_pitch_mm : p->pu, s);
     for (int d = 0; d < 3; ++d) p->bspec[d] = make_axis(out, c.spectrum_j, c.oversample_factor);
     p->bpad = std::min(n_rho / 8, 32);                                       // pipeline.py:169
     const int dr = n_rho + 2 * p->bpad;
@@ -521,7 +527,7 @@ void compute_needed(P* p) {
         const int n_rho = 2 * (int)std::ceil(1.5 * p->n_vol / 2.0);
         int64_t M = (int64_t)n_rho * c.spec.n_theta * c.spec.n_phi;
         add_needed(p, spectrum_chunk(p, M));
-        int64_t per_view = (int64_t)c.n_mu * 2 * p->g.nu;
+        int64_t per_view = (int64_t)c.n_mu * (c.bp_n_t > 0 ? c.bp_n_t : 2 * p->g.nu);
         for (auto& b : view_batches(p->g.n_views, per_view, target_batch(p)))
             add_needed(p, per_view * (b.second - b.first));
         add_needed(p, per_view);
@@ -554,8 +560,10 @@ int64_t ktot(const AxisPlan* ax) { return (int64_t)ax[0].K * ax[1].K * ax[2].K; 
 
 // ---------------------------------------------------------------- forward
 
-// radial lattice in raw layout (IFFT output, ifftshifted rho) into p->lattice
-void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
+// radial lattice in raw layout (IFFT output, ifftshifted rho) into p->lattice;
+// with `spectrum` the image_to_radial_spectrum values go there instead (node
+// order, no basis transfer / derivative / IFFT)
+void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum = nullptr) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fspec;
     const int64_t M = r.nodes();
@@ -565,13 +573,19 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
     p->lattice.ensure((size_t)M);
     const int smax = n;
     p->s32.ensure(3 * (size_t)smax);
-    // scaling fit on the first sub-plan of nufft_forward_chunked (nufft.py:250-265)
-    int nrows;
-    const int64_t* rows = rows_for(p, spectrum_chunk(p, M), nrows);
     RemapAxis rax[3];
     {
         StageScope st(p->timer, "spectrum_fit", s);
-        ls_fit<3>(r.src(), rows, nrows, ax, p->ls, p->s32.p, smax, s);
+        if (!p->fspec_fit) {
+            // scaling of the first sub-plan of nufft_forward_chunked (nufft.py:250-265), cached
+            int nrows;
+            const int64_t* rows = rows_for(p, spectrum_chunk(p, M), nrows);
+            p->fspec_s32.alloc(3 * (size_t)smax);
+            ls_fit<3>(r.src(), rows, nrows, ax, p->ls, p->fspec_s32.p, smax, s);
+            p->fspec_fit = true;
+        }
+        CBN_CUDA(cudaMemcpyAsync(p->s32.p, p->fspec_s32.p, sizeof(float) * 3 * smax,
+                                 cudaMemcpyDeviceToDevice, s));
         const int64_t sstr[3] = {(int64_t)n * n, n, 1};
         build_tables(p, kTabPad, ax, smax, s, rax, sstr);
     }
@@ -586,11 +600,12 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
         p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
     }
     SpecOut epi;
-    epi.out = p->lattice.p;
+    epi.out = spectrum ? spectrum : p->lattice.p;
     epi.om_phys = r.om_phys.p;
     for (int d = 0; d < 3; ++d) epi.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
     epi.n_rho = r.n_rho;
     epi.tri = p->c.basis == 0;
+    epi.spectrum_only = spectrum != nullptr;
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
     if (!p->fspec_bins.ready) {
@@ -612,6 +627,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s) {
         });
         CBN_LAUNCH_CHECK();
     }
+    if (spectrum) return;
     // centred IFFT along rho (radon_fourier.py:122-124,133-135); 1/(n d_rho) applied by consumers
     long long nr1[1] = {r.n_rho};
     StageScope st(p->timer, "radial_ifft", s);
@@ -1032,6 +1048,19 @@ int cbn_projector_radial_lattice(cbn_projector* p, const float* vol, void* latti
                                                            r.n_rho, M,
                                                            (float)(1.0 / (r.n_rho * r.d_rho)));
         CBN_LAUNCH_CHECK();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_radial_spectrum(cbn_projector* p, const float* vol, void* spectrum, void* stream) {
+    try {
+        CBN_REQUIRE(p && vol && spectrum, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        radial_lattice_raw(p, vol, s, static_cast<float2*>(spectrum));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

@@ -104,6 +104,8 @@ struct cbn_projector_s {
     bool fw_built = false;
     cbn::BatchPlan fbatch;
     cbn::BinPlan fspec_bins;     // radial nodes sorted by spectrum-grid tile
+    bool fspec_fit = false;
+    cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT
 
     // ---- back
     cbn::RadialTables brad;

@@ -95,7 +95,8 @@ class Projector:
     """Device plan of the forward projector and/or backprojector."""
 
     def __init__(self, geom, cfg, n: int, voxel_mm: float, direction: int = 3,
-                 target_batch: int | None = None, plan_chunk: int | None = None):
+                 target_batch: int | None = None, plan_chunk: int | None = None,
+                 bp_n_t: int | None = None, bp_t_pitch_mm: float | None = None):
         from . import nufft as _nufft
         lib = _lib.load()
         _device.require_cuda()
@@ -105,6 +106,9 @@ class Projector:
         pc = _nufft._PLAN_CHUNK if plan_chunk is None else int(plan_chunk)
         self._g = _geometry_struct(geom)
         self._c = _config_struct(cfg, tb, pc)
+        self.bp_n_t = 2 * int(geom.nu) if bp_n_t is None else int(bp_n_t)
+        self._c.bp_n_t = self.bp_n_t
+        self._c.bp_t_pitch_mm = -1.0 if bp_t_pitch_mm is None else float(bp_t_pitch_mm)
         h = ctypes.c_void_p()
         _lib.check(lib.cbn_projector_create(ctypes.byref(h), ctypes.byref(self._g),
                                             ctypes.byref(self._c), self.n, self.voxel,
@@ -185,7 +189,7 @@ class Projector:
         t = _device.require_cuda()
         f = _device.to_device(frames, t.float32)
         nb = f.shape[0]
-        out = t.empty((nb, self.cfg.n_mu, 2 * self.geom.nu), dtype=t.float32, device="cuda")
+        out = t.empty((nb, self.cfg.n_mu, self.bp_n_t), dtype=t.float32, device="cuda")
         _lib.check(_lib.load().cbn_projector_grangeat_forward(self._h, _device.ptr(f),
                                                               _device.ptr(out), nb, self._s))
         return out
