@@ -146,11 +146,14 @@ def test_grangeat_views_golden(gr, golden_n16):
 
 
 def test_fbp2d_roundtrip(rf):
-    """2D radial spectrum -> NUFFT FBP recovers a smooth image (device NUFFTs)."""
+    """Radial spectrum -> NUFFT FBP recovers a smooth image, device NUFFTs
+    (pkg/tests/test_radon_fourier.py:130-143)."""
     n = 32
-    c = (np.arange(n) - n / 2 + 0.5) / (n / 2)
+    c = (np.arange(n) - n / 2.0 + 0.5) / (n / 2.0)
     xx, yy = np.meshgrid(c, c, indexing="ij")
-    img = np.maximum(1 - (xx ** 2 + yy ** 2) / 0.5, 0) ** 2
-    spec = rf.image_to_radial_spectrum_2d(img, 4 * n, 3 * n)
+    img = np.maximum(1.0 - (xx ** 2 + yy ** 2) / 0.49, 0.0) ** 2
+    spec = rf.image_to_radial_spectrum_2d(img, 2 * n, 100)
     rec, imag_ratio = rf.fbp2d_nufft(spec, n)
-    assert rel_l2(rec, img) < 0.05 and imag_ratio < 1e-2
+    assert imag_ratio < 1e-3
+    mask = xx ** 2 + yy ** 2 <= 1.0
+    assert np.mean(np.abs(rec - img)[mask]) / np.mean(np.abs(img[mask])) < 0.05
