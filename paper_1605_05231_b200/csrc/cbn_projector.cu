@@ -125,6 +125,65 @@ struct UmbOut {
     }
 };
 
+// Resample gather with views in lanes, for geometries where consecutive views'
+// targets differ by a whole number of oversampled phi cells (2 n_phi / V
+// integer) and share one resample grid.  The grid is stored phi-fastest
+// [rho][theta][phi]; a warp takes one base target and lanes take 32 views, so
+// the rho/theta taps and index math are warp-uniform and the phi taps of
+// the lanes are consecutive cells.  32 base targets per CTA; values are
+// transposed through shared memory so each view's row is stored coalesced.
+template <int J>
+__global__ void __launch_bounds__(256)
+k_resample_views(const float2* __restrict__ G, KBSet kb, UmbrellaSrc src, int64_t per_view,
+                 int nviews, float* __restrict__ vals) {
+    __shared__ float tile[32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t0 = (int64_t)blockIdx.x * 32;
+    const int K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        const int tl = warp * 4 + q;
+        const int64_t t = t0 + tl;
+        float out = 0.f;
+        if (t < per_view && lane < nviews) {
+            double wd[3];
+            UmbrellaSrc::Aux aux;
+            src.node((int64_t)lane * per_view + t, wd, aux);   // device order (phi, theta, rho)
+            if (aux.valid) {
+                const double w[3] = {wd[2], wd[1], wd[0]};        // grid order (rho, theta, phi)
+                int first[3];
+                float wt[3][J];
+                tap_setup<3, J>(kb, w, first, wt);
+                int c2[J];
+#pragma unroll
+                for (int c = 0; c < J; ++c) c2[c] = wrapc(first[2] + c, K2);
+                float acc = 0.f;
+#pragma unroll
+                for (int a = 0; a < J; ++a) {
+                    const float2* plane = G + (size_t)wrapc(first[0] + a, kb.ax[0].K) * K1 * K2;
+                    float pa = 0.f;
+#pragma unroll
+                    for (int b = 0; b < J; ++b) {
+                        const float2* row = plane + (size_t)wrapc(first[1] + b, K1) * K2;
+                        float r = 0.f;
+#pragma unroll
+                        for (int c = 0; c < J; ++c) r = fmaf(wt[2][c], __ldg(row + c2[c]).x, r);
+                        pa = fmaf(wt[1][b], r, pa);
+                    }
+                    acc = fmaf(wt[0][a], pa, acc);
+                }
+                out = acc;   // Re(resample_apply): only the real part is kept
+            }
+        }
+        tile[lane][tl] = out;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int v = e >> 5, tt = e & 31;
+        if (v < nviews && t0 + tt < per_view) vals[(size_t)v * per_view + t0 + tt] = tile[v][tt];
+    }
+}
+
 // ----------------------------------------------------------------- kernels
 
 // lattice[line][j] = raw[line][(j - n//2) mod n] * scale   (fftshift of the IFFT)
@@ -704,9 +763,10 @@ void ensure_batch_plan(P* p, BatchPlan& bp, const UmbrellaTables& u, const Radia
 
 // G = FFT_2x(pad(fftshift(F) / size * scaling)) for a batch's scalings
 // (resample_apply + nufft_forward, resampling.py:146-147, nufft.py:226-231)
-void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s) {
+// phi_fast: grid stored [rho][theta][phi] for k_resample_views, else [phi][theta][rho]
+void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool phi_fast = false) {
     const RadialTables& r = p->frad;
-    const AxisPlan* ax = p->fres;
+    const AxisPlan* ax = p->fres;   // (phi, theta, rho)
     const int dr = r.n_rho + 2 * p->fpad;
     RemapAxis rax[3];
     const int64_t sstr[3] = {(int64_t)r.n_theta * dr, dr, 1};
@@ -720,6 +780,7 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s) {
         rax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, ax[d].K, sstr[d]};
         off += ax[d].K;
     }
+    if (phi_fast) std::swap(rax[0], rax[2]);
     p->big.ensure((size_t)ktot(ax));
     const double size = (double)dr * r.n_theta * r.n_phi;
     {
@@ -728,8 +789,35 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s) {
         CBN_LAUNCH_CHECK();
     }
     long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    if (phi_fast) std::swap(kd[0], kd[2]);
     StageScope st(p->timer, "resample_fft", s);
     p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+}
+
+// views-in-lanes path applies when every view's targets are view 0's shifted by
+// a whole number of oversampled phi cells: 2 n_phi k / V integer for all k
+bool views_in_lanes(const P* p) {
+    const int V = p->g.n_views;
+    return (2LL * p->frad.n_phi) % V == 0 && p->fres[0].K == 2 * p->frad.n_phi;
+}
+
+// Re(resample_apply) for nb <= 32 consecutive views [v0, v0 + nb) from a phi-fast grid
+void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s) {
+    const AxisPlan* ax = p->fres;
+    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+    UmbrellaSrc src = cached_umbrella(p, p->fumb, p->frad, p->fpad, v0, s);
+    KBSet kb;
+    kb.ax[0] = ax[2].kb;
+    kb.ax[1] = ax[1].kb;
+    kb.ax[2] = ax[0].kb;
+    StageScope st(p->timer, "resample_gather", s);
+    dispatch_j(ax[0].J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(p->big.p, kb, src,
+                                                                             per_view, nb, vals);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
 }
 
 // Re(resample_apply) at the umbrella targets of views [lo, hi) from the current grid
@@ -852,21 +940,30 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         blk_lo += blk_n;
         blk_n = 0;
     };
+    const bool lanes = views_in_lanes(p);
+    auto gather = [&](int v, int n, float* out) {
+        if (!lanes) {
+            gather_views(p, v, v + n, out, s);
+            return;
+        }
+        for (int k = 0; k < n; k += 32)
+            gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, s);
+    };
     for (size_t b = 0; b < bp.batches.size(); ++b) {
         const int vlo = std::max(lo, bp.batches[b].first), vhi = std::min(hi, bp.batches[b].second);
         if (vlo >= vhi) continue;
         const int g = bp.group[b];
         if (g != cur) {
-            build_resample_grid(p, bp.s32.p + (size_t)g * 3 * bp.smax, bp.smax, s);
+            build_resample_grid(p, bp.s32.p + (size_t)g * 3 * bp.smax, bp.smax, s, lanes);
             cur = g;
         }
         if (values_out) {
-            gather_views(p, vlo, vhi, values_out + (size_t)(vlo - lo) * per_view, s);
+            gather(vlo, vhi - vlo, values_out + (size_t)(vlo - lo) * per_view);
             continue;
         }
         for (int v = vlo; v < vhi;) {
             const int take = std::min(vhi - v, kViewBlock - blk_n);
-            gather_views(p, v, v + take, p->values.p + (size_t)blk_n * per_view, s);
+            gather(v, take, p->values.p + (size_t)blk_n * per_view);
             blk_n += take;
             v += take;
             if (blk_n == kViewBlock) flush();
