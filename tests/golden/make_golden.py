@@ -173,6 +173,13 @@ def main():
         np.savez_compressed(os.path.join(HERE, "pipeline_n12_dirac.npz"),
                             **pipeline_small(12, 8, 3, "dirac"))
         print(f"small fixtures {time.time() - t:.1f}s", flush=True)
+    if "small" in which or "rot" in which:
+        # geometries where 2 n_phi / V is an integer (whole oversampled phi cells
+        # per view): the device's views-in-lanes resample path
+        np.savez_compressed(os.path.join(HERE, "pipeline_n16_v8.npz"),
+                            **pipeline_small(16, 8, 21, "trilinear"))
+        np.savez_compressed(os.path.join(HERE, "pipeline_n12_v48.npz"),
+                            **pipeline_small(12, 48, 22, "trilinear"))
     if "big" in which:
         np.savez_compressed(os.path.join(HERE, "config0.npz"), **config0())
 

@@ -69,3 +69,13 @@ def test_oracle_end_to_end(which, golden_n16, golden_n12):
         assert rel_l2(fb5, g["frames_b5"]) < 1e-11
         assert rel_l2(orc.backproject(g["frames"], geom, cfg, n, voxel, target_batch=4096),
                       g["bp_b4"]) < 1e-11
+
+
+@pytest.mark.parametrize("name", ["pipeline_n16_v8", "pipeline_n12_v48"])
+def test_oracle_rotation_aligned(name):
+    import os
+    from conftest import GOLDEN
+    g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    assert rel_l2(orc.forward_project(g["vol"], voxel, geom, cfg), g["frames"]) < 1e-11
