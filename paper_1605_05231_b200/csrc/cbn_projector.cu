@@ -10,6 +10,7 @@
 // Backprojector (pipeline.py:150-212): the transposed chain.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -797,6 +798,8 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
 // views-in-lanes path applies when every view's targets are view 0's shifted by
 // a whole number of oversampled phi cells: 2 n_phi k / V integer for all k
 bool views_in_lanes(const P* p) {
+    const char* off = std::getenv("CBN_NO_VIEW_LANES");
+    if (off && off[0] == '1') return false;
     const int V = p->g.n_views;
     return (2LL * p->frad.n_phi) % V == 0 && p->fres[0].K == 2 * p->frad.n_phi;
 }
