@@ -133,45 +133,79 @@ struct UmbOut {
 // the rho/theta taps and index math are warp-uniform and the phi taps of
 // the lanes are consecutive cells.  32 base targets per CTA; values are
 // transposed through shared memory so each view's row is stored coalesced.
+// Taps of one base-view (view 0) umbrella target in grid order (rho, theta,
+// phi): view v's phi taps are these shifted by v * (2 n_phi / V) cells with the
+// same weights (u_phi(v) = u_phi(0) - 2 v n_phi / V exactly), so the per-view
+// kernel does no index math at all.
+template <int J>
+struct RsTap {
+    int f[3];       // first tap per axis, wrapped into [0, K)
+    int valid;
+    float w[3][J];
+};
+
+template <int J>
+__global__ void k_rs_taps(UmbrellaSrc src, KBSet kb, int64_t n, RsTap<J>* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double wd[3];
+    UmbrellaSrc::Aux aux;
+    src.node(i, wd, aux);                               // device order (phi, theta, rho)
+    const double w[3] = {wd[2], wd[1], wd[0]};          // grid order (rho, theta, phi)
+    int first[3];
+    float wt[3][J];
+    tap_setup<3, J>(kb, w, first, wt);
+    RsTap<J> t;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        t.f[d] = wrapc(first[d], kb.ax[d].K);
+#pragma unroll
+        for (int p = 0; p < J; ++p) t.w[d][p] = wt[d][p];
+    }
+    t.valid = aux.valid ? 1 : 0;
+    out[i] = t;
+}
+
 template <int J>
 __global__ void __launch_bounds__(256)
-k_resample_views(const float2* __restrict__ G, KBSet kb, UmbrellaSrc src, int64_t per_view,
-                 int nviews, float* __restrict__ vals) {
+k_resample_views(const float2* __restrict__ G, int K0, int K1, int K2,
+                 const RsTap<J>* __restrict__ taps, int64_t per_view, int v0, int nviews,
+                 int shift, float* __restrict__ vals) {
     __shared__ float tile[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t0 = (int64_t)blockIdx.x * 32;
-    const int K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+    const int v = v0 + lane;
+    const int pshift = (int)(((int64_t)v * shift) % K2);
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
         const int tl = warp * 4 + q;
         const int64_t t = t0 + tl;
         float out = 0.f;
-        if (t < per_view && lane < nviews) {
-            double wd[3];
-            UmbrellaSrc::Aux aux;
-            src.node((int64_t)lane * per_view + t, wd, aux);   // device order (phi, theta, rho)
-            if (aux.valid) {
-                const double w[3] = {wd[2], wd[1], wd[0]};        // grid order (rho, theta, phi)
-                int first[3];
-                float wt[3][J];
-                tap_setup<3, J>(kb, w, first, wt);
+        if (t < per_view) {
+            const RsTap<J> tp = taps[t];
+            if (tp.valid && lane < nviews) {
+                const int fp = tp.f[2] - pshift;
                 int c2[J];
 #pragma unroll
-                for (int c = 0; c < J; ++c) c2[c] = wrapc(first[2] + c, K2);
+                for (int c = 0; c < J; ++c) {
+                    int x = fp + c;
+                    x = x < 0 ? x + K2 : x;
+                    c2[c] = x >= K2 ? x - K2 : x;
+                }
                 float acc = 0.f;
 #pragma unroll
                 for (int a = 0; a < J; ++a) {
-                    const float2* plane = G + (size_t)wrapc(first[0] + a, kb.ax[0].K) * K1 * K2;
+                    const float2* plane = G + (size_t)wrapc(tp.f[0] + a, K0) * K1 * K2;
                     float pa = 0.f;
 #pragma unroll
                     for (int b = 0; b < J; ++b) {
-                        const float2* row = plane + (size_t)wrapc(first[1] + b, K1) * K2;
+                        const float2* row = plane + (size_t)wrapc(tp.f[1] + b, K1) * K2;
                         float r = 0.f;
 #pragma unroll
-                        for (int c = 0; c < J; ++c) r = fmaf(wt[2][c], __ldg(row + c2[c]).x, r);
-                        pa = fmaf(wt[1][b], r, pa);
+                        for (int c = 0; c < J; ++c) r = fmaf(tp.w[2][c], __ldg(row + c2[c]).x, r);
+                        pa = fmaf(tp.w[1][b], r, pa);
                     }
-                    acc = fmaf(wt[0][a], pa, acc);
+                    acc = fmaf(tp.w[0][a], pa, acc);
                 }
                 out = acc;   // Re(resample_apply): only the real part is kept
             }
@@ -487,7 +521,8 @@ UmbrellaSrc cached_umbrella(P* p, UmbrellaTables& u, const RadialTables& r, int 
         u.base_ready = true;
     }
     src.view0 = view0;
-    src.cache = u.base.p;
+    const char* off = std::getenv("CBN_NO_UMB_CACHE");
+    src.cache = (off && off[0] == '1') ? nullptr : u.base.p;
     return src;
 }
 
@@ -808,19 +843,29 @@ bool views_in_lanes(const P* p) {
 void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s) {
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
-    UmbrellaSrc src = cached_umbrella(p, p->fumb, p->frad, p->fpad, v0, s);
-    KBSet kb;
-    kb.ax[0] = ax[2].kb;
-    kb.ax[1] = ax[1].kb;
-    kb.ax[2] = ax[0].kb;
-    StageScope st(p->timer, "resample_gather", s);
+    const int shift = (int)(2LL * p->frad.n_phi / p->g.n_views);
     dispatch_j(ax[0].J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
-        k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(p->big.p, kb, src,
-                                                                             per_view, nb, vals);
+        UmbrellaTables& u = p->fumb;
+        if (!u.taps_ready) {
+            UmbrellaSrc src = cached_umbrella(p, u, p->frad, p->fpad, 0, s);
+            KBSet kb;
+            kb.ax[0] = ax[2].kb;
+            kb.ax[1] = ax[1].kb;
+            kb.ax[2] = ax[0].kb;
+            u.taps.alloc((size_t)per_view * sizeof(RsTap<J>));
+            k_rs_taps<J><<<blocks_for(per_view, 256), 256, 0, s>>>(
+                src, kb, per_view, reinterpret_cast<RsTap<J>*>(u.taps.p));
+            CBN_LAUNCH_CHECK();
+            u.taps_ready = true;
+        }
+        StageScope st(p->timer, "resample_gather", s);
+        k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
+            p->big.p, ax[2].K, ax[1].K, ax[0].K, reinterpret_cast<const RsTap<J>*>(u.taps.p),
+            per_view, v0, nb, shift, vals);
+        CBN_LAUNCH_CHECK();
         return 0;
     });
-    CBN_LAUNCH_CHECK();
 }
 
 // Re(resample_apply) at the umbrella targets of views [lo, hi) from the current grid
@@ -952,25 +997,40 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         for (int k = 0; k < n; k += 32)
             gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, s);
     };
-    for (size_t b = 0; b < bp.batches.size(); ++b) {
-        const int vlo = std::max(lo, bp.batches[b].first), vhi = std::min(hi, bp.batches[b].second);
-        if (vlo >= vhi) continue;
+    // runs of consecutive batches (clipped to [lo, hi)) sharing one scaling group
+    const size_t nbat = bp.batches.size();
+    size_t b = 0;
+    while (b < nbat) {
+        const int vlo = std::max(lo, bp.batches[b].first);
+        int vhi = std::min(hi, bp.batches[b].second);
+        if (vlo >= vhi) {
+            ++b;
+            continue;
+        }
         const int g = bp.group[b];
+        size_t e = b + 1;
+        while (e < nbat && bp.group[e] == g && bp.batches[e].first < hi) {
+            vhi = std::min(hi, bp.batches[e].second);
+            ++e;
+        }
         if (g != cur) {
             build_resample_grid(p, bp.s32.p + (size_t)g * 3 * bp.smax, bp.smax, s, lanes);
             cur = g;
         }
-        if (values_out) {
-            gather(vlo, vhi - vlo, values_out + (size_t)(vlo - lo) * per_view);
-            continue;
-        }
         for (int v = vlo; v < vhi;) {
+            if (values_out) {
+                const int take = std::min(vhi - v, kViewBlock);
+                gather(v, take, values_out + (size_t)(v - lo) * per_view);
+                v += take;
+                continue;
+            }
             const int take = std::min(vhi - v, kViewBlock - blk_n);
             gather(v, take, p->values.p + (size_t)blk_n * per_view);
             blk_n += take;
             v += take;
             if (blk_n == kViewBlock) flush();
         }
+        b = e;
     }
     flush();
 }

@@ -33,6 +33,8 @@ struct UmbrellaTables {
     DevBuf<double> cos_a, sin_a, cos_mu, sin_mu, omega_t;
     DevBuf<double4> base;   // view-0 target positions (see UmbrellaSrc::cache)
     bool base_ready = false;
+    DevBuf<char> taps;      // view-0 resample taps (RsTap) for the views-in-lanes gather
+    bool taps_ready = false;
     void build(const cbn_geometry& g, int n_mu, int n_t, double dt, cudaStream_t s);
 };
 
