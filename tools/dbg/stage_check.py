@@ -35,3 +35,8 @@ ref_fr = np.stack([orc.grangeat_reverse(ref_vals[k], gp) for k in range(views)])
 ef = [rel_l2(fr[k], ref_fr[k]) for k in range(views)]
 print("grangeat all", rel_l2(fr, ref_fr), "worst view", max(ef), int(np.argmax(ef)))
 print("frames golden vs oracle-chain", rel_l2(ref_fr, g["frames"]))
+# block-size dependence of the reverse Grangeat
+for nb in (1, 4, 8, 16, 32):
+    out = np.concatenate([proj.grangeat_reverse(ref_vals[k:k + nb].astype(np.float32)).cpu().numpy()
+                          for k in range(0, views, nb)])
+    print("grangeat block", nb, rel_l2(out, ref_fr))
