@@ -29,3 +29,17 @@ print("n", n, "worst impulses (err, mu, t):", [(f"{e:.2e}", a, b) for e, a, b in
 v = rng.standard_normal((cfg.n_mu, cfg.n_t))
 print("random input err", rel_l2(proj.grangeat_reverse(v[None].astype(np.float32)).cpu().numpy()[0],
                                 orc.grangeat_reverse(v, gp)))
+# every node as an impulse, 32 views per call
+bad = []
+M = cfg.n_mu * cfg.n_t
+for k0 in range(0, M, 32):
+    ks = list(range(k0, min(M, k0 + 32)))
+    v = np.zeros((len(ks), cfg.n_mu, cfg.n_t))
+    for i, k in enumerate(ks):
+        v[i].flat[k] = 1.0
+    got = proj.grangeat_reverse(v.astype(np.float32)).cpu().numpy()
+    for i, k in enumerate(ks):
+        e = rel_l2(got[i], orc.grangeat_reverse(v[i], gp))
+        if e > 1e-5:
+            bad.append((k // cfg.n_t, k % cfg.n_t, round(e, 3)))
+print("bad nodes (mu, t, err):", len(bad), bad[:20])
