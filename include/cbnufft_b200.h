@@ -152,6 +152,12 @@ int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
  * -> vol [device] float32 N^3 */
 int cbn_backproject(cbn_projector* proj, const float* frames, float* vol, void* stream);
 
+/* Diagnostics: the forward plan's per-node Grangeat records in bin-sorted
+ * order (56-byte records: int16 lu, lv; int32 col; float2 factor; float w[10])
+ * and the sorted node ids [host]; *m in: capacity, out: node count. */
+int cbn_projector_grangeat_records(cbn_projector* proj, void* records, int32_t* perm, int64_t* m,
+                                   void* stream);
+
 /* Stage entry points (for stage parity and the mirrored module API). */
 /* image_to_radial_spectrum (radon_fourier.py:89-108): complex64 node-order
  * values (n_phi, n_theta, n_rho), centre phase applied, no basis transfer */

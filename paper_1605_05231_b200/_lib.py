@@ -67,6 +67,7 @@ _SIGS = {
     "cbn_resample_transpose": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_radial_fft": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i32, c_f64, c_vp]),
     "cbn_projector_radial_spectrum": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cbn_projector_grangeat_records": (ctypes.c_int, [c_vp, c_vp, P_i32, P_i64, c_vp]),
     "cbn_projector_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(Geometry),
                                             ctypes.POINTER(ProjectorConfig), c_i32, c_f64, c_i32]),
     "cbn_projector_destroy": (ctypes.c_int, [c_vp]),

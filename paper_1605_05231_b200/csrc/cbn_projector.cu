@@ -1214,6 +1214,29 @@ int cbn_projector_radial_lattice(cbn_projector* p, const float* vol, void* latti
     }
 }
 
+// diagnostics: the forward plan's sorted polar-node records (GrPoint<5>, 56 B
+// each, sorted order) and the sorted node ids; sizes via *m
+int cbn_projector_grangeat_records(cbn_projector* p, void* records, int32_t* perm, int64_t* m,
+                                   void* stream) {
+    try {
+        CBN_REQUIRE(p && m, "null argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        GrangeatPlan& gp = p->fgr;
+        if (!gp.built) fit_grangeat(p, gp, p->fumb, s);
+        prepare_gr_points(p, gp, p->fumb, true, s);
+        const int64_t cap = *m;
+        *m = gp.m;
+        if (records && cap >= gp.m) {
+            CBN_CUDA(cudaMemcpy(records, gp.pts.p, sizeof(GrPoint<kGrJ>) * gp.m, cudaMemcpyDeviceToHost));
+            CBN_CUDA(cudaMemcpy(perm, gp.bins.perm.p, sizeof(int) * gp.m, cudaMemcpyDeviceToHost));
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int cbn_projector_radial_spectrum(cbn_projector* p, const float* vol, void* spectrum, void* stream) {
     try {
         CBN_REQUIRE(p && vol && spectrum, "null argument");
