@@ -36,3 +36,25 @@ for k in bad[:10]:
     print("node", i, "mu", i // cfg.n_t, "t", i % cfg.n_t, "dev", np.round(w_dev[k], 5),
           "ref", np.round(w_ref[k], 5))
 print("col ok:", np.array_equal(rec["col"] // cfg.n_t, perm // cfg.n_t))
+# bin origins implied by the records, and a host emulation of the binned spread
+K = 2 * n
+fu = np.mod(gp.plan.first[0], K).astype(int)[perm]
+fv = np.mod(gp.plan.first[1], K).astype(int)[perm]
+ou, ov = fu - rec["lu"], fv - rec["lv"]
+print("lu/lv in [0,8):", bool(((rec["lu"] >= 0) & (rec["lu"] < 8) & (rec["lv"] >= 0) & (rec["lv"] < 8)).all()),
+      "origins multiple of 8:", bool(((ou % 8) == 0).all() and ((ov % 8) == 0).all()))
+rng = np.random.default_rng(3)
+y = rng.standard_normal(m.value) + 1j * rng.standard_normal(m.value)   # per sorted record
+grid = np.zeros((K, K), complex)
+for k in range(m.value):
+    for a in range(5):
+        for b in range(5):
+            grid[(ou[k] + rec["lu"][k] + a) % K, (ov[k] + rec["lv"][k] + b) % K] += rec["w"][k][a] * rec["w"][k][5 + b] * y[k]
+ref = np.zeros((K, K), complex)
+for k in range(m.value):
+    i = perm[k]
+    for a in range(5):
+        for b in range(5):
+            ref[(gp.plan.first[0][i] + a) % K, (gp.plan.first[1][i] + b) % K] += gp.plan.weights[0][i][a] * gp.plan.weights[1][i][b] * y[k]
+ref /= orc.kb_kernel(0.0, 5, gp.plan.betas[0]) ** 2
+print("host emulation vs oracle spread:", np.linalg.norm(grid - ref) / np.linalg.norm(ref))
