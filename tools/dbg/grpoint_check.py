@@ -55,6 +55,6 @@ for k in range(m.value):
     i = perm[k]
     for a in range(5):
         for b in range(5):
-            ref[(gp.plan.first[0][i] + a) % K, (gp.plan.first[1][i] + b) % K] += gp.plan.weights[0][i][a] * gp.plan.weights[1][i][b] * y[k]
+            ref[int(gp.plan.first[0][i] + a) % K, int(gp.plan.first[1][i] + b) % K] += gp.plan.weights[0][i][a] * gp.plan.weights[1][i][b] * y[k]
 ref /= orc.kb_kernel(0.0, 5, gp.plan.betas[0]) ** 2
 print("host emulation vs oracle spread:", np.linalg.norm(grid - ref) / np.linalg.norm(ref))
