@@ -941,7 +941,24 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_FORWARD, s);
     CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
     if (p->timer.on) p->timer.end(s);
-    {
+    const char* old_spread = std::getenv("CBN_GR_ATOMIC");
+    if (old_spread && old_spread[0] == '1') {
+        // diagnostics: the plain global-atomic spread
+        GrRevParams rp;
+        rp.n_mu = u.n_mu;
+        rp.n_t = u.n_t;
+        rp.nu = p->g.nu;
+        rp.nv = p->g.nv;
+        rp.Ku = Ku;
+        rp.Kv = Kv;
+        rp.pc0 = (double)p->g.nu / 2.0 - 0.5 - (double)(p->g.nu / 2);
+        rp.pc1 = (double)p->g.nv / 2.0 - 0.5 - (double)(p->g.nv / 2);
+        rp.q = gp.fac_im.p;
+        PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+        k_gr_spread<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, p->gr_t.p,
+                                                            rp, nb);
+        CBN_LAUNCH_CHECK();
+    } else {
         StageScope st(p->timer, "grangeat_spread", s);
         const BinPlan& bb = gp.bins;
         const size_t smem = sizeof(float2) * kGrWarps * 32 * bb.nreg;
