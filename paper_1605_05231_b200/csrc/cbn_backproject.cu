@@ -71,56 +71,6 @@ __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int 
     grids[e] = out;
 }
 
-struct GrFwdParams {
-    int n_mu, n_t, Ku, Kv;
-    double pc0, pc1;     // plan phase * centre phase: exp(+i w.pc)
-    float pupv;
-};
-
-template <int J>
-__global__ void __launch_bounds__(256)
-k_grf_gather(const float2* __restrict__ grids, KBSet kb, PolarSrc src, GrFwdParams p,
-             const double* __restrict__ omega, int nb, float2* __restrict__ out) {
-    const int64_t m = (int64_t)p.n_mu * p.n_t;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    double w[2];
-    PolarSrc::Aux aux;
-    src.node(i, w, aux);
-    double sn, cs;
-    sincos(w[0] * p.pc0 + w[1] * p.pc1, &sn, &cs);
-    const float om = (float)omega[aux.jt] * p.pupv;
-    // phase * pu pv * (i omega)
-    const float2 fac = make_float2(-(float)sn * om, (float)cs * om);
-    int first[2];
-    float wt[2][J];
-    tap_setup<2, J>(kb, w, first, wt);
-    int c1[J];
-#pragma unroll
-    for (int b = 0; b < J; ++b) c1[b] = wrapc(first[1] + b, p.Kv);
-    const int im = (int)(i / p.n_t);
-    const int col = (aux.jt - p.n_t / 2 + p.n_t) % p.n_t;   // ifftshift for the t IFFT
-    const size_t gsz = (size_t)p.Ku * p.Kv;
-    for (int v = 0; v < nb; ++v) {
-        const float2* grid = grids + v * gsz;
-        float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int a = 0; a < J; ++a) {
-            const float2* row = grid + (size_t)wrapc(first[0] + a, p.Ku) * p.Kv;
-            float2 r = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int b = 0; b < J; ++b) {
-                float2 g = __ldg(row + c1[b]);
-                r.x = fmaf(wt[1][b], g.x, r.x);
-                r.y = fmaf(wt[1][b], g.y, r.y);
-            }
-            acc.x = fmaf(wt[0][a], r.x, acc.x);
-            acc.y = fmaf(wt[0][a], r.y, acc.y);
-        }
-        out[((size_t)v * p.n_mu + im) * p.n_t + col] = cmul(acc, fac);
-    }
-}
-
 // values = Re(fftshift(ifft)) / dt * w2   (grangeat.py:144-145)
 __global__ void k_grf_post(const float2* __restrict__ t, const float* __restrict__ w2, int n_t,
                            double inv, int64_t total, float* __restrict__ vals) {
@@ -237,7 +187,7 @@ struct BpSrc : RadialSrc {
     const float2* X;
     const float* q;        // per rho bin: omega * apod * c3 * d_rho
     const float* sin_th;
-    double pc[3];
+    int N[3];              // output dims (centre / plan phases per node representative)
     int tri;
     CBN_D float2 value(int64_t i, const double (&w)[3], const RadialSrc::Aux& a) const {
         const int64_t line = i / n_rho;
@@ -255,7 +205,7 @@ struct BpSrc : RadialSrc {
             v = cscale(v, t);
         }
         double sn, cs;
-        sincos(-(w[0] * pc[0] + w[1] * pc[1] + w[2] * pc[2]), &sn, &cs);
+        sincos(-centre_plan_angle<3>(a.wc, w, N), &sn, &cs);   // conj(centre) * conj(plan)
         return cmul(v, make_float2((float)cs, (float)sn));
     }
 };
@@ -456,7 +406,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     bsrc.X = p->lattice.p;
     bsrc.q = p->ramp_q.p;
     bsrc.sin_th = r.sin_theta.p;
-    for (int d = 0; d < 3; ++d) bsrc.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
+    for (int d = 0; d < 3; ++d) bsrc.N[d] = n;
     bsrc.tri = c.basis == 0;
     {
         StageScope st_sp(p->timer, "bp_spread", s);

@@ -26,7 +26,7 @@ struct GrPoint {
 struct GrFactor {
     int n_t;
     int reverse;               // 1: conj phases * (i q_t); 0: phases * pu pv * (i omega_t)
-    double pc0, pc1;           // N/2 - 1/2 - N//2 per axis
+    int N[2];                  // detector dims (centre / plan phases, grangeat.py:119,140)
     const float* q;            // reverse: -sign(omega) taper dt c2 per t
     const double* omega;       // forward: omega_t
     float pupv;
@@ -54,11 +54,11 @@ __global__ void k_gr_points(KBSet kb, TileGeom<2> tg, PolarSrc src, GrFactor f,
         g.col = im * f.n_t + (aux.jt - f.n_t / 2 + f.n_t) % f.n_t;
         double sn, cs;
         if (f.reverse) {
-            sincos(-(w[0] * f.pc0 + w[1] * f.pc1), &sn, &cs);
+            sincos(-centre_plan_angle<2>(aux.wc, w, f.N), &sn, &cs);
             const float q = f.q[aux.jt];
             g.fac = make_float2(-(float)sn * q, (float)cs * q);
         } else {
-            sincos(w[0] * f.pc0 + w[1] * f.pc1, &sn, &cs);
+            sincos(centre_plan_angle<2>(aux.wc, w, f.N), &sn, &cs);
             const float om = (float)f.omega[aux.jt] * f.pupv;
             g.fac = make_float2(-(float)sn * om, (float)cs * om);
         }

@@ -89,12 +89,12 @@ void UmbrellaTables::build(const cbn_geometry& g, int nmu, int nt, double pitch,
 struct SpecOut {
     float2* out;
     const float* om_phys;
-    double pc[3];          // N/2 - 1/2 - N//2 per axis (centre phase * plan phase)
+    int N[3];              // volume dims (centre phase * plan phase, per node representative)
     int n_rho;
     int tri;
     int spectrum_only;     // 1: image_to_radial_spectrum values in node order
     CBN_D void put(int64_t i, float2 v, const double (&w)[3], const RadialSrc::Aux& a) const {
-        double ang = w[0] * pc[0] + w[1] * pc[1] + w[2] * pc[2];
+        double ang = centre_plan_angle<3>(a.wc, w, N);
         double sn, cs;
         sincos(ang, &sn, &cs);
         float2 r = cmul(v, make_float2((float)cs, (float)sn));
@@ -313,7 +313,6 @@ __global__ void k_pad_lattice(const float2* __restrict__ src, int shift, float s
 struct GrRevParams {
     int n_mu, n_t;
     int nu, nv, Ku, Kv;
-    double pc0, pc1;       // conj(centre phase) * conj(plan phase): exp(-i w.pc)
     const float* q;        // per t: -sign(omega) taper dt c2  (y = S * i q)
 };
 
@@ -339,7 +338,8 @@ k_gr_spread(float2* __restrict__ grids, KBSet kb, PolarSrc src, const float2* __
     const float q = p.q[aux.jt];
     if (q == 0.f) return;
     double sn, cs;
-    sincos(-(w[0] * p.pc0 + w[1] * p.pc1), &sn, &cs);
+    const int N[2] = {p.nu, p.nv};
+    sincos(-centre_plan_angle<2>(aux.wc, w, N), &sn, &cs);   // conj(centre) * conj(plan)
     // factor = phase * (i q)
     const float2 fac = make_float2(-(float)sn * q, (float)cs * q);
     int first[2];
@@ -697,7 +697,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     SpecOut epi;
     epi.out = spectrum ? spectrum : p->lattice.p;
     epi.om_phys = r.om_phys.p;
-    for (int d = 0; d < 3; ++d) epi.pc[d] = (double)n / 2.0 - 0.5 - (double)(n / 2);
+    for (int d = 0; d < 3; ++d) epi.N[d] = n;
     epi.n_rho = r.n_rho;
     epi.tri = p->c.basis == 0;
     epi.spectrum_only = spectrum != nullptr;
@@ -898,8 +898,8 @@ void prepare_gr_points(P* p, GrangeatPlan& gp, const UmbrellaTables& u, bool rev
     GrFactor f;
     f.n_t = u.n_t;
     f.reverse = reverse ? 1 : 0;
-    f.pc0 = (double)p->g.nu / 2.0 - 0.5 - (double)(p->g.nu / 2);
-    f.pc1 = (double)p->g.nv / 2.0 - 0.5 - (double)(p->g.nv / 2);
+    f.N[0] = p->g.nu;
+    f.N[1] = p->g.nv;
     f.q = gp.fac_im.p;
     f.omega = u.omega_t.p;
     f.pupv = (float)(gp.pu * gp.pv);
@@ -951,8 +951,6 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         rp.nv = p->g.nv;
         rp.Ku = Ku;
         rp.Kv = Kv;
-        rp.pc0 = (double)p->g.nu / 2.0 - 0.5 - (double)(p->g.nu / 2);
-        rp.pc1 = (double)p->g.nv / 2.0 - 0.5 - (double)(p->g.nv / 2);
         rp.q = gp.fac_im.p;
         PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
         k_gr_spread<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, p->gr_t.p,

@@ -28,6 +28,7 @@ struct RadialSrc {
     int n_rho, n_theta;
     struct Aux {
         double raw[3];    // unwrapped node (for the trilinear transfer)
+        double wc[3];     // wrapped once: the centre phase's node (radon_fourier.py:102,106)
         int ir, it;
     };
     CBN_D void node(int64_t i, double (&w)[3], Aux& a) const {
@@ -43,9 +44,28 @@ struct RadialSrc {
         a.ir = ir;
         a.it = it;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) w[d] = wrap_pi(wrap_pi(a.raw[d]));
+        for (int d = 0; d < 3; ++d) {
+            a.wc[d] = wrap_pi(a.raw[d]);
+            w[d] = wrap_pi(a.wc[d]);      // plan_nufft wraps again (nufft.py:150)
+        }
     }
 };
+
+// Centre phase x plan phase of the reference, each on its own node
+// representative: the centre phase uses the once-wrapped node, the plan phase
+// the twice-wrapped one; a node at +pi can wrap to -pi the second time, and
+// for even N the two representatives give opposite signs, so the product is
+// not a function of one node value.  Returns the angle of
+//   exp(+i wc.(N/2 - 1/2)) * exp(-i wp.(N//2))   (centre * plan phase);
+// the adjoint uses its negative.
+template <int D>
+CBN_D double centre_plan_angle(const double (&wc)[D], const double (&wp)[D], const int (&N)[D]) {
+    double a = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        a += wc[d] * ((double)N[d] / 2.0 - 0.5) - wp[d] * (double)(N[d] / 2);
+    return a;
+}
 
 struct UmbrellaGeom {
     const double* cos_a;   // per view: cos / sin of the source angle
@@ -180,13 +200,16 @@ struct PolarSrc {
     int n_t;
     struct Aux {
         int jt;
+        double wc[2];     // wrapped once: the centre phase's node (grangeat.py:117-119)
     };
     CBN_D void node(int64_t i, double (&w)[2], Aux& a) const {
         const int im = (int)(i / n_t);
         a.jt = (int)(i % n_t);
         const double o = omega[a.jt];
-        w[0] = wrap_pi(wrap_pi(dmul(dmul(o, cos_mu[im]), pu)));
-        w[1] = wrap_pi(wrap_pi(dmul(dmul(o, sin_mu[im]), pv)));
+        a.wc[0] = wrap_pi(dmul(dmul(o, cos_mu[im]), pu));
+        a.wc[1] = wrap_pi(dmul(dmul(o, sin_mu[im]), pv));
+        w[0] = wrap_pi(a.wc[0]);
+        w[1] = wrap_pi(a.wc[1]);
     }
 };
 
