@@ -320,6 +320,214 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------- config 4: NUFFT stress microbench
+C4_POINTS = 100_000_000
+C4_GRID = 256
+C4_J = 8
+
+
+def run_nufft4(args):
+    """BASELINE config 4: type-2 gather + type-1 spread of 100M float32 points
+    (i.i.d. uniform in [-pi, pi)^3) against a 256^3 CN(0,1) grid, KB J=8,
+    sigma 2.  One step = one type-2 and one type-1 over every point; the
+    metric counts points per second through that pair.  Under torchrun the
+    points are split evenly across ranks; type-2 needs no exchange (x is
+    replicated), type-1's 256^3 outputs are summed and scattered by z-slab
+    with one NCCL reduce-scatter (linear, so reducing after the crop moves
+    1/8 of the oversampled grid's bytes)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1605_05231_b200 import _lib, nufft
+    from paper_1605_05231_b200.workloads import config4_inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    m_total = int(os.environ.get("CBN_C4_POINTS", C4_POINTS))
+    x_host, pts = config4_inputs(n_points=m_total, grid=C4_GRID)
+    lo = m_total * rank // world
+    hi = m_total * (rank + 1) // world
+    pts = np.ascontiguousarray(pts[lo:hi])
+    m = hi - lo
+    lib = _lib.load()
+    torch.cuda.synchronize()
+    tp = time.perf_counter()
+    plan = nufft.plan_nufft((C4_GRID,) * 3, pts, 2.0, C4_J)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - tp
+    stream = torch.cuda.current_stream()
+    import ctypes
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    x = torch.from_numpy(x_host).cuda()
+    y = torch.empty(m, dtype=torch.complex64, device="cuda")
+    xa = torch.empty((C4_GRID,) * 3, dtype=torch.complex64, device="cuda")
+    slab = torch.empty((C4_GRID // world, C4_GRID, C4_GRID), dtype=torch.complex64, device="cuda") \
+        if world > 1 else None
+
+    def type2():
+        _lib.check(lib.cbn_nufft_type2(plan.handle, ctypes.c_void_p(x.data_ptr()),
+                                       ctypes.c_void_p(y.data_ptr()), sp))
+
+    def type1():
+        _lib.check(lib.cbn_nufft_type1(plan.handle, ctypes.c_void_p(y.data_ptr()),
+                                       ctypes.c_void_p(xa.data_ptr()), sp))
+        if world > 1:
+            dist.reduce_scatter_tensor(slab, xa)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        type2()
+        type1()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = lib.cbn_launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
+    torch.cuda.synchronize()
+    barrier()
+    ev[0].record(stream)
+    for k in range(args.steps):
+        type2()
+        ev[2 * k + 1].record(stream)
+        type1()
+        ev[2 * k + 2].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = lib.cbn_launch_count() - n0
+    clk = clocks.stop()
+    t2 = sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps)) / args.steps
+    t1 = sum(ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(args.steps)) / args.steps
+    ms = ev[0].elapsed_time(ev[-1])
+    tt = torch.tensor([ms, t2, t1], device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_max, t2, t1 = (float(v) for v in tt.tolist())
+    value = m_total * args.steps / (ms_max / 1e3) / 1e6
+
+    e2e = None
+    if not args.no_e2e:
+        # public API with pinned host buffers: x and the node values in, results out
+        hx = torch.from_numpy(x_host).pin_memory()
+        hy = torch.from_numpy(np.zeros(m, np.complex64)).pin_memory()
+        hxa = torch.empty((C4_GRID,) * 3, dtype=torch.complex64).pin_memory()
+
+        def e2e_step():
+            xd = nufft.nufft_forward(plan, hx.to("cuda", non_blocking=True))
+            hy.copy_(xd, non_blocking=True)
+            yd = hy.to("cuda", non_blocking=True)
+            hxa.copy_(nufft.nufft_adjoint(plan, yd), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        et = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        e2e = {"value": round(m_total * args.steps / (e_ms / 1e3) / 1e6, 3), "unit": "Msamples/s",
+               "h2d_bytes_per_step": int(hx.numel() * 8 + hy.numel() * 8),
+               "d2h_bytes_per_step": int(hy.numel() * 8 + hxa.numel() * 8),
+               "api": "nufft_forward / nufft_adjoint on pinned host-staged tensors"}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = hbm_peak()
+    K3 = (2 * C4_GRID) ** 3
+    # compulsory bytes: gather reads the oversampled grid once + 12 B nodes +
+    # 8 B output per point; spread reads 12 B nodes + 8 B values and writes
+    # the grid once (DESIGN.md section 4)
+    gb = {"type2_step": 8.0 * K3 + 20.0 * m, "type1_step": 8.0 * K3 + 20.0 * m}
+    taps = C4_J ** 3
+    kernels = {
+        "type2": {"ms_per_step": round(t2, 3), "achieved_gbs": round(gb["type2_step"] / t2 / 1e6, 1),
+                  "onchip_tap_bytes": 8.0 * taps * m,
+                  "onchip_tbs": round(8.0 * taps * m / t2 / 1e9, 2),
+                  "msamples_s": round(m / t2 / 1e3, 2)},
+        "type1": {"ms_per_step": round(t1, 3), "achieved_gbs": round(gb["type1_step"] / t1 / 1e6, 1),
+                  "onchip_tap_bytes": 8.0 * taps * m,
+                  "onchip_tbs": round(8.0 * taps * m / t1 / 1e9, 2),
+                  "msamples_s": round(m / t1 / 1e3, 2)},
+    }
+    st = "type1" if t1 >= t2 else "type2"
+    roofline = {"kernel": st + " (whole transform incl. FFT)", "bound": "hbm",
+                "achieved": kernels[st]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": round(kernels[st]["achieved_gbs"] / peak, 4), "traffic": None,
+                "peak_kind": peak_kind, "onchip_tbs": kernels[st]["onchip_tbs"]}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample_nufft4()
+    out = {
+        "metric": "NUFFT nonuniform Msamples/s (fwd+adj)",
+        "value": round(value, 3), "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c64/f32 (fp64 index math)",
+        "data": "synthetic: 256^3 CN(0,1) grid (seed 4), float32 points U[-pi,pi)^3 (seed 5)",
+        "config": {"workload": f"config4: {m_total} points, {C4_GRID}^3 grid, KB J={C4_J}, sigma 2, "
+                               "one type-2 + one type-1 per step",
+                   "points_per_rank": m, "parallelism": f"points sharded x{world}",
+                   "plan_s": round(plan_s, 3),
+                   "l2": "working set > L2 (1.07 GB oversampled grid, 1.2 GB nodes)"},
+        "e2e": e2e, "gpu_launches": int(launches),
+        "gpu_launches_per_step": int(launches) // max(args.steps, 1),
+        "clocks": clk, "roofline": roofline, "kernels": kernels,
+        "stages_ms_per_step": {"type2": round(t2, 3), "type1": round(t1, 3)},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_sample_nufft4(n_sample: int = 1 << 17):
+    """Oracle port on a 2^17-point sample of config 4 (plan excluded, like the
+    GPU value): per-point type-2 + type-1 cost, plus one 512^3 FFT per
+    transform, extrapolated to 100M points."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import cbn_oracle as orc
+    from paper_1605_05231_b200.workloads import config4_inputs
+    cores = os.cpu_count() or 1
+    orc.WORKERS = cores
+    x, pts = config4_inputs(n_points=n_sample, grid=C4_GRID)
+    x = x.astype(np.complex128)
+    plan = orc.make_plan((C4_GRID,) * 3, pts.astype(np.float64), 2.0, C4_J)
+    y = np.ones(n_sample, np.complex128)
+    t = time.perf_counter()
+    orc.type2(plan, x)
+    t2 = time.perf_counter() - t
+    t = time.perf_counter()
+    orc.type1(plan, y)
+    t1 = time.perf_counter() - t
+    # separate the FFT (fixed per transform) from the per-point part
+    g = np.zeros((2 * C4_GRID,) * 3, np.complex128)
+    t = time.perf_counter()
+    orc.sfft.fftn(g, overwrite_x=True, workers=orc.WORKERS)
+    tf = time.perf_counter() - t
+    per_point = max(t2 + t1 - 2 * tf, 1e-12) / n_sample
+    total = per_point * C4_POINTS + 2 * tf
+    return {"value": round(C4_POINTS / total / 1e6, 6), "unit": "Msamples/s", "cores": cores,
+            "kind": "port",
+            "sample": f"oracle port: type-2 {t2:.2f}s + type-1 {t1:.2f}s on {n_sample} points "
+                      f"(512^3 FFT {tf:.2f}s each), per-point part extrapolated to {C4_POINTS}",
+            "extrapolated": True}
+
+
 # --------------------------------------------------------- CPU (oracle) leg
 def cpu_sample(w, direction: int, n_samples: int = 1):
     """Time the oracle port on a bounded sample and extrapolate to the full
@@ -414,9 +622,36 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def run_reference_nufft4(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    t0 = time.perf_counter()
+    vals = [cpu_sample_nufft4() for _ in range(max(args.warmup, 0) + args.steps)]
+    timed = vals[max(args.warmup, 0):]
+    value = float(np.mean([v["value"] for v in timed]))
+    cpu = dict(timed[-1])
+    cpu["value"] = round(value, 6)
+    print(json.dumps({
+        "impl": "reference", "metric": "NUFFT nonuniform Msamples/s (fwd+adj)",
+        "value": round(value, 6), "unit": "Msamples/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * C4_POINTS / (value * 1e6), 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/c128",
+        "data": "synthetic: config 4 inputs",
+        "config": {"workload": "config4 (CPU oracle port, extrapolated)"}, "cpu_baseline": cpu,
+        "e2e": {"value": round(value, 6), "unit": "Msamples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(time.perf_counter() - t0, 1)}), flush=True)
+
+
 def main():
     args = parse_args()
-    if args.impl == "reference":
+    if args.config == 4:
+        if args.impl == "reference":
+            run_reference_nufft4(args)
+        else:
+            run_nufft4(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -57,6 +57,13 @@ typedef struct cbn_nufft_s cbn_nufft;
 int cbn_nufft_create(cbn_nufft** plan, int ndim, const int64_t* dims, const int32_t* taps,
                      double oversample_factor, const double* nodes, int64_t m,
                      const int64_t* ls_rows, int64_t n_ls, void* stream);
+/* Same plan over float32 nodes (m x ndim, [host]), kept in float32 on the
+ * device and wrapped to [-pi, pi) in float64 inside the kernels -- the
+ * large-m path (100M nodes, 256^3, J=8).  Matches
+ * plan_nufft(dims, nodes.astype(float64), ...) exactly. */
+int cbn_nufft_create_f32(cbn_nufft** plan, int ndim, const int64_t* dims, const int32_t* taps,
+                         double oversample_factor, const float* nodes, int64_t m,
+                         const int64_t* ls_rows, int64_t n_ls, void* stream);
 int cbn_nufft_destroy(cbn_nufft* plan);
 /* per-axis float64 LS scaling vectors, concatenated (sum(dims) values) [host] */
 int cbn_nufft_scaling(const cbn_nufft* plan, double* out);

@@ -53,6 +53,8 @@ _SIGS = {
     "cbn_beatty_beta": (c_f64, [ctypes.c_int, c_f64]),
     "cbn_nufft_create": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int, P_i64, P_i32, c_f64,
                                         P_f64, c_i64, P_i64, c_i64, c_vp]),
+    "cbn_nufft_create_f32": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int, P_i64, P_i32, c_f64,
+                                            c_vp, c_i64, P_i64, c_i64, c_vp]),
     "cbn_nufft_destroy": (ctypes.c_int, [c_vp]),
     "cbn_nufft_scaling": (ctypes.c_int, [c_vp, P_f64]),
     "cbn_nufft_wrapped_nodes": (ctypes.c_int, [c_vp, P_f64]),

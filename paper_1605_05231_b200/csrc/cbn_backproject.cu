@@ -383,7 +383,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->bspec_s32.p, n, s);
         const int tile[3] = {kTile3, kTile3, kTile3};
         dispatch_j(sax[0].J, [&](auto jc) {
-            build_bins<3, decltype(jc)::value>(p->bspec_bins, r.src(), kbs, M, tile, kMaxSub, s);
+            build_bins<3, decltype(jc)::value>(p->bspec_bins, r.src(), kbs, M, tile, kMaxSub, s, true);
             return 0;
         });
         p->bspec_fit = true;
@@ -413,16 +413,9 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
         const BinPlan& bb = p->bspec_bins;
         dispatch_j(sax[0].J, [&](auto jc) {
-            constexpr int J = decltype(jc)::value;
-            constexpr int W = 4;
-            const size_t smem = spread_smem_bytes<3, J, W>(bb.nreg);
-            CBN_CUDA(cudaFuncSetAttribute(k_spread_binned<3, J, W, BpSrc>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_spread_binned<3, J, W><<<bb.nsubs, W * 32, smem, s>>>(p->big.p, kbs, bb.geom<3>(), bsrc,
-                                                                   bb.perm.p, bb.subs.p);
+            launch_spread3<decltype(jc)::value>(p->big.p, kbs, bb, bsrc, s);
             return 0;
         });
-        CBN_LAUNCH_CHECK();
     }
     long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
     StageScope st_ff(p->timer, "bp_ifft_crop", s);

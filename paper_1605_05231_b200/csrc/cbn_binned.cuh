@@ -7,11 +7,20 @@
 // staged in shared memory:
 //  * gather: the region is loaded once (wrapped, coalesced along the fastest
 //    axis), then one thread per point reads its J^D taps from shared memory;
-//  * spread: each warp owns a private copy of the region and processes one
-//    point at a time with its lanes covering the J^D taps, so shared-memory
-//    updates are plain load/add/store (sm_100a has no native shared fp32
-//    atomic add -- it lowers to a CAS loop); the copies are summed and
-//    flushed with one global RED per non-zero cell.
+//  * spread (2D): each warp owns a private copy of the region and processes
+//    one point at a time with its lanes covering the J^D taps, so
+//    shared-memory updates are plain load/add/store (sm_100a has no native
+//    shared fp32 atomic add -- it lowers to a CAS loop); the copies are
+//    summed and flushed with one global RED per non-zero cell;
+//  * spread (3D): one region copy per CTA, cells owned by warp: warp w
+//    updates only the region rows (axis 0) congruent to w mod W, so every
+//    warp walks every point of the subproblem but touches only its rows --
+//    no atomics, no private copies, and W x 32 threads share one region.
+// The 3D region's fastest axis is stored with a pitch P = J (mod 16) so that
+// 16 lanes covering consecutive (b, c) tap pairs hit 16 distinct bank pairs.
+// Within a subproblem the points are interleaved by the bank residue of
+// their region offset (k_bin_interleave), so the 16 lanes of a half-warp in
+// the thread-per-point gather read 16 distinct bank pairs at every tap.
 #pragma once
 
 #include "cbn_kernels.cuh"
@@ -31,6 +40,7 @@ struct TileGeom {
     int R[3];        // region edge per axis (T + J - 1)
     int nb[3];       // bins per axis
     int K[3];        // grid extent per axis
+    int P;           // shared-memory pitch of the last axis (>= R[D-1])
 };
 
 template <int D>
@@ -79,10 +89,12 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<D>(tg, sp.bin, o);
-    const int R0 = tg.R[0], R1 = tg.R[1], R2 = D == 3 ? tg.R[2] : 1;
-    const int nreg = R0 * R1 * R2;
+    const int R0 = tg.R[0], R1 = D == 3 ? tg.R[1] : tg.P, R2 = D == 3 ? tg.R[2] : 1;
+    const int P2 = D == 3 ? tg.P : 1;
+    const int nreg = R0 * R1 * P2;
     for (int e = threadIdx.x; e < nreg; e += blockDim.x) {
-        const int r2 = e % R2, r01 = e / R2, r1 = r01 % R1, r0 = r01 / R1;
+        const int r2 = e % P2, r01 = e / P2, r1 = r01 % R1, r0 = r01 / R1;
+        if (r2 >= R2 || (D == 2 && r1 >= tg.R[1])) continue;
         size_t g;
         if constexpr (D == 3)
             g = ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1])) * tg.K[2] +
@@ -115,7 +127,7 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
                 float2 pa = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int b = 0; b < J; ++b) {
-                    const float2* row = tile + ((l[0] + a) * R1 + l[1] + b) * R2 + l[2];
+                    const float2* row = tile + ((l[0] + a) * R1 + l[1] + b) * P2 + l[2];
                     float2 r = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int c = 0; c < J; ++c) {
@@ -160,6 +172,7 @@ template <int D, int J, int WARPS, class Src>
 __global__ void __launch_bounds__(WARPS * 32)
 k_spread_binned(float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src,
                 const int* __restrict__ perm, const SubProblem* __restrict__ subs) {
+    static_assert(D == 2, "3D spreads use k_spread_owned");
     extern __shared__ float2 smem[];
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
@@ -255,6 +268,179 @@ constexpr size_t spread_smem_bytes(int nreg) {
     return (size_t)WARPS * nreg * sizeof(float2) + (size_t)WARPS * 32 * D * J * sizeof(float);
 }
 
+
+// ------------------------------------------------------ owner-computes spread
+// 3D spread with one shared region per CTA.  Round structure: every thread
+// stages one point (local first taps, D x J weights, value), then each warp
+// walks all staged points and applies the taps of the region rows it owns
+// (row = l0 + a, owned by warp (l0 + a) mod W).  Lanes cover consecutive
+// (b, c) tap pairs of a row.  Cells of distinct warps are disjoint and a warp
+// applies one point at a time, so the read-add-write needs no atomics.
+template <int J>
+constexpr int owned_stage_stride() {
+    return (3 * J) | 1;   // odd: conflict-free staging writes
+}
+
+template <int J, int W>
+constexpr size_t spread_owned_smem_bytes(int nreg) {
+    return (size_t)nreg * sizeof(float2) + (size_t)W * 32 * owned_stage_stride<J>() * sizeof(float) +
+           (size_t)W * 32 * (sizeof(float2) + sizeof(int)) + 8;
+}
+
+template <int J, int W, class Src>
+__global__ void __launch_bounds__(W * 32)
+k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
+               const int* __restrict__ perm, const SubProblem* __restrict__ subs) {
+    constexpr int NP = W * 32;
+    constexpr int SW = owned_stage_stride<J>();
+    constexpr int ROWS = (J + W - 1) / W;           // max rows per warp per point
+    constexpr int JJ = J * J;
+    constexpr int ITERS = (ROWS * JJ + 31) / 32;
+    extern __shared__ float4 smem4[];
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<3>(tg, sp.bin, o);
+    const int R0 = tg.R[0], R1 = tg.R[1], R2 = tg.R[2], P = tg.P;
+    const int nreg = R0 * R1 * P;
+    float2* reg = reinterpret_cast<float2*>(smem4);
+    float* stw = reinterpret_cast<float*>(reg + nreg);
+    float2* stv = reinterpret_cast<float2*>(stw + ((NP * SW + 1) & ~1));
+    int* stl = reinterpret_cast<int*>(stv + NP);
+    for (int e = threadIdx.x; e < nreg; e += NP) reg[e] = make_float2(0.f, 0.f);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int base = 0; base < sp.count; base += NP) {
+        __syncthreads();   // region zeroed / previous round's points consumed
+        const int k = base + threadIdx.x;
+        if (k < sp.count) {
+            const int64_t i = perm[sp.start + k];
+            double w[3];
+            typename Src::Aux aux;
+            src.node(i, w, aux);
+            const float2 v = src.value(i, w, aux);
+            int first[3];
+            float wt[3][J];
+            tap_setup<3, J>(kb, w, first, wt);
+            const int l0 = wrapc(first[0], tg.K[0]) - o[0];
+            const int l1 = wrapc(first[1], tg.K[1]) - o[1];
+            const int l2 = wrapc(first[2], tg.K[2]) - o[2];
+            stl[threadIdx.x] = (l0 << 20) | (l1 << 10) | l2;
+            stv[threadIdx.x] = v;
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int p = 0; p < J; ++p) stw[threadIdx.x * SW + d * J + p] = wt[d][p];
+        }
+        __syncthreads();
+        const int npts = min(NP, sp.count - base);
+        for (int j = 0; j < npts; ++j) {
+            const float2 v = stv[j];
+            if (v.x == 0.f && v.y == 0.f) continue;     // uniform over the CTA
+            const int pl = stl[j];
+            const int l0 = pl >> 20, l1 = (pl >> 10) & 1023, l2 = pl & 1023;
+            const float* ws = stw + j * SW;
+            int a0 = (warp - l0) % W;
+            a0 += a0 < 0 ? W : 0;
+            const int nrows = a0 < J ? (J - 1 - a0) / W + 1 : 0;
+            float2* base_row = reg + ((l0 + a0) * R1 + l1) * P + l2;
+#pragma unroll
+            for (int it = 0; it < ITERS; ++it) {
+                const int t = it * 32 + lane;
+                const int r = t / JJ, pq = t % JJ;
+                if (r < nrows) {
+                    const int b = pq / J, c = pq % J;
+                    const float wk = ws[a0 + r * W] * ws[J + b] * ws[2 * J + c];
+                    float2* cell = base_row + (r * W * R1 + b) * P + c;
+                    float2 cur = *cell;
+                    cur.x = fmaf(wk, v.x, cur.x);
+                    cur.y = fmaf(wk, v.y, cur.y);
+                    *cell = cur;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nreg; e += NP) {
+        const int r2 = e % P, r01 = e / P, r1 = r01 % R1, r0 = r01 / R1;
+        if (r2 >= R2) continue;
+        const float2 s = reg[e];
+        if (s.x == 0.f && s.y == 0.f) continue;
+        const size_t g = ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1])) *
+                             tg.K[2] + wrapc(o[2] + r2, tg.K[2]);
+        atomicAdd(grid + g, s);
+    }
+}
+
+// ------------------------------------------- bank-residue interleaved order
+// Reorders each subproblem's points (plan time) so consecutive points have
+// distinct region-offset residues mod 16 for as long as the residue classes
+// last: stable rank q within the class, then order by (q, residue).
+constexpr int kInterleaveMax = 1024;
+
+template <int D, int J, class Src>
+__global__ void __launch_bounds__(256)
+k_bin_interleave(Src src, KBSet kb, TileGeom<D> tg, int* __restrict__ perm,
+                 const SubProblem* __restrict__ subs) {
+    __shared__ int ids[kInterleaveMax];
+    __shared__ short rank[kInterleaveMax];
+    __shared__ unsigned char res[kInterleaveMax];
+    __shared__ int wcnt[8][16];
+    __shared__ int cnt[16];
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<D>(tg, sp.bin, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < 16) cnt[threadIdx.x] = 0;
+    for (int c0 = 0; c0 < sp.count; c0 += 256) {
+        const int k = c0 + threadIdx.x;
+        int r = -1;
+        if (k < sp.count) {
+            const int64_t i = perm[sp.start + k];
+            double w[D];
+            typename Src::Aux aux;
+            src.node(i, w, aux);
+            int l[3] = {0, 0, 0};
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                int f;
+                axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, f);
+                l[d] = wrapc(f, kb.ax[d].K) - o[d];
+            }
+            const int off = D == 3 ? (l[0] * tg.R[1] + l[1]) * tg.P + l[2] : l[0] * tg.P + l[1];
+            r = off & 15;
+            ids[k] = (int)i;
+            res[k] = (unsigned char)r;
+        }
+        int q = 0;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) {
+            const unsigned m = __ballot_sync(0xffffffffu, r == rr);
+            if (r == rr) q = __popc(m & ((1u << lane) - 1u));
+            if (lane == 0) wcnt[warp][rr] = __popc(m);
+        }
+        __syncthreads();
+        if (r >= 0) {
+            q += cnt[r];
+            for (int w2 = 0; w2 < warp; ++w2) q += wcnt[w2][r];
+            rank[k] = (short)q;
+        }
+        __syncthreads();
+        if (threadIdx.x < 16) {
+            int add = 0;
+            for (int w2 = 0; w2 < 8; ++w2) add += wcnt[w2][threadIdx.x];
+            cnt[threadIdx.x] += add;
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < sp.count; k += 256) {
+        const int q = rank[k], r = res[k];
+        int pos = 0;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr) pos += min(cnt[rr], q) + (rr < r && cnt[rr] > q ? 1 : 0);
+        perm[sp.start + pos] = ids[k];
+    }
+}
+
 }  // namespace cbn
 
 #include "cbn_runtime.h"
@@ -280,6 +466,7 @@ struct BinPlan {
             g.nb[d] = tg.nb[d];
             g.K[d] = tg.K[d];
         }
+        g.P = tg.P;
         return g;
     }
 };
@@ -289,9 +476,12 @@ struct BinPlan {
 void finish_bins(BinPlan& bp, DevBuf<int>& keys, DevBuf<int>& counts, int64_t nbins, int max_sub,
                  cudaStream_t s);
 
+// pitch_pad: store the last region axis with pitch = J (mod 16) (required by
+// k_spread_owned; harmless for the gather)
 template <int D, int J, class Src>
 void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const int* tile,
-                int max_sub, cudaStream_t s) {
+                int max_sub, cudaStream_t s, bool pitch_pad = false) {
+    CBN_REQUIRE(max_sub <= kInterleaveMax, "subproblem size above the interleave limit");
     bp.D = D;
     bp.J = J;
     bp.m = m;
@@ -309,12 +499,39 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
             bp.tg.K[d] = bp.tg.T[d] = bp.tg.R[d] = bp.tg.nb[d] = 1;
         }
     }
+    bp.tg.P = bp.tg.R[D - 1];
+    if (D == 3 && pitch_pad) bp.tg.P += (((J - bp.tg.P) % 16) + 16) % 16;
+    bp.nreg = bp.nreg / bp.tg.R[D - 1] * bp.tg.P;
     DevBuf<int> keys((size_t)m), counts((size_t)nbins);
     CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * nbins, s));
     TileGeom<D> tg = bp.geom<D>();
     k_bin_keys<D, J, Src><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(src, kb, tg, m, keys.p, counts.p);
     CBN_LAUNCH_CHECK();
     finish_bins(bp, keys, counts, nbins, max_sub, s);
+    if (bp.nsubs > 0) {
+        k_bin_interleave<D, J, Src><<<bp.nsubs, 256, 0, s>>>(src, kb, bp.geom<D>(), bp.perm.p, bp.subs.p);
+        CBN_LAUNCH_CHECK();
+    }
+}
+
+// warps per CTA of the 3D owner-computes spread: rows per warp x J^2 taps
+// should fill whole 32-lane iterations (J=8: 1 row x 64; J=6: 2 rows x 36)
+template <int J>
+constexpr int owned_warps() {
+    return J == 6 ? 3 : (J < 8 ? J : 8);
+}
+
+template <int J, class Src>
+void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s) {
+    constexpr int W = owned_warps<J>();
+    CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
+    const size_t smem = spread_owned_smem_bytes<J, W>(bb.nreg);
+    CBN_CUDA(cudaFuncSetAttribute(k_spread_owned<J, W, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    if (bb.nsubs > 0)
+        k_spread_owned<J, W><<<bb.nsubs, W * 32, smem, s>>>(grid, kb, bb.geom<3>(), src, bb.perm.p,
+                                                            bb.subs.p);
+    CBN_LAUNCH_CHECK();
 }
 
 }  // namespace cbn

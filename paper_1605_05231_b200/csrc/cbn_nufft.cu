@@ -1,23 +1,32 @@
 // Generic NUFFT plan over explicit nodes: the device replacement of
 // plan_nufft / nufft_forward / nufft_adjoint (nufft.py:137-247).
 //
-// Plan state is O(m*d) wrapped float64 nodes plus per-axis scalings and remap
-// tables; interpolation weights are recomputed inside the gather/spread
-// kernels instead of being stored (the reference stores J^d per node).
+// Plan state is O(m*d) nodes (wrapped float64, or the caller's float32 values
+// wrapped on the fly in float64), per-axis scalings, remap tables and -- for
+// 2D/3D -- the bin-sorted node order with its subproblem list; interpolation
+// weights are recomputed inside the gather/spread kernels instead of being
+// stored (the reference stores J^d per node).
 #include <cstring>
 #include <vector>
 
+#include "cbn_binned.cuh"
 #include "cbn_plan.h"
 
 namespace cbn {
 
 template <int D>
 struct ExplicitSrc {
-    const double* nodes;  // wrapped, m x D
+    const double* nodes64;  // wrapped, m x D (or null)
+    const float* nodes32;   // caller's float32 values, m x D, wrapped here (or null)
     struct Aux {};
     CBN_D void node(int64_t i, double (&w)[D], Aux&) const {
+        if (nodes64) {
 #pragma unroll
-        for (int d = 0; d < D; ++d) w[d] = nodes[i * D + d];
+            for (int d = 0; d < D; ++d) w[d] = nodes64[i * D + d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < D; ++d) w[d] = wrap_pi((double)nodes32[i * D + d]);
+        }
     }
 };
 
@@ -56,16 +65,24 @@ __global__ void k_wrap_nodes(const double* __restrict__ in, double* __restrict__
 }
 
 template <int D>
-__global__ void k_first(const double* __restrict__ nodes, KBSet kb, int64_t m, int32_t* out) {
+__global__ void k_first(ExplicitSrc<D> src, KBSet kb, int64_t m, int32_t* out, double* wrapped) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
+    double w[D];
+    typename ExplicitSrc<D>::Aux aux;
+    src.node(i, w, aux);
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-        int f;
-        axis_coord(nodes[i * D + d], kb.ax[d].K, 0.5 * (double)kb.ax[d].J, f);
-        out[i * D + d] = wrapc(f, kb.ax[d].K);
+        if (wrapped) wrapped[i * D + d] = w[d];
+        if (out) {
+            int f;
+            axis_coord(w[d], kb.ax[d].K, 0.5 * (double)kb.ax[d].J, f);
+            out[i * D + d] = wrapc(f, kb.ax[d].K);
+        }
     }
 }
+
+constexpr int kSpreadWarps = 4;
 
 }  // namespace cbn
 
@@ -77,16 +94,22 @@ struct cbn_nufft_s {
     int64_t m = 0;
     AxisPlan ax[kMaxDim];
     KBSet kb{};
-    DevBuf<double> nodes;
+    DevBuf<double> nodes;      // wrapped float64 nodes, or
+    DevBuf<float> nodes32;     // float32 nodes (wrapped on the fly)
     DevBuf<float> s32;         // D x smax
     DevBuf<int> pad_idx, crop_idx;
     DevBuf<float> pad_sc, crop_sc;
     DevBuf<float2> grid;
+    BinPlan bins;              // 2D / 3D: bin-sorted order and subproblems
     std::vector<double> s64_host;
     int smax = 0;
     int64_t ktot = 1, ntot = 1;
     FFTCache fft;
     double centre[kMaxDim] = {0, 0, 0};
+    template <int D_>
+    ExplicitSrc<D_> src() const {
+        return ExplicitSrc<D_>{nodes.p, nodes.p ? nullptr : nodes32.p};
+    }
 };
 
 namespace {
@@ -114,10 +137,16 @@ void run_type2(cbn_nufft* p, const float2* x, float2* y, cudaStream_t s) {
     PhaseOut<D> epi;
     epi.y = y;
     for (int d = 0; d < D; ++d) epi.c[d] = p->centre[d];
-    ExplicitSrc<D> src{p->nodes.p};
+    ExplicitSrc<D> src = p->src<D>();
     dispatch_j(p->J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
-        k_gather<D, J><<<blocks_for(p->m, 256), 256, 0, s>>>(p->grid.p, p->kb, src, epi, p->m);
+        if constexpr (D >= 2) {
+            const BinPlan& bb = p->bins;
+            k_gather_binned<D, J><<<bb.nsubs, 256, sizeof(float2) * bb.nreg, s>>>(
+                p->grid.p, p->kb, bb.geom<D>(), src, epi, bb.perm.p, bb.subs.p);
+        } else {
+            k_gather<D, J><<<blocks_for(p->m, 256), 256, 0, s>>>(p->grid.p, p->kb, src, epi, p->m);
+        }
         return 0;
     });
     CBN_LAUNCH_CHECK();
@@ -127,12 +156,23 @@ template <int D>
 void run_type1(cbn_nufft* p, const float2* y, float2* x, cudaStream_t s) {
     CBN_CUDA(cudaMemsetAsync(p->grid.p, 0, p->grid.bytes(), s));
     PhaseIn<D> src;
-    src.nodes = p->nodes.p;
+    static_cast<ExplicitSrc<D>&>(src) = p->src<D>();
     src.yin = y;
     for (int d = 0; d < D; ++d) src.c[d] = p->centre[d];
     dispatch_j(p->J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
-        k_spread<D, J><<<blocks_for(p->m, 256), 256, 0, s>>>(p->grid.p, p->kb, src, p->m);
+        if constexpr (D == 3) {
+            launch_spread3<J>(p->grid.p, p->kb, p->bins, src, s);
+        } else if constexpr (D == 2) {
+            const BinPlan& bb = p->bins;
+            const size_t smem = spread_smem_bytes<D, J, kSpreadWarps>(bb.nreg);
+            CBN_CUDA(cudaFuncSetAttribute(k_spread_binned<D, J, kSpreadWarps, PhaseIn<D>>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_spread_binned<D, J, kSpreadWarps><<<bb.nsubs, kSpreadWarps * 32, smem, s>>>(
+                p->grid.p, p->kb, bb.geom<D>(), src, bb.perm.p, bb.subs.p);
+        } else {
+            k_spread<D, J><<<blocks_for(p->m, 256), 256, 0, s>>>(p->grid.p, p->kb, src, p->m);
+        }
         return 0;
     });
     CBN_LAUNCH_CHECK();
@@ -161,7 +201,7 @@ void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t
     DevBuf<int64_t> rows;
     rows.upload(rows_host, (size_t)n_ls, s);
     LSScratch sc;
-    ExplicitSrc<D> src{p->nodes.p};
+    ExplicitSrc<D> src = p->src<D>();
     ls_fit<D>(src, rows.p, (int)n_ls, p->ax, sc, p->s32.p, p->smax, s);
     p->s64_host.assign((size_t)D * p->smax, 0.0);
     CBN_CUDA(cudaMemcpyAsync(p->s64_host.data(), sc.s64.p, sizeof(double) * D * p->smax,
@@ -174,6 +214,15 @@ void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t
                     p->crop_idx.p + noff, p->crop_sc.p + noff, s);
         koff += p->ax[d].K;
         noff += p->ax[d].N;
+    }
+    if constexpr (D >= 2) {
+        // bin-sorted order for the shared-memory gather/spread (one-time plan step)
+        const int edge = D == 3 ? 8 : 16;
+        const int tile[3] = {edge, edge, edge};
+        dispatch_j(p->J, [&](auto jc) {
+            build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true);
+            return 0;
+        });
     }
     CBN_CUDA(cudaStreamSynchronize(s));   // rows / host scaling copy must outlive the launch
 }
@@ -188,11 +237,66 @@ auto dispatch_d(int D, F&& f) {
     }
 }
 
+int create_plan(cbn_nufft** out, int ndim, const int64_t* dims, const int32_t* taps,
+                double oversample_factor, const double* nodes64, const float* nodes32, int64_t m,
+                const int64_t* ls_rows, int64_t n_ls, void* stream) {
+    CBN_REQUIRE(out && dims && taps, "null argument");
+    CBN_REQUIRE(ndim >= 1 && ndim <= 3, "ndim must be 1..3");
+    CBN_REQUIRE(oversample_factor >= 1.0, "oversample_factor must be >= 1");
+    CBN_REQUIRE(m >= 1 && (nodes64 || nodes32), "need at least one node");
+    CBN_REQUIRE(m < ((int64_t)1 << 31), "at most 2^31 - 1 nodes per plan");
+    CBN_REQUIRE(n_ls >= 1 && n_ls <= kMaxLS && ls_rows, "scaling-fit rows must number 1..8192");
+    for (int d = 0; d < ndim; ++d) {
+        CBN_REQUIRE(dims[d] >= 1, "dims must be >= 1");
+        CBN_REQUIRE(taps[d] >= 1, "tap counts must be >= 1");
+        CBN_REQUIRE(taps[d] == taps[0], "per-axis tap counts must be equal on the device path");
+    }
+    for (int64_t r = 0; r < n_ls; ++r) CBN_REQUIRE(ls_rows[r] >= 0 && ls_rows[r] < m, "bad scaling-fit row");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto p = std::make_unique<cbn_nufft_s>();
+    p->D = ndim;
+    p->J = taps[0];
+    p->m = m;
+    for (int d = 0; d < ndim; ++d) {
+        p->ax[d] = make_axis((int)dims[d], taps[d], oversample_factor);
+        p->kb.ax[d] = p->ax[d].kb;
+        p->smax = std::max(p->smax, p->ax[d].N);
+        p->ktot *= p->ax[d].K;
+        p->ntot *= p->ax[d].N;
+        p->centre[d] = (double)(dims[d] / 2);
+    }
+    if (nodes64) {
+        DevBuf<double> raw;
+        raw.upload(nodes64, (size_t)m * ndim, s);
+        p->nodes.alloc((size_t)m * ndim);
+        k_wrap_nodes<<<blocks_for(m * ndim, 256), 256, 0, s>>>(raw.p, p->nodes.p, m * ndim);
+        CBN_LAUNCH_CHECK();
+        CBN_CUDA(cudaStreamSynchronize(s));
+    } else {
+        p->nodes32.upload(nodes32, (size_t)m * ndim, s);
+    }
+    size_t ksum = 0, nsum = 0;
+    for (int d = 0; d < ndim; ++d) {
+        ksum += p->ax[d].K;
+        nsum += p->ax[d].N;
+    }
+    p->s32.alloc((size_t)ndim * p->smax);
+    p->pad_idx.alloc(ksum);
+    p->pad_sc.alloc(ksum);
+    p->crop_idx.alloc(nsum);
+    p->crop_sc.alloc(nsum);
+    p->grid.alloc((size_t)p->ktot);
+    dispatch_d(ndim, [&](auto dc) {
+        fit_plan<decltype(dc)::value>(p.get(), ls_rows, n_ls, s);
+        return 0;
+    });
+    *out = p.release();
+    return CBN_OK;
+}
+
 }  // namespace
 
 extern "C" {
-
-const char* cbn_last_error(void);
 
 int cbn_version(void) { return 1; }
 
@@ -202,52 +306,19 @@ int cbn_nufft_create(cbn_nufft** out, int ndim, const int64_t* dims, const int32
                      double oversample_factor, const double* nodes, int64_t m,
                      const int64_t* ls_rows, int64_t n_ls, void* stream) {
     try {
-        CBN_REQUIRE(out && dims && taps, "null argument");
-        CBN_REQUIRE(ndim >= 1 && ndim <= 3, "ndim must be 1..3");
-        CBN_REQUIRE(oversample_factor >= 1.0, "oversample_factor must be >= 1");
-        CBN_REQUIRE(m >= 1 && nodes, "need at least one node");
-        CBN_REQUIRE(n_ls >= 1 && n_ls <= kMaxLS && ls_rows, "scaling-fit rows must number 1..8192");
-        for (int d = 0; d < ndim; ++d) {
-            CBN_REQUIRE(dims[d] >= 1, "dims must be >= 1");
-            CBN_REQUIRE(taps[d] >= 1, "tap counts must be >= 1");
-            CBN_REQUIRE(taps[d] == taps[0], "per-axis tap counts must be equal on the device path");
-        }
-        for (int64_t r = 0; r < n_ls; ++r) CBN_REQUIRE(ls_rows[r] >= 0 && ls_rows[r] < m, "bad scaling-fit row");
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
-        auto p = std::make_unique<cbn_nufft_s>();
-        p->D = ndim;
-        p->J = taps[0];
-        p->m = m;
-        for (int d = 0; d < ndim; ++d) {
-            p->ax[d] = make_axis((int)dims[d], taps[d], oversample_factor);
-            p->kb.ax[d] = p->ax[d].kb;
-            p->smax = std::max(p->smax, p->ax[d].N);
-            p->ktot *= p->ax[d].K;
-            p->ntot *= p->ax[d].N;
-            p->centre[d] = (double)(dims[d] / 2);
-        }
-        DevBuf<double> raw;
-        raw.upload(nodes, (size_t)m * ndim, s);
-        p->nodes.alloc((size_t)m * ndim);
-        k_wrap_nodes<<<blocks_for(m * ndim, 256), 256, 0, s>>>(raw.p, p->nodes.p, m * ndim);
-        CBN_LAUNCH_CHECK();
-        size_t ksum = 0, nsum = 0;
-        for (int d = 0; d < ndim; ++d) {
-            ksum += p->ax[d].K;
-            nsum += p->ax[d].N;
-        }
-        p->s32.alloc((size_t)ndim * p->smax);
-        p->pad_idx.alloc(ksum);
-        p->pad_sc.alloc(ksum);
-        p->crop_idx.alloc(nsum);
-        p->crop_sc.alloc(nsum);
-        p->grid.alloc((size_t)p->ktot);
-        dispatch_d(ndim, [&](auto dc) {
-            fit_plan<decltype(dc)::value>(p.get(), ls_rows, n_ls, s);
-            return 0;
-        });
-        *out = p.release();
-        return CBN_OK;
+        return create_plan(out, ndim, dims, taps, oversample_factor, nodes, nullptr, m, ls_rows,
+                           n_ls, stream);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_create_f32(cbn_nufft** out, int ndim, const int64_t* dims, const int32_t* taps,
+                         double oversample_factor, const float* nodes, int64_t m,
+                         const int64_t* ls_rows, int64_t n_ls, void* stream) {
+    try {
+        return create_plan(out, ndim, dims, taps, oversample_factor, nullptr, nodes, m, ls_rows,
+                           n_ls, stream);
     } catch (const std::exception& e) {
         return fail(e);
     }
@@ -283,7 +354,14 @@ int cbn_nufft_scaling(const cbn_nufft* p, double* out) {
 int cbn_nufft_wrapped_nodes(const cbn_nufft* p, double* out) {
     try {
         CBN_REQUIRE(p && out, "null argument");
-        CBN_CUDA(cudaMemcpy(out, p->nodes.p, sizeof(double) * p->m * p->D, cudaMemcpyDeviceToHost));
+        DevBuf<double> dev((size_t)p->m * p->D);
+        dispatch_d(p->D, [&](auto dc) {
+            constexpr int D = decltype(dc)::value;
+            k_first<D><<<blocks_for(p->m, 256), 256>>>(p->src<D>(), p->kb, p->m, nullptr, dev.p);
+            return 0;
+        });
+        CBN_LAUNCH_CHECK();
+        CBN_CUDA(cudaMemcpy(out, dev.p, sizeof(double) * p->m * p->D, cudaMemcpyDeviceToHost));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);
@@ -297,7 +375,8 @@ int cbn_nufft_first_indices(const cbn_nufft* p, int32_t* out, void* stream) {
         DevBuf<int32_t> dev((size_t)p->m * p->D);
         dispatch_d(p->D, [&](auto dc) {
             constexpr int D = decltype(dc)::value;
-            k_first<D><<<blocks_for(p->m, 256), 256, 0, s>>>(p->nodes.p, p->kb, p->m, dev.p);
+            k_first<D><<<blocks_for(p->m, 256), 256, 0, s>>>(p->src<D>(), p->kb, p->m, dev.p,
+                                                             nullptr);
             return 0;
         });
         CBN_LAUNCH_CHECK();

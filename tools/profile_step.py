@@ -20,6 +20,24 @@ def main():
     import torch
     from paper_1605_05231_b200.pipeline import Projector
     from paper_1605_05231_b200.workloads import workload
+    if args.config == 4:
+        from paper_1605_05231_b200 import nufft
+        from paper_1605_05231_b200.workloads import config4_inputs
+        x, pts = config4_inputs(int(os.environ.get("CBN_C4_POINTS", 100_000_000)))
+        plan = nufft.plan_nufft(x.shape, pts, 2.0, 8)
+        xd = torch.from_numpy(x).cuda()
+
+        def step():
+            nufft.nufft_adjoint(plan, nufft.nufft_forward(plan, xd))
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print("profiled one config-4 step", flush=True)
+        return
     w = workload(args.config)
     vol = torch.from_numpy(w.volume()).cuda()
     if args.direction == "forward":

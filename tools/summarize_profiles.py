@@ -110,6 +110,15 @@ def main():
         if os.path.exists(r):
             open(os.path.join(dst, f"{tag}_ncu_full_{d}.txt"), "w").write(
                 f"# ncu --set full, config-2 {d} step\n" + full_summary(r) + "\n")
+    p = os.path.join(src, "launches.csv")
+    if os.path.exists(p):
+        open(os.path.join(dst, f"{tag}_launches.txt"), "w").write(
+            "# ncu launch list, one config-4 step (type-2 + type-1, 100M points; "
+            "tools/profile_step.py --config 4)\n" + launch_summary(p) + "\n")
+    r = os.path.join(src, "full.ncu-rep")
+    if os.path.exists(r):
+        open(os.path.join(dst, f"{tag}_ncu_full.txt"), "w").write(
+            "# ncu --set full, config-4 gather / spread\n" + full_summary(r) + "\n")
     for f in ("bench.json", "bench_back.json", "smoke.txt", "pytest_gpu.txt"):
         p = os.path.join(src, f)
         if os.path.exists(p):
