@@ -3,7 +3,17 @@
 
 #include "cbn_binned.cuh"
 
+#include <cstdlib>
+
 namespace cbn {
+
+int spread_warps_override() {
+    static const int w = [] {
+        const char* e = std::getenv("CBN_SPREAD_W");
+        return e ? std::atoi(e) : 0;
+    }();
+    return w;
+}
 
 __global__ void k_bin_scatter(const int* __restrict__ keys, int64_t m, int* __restrict__ cursor,
                               int* __restrict__ perm) {

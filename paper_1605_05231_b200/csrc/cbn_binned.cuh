@@ -308,6 +308,18 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
     int* stl = reinterpret_cast<int*>(stv + NP);
     for (int e = threadIdx.x; e < nreg; e += NP) reg[e] = make_float2(0.f, 0.f);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // this lane's taps of a warp's rows: row index, cell offset, weight slots
+    const int row_stride = R1 * P;
+    int t_row[ITERS], t_off[ITERS], t_wy[ITERS], t_wz[ITERS];
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+        const int t = it * 32 + lane;
+        const int r = t / JJ, pq = t % JJ, b = pq / J, c = pq % J;
+        t_row[it] = t < ROWS * JJ ? r : J;
+        t_off[it] = r * W * row_stride + b * P + c;
+        t_wy[it] = J + b;
+        t_wz[it] = 2 * J + c;
+    }
     for (int base = 0; base < sp.count; base += NP) {
         __syncthreads();   // region zeroed / previous round's points consumed
         const int k = base + threadIdx.x;
@@ -323,7 +335,7 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const int l0 = wrapc(first[0], tg.K[0]) - o[0];
             const int l1 = wrapc(first[1], tg.K[1]) - o[1];
             const int l2 = wrapc(first[2], tg.K[2]) - o[2];
-            stl[threadIdx.x] = (l0 << 20) | (l1 << 10) | l2;
+            stl[threadIdx.x] = (l0 << 24) | ((l0 * R1 + l1) * P + l2);
             stv[threadIdx.x] = v;
 #pragma unroll
             for (int d = 0; d < 3; ++d)
@@ -336,20 +348,16 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const float2 v = stv[j];
             if (v.x == 0.f && v.y == 0.f) continue;     // uniform over the CTA
             const int pl = stl[j];
-            const int l0 = pl >> 20, l1 = (pl >> 10) & 1023, l2 = pl & 1023;
+            const int l0 = pl >> 24;
             const float* ws = stw + j * SW;
-            int a0 = (warp - l0) % W;
-            a0 += a0 < 0 ? W : 0;
-            const int nrows = a0 < J ? (J - 1 - a0) / W + 1 : 0;
-            float2* base_row = reg + ((l0 + a0) * R1 + l1) * P + l2;
+            int a0 = (W & (W - 1)) == 0 ? (warp - l0) & (W - 1) : ((warp - l0) % W + W) % W;
+            const int nrows = J % W == 0 ? J / W : (a0 < J ? (J - 1 - a0) / W + 1 : 0);
+            float2* base_row = reg + (pl & 0xffffff) + a0 * row_stride;
 #pragma unroll
             for (int it = 0; it < ITERS; ++it) {
-                const int t = it * 32 + lane;
-                const int r = t / JJ, pq = t % JJ;
-                if (r < nrows) {
-                    const int b = pq / J, c = pq % J;
-                    const float wk = ws[a0 + r * W] * ws[J + b] * ws[2 * J + c];
-                    float2* cell = base_row + (r * W * R1 + b) * P + c;
+                if (t_row[it] < nrows) {
+                    const float wk = ws[a0 + t_row[it] * W] * ws[t_wy[it]] * ws[t_wz[it]];
+                    float2* cell = base_row + t_off[it];
                     float2 cur = *cell;
                     cur.x = fmaf(wk, v.x, cur.x);
                     cur.y = fmaf(wk, v.y, cur.y);
@@ -515,16 +523,15 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
 }
 
 // warps per CTA of the 3D owner-computes spread: rows per warp x J^2 taps
-// should fill whole 32-lane iterations (J=8: 1 row x 64; J=6: 2 rows x 36)
+// (measured on B200: J=8 -> 8 warps, 55 ms vs 64 ms at 4 on config 4; J=6 -> 2
+// warps, 10.4 ms vs 12.7 ms at 3 on the config-2 backprojection)
 template <int J>
 constexpr int owned_warps() {
-    return J == 6 ? 3 : (J < 8 ? J : 8);
+    return J == 6 ? 2 : (J < 8 ? J : 8);
 }
 
-template <int J, class Src>
-void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s) {
-    constexpr int W = owned_warps<J>();
-    CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
+template <int J, int W, class Src>
+void launch_spread3_w(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s) {
     const size_t smem = spread_owned_smem_bytes<J, W>(bb.nreg);
     CBN_CUDA(cudaFuncSetAttribute(k_spread_owned<J, W, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
@@ -532,6 +539,19 @@ void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src&
         k_spread_owned<J, W><<<bb.nsubs, W * 32, smem, s>>>(grid, kb, bb.geom<3>(), src, bb.perm.p,
                                                             bb.subs.p);
     CBN_LAUNCH_CHECK();
+}
+
+int spread_warps_override();   // CBN_SPREAD_W (tuning experiments), 0 = default
+
+template <int J, class Src>
+void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s) {
+    CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
+    switch (spread_warps_override()) {
+        case 1: return launch_spread3_w<J, 1>(grid, kb, bb, src, s);
+        case 2: return launch_spread3_w<J, 2>(grid, kb, bb, src, s);
+        case 4: return launch_spread3_w<J, 4>(grid, kb, bb, src, s);
+        default: return launch_spread3_w<J, owned_warps<J>()>(grid, kb, bb, src, s);
+    }
 }
 
 }  // namespace cbn

@@ -2,10 +2,10 @@
 // views (grangeat.py:131-170).  The polar detector-plane nodes are shared by
 // all views (plan_grangeat), so per plan each node is sorted into a 2D tile,
 // and its local first tap, the J + J KB weights and its complex factor
-// (filter * phase) are precomputed once.  Per (subproblem, view group) a CTA
-// then only streams the per-view values:
-//   reverse: warp-private shared tiles, one view group of VG views per CTA,
-//            lanes = taps, plain load/add/store, one RED per non-zero cell;
+// (filter * phase) are precomputed once.  Per subproblem a CTA then only
+// streams the per-view values:
+//   reverse: one [cell][32 views] shared region, rows owned by warps, lanes =
+//            views (k_gr_spread_owned);
 //   forward: the VG view tiles are staged in shared memory, one thread per
 //            node reads its taps for each view.
 #pragma once
@@ -18,7 +18,10 @@ namespace cbn {
 template <int J>
 struct GrPoint {
     short lu, lv;      // first tap relative to the bin origin
-    int col;           // mu * n_t + (rolled t index) into the per-view t buffer
+    // forward records: mu * n_t + (rolled t index) into the per-view C2C buffer;
+    // reverse records: mu * (n_t/2 + 1) + k into the R2C half spectrum, stored
+    // as ~index when the value is the conjugate of bin n_t - k (Hermitian half)
+    int col;
     float2 fac;        // complex factor (filter * phase), zero if the node is inert
     float w[2 * J];    // u weights, then v weights
 };
@@ -51,11 +54,17 @@ __global__ void k_gr_points(KBSet kb, TileGeom<2> tg, PolarSrc src, GrFactor f,
         g.lu = (short)(wrapc(first[0], tg.K[0]) - o[0]);
         g.lv = (short)(wrapc(first[1], tg.K[1]) - o[1]);
         const int im = i / f.n_t;
-        g.col = im * f.n_t + (aux.jt - f.n_t / 2 + f.n_t) % f.n_t;
+        const int kr = (aux.jt - f.n_t / 2 + f.n_t) % f.n_t;   // fftshift of the t FFT
+        g.col = im * f.n_t + kr;
         double sn, cs;
         if (f.reverse) {
+            // the reference rolls the line by n_t/2 before a C2C FFT; here the
+            // unrolled real line goes through R2C, so bin kr picks up (-1)^kr
+            // and bins above n_t/2 read the conjugate of bin n_t - kr
+            const int nh = f.n_t / 2 + 1;
+            g.col = kr < nh ? im * nh + kr : ~(im * nh + (f.n_t - kr));
             sincos(-centre_plan_angle<2>(aux.wc, w, f.N), &sn, &cs);
-            const float q = f.q[aux.jt];
+            const float q = (kr & 1) ? -f.q[aux.jt] : f.q[aux.jt];
             g.fac = make_float2(-(float)sn * q, (float)cs * q);
         } else {
             sincos(centre_plan_angle<2>(aux.wc, w, f.N), &sn, &cs);
@@ -71,163 +80,116 @@ __global__ void k_gr_points(KBSet kb, TileGeom<2> tg, PolarSrc src, GrFactor f,
     }
 }
 
-// reverse: grids[v] += sum_points w * (t[v][col] * fac)  for views [v0, v0 + nv)
-template <int J, int VG, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-k_gr_spread_binned(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
-                   const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
-                   const float2* __restrict__ tf, size_t tf_stride, int nviews) {
-    extern __shared__ float2 smem[];
-    const SubProblem sp = subs[blockIdx.x];
-    const int v0 = blockIdx.y * VG;
-    const int nv = min(VG, nviews - v0);
-    int o[3];
-    bin_origin<2>(tg, sp.bin, o);
-    const int R1 = tg.R[1];
-    const int nreg = tg.R[0] * R1;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float2* copy = smem + (size_t)warp * VG * nreg;
-    for (int e = threadIdx.x; e < WARPS * VG * nreg; e += blockDim.x) smem[e] = make_float2(0.f, 0.f);
-    __syncthreads();
-    const int a = lane / J, b = lane % J;
-    const bool active = lane < J * J;
-    const float2* tfv = tf + (size_t)v0 * tf_stride;
-    // PG points x VG views per step: one independent value load per lane, then
-    // the warp walks the PG points with lanes = taps and shuffles the values in
-    constexpr int PG = 32 / VG;
-    for (int base = warp * PG; base < sp.count; base += WARPS * PG) {
-        const int kl = base + lane / VG, vl = lane % VG;
-        float2 y = make_float2(0.f, 0.f);
-        if (kl < sp.count && vl < nv) {
-            const GrPoint<J>& gl = pts[sp.start + kl];
-            y = cmul(__ldg(tfv + vl * tf_stride + gl.col), gl.fac);
-        }
-        const int npg = min(PG, sp.count - base);
-        for (int j = 0; j < npg; ++j) {
-            const GrPoint<J>& g = pts[sp.start + base + j];
-            const float wk = active ? g.w[a] * g.w[J + b] : 0.f;
-            const int cell = (g.lu + a) * R1 + g.lv + b;
-#pragma unroll
-            for (int v = 0; v < VG; ++v) {
-                const float yx = __shfl_sync(0xffffffffu, y.x, j * VG + v);
-                const float yy = __shfl_sync(0xffffffffu, y.y, j * VG + v);
-                if (active && (yx != 0.f || yy != 0.f)) {
-                    float2 cur = copy[v * nreg + cell];
-                    cur.x = fmaf(wk, yx, cur.x);
-                    cur.y = fmaf(wk, yy, cur.y);
-                    copy[v * nreg + cell] = cur;
-                }
-            }
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
-        float2 s = smem[e];
-#pragma unroll
-        for (int wi = 1; wi < WARPS; ++wi) {
-            const float2 x = smem[(size_t)wi * VG * nreg + e];
-            s.x += x.x;
-            s.y += x.y;
-        }
-        if (s.x == 0.f && s.y == 0.f) continue;
-        const int v = e / nreg, c = e % nreg;
-        const int r0 = c / R1, r1 = c % R1;
-        const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
-        atomicAdd(grids + (size_t)(v0 + v) * grid_stride + gi, s);
-    }
-}
-
-// reverse, lanes = views: each warp walks its points, every lane adds its own
-// view's value to a private [cell][32 views] shared tile (consecutive lanes,
-// consecutive words: conflict-free, no shuffles); one RED per non-zero
-// (cell, view) at the end.  nviews <= 32.
-template <int J, int WARPS, int TILE>
-__global__ void __launch_bounds__(WARPS * 32)
-k_gr_spread_views(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
+// reverse, lanes = views, one [cell][32 views] region per CTA with rows owned
+// by warps: J warps, warp w updates only region rows u = w (mod J), so each
+// point's J x J taps are split one row per warp.  Chunks of 32 points are
+// staged in shared memory (record: packed first taps, u / v weights, factor;
+// value: t-spectrum * factor per view), then every warp applies every staged
+// point to its row.  Lanes are views, so no two lanes share a word and warps
+// share no cells: plain read-add-write, no syncs inside a chunk, and J x 32
+// threads per region instead of one warp per private region.
+template <int J, int TILE>
+__global__ void __launch_bounds__(J * 32)
+k_gr_spread_owned(float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
                   const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
                   const float2* __restrict__ tf, size_t tf_stride, int nviews) {
-    extern __shared__ float2 smem[];
+    static_assert(J <= 8, "record layout holds up to 8 weights per axis");
+    constexpr int W = J;
+    constexpr int R1 = TILE + J - 1;
+    constexpr int nreg = R1 * R1;
+    constexpr int CH = 32;
+    constexpr int SW = 16;            // [0, J): v weights, [8, 8 + J): u weights
+    extern __shared__ float4 smem4[];
+    float2* region = reinterpret_cast<float2*>(smem4);       // [nreg][32]
+    float2* sy = region + nreg * 32;                         // [CH][32]
+    float* sw = reinterpret_cast<float*>(sy + CH * 32);      // [CH][SW]
+    float2* sfac = reinterpret_cast<float2*>(sw + CH * SW);  // [CH]
+    int* sl = reinterpret_cast<int*>(sfac + CH);             // [CH] lu | lv << 16
+    int* scol = sl + CH;                                     // [CH]
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<2>(tg, sp.bin, o);
-    constexpr int R1 = TILE + J - 1;
-    constexpr int nreg = R1 * R1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float2* copy = smem + (size_t)warp * nreg * 32;
-    for (int e = threadIdx.x; e < WARPS * nreg * 32; e += blockDim.x) smem[e] = make_float2(0.f, 0.f);
-    __syncthreads();
+    for (int e = threadIdx.x; e < nreg * 32; e += W * 32) region[e] = make_float2(0.f, 0.f);
     const bool live = lane < nviews;
     const float2* tfl = tf + (size_t)lane * tf_stride;
-    // CH points per step: lanes < CH fetch one point record each; then every
-    // lane issues its CH view-value loads back to back (deep memory-level
-    // parallelism at 4 warps / SM), and the CH points are applied from registers
-    constexpr int CH = 16;
-    for (int base0 = warp * CH; base0 < sp.count; base0 += WARPS * CH) {
-        const int npts = min(CH, sp.count - base0);
-        GrPoint<J> mine;
-        if (lane < npts) mine = pts[sp.start + base0 + lane];
-        else {
-            mine.lu = mine.lv = 0;
-            mine.col = 0;
-            mine.fac = make_float2(0.f, 0.f);
+    for (int base = 0; base < sp.count; base += CH) {
+        const int npts = min(CH, sp.count - base);
+        __syncthreads();   // region zeroed / previous chunk consumed
+        if (threadIdx.x < npts) {
+            const GrPoint<J>& g = pts[sp.start + base + threadIdx.x];
+            float* w = sw + threadIdx.x * SW;
 #pragma unroll
-            for (int q = 0; q < 2 * J; ++q) mine.w[q] = 0.f;
+            for (int q = 0; q < J; ++q) {
+                w[q] = g.w[J + q];
+                w[8 + q] = g.w[q];
+            }
+            sfac[threadIdx.x] = g.fac;
+            sl[threadIdx.x] = (int)(unsigned short)g.lu | ((int)g.lv << 16);
+            scol[threadIdx.x] = g.col;
         }
-        float2 yv[CH];
+        __syncthreads();
 #pragma unroll
-        for (int j = 0; j < CH; ++j) {
-            const int col = __shfl_sync(0xffffffffu, mine.col, j);
-            yv[j] = (live && j < npts) ? __ldg(tfl + col) : make_float2(0.f, 0.f);
-        }
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-            const float fx = __shfl_sync(0xffffffffu, mine.fac.x, j);
-            const float fy = __shfl_sync(0xffffffffu, mine.fac.y, j);
-            if (fx == 0.f && fy == 0.f) continue;   // warp-uniform (also past npts)
-            const int lu = __shfl_sync(0xffffffffu, (int)mine.lu, j);
-            const int lv = __shfl_sync(0xffffffffu, (int)mine.lv, j);
-            float w[2 * J];
-#pragma unroll
-            for (int q = 0; q < 2 * J; ++q) w[q] = __shfl_sync(0xffffffffu, mine.w[q], j);
-            const float2 y = cmul(yv[j], make_float2(fx, fy));
-            // the J x J cells are distinct: load all, update, store all
-            float2* base = copy + (lu * R1 + lv) * 32 + lane;
-            float2 cur[J][J];
-#pragma unroll
-            for (int a = 0; a < J; ++a)
-#pragma unroll
-                for (int b = 0; b < J; ++b) cur[a][b] = base[(a * R1 + b) * 32];
-#pragma unroll
-            for (int a = 0; a < J; ++a)
-#pragma unroll
-                for (int b = 0; b < J; ++b) {
-                    const float wk = w[a] * w[J + b];
-                    cur[a][b].x = fmaf(wk, y.x, cur[a][b].x);
-                    cur[a][b].y = fmaf(wk, y.y, cur[a][b].y);
+        for (int p0 = 0; p0 < CH; p0 += W) {
+            const int p = p0 + warp;
+            if (p < npts) {
+                const float2 f = sfac[p];
+                const int c = scol[p];
+                float2 y = make_float2(0.f, 0.f);
+                if (live) {
+                    y = __ldg(tfl + (c >= 0 ? c : ~c));
+                    y.y = c >= 0 ? y.y : -y.y;
+                    y = cmul(y, f);
                 }
+                sy[p * 32 + lane] = y;
+            }
+        }
+        __syncthreads();
+        for (int p = 0; p < npts; ++p) {
+            const float2 f = sfac[p];
+            if (f.x == 0.f && f.y == 0.f) continue;   // inert node, uniform over the CTA
+            const int pl = sl[p];
+            const int lu = pl & 0xffff, lv = pl >> 16;
+            int a0 = (warp - lu) % W;
+            a0 += a0 < 0 ? W : 0;
+            const float* w = sw + p * SW;
+            const float wa = w[8 + a0];
+            float wv[8];
+            const float4 w03 = *reinterpret_cast<const float4*>(w);
+            const float4 w47 = *reinterpret_cast<const float4*>(w + 4);
+            wv[0] = w03.x; wv[1] = w03.y; wv[2] = w03.z; wv[3] = w03.w;
+            wv[4] = w47.x; wv[5] = w47.y; wv[6] = w47.z; wv[7] = w47.w;
+            const float2 y = sy[p * 32 + lane];
+            float2* row = region + ((lu + a0) * R1 + lv) * 32 + lane;
+            float2 cur[J];
 #pragma unroll
-            for (int a = 0; a < J; ++a)
+            for (int b = 0; b < J; ++b) cur[b] = row[b * 32];
 #pragma unroll
-                for (int b = 0; b < J; ++b) base[(a * R1 + b) * 32] = cur[a][b];
+            for (int b = 0; b < J; ++b) {
+                const float wk = wa * wv[b];
+                cur[b].x = fmaf(wk, y.x, cur[b].x);
+                cur[b].y = fmaf(wk, y.y, cur[b].y);
+            }
+#pragma unroll
+            for (int b = 0; b < J; ++b) row[b * 32] = cur[b];
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nreg * 32; e += blockDim.x) {
+    for (int e = threadIdx.x; e < nreg * 32; e += W * 32) {
         const int v = e & 31, c = e >> 5;
         if (v >= nviews) continue;
-        float2 s = smem[e];
-#pragma unroll
-        for (int wi = 1; wi < WARPS; ++wi) {
-            const float2 x = smem[(size_t)wi * nreg * 32 + e];
-            s.x += x.x;
-            s.y += x.y;
-        }
+        const float2 s = region[e];
         if (s.x == 0.f && s.y == 0.f) continue;
         const int r0 = c / R1, r1 = c % R1;
         const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
         atomicAdd(grids + (size_t)v * grid_stride + gi, s);
     }
+}
+
+template <int J, int TILE>
+constexpr size_t gr_spread_owned_smem() {
+    return sizeof(float2) * ((size_t)(TILE + J - 1) * (TILE + J - 1) * 32 + 32 * 32) +
+           sizeof(float) * 32 * 16 + sizeof(float2) * 32 + sizeof(int) * 64;
 }
 
 // forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv)

@@ -121,8 +121,12 @@ struct SpecOut {
 
 struct UmbOut {
     float* vals;
+    const float* tscale = nullptr;   // optional per-t factor (1 / w2 of the Grangeat step)
+    int n_t = 1;
     CBN_D void put(int64_t i, float2 v, const double (&)[3], const UmbrellaSrc::Aux& a) const {
-        vals[i] = a.valid ? v.x : 0.f;   // Re(resample_apply), invalid -> 0 (pipeline.py:136-137)
+        float x = a.valid ? v.x : 0.f;   // Re(resample_apply), invalid -> 0 (pipeline.py:136-137)
+        if (tscale) x *= tscale[i % n_t];
+        vals[i] = x;
     }
 };
 
@@ -170,7 +174,7 @@ template <int J>
 __global__ void __launch_bounds__(256)
 k_resample_views(const float2* __restrict__ G, int K0, int K1, int K2,
                  const RsTap<J>* __restrict__ taps, int64_t per_view, int v0, int nviews,
-                 int shift, float* __restrict__ vals) {
+                 int shift, float* __restrict__ vals, const float* __restrict__ tscale, int n_t) {
     __shared__ float tile[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t0 = (int64_t)blockIdx.x * 32;
@@ -215,7 +219,10 @@ k_resample_views(const float2* __restrict__ G, int K0, int K1, int K2,
     __syncthreads();
     for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
         const int v = e >> 5, tt = e & 31;
-        if (v < nviews && t0 + tt < per_view) vals[(size_t)v * per_view + t0 + tt] = tile[v][tt];
+        if (v < nviews && t0 + tt < per_view) {
+            const float x = tile[v][tt];
+            vals[(size_t)v * per_view + t0 + tt] = tscale ? x * tscale[(t0 + tt) % n_t] : x;
+        }
     }
 }
 
@@ -310,58 +317,12 @@ __global__ void k_pad_lattice(const float2* __restrict__ src, int shift, float s
 }
 
 // ---- reverse Grangeat (grangeat.py:149-170)
-struct GrRevParams {
-    int n_mu, n_t;
-    int nu, nv, Ku, Kv;
-    const float* q;        // per t: -sign(omega) taper dt c2  (y = S * i q)
-};
-
-__global__ void k_gr_pre(const float* __restrict__ vals, const float* __restrict__ w2, int n_t,
-                         int64_t total, float2* __restrict__ out) {
+// rows of vals * (1 / w2[t]) (grangeat.py:152) for callers passing raw values
+__global__ void k_gr_scale(const float* __restrict__ vals, const float* __restrict__ w2inv, int n_t,
+                           int64_t total, float* __restrict__ out) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= total) return;
-    int j = (int)(e % n_t);
-    int64_t row = e / n_t;
-    out[row * n_t + (j - n_t / 2 + n_t) % n_t] = make_float2(vals[e] / w2[j], 0.f);
-}
-
-template <int J>
-__global__ void __launch_bounds__(256)
-k_gr_spread(float2* __restrict__ grids, KBSet kb, PolarSrc src, const float2* __restrict__ tf,
-            GrRevParams p, int nb) {
-    const int64_t m = (int64_t)p.n_mu * p.n_t;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    double w[2];
-    PolarSrc::Aux aux;
-    src.node(i, w, aux);
-    const float q = p.q[aux.jt];
-    if (q == 0.f) return;
-    double sn, cs;
-    const int N[2] = {p.nu, p.nv};
-    sincos(-centre_plan_angle<2>(aux.wc, w, N), &sn, &cs);   // conj(centre) * conj(plan)
-    // factor = phase * (i q)
-    const float2 fac = make_float2(-(float)sn * q, (float)cs * q);
-    int first[2];
-    float wt[2][J];
-    tap_setup<2, J>(kb, w, first, wt);
-    int c1[J];
-#pragma unroll
-    for (int b = 0; b < J; ++b) c1[b] = wrapc(first[1] + b, p.Kv);
-    const int im = (int)(i / p.n_t);
-    const int col = (aux.jt - p.n_t / 2 + p.n_t) % p.n_t;   // fftshift of the t FFT
-    const size_t gsz = (size_t)p.Ku * p.Kv;
-    for (int v = 0; v < nb; ++v) {
-        float2 val = cmul(tf[((size_t)v * p.n_mu + im) * p.n_t + col], fac);
-        float2* grid = grids + v * gsz;
-#pragma unroll
-        for (int a = 0; a < J; ++a) {
-            float2* row = grid + (size_t)wrapc(first[0] + a, p.Ku) * p.Kv;
-            float2 va = cscale(val, wt[0][a]);
-#pragma unroll
-            for (int b = 0; b < J; ++b) atomicAdd(row + c1[b], cscale(va, wt[1][b]));
-        }
-    }
+    out[e] = vals[e] * w2inv[e % n_t];
 }
 
 CBN_D double w1_at(int u, int v, int nu, int nv, double pu, double pv, double so) {
@@ -541,11 +502,12 @@ void build_grangeat(P* p, GrangeatPlan& gp, const UmbrellaTables& u, int taper, 
     double amax = 0;
     for (double o : om) amax = std::max(amax, std::fabs(o));
     const double c2 = 1.0 / (2.0 * u.n_mu * u.n_t * u.dt);
-    std::vector<float> w2(u.n_t), q(u.n_t);
+    std::vector<float> w2(u.n_t), w2inv(u.n_t), q(u.n_t);
     const double so = p->g.so_mm;
     for (int j = 0; j < u.n_t; ++j) {
         double t = (double)(j - u.n_t / 2) * u.dt;
         w2[j] = (float)((so * so + t * t) / (so * so));
+        w2inv[j] = (float)((so * so) / (so * so + t * t));
         double tp = 1.0;
         if (taper == 1) {
             double cv = std::cos(kPi * om[j] / (2.0 * amax));
@@ -555,6 +517,7 @@ void build_grangeat(P* p, GrangeatPlan& gp, const UmbrellaTables& u, int taper, 
         q[j] = (float)(-sg * tp * u.dt * c2);
     }
     gp.w2.upload(w2.data(), w2.size(), s);
+    gp.w2inv.upload(w2inv.data(), w2inv.size(), s);
     gp.fac_im.upload(q.data(), q.size(), s);
     CBN_CUDA(cudaStreamSynchronize(s));
 }
@@ -840,7 +803,8 @@ bool views_in_lanes(const P* p) {
 }
 
 // Re(resample_apply) for nb <= 32 consecutive views [v0, v0 + nb) from a phi-fast grid
-void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s) {
+void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
+                        const float* tscale = nullptr) {
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
     const int shift = (int)(2LL * p->frad.n_phi / p->g.n_views);
@@ -862,14 +826,15 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s) {
         StageScope st(p->timer, "resample_gather", s);
         k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
             p->big.p, ax[2].K, ax[1].K, ax[0].K, reinterpret_cast<const RsTap<J>*>(u.taps.p),
-            per_view, v0, nb, shift, vals);
+            per_view, v0, nb, shift, vals, tscale, p->fumb.n_t);
         CBN_LAUNCH_CHECK();
         return 0;
     });
 }
 
 // Re(resample_apply) at the umbrella targets of views [lo, hi) from the current grid
-void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s) {
+void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s,
+                  const float* tscale = nullptr) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
@@ -880,7 +845,8 @@ void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s) {
     StageScope st(p->timer, "resample_gather", s);
     dispatch_j(ax[0].J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
-        k_gather<3, J><<<blocks_for(m, 256), 256, 0, s>>>(p->big.p, kb, src, UmbOut{vals}, m);
+        k_gather<3, J><<<blocks_for(m, 256), 256, 0, s>>>(p->big.p, kb, src,
+                                                         UmbOut{vals, tscale, p->fumb.n_t}, m);
         return 0;
     });
     CBN_LAUNCH_CHECK();
@@ -931,41 +897,27 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     const UmbrellaTables& u = p->fumb;
     const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
     const int64_t tl = (int64_t)nb * u.n_mu * u.n_t;
-    p->gr_t.ensure((size_t)tl);
+    const int nh = u.n_t / 2 + 1;
+    p->gr_t.ensure((size_t)nb * u.n_mu * nh);
     p->gr_grid.ensure((size_t)nb * Ku * Kv);
     prepare_gr_points(p, gp, u, true, s);
     if (p->timer.on) p->timer.begin("grangeat_tfft", s);
-    k_gr_pre<<<blocks_for(tl, 256), 256, 0, s>>>(vals, gp.w2.p, u.n_t, tl, p->gr_t.p);
-    CBN_LAUNCH_CHECK();
-    long long nt[1] = {u.n_t};
-    p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_FORWARD, s);
+    (void)tl;
+    // vals arrive already divided by w2 (folded into the resample store), so
+    // the t lines go straight through a real-to-complex FFT
+    p->fft.exec_r2c(p->fft.get_r2c(u.n_t, (long long)nb * u.n_mu), vals, p->gr_t.p, s);
     CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
     if (p->timer.on) p->timer.end(s);
-    const char* old_spread = std::getenv("CBN_GR_ATOMIC");
-    if (old_spread && old_spread[0] == '1') {
-        // diagnostics: the plain global-atomic spread
-        GrRevParams rp;
-        rp.n_mu = u.n_mu;
-        rp.n_t = u.n_t;
-        rp.nu = p->g.nu;
-        rp.nv = p->g.nv;
-        rp.Ku = Ku;
-        rp.Kv = Kv;
-        rp.q = gp.fac_im.p;
-        PolarSrc src{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
-        k_gr_spread<5><<<blocks_for(gp.m, 256), 256, 0, s>>>(p->gr_grid.p, gp.kb, src, p->gr_t.p,
-                                                            rp, nb);
-        CBN_LAUNCH_CHECK();
-    } else {
+    {
         StageScope st(p->timer, "grangeat_spread", s);
         const BinPlan& bb = gp.bins;
-        const size_t smem = sizeof(float2) * kGrWarps * 32 * bb.nreg;
-        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_views<kGrJ, kGrWarps, kGrTileRev>,
+        constexpr size_t smem = gr_spread_owned_smem<kGrJ, kGrTileRev>();
+        CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_owned<kGrJ, kGrTileRev>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_gr_spread_views<kGrJ, kGrWarps, kGrTileRev><<<bb.nsubs, kGrWarps * 32, smem, s>>>(
+        k_gr_spread_owned<kGrJ, kGrTileRev><<<bb.nsubs, kGrJ * 32, smem, s>>>(
             p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(),
             reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p), bb.subs.p, p->gr_t.p,
-            (size_t)u.n_mu * u.n_t, nb);
+            (size_t)u.n_mu * nh, nb);
         CBN_LAUNCH_CHECK();
     }
     long long kd[2] = {Ku, Kv};
@@ -1004,13 +956,16 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         blk_n = 0;
     };
     const bool lanes = views_in_lanes(p);
+    // internal values feed the Grangeat step directly: store them divided by w2
+    const float* tscale = values_out ? nullptr : p->fgr.w2inv.p;
     auto gather = [&](int v, int n, float* out) {
         if (!lanes) {
-            gather_views(p, v, v + n, out, s);
+            gather_views(p, v, v + n, out, s, tscale);
             return;
         }
         for (int k = 0; k < n; k += 32)
-            gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, s);
+            gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, s,
+                               tscale);
     };
     // runs of consecutive batches (clipped to [lo, hi)) sharing one scaling group
     const size_t nbat = bp.batches.size();
@@ -1292,9 +1247,14 @@ int cbn_projector_grangeat_reverse(cbn_projector* p, const float* values, float*
         CBN_CUDA(cudaMemsetAsync(p->flag.p, 0, sizeof(int), s));
         const size_t per_view = (size_t)p->fumb.n_mu * p->fumb.n_t;
         const size_t fsz = (size_t)p->g.nu * p->g.nv;
+        p->values.ensure(per_view * 32);
         for (int v = 0; v < nb; v += 32) {
             int k = std::min(32, nb - v);
-            grangeat_reverse(p, values + v * per_view, frames + v * fsz, k, s);
+            const int64_t tot = (int64_t)k * per_view;
+            k_gr_scale<<<blocks_for(tot, 256), 256, 0, s>>>(values + v * per_view, p->fgr.w2inv.p,
+                                                            p->fumb.n_t, tot, p->values.p);
+            CBN_LAUNCH_CHECK();
+            grangeat_reverse(p, p->values.p, frames + v * fsz, k, s);
         }
         return CBN_OK;
     } catch (const std::exception& e) {

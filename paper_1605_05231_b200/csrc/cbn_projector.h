@@ -47,6 +47,7 @@ struct GrangeatPlan {
     double pu = 0, pv = 0;
     int64_t m = 0;
     DevBuf<float> w2, fac_re, fac_im;   // per t: post-weight, reverse filter (complex)
+    DevBuf<float> w2inv;                // per t: 1 / w2, folded into the resample store
     bool built = false;
     BinPlan bins;                       // polar nodes sorted by 2D tile
     DevBuf<char> pts;                   // GrPoint<5> per sorted node
@@ -55,9 +56,8 @@ struct GrangeatPlan {
 
 constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)
 constexpr int kGrTile = 16;    // forward (gather) tile edge
-constexpr int kGrTileRev = 8;  // reverse (views-in-lanes spread) tile edge
-constexpr int kGrVG = 8;       // views per CTA in the binned Grangeat kernels
-constexpr int kGrWarps = 4;
+constexpr int kGrTileRev = 8;  // reverse (owner-computes spread) tile edge
+constexpr int kGrVG = 8;       // views per CTA in the binned Grangeat gather
 
 constexpr int kTile3 = 8;      // 3D bin edge (oversampled cells)
 constexpr int kMaxSub = 1024;  // points per subproblem

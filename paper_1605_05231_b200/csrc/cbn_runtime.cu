@@ -24,7 +24,8 @@ void FFTCache::clear() {
     work_.release();
 }
 
-cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long stride, long long dist) {
+cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long stride, long long dist,
+                           cufftType type) {
     cufftHandle h;
     CBN_CUFFT(cufftCreate(&h));
     CBN_CUFFT(cufftSetAutoAllocation(h, 0));
@@ -35,8 +36,14 @@ cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long st
         for (int i = 0; i < rank; ++i) emb[i] = n[i];
         embed = emb;
     }
-    cufftResult r = cufftMakePlanMany64(h, rank, n, embed, stride, dist, embed, stride, dist,
-                                        CUFFT_C2C, batch, &ws);
+    cufftResult r;
+    if (type == CUFFT_R2C) {
+        long long ie[1] = {n[0]}, oe[1] = {n[0] / 2 + 1};
+        r = cufftMakePlanMany64(h, 1, n, ie, 1, n[0], oe, 1, n[0] / 2 + 1, CUFFT_R2C, batch, &ws);
+    } else {
+        r = cufftMakePlanMany64(h, rank, n, embed, stride, dist, embed, stride, dist, CUFFT_C2C,
+                                batch, &ws);
+    }
     if (r != CUFFT_SUCCESS) {
         cufftDestroy(h);
         throw Error(r == CUFFT_ALLOC_FAILED ? CBN_ENOMEM : CBN_ECUDA,
@@ -74,6 +81,21 @@ cufftHandle FFTCache::get_strided(long long n, long long batch, long long stride
     cufftHandle h = make(1, dims, batch, stride, dist);
     plans_[key] = h;
     return h;
+}
+
+cufftHandle FFTCache::get_r2c(long long n, long long batch) {
+    Key key{-2, n, 0, 0, batch, 1, n};
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return it->second;
+    long long dims[1] = {n};
+    cufftHandle h = make(1, dims, batch, 1, n, CUFFT_R2C);
+    plans_[key] = h;
+    return h;
+}
+
+void FFTCache::exec_r2c(cufftHandle h, const float* in, void* out, cudaStream_t s) {
+    CBN_CUFFT(cufftSetStream(h, s));
+    CBN_CUFFT(cufftExecR2C(h, const_cast<cufftReal*>(in), static_cast<cufftComplex*>(out)));
 }
 
 void FFTCache::exec(cufftHandle h, void* in, void* out, int direction, cudaStream_t s) {

@@ -97,13 +97,18 @@ public:
     // 1D transforms of length n over `batch` lines with element stride / distance
     cufftHandle get_strided(long long n, long long batch, long long stride, long long dist);
     void exec(cufftHandle h, void* in, void* out, int direction, cudaStream_t s);
+    // real-to-complex 1D transforms of `batch` contiguous lines of length n
+    // (n/2 + 1 complex outputs per line, out of place)
+    cufftHandle get_r2c(long long n, long long batch);
+    void exec_r2c(cufftHandle h, const float* in, void* out, cudaStream_t s);
     void clear();
 
 private:
     using Key = std::tuple<int, long long, long long, long long, long long, long long, long long>;
     std::map<Key, cufftHandle> plans_;
     DevBuf<char> work_;
-    cufftHandle make(int rank, long long* n, long long batch, long long stride, long long dist);
+    cufftHandle make(int rank, long long* n, long long batch, long long stride, long long dist,
+                     cufftType type = CUFFT_C2C);
 };
 
 // Per-stage CUDA-event timing (enabled per plan; off by default).

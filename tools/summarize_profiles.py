@@ -119,7 +119,7 @@ def main():
     if os.path.exists(r):
         open(os.path.join(dst, f"{tag}_ncu_full.txt"), "w").write(
             "# ncu --set full, config-4 gather / spread\n" + full_summary(r) + "\n")
-    for f in ("bench.json", "bench_back.json", "smoke.txt", "pytest_gpu.txt"):
+    for f in ("bench.json", "bench_back.json", "bench_c4.json", "smoke.txt", "pytest_gpu.txt"):
         p = os.path.join(src, f)
         if os.path.exists(p):
             open(os.path.join(dst, f"{tag}_{f}"), "w").write(open(p).read())
