@@ -284,11 +284,6 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     // transposed resample of one group of batches sharing a scaling: one
     // inverse FFT of the summed spreads, crop * scaling, accumulate
     auto flush = [&](int g) {
-        {
-            StageScope st(p->timer, "transpose_ifft", s);
-            p->fft.exec(p->fft.get(3, kd3, nch), p->big.p, p->big.p, CUFFT_INVERSE, s);
-        }
-        StageScope st(p->timer, "transpose_crop", s);
         size_t need = (size_t)rax[0].N + rax[1].N + rax[2].N;
         p->tab_idx.ensure(need);
         p->tab_sc.ensure(need);
@@ -300,6 +295,13 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
             ax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, rax[d].N, sstr[d]};
             off += rax[d].N;
         }
+        // the crop reads only some slowest-axis planes: inverse-FFT just those in 2D
+        if (p->bres_planes.empty()) p->bres_planes = index_runs(p->tab_idx.p, rax[0].N, false, s);
+        {
+            StageScope st(p->timer, "transpose_ifft", s);
+            fft3_pruned(p->fft, p->big.p, kd3, nch, p->bres_planes, CUFFT_INVERSE, s);
+        }
+        StageScope st(p->timer, "transpose_crop", s);
         launch_remap<float2, kAccumC>(3, p->big.p, acc_num, ax, 1.0f, s);
         CBN_LAUNCH_CHECK();
         if (need_den) {

@@ -789,8 +789,16 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
     }
     long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
     if (phi_fast) std::swap(kd[0], kd[2]);
+    // the zero padding leaves whole slowest-axis planes empty: skip their 2D FFTs
+    const int slow = phi_fast ? 2 : 0;
+    if (p->fres_planes.empty() || p->fres_planes_slow != slow) {
+        size_t o = 0;
+        for (int d = 0; d < slow; ++d) o += ax[d].K;
+        p->fres_planes = index_runs(p->tab_idx.p + o, ax[slow].K, true, s);
+        p->fres_planes_slow = slow;
+    }
     StageScope st(p->timer, "resample_fft", s);
-    p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+    fft3_pruned(p->fft, p->big.p, kd, 1, p->fres_planes, CUFFT_FORWARD, s);
 }
 
 // views-in-lanes path applies when every view's targets are view 0's shifted by

@@ -105,6 +105,8 @@ struct cbn_projector_s {
     int fpad = 0;
     bool fw_built = false;
     cbn::BatchPlan fbatch;
+    std::vector<std::pair<int, int>> fres_planes;   // non-zero slowest-axis planes of the resample grid
+    int fres_planes_slow = -1;
     cbn::BinPlan fspec_bins;     // radial nodes sorted by spectrum-grid tile
     bool fspec_fit = false;
     cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT
@@ -118,6 +120,7 @@ struct cbn_projector_s {
     int bpad = 0;
     bool bw_built = false;
     cbn::BatchPlan bbatch;
+    std::vector<std::pair<int, int>> bres_planes;   // slowest-axis planes the transpose crop reads
     cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
     bool bspec_fit = false;
     cbn::DevBuf<float> bspec_s32;   // cached first-sub-plan scaling of the 3D adjoint

@@ -1,5 +1,6 @@
 #include "cbn_runtime.h"
 
+#include <algorithm>
 #include <cstring>
 
 namespace cbn {
@@ -102,6 +103,44 @@ void FFTCache::exec(cufftHandle h, void* in, void* out, int direction, cudaStrea
     CBN_CUFFT(cufftSetStream(h, s));
     CBN_CUFFT(cufftExecC2C(h, static_cast<cufftComplex*>(in), static_cast<cufftComplex*>(out),
                            direction));
+}
+
+std::vector<std::pair<int, int>> index_runs(const int* idx_dev, int n, bool positions, cudaStream_t s) {
+    std::vector<int> h((size_t)n);
+    CBN_CUDA(cudaMemcpyAsync(h.data(), idx_dev, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> ks;
+    for (int k = 0; k < n; ++k)
+        if (h[(size_t)k] >= 0) ks.push_back(positions ? k : h[(size_t)k]);
+    std::sort(ks.begin(), ks.end());
+    ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+    std::vector<std::pair<int, int>> runs;
+    for (int k : ks) {
+        if (!runs.empty() && runs.back().second == k) ++runs.back().second;
+        else runs.emplace_back(k, k + 1);
+    }
+    return runs;
+}
+
+void fft3_pruned(FFTCache& fft, float2* g, const long long* kd, long long nbatch,
+                 const std::vector<std::pair<int, int>>& planes, int direction, cudaStream_t s) {
+    const long long plane = kd[1] * kd[2], total = kd[0] * plane;
+    const long long k2[2] = {kd[1], kd[2]};
+    cufftHandle col = fft.get_strided(kd[0], plane, plane, 1);
+    for (long long b = 0; b < nbatch; ++b) {
+        float2* gb = g + b * total;
+        if (direction == CUFFT_FORWARD) {
+            for (const auto& r : planes)
+                fft.exec(fft.get(2, k2, r.second - r.first), gb + r.first * plane,
+                         gb + r.first * plane, direction, s);
+            fft.exec(col, gb, gb, direction, s);
+        } else {
+            fft.exec(col, gb, gb, direction, s);
+            for (const auto& r : planes)
+                fft.exec(fft.get(2, k2, r.second - r.first), gb + r.first * plane,
+                         gb + r.first * plane, direction, s);
+        }
+    }
 }
 
 StageTimer::~StageTimer() {

@@ -111,6 +111,19 @@ private:
                      cufftType type = CUFFT_C2C);
 };
 
+// [a, b) runs of grid indices taken from a remap table idx[0..n) (device array,
+// copied to the host): positions=true -> the k with idx[k] >= 0 (a pad table's
+// written cells); false -> the distinct values idx[k] >= 0 (a crop table's reads)
+std::vector<std::pair<int, int>> index_runs(const int* idx_dev, int n, bool positions, cudaStream_t s);
+
+// 3D C2C FFT of nbatch contiguous grids kd[0] x kd[1] x kd[2] when only the
+// slowest-axis planes in `planes` matter on the sparse side: forward, the
+// other planes are zero on input (2D FFTs of the listed planes, then the 1D
+// FFT along the slowest axis); inverse, only the listed planes are read
+// afterwards (1D FFT along the slowest axis, then 2D FFTs of those planes).
+void fft3_pruned(FFTCache& fft, float2* g, const long long* kd, long long nbatch,
+                 const std::vector<std::pair<int, int>>& planes, int direction, cudaStream_t s);
+
 // Per-stage CUDA-event timing (enabled per plan; off by default).
 class StageTimer {
 public:
