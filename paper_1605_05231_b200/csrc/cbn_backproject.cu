@@ -11,8 +11,11 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
+#include <numeric>
 
 #include "cbn_projector.h"
+#include "cbn_resample_views.cuh"
 
 namespace cbn {
 
@@ -272,14 +275,60 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     float2* acc_num = p->padded.p;
     float2* acc_den = need_den ? p->padded.p + dsize : nullptr;
     CBN_CUDA(cudaMemsetAsync(p->padded.p, 0, sizeof(float2) * nch * dsize, s));
-    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
     const int64_t per_view = (int64_t)u.n_mu * u.n_t;
     const int nu = p->g.nu, nv = p->g.nv;
     p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
     KBSet kbr;
     for (int d = 0; d < 3; ++d) kbr.ax[d] = rax[d].kb;
+    // views in lanes (as the forward gather): when view k's targets are view 0's
+    // shifted by whole oversampled phi cells, the transposed grid is stored
+    // phi-fastest [rho][theta][phi] and built by the column gather
+    // (k_rs_gather_cols) instead of the atomic scatter
+    const char* no_lanes = std::getenv("CBN_NO_VIEW_LANES");
+    const bool lanes = !(no_lanes && no_lanes[0] == '1') && rax[0].J == 3 &&
+                       (2LL * r.n_phi) % p->g.n_views == 0 && rax[0].K == 2 * r.n_phi;
+    const int shift = (int)(2LL * r.n_phi / p->g.n_views);
     long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
-    const int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
+    int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
+    if (lanes) {
+        kd3[0] = rax[2].K;
+        kd3[2] = rax[0].K;
+        sstr[0] = 1;
+        sstr[1] = rax[0].K;
+        sstr[2] = (int64_t)rax[1].K * rax[0].K;
+        if (!p->bcol_ptr.p) {
+            // plan step: view-0 taps, then the per-column CSR of (target, tap) entries
+            UmbrellaSrc src0 = projector_cached_umbrella(p, p->bumb, r, p->bpad, 0, s);
+            KBSet kb;
+            kb.ax[0] = rax[2].kb;
+            kb.ax[1] = rax[1].kb;
+            kb.ax[2] = rax[0].kb;
+            const int64_t n = per_view;
+            DevBuf<RsTap<3>> taps((size_t)n);
+            k_rs_taps<3><<<blocks_for(n, 256), 256, 0, s>>>(src0, kb, n, taps.p);
+            CBN_LAUNCH_CHECK();
+            const int64_t ncol = kd3[0] * kd3[1];
+            DevBuf<int> counts((size_t)ncol);
+            CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncol, s));
+            k_rs_col_count<3><<<blocks_for(n, 256), 256, 0, s>>>(taps.p, n, (int)kd3[0], (int)kd3[1],
+                                                                counts.p);
+            CBN_LAUNCH_CHECK();
+            std::vector<int> h((size_t)ncol + 1, 0);
+            CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncol, cudaMemcpyDeviceToHost, s));
+            CBN_CUDA(cudaStreamSynchronize(s));
+            std::partial_sum(h.begin(), h.end(), h.begin());
+            p->bcol_ptr.upload(h.data(), h.size(), s);
+            p->bcol_ent.alloc(sizeof(RsColEntry) * (size_t)std::max(h.back(), 1));
+            CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncol, cudaMemcpyHostToDevice, s));
+            k_rs_col_fill<3><<<blocks_for(n, 256), 256, 0, s>>>(
+                taps.p, n, (int)kd3[0], (int)kd3[1], counts.p,
+                reinterpret_cast<RsColEntry*>(p->bcol_ent.p));
+            CBN_LAUNCH_CHECK();
+            CBN_CUDA(cudaStreamSynchronize(s));
+        }
+    }
+    const int slow_axis = lanes ? 2 : 0;
+    if (!lanes) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
 
     // transposed resample of one group of batches sharing a scaling: one
     // inverse FFT of the summed spreads, crop * scaling, accumulate
@@ -296,7 +345,12 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
             off += rax[d].N;
         }
         // the crop reads only some slowest-axis planes: inverse-FFT just those in 2D
-        if (p->bres_planes.empty()) p->bres_planes = index_runs(p->tab_idx.p, rax[0].N, false, s);
+        if (p->bres_planes.empty() || p->bres_planes_slow != slow_axis) {
+            size_t o = 0;
+            for (int d = 0; d < slow_axis; ++d) o += rax[d].N;
+            p->bres_planes = index_runs(p->tab_idx.p + o, rax[slow_axis].N, false, s);
+            p->bres_planes_slow = slow_axis;
+        }
         {
             StageScope st(p->timer, "transpose_ifft", s);
             fft3_pruned(p->fft, p->big.p, kd3, nch, p->bres_planes, CUFFT_INVERSE, s);
@@ -308,11 +362,47 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
             launch_remap<float2, kAccumC>(3, p->big.p + kres, acc_den, ax, 1.0f, s);
             CBN_LAUNCH_CHECK();
         }
-        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
+        if (!lanes) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
     };
 
+    if (lanes) {
+        // runs of consecutive batches sharing a scaling group: forward Grangeat
+        // of the run's views, target-major transpose, column gather, flush
+        const size_t nbat = bp.batches.size();
+        size_t bi = 0;
+        while (bi < nbat) {
+            const int g = bp.group[bi];
+            size_t e = bi + 1;
+            while (e < nbat && bp.group[e] == g) ++e;
+            const int vlo = bp.batches[bi].first, vhi = bp.batches[e - 1].second;
+            const int nvr = vhi - vlo;
+            p->values.ensure((size_t)per_view * nvr);
+            p->values_t.ensure((size_t)per_view * nvr);
+            for (int v0 = 0; v0 < nvr; v0 += 32) {
+                StageScope st(p->timer, "grangeat_forward", s);
+                const int nb = std::min(32, nvr - v0);
+                grangeat_forward_block(p, frames + (size_t)(vlo + v0) * nu * nv, nb,
+                                       p->values.p + (size_t)v0 * per_view, s);
+            }
+            {
+                StageScope st(p->timer, "transpose_spread", s);
+                dim3 tg((unsigned)((per_view + 31) / 32), (unsigned)((nvr + 31) / 32));
+                k_transpose_vals<<<tg, 256, 0, s>>>(p->values.p, nvr, per_view, p->values_t.p);
+                CBN_LAUNCH_CHECK();
+                CBN_REQUIRE(kd3[2] <= kRsColMaxPhi, "phi extent above the column-gather limit");
+                k_rs_gather_cols<<<(unsigned)(kd3[0] * kd3[1]), kRsColThreads, 0, s>>>(
+                    p->big.p, need_den ? p->big.p + kres : nullptr, (int)kd3[2], p->bcol_ptr.p,
+                    reinterpret_cast<const RsColEntry*>(p->bcol_ent.p), p->values_t.p, vlo, nvr,
+                    shift);
+                CBN_LAUNCH_CHECK();
+            }
+            flush(g);
+            bi = e;
+        }
+    }
+
     int cur = -1;
-    for (size_t bi = 0; bi < bp.batches.size(); ++bi) {
+    for (size_t bi = 0; !lanes && bi < bp.batches.size(); ++bi) {
         const auto& b = bp.batches[bi];
         const int g = bp.group[bi];
         if (cur >= 0 && g != cur) flush(cur);

@@ -15,6 +15,7 @@
 #include <memory>
 
 #include "cbn_projector.h"
+#include "cbn_resample_views.cuh"
 
 using namespace cbn;
 
@@ -137,39 +138,6 @@ struct UmbOut {
 // the rho/theta taps and index math are warp-uniform and the phi taps of
 // the lanes are consecutive cells.  32 base targets per CTA; values are
 // transposed through shared memory so each view's row is stored coalesced.
-// Taps of one base-view (view 0) umbrella target in grid order (rho, theta,
-// phi): view v's phi taps are these shifted by v * (2 n_phi / V) cells with the
-// same weights (u_phi(v) = u_phi(0) - 2 v n_phi / V exactly), so the per-view
-// kernel does no index math at all.
-template <int J>
-struct RsTap {
-    int f[3];       // first tap per axis, wrapped into [0, K)
-    int valid;
-    float w[3][J];
-};
-
-template <int J>
-__global__ void k_rs_taps(UmbrellaSrc src, KBSet kb, int64_t n, RsTap<J>* __restrict__ out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double wd[3];
-    UmbrellaSrc::Aux aux;
-    src.node(i, wd, aux);                               // device order (phi, theta, rho)
-    const double w[3] = {wd[2], wd[1], wd[0]};          // grid order (rho, theta, phi)
-    int first[3];
-    float wt[3][J];
-    tap_setup<3, J>(kb, w, first, wt);
-    RsTap<J> t;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        t.f[d] = wrapc(first[d], kb.ax[d].K);
-#pragma unroll
-        for (int p = 0; p < J; ++p) t.w[d][p] = wt[d][p];
-    }
-    t.valid = aux.valid ? 1 : 0;
-    out[i] = t;
-}
-
 template <int J>
 __global__ void __launch_bounds__(256)
 k_resample_views(const float2* __restrict__ G, int K0, int K1, int K2,

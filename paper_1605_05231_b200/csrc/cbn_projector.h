@@ -121,6 +121,10 @@ struct cbn_projector_s {
     bool bw_built = false;
     cbn::BatchPlan bbatch;
     std::vector<std::pair<int, int>> bres_planes;   // slowest-axis planes the transpose crop reads
+    int bres_planes_slow = -1;
+    cbn::DevBuf<int> bcol_ptr;      // transposed-resample CSR: column -> entries (views in lanes)
+    cbn::DevBuf<char> bcol_ent;     // RsColEntry per (target, rho tap, theta tap)
+    cbn::DevBuf<float> values_t;    // umbrella values of a view run, target-major
     cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
     bool bspec_fit = false;
     cbn::DevBuf<float> bspec_s32;   // cached first-sub-plan scaling of the 3D adjoint

@@ -1,0 +1,160 @@
+// Views-in-lanes resampling records shared by the forward gather
+// (cbn_projector.cu) and the backprojector's transposed spread
+// (cbn_backproject.cu).
+#pragma once
+
+#include "cbn_kernels.cuh"
+#include "cbn_sources.cuh"
+
+namespace cbn {
+
+// Taps of one base-view (view 0) umbrella target in grid order (rho, theta,
+// phi): view v's phi taps are these shifted by v * (2 n_phi / V) cells with the
+// same weights (u_phi(v) = u_phi(0) - 2 v n_phi / V exactly), so the per-view
+// kernel does no index math at all.
+template <int J>
+struct RsTap {
+    int f[3];       // first tap per axis, wrapped into [0, K)
+    int valid;
+    float w[3][J];
+};
+
+template <int J>
+__global__ void k_rs_taps(UmbrellaSrc src, KBSet kb, int64_t n, RsTap<J>* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double wd[3];
+    UmbrellaSrc::Aux aux;
+    src.node(i, wd, aux);                               // device order (phi, theta, rho)
+    const double w[3] = {wd[2], wd[1], wd[0]};          // grid order (rho, theta, phi)
+    int first[3];
+    float wt[3][J];
+    tap_setup<3, J>(kb, w, first, wt);
+    RsTap<J> t;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        t.f[d] = wrapc(first[d], kb.ax[d].K);
+#pragma unroll
+        for (int p = 0; p < J; ++p) t.w[d][p] = wt[d][p];
+    }
+    t.valid = aux.valid ? 1 : 0;
+    out[i] = t;
+}
+
+// ----------------------------------------------------------------------
+// Transposed resample (resample_transpose, pipeline.py:183-184) as a gather.
+// With views in lanes the transpose is a scatter of 283 M targets x 27 taps
+// of fp32 REDs per step at config 2, bound by L2 atomic element throughput
+// (consecutive-address REDs from views-in-lanes measured slower still).  The
+// targets of view v are view 0's shifted by v * shift phi cells, so a grid
+// column (rho, theta) of the phi-fast grid receives exactly the view-0
+// targets whose rho/theta taps cover it, each at every view: a per-plan CSR
+// of (target, rho/theta weight) entries per column turns the transpose into
+// a gather with one thread per phi cell, register accumulation, and one
+// plain store of every grid cell (no atomics, no memset).
+struct RsColEntry {
+    int t;          // view-0 target (row of the transposed values)
+    int f2;         // first phi tap of view 0
+    float wab;      // rho x theta weight of this column
+    float w2[3];    // phi weights (J = 3)
+};
+
+template <int J>
+__global__ void k_rs_col_count(const RsTap<J>* __restrict__ taps, int64_t n, int K0, int K1,
+                               int* __restrict__ counts) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const RsTap<J> tp = taps[t];
+    if (!tp.valid) return;
+#pragma unroll
+    for (int a = 0; a < J; ++a)
+#pragma unroll
+        for (int b = 0; b < J; ++b)
+            atomicAdd(counts + (size_t)wrapc(tp.f[0] + a, K0) * K1 + wrapc(tp.f[1] + b, K1), 1);
+}
+
+template <int J>
+__global__ void k_rs_col_fill(const RsTap<J>* __restrict__ taps, int64_t n, int K0, int K1,
+                              int* __restrict__ cursor, RsColEntry* __restrict__ out) {
+    static_assert(J == 3, "column entries hold three phi weights");
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const RsTap<J> tp = taps[t];
+    if (!tp.valid) return;
+#pragma unroll
+    for (int a = 0; a < J; ++a)
+#pragma unroll
+        for (int b = 0; b < J; ++b) {
+            const size_t col = (size_t)wrapc(tp.f[0] + a, K0) * K1 + wrapc(tp.f[1] + b, K1);
+            RsColEntry e;
+            e.t = (int)t;
+            e.f2 = tp.f[2];
+            e.wab = tp.w[0][a] * tp.w[1][b];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) e.w2[c] = tp.w[2][c];
+            out[atomicAdd(cursor + col, 1)] = e;
+        }
+}
+
+// vals [nv][n] -> valsT [n][nv]
+static __global__ void k_transpose_vals(const float* __restrict__ in, int nv, int64_t n,
+                                 float* __restrict__ out) {
+    __shared__ float tile[32][33];
+    const int64_t t0 = (int64_t)blockIdx.x * 32;
+    const int v0 = blockIdx.y * 32;
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+        const int v = e >> 5, tt = e & 31;
+        if (v0 + v < nv && t0 + tt < n) tile[v][tt] = in[(size_t)(v0 + v) * n + t0 + tt];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+        const int tt = e >> 5, v = e & 31;
+        if (v0 + v < nv && t0 + tt < n) out[(size_t)(t0 + tt) * nv + v0 + v] = tile[v][tt];
+    }
+}
+
+// One CTA per grid column (rho, theta); threads over phi.  Views [vlo, vlo+nv)
+// of valsT [target][nv]; writes (num, 0) -- and (den, 0) if gden -- to every
+// cell of the column.
+constexpr int kRsColThreads = 256;
+constexpr int kRsColMaxPhi = 3 * kRsColThreads;
+
+static __global__ void __launch_bounds__(kRsColThreads)
+k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
+                 const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
+                 const float* __restrict__ valsT, int vlo, int nv, int shift) {
+    const size_t col = blockIdx.x;
+    const int beg = col_ptr[col], end = col_ptr[col + 1];
+    float num[3] = {0.f, 0.f, 0.f}, den[3] = {0.f, 0.f, 0.f};
+    for (int k = beg; k < end; ++k) {
+        const RsColEntry e = ent[k];
+        const float* vt = valsT + (size_t)e.t * nv;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const int phi = threadIdx.x + r * kRsColThreads;
+            if (phi >= K2) break;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                // view v covers phi = f2 - v shift + c  (mod K2)
+                int d = e.f2 + c - phi;
+                d = d < 0 ? d + K2 : (d >= K2 ? d - K2 : d);
+                const int v = d / shift;
+                const int rel = v - vlo;
+                if (v * shift == d && rel >= 0 && rel < nv) {
+                    const float wk = e.wab * e.w2[c];
+                    num[r] = fmaf(wk, __ldg(vt + rel), num[r]);
+                    den[r] += wk;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int phi = threadIdx.x + r * kRsColThreads;
+        if (phi >= K2) break;
+        gnum[col * K2 + phi] = make_float2(num[r], 0.f);
+        if (gden) gden[col * K2 + phi] = make_float2(den[r], 0.f);
+    }
+}
+
+}  // namespace cbn
