@@ -389,11 +389,18 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
                 dim3 tg((unsigned)((per_view + 31) / 32), (unsigned)((nvr + 31) / 32));
                 k_transpose_vals<<<tg, 256, 0, s>>>(p->values.p, nvr, per_view, p->values_t.p);
                 CBN_LAUNCH_CHECK();
-                CBN_REQUIRE(kd3[2] <= kRsColMaxPhi, "phi extent above the column-gather limit");
-                k_rs_gather_cols<<<(unsigned)(kd3[0] * kd3[1]), kRsColThreads, 0, s>>>(
-                    p->big.p, need_den ? p->big.p + kres : nullptr, (int)kd3[2], p->bcol_ptr.p,
-                    reinterpret_cast<const RsColEntry*>(p->bcol_ent.p), p->values_t.p, vlo, nvr,
-                    shift);
+                const unsigned ncol = (unsigned)(kd3[0] * kd3[1]);
+                const RsColEntry* ent = reinterpret_cast<const RsColEntry*>(p->bcol_ent.p);
+                if (shift == 2 && p->g.n_views <= kRsPairThreads) {
+                    k_rs_gather_cols2<<<ncol, kRsPairThreads, 0, s>>>(
+                        p->big.p, need_den ? p->big.p + kres : nullptr, p->g.n_views,
+                        p->bcol_ptr.p, ent, p->values_t.p, vlo, nvr);
+                } else {
+                    CBN_REQUIRE(kd3[2] <= kRsColMaxPhi, "phi extent above the column-gather limit");
+                    k_rs_gather_cols<<<ncol, kRsColThreads, 0, s>>>(
+                        p->big.p, need_den ? p->big.p + kres : nullptr, (int)kd3[2], p->bcol_ptr.p,
+                        ent, p->values_t.p, vlo, nvr, shift);
+                }
                 CBN_LAUNCH_CHECK();
             }
             flush(g);

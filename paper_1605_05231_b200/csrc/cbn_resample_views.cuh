@@ -157,4 +157,54 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
     }
 }
 
+// shift = 2 (K2 = 2 V, configs 2 and 3): thread i owns the cell pair
+// (2i, 2i+1).  With d = f2 - 2i and base = floor(d / 2), the three phi taps of
+// an entry land as
+//   d even: cell 2i   <- w0 val[base] + w2 val[base+1],  cell 2i+1 <- w1 val[base]
+//   d odd:  cell 2i+1 <- w0 val[base] + w2 val[base+1],  cell 2i   <- w1 val[base+1]
+// so every entry costs two value loads and three FMAs per thread, no search.
+constexpr int kRsPairThreads = 384;
+
+static __global__ void __launch_bounds__(kRsPairThreads)
+k_rs_gather_cols2(float2* __restrict__ gnum, float2* __restrict__ gden, int V,
+                  const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
+                  const float* __restrict__ valsT, int vlo, int nv) {
+    const size_t col = blockIdx.x;
+    const int i = threadIdx.x;
+    if (i >= V) return;
+    const int beg = col_ptr[col], end = col_ptr[col + 1];
+    float ne = 0.f, no = 0.f, de = 0.f, dn = 0.f;
+    for (int k = beg; k < end; ++k) {
+        const RsColEntry e = ent[k];
+        const int d = e.f2 - 2 * i;
+        int b0 = d >> 1;                       // floor(d / 2)
+        b0 += b0 < 0 ? V : 0;
+        int b1 = b0 + 1;
+        b1 -= b1 >= V ? V : 0;
+        int r0 = b0 - vlo, r1 = b1 - vlo;
+        r0 += r0 < 0 ? V : 0;
+        r1 += r1 < 0 ? V : 0;
+        const bool ok0 = r0 < nv, ok1 = r1 < nv;
+        const float* vt = valsT + (size_t)e.t * nv;
+        const float x0 = ok0 ? __ldg(vt + r0) : 0.f;
+        const float x1 = ok1 ? __ldg(vt + r1) : 0.f;
+        const float u0 = ok0 ? 1.f : 0.f, u1 = ok1 ? 1.f : 0.f;
+        const float w0 = e.wab * e.w2[0], w1 = e.wab * e.w2[1], w2 = e.wab * e.w2[2];
+        if ((d & 1) == 0) {
+            ne = fmaf(w0, x0, fmaf(w2, x1, ne));
+            no = fmaf(w1, x0, no);
+            de = fmaf(w0, u0, fmaf(w2, u1, de));
+            dn = fmaf(w1, u0, dn);
+        } else {
+            no = fmaf(w0, x0, fmaf(w2, x1, no));
+            ne = fmaf(w1, x1, ne);
+            dn = fmaf(w0, u0, fmaf(w2, u1, dn));
+            de = fmaf(w1, u1, de);
+        }
+    }
+    float4* gn = reinterpret_cast<float4*>(gnum + col * 2 * V) + i;
+    *gn = make_float4(ne, 0.f, no, 0.f);
+    if (gden) *(reinterpret_cast<float4*>(gden + col * 2 * V) + i) = make_float4(de, 0.f, dn, 0.f);
+}
+
 }  // namespace cbn

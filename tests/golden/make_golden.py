@@ -180,6 +180,11 @@ def main():
                             **pipeline_small(16, 8, 21, "trilinear"))
         np.savez_compressed(os.path.join(HERE, "pipeline_n12_v48.npz"),
                             **pipeline_small(12, 48, 22, "trilinear"))
+    if "small" in which or "rot2" in which:
+        # 2 n_phi / V = 2 (as configs 2 and 3): the paired column gather of the
+        # backprojector's transposed resample
+        np.savez_compressed(os.path.join(HERE, "pipeline_n12_v24.npz"),
+                            **pipeline_small(12, 24, 23, "trilinear"))
     if "big" in which:
         np.savez_compressed(os.path.join(HERE, "config0.npz"), **config0())
 

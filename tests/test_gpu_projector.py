@@ -125,9 +125,11 @@ def test_config0_forward_and_config1_backproject(pl):
     assert err < TOL, err
 
 
-@pytest.mark.parametrize("name", ["pipeline_n16_v8", "pipeline_n12_v48"])
+@pytest.mark.parametrize("name", ["pipeline_n16_v8", "pipeline_n12_v48", "pipeline_n12_v24"])
 def test_rotation_aligned_geometries(pl, name):
-    """2 n_phi / V integer: the views-in-lanes resample gather (k_resample_views)."""
+    """2 n_phi / V integer: the views-in-lanes resample gather (k_resample_views) and the
+    backprojector's column gather (k_rs_gather_cols; k_rs_gather_cols2 when 2 n_phi / V = 2,
+    as at configs 2 and 3), with one and with several view batches."""
     from paper_1605_05231_b200.grangeat import DetectorFrame
     from paper_1605_05231_b200.phantom import Volume3D
     g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
@@ -138,6 +140,13 @@ def test_rotation_aligned_geometries(pl, name):
     assert err < TOL, err
     fr = [DetectorFrame(k, g["frames"][k], geom.pixel_mm) for k in range(views)]
     err = rel_l2(pl.nufft_backproject(fr, geom, cfg, n, voxel).data, g["bp"])
+    assert err < TOL, err
+    saved = pl._TARGET_BATCH
+    try:
+        pl._TARGET_BATCH = 4096
+        err = rel_l2(pl.nufft_backproject(fr, geom, cfg, n, voxel).data, g["bp_b4"])
+    finally:
+        pl._TARGET_BATCH = saved
     assert err < TOL, err
 
 
