@@ -33,10 +33,12 @@ sys.path.insert(0, REPO)
 PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 # dram__bytes_read.sum + dram__bytes_write.sum per config-2 step, summed over
-# the stage's launches, from the committed ncu launch list
-# (profiles/r1a_launches_fwd.txt); stages not captured there report null
-TRAFFIC: dict = {"resample_gather": 14.581e9, "grangeat_spread": 4.195e9,
-                 "spectrum_gather": 1.027e9}
+# the stage's launches, from the committed ncu launch lists
+# (profiles/r1c_launches_fwd.txt, profiles/r1c_launches_bp.txt); stages not
+# captured there report null
+TRAFFIC: dict = {"resample_gather": 2.487e9, "grangeat_spread": 3.703e9,
+                 "spectrum_gather": 1.037e9, "bp_spread": 1.079e9,
+                 "transpose_spread": 2.230e9 + 0.725e9}
 
 
 def parse_args():
@@ -134,6 +136,10 @@ def stage_bytes(stage: str, w, views: int):
         return 8.0 * Kr + 4.0 * tpv * views + 32.0 * tpv, 8.0 * Jr ** 3 * tpv * views
     if stage == "grangeat_spread":             # read t-spectra, RED the 2D grids once
         return 8.0 * tpv * views + 8.0 * grid2 * views + 56.0 * tpv, 16.0 * Jg ** 2 * tpv * views
+    if stage == "bp_spread":                   # read M lattice values, write K^3 grid once
+        return 8.0 * M + 8.0 * K3, 16.0 * J ** 3 * M
+    if stage == "transpose_spread":            # transpose + gather: values 3x, grid once
+        return 3 * 4.0 * tpv * views + 8.0 * Kr, 4.0 * Jr ** 3 * tpv * views
     if stage == "spectrum_pad":
         return 4.0 * n ** 3 + 8.0 * K3, 0.0
     if stage == "resample_pad":
@@ -460,8 +466,8 @@ def run_nufft4(args):
                   "onchip_tbs": round(8.0 * taps * m / t2 / 1e9, 2),
                   "msamples_s": round(m / t2 / 1e3, 2)},
         "type1": {"ms_per_step": round(t1, 3), "achieved_gbs": round(gb["type1_step"] / t1 / 1e6, 1),
-                  "onchip_tap_bytes": 8.0 * taps * m,
-                  "onchip_tbs": round(8.0 * taps * m / t1 / 1e9, 2),
+                  "onchip_tap_bytes": 16.0 * taps * m,          # shared-memory read + write per tap
+                  "onchip_tbs": round(16.0 * taps * m / t1 / 1e9, 2),
                   "msamples_s": round(m / t1 / 1e3, 2)},
     }
     st = "type1" if t1 >= t2 else "type2"
