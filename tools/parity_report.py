@@ -34,7 +34,8 @@ def main():
     print()
     print(f"{'projector case':34s} {'forward rel L2':>15s} {'worst view':>11s} {'backproject':>12s}")
     cases = [("pipeline_n16", 16, 12, "trilinear"), ("pipeline_n12_dirac", 12, 8, "dirac"),
-             ("pipeline_n16_v8", 16, 8, "trilinear"), ("pipeline_n12_v48", 12, 48, "trilinear")]
+             ("pipeline_n16_v8", 16, 8, "trilinear"), ("pipeline_n12_v48", 12, 48, "trilinear"),
+             ("pipeline_n12_v24", 12, 24, "trilinear")]
     for name, n, views, basis in cases:
         g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
         geom, voxel, spec, cfg = small_setup(n, views, basis)
@@ -52,6 +53,17 @@ def main():
     bp = pl.nufft_backproject(frames, geom, cfg, 64, voxel).data
     print(f"{'config0 fwd / config1 bp (64^3, 90v)':34s} {rel_l2(fr, z['frames']):15.2e} {worst:11.2e} "
           f"{rel_l2(bp, z['bp']):12.2e}")
+    # config 4 shapes: 256^3 grid, 1M float32 points, J=8, against the direct DFT
+    import cbn_oracle as orc
+    from paper_1605_05231_b200.workloads import config4_inputs
+    x, pts = config4_inputs(n_points=1 << 20)
+    plan = nufft.plan_nufft(x.shape, pts, 2.0, 8)
+    y = nufft.nufft_forward(plan, x)
+    sel = np.random.default_rng(7).choice(pts.shape[0], 2000, replace=False)
+    ref = orc.separable_dft(x.astype(np.complex128), orc.wrap(pts[sel].astype(np.float64)))
+    print()
+    print(f"config 4 shapes (256^3, 1M fp32 points, J=8): type-2 vs direct DFT at 2000 points "
+          f"{rel_l2(y[sel], ref):.2e}")
 
 
 if __name__ == "__main__":
