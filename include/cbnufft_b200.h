@@ -80,8 +80,8 @@ int cbn_nufft_type1(cbn_nufft* plan, const void* y, void* x, void* stream);
 int cbn_nufft_set_phase(cbn_nufft* plan, int32_t on);
 
 /* ------------------------------------------------------------ resampling
- * plan_resample / resample_apply / resample_transpose, method A
- * (resampling.py:79-103,136-148,164-196).  targets [host] m x 3 float64
+ * plan_resample / resample_apply / resample_transpose, methods A and B
+ * (resampling.py:79-103,136-161,164-196).  targets [host] m x 3 float64
  * fractional lattice indices (rho, theta, phi); lattice arrays [device]
  * complex64 in the reference layout (n_rho, n_theta, n_phi).
  */
@@ -90,6 +90,12 @@ int cbn_resample_create(cbn_resample** plan, int32_t n_rho, int32_t n_theta, int
                         int32_t rho_pad, const int32_t* taps, double oversample_factor,
                         const double* targets, int64_t m, const int64_t* ls_rows, int64_t n_ls,
                         void* stream);
+/* method B (resampling.py:126-161,164-196): truncated centred periodic sinc,
+ * side_lobes + 1 taps per axis on the rho-padded lattice itself; the plan
+ * keeps only the targets */
+int cbn_resample_create_b(cbn_resample** plan, int32_t n_rho, int32_t n_theta, int32_t n_phi,
+                          int32_t rho_pad, int32_t side_lobes, const double* targets, int64_t m,
+                          void* stream);
 int cbn_resample_destroy(cbn_resample* plan);
 int cbn_resample_apply(cbn_resample* plan, const void* lattice, void* values, void* stream);
 int cbn_resample_transpose(cbn_resample* plan, const void* values, void* lattice, void* stream);
@@ -116,14 +122,14 @@ typedef struct {
 } cbn_radial_spec;
 
 typedef struct {
-    int32_t method;            /* 0 = 'a' (only method implemented on device) */
+    int32_t method;            /* 0 = 'a' (NUFFT resample), 1 = 'b' (periodic sinc) */
     cbn_radial_spec spec;
     int32_t n_mu, n_t;
     double t_pitch_mm;         /* <= 0 : None (virtual pixel pitch) */
     int32_t t_taper;           /* 0 = none, 1 = hann */
     int32_t spectrum_j;
     int32_t resample_j[3];
-    int32_t side_lobes;
+    int32_t side_lobes;        /* method 'b': side_lobes + 1 taps per axis */
     double oversample_factor;
     int32_t rho_pad;           /* < 0 : None (n_rho / 2) */
     int32_t basis;             /* 0 = trilinear, 1 = dirac */

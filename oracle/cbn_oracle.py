@@ -472,6 +472,62 @@ def resample_adjoint(rs: Resampler, values):
     return origin_average(g, rs.spec)
 
 
+def dirichlet(t, n: int):
+    """Periodic interpolating kernel (nufft.py:285-298): phasor x periodic sinc."""
+    t = np.asarray(t, dtype=np.float64)
+    phase = np.exp(1j * np.pi * t * (n - 1) / n)
+    den = n * np.sin(np.pi * t / n)
+    near = np.abs(den) < 1e-9
+    ratio = np.where(near, np.cos(np.pi * t) / np.cos(np.pi * t / n),
+                     np.sin(np.pi * t) / np.where(near, 1.0, den))
+    return phase * ratio
+
+
+def b_axis_taps(pos, dim: int, taps: int):
+    """The `taps` nearest centred periodic-sinc taps of one axis (resampling.py:126-133)."""
+    first = np.ceil(pos - taps / 2.0)
+    offs = first[:, None] + np.arange(taps)[None, :]
+    t = pos[:, None] - offs
+    w = dirichlet(t, dim) * np.exp(-2j * np.pi * (dim // 2) * t / dim)
+    return np.mod(offs.astype(np.int64), dim), w
+
+
+def _b_index(spec, targets, rho_pad, side_lobes):
+    n_r, n_t, n_p = int(spec.n_rho), int(spec.n_theta), int(spec.n_phi)
+    pad = n_r // 2 if rho_pad is None else int(rho_pad)
+    dims = (n_r + 2 * pad, n_t, n_p)
+    pos = np.atleast_2d(np.asarray(targets, dtype=np.float64)).copy()
+    pos[:, 0] += pad
+    taps = side_lobes + 1
+    c0, w0 = b_axis_taps(pos[:, 0], dims[0], taps)
+    c1, w1 = b_axis_taps(pos[:, 1], dims[1], taps)
+    c2, w2 = b_axis_taps(pos[:, 2], dims[2], taps)
+    idx = (c0[:, :, None, None] * dims[1] + c1[:, None, :, None]) * dims[2] + c2[:, None, None, :]
+    return pad, dims, idx, (w0, w1, w2)
+
+
+def resample_b_forward(spec, targets, lattice, rho_pad=None, side_lobes=2):
+    """resample_apply, method B (resampling.py:149-161)."""
+    pad, dims, idx, (w0, w1, w2) = _b_index(spec, targets, rho_pad, side_lobes)
+    x = origin_average(np.asarray(lattice, dtype=np.complex128), spec)
+    if pad:
+        x = np.pad(x, ((pad, pad), (0, 0), (0, 0)))
+    return np.einsum("ma,mb,mc,mabc->m", w0, w1, w2, x.ravel()[idx])
+
+
+def resample_b_adjoint(spec, targets, values, rho_pad=None, side_lobes=2):
+    """resample_transpose, method B (resampling.py:176-196)."""
+    pad, dims, idx, (w0, w1, w2) = _b_index(spec, targets, rho_pad, side_lobes)
+    vals = np.einsum("m,ma,mb,mc->mabc", np.asarray(values, dtype=np.complex128),
+                     np.conj(w0), np.conj(w1), np.conj(w2))
+    flat = np.zeros(int(np.prod(dims)), dtype=np.complex128)
+    np.add.at(flat, idx.ravel(), vals.ravel())
+    g = flat.reshape(dims)
+    if pad:
+        g = g[pad:pad + int(spec.n_rho)]
+    return origin_average(g, spec)
+
+
 # --------------------------------------------------------------------------
 # Per-view Grangeat   (grangeat.py:58-170)
 # --------------------------------------------------------------------------
@@ -550,13 +606,13 @@ def _cfg_dt(geom, cfg):
 
 
 def forward_project(vol, voxel_mm, geom, cfg, target_batch=None, views=None):
-    """nufft_forward_project, method A (pipeline.py:122-147) -> (V, nu, nv).
+    """nufft_forward_project, methods A and B (pipeline.py:122-147) -> (V, nu, nv).
 
     ``views`` restricts the output to a subset of the views (bounded CPU
     samples); each batch still uses the reference's batch boundaries.
     """
-    if cfg.method != "a":
-        raise NotImplementedError("oracle restates method A only")
+    if cfg.method not in ("a", "b"):
+        raise ValueError("method must be 'a' or 'b'")
     spec = cfg.radial_spec
     lattice = radial_lattice(np.asarray(vol, dtype=np.float64), voxel_mm, spec,
                              cfg.spectrum_j, cfg.oversample_factor, cfg.basis)
@@ -568,8 +624,11 @@ def forward_project(vol, voxel_mm, geom, cfg, target_batch=None, views=None):
         if views is not None and not any(k in views for k in batch):
             continue
         targets, valid = umbrella_targets(geom, spec, batch, cfg.n_mu, cfg.n_t, dt)
-        rs = make_resampler(spec, targets, cfg.rho_pad, cfg.resample_j, cfg.oversample_factor)
-        vals = np.real(resample_forward(rs, lattice))
+        if cfg.method == "b":
+            vals = np.real(resample_b_forward(spec, targets, lattice, cfg.rho_pad, cfg.side_lobes))
+        else:
+            rs = make_resampler(spec, targets, cfg.rho_pad, cfg.resample_j, cfg.oversample_factor)
+            vals = np.real(resample_forward(rs, lattice))
         vals[~valid] = 0.0
         for i, k in enumerate(batch):
             if views is not None and k not in views:
@@ -581,9 +640,9 @@ def forward_project(vol, voxel_mm, geom, cfg, target_batch=None, views=None):
 
 
 def backproject(frames, geom, cfg, out_size, voxel_mm, target_batch=None):
-    """nufft_backproject, method A (pipeline.py:150-212) -> (N, N, N) real."""
-    if cfg.method != "a":
-        raise NotImplementedError("oracle restates method A only")
+    """nufft_backproject, methods A and B (pipeline.py:150-212) -> (N, N, N) real."""
+    if cfg.method not in ("a", "b"):
+        raise ValueError("method must be 'a' or 'b'")
     frames = np.asarray(frames)
     extent = out_size * voxel_mm
 
@@ -605,9 +664,14 @@ def backproject(frames, geom, cfg, out_size, voxel_mm, target_batch=None):
         vals = np.concatenate([grangeat_forward(frames[k], gp).ravel() for k in batch])
         targets, valid = umbrella_targets(geom, spec, batch, cfg.n_mu, n_t, dt)
         vals = np.where(valid, vals, 0.0)
-        rs = make_resampler(spec, targets, pad, cfg.resample_j, cfg.oversample_factor)
-        num += resample_adjoint(rs, vals.astype(np.complex128))
-        den += np.real(resample_adjoint(rs, valid.astype(np.complex128)))
+        if cfg.method == "b":
+            num += resample_b_adjoint(spec, targets, vals.astype(np.complex128), pad, cfg.side_lobes)
+            den += np.real(resample_b_adjoint(spec, targets, valid.astype(np.complex128), pad,
+                                              cfg.side_lobes))
+        else:
+            rs = make_resampler(spec, targets, pad, cfg.resample_j, cfg.oversample_factor)
+            num += resample_adjoint(rs, vals.astype(np.complex128))
+            den += np.real(resample_adjoint(rs, valid.astype(np.complex128)))
     keep = den > cfg.den_tol * den.max()
     lat = np.where(keep, num / np.where(keep, den, 1.0), 0.0)
     n_r, n_th, n_ph, _, d_rho, theta, _ = spec_arrays(spec)

@@ -64,6 +64,8 @@ _SIGS = {
     "cbn_nufft_set_phase": (ctypes.c_int, [c_vp, c_i32]),
     "cbn_resample_create": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, c_i32, P_i32,
                                            c_f64, P_f64, c_i64, P_i64, c_i64, c_vp]),
+    "cbn_resample_create_b": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, c_i32,
+                                             c_i32, P_f64, c_i64, c_vp]),
     "cbn_resample_destroy": (ctypes.c_int, [c_vp]),
     "cbn_resample_apply": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_resample_transpose": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),

@@ -16,6 +16,7 @@
 
 #include "cbn_projector.h"
 #include "cbn_resample_views.cuh"
+#include "cbn_dirichlet.cuh"
 
 namespace cbn {
 
@@ -261,7 +262,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     if (!gp.built) projector_fit_grangeat(p, gp, u, s);
     const AxisPlan* rax = p->bres;
     BatchPlan& bp = p->bbatch;
-    projector_batch_plan(p, bp, u, r, p->bpad, rax, s);
+    if (c.method == 0) projector_batch_plan(p, bp, u, r, p->bpad, rax, s);   // method A scalings
     const int dr = r.n_rho + 2 * p->bpad;
     const int64_t dsize = (int64_t)dr * r.n_theta * r.n_phi;
     const int64_t kres = (int64_t)rax[0].K * rax[1].K * rax[2].K;
@@ -285,7 +286,8 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     // phi-fastest [rho][theta][phi] and built by the column gather
     // (k_rs_gather_cols) instead of the atomic scatter
     const char* no_lanes = std::getenv("CBN_NO_VIEW_LANES");
-    const bool lanes = !(no_lanes && no_lanes[0] == '1') && rax[0].J == 3 &&
+    const bool method_b = c.method == 1;
+    const bool lanes = !method_b && !(no_lanes && no_lanes[0] == '1') && rax[0].J == 3 &&
                        (2LL * r.n_phi) % p->g.n_views == 0 && rax[0].K == 2 * r.n_phi;
     const int shift = (int)(2LL * r.n_phi / p->g.n_views);
     long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
@@ -328,7 +330,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         }
     }
     const int slow_axis = lanes ? 2 : 0;
-    if (!lanes) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
+    if (!lanes && !method_b) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
 
     // transposed resample of one group of batches sharing a scaling: one
     // inverse FFT of the summed spreads, crop * scaling, accumulate
@@ -365,7 +367,30 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         if (!lanes) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
     };
 
-    if (lanes) {
+    if (method_b) {
+        // method B (resampling.py:176-189): views in blocks of 32, forward
+        // Grangeat, then the conjugate periodic-sinc spread of the values (and
+        // of the validity mask) straight into the padded-lattice accumulators
+        const int V = p->g.n_views;
+        p->values.ensure((size_t)per_view * 32);
+        const DirGrid dg{{dr, r.n_theta, r.n_phi}, {1, (int64_t)dr, (int64_t)r.n_theta * dr}};
+        for (int v0 = 0; v0 < V; v0 += 32) {
+            const int nb = std::min(32, V - v0);
+            {
+                StageScope st(p->timer, "grangeat_forward", s);
+                grangeat_forward_block(p, frames + (size_t)v0 * nu * nv, nb, p->values.p, s);
+            }
+            UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, v0, s);
+            StageScope st(p->timer, "transpose_spread", s);
+            const int64_t mb = per_view * nb;
+            dispatch_taps(c.side_lobes + 1, [&](auto tc) {
+                k_dir_spread<decltype(tc)::value><<<blocks_for(mb, 256), 256, 0, s>>>(
+                    acc_num, need_den ? acc_den : nullptr, dg, src, mb, nullptr, p->values.p);
+                return 0;
+            });
+            CBN_LAUNCH_CHECK();
+        }
+    } else if (lanes) {
         // runs of consecutive batches sharing a scaling group: forward Grangeat
         // of the run's views, target-major transpose, column gather, flush
         const size_t nbat = bp.batches.size();
@@ -409,7 +434,7 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     }
 
     int cur = -1;
-    for (size_t bi = 0; !lanes && bi < bp.batches.size(); ++bi) {
+    for (size_t bi = 0; !lanes && !method_b && bi < bp.batches.size(); ++bi) {
         const auto& b = bp.batches[bi];
         const int g = bp.group[bi];
         if (cur >= 0 && g != cur) flush(cur);
@@ -441,8 +466,9 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     // ---- ifftn of the accumulated ifftshifted grids, rho crop, origin average
     if (p->timer.on) p->timer.begin("bp_lattice", s);
     long long dd[3] = {r.n_phi, r.n_theta, dr};
-    p->fft.exec(p->fft.get(3, dd, nch), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
-    const double inv = 1.0 / (double)dsize;
+    // method A ends in ifftn (incl. 1 / size); method B's spread is the result
+    if (!method_b) p->fft.exec(p->fft.get(3, dd, nch), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
+    const double inv = method_b ? 1.0 : 1.0 / (double)dsize;
     p->red.ensure(2 * kRed + 64);
     double* means = p->red.p + 2 * kRed;        // num re, num im, den re, den im
     projector_column_mean(acc_num, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p, means, s);

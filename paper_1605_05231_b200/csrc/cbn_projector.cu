@@ -16,6 +16,7 @@
 
 #include "cbn_projector.h"
 #include "cbn_resample_views.cuh"
+#include "cbn_dirichlet.cuh"
 
 using namespace cbn;
 
@@ -501,7 +502,9 @@ void fit_grangeat(P* p, GrangeatPlan& gp, const UmbrellaTables& u, cudaStream_t 
 void build_forward(P* p, cudaStream_t s) {
     if (p->fw_built) return;
     const cbn_projector_config& c = p->c;
-    CBN_REQUIRE(c.method == 0, "only method 'a' runs on the device");
+    CBN_REQUIRE(c.method == 0 || c.method == 1, "method must be 0 ('a') or 1 ('b')");
+    CBN_REQUIRE(c.method == 0 || (c.side_lobes >= 0 && c.side_lobes + 1 <= kMaxDirTaps),
+                "side_lobes must be 0..7");
     CBN_REQUIRE(c.spectrum_j >= 2 && c.spectrum_j <= 8, "spectrum_j must be 2..8");
     require_uniform(c.resample_j, "resample_j");
     p->frad.build(c.spec.n_rho, c.spec.n_theta, c.spec.n_phi, c.spec.rho_max, p->voxel, s);
@@ -520,7 +523,9 @@ void build_forward(P* p, cudaStream_t s) {
 void build_backward(P* p, cudaStream_t s) {
     if (p->bw_built) return;
     const cbn_projector_config& c = p->c;
-    CBN_REQUIRE(c.method == 0, "only method 'a' runs on the device");
+    CBN_REQUIRE(c.method == 0 || c.method == 1, "method must be 0 ('a') or 1 ('b')");
+    CBN_REQUIRE(c.method == 0 || (c.side_lobes >= 0 && c.side_lobes + 1 <= kMaxDirTaps),
+                "side_lobes must be 0..7");
     require_uniform(c.resample_j, "resample_j");
     const int out = p->n_vol;
     const double extent = out * p->voxel;
@@ -674,8 +679,27 @@ void lattice_spectrum(P* p, const float2* src, int shift, float scale, cudaStrea
     k_pad_lattice<<<blocks_for(total, 256), 256, 0, s>>>(src, shift, scale, r.n_rho, p->fpad, dr,
                                                          total, mean, p->padded.p);
     CBN_LAUNCH_CHECK();
+    if (p->c.method == 1) return;   // method B interpolates the padded lattice itself
     long long dims[3] = {r.n_phi, r.n_theta, dr};
     p->fft.exec(p->fft.get(3, dims, 1), p->padded.p, p->padded.p, CUFFT_FORWARD, s);
+}
+
+// method B (resampling.py:149-161): Re(periodic-sinc gather) at the umbrella
+// targets of views [v0, v0 + nb) straight from the padded lattice
+void gather_views_b(P* p, int v0, int nb, float* vals, cudaStream_t s, const float* tscale) {
+    const RadialTables& r = p->frad;
+    const int dr = r.n_rho + 2 * p->fpad;
+    const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+    const int64_t m = per_view * nb;
+    UmbrellaSrc src = cached_umbrella(p, p->fumb, r, p->fpad, v0, s);
+    const DirGrid g{{dr, r.n_theta, r.n_phi}, {1, (int64_t)dr, (int64_t)r.n_theta * dr}};
+    StageScope st(p->timer, "resample_gather", s);
+    dispatch_taps(p->c.side_lobes + 1, [&](auto tc) {
+        k_dir_gather<decltype(tc)::value><<<blocks_for(m, 256), 256, 0, s>>>(
+            p->padded.p, g, src, m, nullptr, vals, tscale, p->fumb.n_t);
+        return 0;
+    });
+    CBN_LAUNCH_CHECK();
 }
 
 // Fit the resample scalings of every view batch once (plan_resample's
@@ -919,6 +943,20 @@ constexpr int kViewBlock = 32;
 // are produced (stage API).
 void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
                           float* values_out = nullptr) {
+    if (p->c.method == 1) {
+        const int64_t pv = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+        if (!values_out) p->values.ensure((size_t)pv * kViewBlock);
+        for (int v = lo; v < hi; v += kViewBlock) {
+            const int nb = std::min(kViewBlock, hi - v);
+            if (values_out) {
+                gather_views_b(p, v, nb, values_out + (size_t)(v - lo) * pv, s, nullptr);
+                continue;
+            }
+            gather_views_b(p, v, nb, p->values.p, s, p->fgr.w2inv.p);
+            grangeat_reverse(p, p->values.p, frames + (size_t)(v - lo) * p->g.nu * p->g.nv, nb, s);
+        }
+        return;
+    }
     BatchPlan& bp = p->fbatch;
     ensure_batch_plan(p, bp, p->fumb, p->frad, p->fpad, p->fres, s);
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;

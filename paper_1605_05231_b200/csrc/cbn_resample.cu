@@ -1,7 +1,9 @@
 // Stand-alone resampling plan and centred radial FFT, for the module-level API
 // of the reference (resampling.py:79-196, radon_fourier.py:117-135).
 //
-// cbn_resample mirrors ResamplePlan (method A): arbitrary fractional lattice
+// cbn_resample mirrors ResamplePlan.  Method B (cbn_resample_create_b) keeps
+// only the targets and runs the truncated periodic-sinc gather / spread of
+// cbn_dirichlet.cuh on the padded lattice.  Method A: arbitrary fractional lattice
 // targets, a generic NUFFT plan on the rho-padded lattice with nodes
 // -2 pi pos / padded (resampling.py:97-102), and
 //   apply:     pad(origin_avg(x)) -> fftn -> fftshift / size -> type 2   (146-148)
@@ -11,6 +13,7 @@
 // reference layout (rho, theta, phi), rho slowest.
 #include <mutex>
 
+#include "cbn_dirichlet.cuh"
 #include "cbn_plan.h"
 
 extern "C" {
@@ -122,6 +125,9 @@ using namespace cbn;
 struct cbn_resample_s {
     int n_rho = 0, n_theta = 0, n_phi = 0, pad = 0, dr = 0;
     int64_t m = 0;
+    int method = 0;                 // 0: A (NUFFT), 1: B (truncated periodic sinc)
+    int taps = 3;                   // method B: side_lobes + 1
+    DevBuf<double> targets;         // method B: (m, 3) fractional indices
     cbn_nufft_s* plan = nullptr;
     FFTCache fft;
     DevBuf<float2> a, b;
@@ -174,6 +180,36 @@ int cbn_resample_create(cbn_resample_s** out, int32_t n_rho, int32_t n_theta, in
     }
 }
 
+int cbn_resample_create_b(cbn_resample_s** out, int32_t n_rho, int32_t n_theta, int32_t n_phi,
+                          int32_t rho_pad, int32_t side_lobes, const double* targets, int64_t m,
+                          void* stream) {
+    try {
+        CBN_REQUIRE(out && targets && m >= 1, "bad argument");
+        CBN_REQUIRE(n_rho >= 2 && n_rho % 2 == 0 && n_theta >= 1 && n_phi >= 1, "bad radial spec");
+        CBN_REQUIRE(rho_pad >= 0, "rho_pad must be >= 0");
+        CBN_REQUIRE(side_lobes >= 0 && side_lobes + 1 <= kMaxDirTaps, "side_lobes must be 0..7");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto p = std::make_unique<cbn_resample_s>();
+        p->n_rho = n_rho;
+        p->n_theta = n_theta;
+        p->n_phi = n_phi;
+        p->pad = rho_pad;
+        p->dr = n_rho + 2 * rho_pad;
+        p->m = m;
+        p->method = 1;
+        p->taps = side_lobes + 1;
+        p->targets.upload(targets, (size_t)m * 3, s);
+        const size_t big = (size_t)p->dr * n_theta * n_phi;
+        p->a.alloc(big);
+        p->mean.alloc(2);
+        CBN_CUDA(cudaStreamSynchronize(s));
+        *out = p.release();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int cbn_resample_destroy(cbn_resample_s* p) {
     delete p;
     return CBN_OK;
@@ -190,6 +226,17 @@ int cbn_resample_apply(cbn_resample_s* p, const void* data, void* values, void* 
         CBN_LAUNCH_CHECK();
         k_rs_pad<<<blocks_for(tot, 256), 256, 0, s>>>(x, p->n_rho, L, p->pad, p->mean.p, p->a.p);
         CBN_LAUNCH_CHECK();
+        if (p->method == 1) {
+            const DirGrid g{{p->dr, p->n_theta, p->n_phi}, {L, (int64_t)p->n_phi, 1}};
+            const ExplicitPos src{p->targets.p, p->pad};
+            dispatch_taps(p->taps, [&](auto tc) {
+                k_dir_gather<decltype(tc)::value><<<blocks_for(p->m, 256), 256, 0, s>>>(
+                    p->a.p, g, src, p->m, static_cast<float2*>(values), nullptr, nullptr, 1);
+                return 0;
+            });
+            CBN_LAUNCH_CHECK();
+            return CBN_OK;
+        }
         long long dims[3] = {p->dr, p->n_theta, p->n_phi};
         p->fft.exec(p->fft.get(3, dims, 1), p->a.p, p->a.p, CUFFT_FORWARD, s);
         // spectrum = fftshift(F) / size: out[k] = F[(k - n//2) mod n] = F[(k + n - n//2) mod n]
@@ -207,10 +254,30 @@ int cbn_resample_transpose(cbn_resample_s* p, const void* values, void* data, vo
     try {
         CBN_REQUIRE(p && data && values, "null argument");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        int st = cbn_nufft_type1(p->plan, values, p->a.p, stream);
-        if (st != CBN_OK) return st;
         const int64_t L = (int64_t)p->n_theta * p->n_phi;
         const int64_t tot = (int64_t)p->dr * L;
+        if (p->method == 1) {
+            CBN_CUDA(cudaMemsetAsync(p->a.p, 0, sizeof(float2) * tot, s));
+            const DirGrid g{{p->dr, p->n_theta, p->n_phi}, {L, (int64_t)p->n_phi, 1}};
+            const ExplicitPos src{p->targets.p, p->pad};
+            dispatch_taps(p->taps, [&](auto tc) {
+                k_dir_spread<decltype(tc)::value><<<blocks_for(p->m, 256), 256, 0, s>>>(
+                    p->a.p, nullptr, g, src, p->m, static_cast<const float2*>(values), nullptr);
+                return 0;
+            });
+            CBN_LAUNCH_CHECK();
+            float2* out = static_cast<float2*>(data);
+            const int64_t nout = (int64_t)p->n_rho * L;
+            k_rs_crop<<<blocks_for(nout, 256), 256, 0, s>>>(p->a.p, p->n_rho, L, p->pad, 1.0f, out);
+            CBN_LAUNCH_CHECK();
+            k_row_mean<<<1, 256, 0, s>>>(out, L, p->n_rho / 2, 1.0, p->mean.p);
+            CBN_LAUNCH_CHECK();
+            k_set_row<<<blocks_for(L, 256), 256, 0, s>>>(out, L, p->n_rho / 2, p->mean.p);
+            CBN_LAUNCH_CHECK();
+            return CBN_OK;
+        }
+        int st = cbn_nufft_type1(p->plan, values, p->a.p, stream);
+        if (st != CBN_OK) return st;
         // ifftshift: out[k] = in[(k + n//2) mod n]
         k_shift3<<<blocks_for(tot, 256), 256, 0, s>>>(p->a.p, p->b.p, p->dr, p->n_theta, p->n_phi,
                                                       p->dr / 2, p->n_theta / 2, p->n_phi / 2, 1.0f);

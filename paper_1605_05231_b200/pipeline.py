@@ -44,9 +44,8 @@ def _config_struct(cfg, target_batch: int, plan_chunk: int) -> _lib.ProjectorCon
     method = str(cfg.method).lower()
     if method not in ("a", "b"):
         raise ValueError("method must be 'a' or 'b'")
-    if method == "b":
-        raise NotImplementedError("resample method 'b' is not on the device path yet "
-                                  "(SURVEY.md 8(f) next item 1)")
+    if method == "b" and not 0 <= int(cfg.side_lobes) <= 7:
+        raise ValueError("side_lobes must be 0..7")
     if cfg.t_taper not in ("none", "hann"):
         raise ValueError("t_taper must be 'none' or 'hann'")
     if cfg.basis not in ("trilinear", "dirac"):
@@ -54,7 +53,7 @@ def _config_struct(cfg, target_batch: int, plan_chunk: int) -> _lib.ProjectorCon
     rj = np.broadcast_to(np.atleast_1d(cfg.resample_j), (3,)).astype(int)
     spec = cfg.radial_spec
     c = _lib.ProjectorConfig()
-    c.method = 0
+    c.method = 0 if method == "a" else 1
     c.spec = _lib.RadialSpec(int(spec.n_rho), int(spec.n_theta), int(spec.n_phi),
                              float(spec.rho_max))
     c.n_mu = int(cfg.n_mu)
@@ -87,7 +86,8 @@ def _key(geom, cfg, n, voxel, direction, target_batch, plan_chunk):
             str(cfg.method), int(cfg.n_mu), int(cfg.n_t), cfg.t_pitch_mm, cfg.t_taper,
             int(cfg.spectrum_j), tuple(np.broadcast_to(np.atleast_1d(cfg.resample_j), (3,)).tolist()),
             float(cfg.oversample_factor), cfg.rho_pad, cfg.basis, float(cfg.normalization),
-            float(cfg.bp_normalization), float(cfg.den_tol), int(n), float(voxel), direction,
+            float(cfg.bp_normalization), float(cfg.den_tol), int(cfg.side_lobes), int(n),
+            float(voxel), direction,
             int(target_batch), int(plan_chunk))
 
 

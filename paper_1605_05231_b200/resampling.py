@@ -1,11 +1,12 @@
-"""Radial -> umbrella resampling (drop-in for ``cbnufft/resampling.py``, method A).
+"""Radial -> umbrella resampling (drop-in for ``cbnufft/resampling.py``).
 
-``plan_resample`` builds a device plan (``cbn_resample_*``): a NUFFT plan on the
-rho-padded lattice at nodes -2 pi pos / padded with the reference's own
-least-squares scaling; ``resample_apply`` / ``resample_transpose`` run the
-origin average, padding, FFTs and the J=3 gather / spread on the device.
-Method B (truncated periodic sinc) is the next item of SURVEY.md 8(f) and
-raises NotImplementedError.
+``plan_resample`` builds a device plan (``cbn_resample_*``).  Method A: a NUFFT
+plan on the rho-padded lattice at nodes -2 pi pos / padded with the
+reference's own least-squares scaling; ``resample_apply`` /
+``resample_transpose`` run the origin average, padding, FFTs and the J=3
+gather / spread on the device.  Method B: truncated centred periodic-sinc taps
+(side_lobes + 1 per axis) applied to the padded lattice directly
+(resampling.py:126-161,176-189).
 """
 
 from __future__ import annotations
@@ -77,7 +78,16 @@ def plan_resample(spec, targets, method: str = "a", rho_pad: int | None = None, 
     padded = (n_r + 2 * rho_pad, n_t, n_p)
     plan = ResamplePlan(method, spec, targets, int(rho_pad), side_lobes, padded_dims=padded)
     if method == "b":
-        raise NotImplementedError("resample method 'b' is not on the device path yet")
+        if not 0 <= int(side_lobes) <= 7:
+            raise ValueError("side_lobes must be 0..7")
+        _device.require_cuda()
+        tg, tp = _lib.f64_array(targets)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().cbn_resample_create_b(
+            ctypes.byref(h), n_r, n_t, n_p, int(rho_pad), int(side_lobes), tp, targets.shape[0],
+            ctypes.c_void_p(_device.stream_ptr())), "plan_resample")
+        plan._handle = h.value
+        return plan
     taps = np.ascontiguousarray(np.broadcast_to(np.atleast_1d(j), (3,)), dtype=np.int32)
     _device.require_cuda()
     rows, rp = _lib.i64_array(_device.ls_rows(targets.shape[0]))

@@ -99,9 +99,10 @@ def frames_array(frames):
     return np.stack([f.data for f in frames])
 
 
-def pipeline_small(n=16, views=12, seed=11, basis="trilinear"):
+def pipeline_small(n=16, views=12, seed=11, basis="trilinear", method="a"):
     geom, voxel, spec, cfg = small_geometry(n, views)
     cfg.basis = basis
+    cfg.method = method
     vol32 = random_ellipsoid_phantom(n, 5, seed)
     vol = Volume3D(vol32, voxel)
     out = dict(vol=vol32, voxel=voxel, n=n, views=views,
@@ -122,7 +123,7 @@ def pipeline_small(n=16, views=12, seed=11, basis="trilinear"):
     out["bp"] = rpipe.nufft_backproject(frames, geom, cfg, n, voxel).data
     # stage fixtures: resample of views 0..2, grangeat of view 1
     targets, valid = rpipe._umbrella_targets(geom, cfg, range(0, 3))
-    rp = plan_resample(spec, targets, "a", rho_pad=cfg.rho_pad, j=cfg.resample_j)
+    rp = plan_resample(spec, targets, method, rho_pad=cfg.rho_pad, j=cfg.resample_j)
     out["rs_targets"] = targets
     out["rs_valid"] = valid
     out["rs_apply"] = resample_apply(rp, out["lattice"])
@@ -185,6 +186,11 @@ def main():
         # backprojector's transposed resample
         np.savez_compressed(os.path.join(HERE, "pipeline_n12_v24.npz"),
                             **pipeline_small(12, 24, 23, "trilinear"))
+    if "small" in which or "methodb" in which:
+        # resample method B (truncated periodic sinc, side_lobes 2): stage
+        # fixtures (apply / transpose) and both projectors, one and several batches
+        np.savez_compressed(os.path.join(HERE, "pipeline_n12_b.npz"),
+                            **pipeline_small(12, 10, 31, "trilinear", "b"))
     if "big" in which:
         np.savez_compressed(os.path.join(HERE, "config0.npz"), **config0())
 

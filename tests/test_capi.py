@@ -61,11 +61,17 @@ def test_projector_create_validates_on_host():
     assert b"n_rho" in lib.cbn_last_error()
 
 
-def test_method_b_and_bad_taper_raise():
+def test_method_b_config_and_bad_taper():
     from paper_1605_05231_b200.pipeline import _config_struct
     geom, voxel, spec, cfg = small_setup()
     cfg.method = "b"
-    with pytest.raises(NotImplementedError):
+    assert _config_struct(cfg, 1, 1).method == 1
+    cfg.side_lobes = 9
+    with pytest.raises(ValueError):
+        _config_struct(cfg, 1, 1)
+    cfg.side_lobes = 2
+    cfg.method = "c"
+    with pytest.raises(ValueError):
         _config_struct(cfg, 1, 1)
     cfg.method = "a"
     cfg.t_taper = "tukey"

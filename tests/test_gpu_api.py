@@ -123,8 +123,8 @@ def test_resample_validation(rs):
         rs.plan_resample(spec, np.zeros((4, 3)), "c")
     with pytest.raises(ValueError):
         rs.plan_resample(spec, np.full((4, 3), -5.0), "a")
-    with pytest.raises(NotImplementedError):
-        rs.plan_resample(spec, np.zeros((4, 3)), "b")
+    with pytest.raises(ValueError):
+        rs.plan_resample(spec, np.zeros((4, 3)), "b", side_lobes=8)
     plan = rs.plan_resample(spec, np.zeros((4, 3)), "a")
     with pytest.raises(ValueError):
         rs.resample_apply(plan, np.zeros((3, 3, 3)))

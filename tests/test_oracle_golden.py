@@ -71,7 +71,23 @@ def test_oracle_end_to_end(which, golden_n16, golden_n12):
                       g["bp_b4"]) < 1e-11
 
 
-@pytest.mark.parametrize("name", ["pipeline_n16_v8", "pipeline_n12_v48"])
+def test_oracle_method_b():
+    """Resample method B (periodic sinc) stages and both projectors vs the reference."""
+    import os
+    from conftest import GOLDEN
+    g = dict(np.load(os.path.join(GOLDEN, "pipeline_n12_b.npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    cfg.method = "b"
+    assert rel_l2(orc.resample_b_forward(spec, g["rs_targets"], g["lattice"], cfg.rho_pad),
+                  g["rs_apply"]) < 1e-12
+    assert rel_l2(orc.resample_b_adjoint(spec, g["rs_targets"], g["rs_y"], cfg.rho_pad),
+                  g["rs_transpose"]) < 1e-12
+    assert rel_l2(orc.forward_project(g["vol"], voxel, geom, cfg), g["frames"]) < 1e-11
+    assert rel_l2(orc.backproject(g["frames"], geom, cfg, n, voxel), g["bp"]) < 1e-11
+
+
+@pytest.mark.parametrize("name", ["pipeline_n16_v8", "pipeline_n12_v48", "pipeline_n12_v24"])
 def test_oracle_rotation_aligned(name):
     import os
     from conftest import GOLDEN
