@@ -202,6 +202,15 @@ int cbn_projector_set_timing(cbn_projector* proj, int32_t on);
 int cbn_projector_stage_times(cbn_projector* proj, double* ms, int32_t* count,
                               char* names, int32_t names_len, int32_t reset);
 
+/* ------------------------------------------------------------ baseline
+ * ct_project_linear (baseline.py:52-98): ray-driven cone-beam projection with
+ * trilinear volume sampling, N midpoint samples per clipped chord -- the
+ * projector calibrate_bp_normalization runs (pipeline.py:245-257).
+ * vol [device] float32 n^3 [ix][iy][iz]; frames [device] float32
+ * n_views x nu x nv. */
+int cbn_ct_project_linear(const cbn_geometry* geom, const float* vol, int32_t n, double voxel_mm,
+                          float* frames, void* stream);
+
 /* Number of kernels this library has launched in the process (cuFFT's own
  * kernels are not counted). */
 long long cbn_launch_count(void);

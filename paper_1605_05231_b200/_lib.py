@@ -87,6 +87,8 @@ _SIGS = {
     "cbn_projector_set_timing": (ctypes.c_int, [c_vp, c_i32]),
     "cbn_projector_stage_times": (ctypes.c_int, [c_vp, P_f64, P_i32, ctypes.c_char_p, c_i32,
                                                  c_i32]),
+    "cbn_ct_project_linear": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i32, c_f64, c_vp,
+                                             c_vp]),
     "cbn_launch_count": (ctypes.c_longlong, []),
 }
 

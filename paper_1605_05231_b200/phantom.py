@@ -97,3 +97,25 @@ def random_ellipsoid_phantom(n: int, n_ellipsoids: int, seed: int,
                 q = q + bk * bk
             vol[x0:x0 + xs.size, j0:j1, k0:k1] += density * (q <= 1.0)
     return vol.astype(dtype)
+
+
+def smooth_ball_volume(n: int, voxel_mm: float, radius_mm: float, density: float = 1.0,
+                       center_mm=(0.0, 0.0, 0.0)) -> Volume3D:
+    """C1 bump density (1 - r^2/R^2)^2 inside R, voxel-centre sampled -- the
+    calibration phantom of the reference (phantom.py:207-214)."""
+    c = (np.arange(n) - n / 2.0 + 0.5) * voxel_mm
+    x, y, z = np.meshgrid(c - center_mm[0], c - center_mm[1], c - center_mm[2], indexing="ij")
+    r2 = (x * x + y * y + z * z) / radius_mm ** 2
+    return Volume3D(density * np.maximum(1.0 - r2, 0.0) ** 2, voxel_mm)
+
+
+def smooth_ball_line_integral(point, direction, center=(0.0, 0.0, 0.0), radius: float = 1.0,
+                              density: float = 1.0):
+    """Closed-form line integral of the same bump, 16 density L^5 / (15 R^4) with L
+    the half chord (phantom.py:179-191); rows of (M, 3) points / unit directions."""
+    p = np.atleast_2d(np.asarray(point, dtype=np.float64)) - np.asarray(center)
+    d = np.atleast_2d(np.asarray(direction, dtype=np.float64))
+    b = np.sum(p * d, axis=-1)
+    d2 = np.sum(p * p, axis=-1) - b * b
+    half = np.sqrt(np.maximum(radius ** 2 - d2, 0.0))
+    return 16.0 * density * half ** 5 / (15.0 * radius ** 4)

@@ -228,3 +228,47 @@ def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volu
     proj = get_projector(geom, cfg, out_size, voxel_mm, _BACK)
     vol = proj.backproject(data).cpu().numpy().astype(np.float64)
     return Volume3D(vol, voxel_mm)
+
+
+def calibrate_normalization(geom, n: int, cfg, voxel_mm: float) -> float:
+    """Forward-projector scale fitted on the analytic smooth ball (pipeline.py:215-242):
+    least-squares ratio between the closed-form view-0 projection and the
+    projector's view-0 output; stored in cfg.normalization and returned."""
+    from .phantom import smooth_ball_line_integral, smooth_ball_volume
+    radius = 0.28 * n * voxel_mm
+    vol = smooth_ball_volume(n, voxel_mm, radius)
+    cfg.normalization = 1.0
+    proj = get_projector(geom, cfg, n, voxel_mm, _FORWARD)
+    got = proj.forward(vol.data, 0, 1).cpu().numpy().astype(np.float64)[0].ravel()
+    s = geom.source_position(0)
+    pu, pv = geom.pixel_mm
+    u = (np.arange(geom.nu) - geom.nu / 2.0 + 0.5) * pu
+    v = (np.arange(geom.nv) - geom.nv / 2.0 + 0.5) * pv
+    uu, vv = np.meshgrid(u, v, indexing="ij")
+    a = geom.view_angle(0)
+    s_hat = np.array([np.cos(a), np.sin(a), 0.0])
+    u_hat = np.array([-np.sin(a), np.cos(a), 0.0])
+    v_hat = np.array([0.0, 0.0, 1.0])
+    pts = (s - geom.sd_mm * s_hat)[None, :] \
+        + uu.ravel()[:, None] * u_hat + vv.ravel()[:, None] * v_hat
+    d = pts - s
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    ref = smooth_ball_line_integral(np.broadcast_to(s, d.shape), d, radius=radius)
+    cfg.normalization = float(np.dot(ref, got) / np.dot(got, got))
+    return cfg.normalization
+
+
+def calibrate_bp_normalization(geom, n: int, cfg, voxel_mm: float) -> float:
+    """Backprojector scale fitted on the smooth ball through the baseline
+    ray-driven projector (pipeline.py:245-257); stored in cfg.bp_normalization."""
+    from .baseline import ct_project_linear
+    from .phantom import smooth_ball_volume
+    radius = 0.28 * n * voxel_mm
+    vol = smooth_ball_volume(n, voxel_mm, radius)
+    frames = ct_project_linear(vol, geom)
+    cfg.bp_normalization = 1.0
+    rec = nufft_backproject(frames, geom, cfg, n, voxel_mm)
+    mask = vol.data > 0.05
+    cfg.bp_normalization = float(np.dot(vol.data[mask], rec.data[mask])
+                                 / np.dot(rec.data[mask], rec.data[mask]))
+    return cfg.bp_normalization

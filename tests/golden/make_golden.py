@@ -143,6 +143,25 @@ def pipeline_small(n=16, views=12, seed=11, basis="trilinear", method="a"):
     return out
 
 
+def calibration(n=16, views=12):
+    """calibrate_normalization / calibrate_bp_normalization (pipeline.py:215-257)
+    and the baseline ray-driven projector they rely on (baseline.py:52-98)."""
+    from cbnufft.baseline import ct_project_linear
+    from cbnufft.phantom import smooth_ball_volume
+    geom, voxel, spec, cfg = small_geometry(n, views)
+    out = dict(n=n, views=views)
+    out["norm"] = rpipe.calibrate_normalization(geom, n, cfg, voxel)
+    geom, voxel, spec, cfg = small_geometry(n, views)
+    out["bp_norm"] = rpipe.calibrate_bp_normalization(geom, n, cfg, voxel)
+    ball = smooth_ball_volume(n, voxel, 0.28 * n * voxel)
+    out["ball"] = ball.data
+    out["ball_frames"] = frames_array(ct_project_linear(ball, geom))
+    vol32 = random_ellipsoid_phantom(n, 5, 41)
+    out["vol"] = vol32
+    out["vol_frames"] = frames_array(ct_project_linear(Volume3D(vol32, voxel), geom))
+    return out
+
+
 def config0():
     geom = ConeGeometry(3.0, 6.0, 2.0, 2.0, 64, 64, 90, 2.0)
     n = 64
@@ -191,6 +210,8 @@ def main():
         # fixtures (apply / transpose) and both projectors, one and several batches
         np.savez_compressed(os.path.join(HERE, "pipeline_n12_b.npz"),
                             **pipeline_small(12, 10, 31, "trilinear", "b"))
+    if "small" in which or "calib" in which:
+        np.savez_compressed(os.path.join(HERE, "calibration_n16.npz"), **calibration())
     if "big" in which:
         np.savez_compressed(os.path.join(HERE, "config0.npz"), **config0())
 

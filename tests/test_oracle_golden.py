@@ -95,3 +95,19 @@ def test_oracle_rotation_aligned(name):
     n, views = int(g["n"]), int(g["views"])
     geom, voxel, spec, cfg = small_setup(n, views)
     assert rel_l2(orc.forward_project(g["vol"], voxel, geom, cfg), g["frames"]) < 1e-11
+
+
+def test_smooth_ball_phantom_matches_reference():
+    """Host restatement of the calibration phantom (phantom.py:179-214)."""
+    import os
+    from conftest import GOLDEN
+    from paper_1605_05231_b200.phantom import smooth_ball_line_integral, smooth_ball_volume
+    g = dict(np.load(os.path.join(GOLDEN, "calibration_n16.npz")))
+    n = int(g["n"])
+    voxel = 2.0 / n
+    assert np.array_equal(smooth_ball_volume(n, voxel, 0.28 * n * voxel).data, g["ball"])
+    d = np.array([[1.0, 0.0, 0.0], [0.0, 0.6, 0.8]])
+    p = np.array([[-3.0, 0.1, 0.0], [0.0, 0.0, 0.0]])
+    got = smooth_ball_line_integral(p, d, radius=0.5)
+    half = np.sqrt(np.maximum(0.25 - np.array([0.01, 0.0]), 0.0))
+    assert np.allclose(got, 16.0 * half ** 5 / (15.0 * 0.5 ** 4), rtol=1e-14)
