@@ -162,6 +162,28 @@ def calibration(n=16, views=12):
     return out
 
 
+def io_and_cli(out_dir):
+    """Files written by the reference's io.py, and its CLI project/backproject
+    outputs on a small volume (cli.py:78-100)."""
+    import cbnufft.io as rio
+    from cbnufft.cli import main as rcli
+    os.makedirs(out_dir, exist_ok=True)
+    geom, voxel, spec, cfg = small_geometry(12, 8)
+    vol = Volume3D(random_ellipsoid_phantom(12, 4, 51), voxel)
+    rio.write_volume(os.path.join(out_dir, "vol.raw"), vol)
+    rio.save_geometry(os.path.join(out_dir, "geom.json"), geom)
+    for method in ("nufft-a", "nufft-b", "linear"):
+        code = rcli(["project", "--method", method, "--volume", os.path.join(out_dir, "vol.raw"),
+                     "--geometry", os.path.join(out_dir, "geom.json"),
+                     "--out", os.path.join(out_dir, f"proj_{method}.raw")])
+        assert code == 0
+    for method in ("nufft-a", "nufft-b"):
+        code = rcli(["backproject", "--method", method,
+                     "--projections", os.path.join(out_dir, "proj_nufft-a.raw"), "--n", "12",
+                     "--out", os.path.join(out_dir, f"bp_{method}.raw")])
+        assert code == 0
+
+
 def config0():
     geom = ConeGeometry(3.0, 6.0, 2.0, 2.0, 64, 64, 90, 2.0)
     n = 64
@@ -212,6 +234,8 @@ def main():
                             **pipeline_small(12, 10, 31, "trilinear", "b"))
     if "small" in which or "calib" in which:
         np.savez_compressed(os.path.join(HERE, "calibration_n16.npz"), **calibration())
+    if "small" in which or "io" in which:
+        io_and_cli(os.path.join(HERE, "io"))
     if "big" in which:
         np.savez_compressed(os.path.join(HERE, "config0.npz"), **config0())
 
