@@ -185,9 +185,15 @@ def run_ours(args):
     else:
         frames_dev = Projector(w.geom, w.cfg, w.n, w.voxel, 1).forward(torch.from_numpy(vol_host).cuda())
         x_dev = frames_dev
+        if world > 1:
+            # views and radial nodes sharded; lattice and grid summed with NCCL
+            x_loc = x_dev[lo:hi].contiguous()
 
-        def step():
-            return proj.backproject(x_dev)
+            def step():
+                return proj.backproject_sharded(x_loc, lo, hi)
+        else:
+            def step():
+                return proj.backproject(x_dev)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -237,7 +243,12 @@ def run_ours(args):
 
         def e2e_step():
             dev = host_in.to("cuda", non_blocking=True)
-            out = proj.forward(dev, lo, hi) if direction == 1 else proj.backproject(dev)
+            if direction == 1:
+                out = proj.forward(dev, lo, hi)
+            elif world > 1:
+                out = proj.backproject_sharded(dev[lo:hi].contiguous(), lo, hi)
+            else:
+                out = proj.backproject(dev)
             host_out.copy_(out, non_blocking=True)
 
         for _ in range(2):
@@ -310,7 +321,10 @@ def run_ours(args):
         "config": {"workload": f"{w.name} {args.direction}: {w.n}^3 volume, "
                                f"{w.spec.n_rho}x{w.spec.n_theta}x{w.spec.n_phi} radial lattice, "
                                f"{V} views of {w.geom.nu}^2, KB J=6 sigma=2, resample J=3",
-                   "views": V, "views_per_rank": hi - lo, "parallelism": f"views sharded x{world}",
+                   "views": V, "views_per_rank": hi - lo,
+                   "parallelism": f"views sharded x{world}" + ("" if direction == 1 or world == 1
+                                                               else ", radial nodes sharded, "
+                                                               "NCCL all-reduce of lattice + grid"),
                    "l2": "working set > L2 (resample grid 2.4 GB per view batch)"},
         "e2e": e2e,
         "gpu_launches": int(launches),

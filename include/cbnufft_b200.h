@@ -165,6 +165,24 @@ int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
  * -> vol [device] float32 N^3 */
 int cbn_backproject(cbn_projector* proj, const float* frames, float* vol, void* stream);
 
+/* nufft_backproject in three phases, for sharding views and nodes across
+ * devices; cbn_backproject == views(all) + finish(0 of 1) +
+ * crop.  Buffers [device] complex64, caller-owned:
+ *   lattice: lattice_elems  (padded-lattice accumulator; sum it over ranks)
+ *   grid:    grid_elems     ((2N)^3 adjoint grid; sum it over ranks)
+ * views:  transposed resample of views [lo, hi) -- `frames` holds those views
+ *         (hi - lo frames of nu x nv) -- into `lattice` (overwritten)
+ * finish: consumes the summed `lattice`; spreads part `part` of `nparts`
+ *         of the radial nodes into `grid` (overwritten)
+ * crop:   consumes the summed `grid`; vol [device] float32 N^3 */
+int cbn_backproject_sizes(cbn_projector* proj, int64_t* lattice_elems, int64_t* grid_elems,
+                          void* stream);
+int cbn_backproject_views(cbn_projector* proj, const float* frames, int32_t lo, int32_t hi,
+                          void* lattice, void* stream);
+int cbn_backproject_finish(cbn_projector* proj, void* lattice, int32_t part, int32_t nparts,
+                           void* grid, void* stream);
+int cbn_backproject_crop(cbn_projector* proj, void* grid, float* vol, void* stream);
+
 /* Diagnostics: the forward plan's per-node Grangeat records in bin-sorted
  * order (56-byte records: int16 lu, lv; int32 col; float2 factor; float w[10])
  * and the sorted node ids [host]; *m in: capacity, out: node count. */

@@ -80,6 +80,10 @@ _SIGS = {
     "cbn_projector_scratch_bytes": (ctypes.c_int, [c_vp, P_i64]),
     "cbn_forward_project": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_backproject": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cbn_backproject_sizes": (ctypes.c_int, [c_vp, P_i64, P_i64, c_vp]),
+    "cbn_backproject_views": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "cbn_backproject_finish": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "cbn_backproject_crop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_projector_radial_lattice": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_projector_resample_views": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_projector_grangeat_reverse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),

@@ -99,7 +99,7 @@ k_rs_spread2(float* __restrict__ gnum, float* __restrict__ gden, KBSet kb, Umbre
     UmbrellaSrc::Aux aux;
     src.node(i, w, aux);
     if (!aux.valid) return;
-    const float vn = vals[i];
+    const float vn = (vals && gnum) ? vals[i] : 0.f;   // den-only passes: no values
     if (vn == 0.f && !gden) return;
     int first[3];
     float wt[3][J];
@@ -253,7 +253,26 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     CBN_LAUNCH_CHECK();
 }
 
-void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s) {
+// ------------------------------------------------------------------ phases
+// The backprojector runs in three phases so that views and nodes can be
+// sharded across ranks:
+//   1. bp_views:  transposed resample of a view range into a padded-lattice
+//                 accumulator (ranks' accumulators are summed);
+//   2. bp_finish: lattice division by the cached den, ramp, and the 3D spread
+//                 of a share of the bin subproblems into a K^3 grid (summed);
+//   3. bp_crop:   inverse FFT, crop, deapodisation and Re * bp_normalization.
+// cbn_backproject runs all three on one device.
+struct BpCtx {
+    int dr = 0;
+    int64_t dsize = 0, kres = 0, k3 = 0, per_view = 0;
+    bool method_b = false, lanes = false;
+    int shift = 0, slow_axis = 0;
+    long long kd3[3] = {0, 0, 0};
+    int64_t sstr[3] = {0, 0, 0};
+    KBSet kbr{};
+};
+
+BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
     build_backward_plan(p, s);
     const cbn_projector_config& c = p->c;
     const RadialTables& r = p->brad;
@@ -263,41 +282,34 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     const AxisPlan* rax = p->bres;
     BatchPlan& bp = p->bbatch;
     if (c.method == 0) projector_batch_plan(p, bp, u, r, p->bpad, rax, s);   // method A scalings
-    const int dr = r.n_rho + 2 * p->bpad;
-    const int64_t dsize = (int64_t)dr * r.n_theta * r.n_phi;
-    const int64_t kres = (int64_t)rax[0].K * rax[1].K * rax[2].K;
-    const int64_t k3 = (int64_t)p->bspec[0].K * p->bspec[1].K * p->bspec[2].K;
-    // den (the transposed validity mask) depends on the geometry only: the first
-    // call computes and caches it, later calls spread the values alone
-    const bool need_den = !p->den_cached;
-    const int nch = need_den ? 2 : 1;
-    p->big.ensure((size_t)std::max(nch * kres, k3));
-    p->padded.ensure((size_t)nch * dsize);
-    float2* acc_num = p->padded.p;
-    float2* acc_den = need_den ? p->padded.p + dsize : nullptr;
-    CBN_CUDA(cudaMemsetAsync(p->padded.p, 0, sizeof(float2) * nch * dsize, s));
-    const int64_t per_view = (int64_t)u.n_mu * u.n_t;
-    const int nu = p->g.nu, nv = p->g.nv;
-    p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
-    KBSet kbr;
-    for (int d = 0; d < 3; ++d) kbr.ax[d] = rax[d].kb;
+    BpCtx x;
+    x.dr = r.n_rho + 2 * p->bpad;
+    x.dsize = (int64_t)x.dr * r.n_theta * r.n_phi;
+    x.kres = (int64_t)rax[0].K * rax[1].K * rax[2].K;
+    x.k3 = (int64_t)p->bspec[0].K * p->bspec[1].K * p->bspec[2].K;
+    x.per_view = (int64_t)u.n_mu * u.n_t;
+    for (int d = 0; d < 3; ++d) x.kbr.ax[d] = rax[d].kb;
     // views in lanes (as the forward gather): when view k's targets are view 0's
     // shifted by whole oversampled phi cells, the transposed grid is stored
     // phi-fastest [rho][theta][phi] and built by the column gather
     // (k_rs_gather_cols) instead of the atomic scatter
     const char* no_lanes = std::getenv("CBN_NO_VIEW_LANES");
-    const bool method_b = c.method == 1;
-    const bool lanes = !method_b && !(no_lanes && no_lanes[0] == '1') && rax[0].J == 3 &&
-                       (2LL * r.n_phi) % p->g.n_views == 0 && rax[0].K == 2 * r.n_phi;
-    const int shift = (int)(2LL * r.n_phi / p->g.n_views);
-    long long kd3[3] = {rax[0].K, rax[1].K, rax[2].K};
-    int64_t sstr[3] = {(int64_t)rax[1].K * rax[2].K, rax[2].K, 1};
-    if (lanes) {
-        kd3[0] = rax[2].K;
-        kd3[2] = rax[0].K;
-        sstr[0] = 1;
-        sstr[1] = rax[0].K;
-        sstr[2] = (int64_t)rax[1].K * rax[0].K;
+    x.method_b = c.method == 1;
+    x.lanes = !x.method_b && !(no_lanes && no_lanes[0] == '1') && rax[0].J == 3 &&
+              (2LL * r.n_phi) % p->g.n_views == 0 && rax[0].K == 2 * r.n_phi;
+    x.shift = (int)(2LL * r.n_phi / p->g.n_views);
+    x.kd3[0] = rax[0].K;
+    x.kd3[1] = rax[1].K;
+    x.kd3[2] = rax[2].K;
+    x.sstr[0] = (int64_t)rax[1].K * rax[2].K;
+    x.sstr[1] = rax[2].K;
+    x.sstr[2] = 1;
+    if (x.lanes) {
+        x.kd3[0] = rax[2].K;
+        x.kd3[2] = rax[0].K;
+        x.sstr[0] = 1;
+        x.sstr[1] = rax[0].K;
+        x.sstr[2] = (int64_t)rax[1].K * rax[0].K;
         if (!p->bcol_ptr.p) {
             // plan step: view-0 taps, then the per-column CSR of (target, tap) entries
             UmbrellaSrc src0 = projector_cached_umbrella(p, p->bumb, r, p->bpad, 0, s);
@@ -305,35 +317,62 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
             kb.ax[0] = rax[2].kb;
             kb.ax[1] = rax[1].kb;
             kb.ax[2] = rax[0].kb;
-            const int64_t n = per_view;
+            const int64_t n = x.per_view;
             DevBuf<RsTap<3>> taps((size_t)n);
             k_rs_taps<3><<<blocks_for(n, 256), 256, 0, s>>>(src0, kb, n, taps.p);
             CBN_LAUNCH_CHECK();
-            const int64_t ncol = kd3[0] * kd3[1];
+            const int64_t ncol = x.kd3[0] * x.kd3[1];
             DevBuf<int> counts((size_t)ncol);
             CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncol, s));
-            k_rs_col_count<3><<<blocks_for(n, 256), 256, 0, s>>>(taps.p, n, (int)kd3[0], (int)kd3[1],
-                                                                counts.p);
+            k_rs_col_count<3><<<blocks_for(n, 256), 256, 0, s>>>(taps.p, n, (int)x.kd3[0],
+                                                                (int)x.kd3[1], counts.p);
             CBN_LAUNCH_CHECK();
             std::vector<int> h((size_t)ncol + 1, 0);
-            CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncol, cudaMemcpyDeviceToHost, s));
+            CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncol,
+                                     cudaMemcpyDeviceToHost, s));
             CBN_CUDA(cudaStreamSynchronize(s));
             std::partial_sum(h.begin(), h.end(), h.begin());
             p->bcol_ptr.upload(h.data(), h.size(), s);
             p->bcol_ent.alloc(sizeof(RsColEntry) * (size_t)std::max(h.back(), 1));
-            CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncol, cudaMemcpyHostToDevice, s));
+            CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncol, cudaMemcpyHostToDevice,
+                                     s));
             k_rs_col_fill<3><<<blocks_for(n, 256), 256, 0, s>>>(
-                taps.p, n, (int)kd3[0], (int)kd3[1], counts.p,
+                taps.p, n, (int)x.kd3[0], (int)x.kd3[1], counts.p,
                 reinterpret_cast<RsColEntry*>(p->bcol_ent.p));
             CBN_LAUNCH_CHECK();
             CBN_CUDA(cudaStreamSynchronize(s));
         }
     }
-    const int slow_axis = lanes ? 2 : 0;
-    if (!lanes && !method_b) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
+    x.slow_axis = x.lanes ? 2 : 0;
+    p->big.ensure((size_t)std::max(x.kres, x.k3));
+    p->padded.ensure((size_t)2 * x.dsize);
+    return x;
+}
 
-    // transposed resample of one group of batches sharing a scaling: one
-    // inverse FFT of the summed spreads, crop * scaling, accumulate
+// transposed resample of views [lo, hi) accumulated into acc (dsize complex,
+// zeroed here): the values of `frames` (views lo..hi-1), or -- den_only -- the
+// validity mask of the same views (resample_transpose(valid), pipeline.py:184)
+void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int lo, int hi,
+                  float2* acc, bool den_only, cudaStream_t s) {
+    const cbn_projector_config& c = p->c;
+    const RadialTables& r = p->brad;
+    const AxisPlan* rax = p->bres;
+    BatchPlan& bp = p->bbatch;
+    const int64_t per_view = x.per_view;
+    const int nu = p->g.nu, nv = p->g.nv;
+    CBN_CUDA(cudaMemsetAsync(acc, 0, sizeof(float2) * x.dsize, s));
+    p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
+    auto forward_grangeat = [&](int v0, int nb, float* out) {
+        for (int k = 0; k < nb; k += 32) {
+            StageScope st(p->timer, "grangeat_forward", s);
+            const int n = std::min(32, nb - k);
+            grangeat_forward_block(p, frames + (size_t)(v0 + k - lo) * nu * nv, n,
+                                   out + (size_t)k * per_view, s);
+        }
+    };
+    float* gn = reinterpret_cast<float*>(p->big.p);    // the transposed grid (real parts)
+    // one group of batches sharing a scaling: inverse FFT of the summed
+    // spreads, crop * scaling, accumulate into acc
     auto flush = [&](int g) {
         size_t need = (size_t)rax[0].N + rax[1].N + rax[2].N;
         p->tab_idx.ensure(need);
@@ -343,152 +382,180 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
         for (int d = 0; d < 3; ++d) {
             build_table(kTabCropShift, rax[d].N, rax[d].K, bp.s32.p + ((size_t)g * 3 + d) * bp.smax,
                         p->tab_idx.p + off, p->tab_sc.p + off, s);
-            ax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, rax[d].N, sstr[d]};
+            ax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, rax[d].N, x.sstr[d]};
             off += rax[d].N;
         }
         // the crop reads only some slowest-axis planes: inverse-FFT just those in 2D
-        if (p->bres_planes.empty() || p->bres_planes_slow != slow_axis) {
+        if (p->bres_planes.empty() || p->bres_planes_slow != x.slow_axis) {
             size_t o = 0;
-            for (int d = 0; d < slow_axis; ++d) o += rax[d].N;
-            p->bres_planes = index_runs(p->tab_idx.p + o, rax[slow_axis].N, false, s);
-            p->bres_planes_slow = slow_axis;
+            for (int d = 0; d < x.slow_axis; ++d) o += rax[d].N;
+            p->bres_planes = index_runs(p->tab_idx.p + o, rax[x.slow_axis].N, false, s);
+            p->bres_planes_slow = x.slow_axis;
         }
         {
             StageScope st(p->timer, "transpose_ifft", s);
-            fft3_pruned(p->fft, p->big.p, kd3, nch, p->bres_planes, CUFFT_INVERSE, s);
+            fft3_pruned(p->fft, p->big.p, x.kd3, 1, p->bres_planes, CUFFT_INVERSE, s);
         }
         StageScope st(p->timer, "transpose_crop", s);
-        launch_remap<float2, kAccumC>(3, p->big.p, acc_num, ax, 1.0f, s);
+        launch_remap<float2, kAccumC>(3, p->big.p, acc, ax, 1.0f, s);
         CBN_LAUNCH_CHECK();
-        if (need_den) {
-            launch_remap<float2, kAccumC>(3, p->big.p + kres, acc_den, ax, 1.0f, s);
-            CBN_LAUNCH_CHECK();
-        }
-        if (!lanes) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * nch * kres, s));
+        if (!x.lanes) CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * x.kres, s));
     };
 
-    if (method_b) {
+    if (x.method_b) {
         // method B (resampling.py:176-189): views in blocks of 32, forward
-        // Grangeat, then the conjugate periodic-sinc spread of the values (and
-        // of the validity mask) straight into the padded-lattice accumulators
-        const int V = p->g.n_views;
+        // Grangeat, then the conjugate periodic-sinc spread straight into acc
         p->values.ensure((size_t)per_view * 32);
-        const DirGrid dg{{dr, r.n_theta, r.n_phi}, {1, (int64_t)dr, (int64_t)r.n_theta * dr}};
-        for (int v0 = 0; v0 < V; v0 += 32) {
-            const int nb = std::min(32, V - v0);
-            {
-                StageScope st(p->timer, "grangeat_forward", s);
-                grangeat_forward_block(p, frames + (size_t)v0 * nu * nv, nb, p->values.p, s);
-            }
+        const DirGrid dg{{x.dr, r.n_theta, r.n_phi}, {1, (int64_t)x.dr, (int64_t)r.n_theta * x.dr}};
+        for (int v0 = lo; v0 < hi; v0 += 32) {
+            const int nb = std::min(32, hi - v0);
+            if (!den_only) forward_grangeat(v0, nb, p->values.p);
             UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, v0, s);
             StageScope st(p->timer, "transpose_spread", s);
             const int64_t mb = per_view * nb;
             dispatch_taps(c.side_lobes + 1, [&](auto tc) {
                 k_dir_spread<decltype(tc)::value><<<blocks_for(mb, 256), 256, 0, s>>>(
-                    acc_num, need_den ? acc_den : nullptr, dg, src, mb, nullptr, p->values.p);
+                    den_only ? nullptr : acc, den_only ? acc : nullptr, dg, src, mb, nullptr,
+                    den_only ? nullptr : p->values.p);
                 return 0;
             });
             CBN_LAUNCH_CHECK();
         }
-    } else if (lanes) {
-        // runs of consecutive batches sharing a scaling group: forward Grangeat
-        // of the run's views, target-major transpose, column gather, flush
+        return;
+    }
+    if (x.lanes) {
+        // runs of consecutive batches sharing a scaling group, clipped to
+        // [lo, hi): forward Grangeat, target-major transpose, column gather
         const size_t nbat = bp.batches.size();
         size_t bi = 0;
         while (bi < nbat) {
             const int g = bp.group[bi];
             size_t e = bi + 1;
             while (e < nbat && bp.group[e] == g) ++e;
-            const int vlo = bp.batches[bi].first, vhi = bp.batches[e - 1].second;
+            const int vlo = std::max(lo, bp.batches[bi].first);
+            const int vhi = std::min(hi, bp.batches[e - 1].second);
+            bi = e;
+            if (vlo >= vhi) continue;
             const int nvr = vhi - vlo;
-            p->values.ensure((size_t)per_view * nvr);
-            p->values_t.ensure((size_t)per_view * nvr);
-            for (int v0 = 0; v0 < nvr; v0 += 32) {
-                StageScope st(p->timer, "grangeat_forward", s);
-                const int nb = std::min(32, nvr - v0);
-                grangeat_forward_block(p, frames + (size_t)(vlo + v0) * nu * nv, nb,
-                                       p->values.p + (size_t)v0 * per_view, s);
+            if (!den_only) {
+                p->values.ensure((size_t)per_view * nvr);
+                p->values_t.ensure((size_t)per_view * nvr);
+                forward_grangeat(vlo, nvr, p->values.p);
             }
             {
                 StageScope st(p->timer, "transpose_spread", s);
-                dim3 tg((unsigned)((per_view + 31) / 32), (unsigned)((nvr + 31) / 32));
-                k_transpose_vals<<<tg, 256, 0, s>>>(p->values.p, nvr, per_view, p->values_t.p);
-                CBN_LAUNCH_CHECK();
-                const unsigned ncol = (unsigned)(kd3[0] * kd3[1]);
+                if (!den_only) {
+                    dim3 tg((unsigned)((per_view + 31) / 32), (unsigned)((nvr + 31) / 32));
+                    k_transpose_vals<<<tg, 256, 0, s>>>(p->values.p, nvr, per_view, p->values_t.p);
+                    CBN_LAUNCH_CHECK();
+                }
+                const unsigned ncol = (unsigned)(x.kd3[0] * x.kd3[1]);
                 const RsColEntry* ent = reinterpret_cast<const RsColEntry*>(p->bcol_ent.p);
-                if (shift == 2 && p->g.n_views <= kRsPairThreads) {
+                float2* gnum = den_only ? nullptr : p->big.p;
+                float2* gden = den_only ? p->big.p : nullptr;
+                const float* vt = den_only ? nullptr : p->values_t.p;
+                if (x.shift == 2 && p->g.n_views <= kRsPairThreads) {
                     k_rs_gather_cols2<<<ncol, kRsPairThreads, 0, s>>>(
-                        p->big.p, need_den ? p->big.p + kres : nullptr, p->g.n_views,
-                        p->bcol_ptr.p, ent, p->values_t.p, vlo, nvr);
+                        gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
                 } else {
-                    CBN_REQUIRE(kd3[2] <= kRsColMaxPhi, "phi extent above the column-gather limit");
+                    CBN_REQUIRE(x.kd3[2] <= kRsColMaxPhi, "phi extent above the column-gather limit");
                     k_rs_gather_cols<<<ncol, kRsColThreads, 0, s>>>(
-                        p->big.p, need_den ? p->big.p + kres : nullptr, (int)kd3[2], p->bcol_ptr.p,
-                        ent, p->values_t.p, vlo, nvr, shift);
+                        gnum, gden, (int)x.kd3[2], p->bcol_ptr.p, ent, vt, vlo, nvr, x.shift);
                 }
                 CBN_LAUNCH_CHECK();
             }
             flush(g);
-            bi = e;
         }
+        return;
     }
-
+    // atomic scatter per batch (clipped to [lo, hi)), flushed per scaling group
+    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * x.kres, s));
     int cur = -1;
-    for (size_t bi = 0; !lanes && !method_b && bi < bp.batches.size(); ++bi) {
-        const auto& b = bp.batches[bi];
+    for (size_t bi = 0; bi < bp.batches.size(); ++bi) {
+        const int bl = std::max(lo, bp.batches[bi].first);
+        const int bh = std::min(hi, bp.batches[bi].second);
+        if (bl >= bh) continue;
         const int g = bp.group[bi];
         if (cur >= 0 && g != cur) flush(cur);
         cur = g;
-        const int nbv = b.second - b.first;
+        const int nbv = bh - bl;
         const int64_t mb = per_view * nbv;
-        p->values.ensure((size_t)mb);
-        // ---- forward Grangeat of the batch's frames, in blocks of views
-        for (int v0 = 0; v0 < nbv; v0 += 32) {
-            StageScope st(p->timer, "grangeat_forward", s);
-            const int nb = std::min(32, nbv - v0);
-            grangeat_forward_block(p, frames + (size_t)(b.first + v0) * nu * nv, nb,
-                                   p->values.p + (size_t)v0 * per_view, s);
+        if (!den_only) {
+            p->values.ensure((size_t)mb);
+            forward_grangeat(bl, nbv, p->values.p);
         }
-        // ---- spread of the batch's values (and mask) at its umbrella targets
-        UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, b.first, s);
+        UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, bl, s);
         StageScope st_sp(p->timer, "transpose_spread", s);
         dispatch_j(rax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             k_rs_spread2<J><<<blocks_for(mb, 256), 256, 0, s>>>(
-                reinterpret_cast<float*>(p->big.p),
-                need_den ? reinterpret_cast<float*>(p->big.p + kres) : nullptr, kbr, src,
-                p->values.p, mb);
+                den_only ? nullptr : gn, den_only ? gn : nullptr, x.kbr, src,
+                den_only ? nullptr : p->values.p, mb);
             return 0;
         });
         CBN_LAUNCH_CHECK();
     }
     if (cur >= 0) flush(cur);
-    // ---- ifftn of the accumulated ifftshifted grids, rho crop, origin average
-    if (p->timer.on) p->timer.begin("bp_lattice", s);
-    long long dd[3] = {r.n_phi, r.n_theta, dr};
+}
+
+// lattice-domain inverse of a transposed accumulator: ifftn (method A, incl.
+// 1/size) in place; returns the scale the origin mean / division use
+double bp_lattice_ifft(cbn_projector_s* p, const BpCtx& x, float2* acc, cudaStream_t s) {
+    const RadialTables& r = p->brad;
+    long long dd[3] = {r.n_phi, r.n_theta, x.dr};
     // method A ends in ifftn (incl. 1 / size); method B's spread is the result
-    if (!method_b) p->fft.exec(p->fft.get(3, dd, nch), p->padded.p, p->padded.p, CUFFT_INVERSE, s);
-    const double inv = method_b ? 1.0 : 1.0 / (double)dsize;
+    if (!x.method_b) p->fft.exec(p->fft.get(3, dd, 1), acc, acc, CUFFT_INVERSE, s);
+    return x.method_b ? 1.0 : 1.0 / (double)x.dsize;
+}
+
+// den (the transposed validity mask over every view) depends on the geometry
+// only: computed once per plan and cached in lattice node order
+void bp_den(cbn_projector_s* p, const BpCtx& x, cudaStream_t s) {
+    if (p->den_cached) return;
+    const RadialTables& r = p->brad;
+    float2* acc_den = p->padded.p + x.dsize;
+    bp_transpose(p, x, nullptr, 0, p->g.n_views, acc_den, true, s);
+    const double inv = bp_lattice_ifft(p, x, acc_den, s);
     p->red.ensure(2 * kRed + 64);
-    double* means = p->red.p + 2 * kRed;        // num re, num im, den re, den im
-    projector_column_mean(acc_num, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p, means, s);
+    double* means = p->red.p + 2 * kRed;
+    projector_column_mean(acc_den, r.lines(), x.dr, p->bpad + r.n_rho / 2, inv, p->red.p,
+                          means + 2, s);
     const int64_t M = r.nodes();
-    if (need_den) {
-        projector_column_mean(acc_den, r.lines(), dr, p->bpad + r.n_rho / 2, inv, p->red.p,
-                              means + 2, s);
-        p->den_cache.alloc((size_t)M);
-        p->den_max.alloc(1);
-        k_den_final<<<blocks_for(M, 256), 256, 0, s>>>(acc_den, r.lines(), dr, p->bpad, r.n_rho,
-                                                        inv, means + 2, p->den_cache.p);
-        CBN_LAUNCH_CHECK();
-        k_max_partial<<<kRed, 256, 0, s>>>(p->den_cache.p, M, p->red.p);
-        CBN_LAUNCH_CHECK();
-        k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, p->den_max.p);
-        CBN_LAUNCH_CHECK();
-        p->den_cached = true;
-    }
+    p->den_cache.alloc((size_t)M);
+    p->den_max.alloc(1);
+    k_den_final<<<blocks_for(M, 256), 256, 0, s>>>(acc_den, r.lines(), x.dr, p->bpad, r.n_rho, inv,
+                                                    means + 2, p->den_cache.p);
+    CBN_LAUNCH_CHECK();
+    k_max_partial<<<kRed, 256, 0, s>>>(p->den_cache.p, M, p->red.p);
+    CBN_LAUNCH_CHECK();
+    k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, p->den_max.p);
+    CBN_LAUNCH_CHECK();
+    p->den_cached = true;
+}
+
+// phase 1
+void bp_views(cbn_projector_s* p, const float* frames, int lo, int hi, float2* acc,
+              cudaStream_t s) {
+    BpCtx x = bp_context(p, s);
+    bp_den(p, x, s);
+    bp_transpose(p, x, frames, lo, hi, acc, false, s);
+}
+
+// phase 2: acc (the summed accumulator) is consumed in place
+void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* grid,
+               cudaStream_t s) {
+    BpCtx x = bp_context(p, s);
+    bp_den(p, x, s);
+    const cbn_projector_config& c = p->c;
+    const RadialTables& r = p->brad;
+    if (p->timer.on) p->timer.begin("bp_lattice", s);
+    const double inv = bp_lattice_ifft(p, x, acc, s);
+    p->red.ensure(2 * kRed + 64);
+    double* means = p->red.p + 2 * kRed;        // num re, num im
+    projector_column_mean(acc, r.lines(), x.dr, p->bpad + r.n_rho / 2, inv, p->red.p, means, s);
+    const int64_t M = r.nodes();
     p->lattice.ensure((size_t)M);
-    k_bp_div<<<blocks_for(M, 256), 256, 0, s>>>(acc_num, p->den_cache.p, r.lines(), dr, p->bpad,
+    k_bp_div<<<blocks_for(M, 256), 256, 0, s>>>(acc, p->den_cache.p, r.lines(), x.dr, p->bpad,
                                                  r.n_rho, inv, means, p->den_max.p, c.den_tol,
                                                  p->lattice.p);
     CBN_LAUNCH_CHECK();
@@ -533,26 +600,49 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
     bsrc.sin_th = r.sin_theta.p;
     for (int d = 0; d < 3; ++d) bsrc.N[d] = n;
     bsrc.tri = c.basis == 0;
-    {
-        StageScope st_sp(p->timer, "bp_spread", s);
-        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * k3, s));
-        const BinPlan& bb = p->bspec_bins;
-        dispatch_j(sax[0].J, [&](auto jc) {
-            launch_spread3<decltype(jc)::value>(p->big.p, kbs, bb, bsrc, s);
-            return 0;
-        });
-    }
+    StageScope st_sp(p->timer, "bp_spread", s);
+    CBN_CUDA(cudaMemsetAsync(grid, 0, sizeof(float2) * x.k3, s));
+    // this part's share of the bin subproblems (each node belongs to one)
+    const BinPlan& bb = p->bspec_bins;
+    const int s0 = (int)((int64_t)bb.nsubs * part / nparts);
+    const int s1 = (int)((int64_t)bb.nsubs * (part + 1) / nparts);
+    dispatch_j(sax[0].J, [&](auto jc) {
+        launch_spread3<decltype(jc)::value>(grid, kbs, bb, bsrc, s, s0, s1);
+        return 0;
+    });
+}
+
+// phase 3: grid (the summed spread) is consumed in place
+void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s) {
+    build_backward_plan(p, s);
+    CBN_REQUIRE(p->bspec_fit, "bp_crop before bp_finish");
+    const AxisPlan* sax = p->bspec;
+    const int n = p->n_vol;
     long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
     StageScope st_ff(p->timer, "bp_ifft_crop", s);
-    p->fft.exec(p->fft.get(3, k3d, 1), p->big.p, p->big.p, CUFFT_INVERSE, s);
+    p->fft.exec(p->fft.get(3, k3d, 1), grid, grid, CUFFT_INVERSE, s);
     RemapAxis cax[3];
     const int64_t cstr[3] = {(int64_t)sax[1].K * sax[2].K, sax[2].K, 1};
     p->s32.ensure(3 * (size_t)n);
     CBN_CUDA(cudaMemcpyAsync(p->s32.p, p->bspec_s32.p, sizeof(float) * 3 * n,
                              cudaMemcpyDeviceToDevice, s));
     projector_build_tables(p, kTabCrop, sax, n, s, cax, cstr);
-    launch_remap<float2, kStoreRe>(3, p->big.p, vol, cax, (float)c.bp_normalization, s);
+    launch_remap<float2, kStoreRe>(3, grid, vol, cax, (float)p->c.bp_normalization, s);
     CBN_LAUNCH_CHECK();
+}
+
+void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s) {
+    BpCtx x = bp_context(p, s);
+    bp_views(p, frames, 0, p->g.n_views, p->padded.p, s);
+    bp_finish(p, p->padded.p, 0, 1, p->big.p, s);
+    bp_crop(p, p->big.p, vol, s);
+    (void)x;
+}
+
+void bp_sizes(cbn_projector_s* p, int64_t* lattice, int64_t* grid, cudaStream_t s) {
+    BpCtx x = bp_context(p, s);
+    *lattice = x.dsize;
+    *grid = x.k3;
 }
 
 }  // namespace cbn

@@ -531,26 +531,30 @@ constexpr int owned_warps() {
 }
 
 template <int J, int W, class Src>
-void launch_spread3_w(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s) {
+void launch_spread3_w(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s,
+                      int s0, int s1) {
     const size_t smem = spread_owned_smem_bytes<J, W>(bb.nreg);
     CBN_CUDA(cudaFuncSetAttribute(k_spread_owned<J, W, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    if (bb.nsubs > 0)
-        k_spread_owned<J, W><<<bb.nsubs, W * 32, smem, s>>>(grid, kb, bb.geom<3>(), src, bb.perm.p,
-                                                            bb.subs.p);
+    if (s1 > s0)
+        k_spread_owned<J, W><<<s1 - s0, W * 32, smem, s>>>(grid, kb, bb.geom<3>(), src, bb.perm.p,
+                                                           bb.subs.p + s0);
     CBN_LAUNCH_CHECK();
 }
 
 int spread_warps_override();   // CBN_SPREAD_W (tuning experiments), 0 = default
 
+// subproblems [s0, s1) of the plan (default: all)
 template <int J, class Src>
-void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s) {
+void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src& src, cudaStream_t s,
+                    int s0 = 0, int s1 = -1) {
     CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
+    if (s1 < 0) s1 = bb.nsubs;
     switch (spread_warps_override()) {
-        case 1: return launch_spread3_w<J, 1>(grid, kb, bb, src, s);
-        case 2: return launch_spread3_w<J, 2>(grid, kb, bb, src, s);
-        case 4: return launch_spread3_w<J, 4>(grid, kb, bb, src, s);
-        default: return launch_spread3_w<J, owned_warps<J>()>(grid, kb, bb, src, s);
+        case 1: return launch_spread3_w<J, 1>(grid, kb, bb, src, s, s0, s1);
+        case 2: return launch_spread3_w<J, 2>(grid, kb, bb, src, s, s0, s1);
+        case 4: return launch_spread3_w<J, 4>(grid, kb, bb, src, s, s0, s1);
+        default: return launch_spread3_w<J, owned_warps<J>()>(grid, kb, bb, src, s, s0, s1);
     }
 }
 

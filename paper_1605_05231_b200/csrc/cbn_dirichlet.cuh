@@ -117,7 +117,7 @@ k_dir_spread(float2* __restrict__ x, float2* __restrict__ den, DirGrid g, Pos sr
     bool valid;
     src.position(i, pos, valid);
     if (!valid) return;
-    const float2 y = cin ? cin[i] : make_float2(rin[i], 0.f);
+    const float2 y = !x ? make_float2(0.f, 0.f) : (cin ? cin[i] : make_float2(rin[i], 0.f));
     if (y.x == 0.f && y.y == 0.f && !den) return;
     int c0[T], c1[T], c2[T];
     float2 w0[T], w1[T], w2[T];
@@ -134,7 +134,7 @@ k_dir_spread(float2* __restrict__ x, float2* __restrict__ den, DirGrid g, Pos sr
             for (int c = 0; c < T; ++c) {
                 const float2 wk = cmul(wab, w2[c]);     // conj(wk) * y
                 const int64_t e = row + c2[c] * g.st[2];
-                if (y.x != 0.f || y.y != 0.f)
+                if (x && (y.x != 0.f || y.y != 0.f))
                     atomicAdd(x + e, make_float2(wk.x * y.x + wk.y * y.y, wk.x * y.y - wk.y * y.x));
                 if (den) atomicAdd(den + e, make_float2(wk.x, -wk.y));
             }

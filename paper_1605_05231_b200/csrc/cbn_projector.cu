@@ -1038,6 +1038,10 @@ void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cuda
 // backprojector lives in cbn_backproject.cu
 namespace cbn {
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s);
+void bp_views(cbn_projector_s* p, const float* frames, int lo, int hi, float2* acc, cudaStream_t s);
+void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* grid, cudaStream_t s);
+void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s);
+void bp_sizes(cbn_projector_s* p, int64_t* lattice, int64_t* grid, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
 void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
                                  bool reverse, cudaStream_t s) {
@@ -1173,6 +1177,56 @@ int cbn_backproject(cbn_projector* p, const float* frames, float* vol, void* str
         CBN_REQUIRE(p && vol && frames, "null argument");
         CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
         backproject_impl(p, frames, vol, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject_sizes(cbn_projector* p, int64_t* lattice_elems, int64_t* grid_elems,
+                          void* stream) {
+    try {
+        CBN_REQUIRE(p && lattice_elems && grid_elems, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        bp_sizes(p, lattice_elems, grid_elems, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject_views(cbn_projector* p, const float* frames, int32_t lo, int32_t hi,
+                          void* lattice, void* stream) {
+    try {
+        CBN_REQUIRE(p && frames && lattice, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        bp_views(p, frames, lo, hi, static_cast<float2*>(lattice), static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject_finish(cbn_projector* p, void* lattice, int32_t part, int32_t nparts, void* grid,
+                           void* stream) {
+    try {
+        CBN_REQUIRE(p && lattice && grid, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        CBN_REQUIRE(nparts >= 1 && 0 <= part && part < nparts, "bad part");
+        bp_finish(p, static_cast<float2*>(lattice), part, nparts, static_cast<float2*>(grid),
+                  static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject_crop(cbn_projector* p, void* grid, float* vol, void* stream) {
+    try {
+        CBN_REQUIRE(p && grid && vol, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        bp_crop(p, static_cast<float2*>(grid), vol, static_cast<cudaStream_t>(stream));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

@@ -114,8 +114,8 @@ static __global__ void k_transpose_vals(const float* __restrict__ in, int nv, in
 }
 
 // One CTA per grid column (rho, theta); threads over phi.  Views [vlo, vlo+nv)
-// of valsT [target][nv]; writes (num, 0) -- and (den, 0) if gden -- to every
-// cell of the column.
+// of valsT [target][nv]; writes (num, 0) if gnum -- and (den, 0) if gden -- to
+// every cell of the column (den-only passes: gnum and valsT null).
 constexpr int kRsColThreads = 256;
 constexpr int kRsColMaxPhi = 3 * kRsColThreads;
 
@@ -142,7 +142,7 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
                 const int rel = v - vlo;
                 if (v * shift == d && rel >= 0 && rel < nv) {
                     const float wk = e.wab * e.w2[c];
-                    num[r] = fmaf(wk, __ldg(vt + rel), num[r]);
+                    if (valsT) num[r] = fmaf(wk, __ldg(vt + rel), num[r]);
                     den[r] += wk;
                 }
             }
@@ -152,7 +152,7 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
     for (int r = 0; r < 3; ++r) {
         const int phi = threadIdx.x + r * kRsColThreads;
         if (phi >= K2) break;
-        gnum[col * K2 + phi] = make_float2(num[r], 0.f);
+        if (gnum) gnum[col * K2 + phi] = make_float2(num[r], 0.f);
         if (gden) gden[col * K2 + phi] = make_float2(den[r], 0.f);
     }
 }
@@ -186,8 +186,8 @@ k_rs_gather_cols2(float2* __restrict__ gnum, float2* __restrict__ gden, int V,
         r1 += r1 < 0 ? V : 0;
         const bool ok0 = r0 < nv, ok1 = r1 < nv;
         const float* vt = valsT + (size_t)e.t * nv;
-        const float x0 = ok0 ? __ldg(vt + r0) : 0.f;
-        const float x1 = ok1 ? __ldg(vt + r1) : 0.f;
+        const float x0 = (ok0 && valsT) ? __ldg(vt + r0) : 0.f;
+        const float x1 = (ok1 && valsT) ? __ldg(vt + r1) : 0.f;
         const float u0 = ok0 ? 1.f : 0.f, u1 = ok1 ? 1.f : 0.f;
         const float w0 = e.wab * e.w2[0], w1 = e.wab * e.w2[1], w2 = e.wab * e.w2[2];
         if ((d & 1) == 0) {
@@ -202,8 +202,7 @@ k_rs_gather_cols2(float2* __restrict__ gnum, float2* __restrict__ gden, int V,
             de = fmaf(w1, u1, de);
         }
     }
-    float4* gn = reinterpret_cast<float4*>(gnum + col * 2 * V) + i;
-    *gn = make_float4(ne, 0.f, no, 0.f);
+    if (gnum) *(reinterpret_cast<float4*>(gnum + col * 2 * V) + i) = make_float4(ne, 0.f, no, 0.f);
     if (gden) *(reinterpret_cast<float4*>(gden + col * 2 * V) + i) = make_float4(de, 0.f, dn, 0.f);
 }
 

@@ -155,6 +155,61 @@ class Projector:
                    "nufft_backproject")
         return out
 
+    # ---- backprojector phases (view / node sharding)
+    def backproject_sizes(self):
+        """(lattice_elems, grid_elems): complex64 sizes of the phase buffers."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.load().cbn_backproject_sizes(self._h, ctypes.byref(a), ctypes.byref(b),
+                                                     self._s), "nufft_backproject")
+        return int(a.value), int(b.value)
+
+    def backproject_views(self, frames, view_lo: int, view_hi: int, out=None):
+        """Phase 1: transposed resample of views [view_lo, view_hi) (frames holds
+        exactly those views) into a padded-lattice accumulator."""
+        t = _device.require_cuda()
+        f = _device.to_device(frames, t.float32)
+        if tuple(f.shape) != (view_hi - view_lo, self.geom.nu, self.geom.nv):
+            raise ValueError("frames must be (view_hi - view_lo, nu, nv)")
+        n_lat, _ = self.backproject_sizes()
+        out = t.empty(n_lat, dtype=t.complex64, device="cuda") if out is None else out
+        _lib.check(_lib.load().cbn_backproject_views(self._h, _device.ptr(f), int(view_lo),
+                                                     int(view_hi), _device.ptr(out), self._s),
+                   "nufft_backproject")
+        return out
+
+    def backproject_finish(self, lattice, part: int = 0, nparts: int = 1, out=None):
+        """Phase 2: from the summed accumulator (consumed), spread node part
+        `part` of `nparts` into a (2N)^3 grid."""
+        t = _device.require_cuda()
+        _, n_grid = self.backproject_sizes()
+        out = t.empty(n_grid, dtype=t.complex64, device="cuda") if out is None else out
+        _lib.check(_lib.load().cbn_backproject_finish(self._h, _device.ptr(lattice), int(part),
+                                                      int(nparts), _device.ptr(out), self._s),
+                   "nufft_backproject")
+        return out
+
+    def backproject_crop(self, grid):
+        """Phase 3: inverse FFT, crop and deapodisation of the summed grid (consumed)."""
+        t = _device.require_cuda()
+        out = t.empty((self.n,) * 3, dtype=t.float32, device="cuda")
+        _lib.check(_lib.load().cbn_backproject_crop(self._h, _device.ptr(grid), _device.ptr(out),
+                                                    self._s), "nufft_backproject")
+        return out
+
+    def backproject_sharded(self, frames_local, view_lo: int, view_hi: int, group=None):
+        """nufft_backproject over a process group: this rank's views and 1/world of
+        the radial nodes, with the two sums as NCCL all-reduces."""
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        lat = self.backproject_views(frames_local, view_lo, view_hi)
+        if world > 1:
+            dist.all_reduce(lat, group=group)
+        grid = self.backproject_finish(lat, rank, world)
+        if world > 1:
+            dist.all_reduce(grid, group=group)
+        return self.backproject_crop(grid)
+
     # ---- stages
     def radial_lattice(self, vol):
         """Complex lattice in node order (n_phi, n_theta, n_rho)."""

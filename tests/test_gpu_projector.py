@@ -180,3 +180,25 @@ def test_view_range_matches_full(pl, golden_n16):
     full = proj.forward(g["vol"]).cpu().numpy()
     parts = [proj.forward(g["vol"], lo, hi).cpu().numpy() for lo, hi in ((0, 3), (3, 7), (7, 12))]
     assert rel_l2(np.concatenate(parts), full) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["pipeline_n16", "pipeline_n12_v24"])
+def test_backprojector_phases_shard_exactly(pl, name):
+    """The three backprojector phases split over 'ranks' (view ranges and node
+    parts, sums done here) reproduce the one-call backprojection -- the
+    decomposition the NCCL all-reduces of backproject_sharded rely on."""
+    g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    proj = pl.Projector(geom, cfg, n, voxel, 2)
+    import torch
+    frames = torch.from_numpy(g["frames"].astype(np.float32)).cuda()
+    one = proj.backproject(frames).cpu().numpy()
+    for world in (2, 3):
+        cuts = [views * r // world for r in range(world + 1)]
+        lat = sum(proj.backproject_views(frames[cuts[r]:cuts[r + 1]], cuts[r], cuts[r + 1])
+                  for r in range(world))
+        grid = sum(proj.backproject_finish(lat.clone(), r, world) for r in range(world))
+        got = proj.backproject_crop(grid).cpu().numpy()
+        assert rel_l2(got, one) < 1e-5, world
+    assert rel_l2(one, g["bp"]) < TOL
