@@ -179,9 +179,13 @@ def run_ours(args):
 
     if direction == 1:
         x_dev = torch.from_numpy(vol_host).cuda()
-
-        def step():
-            return proj.forward(x_dev, lo, hi)
+        if world > 1:
+            # radial nodes and views sharded; the lattice summed with one NCCL all-reduce
+            def step():
+                return proj.forward_sharded(x_dev, lo, hi)
+        else:
+            def step():
+                return proj.forward(x_dev, lo, hi)
     else:
         frames_dev = Projector(w.geom, w.cfg, w.n, w.voxel, 1).forward(torch.from_numpy(vol_host).cuda())
         x_dev = frames_dev
@@ -244,7 +248,7 @@ def run_ours(args):
         def e2e_step():
             dev = host_in.to("cuda", non_blocking=True)
             if direction == 1:
-                out = proj.forward(dev, lo, hi)
+                out = proj.forward_sharded(dev, lo, hi) if world > 1 else proj.forward(dev, lo, hi)
             elif world > 1:
                 out = proj.backproject_sharded(dev[lo:hi].contiguous(), lo, hi)
             else:
@@ -322,9 +326,9 @@ def run_ours(args):
                                f"{w.spec.n_rho}x{w.spec.n_theta}x{w.spec.n_phi} radial lattice, "
                                f"{V} views of {w.geom.nu}^2, KB J=6 sigma=2, resample J=3",
                    "views": V, "views_per_rank": hi - lo,
-                   "parallelism": f"views sharded x{world}" + ("" if direction == 1 or world == 1
-                                                               else ", radial nodes sharded, "
-                                                               "NCCL all-reduce of lattice + grid"),
+                   "parallelism": f"views sharded x{world}" + (
+                       "" if world == 1 else ", radial nodes sharded, NCCL all-reduce of the "
+                       + ("lattice" if direction == 1 else "lattice + grid")),
                    "l2": "working set > L2 (resample grid 2.4 GB per view batch)"},
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -161,6 +161,18 @@ int cbn_projector_scratch_bytes(const cbn_projector* proj, int64_t* bytes);
  * projection value is non-finite (checked on device, synchronises). */
 int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
                         int32_t view_lo, int32_t view_hi, void* stream);
+/* nufft_forward_project in two phases, for sharding the radial nodes and the
+ * views across devices; cbn_forward_project == lattice(0 of 1)
+ * + views.  lattice [device] complex64 x lattice_elems, caller-owned:
+ * lattice: spectrum-gather values of node part `part` of `nparts` (zero at the
+ *          other nodes, before the radial IFFT) -- sum the parts over ranks
+ * views:   consumes the summed lattice; views [lo, hi) into frames [device]
+ *          float32 (hi - lo) x nu x nv; CBN_ENONFINITE as cbn_forward_project */
+int cbn_forward_lattice_size(cbn_projector* proj, int64_t* lattice_elems, void* stream);
+int cbn_forward_lattice(cbn_projector* proj, const float* vol, int32_t part, int32_t nparts,
+                        void* lattice, void* stream);
+int cbn_forward_views(cbn_projector* proj, void* lattice, float* frames, int32_t lo, int32_t hi,
+                      void* stream);
 /* nufft_backproject (pipeline.py:150-212): frames [device] float32 V x nu x nv
  * -> vol [device] float32 N^3 */
 int cbn_backproject(cbn_projector* proj, const float* frames, float* vol, void* stream);

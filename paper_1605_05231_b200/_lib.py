@@ -79,6 +79,9 @@ _SIGS = {
     "cbn_projector_set_ls_rows": (ctypes.c_int, [c_vp, c_i64, P_i64, c_i64]),
     "cbn_projector_scratch_bytes": (ctypes.c_int, [c_vp, P_i64]),
     "cbn_forward_project": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "cbn_forward_lattice_size": (ctypes.c_int, [c_vp, P_i64, c_vp]),
+    "cbn_forward_lattice": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "cbn_forward_views": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_backproject": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_backproject_sizes": (ctypes.c_int, [c_vp, P_i64, P_i64, c_vp]),
     "cbn_backproject_views": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),

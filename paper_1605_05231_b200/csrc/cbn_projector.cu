@@ -594,7 +594,14 @@ int64_t ktot(const AxisPlan* ax) { return (int64_t)ax[0].K * ax[1].K * ax[2].K; 
 // radial lattice in raw layout (IFFT output, ifftshifted rho) into p->lattice;
 // with `spectrum` the image_to_radial_spectrum values go there instead (node
 // order, no basis transfer / derivative / IFFT)
-void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum = nullptr) {
+// spectrum gather at the radial nodes: `spectrum` set -> image_to_radial_spectrum
+// values in node order; else the pre-IFFT lattice into `lat` (default
+// p->lattice) followed by the radial IFFT.  nparts > 1: only the nodes of
+// bin-subproblem share `part` (lat zeroed first); raw_only: stop before the
+// IFFT (the sharded caller sums the shares, then fwd_views runs it)
+void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum = nullptr,
+                        int part = 0, int nparts = 1, float2* lat = nullptr,
+                        bool raw_only = false) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fspec;
     const int64_t M = r.nodes();
@@ -630,8 +637,10 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         StageScope st(p->timer, "spectrum_fft", s);
         p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
     }
+    if (!lat) lat = p->lattice.p;
+    if (nparts > 1) CBN_CUDA(cudaMemsetAsync(lat, 0, sizeof(float2) * M, s));
     SpecOut epi;
-    epi.out = spectrum ? spectrum : p->lattice.p;
+    epi.out = spectrum ? spectrum : lat;
     epi.om_phys = r.om_phys.p;
     for (int d = 0; d < 3; ++d) epi.N[d] = n;
     epi.n_rho = r.n_rho;
@@ -650,19 +659,22 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     {
         StageScope st(p->timer, "spectrum_gather", s);
         const BinPlan& bp = p->fspec_bins;
+        const int s0 = (int)((int64_t)bp.nsubs * part / nparts);
+        const int s1 = (int)((int64_t)bp.nsubs * (part + 1) / nparts);
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
-            k_gather_binned<3, J><<<bp.nsubs, 256, sizeof(float2) * bp.nreg, s>>>(
-                p->big.p, kb, bp.geom<3>(), r.src(), epi, bp.perm.p, bp.subs.p);
+            if (s1 > s0)
+                k_gather_binned<3, J><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
+                    p->big.p, kb, bp.geom<3>(), r.src(), epi, bp.perm.p, bp.subs.p + s0);
             return 0;
         });
         CBN_LAUNCH_CHECK();
     }
-    if (spectrum) return;
+    if (spectrum || raw_only) return;
     // centred IFFT along rho (radon_fourier.py:122-124,133-135); 1/(n d_rho) applied by consumers
     long long nr1[1] = {r.n_rho};
     StageScope st(p->timer, "radial_ifft", s);
-    p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_INVERSE, s);
+    p->fft.exec(p->fft.get(1, nr1, r.lines()), lat, lat, CUFFT_INVERSE, s);
 }
 
 // lattice spectrum for resampling: fftn(pad(origin_avg(lattice))) into p->padded
@@ -1019,18 +1031,35 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
     flush();
 }
 
-void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s) {
-    build_forward(p, s);
+// views [lo, hi) from a radial lattice (after the radial IFFT) -> frames
+void project_views(P* p, const float2* lat, float* frames, int lo, int hi, cudaStream_t s) {
     p->flag.ensure(1);
     CBN_CUDA(cudaMemsetAsync(p->flag.p, 0, sizeof(int), s));
-    radial_lattice_raw(p, vol, s);
     const RadialTables& r = p->frad;
-    lattice_spectrum(p, p->lattice.p, r.n_rho - r.n_rho / 2, (float)(1.0 / (r.n_rho * r.d_rho)), s);
+    lattice_spectrum(p, lat, r.n_rho - r.n_rho / 2, (float)(1.0 / (r.n_rho * r.d_rho)), s);
     resample_and_reverse(p, lo, hi, frames, s);
     int flag = 0;
     CBN_CUDA(cudaMemcpyAsync(&flag, p->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     CBN_CUDA(cudaStreamSynchronize(s));
     if (flag) throw Error(CBN_ENONFINITE, "non-finite projection values");
+}
+
+// sharded forward, phase 2: the summed pre-IFFT lattice (consumed) -> views
+void fwd_views(P* p, float2* lat, float* frames, int lo, int hi, cudaStream_t s) {
+    build_forward(p, s);
+    const RadialTables& r = p->frad;
+    long long nr1[1] = {r.n_rho};
+    {
+        StageScope st(p->timer, "radial_ifft", s);
+        p->fft.exec(p->fft.get(1, nr1, r.lines()), lat, lat, CUFFT_INVERSE, s);
+    }
+    project_views(p, lat, frames, lo, hi, s);
+}
+
+void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s) {
+    build_forward(p, s);
+    radial_lattice_raw(p, vol, s);
+    project_views(p, p->lattice.p, frames, lo, hi, s);
 }
 
 }  // namespace
@@ -1177,6 +1206,47 @@ int cbn_backproject(cbn_projector* p, const float* frames, float* vol, void* str
         CBN_REQUIRE(p && vol && frames, "null argument");
         CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
         backproject_impl(p, frames, vol, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_lattice_size(cbn_projector* p, int64_t* lattice_elems, void* stream) {
+    try {
+        CBN_REQUIRE(p && lattice_elems, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        build_forward(p, static_cast<cudaStream_t>(stream));
+        *lattice_elems = p->frad.nodes();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_lattice(cbn_projector* p, const float* vol, int32_t part, int32_t nparts,
+                        void* lattice, void* stream) {
+    try {
+        CBN_REQUIRE(p && vol && lattice, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(nparts >= 1 && 0 <= part && part < nparts, "bad part");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        // the pre-IFFT lattice values of this share (fwd_views runs the IFFT)
+        radial_lattice_raw(p, vol, s, nullptr, part, nparts, static_cast<float2*>(lattice), true);
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_views(cbn_projector* p, void* lattice, float* frames, int32_t lo, int32_t hi,
+                      void* stream) {
+    try {
+        CBN_REQUIRE(p && lattice && frames, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        fwd_views(p, static_cast<float2*>(lattice), frames, lo, hi, static_cast<cudaStream_t>(stream));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

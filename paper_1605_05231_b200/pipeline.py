@@ -155,6 +155,44 @@ class Projector:
                    "nufft_backproject")
         return out
 
+    # ---- forward phases (node / view sharding)
+    def forward_lattice(self, vol, part: int = 0, nparts: int = 1, out=None):
+        """Phase 1: spectrum-gather values of radial-node part `part` of `nparts`
+        (zeros elsewhere), before the radial IFFT."""
+        t = _device.require_cuda()
+        v = _device.to_device(vol, t.float32)
+        if tuple(v.shape) != (self.n,) * 3:
+            raise ValueError(f"volume must be ({self.n},)*3")
+        m = ctypes.c_int64()
+        _lib.check(_lib.load().cbn_forward_lattice_size(self._h, ctypes.byref(m), self._s))
+        out = t.empty(int(m.value), dtype=t.complex64, device="cuda") if out is None else out
+        _lib.check(_lib.load().cbn_forward_lattice(self._h, _device.ptr(v), int(part), int(nparts),
+                                                   _device.ptr(out), self._s),
+                   "nufft_forward_project")
+        return out
+
+    def forward_views(self, lattice, view_lo: int = 0, view_hi: int | None = None):
+        """Phase 2: from the summed lattice (consumed), views [view_lo, view_hi)."""
+        t = _device.require_cuda()
+        view_hi = self.geom.n_views if view_hi is None else view_hi
+        out = t.empty((view_hi - view_lo, self.geom.nu, self.geom.nv), dtype=t.float32,
+                      device="cuda")
+        _lib.check(_lib.load().cbn_forward_views(self._h, _device.ptr(lattice), _device.ptr(out),
+                                                 int(view_lo), int(view_hi), self._s),
+                   "nufft_forward_project")
+        return out
+
+    def forward_sharded(self, vol, view_lo: int, view_hi: int, group=None):
+        """nufft_forward_project over a process group: 1/world of the radial nodes
+        (lattice summed with one NCCL all-reduce), then this rank's views."""
+        import torch.distributed as dist
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        lat = self.forward_lattice(vol, rank, world)
+        if world > 1:
+            dist.all_reduce(lat, group=group)
+        return self.forward_views(lat, view_lo, view_hi)
+
     # ---- backprojector phases (view / node sharding, SURVEY.md 8(e))
     def backproject_sizes(self):
         """(lattice_elems, grid_elems): complex64 sizes of the phase buffers."""

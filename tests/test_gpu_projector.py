@@ -202,3 +202,24 @@ def test_backprojector_phases_shard_exactly(pl, name):
         got = proj.backproject_crop(grid).cpu().numpy()
         assert rel_l2(got, one) < 1e-5, world
     assert rel_l2(one, g["bp"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["pipeline_n16", "pipeline_n12_v24"])
+def test_forward_phases_shard_exactly(pl, name):
+    """Forward phases split over 'ranks' (radial-node parts summed, then view
+    ranges) reproduce the one-call forward projection -- what the NCCL
+    all-reduce of forward_sharded relies on."""
+    import torch
+    g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    proj = pl.Projector(geom, cfg, n, voxel, 1)
+    vol = torch.from_numpy(g["vol"]).cuda()
+    one = proj.forward(vol).cpu().numpy()
+    assert rel_l2(one, g["frames"]) < TOL
+    for world in (1, 2, 3):
+        lat = sum(proj.forward_lattice(vol, r, world) for r in range(world))
+        cuts = [views * r // world for r in range(world + 1)]
+        got = np.concatenate([proj.forward_views(lat.clone(), cuts[r], cuts[r + 1]).cpu().numpy()
+                              for r in range(world)])
+        assert rel_l2(got, one) < 1e-6, world
