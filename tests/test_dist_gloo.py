@@ -79,3 +79,77 @@ def test_gloo_sharded_forward_matches_single(tmp_path):
     ref = orc.forward_project(vol, voxel, geom, cfg, target_batch=cfg.n_mu * cfg.n_t * 3)
     assert np.allclose(res["full"], ref, rtol=0, atol=1e-12 * np.abs(ref).max())
     assert float(res["t"]) == 2.0
+
+
+class _FakeProjector:
+    """CPU stand-in for the device phases: fixed random linear maps with the same
+    sharding contract (node parts summed over ranks, view ranges local)."""
+
+    def __init__(self, views=6, n_vox=5, m=9):
+        import torch
+        g = torch.Generator().manual_seed(0)
+        self.views = views
+        self.A = torch.randn(m, n_vox, generator=g, dtype=torch.float64)       # vol -> lattice
+        self.B = torch.randn(views, m, generator=g, dtype=torch.float64)       # lattice -> views
+        self.C = torch.randn(m, views, generator=g, dtype=torch.float64)       # views -> lattice
+        self.D = torch.randn(7, m, generator=g, dtype=torch.float64)           # lattice -> grid
+        self.E = torch.randn(n_vox, 7, generator=g, dtype=torch.float64)       # grid -> volume
+
+    @staticmethod
+    def _rows(n, part, nparts):
+        import torch
+        mask = torch.zeros(n, 1, dtype=torch.float64)
+        mask[part::nparts] = 1.0
+        return mask
+
+    def forward_lattice(self, vol, part, nparts):
+        return (self.A @ vol) * self._rows(self.A.shape[0], part, nparts)[:, 0]
+
+    def forward_views(self, lat, lo, hi):
+        return (self.B @ lat)[lo:hi]
+
+    def backproject_views(self, frames_local, lo, hi):
+        return self.C[:, lo:hi] @ frames_local
+
+    def backproject_finish(self, lat, part, nparts):
+        return (self.D * self._rows(self.D.shape[1], part, nparts)[:, 0]) @ lat
+
+    def backproject_crop(self, grid):
+        return self.E @ grid
+
+
+def _sharded_worker(rank, world, port, result_path):
+    import sys
+    import torch
+    import torch.distributed as dist
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    from paper_1605_05231_b200 import sharding
+    from paper_1605_05231_b200.pipeline import Projector
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    fake = _FakeProjector()
+    vol = torch.arange(5, dtype=torch.float64) + 1.0
+    frames = torch.linspace(-1.0, 2.0, fake.views, dtype=torch.float64)
+    lo, hi = sharding.view_shard(fake.views, world, rank)
+    fwd_local = Projector.forward_sharded(fake, vol, lo, hi)
+    fwd = sharding.gather_views(fwd_local, fake.views)
+    bp = Projector.backproject_sharded(fake, frames[lo:hi], lo, hi)
+    if rank == 0:
+        np.savez(result_path, fwd=fwd.numpy(), bp=bp.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_sharded_phase_orchestration(tmp_path):
+    """Projector.forward_sharded / backproject_sharded over a gloo world of 2: the
+    node-part sums (all-reduce) and view ranges give the single-process maps."""
+    out = str(tmp_path / "res.npz")
+    mp.spawn(_sharded_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    res = np.load(out)
+    f = _FakeProjector()
+    import torch
+    vol = torch.arange(5, dtype=torch.float64) + 1.0
+    frames = torch.linspace(-1.0, 2.0, f.views, dtype=torch.float64)
+    assert np.allclose(res["fwd"], (f.B @ (f.A @ vol)).numpy(), rtol=1e-12)
+    assert np.allclose(res["bp"], (f.E @ (f.D @ (f.C @ frames))).numpy(), rtol=1e-12)
