@@ -573,7 +573,7 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
         const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
         p->bspec_s32.alloc(3 * (size_t)n);
         ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->bspec_s32.p, n, s);
-        const int tile[3] = {kTile3, kTile3, kTile3};
+        const int tile[3] = {kTile3, kTile3, kTile3Fast};
         dispatch_j(sax[0].J, [&](auto jc) {
             build_bins<3, decltype(jc)::value>(p->bspec_bins, r.src(), kbs, M, tile, kMaxSub, s, true);
             return 0;

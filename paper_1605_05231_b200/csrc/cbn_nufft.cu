@@ -217,8 +217,9 @@ void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t
     }
     if constexpr (D >= 2) {
         // bin-sorted order for the shared-memory gather/spread (one-time plan step)
-        const int edge = D == 3 ? 8 : 16;
-        const int tile[3] = {edge, edge, edge};
+        // 3D: 8 x 8 x 16 cells (the pitch-padded region holds 16 + J - 1 along z
+        // at no extra shared memory for J = 6, 8); 2D: 16 x 16
+        const int tile[3] = {D == 3 ? 8 : 16, D == 3 ? 8 : 16, 16};
         dispatch_j(p->J, [&](auto jc) {
             build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true);
             return 0;

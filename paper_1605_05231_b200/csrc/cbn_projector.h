@@ -59,7 +59,9 @@ constexpr int kGrTile = 16;    // forward (gather) tile edge
 constexpr int kGrTileRev = 8;  // reverse (owner-computes spread) tile edge
 constexpr int kGrVG = 8;       // views per CTA in the binned Grangeat gather
 
-constexpr int kTile3 = 8;      // 3D bin edge (oversampled cells)
+constexpr int kTile3 = 8;      // 3D bin edge (oversampled cells), axes 0 and 1
+constexpr int kTile3Fast = 16; // 3D bin edge along the fastest axis: the region's pitch
+                               // padding (P = J mod 16) already covers 16 + J - 1 cells
 constexpr int kMaxSub = 1024;  // points per subproblem
 
 // Per-batch resample scalings of one direction (plan data: they depend only on
