@@ -650,7 +650,8 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
     if (!p->fspec_bins.ready) {
         StageScope st(p->timer, "spectrum_bins", s);
-        const int tile[3] = {kTile3, 2 * kTile3, kTile3Fast};   // gather-only: no staging, larger tile
+        // gather-only plan (no staging): 8 x 16 x 16 while the region stays under 48 KB
+        const int tile[3] = {kTile3, ax[0].J <= 6 ? 2 * kTile3 : kTile3, kTile3Fast};
         dispatch_j(ax[0].J, [&](auto jc) {
             build_bins<3, decltype(jc)::value>(p->fspec_bins, r.src(), kb, M, tile, kMaxSub, s);
             return 0;
