@@ -100,4 +100,34 @@ __global__ void k_build_table(int mode, int N, int K, const float* __restrict__ 
     }
 }
 
+__global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict__ dst,
+                              RemapAxis a0, RemapAxis a1, RemapAxis a2, float gain) {
+    const int h2 = a2.n / 2 + 1;
+    const int e2 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e2 >= h2) return;
+    const int e[3] = {(int)blockIdx.z, (int)blockIdx.y, e2};
+    const RemapAxis ax[3] = {a0, a1, a2};
+    float2 v[2];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        float sc = gain;
+        int64_t so = 0;
+        bool zero = false;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            int k = e[d];
+            if (side) k = k == 0 ? 0 : ax[d].n - k;     // (-k) mod n
+            const int id = ax[d].idx[k];
+            zero |= id < 0;
+            so += (int64_t)id * ax[d].sstride;
+            sc *= ax[d].scale[k];
+        }
+        const float2 g = zero ? make_float2(0.f, 0.f) : src[so];
+        v[side] = make_float2(g.x * sc, g.y * sc);
+    }
+    // conj(P[e]) + P[-e], halved
+    dst[((size_t)e[0] * a1.n + e[1]) * h2 + e2] =
+        make_float2(0.5f * (v[0].x + v[1].x), 0.5f * (v[1].y - v[0].y));
+}
+
 }  // namespace cbn

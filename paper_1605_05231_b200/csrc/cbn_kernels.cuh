@@ -256,6 +256,13 @@ __global__ void k_remap(const SrcT* __restrict__ src, void* __restrict__ dst, Re
     }
 }
 
+// 3D pad to the half spectrum of a real transform: out[e0][e1][e2], e2 <=
+// n2 / 2, holds conj of the Hermitian part of the padded grid P,
+// (conj(P[e]) + P[-e]) / 2, so that a complex-to-real FFT of it gives
+// Re(forward FFT of P) (the only part the resample gather reads).
+__global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict__ dst,
+                              RemapAxis a0, RemapAxis a1, RemapAxis a2, float gain);
+
 // Table modes for k_build_table.
 enum TableMode {
     kTabPad = 0,      // g in [0,K): source n of the rolled placement (n - N//2) mod K, scale s[n]

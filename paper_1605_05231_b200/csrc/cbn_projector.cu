@@ -195,6 +195,86 @@ k_resample_views(const float2* __restrict__ G, int K0, int K1, int K2,
     }
 }
 
+// J = 3 (the reference default) view-lane gather on precomputed rows: the nine
+// (rho, theta) tap rows of a view-0 target as 32-bit cell offsets of the
+// phi-fast grid and the nine rho x theta weight products, so a lane's work is
+// nine row bases, 27 loads of real parts and 36 FMAs -- the warp-uniform
+// index math of k_resample_views is done once per plan instead of per lane.
+struct RsRow3 {
+    unsigned int row[9];   // (wrap(f0 + a) K1 + wrap(f1 + b)) K2, a major
+    int f2;                // first phi tap of view 0
+    int valid;
+    float w2[3];
+    float wab[9];          // w0[a] w1[b]
+};
+
+__global__ void k_rs_rows3(const RsTap<3>* __restrict__ taps, int64_t n, int K0, int K1, int K2,
+                           RsRow3* __restrict__ out) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const RsTap<3> tp = taps[t];
+    RsRow3 r;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            r.row[a * 3 + b] = (unsigned)(((int64_t)wrapc(tp.f[0] + a, K0) * K1 +
+                                           wrapc(tp.f[1] + b, K1)) * K2);
+            r.wab[a * 3 + b] = tp.w[0][a] * tp.w[1][b];
+        }
+    r.f2 = tp.f[2];
+    r.valid = tp.valid;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) r.w2[c] = tp.w[2][c];
+    out[t] = r;
+}
+
+__global__ void __launch_bounds__(256)
+k_resample_rows3(const float* __restrict__ G, int es, int K2, const RsRow3* __restrict__ rows,
+                 int64_t per_view, int v0, int nviews, int shift, float* __restrict__ vals,
+                 const float* __restrict__ tscale, int n_t) {
+    __shared__ float tile[32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t0 = (int64_t)blockIdx.x * 32;
+    const int pshift = (int)(((int64_t)(v0 + lane) * shift) % K2);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        const int tl = warp * 4 + q;
+        const int64_t t = t0 + tl;
+        float out = 0.f;
+        if (t < per_view) {
+            const RsRow3& rr = rows[t];
+            if (rr.valid && lane < nviews) {
+                int c0 = rr.f2 - pshift;
+                c0 += c0 < 0 ? K2 : 0;
+                int c1 = c0 + 1, c2 = c0 + 2;
+                c1 -= c1 >= K2 ? K2 : 0;
+                c2 -= c2 >= K2 ? K2 : 0;
+                const float w0 = rr.w2[0], w1 = rr.w2[1], w2 = rr.w2[2];
+                float acc = 0.f;
+#pragma unroll
+                for (int ab = 0; ab < 9; ++ab) {
+                    const float* base = G + (size_t)es * rr.row[ab];   // es: floats per cell
+                    float r = w0 * __ldg(base + es * c0);
+                    r = fmaf(w1, __ldg(base + es * c1), r);
+                    r = fmaf(w2, __ldg(base + es * c2), r);
+                    acc = fmaf(rr.wab[ab], r, acc);
+                }
+                out = acc;   // Re(resample_apply): the real part of each cell
+            }
+        }
+        tile[lane][tl] = out;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int v = e >> 5, tt = e & 31;
+        if (v < nviews && t0 + tt < per_view) {
+            const float x = tile[v][tt];
+            vals[(size_t)v * per_view + t0 + tt] = tscale ? x * tscale[(t0 + tt) % n_t] : x;
+        }
+    }
+}
+
 // ----------------------------------------------------------------- kernels
 
 // lattice[line][j] = raw[line][(j - n//2) mod n] * scale   (fftshift of the IFFT)
@@ -768,6 +848,15 @@ void ensure_batch_plan(P* p, BatchPlan& bp, const UmbrellaTables& u, const Radia
 // G = FFT_2x(pad(fftshift(F) / size * scaling)) for a batch's scalings
 // (resample_apply + nufft_forward, resampling.py:146-147, nufft.py:226-231)
 // phi_fast: grid stored [rho][theta][phi] for k_resample_views, else [phi][theta][rho]
+bool views_in_lanes(const P* p);
+
+// the resample grid is kept as Re(G) only (C2R) on the views-in-lanes J = 3 path
+bool real_grid(const P* p) {
+    const char* off = std::getenv("CBN_COMPLEX_GRID");
+    if (off && off[0] == '1') return false;
+    return views_in_lanes(p) && p->fres[0].J == 3 && p->c.method == 0;
+}
+
 void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool phi_fast = false) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fres;   // (phi, theta, rho)
@@ -785,8 +874,28 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
         off += ax[d].K;
     }
     if (phi_fast) std::swap(rax[0], rax[2]);
-    p->big.ensure((size_t)ktot(ax));
     const double size = (double)dr * r.n_theta * r.n_phi;
+    if (real_grid(p)) {
+        // only Re(G) is read (real weights, Re of the result): pad straight to
+        // the conjugated Hermitian half spectrum and complex-to-real FFT it,
+        // into a float grid behind the half spectrum in `big`
+        const long long kd3[3] = {rax[0].n, rax[1].n, rax[2].n};
+        const int64_t half = (int64_t)kd3[0] * kd3[1] * (kd3[2] / 2 + 1);
+        p->big.ensure((size_t)half + (size_t)(kd3[0] * kd3[1] * kd3[2] + 1) / 2);
+        {
+            StageScope st(p->timer, "resample_pad", s);
+            dim3 grid((unsigned)((kd3[2] / 2 + 1 + 255) / 256), (unsigned)kd3[1], (unsigned)kd3[0]);
+            k_remap_herm3<<<grid, 256, 0, s>>>(p->padded.p, p->big.p, rax[0], rax[1], rax[2],
+                                               (float)(1.0 / size));
+            CBN_LAUNCH_CHECK();
+        }
+        StageScope st(p->timer, "resample_fft", s);
+        p->fft.exec_c2r(p->fft.get_c2r3(kd3), p->big.p,
+                        reinterpret_cast<float*>(p->big.p + half), s);
+        p->grid_re = reinterpret_cast<float*>(p->big.p + half);
+        return;
+    }
+    p->big.ensure((size_t)ktot(ax));
     {
         StageScope st(p->timer, "resample_pad", s);
         launch_remap<float2, kStoreC>(3, p->padded.p, p->big.p, rax, (float)(1.0 / size), s);
@@ -834,9 +943,27 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
             k_rs_taps<J><<<blocks_for(per_view, 256), 256, 0, s>>>(
                 src, kb, per_view, reinterpret_cast<RsTap<J>*>(u.taps.p));
             CBN_LAUNCH_CHECK();
+            if constexpr (J == 3) {
+                CBN_REQUIRE((int64_t)ax[2].K * ax[1].K * ax[0].K < (1LL << 32),
+                            "resample grid above 2^32 cells");
+                u.rows.alloc((size_t)per_view * sizeof(RsRow3));
+                k_rs_rows3<<<blocks_for(per_view, 256), 256, 0, s>>>(
+                    reinterpret_cast<const RsTap<3>*>(u.taps.p), per_view, ax[2].K, ax[1].K,
+                    ax[0].K, reinterpret_cast<RsRow3*>(u.rows.p));
+                CBN_LAUNCH_CHECK();
+            }
             u.taps_ready = true;
         }
         StageScope st(p->timer, "resample_gather", s);
+        if constexpr (J == 3) {
+            const bool re = real_grid(p);
+            k_resample_rows3<<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
+                re ? p->grid_re : reinterpret_cast<const float*>(p->big.p), re ? 1 : 2, ax[0].K,
+                reinterpret_cast<const RsRow3*>(u.rows.p), per_view, v0, nb, shift, vals, tscale,
+                p->fumb.n_t);
+            CBN_LAUNCH_CHECK();
+            return 0;
+        }
         k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
             p->big.p, ax[2].K, ax[1].K, ax[0].K, reinterpret_cast<const RsTap<J>*>(u.taps.p),
             per_view, v0, nb, shift, vals, tscale, p->fumb.n_t);

@@ -35,6 +35,7 @@ struct UmbrellaTables {
     bool base_ready = false;
     DevBuf<char> taps;      // view-0 resample taps (RsTap) for the views-in-lanes gather
     bool taps_ready = false;
+    DevBuf<char> rows;      // J = 3: the same taps as grid-row offsets + weight products (RsRow3)
     void build(const cbn_geometry& g, int n_mu, int n_t, double dt, cudaStream_t s);
 };
 
@@ -137,6 +138,7 @@ struct cbn_projector_s {
 
     // ---- scratch (shared by both directions, sized on demand)
     cbn::DevBuf<float2> big;        // spectrum grid / resample grid(s)
+    const float* grid_re = nullptr; // Re(resample grid) inside `big` (real_grid path)
     cbn::DevBuf<float2> lattice;    // radial lattice (raw IFFT layout)
     cbn::DevBuf<float2> padded;     // padded lattice and its FFT / transpose accumulators
     cbn::DevBuf<float2> gr_t;       // Grangeat t-line buffers

@@ -101,6 +101,10 @@ public:
     // (n/2 + 1 complex outputs per line, out of place)
     cufftHandle get_r2c(long long n, long long batch);
     void exec_r2c(cufftHandle h, const float* in, void* out, cudaStream_t s);
+    // complex-to-real 3D transform of a [n0][n1][n2/2+1] half spectrum to
+    // [n0][n1][n2] real (out of place)
+    cufftHandle get_c2r3(const long long* n);
+    void exec_c2r(cufftHandle h, const void* in, float* out, cudaStream_t s);
     void clear();
 
 private:
