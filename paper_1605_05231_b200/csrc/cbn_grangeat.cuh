@@ -192,6 +192,124 @@ constexpr size_t gr_spread_owned_smem() {
            sizeof(float) * 32 * 16 + sizeof(float2) * 32 + sizeof(int) * 64;
 }
 
+// ---------------------------------------------- reverse as a cell gather
+// The reverse spread onto the detector grids is a sparse product with a
+// geometry-only matrix (the polar nodes are shared by every view):
+// grid_v[cell] = sum_p W[cell, p] y_v[p].  Per plan, each cell's (node,
+// complex weight = w_u w_v fac) entries are listed (CSR); per call, one warp
+// sums a cell's entries with lanes = views, reading each node's 32 view
+// values as one 256-byte row of the view-fastest t-spectra.  No shared-memory
+// read-modify-write, no atomics, and every grid cell is written once.
+struct GrEntry {
+    int col;        // R2C half-spectrum index of the node's value (~index: conjugate)
+    float wx, wy;   // w_u[a] w_v[b] * fac
+    int pad;
+};
+
+template <int J>
+__global__ void k_gr_csr_count(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts,
+                               const SubProblem* __restrict__ subs, int* __restrict__ counts) {
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<2>(tg, sp.bin, o);
+    for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
+        const GrPoint<J>& g = pts[sp.start + k];
+        if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
+#pragma unroll
+        for (int a = 0; a < J; ++a)
+#pragma unroll
+            for (int b = 0; b < J; ++b)
+                atomicAdd(counts + (size_t)wrapc(o[0] + g.lu + a, tg.K[0]) * tg.K[1] +
+                              wrapc(o[1] + g.lv + b, tg.K[1]),
+                          1);
+    }
+}
+
+template <int J>
+__global__ void k_gr_csr_fill(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts,
+                              const SubProblem* __restrict__ subs, int* __restrict__ cursor,
+                              GrEntry* __restrict__ ent) {
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<2>(tg, sp.bin, o);
+    for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
+        const GrPoint<J>& g = pts[sp.start + k];
+        if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
+#pragma unroll
+        for (int a = 0; a < J; ++a)
+#pragma unroll
+            for (int b = 0; b < J; ++b) {
+                const size_t cell = (size_t)wrapc(o[0] + g.lu + a, tg.K[0]) * tg.K[1] +
+                                    wrapc(o[1] + g.lv + b, tg.K[1]);
+                const float w = g.w[a] * g.w[J + b];
+                GrEntry e;
+                e.col = g.col;
+                e.wx = w * g.fac.x;
+                e.wy = w * g.fac.y;
+                e.pad = 0;
+                ent[atomicAdd(cursor + cell, 1)] = e;
+            }
+    }
+}
+
+// 32 consecutive cells per CTA, 8 warps x 4 cells, lanes = views; the
+// [cell][view] results are transposed through shared memory so each view's 32
+// cells are stored as one contiguous 256-byte row
+constexpr int kGrRows = 8;    // value rows in flight per warp (16: 10.1 ms, 8: 8.3 ms per step at cfg 2)
+
+static __global__ void __launch_bounds__(256)
+k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
+                  const int* __restrict__ col_ptr, const GrEntry* __restrict__ ent,
+                  const float2* __restrict__ tfv, int nviews) {
+    __shared__ float2 tile[32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        const int cl = warp + 8 * q;
+        const int64_t c = c0 + cl;
+        float2 acc = make_float2(0.f, 0.f);
+        if (c < ncell) {
+            const int e1 = col_ptr[c + 1];
+            // 32 entry records per coalesced load (one per lane), handed out by
+            // shuffles; kGrRows value rows in flight
+            for (int base = col_ptr[c]; base < e1; base += 32) {
+                const int n = min(32, e1 - base);
+                GrEntry mine{0, 0.f, 0.f, 0};
+                if (lane < n) mine = ent[base + lane];
+                for (int j0 = 0; j0 < n; j0 += kGrRows) {
+                    float2 y[kGrRows];
+                    float wx[kGrRows], wy[kGrRows];
+#pragma unroll
+                    for (int j = 0; j < kGrRows; ++j) {
+                        const int src = j0 + j;               // < 32; entries past n have w = 0
+                        const int col = __shfl_sync(0xffffffffu, mine.col, src);
+                        wx[j] = __shfl_sync(0xffffffffu, mine.wx, src);
+                        wy[j] = __shfl_sync(0xffffffffu, mine.wy, src);
+                        y[j] = __ldg(tfv + (size_t)(col >= 0 ? col : ~col) * 32 + lane);
+                        y[j].y = col >= 0 ? y[j].y : -y[j].y;   // Hermitian half: conj
+                    }
+#pragma unroll
+                    for (int j = 0; j < kGrRows; ++j) {
+                        acc.x = fmaf(wx[j], y[j].x, fmaf(-wy[j], y[j].y, acc.x));
+                        acc.y = fmaf(wx[j], y[j].y, fmaf(wy[j], y[j].x, acc.y));
+                    }
+                }
+            }
+        }
+        tile[cl][lane] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int v = e >> 5, cl = e & 31;
+        if (v < nviews && c0 + cl < ncell) grids[(size_t)v * grid_stride + c0 + cl] = tile[cl][v];
+    }
+}
+
+// [nb views][n] -> [n][32] (views >= nb unwritten; the readers mask them)
+__global__ void k_views_last(const float2* __restrict__ in, int nb, int64_t n,
+                             float2* __restrict__ out);
+
 // forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv)
 template <int J, int VG>
 __global__ void __launch_bounds__(256)

@@ -366,6 +366,21 @@ __global__ void k_pad_lattice(const float2* __restrict__ src, int shift, float s
 }
 
 // ---- reverse Grangeat (grangeat.py:149-170)
+__global__ void k_views_last(const float2* __restrict__ in, int nb, int64_t n,
+                             float2* __restrict__ out) {
+    __shared__ float2 tile[32][33];
+    const int64_t e0 = (int64_t)blockIdx.x * 32;
+    for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
+        const int v = q >> 5, e = q & 31;
+        if (v < nb && e0 + e < n) tile[v][e] = in[(size_t)v * n + e0 + e];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
+        const int e = q >> 5, v = q & 31;
+        if (v < nb && e0 + e < n) out[(size_t)(e0 + e) * 32 + v] = tile[v][e];
+    }
+}
+
 // rows of vals * (1 / w2[t]) (grangeat.py:152) for callers passing raw values
 __global__ void k_gr_scale(const float* __restrict__ vals, const float* __restrict__ w2inv, int n_t,
                            int64_t total, float* __restrict__ out) {
@@ -1046,9 +1061,44 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     // vals arrive already divided by w2 (folded into the resample store), so
     // the t lines go straight through a real-to-complex FFT
     p->fft.exec_r2c(p->fft.get_r2c(u.n_t, (long long)nb * u.n_mu), vals, p->gr_t.p, s);
-    CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
+    const char* spread_env = std::getenv("CBN_GR_SPREAD");
+    const bool cell_gather = !(spread_env && spread_env[0] == '1');
+    if (!cell_gather) CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
     if (p->timer.on) p->timer.end(s);
-    {
+    if (cell_gather) {
+        const int64_t ncell = (int64_t)Ku * Kv;
+        if (!gp.cell_ptr.p) {
+            // plan step: per-cell CSR of (node, complex weight) entries
+            const BinPlan& bb = gp.bins;
+            DevBuf<int> counts((size_t)ncell);
+            CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncell, s));
+            const GrPoint<kGrJ>* pts = reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p);
+            k_gr_csr_count<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, counts.p);
+            CBN_LAUNCH_CHECK();
+            std::vector<int> h((size_t)ncell + 1, 0);
+            CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncell,
+                                     cudaMemcpyDeviceToHost, s));
+            CBN_CUDA(cudaStreamSynchronize(s));
+            for (size_t q = 1; q < h.size(); ++q) h[q] += h[q - 1];
+            gp.cell_ptr.upload(h.data(), h.size(), s);
+            gp.cell_ent.alloc(sizeof(GrEntry) * (size_t)std::max(h.back(), 1));
+            CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncell, cudaMemcpyHostToDevice,
+                                     s));
+            k_gr_csr_fill<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, counts.p,
+                                                         reinterpret_cast<GrEntry*>(gp.cell_ent.p));
+            CBN_LAUNCH_CHECK();
+            CBN_CUDA(cudaStreamSynchronize(s));
+        }
+        StageScope st(p->timer, "grangeat_spread", s);
+        const int64_t nspec = (int64_t)u.n_mu * nh;
+        p->gr_tv.ensure((size_t)nspec * 32);
+        k_views_last<<<(unsigned)((nspec + 31) / 32), 256, 0, s>>>(p->gr_t.p, nb, nspec, p->gr_tv.p);
+        CBN_LAUNCH_CHECK();
+        k_gr_gather_cells<<<(unsigned)((ncell + 31) / 32), 256, 0, s>>>(
+            p->gr_grid.p, (size_t)ncell, ncell, gp.cell_ptr.p,
+            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), p->gr_tv.p, nb);
+        CBN_LAUNCH_CHECK();
+    } else {
         StageScope st(p->timer, "grangeat_spread", s);
         const BinPlan& bb = gp.bins;
         constexpr size_t smem = gr_spread_owned_smem<kGrJ, kGrTileRev>();

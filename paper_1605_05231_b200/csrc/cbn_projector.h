@@ -53,6 +53,8 @@ struct GrangeatPlan {
     BinPlan bins;                       // polar nodes sorted by 2D tile
     DevBuf<char> pts;                   // GrPoint<5> per sorted node
     bool pts_ready = false;
+    DevBuf<int> cell_ptr;               // reverse: CSR of (node, weight) entries per grid cell
+    DevBuf<char> cell_ent;              // GrEntry per (node, tap)
 };
 
 constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)
@@ -142,6 +144,7 @@ struct cbn_projector_s {
     cbn::DevBuf<float2> lattice;    // radial lattice (raw IFFT layout)
     cbn::DevBuf<float2> padded;     // padded lattice and its FFT / transpose accumulators
     cbn::DevBuf<float2> gr_t;       // Grangeat t-line buffers
+    cbn::DevBuf<float2> gr_tv;      // reverse Grangeat t-spectra, view-fastest [mu][k][32 views]
     cbn::DevBuf<float2> gr_grid;    // Grangeat 2D grids
     cbn::DevBuf<float> values;      // umbrella values of a view batch
     cbn::DevBuf<float> s32;         // per-plan float32 scalings (3 x smax)
