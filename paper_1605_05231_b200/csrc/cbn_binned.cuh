@@ -81,7 +81,9 @@ __global__ void k_bin_scatter(const int* __restrict__ keys, int64_t m, int* __re
                               int* __restrict__ perm);
 
 // ---------------------------------------------------------------- gather
-template <int D, int J, class Src, class Epi>
+// HALF (3D): `grid` is the [K0][K1][K2/2+1] half spectrum of a real input
+// (R2C); cells with k2 > K2/2 are read as conj(G[-k]).
+template <int D, int J, class Src, class Epi, bool HALF = false>
 __global__ void __launch_bounds__(256)
 k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src, Epi epi,
                 const int* __restrict__ perm, const SubProblem* __restrict__ subs) {
@@ -96,7 +98,20 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
         const int r2 = e % P2, r01 = e / P2, r1 = r01 % R1, r0 = r01 / R1;
         if (r2 >= R2 || (D == 2 && r1 >= tg.R[1])) continue;
         size_t g;
-        if constexpr (D == 3)
+        if constexpr (D == 3 && HALF) {
+            int i0 = wrapc(o[0] + r0, tg.K[0]), i1 = wrapc(o[1] + r1, tg.K[1]);
+            int i2 = wrapc(o[2] + r2, tg.K[2]);
+            const int h2 = tg.K[2] / 2 + 1;
+            if (i2 >= h2) {
+                i0 = i0 ? tg.K[0] - i0 : 0;
+                i1 = i1 ? tg.K[1] - i1 : 0;
+                i2 = tg.K[2] - i2;
+                const float2 v = __ldg(grid + ((size_t)i0 * tg.K[1] + i1) * h2 + i2);
+                tile[e] = make_float2(v.x, -v.y);
+                continue;
+            }
+            g = ((size_t)i0 * tg.K[1] + i1) * h2 + i2;
+        } else if constexpr (D == 3)
             g = ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1])) * tg.K[2] +
                 wrapc(o[2] + r2, tg.K[2]);
         else

@@ -722,16 +722,25 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         const int64_t sstr[3] = {(int64_t)n * n, n, 1};
         build_tables(p, kTabPad, ax, smax, s, rax, sstr);
     }
+    // the deapodised, padded volume is real: R2C to the half spectrum (the
+    // gather reads k2 > K2/2 as conj(G[-k])); real grid at the front of `big`,
+    // half spectrum behind it
+    long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    const int64_t real_cells = (int64_t)kd[0] * kd[1] * kd[2];
+    const int64_t half_off = (real_cells + 1) / 2;                // float2 units
+    const int64_t half_cells = (int64_t)kd[0] * kd[1] * (kd[2] / 2 + 1);
+    p->big.ensure((size_t)(half_off + half_cells));
     {
         StageScope st(p->timer, "spectrum_pad", s);
-        launch_remap<float, kStoreC>(3, vol, p->big.p, rax, 1.0f, s);
+        launch_remap<float, kStoreRe>(3, vol, p->big.p, rax, 1.0f, s);
         CBN_LAUNCH_CHECK();
     }
-    long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
     {
         StageScope st(p->timer, "spectrum_fft", s);
-        p->fft.exec(p->fft.get(3, kd, 1), p->big.p, p->big.p, CUFFT_FORWARD, s);
+        p->fft.exec_r2c3(p->fft.get_r2c3(kd), reinterpret_cast<const float*>(p->big.p),
+                         p->big.p + half_off, s);
     }
+    const float2* spec_half = p->big.p + half_off;
     if (!lat) lat = p->lattice.p;
     if (nparts > 1) CBN_CUDA(cudaMemsetAsync(lat, 0, sizeof(float2) * M, s));
     SpecOut epi;
@@ -760,8 +769,8 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             if (s1 > s0)
-                k_gather_binned<3, J><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
-                    p->big.p, kb, bp.geom<3>(), r.src(), epi, bp.perm.p, bp.subs.p + s0);
+                k_gather_binned<3, J, RadialSrc, SpecOut, true><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
+                    spec_half, kb, bp.geom<3>(), r.src(), epi, bp.perm.p, bp.subs.p + s0);
             return 0;
         });
         CBN_LAUNCH_CHECK();

@@ -38,7 +38,9 @@ cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long st
         embed = emb;
     }
     cufftResult r;
-    if (type == CUFFT_C2R) {
+    if (type == CUFFT_R2C && rank == 3) {
+        r = cufftMakePlanMany64(h, rank, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_R2C, batch, &ws);
+    } else if (type == CUFFT_C2R) {
         r = cufftMakePlanMany64(h, rank, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_C2R, batch, &ws);
     } else if (type == CUFFT_R2C) {
         long long ie[1] = {n[0]}, oe[1] = {n[0] / 2 + 1};
@@ -104,6 +106,21 @@ cufftHandle FFTCache::get_c2r3(const long long* n) {
     cufftHandle h = make(3, dims, 1, 1, 0, CUFFT_C2R);
     plans_[key] = h;
     return h;
+}
+
+cufftHandle FFTCache::get_r2c3(const long long* n) {
+    Key key{-4, n[0], n[1], n[2], 1, 1, 0};
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return it->second;
+    long long dims[3] = {n[0], n[1], n[2]};
+    cufftHandle h = make(3, dims, 1, 1, 0, CUFFT_R2C);
+    plans_[key] = h;
+    return h;
+}
+
+void FFTCache::exec_r2c3(cufftHandle h, const float* in, void* out, cudaStream_t s) {
+    CBN_CUFFT(cufftSetStream(h, s));
+    CBN_CUFFT(cufftExecR2C(h, const_cast<cufftReal*>(in), static_cast<cufftComplex*>(out)));
 }
 
 void FFTCache::exec_c2r(cufftHandle h, const void* in, float* out, cudaStream_t s) {

@@ -104,6 +104,9 @@ public:
     // complex-to-real 3D transform of a [n0][n1][n2/2+1] half spectrum to
     // [n0][n1][n2] real (out of place)
     cufftHandle get_c2r3(const long long* n);
+    // real-to-complex 3D transform [n0][n1][n2] -> [n0][n1][n2/2+1] (out of place)
+    cufftHandle get_r2c3(const long long* n);
+    void exec_r2c3(cufftHandle h, const float* in, void* out, cudaStream_t s);
     void exec_c2r(cufftHandle h, const void* in, float* out, cudaStream_t s);
     void clear();
 
