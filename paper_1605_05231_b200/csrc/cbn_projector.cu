@@ -88,6 +88,56 @@ void UmbrellaTables::build(const cbn_geometry& g, int nmu, int nt, double pitch,
 // radial spectrum -> i omega * trilinear * phase, written at the ifftshifted
 // rho position of its line (image_to_radial_spectrum + trilinear_transfer +
 // spectral_rho_derivative + the input shift of _centered_ifft).
+// the nonzero taps of w and of its mirror wm are mirror images (mod K): same
+// count, and the mirror's lowest nonzero tap is minus the node's highest.  The
+// reference's exact support test can drop the edge tap on one side only
+// (u - J/2 an integer on one side, a rounding ulp off it on the other).
+__device__ bool mirror_taps_match(int K, int J, double w, double wm) {
+    int f, fm;
+    const double u = axis_coord(w, K, 0.5 * J, f);
+    const double um = axis_coord(wm, K, 0.5 * J, fm);
+    const double edge = 0.5 * J * (1.0 - 1e-12);
+    const int e0 = (u - f) >= edge && !kb_inside(u - f, J) ? 1 : 0;
+    const int e0m = (um - fm) >= edge && !kb_inside(um - fm, J) ? 1 : 0;
+    return e0 == e0m && wrap_index(fm + e0m + f + J - 1, K) == 0;
+}
+
+__global__ void k_radial_pairs(RadialSrc r, KBSet kb, int J, int64_t lines, int* __restrict__ idx,
+                               int* __restrict__ extra, int64_t base_count) {
+    const int n = r.n_rho, nh = n / 2 + 1;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= lines * nh) return;
+    const int k = (int)(e % nh);
+    const int64_t line = e / nh;
+    const int64_t f = line * n + k;
+    if (k == 0 || k == n / 2) {
+        idx[e] = ~(int)f;
+        return;
+    }
+    double w[3], wm[3];
+    RadialSrc::Aux a, am;
+    r.node(f, w, a);
+    r.node(line * n + (n - k), wm, am);
+    bool exact = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+        exact = exact && __double_as_longlong(w[d]) == __double_as_longlong(-wm[d]) &&
+                __double_as_longlong(a.wc[d]) == __double_as_longlong(-am.wc[d]) &&
+                mirror_taps_match(kb.ax[d].K, J, w[d], wm[d]);
+    if (exact) {
+        idx[e] = (int)f;
+    } else {
+        idx[e] = ~(int)f;
+        idx[base_count + atomicAdd(extra, 1)] = ~(int)(line * n + (n - k));
+    }
+}
+
+// perm[k] = idx[perm[k]] (in place)
+__global__ void k_gather_index(const int* __restrict__ idx, int64_t n, int* __restrict__ perm) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) perm[k] = idx[perm[k]];
+}
+
 struct SpecOut {
     float2* out;
     const float* om_phys;
@@ -95,13 +145,17 @@ struct SpecOut {
     int n_rho;
     int tri;
     int spectrum_only;     // 1: image_to_radial_spectrum values in node order
+    int packed = 0;   // 1: i is a RadialPackedSrc entry (f: mirror too, ~f: node alone)
     CBN_D void put(int64_t i, float2 v, const double (&w)[3], const RadialSrc::Aux& a) const {
         double ang = centre_plan_angle<3>(a.wc, w, N);
         double sn, cs;
         sincos(ang, &sn, &cs);
         float2 r = cmul(v, make_float2((float)cs, (float)sn));
+        const int64_t line = (i >= 0 ? i : ~i) / n_rho;
+        const bool mirror = packed && i >= 0;   // the conjugate goes to rho index n_rho - ir
         if (spectrum_only) {
-            out[i] = r;
+            out[line * n_rho + a.ir] = r;
+            if (mirror) out[line * n_rho + (n_rho - a.ir)] = make_float2(r.x, -r.y);
             return;
         }
         if (tri) {
@@ -115,9 +169,11 @@ struct SpecOut {
             r = cscale(r, t);
         }
         const float o = om_phys[a.ir];
-        const int64_t line = i / n_rho;
         const int k = (a.ir + n_rho - n_rho / 2) % n_rho;
-        out[line * n_rho + k] = make_float2(-r.y * o, r.x * o);
+        const float2 val = make_float2(-r.y * o, r.x * o);
+        out[line * n_rho + k] = val;
+        if (mirror)   // the derivative spectrum of a real volume is Hermitian along the line
+            out[line * n_rho + (n_rho - a.ir + n_rho - n_rho / 2) % n_rho] = make_float2(val.x, -val.y);
     }
 };
 
@@ -750,6 +806,26 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     epi.n_rho = r.n_rho;
     epi.tri = p->c.basis == 0;
     epi.spectrum_only = spectrum != nullptr;
+    // half the nodes: rho indices 0..n_rho/2 of every line, mirrors by conjugation
+    if (!p->fpairs_n) {
+        // plan step: the primary nodes (about half: conjugate pairs along each line)
+        const int64_t base_n = r.lines() * (r.n_rho / 2 + 1);
+        p->fpairs.alloc((size_t)base_n + (size_t)r.lines() * (r.n_rho / 2));
+        DevBuf<int> extra(1);
+        CBN_CUDA(cudaMemsetAsync(extra.p, 0, sizeof(int), s));
+        KBSet kbp;
+        for (int d = 0; d < 3; ++d) kbp.ax[d] = ax[d].kb;
+        k_radial_pairs<<<blocks_for(base_n, 256), 256, 0, s>>>(r.src(), kbp, ax[0].J, r.lines(),
+                                                               p->fpairs.p, extra.p, base_n);
+        CBN_LAUNCH_CHECK();
+        int h_extra = 0;
+        CBN_CUDA(cudaMemcpyAsync(&h_extra, extra.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CBN_CUDA(cudaStreamSynchronize(s));
+        p->fpairs_n = base_n + h_extra;
+    }
+    const RadialPairSrc hsrc{r.src(), p->fpairs.p};
+    const int64_t Mh = p->fpairs_n;
+    epi.packed = 1;
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
     if (!p->fspec_bins.ready) {
@@ -757,9 +833,12 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         // gather-only plan (no staging): 8 x 16 x 16 while the region stays under 48 KB
         const int tile[3] = {kTile3, ax[0].J <= 6 ? 2 * kTile3 : kTile3, kTile3Fast};
         dispatch_j(ax[0].J, [&](auto jc) {
-            build_bins<3, decltype(jc)::value>(p->fspec_bins, r.src(), kb, M, tile, kMaxSub, s);
+            build_bins<3, decltype(jc)::value>(p->fspec_bins, hsrc, kb, Mh, tile, kMaxSub, s);
             return 0;
         });
+        // the sorted order stores the packed node entries themselves
+        k_gather_index<<<blocks_for(Mh, 256), 256, 0, s>>>(p->fpairs.p, Mh, p->fspec_bins.perm.p);
+        CBN_LAUNCH_CHECK();
     }
     {
         StageScope st(p->timer, "spectrum_gather", s);
@@ -769,8 +848,9 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             if (s1 > s0)
-                k_gather_binned<3, J, RadialSrc, SpecOut, true><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
-                    spec_half, kb, bp.geom<3>(), r.src(), epi, bp.perm.p, bp.subs.p + s0);
+                k_gather_binned<3, J, RadialPackedSrc, SpecOut, true><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
+                    spec_half, kb, bp.geom<3>(), RadialPackedSrc{r.src()}, epi, bp.perm.p,
+                    bp.subs.p + s0);
             return 0;
         });
         CBN_LAUNCH_CHECK();

@@ -113,6 +113,8 @@ struct cbn_projector_s {
     std::vector<std::pair<int, int>> fres_planes;   // non-zero slowest-axis planes of the resample grid
     int fres_planes_slow = -1;
     cbn::BinPlan fspec_bins;     // radial nodes sorted by spectrum-grid tile
+    cbn::DevBuf<int> fpairs;     // primary radial nodes (RadialPairSrc); mirrors by conjugation
+    int64_t fpairs_n = 0;
     bool fspec_fit = false;
     cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT
 

@@ -51,6 +51,38 @@ struct RadialSrc {
     }
 };
 
+// The radial lattice of a real volume is Hermitian: the node at rho index
+// n_rho - k is the mirror (-w) of the node at k, and its value is the
+// conjugate -- exactly so whenever both of its node representatives (once-
+// and twice-wrapped) are the bitwise negations of the partner's.  That fails
+// only at wrap ties (a component at an odd multiple of pi), where the
+// reference's wrapping is not odd.  RadialPairSrc enumerates a plan-time list
+// of primary nodes: idx >= 0 -> node idx, whose mirror is written as the
+// conjugate; idx < 0 -> node ~idx on its own (k = 0, k = n_rho/2, tie pairs).
+struct RadialPairSrc {
+    RadialSrc base;
+    const int* idx;
+    using Aux = RadialSrc::Aux;
+    CBN_D void node(int64_t i, double (&w)[3], Aux& a) const {
+        const int f = idx[i];
+        base.node(f >= 0 ? f : ~f, w, a);
+    }
+};
+
+// RadialPairSrc after the bin sort: the sorted order holds the packed entries
+// themselves (f or ~f), so the gather decodes its index argument directly
+struct RadialPackedSrc {
+    RadialSrc base;
+    using Aux = RadialSrc::Aux;
+    CBN_D void node(int64_t i, double (&w)[3], Aux& a) const { base.node(i >= 0 ? i : ~i, w, a); }
+};
+
+// plan step: for every line and rho index 0..n/2, the primary entry; a
+// lower-half node whose mirror is not exactly its negation is entered
+// without mirroring and its mirror is appended (counter `extra`)
+__global__ void k_radial_pairs(RadialSrc r, int64_t lines, int* __restrict__ idx,
+                               int* __restrict__ extra, int64_t base_count);
+
 // Centre phase x plan phase of the reference, each on its own node
 // representative: the centre phase uses the once-wrapped node, the plan phase
 // the twice-wrapped one; a node at +pi can wrap to -pi the second time, and
