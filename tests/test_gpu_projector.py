@@ -223,3 +223,25 @@ def test_forward_phases_shard_exactly(pl, name):
         got = np.concatenate([proj.forward_views(lat.clone(), cuts[r], cuts[r + 1]).cpu().numpy()
                               for r in range(world)])
         assert rel_l2(got, one) < 1e-6, world
+
+
+def test_radial_lattice_conjugate_pairs_at_wrap_ties(pl):
+    """The spectrum gather computes one node per +-rho pair and writes the mirror
+    as the conjugate; where the reference's wrapping or its exact support test
+    is not symmetric (components at odd multiples of pi, u - J/2 an integer on
+    one side only -- the CLI's default config has both: J = 3, n_rho = 54,
+    rho_max = sqrt(3)), the plan keeps the pair apart.  Lattice vs the oracle."""
+    import torch
+    import cbn_oracle as orc
+    from paper_1605_05231_b200 import io as cbio
+    from paper_1605_05231_b200.config import make_projector_config
+    io_dir = os.path.join(GOLDEN, "io")
+    geom = cbio.load_geometry(os.path.join(io_dir, "geom.json"))
+    vol = cbio.read_volume(os.path.join(io_dir, "vol.raw"))
+    cfg = make_projector_config(geom, vol.n, "a")
+    spec = cfg.radial_spec
+    ref = orc.radial_lattice(vol.data, vol.voxel_mm, spec, cfg.spectrum_j, 2.0, cfg.basis)
+    proj = pl.Projector(geom, cfg, vol.n, vol.voxel_mm, 1)
+    got = proj.radial_lattice(torch.from_numpy(vol.data.astype(np.float32)).cuda())
+    got = got.cpu().numpy().transpose(2, 1, 0)
+    assert rel_l2(got, ref) < 1e-5
