@@ -214,6 +214,29 @@ struct BpSrc : RadialSrc {
     }
 };
 
+// BpSrc over packed conjugate-pair entries: for a pair entry f the adjoint
+// only needs Re(IFFT) of the spread, so node f carries v(f) + conj(v(mirror))
+// and the mirror is not spread (the Hermitian part of the grid is unchanged)
+struct BpPairSrc : BpSrc {
+    CBN_D void node(int64_t i, double (&w)[3], Aux& a) const {
+        RadialSrc::node(i >= 0 ? i : ~i, w, a);
+    }
+    CBN_D float2 value(int64_t i, const double (&w)[3], const RadialSrc::Aux& a) const {
+        const int64_t f = i >= 0 ? i : ~i;
+        float2 v = BpSrc::value(f, w, a);
+        if (i >= 0) {
+            const int64_t fm = f / n_rho * n_rho + (n_rho - a.ir);
+            double wm[3];
+            RadialSrc::Aux am;
+            RadialSrc::node(fm, wm, am);
+            const float2 vm = BpSrc::value(fm, wm, am);
+            v.x += vm.x;
+            v.y -= vm.y;
+        }
+        return v;
+    }
+};
+
 }  // namespace
 
 void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
@@ -573,11 +596,28 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
         const int64_t* rows = projector_rows(p, projector_chunk(p, M), nrows);
         p->bspec_s32.alloc(3 * (size_t)n);
         ls_fit<3>(r.src(), rows, nrows, sax, p->ls, p->bspec_s32.p, n, s);
+        // one node per +-rho pair (exact mirrors only), then bins over them
+        const int64_t base_n = r.lines() * (r.n_rho / 2 + 1);
+        p->bpairs.alloc((size_t)base_n + (size_t)r.lines() * (r.n_rho / 2));
+        DevBuf<int> extra(1);
+        CBN_CUDA(cudaMemsetAsync(extra.p, 0, sizeof(int), s));
+        k_radial_pairs<<<blocks_for(base_n, 256), 256, 0, s>>>(r.src(), kbs, sax[0].J, r.lines(),
+                                                               p->bpairs.p, extra.p, base_n);
+        CBN_LAUNCH_CHECK();
+        int h_extra = 0;
+        CBN_CUDA(cudaMemcpyAsync(&h_extra, extra.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CBN_CUDA(cudaStreamSynchronize(s));
+        p->bpairs_n = base_n + h_extra;
+        const RadialPairSrc psrc{r.src(), p->bpairs.p};
         const int tile[3] = {kTile3, kTile3, kTile3Fast};
         dispatch_j(sax[0].J, [&](auto jc) {
-            build_bins<3, decltype(jc)::value>(p->bspec_bins, r.src(), kbs, M, tile, kMaxSub, s, true);
+            build_bins<3, decltype(jc)::value>(p->bspec_bins, psrc, kbs, p->bpairs_n, tile, kMaxSub,
+                                               s, true);
             return 0;
         });
+        k_gather_index<<<blocks_for(p->bpairs_n, 256), 256, 0, s>>>(p->bpairs.p, p->bpairs_n,
+                                                                   p->bspec_bins.perm.p);
+        CBN_LAUNCH_CHECK();
         p->bspec_fit = true;
     }
     if (!p->ramp_q.p) {
@@ -593,7 +633,7 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
         p->ramp_q.upload(q.data(), q.size(), s);
         CBN_CUDA(cudaStreamSynchronize(s));
     }
-    BpSrc bsrc;
+    BpPairSrc bsrc;
     static_cast<RadialSrc&>(bsrc) = r.src();
     bsrc.X = p->lattice.p;
     bsrc.q = p->ramp_q.p;

@@ -133,6 +133,8 @@ struct cbn_projector_s {
     cbn::DevBuf<char> bcol_ent;     // RsColEntry per (target, rho tap, theta tap)
     cbn::DevBuf<float> values_t;    // umbrella values of a view run, target-major
     cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
+    cbn::DevBuf<int> bpairs;     // primary radial nodes of the 3D adjoint (conjugate pairs)
+    int64_t bpairs_n = 0;
     bool bspec_fit = false;
     cbn::DevBuf<float> bspec_s32;   // cached first-sub-plan scaling of the 3D adjoint
     bool den_cached = false;

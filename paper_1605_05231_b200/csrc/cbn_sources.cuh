@@ -80,8 +80,10 @@ struct RadialPackedSrc {
 // plan step: for every line and rho index 0..n/2, the primary entry; a
 // lower-half node whose mirror is not exactly its negation is entered
 // without mirroring and its mirror is appended (counter `extra`)
-__global__ void k_radial_pairs(RadialSrc r, int64_t lines, int* __restrict__ idx,
+__global__ void k_radial_pairs(RadialSrc r, KBSet kb, int J, int64_t lines, int* __restrict__ idx,
                                int* __restrict__ extra, int64_t base_count);
+// perm[k] = idx[perm[k]] (in place): a bin order over RadialPairSrc -> packed entries
+__global__ void k_gather_index(const int* __restrict__ idx, int64_t n, int* __restrict__ perm);
 
 // Centre phase x plan phase of the reference, each on its own node
 // representative: the centre phase uses the once-wrapped node, the plan phase
