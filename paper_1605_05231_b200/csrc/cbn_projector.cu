@@ -121,8 +121,8 @@ __global__ void k_radial_pairs(RadialSrc r, KBSet kb, int J, int64_t lines, int*
     bool exact = true;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
-        exact = exact && __double_as_longlong(w[d]) == __double_as_longlong(-wm[d]) &&
-                __double_as_longlong(a.wc[d]) == __double_as_longlong(-am.wc[d]) &&
+        // mirrored up to rounding (no 2 pi jump at a wrap tie), same tap structure
+        exact = exact && fabs(w[d] + wm[d]) < 1e-12 && fabs(a.wc[d] + am.wc[d]) < 1e-12 &&
                 mirror_taps_match(kb.ax[d].K, J, w[d], wm[d]);
     if (exact) {
         idx[e] = (int)f;

@@ -53,10 +53,11 @@ struct RadialSrc {
 
 // The radial lattice of a real volume is Hermitian: the node at rho index
 // n_rho - k is the mirror (-w) of the node at k, and its value is the
-// conjugate -- exactly so whenever both of its node representatives (once-
-// and twice-wrapped) are the bitwise negations of the partner's.  That fails
-// only at wrap ties (a component at an odd multiple of pi), where the
-// reference's wrapping is not odd.  RadialPairSrc enumerates a plan-time list
+// conjugate -- up to rounding whenever both of its node representatives (once-
+// and twice-wrapped) are the negations of the partner's and the taps mirror
+// (same support after the reference's exact edge test).  That fails at wrap
+// ties (a component at an odd multiple of pi, where the reference's wrapping
+// is not odd) and where u - J/2 is an integer on one side only.  RadialPairSrc enumerates a plan-time list
 // of primary nodes: idx >= 0 -> node idx, whose mirror is written as the
 // conjugate; idx < 0 -> node ~idx on its own (k = 0, k = n_rho/2, tie pairs).
 struct RadialPairSrc {
