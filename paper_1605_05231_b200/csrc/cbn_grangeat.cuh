@@ -206,15 +206,40 @@ struct GrEntry {
     int pad;
 };
 
+// Reverse Grangeat values are conjugate-symmetric in t (real detector lines,
+// odd filter), so the spread grid is Hermitian and only Re of its inverse FFT
+// is used: a node and its mirror (same mu, t -> -t) can be merged into one
+// entry of doubled weight when they mirror exactly (no wrap jump, mirrored
+// taps after the reference's edge test).  Returns the node's weight factor:
+// 2 (kept side of a merged pair), 0 (dropped side) or 1.
+CBN_D int gr_pair_factor(const PolarSrc& src, const KBSet& kb, int J, int i) {
+    const int n_t = src.n_t;
+    const int jt = i % n_t;
+    if (jt == 0 || 2 * jt == n_t) return 1;
+    double w[2], wm[2];
+    PolarSrc::Aux a, am;
+    src.node(i, w, a);
+    src.node(i - jt + (n_t - jt), wm, am);
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+        ok = ok && fabs(w[d] + wm[d]) < 1e-12 && fabs(a.wc[d] + am.wc[d]) < 1e-12 &&
+             mirror_taps_match(kb.ax[d].K, J, w[d], wm[d]);
+    if (!ok) return 1;
+    return 2 * jt < n_t ? 2 : 0;
+}
+
 template <int J>
 __global__ void k_gr_csr_count(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts,
-                               const SubProblem* __restrict__ subs, int* __restrict__ counts) {
+                               const SubProblem* __restrict__ subs, const int* __restrict__ perm,
+                               PolarSrc src, KBSet kb, int* __restrict__ counts) {
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<2>(tg, sp.bin, o);
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
         const GrPoint<J>& g = pts[sp.start + k];
         if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
+        if (gr_pair_factor(src, kb, J, perm[sp.start + k]) == 0) continue;
 #pragma unroll
         for (int a = 0; a < J; ++a)
 #pragma unroll
@@ -227,7 +252,8 @@ __global__ void k_gr_csr_count(TileGeom<2> tg, const GrPoint<J>* __restrict__ pt
 
 template <int J>
 __global__ void k_gr_csr_fill(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts,
-                              const SubProblem* __restrict__ subs, int* __restrict__ cursor,
+                              const SubProblem* __restrict__ subs, const int* __restrict__ perm,
+                              PolarSrc src, KBSet kb, int* __restrict__ cursor,
                               GrEntry* __restrict__ ent) {
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
@@ -235,13 +261,15 @@ __global__ void k_gr_csr_fill(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
         const GrPoint<J>& g = pts[sp.start + k];
         if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
+        const int mult = gr_pair_factor(src, kb, J, perm[sp.start + k]);
+        if (mult == 0) continue;
 #pragma unroll
         for (int a = 0; a < J; ++a)
 #pragma unroll
             for (int b = 0; b < J; ++b) {
                 const size_t cell = (size_t)wrapc(o[0] + g.lu + a, tg.K[0]) * tg.K[1] +
                                     wrapc(o[1] + g.lv + b, tg.K[1]);
-                const float w = g.w[a] * g.w[J + b];
+                const float w = g.w[a] * g.w[J + b] * (float)mult;
                 GrEntry e;
                 e.col = g.col;
                 e.wx = w * g.fac.x;

@@ -40,6 +40,21 @@ CBN_D int wrapc(int c, int K) {
     return c >= K ? c - K : c;
 }
 
+// the nonzero taps of w and of its mirror wm are mirror images (mod K): same
+// count, and the mirror's lowest nonzero tap is minus the node's highest.  The
+// reference's exact support test can drop the edge tap on one side only
+// (u - J/2 an integer on one side, a rounding ulp off it on the other).
+CBN_D bool mirror_taps_match(int K, int J, double w, double wm) {
+    int f, fm;
+    const double u = axis_coord(w, K, 0.5 * J, f);
+    const double um = axis_coord(wm, K, 0.5 * J, fm);
+    const double edge = 0.5 * J * (1.0 - 1e-12);
+    const int e0 = (u - f) >= edge && !kb_inside(u - f, J) ? 1 : 0;
+    const int e0m = (um - fm) >= edge && !kb_inside(um - fm, J) ? 1 : 0;
+    return e0 == e0m && wrap_index(fm + e0m + f + J - 1, K) == 0;
+}
+
+
 // ------------------------------------------------------------------ gather
 // y_i = sum_taps w0 w1 w2 G[c0, c1, c2]  (SparseInterpolator.apply, nufft.py:68-74)
 template <int D, int J, class Src, class Epi>

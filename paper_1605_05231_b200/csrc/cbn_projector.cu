@@ -88,20 +88,6 @@ void UmbrellaTables::build(const cbn_geometry& g, int nmu, int nt, double pitch,
 // radial spectrum -> i omega * trilinear * phase, written at the ifftshifted
 // rho position of its line (image_to_radial_spectrum + trilinear_transfer +
 // spectral_rho_derivative + the input shift of _centered_ifft).
-// the nonzero taps of w and of its mirror wm are mirror images (mod K): same
-// count, and the mirror's lowest nonzero tap is minus the node's highest.  The
-// reference's exact support test can drop the edge tap on one side only
-// (u - J/2 an integer on one side, a rounding ulp off it on the other).
-__device__ bool mirror_taps_match(int K, int J, double w, double wm) {
-    int f, fm;
-    const double u = axis_coord(w, K, 0.5 * J, f);
-    const double um = axis_coord(wm, K, 0.5 * J, fm);
-    const double edge = 0.5 * J * (1.0 - 1e-12);
-    const int e0 = (u - f) >= edge && !kb_inside(u - f, J) ? 1 : 0;
-    const int e0m = (um - fm) >= edge && !kb_inside(um - fm, J) ? 1 : 0;
-    return e0 == e0m && wrap_index(fm + e0m + f + J - 1, K) == 0;
-}
-
 __global__ void k_radial_pairs(RadialSrc r, KBSet kb, int J, int64_t lines, int* __restrict__ idx,
                                int* __restrict__ extra, int64_t base_count) {
     const int n = r.n_rho, nh = n / 2 + 1;
@@ -1162,7 +1148,9 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
             DevBuf<int> counts((size_t)ncell);
             CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncell, s));
             const GrPoint<kGrJ>* pts = reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p);
-            k_gr_csr_count<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, counts.p);
+            const PolarSrc psrc{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
+            k_gr_csr_count<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, bb.perm.p,
+                                                         psrc, gp.kb, counts.p);
             CBN_LAUNCH_CHECK();
             std::vector<int> h((size_t)ncell + 1, 0);
             CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncell,
@@ -1173,7 +1161,8 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
             gp.cell_ent.alloc(sizeof(GrEntry) * (size_t)std::max(h.back(), 1));
             CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncell, cudaMemcpyHostToDevice,
                                      s));
-            k_gr_csr_fill<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, counts.p,
+            k_gr_csr_fill<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, bb.perm.p,
+                                                         psrc, gp.kb, counts.p,
                                                          reinterpret_cast<GrEntry*>(gp.cell_ent.p));
             CBN_LAUNCH_CHECK();
             CBN_CUDA(cudaStreamSynchronize(s));
