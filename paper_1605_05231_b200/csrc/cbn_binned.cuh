@@ -394,6 +394,98 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
     }
 }
 
+// J = 8, W = 8: one row per warp per point, lanes on (b, c) = (lane / 8, lane % 8)
+// and (b + 4, c).  The staging packs each point's value and packed first taps
+// into one 16-byte header and stores the y weights as (b, b + 4) pairs, so a
+// warp reads 4 shared-memory wavefronts of point data per point instead of 6.
+constexpr int kOwned8Stride = 26;   // floats per staged point: 8 x, 8 y pairs, 8 z, 2 pad
+
+inline constexpr size_t spread_owned8_smem_bytes(int nreg) {
+    return (size_t)nreg * sizeof(float2) + 256 * (sizeof(float4) + kOwned8Stride * sizeof(float));
+}
+
+template <class Src>
+__global__ void __launch_bounds__(256)
+k_spread_owned8(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
+                const int* __restrict__ perm, const SubProblem* __restrict__ subs) {
+    constexpr int J = 8, NP = 256, SW = kOwned8Stride;
+    extern __shared__ float4 smem4[];
+    const SubProblem sp = subs[blockIdx.x];
+    int o[3];
+    bin_origin<3>(tg, sp.bin, o);
+    const int R0 = tg.R[0], R1 = tg.R[1], R2 = tg.R[2], P = tg.P;
+    const int nreg = R0 * R1 * P;
+    float2* reg = reinterpret_cast<float2*>(smem4);
+    float4* hdr = reinterpret_cast<float4*>(reg + ((nreg + 1) & ~1));
+    float* stw = reinterpret_cast<float*>(hdr + NP);
+    for (int e = threadIdx.x; e < nreg; e += NP) reg[e] = make_float2(0.f, 0.f);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row_stride = R1 * P;
+    const int b = lane >> 3, c = lane & 7;
+    const int off0 = b * P + c, off1 = (b + 4) * P + c;
+    for (int base = 0; base < sp.count; base += NP) {
+        __syncthreads();   // region zeroed / previous round's points consumed
+        const int k = base + threadIdx.x;
+        if (k < sp.count) {
+            const int64_t i = perm[sp.start + k];
+            double w[3];
+            typename Src::Aux aux;
+            src.node(i, w, aux);
+            const float2 v = src.value(i, w, aux);
+            int first[3];
+            float wt[3][J];
+            tap_setup<3, J>(kb, w, first, wt);
+            const int l0 = wrapc(first[0], tg.K[0]) - o[0];
+            const int l1 = wrapc(first[1], tg.K[1]) - o[1];
+            const int l2 = wrapc(first[2], tg.K[2]) - o[2];
+            hdr[threadIdx.x] = make_float4(v.x, v.y, __int_as_float((l0 << 24) | ((l0 * R1 + l1) * P + l2)),
+                                           0.f);
+            float* ws = stw + threadIdx.x * SW;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) ws[p] = wt[0][p];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                ws[8 + 2 * q] = wt[1][q];
+                ws[9 + 2 * q] = wt[1][q + 4];
+            }
+#pragma unroll
+            for (int p = 0; p < 8; ++p) ws[16 + p] = wt[2][p];
+        }
+        __syncthreads();
+        const int npts = min(NP, sp.count - base);
+        for (int j = 0; j < npts; ++j) {
+            const float4 h = hdr[j];
+            if (h.x == 0.f && h.y == 0.f) continue;     // uniform over the CTA
+            const int pl = __float_as_int(h.z);
+            const int a0 = (warp - (pl >> 24)) & 7;
+            const float* ws = stw + j * SW;
+            const float wx = ws[a0];
+            const float2 wy = *reinterpret_cast<const float2*>(ws + 8 + 2 * b);
+            const float wz = ws[16 + c];
+            float2* row = reg + (pl & 0xffffff) + a0 * row_stride;
+            const float wk0 = wx * wy.x * wz, wk1 = wx * wy.y * wz;
+            float2 c0 = row[off0], c1 = row[off1];
+            c0.x = fmaf(wk0, h.x, c0.x);
+            c0.y = fmaf(wk0, h.y, c0.y);
+            c1.x = fmaf(wk1, h.x, c1.x);
+            c1.y = fmaf(wk1, h.y, c1.y);
+            row[off0] = c0;
+            row[off1] = c1;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nreg; e += NP) {
+        const int r2 = e % P, r01 = e / P, r1 = r01 % R1, r0 = r01 / R1;
+        if (r2 >= R2) continue;
+        const float2 sv = reg[e];
+        if (sv.x == 0.f && sv.y == 0.f) continue;
+        const size_t g = ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1])) *
+                             tg.K[2] + wrapc(o[2] + r2, tg.K[2]);
+        atomicAdd(grid + g, sv);
+    }
+}
+
 // ------------------------------------------- bank-residue interleaved order
 // Reorders each subproblem's points (plan time) so consecutive points have
 // distinct region-offset residues mod 16 for as long as the residue classes
@@ -565,6 +657,18 @@ void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src&
                     int s0 = 0, int s1 = -1) {
     CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
     if (s1 < 0) s1 = bb.nsubs;
+    if constexpr (J == 8) {
+        if (spread_warps_override() == 0) {
+            const size_t smem = spread_owned8_smem_bytes(bb.nreg);
+            CBN_CUDA(cudaFuncSetAttribute(k_spread_owned8<Src>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (s1 > s0)
+                k_spread_owned8<<<s1 - s0, 256, smem, s>>>(grid, kb, bb.geom<3>(), src, bb.perm.p,
+                                                           bb.subs.p + s0);
+            CBN_LAUNCH_CHECK();
+            return;
+        }
+    }
     switch (spread_warps_override()) {
         case 1: return launch_spread3_w<J, 1>(grid, kb, bb, src, s, s0, s1);
         case 2: return launch_spread3_w<J, 2>(grid, kb, bb, src, s, s0, s1);
