@@ -321,7 +321,7 @@ def run_ours(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "c64/f32 (fp64 index math)",
-        "data": "synthetic: seeded 30-ellipsoid phantom (BASELINE config 2)",
+        "data": f"synthetic: seeded random-ellipsoid phantom (BASELINE {w.name})",
         "config": {"workload": f"{w.name} {args.direction}: {w.n}^3 volume, "
                                f"{w.spec.n_rho}x{w.spec.n_theta}x{w.spec.n_phi} radial lattice, "
                                f"{V} views of {w.geom.nu}^2, KB J=6 sigma=2, resample J=3",
@@ -637,7 +637,7 @@ def run_reference(args):
            "value": round(value, 6), "unit": "views/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * w.geom.n_views / value, 1),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-           "dtype": "f64/c128", "data": "synthetic: seeded 30-ellipsoid phantom (BASELINE config 2)",
+           "dtype": "f64/c128", "data": f"synthetic: seeded random-ellipsoid phantom (BASELINE {w.name})",
            "config": {"workload": f"{w.name} {args.direction} (CPU oracle port, extrapolated)"},
            "cpu_baseline": cpu,
            "e2e": {"value": round(value, 6), "unit": "views/s", "h2d_bytes_per_step": 0,

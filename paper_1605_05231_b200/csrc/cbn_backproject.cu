@@ -477,11 +477,10 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 float2* gnum = den_only ? nullptr : p->big.p;
                 float2* gden = den_only ? p->big.p : nullptr;
                 const float* vt = den_only ? nullptr : p->values_t.p;
-                if (x.shift == 2 && p->g.n_views <= kRsPairThreads) {
+                if (x.shift == 2) {
                     k_rs_gather_cols2<<<ncol, kRsPairThreads, 0, s>>>(
                         gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
                 } else {
-                    CBN_REQUIRE(x.kd3[2] <= kRsColMaxPhi, "phi extent above the column-gather limit");
                     k_rs_gather_cols<<<ncol, kRsColThreads, 0, s>>>(
                         gnum, gden, (int)x.kd3[2], p->bcol_ptr.p, ent, vt, vlo, nvr, x.shift);
                 }

@@ -117,7 +117,6 @@ static __global__ void k_transpose_vals(const float* __restrict__ in, int nv, in
 // of valsT [target][nv]; writes (num, 0) if gnum -- and (den, 0) if gden -- to
 // every cell of the column (den-only passes: gnum and valsT null).
 constexpr int kRsColThreads = 256;
-constexpr int kRsColMaxPhi = 3 * kRsColThreads;
 
 static __global__ void __launch_bounds__(kRsColThreads)
 k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
@@ -125,14 +124,11 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
                  const float* __restrict__ valsT, int vlo, int nv, int shift) {
     const size_t col = blockIdx.x;
     const int beg = col_ptr[col], end = col_ptr[col + 1];
-    float num[3] = {0.f, 0.f, 0.f}, den[3] = {0.f, 0.f, 0.f};
-    for (int k = beg; k < end; ++k) {
-        const RsColEntry e = ent[k];
-        const float* vt = valsT + (size_t)e.t * nv;
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            const int phi = threadIdx.x + r * kRsColThreads;
-            if (phi >= K2) break;
+    for (int phi = threadIdx.x; phi < K2; phi += kRsColThreads) {
+        float num = 0.f, den = 0.f;
+        for (int k = beg; k < end; ++k) {
+            const RsColEntry e = ent[k];
+            const float* vt = valsT + (size_t)e.t * nv;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 // view v covers phi = f2 - v shift + c  (mod K2)
@@ -142,18 +138,13 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
                 const int rel = v - vlo;
                 if (v * shift == d && rel >= 0 && rel < nv) {
                     const float wk = e.wab * e.w2[c];
-                    if (valsT) num[r] = fmaf(wk, __ldg(vt + rel), num[r]);
-                    den[r] += wk;
+                    if (valsT) num = fmaf(wk, __ldg(vt + rel), num);
+                    den += wk;
                 }
             }
         }
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const int phi = threadIdx.x + r * kRsColThreads;
-        if (phi >= K2) break;
-        if (gnum) gnum[col * K2 + phi] = make_float2(num[r], 0.f);
-        if (gden) gden[col * K2 + phi] = make_float2(den[r], 0.f);
+        if (gnum) gnum[col * K2 + phi] = make_float2(num, 0.f);
+        if (gden) gden[col * K2 + phi] = make_float2(den, 0.f);
     }
 }
 
@@ -170,40 +161,42 @@ k_rs_gather_cols2(float2* __restrict__ gnum, float2* __restrict__ gden, int V,
                   const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
                   const float* __restrict__ valsT, int vlo, int nv) {
     const size_t col = blockIdx.x;
-    const int i = threadIdx.x;
-    if (i >= V) return;
     const int beg = col_ptr[col], end = col_ptr[col + 1];
-    float ne = 0.f, no = 0.f, de = 0.f, dn = 0.f;
-    for (int k = beg; k < end; ++k) {
-        const RsColEntry e = ent[k];
-        const int d = e.f2 - 2 * i;
-        int b0 = d >> 1;                       // floor(d / 2)
-        b0 += b0 < 0 ? V : 0;
-        int b1 = b0 + 1;
-        b1 -= b1 >= V ? V : 0;
-        int r0 = b0 - vlo, r1 = b1 - vlo;
-        r0 += r0 < 0 ? V : 0;
-        r1 += r1 < 0 ? V : 0;
-        const bool ok0 = r0 < nv, ok1 = r1 < nv;
-        const float* vt = valsT + (size_t)e.t * nv;
-        const float x0 = (ok0 && valsT) ? __ldg(vt + r0) : 0.f;
-        const float x1 = (ok1 && valsT) ? __ldg(vt + r1) : 0.f;
-        const float u0 = ok0 ? 1.f : 0.f, u1 = ok1 ? 1.f : 0.f;
-        const float w0 = e.wab * e.w2[0], w1 = e.wab * e.w2[1], w2 = e.wab * e.w2[2];
-        if ((d & 1) == 0) {
-            ne = fmaf(w0, x0, fmaf(w2, x1, ne));
-            no = fmaf(w1, x0, no);
-            de = fmaf(w0, u0, fmaf(w2, u1, de));
-            dn = fmaf(w1, u0, dn);
-        } else {
-            no = fmaf(w0, x0, fmaf(w2, x1, no));
-            ne = fmaf(w1, x1, ne);
-            dn = fmaf(w0, u0, fmaf(w2, u1, dn));
-            de = fmaf(w1, u1, de);
+    for (int i = threadIdx.x; i < V; i += kRsPairThreads) {
+        float ne = 0.f, no = 0.f, de = 0.f, dn = 0.f;
+        for (int k = beg; k < end; ++k) {
+            const RsColEntry e = ent[k];
+            const int d = e.f2 - 2 * i;
+            int b0 = d >> 1;                       // floor(d / 2)
+            b0 += b0 < 0 ? V : 0;
+            int b1 = b0 + 1;
+            b1 -= b1 >= V ? V : 0;
+            int r0 = b0 - vlo, r1 = b1 - vlo;
+            r0 += r0 < 0 ? V : 0;
+            r1 += r1 < 0 ? V : 0;
+            const bool ok0 = r0 < nv, ok1 = r1 < nv;
+            const float* vt = valsT + (size_t)e.t * nv;
+            const float x0 = (ok0 && valsT) ? __ldg(vt + r0) : 0.f;
+            const float x1 = (ok1 && valsT) ? __ldg(vt + r1) : 0.f;
+            const float u0 = ok0 ? 1.f : 0.f, u1 = ok1 ? 1.f : 0.f;
+            const float w0 = e.wab * e.w2[0], w1 = e.wab * e.w2[1], w2 = e.wab * e.w2[2];
+            if ((d & 1) == 0) {
+                ne = fmaf(w0, x0, fmaf(w2, x1, ne));
+                no = fmaf(w1, x0, no);
+                de = fmaf(w0, u0, fmaf(w2, u1, de));
+                dn = fmaf(w1, u0, dn);
+            } else {
+                no = fmaf(w0, x0, fmaf(w2, x1, no));
+                ne = fmaf(w1, x1, ne);
+                dn = fmaf(w0, u0, fmaf(w2, u1, dn));
+                de = fmaf(w1, u1, de);
+            }
         }
+        if (gnum)
+            *(reinterpret_cast<float4*>(gnum + col * 2 * V) + i) = make_float4(ne, 0.f, no, 0.f);
+        if (gden)
+            *(reinterpret_cast<float4*>(gden + col * 2 * V) + i) = make_float4(de, 0.f, dn, 0.f);
     }
-    if (gnum) *(reinterpret_cast<float4*>(gnum + col * 2 * V) + i) = make_float4(ne, 0.f, no, 0.f);
-    if (gden) *(reinterpret_cast<float4*>(gden + col * 2 * V) + i) = make_float4(de, 0.f, dn, 0.f);
 }
 
 }  // namespace cbn
