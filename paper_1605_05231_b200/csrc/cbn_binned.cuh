@@ -490,7 +490,7 @@ k_spread_owned8(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
 // Reorders each subproblem's points (plan time) so consecutive points have
 // distinct region-offset residues mod 16 for as long as the residue classes
 // last: stable rank q within the class, then order by (q, residue).
-constexpr int kInterleaveMax = 1024;
+constexpr int kInterleaveMax = 4096;
 
 template <int D, int J, class Src>
 __global__ void __launch_bounds__(256)

@@ -819,7 +819,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         // gather-only plan (no staging): 8 x 16 x 16 while the region stays under 48 KB
         const int tile[3] = {kTile3, ax[0].J <= 6 ? 2 * kTile3 : kTile3, kTile3Fast};
         dispatch_j(ax[0].J, [&](auto jc) {
-            build_bins<3, decltype(jc)::value>(p->fspec_bins, hsrc, kb, Mh, tile, kMaxSub, s);
+            build_bins<3, decltype(jc)::value>(p->fspec_bins, hsrc, kb, Mh, tile, 4 * kMaxSub, s);   // gather only: larger subproblems, fewer region loads
             return 0;
         });
         // the sorted order stores the packed node entries themselves
