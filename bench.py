@@ -245,27 +245,53 @@ def run_ours(args):
             host_in = x_dev.cpu().pin_memory()
             host_out = torch.empty((w.n,) * 3, dtype=torch.float32).pin_memory()
 
-        def e2e_step():
-            dev = host_in.to("cuda", non_blocking=True)
+        def run(dev):
             if direction == 1:
-                out = proj.forward_sharded(dev, lo, hi) if world > 1 else proj.forward(dev, lo, hi)
-            elif world > 1:
-                out = proj.backproject_sharded(dev[lo:hi].contiguous(), lo, hi)
-            else:
-                out = proj.backproject(dev)
-            host_out.copy_(out, non_blocking=True)
+                return proj.forward_sharded(dev, lo, hi) if world > 1 else proj.forward(dev, lo, hi)
+            if world > 1:
+                return proj.backproject_sharded(dev[lo:hi].contiguous(), lo, hi)
+            return proj.backproject(dev)
 
-        for _ in range(2):
-            e2e_step()
+        # Pipelined through the public API: a copy stream brings step k+1's input
+        # in while step k computes and takes step k-1's result out, so every
+        # step's H2D and D2H are inside the timed region but overlap the compute
+        copy_s = torch.cuda.Stream()
+        dev_in = [torch.empty(host_in.shape, dtype=host_in.dtype, device="cuda") for _ in range(2)]
+        host_outs = [host_out, torch.empty_like(host_out).pin_memory()]
+        in_ready = [torch.cuda.Event() for _ in range(2)]
+        out_ready = [torch.cuda.Event() for _ in range(2)]
+
+        def pipeline(nsteps, start_event=None):
+            with torch.cuda.stream(copy_s):
+                if start_event is not None:
+                    copy_s.wait_event(start_event)
+                dev_in[0].copy_(host_in, non_blocking=True)
+                in_ready[0].record(copy_s)
+            for k in range(nsteps):
+                slot = k % 2
+                if k + 1 < nsteps:               # next input, once step k-1 released its slot
+                    with torch.cuda.stream(copy_s):
+                        if k >= 1:
+                            copy_s.wait_event(out_ready[1 - slot])
+                        dev_in[1 - slot].copy_(host_in, non_blocking=True)
+                        in_ready[1 - slot].record(copy_s)
+                stream.wait_event(in_ready[slot])
+                out = run(dev_in[slot])
+                out_ready[slot].record(stream)
+                with torch.cuda.stream(copy_s):
+                    copy_s.wait_event(out_ready[slot])
+                    host_outs[slot].copy_(out, non_blocking=True)
+                out.record_stream(copy_s)
+
+        pipeline(2)
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         wall0 = time.perf_counter()
         e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
+        pipeline(args.steps, e0)
+        e1.record(copy_s)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
         barrier()
@@ -276,7 +302,8 @@ def run_ours(args):
         e2e = {"value": units * args.steps / (e_ms / 1e3), "unit": "views/s",
                "h2d_bytes_per_step": int(host_in.numel() * 4),
                "d2h_bytes_per_step": int(host_out.numel() * 4),
-               "wall_s": wall, "api": "Projector.forward/backproject with pinned host tensors"}
+               "wall_s": wall, "api": "Projector.forward/backproject with pinned host tensors, "
+                                      "copies on a second stream overlapping the previous/next step"}
 
     if rank != 0:
         if world > 1:
