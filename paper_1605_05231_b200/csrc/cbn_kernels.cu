@@ -130,4 +130,50 @@ __global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict
         make_float2(0.5f * (v[0].x + v[1].x), 0.5f * (v[1].y - v[0].y));
 }
 
+__global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __restrict__ dst,
+                                   RemapAxis a0, RemapAxis a1, RemapAxis a2,
+                                   const int* __restrict__ l0, const int* __restrict__ l1,
+                                   const int* __restrict__ l2, int n1l, int n2l, int64_t total,
+                                   float gain) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= total) return;
+    const int h2 = a2.n / 2 + 1;
+    const int e[3] = {l0[q / ((int64_t)n1l * n2l)], l1[(q / n2l) % n1l], l2[q % n2l]};
+    const RemapAxis ax[3] = {a0, a1, a2};
+    float2 v[2];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        float sc = gain;
+        int64_t so = 0;
+        bool zero = false;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            int k = e[d];
+            if (side) k = k == 0 ? 0 : ax[d].n - k;     // (-k) mod n
+            const int id = ax[d].idx[k];
+            zero |= id < 0;
+            so += (int64_t)id * ax[d].sstride;
+            sc *= ax[d].scale[k];
+        }
+        const float2 g = zero ? make_float2(0.f, 0.f) : src[so];
+        v[side] = make_float2(g.x * sc, g.y * sc);
+    }
+    dst[((size_t)e[0] * a1.n + e[1]) * h2 + e[2]] =
+        make_float2(0.5f * (v[0].x + v[1].x), 0.5f * (v[1].y - v[0].y));
+}
+
+std::vector<int> pad_positions(int N, int K, bool mirror, bool half) {
+    std::vector<char> on((size_t)K, 0);
+    const int h = N / 2;
+    for (int n = 0; n < N; ++n) {
+        const int k = ((n - h) % K + K) % K;
+        on[(size_t)k] = 1;
+        if (mirror) on[(size_t)((K - k) % K)] = 1;
+    }
+    std::vector<int> out;
+    for (int k = 0; k < K; ++k)
+        if (on[(size_t)k] && (!half || k <= K / 2)) out.push_back(k);
+    return out;
+}
+
 }  // namespace cbn

@@ -12,6 +12,8 @@
 // Spread values:    __device__ float2 value(int64_t i, const double (&w)[D], const Aux&) const;
 #pragma once
 
+#include <vector>
+
 #include "cbn_common.cuh"
 
 namespace cbn {
@@ -277,6 +279,46 @@ __global__ void k_remap(const SrcT* __restrict__ src, void* __restrict__ dst, Re
 // Re(forward FFT of P) (the only part the resample gather reads).
 __global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict__ dst,
                               RemapAxis a0, RemapAxis a1, RemapAxis a2, float gain);
+
+// The same remaps restricted to the destination cells a pad table can make
+// non-zero (compact per-axis index lists `l`, lengths nl; the caller zeroes
+// the rest of the destination first): k_remap (3D, kStoreRe / kStoreC) and
+// k_remap_herm3 (list on the half axis limited to <= n2 / 2).
+template <class SrcT, int MODE>
+__global__ void k_remap_list3(const SrcT* __restrict__ src, void* __restrict__ dst, RemapAxis a0,
+                              RemapAxis a1, RemapAxis a2, const int* __restrict__ l0,
+                              const int* __restrict__ l1, const int* __restrict__ l2, int n1l,
+                              int n2l, int64_t total, float gain) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int e0 = l0[e / ((int64_t)n1l * n2l)], e1 = l1[(e / n2l) % n1l], e2 = l2[e % n2l];
+    const int id0 = a0.idx[e0], id1 = a1.idx[e1], id2 = a2.idx[e2];
+    const size_t doff = ((size_t)e0 * a1.n + e1) * a2.n + e2;
+    float2 v = make_float2(0.f, 0.f);
+    if (id0 >= 0 && id1 >= 0 && id2 >= 0) {
+        const float sc = gain * a0.scale[e0] * a1.scale[e1] * a2.scale[e2];
+        const int64_t so = (int64_t)id0 * a0.sstride + (int64_t)id1 * a1.sstride + (int64_t)id2 * a2.sstride;
+        if constexpr (sizeof(SrcT) == sizeof(float)) {
+            v.x = sc * (float)src[so];
+        } else {
+            const float2 g = src[so];
+            v = make_float2(g.x * sc, g.y * sc);
+        }
+    }
+    if constexpr (MODE == kStoreRe) static_cast<float*>(dst)[doff] = v.x;
+    else static_cast<float2*>(dst)[doff] = v;
+}
+
+__global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __restrict__ dst,
+                                   RemapAxis a0, RemapAxis a1, RemapAxis a2,
+                                   const int* __restrict__ l0, const int* __restrict__ l1,
+                                   const int* __restrict__ l2, int n1l, int n2l, int64_t total,
+                                   float gain);
+
+// destination indices a pad table (kTabPad / kTabPadShift: source n, output
+// k = (n - N//2) mod K) can fill, with their mirrors -k when `mirror`, and
+// only k <= K/2 when `half` (host)
+std::vector<int> pad_positions(int N, int K, bool mirror, bool half);
 
 // Table modes for k_build_table.
 enum TableMode {

@@ -772,9 +772,25 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     const int64_t half_off = (real_cells + 1) / 2;                // float2 units
     const int64_t half_cells = (int64_t)kd[0] * kd[1] * (kd[2] / 2 + 1);
     p->big.ensure((size_t)(half_off + half_cells));
+    if (!p->fspec_list.p) {
+        std::vector<int> all;
+        for (int d = 0; d < 3; ++d) {
+            const std::vector<int> l = pad_positions(ax[d].N, ax[d].K, false, false);
+            p->fspec_nl[d] = (int)l.size();
+            all.insert(all.end(), l.begin(), l.end());
+        }
+        p->fspec_list.upload(all.data(), all.size(), s);
+        CBN_CUDA(cudaStreamSynchronize(s));
+    }
     {
+        // zero the grid, then fill only the cells the pad reaches (1/8 of them)
         StageScope st(p->timer, "spectrum_pad", s);
-        launch_remap<float, kStoreRe>(3, vol, p->big.p, rax, 1.0f, s);
+        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float) * real_cells, s));
+        const int* l = p->fspec_list.p;
+        const int64_t cells = (int64_t)p->fspec_nl[0] * p->fspec_nl[1] * p->fspec_nl[2];
+        k_remap_list3<float, kStoreRe><<<blocks_for(cells, 256), 256, 0, s>>>(
+            vol, p->big.p, rax[0], rax[1], rax[2], l, l + p->fspec_nl[0],
+            l + p->fspec_nl[0] + p->fspec_nl[1], p->fspec_nl[1], p->fspec_nl[2], cells, 1.0f);
         CBN_LAUNCH_CHECK();
     }
     {
@@ -972,11 +988,29 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
         const long long kd3[3] = {rax[0].n, rax[1].n, rax[2].n};
         const int64_t half = (int64_t)kd3[0] * kd3[1] * (kd3[2] / 2 + 1);
         p->big.ensure((size_t)half + (size_t)(kd3[0] * kd3[1] * kd3[2] + 1) / 2);
+        if (!p->fres_list.p) {
+            // per grid axis (after the phi-fast swap): the pad positions and their mirrors
+            const AxisPlan* ga[3] = {&ax[0], &ax[1], &ax[2]};
+            if (phi_fast) std::swap(ga[0], ga[2]);
+            std::vector<int> all;
+            for (int d = 0; d < 3; ++d) {
+                const std::vector<int> l = pad_positions(ga[d]->N, ga[d]->K, true, d == 2);
+                p->fres_nl[d] = (int)l.size();
+                all.insert(all.end(), l.begin(), l.end());
+            }
+            p->fres_list.upload(all.data(), all.size(), s);
+            CBN_CUDA(cudaStreamSynchronize(s));
+        }
         {
+            // zero the half spectrum, then fill only the cells P or its mirror reaches
             StageScope st(p->timer, "resample_pad", s);
-            dim3 grid((unsigned)((kd3[2] / 2 + 1 + 255) / 256), (unsigned)kd3[1], (unsigned)kd3[0]);
-            k_remap_herm3<<<grid, 256, 0, s>>>(p->padded.p, p->big.p, rax[0], rax[1], rax[2],
-                                               (float)(1.0 / size));
+            CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * half, s));
+            const int* l = p->fres_list.p;
+            const int64_t cells = (int64_t)p->fres_nl[0] * p->fres_nl[1] * p->fres_nl[2];
+            k_remap_herm3_list<<<blocks_for(cells, 256), 256, 0, s>>>(
+                p->padded.p, p->big.p, rax[0], rax[1], rax[2], l, l + p->fres_nl[0],
+                l + p->fres_nl[0] + p->fres_nl[1], p->fres_nl[1], p->fres_nl[2], cells,
+                (float)(1.0 / size));
             CBN_LAUNCH_CHECK();
         }
         StageScope st(p->timer, "resample_fft", s);
