@@ -1048,36 +1048,47 @@ bool views_in_lanes(const P* p) {
     return (2LL * p->frad.n_phi) % V == 0 && p->fres[0].K == 2 * p->frad.n_phi;
 }
 
+// per-target resample taps of the views-in-lanes gather (built once)
+void ensure_lane_taps(P* p, cudaStream_t s) {
+    UmbrellaTables& u = p->fumb;
+    if (u.taps_ready) return;
+    const AxisPlan* ax = p->fres;
+    const int64_t per_view = (int64_t)u.n_mu * u.n_t;
+    dispatch_j(ax[0].J, [&](auto jc) {
+        constexpr int J = decltype(jc)::value;
+        UmbrellaSrc src = cached_umbrella(p, u, p->frad, p->fpad, 0, s);
+        KBSet kb;
+        kb.ax[0] = ax[2].kb;
+        kb.ax[1] = ax[1].kb;
+        kb.ax[2] = ax[0].kb;
+        u.taps.alloc((size_t)per_view * sizeof(RsTap<J>));
+        k_rs_taps<J><<<blocks_for(per_view, 256), 256, 0, s>>>(
+            src, kb, per_view, reinterpret_cast<RsTap<J>*>(u.taps.p));
+        CBN_LAUNCH_CHECK();
+        if constexpr (J == 3) {
+            CBN_REQUIRE((int64_t)ax[2].K * ax[1].K * ax[0].K < (1LL << 32),
+                        "resample grid above 2^32 cells");
+            u.rows.alloc((size_t)per_view * sizeof(RsRow3));
+            k_rs_rows3<<<blocks_for(per_view, 256), 256, 0, s>>>(
+                reinterpret_cast<const RsTap<3>*>(u.taps.p), per_view, ax[2].K, ax[1].K,
+                ax[0].K, reinterpret_cast<RsRow3*>(u.rows.p));
+            CBN_LAUNCH_CHECK();
+        }
+        return 0;
+    });
+    u.taps_ready = true;
+}
+
 // Re(resample_apply) for nb <= 32 consecutive views [v0, v0 + nb) from a phi-fast grid
 void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
                         const float* tscale = nullptr) {
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
     const int shift = (int)(2LL * p->frad.n_phi / p->g.n_views);
+    ensure_lane_taps(p, s);
     dispatch_j(ax[0].J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         UmbrellaTables& u = p->fumb;
-        if (!u.taps_ready) {
-            UmbrellaSrc src = cached_umbrella(p, u, p->frad, p->fpad, 0, s);
-            KBSet kb;
-            kb.ax[0] = ax[2].kb;
-            kb.ax[1] = ax[1].kb;
-            kb.ax[2] = ax[0].kb;
-            u.taps.alloc((size_t)per_view * sizeof(RsTap<J>));
-            k_rs_taps<J><<<blocks_for(per_view, 256), 256, 0, s>>>(
-                src, kb, per_view, reinterpret_cast<RsTap<J>*>(u.taps.p));
-            CBN_LAUNCH_CHECK();
-            if constexpr (J == 3) {
-                CBN_REQUIRE((int64_t)ax[2].K * ax[1].K * ax[0].K < (1LL << 32),
-                            "resample grid above 2^32 cells");
-                u.rows.alloc((size_t)per_view * sizeof(RsRow3));
-                k_rs_rows3<<<blocks_for(per_view, 256), 256, 0, s>>>(
-                    reinterpret_cast<const RsTap<3>*>(u.taps.p), per_view, ax[2].K, ax[1].K,
-                    ax[0].K, reinterpret_cast<RsRow3*>(u.rows.p));
-                CBN_LAUNCH_CHECK();
-            }
-            u.taps_ready = true;
-        }
         StageScope st(p->timer, "resample_gather", s);
         if constexpr (J == 3) {
             const bool re = real_grid(p);
@@ -1155,24 +1166,38 @@ GrPost gr_post(const P* p, const GrangeatPlan& gp) {
 }
 
 // reverse_grangeat_view for nb views: vals (nb x n_mu x n_t) -> frames (nb x nu x nv)
-void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s) {
+struct GrBufs {
+    FFTCache& fft;
+    DevBuf<float2>& t;
+    DevBuf<float2>& tv;
+    DevBuf<float2>& grid;
+    DevBuf<double>& red;
+};
+GrBufs main_bufs(P* p) { return {p->fft, p->gr_t, p->gr_tv, p->gr_grid, p->red}; }
+GrBufs lane_bufs(P* p) {
+    auto& l = p->lane1;
+    return {l.fft, l.gr_t, l.gr_tv, l.gr_grid, l.red};
+}
+
+void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s,
+                      GrBufs B) {
     GrangeatPlan& gp = p->fgr;
     if (!gp.built) fit_grangeat(p, gp, p->fumb, s);
     const UmbrellaTables& u = p->fumb;
     const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
     const int64_t tl = (int64_t)nb * u.n_mu * u.n_t;
     const int nh = u.n_t / 2 + 1;
-    p->gr_t.ensure((size_t)nb * u.n_mu * nh);
-    p->gr_grid.ensure((size_t)nb * Ku * Kv);
+    B.t.ensure((size_t)nb * u.n_mu * nh);
+    B.grid.ensure((size_t)nb * Ku * Kv);
     prepare_gr_points(p, gp, u, true, s);
     if (p->timer.on) p->timer.begin("grangeat_tfft", s);
     (void)tl;
     // vals arrive already divided by w2 (folded into the resample store), so
     // the t lines go straight through a real-to-complex FFT
-    p->fft.exec_r2c(p->fft.get_r2c(u.n_t, (long long)nb * u.n_mu), vals, p->gr_t.p, s);
+    B.fft.exec_r2c(B.fft.get_r2c(u.n_t, (long long)nb * u.n_mu), vals, B.t.p, s);
     const char* spread_env = std::getenv("CBN_GR_SPREAD");
     const bool cell_gather = !(spread_env && spread_env[0] == '1');
-    if (!cell_gather) CBN_CUDA(cudaMemsetAsync(p->gr_grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
+    if (!cell_gather) CBN_CUDA(cudaMemsetAsync(B.grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
     if (p->timer.on) p->timer.end(s);
     if (cell_gather) {
         const int64_t ncell = (int64_t)Ku * Kv;
@@ -1203,12 +1228,12 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         }
         StageScope st(p->timer, "grangeat_spread", s);
         const int64_t nspec = (int64_t)u.n_mu * nh;
-        p->gr_tv.ensure((size_t)nspec * 32);
-        k_views_last<<<(unsigned)((nspec + 31) / 32), 256, 0, s>>>(p->gr_t.p, nb, nspec, p->gr_tv.p);
+        B.tv.ensure((size_t)nspec * 32);
+        k_views_last<<<(unsigned)((nspec + 31) / 32), 256, 0, s>>>(B.t.p, nb, nspec, B.tv.p);
         CBN_LAUNCH_CHECK();
         k_gr_gather_cells<<<(unsigned)((ncell + 31) / 32), 256, 0, s>>>(
-            p->gr_grid.p, (size_t)ncell, ncell, gp.cell_ptr.p,
-            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), p->gr_tv.p, nb);
+            B.grid.p, (size_t)ncell, ncell, gp.cell_ptr.p,
+            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb);
         CBN_LAUNCH_CHECK();
     } else {
         StageScope st(p->timer, "grangeat_spread", s);
@@ -1217,24 +1242,28 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         CBN_CUDA(cudaFuncSetAttribute(k_gr_spread_owned<kGrJ, kGrTileRev>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_gr_spread_owned<kGrJ, kGrTileRev><<<bb.nsubs, kGrJ * 32, smem, s>>>(
-            p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(),
-            reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p), bb.subs.p, p->gr_t.p,
+            B.grid.p, (size_t)Ku * Kv, bb.geom<2>(),
+            reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p), bb.subs.p, B.t.p,
             (size_t)u.n_mu * nh, nb);
         CBN_LAUNCH_CHECK();
     }
     long long kd[2] = {Ku, Kv};
     StageScope st(p->timer, "grangeat_ifft_post", s);
-    p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_INVERSE, s);
+    B.fft.exec(B.fft.get(2, kd, nb), B.grid.p, B.grid.p, CUFFT_INVERSE, s);
     GrPost q = gr_post(p, gp);
-    p->red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
-    double* mean = p->red.p + 2 * kRedBlocks + 64;
-    k_gr_ring<<<nb, 256, 0, s>>>(p->gr_grid.p, q, mean);
+    B.red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
+    double* mean = B.red.p + 2 * kRedBlocks + 64;
+    k_gr_ring<<<nb, 256, 0, s>>>(B.grid.p, q, mean);
     CBN_LAUNCH_CHECK();
     const int64_t total = (int64_t)nb * p->g.nu * p->g.nv;
-    k_gr_frame<<<blocks_for(total, 256), 256, 0, s>>>(p->gr_grid.p, q, mean,
+    k_gr_frame<<<blocks_for(total, 256), 256, 0, s>>>(B.grid.p, q, mean,
                                                       (float)p->c.normalization, frames, total,
                                                       p->flag.p);
     CBN_LAUNCH_CHECK();
+}
+
+void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s) {
+    grangeat_reverse(p, vals, frames, nb, s, main_bufs(p));
 }
 
 constexpr int kViewBlock = 32;
@@ -1264,14 +1293,49 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
     const size_t frame_sz = (size_t)p->g.nu * p->g.nv;
     if (!values_out) p->values.ensure((size_t)per_view * kViewBlock);
+    const bool lanes = views_in_lanes(p);
+    // two lanes (the caller's stream and s1) alternate over view blocks so one
+    // block's Grangeat FFTs overlap the next block's resample gather
+    const char* one = std::getenv("CBN_ONE_STREAM");
+    const bool dual = lanes && !values_out && !(one && one[0] == '1');
+    if (dual && !p->s1) {
+        CBN_CUDA(cudaStreamCreateWithFlags(&p->s1, cudaStreamNonBlocking));
+        CBN_CUDA(cudaEventCreateWithFlags(&p->ev_s0, cudaEventDisableTiming));
+        CBN_CUDA(cudaEventCreateWithFlags(&p->ev_s1, cudaEventDisableTiming));
+    }
+    if (dual) {
+        p->lane1.values.ensure((size_t)per_view * kViewBlock);
+        // everything s1 reads besides the grid exists before the first grid event
+        ensure_lane_taps(p, s);
+        if (!p->fgr.built) fit_grangeat(p, p->fgr, p->fumb, s);
+        prepare_gr_points(p, p->fgr, p->fumb, true, s);
+    }
+    int lane = 0;
+    bool s1_used = false, s1_stale = true;   // s1 has not yet waited for the current grid
+    auto lane_stream = [&]() -> cudaStream_t {
+        if (!lane) return s;
+        if (s1_stale) {
+            CBN_CUDA(cudaStreamWaitEvent(p->s1, p->ev_s0, 0));
+            s1_stale = false;
+        }
+        s1_used = true;
+        return p->s1;
+    };
+    auto lane_done = [&]() {
+        if (lane) CBN_CUDA(cudaEventRecord(p->ev_s1, p->s1));
+    };
     int cur = -1, blk_lo = lo, blk_n = 0;
     auto flush = [&]() {
         if (!blk_n) return;
-        grangeat_reverse(p, p->values.p, frames + (size_t)(blk_lo - lo) * frame_sz, blk_n, s);
+        const cudaStream_t ls = lane_stream();
+        grangeat_reverse(p, lane ? p->lane1.values.p : p->values.p,
+                         frames + (size_t)(blk_lo - lo) * frame_sz, blk_n, ls,
+                         lane ? lane_bufs(p) : main_bufs(p));
+        lane_done();
         blk_lo += blk_n;
         blk_n = 0;
+        if (dual) lane ^= 1;
     };
-    const bool lanes = views_in_lanes(p);
     // internal values feed the Grangeat step directly: store them divided by w2
     const float* tscale = values_out ? nullptr : p->fgr.w2inv.p;
     auto gather = [&](int v, int n, float* out) {
@@ -1279,9 +1343,11 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
             gather_views(p, v, v + n, out, s, tscale);
             return;
         }
+        const cudaStream_t ls = values_out ? s : lane_stream();
         for (int k = 0; k < n; k += 32)
-            gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, s,
+            gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, ls,
                                tscale);
+        if (!values_out) lane_done();
     };
     // runs of consecutive batches (clipped to [lo, hi)) sharing one scaling group
     const size_t nbat = bp.batches.size();
@@ -1300,7 +1366,13 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
             ++e;
         }
         if (g != cur) {
+            // the previous grid may still be read on s1
+            if (s1_used) CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
             build_resample_grid(p, bp.s32.p + (size_t)g * 3 * bp.smax, bp.smax, s, lanes);
+            if (dual) {
+                CBN_CUDA(cudaEventRecord(p->ev_s0, s));
+                s1_stale = true;
+            }
             cur = g;
         }
         for (int v = vlo; v < vhi;) {
@@ -1311,7 +1383,7 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
                 continue;
             }
             const int take = std::min(vhi - v, kViewBlock - blk_n);
-            gather(v, take, p->values.p + (size_t)blk_n * per_view);
+            gather(v, take, (lane ? p->lane1.values.p : p->values.p) + (size_t)blk_n * per_view);
             blk_n += take;
             v += take;
             if (blk_n == kViewBlock) flush();
@@ -1319,6 +1391,7 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         b = e;
     }
     flush();
+    if (s1_used) CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
 }
 
 // views [lo, hi) from a radial lattice (after the radial IFFT) -> frames

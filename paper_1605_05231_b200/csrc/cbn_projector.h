@@ -159,7 +159,23 @@ struct cbn_projector_s {
     cbn::DevBuf<double> red;        // reductions
     cbn::DevBuf<int> flag;          // non-finite flag
 
+    // second lane of the forward view-block loop: the resample gather and the
+    // reverse Grangeat of block k+1 run on `s1` while block k finishes on the
+    // caller's stream (own FFT plans/work area and per-block scratch)
+    struct Lane {
+        cbn::FFTCache fft;
+        cbn::DevBuf<float2> gr_t, gr_tv, gr_grid;
+        cbn::DevBuf<float> values;
+        cbn::DevBuf<double> red;
+    };
+    Lane lane1;
+    cudaStream_t s1 = nullptr;
+    cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
+
     ~cbn_projector_s() {
         for (auto& kv : ls_rows) delete kv.second;
+        if (ev_s0) cudaEventDestroy(ev_s0);
+        if (ev_s1) cudaEventDestroy(ev_s1);
+        if (s1) cudaStreamDestroy(s1);
     }
 };
