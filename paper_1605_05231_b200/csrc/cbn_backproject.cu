@@ -245,7 +245,7 @@ void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const Umb
 // forward_grangeat_view for nb (<= 32) views: frames (nb x nu x nv) -> values
 // (nb x n_mu x n_t), grangeat.py:131-146
 void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, float* values,
-                            cudaStream_t s) {
+                            cudaStream_t s, GrBufs B) {
     GrangeatPlan& gp = p->bgr;
     if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
     projector_prepare_gr_points(p, gp, p->bumb, false, s);
@@ -253,27 +253,32 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
     const int nu = p->g.nu, nv = p->g.nv;
     const int64_t per_view = (int64_t)u.n_mu * u.n_t;
-    p->gr_grid.ensure((size_t)nb * Ku * Kv);
-    p->gr_t.ensure((size_t)nb * per_view);
+    B.grid.ensure((size_t)nb * Ku * Kv);
+    B.t.ensure((size_t)nb * per_view);
     const int64_t gtot = (int64_t)nb * Ku * Kv;
     k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames, nu, nv, Ku, Kv, gp.pu, gp.pv,
                                                     p->g.so_mm, gp.s32.p, gp.smax, gtot,
-                                                    p->gr_grid.p);
+                                                    B.grid.p);
     CBN_LAUNCH_CHECK();
     long long kd[2] = {Ku, Kv};
-    p->fft.exec(p->fft.get(2, kd, nb), p->gr_grid.p, p->gr_grid.p, CUFFT_FORWARD, s);
+    B.fft.exec(B.fft.get(2, kd, nb), B.grid.p, B.grid.p, CUFFT_FORWARD, s);
     const BinPlan& bb = gp.bins;
     dim3 grid(bb.nsubs, (nb + kGrVG - 1) / kGrVG);
     k_gr_gather_binned<kGrJ, kGrVG><<<grid, 256, sizeof(float2) * kGrVG * bb.nreg, s>>>(
-        p->gr_grid.p, (size_t)Ku * Kv, bb.geom<2>(), reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p),
-        bb.subs.p, p->gr_t.p, (size_t)per_view, nb);
+        B.grid.p, (size_t)Ku * Kv, bb.geom<2>(), reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p),
+        bb.subs.p, B.t.p, (size_t)per_view, nb);
     CBN_LAUNCH_CHECK();
     long long nt[1] = {u.n_t};
-    p->fft.exec(p->fft.get(1, nt, (long long)nb * u.n_mu), p->gr_t.p, p->gr_t.p, CUFFT_INVERSE, s);
+    B.fft.exec(B.fft.get(1, nt, (long long)nb * u.n_mu), B.t.p, B.t.p, CUFFT_INVERSE, s);
     const int64_t vt = (int64_t)nb * per_view;
-    k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(p->gr_t.p, gp.w2.p, u.n_t,
+    k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(B.t.p, gp.w2.p, u.n_t,
                                                   1.0 / ((double)u.n_t * u.dt), vt, values);
     CBN_LAUNCH_CHECK();
+}
+
+void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, float* values,
+                            cudaStream_t s) {
+    grangeat_forward_block(p, frames, nb, values, s, main_bufs(p));
 }
 
 // ------------------------------------------------------------------ phases
@@ -385,12 +390,30 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
     const int nu = p->g.nu, nv = p->g.nv;
     CBN_CUDA(cudaMemsetAsync(acc, 0, sizeof(float2) * x.dsize, s));
     p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
+    // blocks of 32 views alternate between the caller's stream and s1
     auto forward_grangeat = [&](int v0, int nb, float* out) {
+        const bool dual = nb > 32 && lanes_allowed();
+        if (dual) {
+            // plan state both lanes read, then fork
+            GrangeatPlan& gp = p->bgr;
+            if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
+            projector_prepare_gr_points(p, gp, p->bumb, false, s);
+            ensure_lane1(p);
+            CBN_CUDA(cudaEventRecord(p->ev_s0, s));
+            CBN_CUDA(cudaStreamWaitEvent(p->s1, p->ev_s0, 0));
+        }
         for (int k = 0; k < nb; k += 32) {
-            StageScope st(p->timer, "grangeat_forward", s);
+            const bool l1 = dual && ((k / 32) & 1);
+            const cudaStream_t ls = l1 ? p->s1 : s;
+            StageScope st(p->timer, "grangeat_forward", ls);
             const int n = std::min(32, nb - k);
             grangeat_forward_block(p, frames + (size_t)(v0 + k - lo) * nu * nv, n,
-                                   out + (size_t)k * per_view, s);
+                                   out + (size_t)k * per_view, ls,
+                                   l1 ? lane_bufs(p) : main_bufs(p));
+        }
+        if (dual) {
+            CBN_CUDA(cudaEventRecord(p->ev_s1, p->s1));
+            CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
         }
     };
     float* gn = reinterpret_cast<float*>(p->big.p);    // the transposed grid (real parts)

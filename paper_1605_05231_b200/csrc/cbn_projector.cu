@@ -1166,19 +1166,6 @@ GrPost gr_post(const P* p, const GrangeatPlan& gp) {
 }
 
 // reverse_grangeat_view for nb views: vals (nb x n_mu x n_t) -> frames (nb x nu x nv)
-struct GrBufs {
-    FFTCache& fft;
-    DevBuf<float2>& t;
-    DevBuf<float2>& tv;
-    DevBuf<float2>& grid;
-    DevBuf<double>& red;
-};
-GrBufs main_bufs(P* p) { return {p->fft, p->gr_t, p->gr_tv, p->gr_grid, p->red}; }
-GrBufs lane_bufs(P* p) {
-    auto& l = p->lane1;
-    return {l.fft, l.gr_t, l.gr_tv, l.gr_grid, l.red};
-}
-
 void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s,
                       GrBufs B) {
     GrangeatPlan& gp = p->fgr;
@@ -1296,13 +1283,8 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
     const bool lanes = views_in_lanes(p);
     // two lanes (the caller's stream and s1) alternate over view blocks so one
     // block's Grangeat FFTs overlap the next block's resample gather
-    const char* one = std::getenv("CBN_ONE_STREAM");
-    const bool dual = lanes && !values_out && !(one && one[0] == '1');
-    if (dual && !p->s1) {
-        CBN_CUDA(cudaStreamCreateWithFlags(&p->s1, cudaStreamNonBlocking));
-        CBN_CUDA(cudaEventCreateWithFlags(&p->ev_s0, cudaEventDisableTiming));
-        CBN_CUDA(cudaEventCreateWithFlags(&p->ev_s1, cudaEventDisableTiming));
-    }
+    const bool dual = lanes && !values_out && lanes_allowed();
+    if (dual) ensure_lane1(p);
     if (dual) {
         p->lane1.values.ensure((size_t)per_view * kViewBlock);
         // everything s1 reads besides the grid exists before the first grid event

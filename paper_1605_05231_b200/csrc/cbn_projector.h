@@ -179,3 +179,35 @@ struct cbn_projector_s {
         if (s1) cudaStreamDestroy(s1);
     }
 };
+
+namespace cbn {
+
+// per-lane Grangeat scratch: the projector's own buffers (lane 0, caller's
+// stream) or lane1's (stream s1)
+struct GrBufs {
+    FFTCache& fft;
+    DevBuf<float2>& t;
+    DevBuf<float2>& tv;
+    DevBuf<float2>& grid;
+    DevBuf<double>& red;
+};
+inline GrBufs main_bufs(cbn_projector_s* p) {
+    return {p->fft, p->gr_t, p->gr_tv, p->gr_grid, p->red};
+}
+inline GrBufs lane_bufs(cbn_projector_s* p) {
+    auto& l = p->lane1;
+    return {l.fft, l.gr_t, l.gr_tv, l.gr_grid, l.red};
+}
+inline void ensure_lane1(cbn_projector_s* p) {
+    if (p->s1) return;
+    CBN_CUDA(cudaStreamCreateWithFlags(&p->s1, cudaStreamNonBlocking));
+    CBN_CUDA(cudaEventCreateWithFlags(&p->ev_s0, cudaEventDisableTiming));
+    CBN_CUDA(cudaEventCreateWithFlags(&p->ev_s1, cudaEventDisableTiming));
+}
+// CBN_ONE_STREAM=1 keeps every lane on the caller's stream (diagnostics)
+inline bool lanes_allowed() {
+    const char* one = std::getenv("CBN_ONE_STREAM");
+    return !(one && one[0] == '1');
+}
+
+}  // namespace cbn
