@@ -201,9 +201,18 @@ constexpr size_t gr_spread_owned_smem() {
 // values as one 256-byte row of the view-fastest t-spectra.  No shared-memory
 // read-modify-write, no atomics, and every grid cell is written once.
 struct GrEntry {
-    int col;        // R2C half-spectrum index of the node's value (~index: conjugate)
-    float wx, wy;   // w_u[a] w_v[b] * fac
-    int pad;
+    int id;         // row of the node-scaled t-spectra (GrNode table)
+    float w;        // w_u[a] w_v[b] * pair factor
+};
+
+// One row of the node-scaled reverse t-spectra: fac * (conj?) R2C bin `src`.
+// Rows [0, nspec) are the half-spectrum bins (the live node of that bin, or
+// zero); rows past nspec hold the second node of bins whose two nodes (t and
+// its mirror) both survive the pair merge.
+struct GrNode {
+    int src;        // R2C half-spectrum index
+    int conj;       // 1: the node reads the conjugate of bin src
+    float2 fac;     // node factor (filter * phase)
 };
 
 // Reverse Grangeat values are conjugate-symmetric in t (real detector lines,
@@ -229,17 +238,44 @@ CBN_D int gr_pair_factor(const PolarSrc& src, const KBSet& kb, int J, int i) {
     return 2 * jt < n_t ? 2 : 0;
 }
 
+// node rows: per live point (pts order) its GrNode row id, -1 if inert or
+// dropped by the pair merge (see GrNode)
+template <int J>
+__global__ void k_gr_node_ids(const GrPoint<J>* __restrict__ pts, const int* __restrict__ perm,
+                              int64_t m, PolarSrc src, KBSet kb, int nspec,
+                              int* __restrict__ node_id, int* __restrict__ mult_out,
+                              GrNode* __restrict__ tab, int* __restrict__ nextra) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    const GrPoint<J>& g = pts[q];
+    int mult = 0;
+    if (g.fac.x != 0.f || g.fac.y != 0.f) mult = gr_pair_factor(src, kb, J, perm[q]);
+    int id = -1;
+    if (mult) {
+        const int half = g.col >= 0 ? g.col : ~g.col;
+        // the direct node, or a kept conjugate node whose partner was merged in,
+        // owns row `half`; a conjugate node beside a live partner takes a new row
+        id = (g.col >= 0 || mult == 2) ? half : nspec + atomicAdd(nextra, 1);
+        GrNode n;
+        n.src = half;
+        n.conj = g.col >= 0 ? 0 : 1;
+        n.fac = g.fac;
+        tab[id] = n;
+    }
+    node_id[q] = id;
+    mult_out[q] = mult;
+}
+
 template <int J>
 __global__ void k_gr_csr_count(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts,
-                               const SubProblem* __restrict__ subs, const int* __restrict__ perm,
-                               PolarSrc src, KBSet kb, int* __restrict__ counts) {
+                               const SubProblem* __restrict__ subs,
+                               const int* __restrict__ node_id, int* __restrict__ counts) {
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<2>(tg, sp.bin, o);
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
+        if (node_id[sp.start + k] < 0) continue;
         const GrPoint<J>& g = pts[sp.start + k];
-        if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
-        if (gr_pair_factor(src, kb, J, perm[sp.start + k]) == 0) continue;
 #pragma unroll
         for (int a = 0; a < J; ++a)
 #pragma unroll
@@ -252,29 +288,26 @@ __global__ void k_gr_csr_count(TileGeom<2> tg, const GrPoint<J>* __restrict__ pt
 
 template <int J>
 __global__ void k_gr_csr_fill(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts,
-                              const SubProblem* __restrict__ subs, const int* __restrict__ perm,
-                              PolarSrc src, KBSet kb, int* __restrict__ cursor,
-                              GrEntry* __restrict__ ent) {
+                              const SubProblem* __restrict__ subs,
+                              const int* __restrict__ node_id, const int* __restrict__ mult,
+                              int* __restrict__ cursor, GrEntry* __restrict__ ent) {
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<2>(tg, sp.bin, o);
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
+        const int id = node_id[sp.start + k];
+        if (id < 0) continue;
         const GrPoint<J>& g = pts[sp.start + k];
-        if (g.fac.x == 0.f && g.fac.y == 0.f) continue;
-        const int mult = gr_pair_factor(src, kb, J, perm[sp.start + k]);
-        if (mult == 0) continue;
+        const float fm = (float)mult[sp.start + k];
 #pragma unroll
         for (int a = 0; a < J; ++a)
 #pragma unroll
             for (int b = 0; b < J; ++b) {
                 const size_t cell = (size_t)wrapc(o[0] + g.lu + a, tg.K[0]) * tg.K[1] +
                                     wrapc(o[1] + g.lv + b, tg.K[1]);
-                const float w = g.w[a] * g.w[J + b] * (float)mult;
                 GrEntry e;
-                e.col = g.col;
-                e.wx = w * g.fac.x;
-                e.wy = w * g.fac.y;
-                e.pad = 0;
+                e.id = id;
+                e.w = g.w[a] * g.w[J + b] * fm;
                 ent[atomicAdd(cursor + cell, 1)] = e;
             }
     }
@@ -292,6 +325,7 @@ k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
     __shared__ float2 tile[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c0 = (int64_t)blockIdx.x * 32;
+    const float2* tl = tfv + lane;
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
         const int cl = warp + 8 * q;
@@ -303,24 +337,22 @@ k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
             // shuffles; kGrRows value rows in flight
             for (int base = col_ptr[c]; base < e1; base += 32) {
                 const int n = min(32, e1 - base);
-                GrEntry mine{0, 0.f, 0.f, 0};
+                GrEntry mine{0, 0.f};
                 if (lane < n) mine = ent[base + lane];
                 for (int j0 = 0; j0 < n; j0 += kGrRows) {
                     float2 y[kGrRows];
-                    float wx[kGrRows], wy[kGrRows];
+                    float w[kGrRows];
 #pragma unroll
                     for (int j = 0; j < kGrRows; ++j) {
                         const int src = j0 + j;               // < 32; entries past n have w = 0
-                        const int col = __shfl_sync(0xffffffffu, mine.col, src);
-                        wx[j] = __shfl_sync(0xffffffffu, mine.wx, src);
-                        wy[j] = __shfl_sync(0xffffffffu, mine.wy, src);
-                        y[j] = __ldg(tfv + (size_t)(col >= 0 ? col : ~col) * 32 + lane);
-                        y[j].y = col >= 0 ? y[j].y : -y[j].y;   // Hermitian half: conj
+                        const int id = __shfl_sync(0xffffffffu, mine.id, src);
+                        w[j] = __shfl_sync(0xffffffffu, mine.w, src);
+                        y[j] = __ldg(tl + (size_t)id * 32);
                     }
 #pragma unroll
                     for (int j = 0; j < kGrRows; ++j) {
-                        acc.x = fmaf(wx[j], y[j].x, fmaf(-wy[j], y[j].y, acc.x));
-                        acc.y = fmaf(wx[j], y[j].y, fmaf(wy[j], y[j].x, acc.y));
+                        acc.x = fmaf(w[j], y[j].x, acc.x);
+                        acc.y = fmaf(w[j], y[j].y, acc.y);
                     }
                 }
             }
@@ -334,9 +366,11 @@ k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
     }
 }
 
-// [nb views][n] -> [n][32] (views >= nb unwritten; the readers mask them)
-__global__ void k_views_last(const float2* __restrict__ in, int nb, int64_t n,
-                             float2* __restrict__ out);
+// node-scaled t-spectra: out[id][v] = fac_id * (conj?) in[v][src_id] for
+// ids [0, n), views v < nb (views >= nb unwritten; the readers mask them)
+__global__ void k_views_nodes(const float2* __restrict__ in, int nb, int64_t nspec,
+                              const GrNode* __restrict__ tab, int64_t n,
+                              float2* __restrict__ out);
 
 // forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv)
 template <int J, int VG>

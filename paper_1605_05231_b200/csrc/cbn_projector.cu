@@ -408,13 +408,22 @@ __global__ void k_pad_lattice(const float2* __restrict__ src, int shift, float s
 }
 
 // ---- reverse Grangeat (grangeat.py:149-170)
-__global__ void k_views_last(const float2* __restrict__ in, int nb, int64_t n,
-                             float2* __restrict__ out) {
+__global__ void k_views_nodes(const float2* __restrict__ in, int nb, int64_t nspec,
+                              const GrNode* __restrict__ tab, int64_t n,
+                              float2* __restrict__ out) {
     __shared__ float2 tile[32][33];
+    __shared__ GrNode nd[32];
     const int64_t e0 = (int64_t)blockIdx.x * 32;
+    if (threadIdx.x < 32 && e0 + threadIdx.x < n) nd[threadIdx.x] = tab[e0 + threadIdx.x];
+    __syncthreads();
     for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
         const int v = q >> 5, e = q & 31;
-        if (v < nb && e0 + e < n) tile[v][e] = in[(size_t)v * n + e0 + e];
+        if (v < nb && e0 + e < n) {
+            const GrNode g = nd[e];
+            float2 x = in[(size_t)v * nspec + g.src];
+            if (g.conj) x.y = -x.y;
+            tile[v][e] = make_float2(g.fac.x * x.x - g.fac.y * x.y, g.fac.x * x.y + g.fac.y * x.x);
+        }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
@@ -1189,34 +1198,50 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     if (cell_gather) {
         const int64_t ncell = (int64_t)Ku * Kv;
         if (!gp.cell_ptr.p) {
-            // plan step: per-cell CSR of (node, complex weight) entries
+            // plan step: node rows (GrNode), then the per-cell CSR of (row, weight) entries
             const BinPlan& bb = gp.bins;
-            DevBuf<int> counts((size_t)ncell);
-            CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncell, s));
+            const int64_t nspec = (int64_t)u.n_mu * nh;
             const GrPoint<kGrJ>* pts = reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p);
             const PolarSrc psrc{u.omega_t.p, u.cos_mu.p, u.sin_mu.p, gp.pu, gp.pv, u.n_t};
-            k_gr_csr_count<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, bb.perm.p,
-                                                         psrc, gp.kb, counts.p);
+            const int64_t m = gp.m;
+            DevBuf<int> node_id((size_t)m), mult((size_t)m), nextra(1);
+            DevBuf<GrNode> tab((size_t)(nspec + m));
+            CBN_CUDA(cudaMemsetAsync(tab.p, 0, sizeof(GrNode) * (nspec + m), s));
+            CBN_CUDA(cudaMemsetAsync(nextra.p, 0, sizeof(int), s));
+            k_gr_node_ids<kGrJ><<<blocks_for(m, 256), 256, 0, s>>>(
+                pts, bb.perm.p, m, psrc, gp.kb, (int)nspec, node_id.p, mult.p, tab.p, nextra.p);
+            CBN_LAUNCH_CHECK();
+            int h_extra = 0;
+            CBN_CUDA(cudaMemcpyAsync(&h_extra, nextra.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            DevBuf<int> counts((size_t)ncell);
+            CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncell, s));
+            k_gr_csr_count<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, node_id.p,
+                                                         counts.p);
             CBN_LAUNCH_CHECK();
             std::vector<int> h((size_t)ncell + 1, 0);
             CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncell,
                                      cudaMemcpyDeviceToHost, s));
             CBN_CUDA(cudaStreamSynchronize(s));
+            gp.n_rows = nspec + h_extra;
+            gp.node_tab.alloc((size_t)gp.n_rows);
+            CBN_CUDA(cudaMemcpyAsync(gp.node_tab.p, tab.p, sizeof(GrNode) * gp.n_rows,
+                                     cudaMemcpyDeviceToDevice, s));
             for (size_t q = 1; q < h.size(); ++q) h[q] += h[q - 1];
             gp.cell_ptr.upload(h.data(), h.size(), s);
             gp.cell_ent.alloc(sizeof(GrEntry) * (size_t)std::max(h.back(), 1));
             CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncell, cudaMemcpyHostToDevice,
                                      s));
-            k_gr_csr_fill<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, bb.perm.p,
-                                                         psrc, gp.kb, counts.p,
+            k_gr_csr_fill<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, node_id.p,
+                                                         mult.p, counts.p,
                                                          reinterpret_cast<GrEntry*>(gp.cell_ent.p));
             CBN_LAUNCH_CHECK();
             CBN_CUDA(cudaStreamSynchronize(s));
         }
         StageScope st(p->timer, "grangeat_spread", s);
         const int64_t nspec = (int64_t)u.n_mu * nh;
-        B.tv.ensure((size_t)nspec * 32);
-        k_views_last<<<(unsigned)((nspec + 31) / 32), 256, 0, s>>>(B.t.p, nb, nspec, B.tv.p);
+        B.tv.ensure((size_t)gp.n_rows * 32);
+        k_views_nodes<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
+            B.t.p, nb, nspec, gp.node_tab.p, gp.n_rows, B.tv.p);
         CBN_LAUNCH_CHECK();
         k_gr_gather_cells<<<(unsigned)((ncell + 31) / 32), 256, 0, s>>>(
             B.grid.p, (size_t)ncell, ncell, gp.cell_ptr.p,

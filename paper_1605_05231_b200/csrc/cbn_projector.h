@@ -55,6 +55,8 @@ struct GrangeatPlan {
     bool pts_ready = false;
     DevBuf<int> cell_ptr;               // reverse: CSR of (node, weight) entries per grid cell
     DevBuf<char> cell_ent;              // GrEntry per (node, tap)
+    DevBuf<GrNode> node_tab;            // reverse: node-scaled t-spectrum rows
+    int64_t n_rows = 0;                 // rows of node_tab (nspec + second nodes)
 };
 
 constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)
