@@ -242,12 +242,13 @@ k_resample_views(const float2* __restrict__ G, int K0, int K1, int K2,
 // phi-fast grid and the nine rho x theta weight products, so a lane's work is
 // nine row bases, 27 loads of real parts and 36 FMAs -- the warp-uniform
 // index math of k_resample_views is done once per plan instead of per lane.
-struct RsRow3 {
+struct alignas(16) RsRow3 {
     unsigned int row[9];   // (wrap(f0 + a) K1 + wrap(f1 + b)) K2, a major
     int f2;                // first phi tap of view 0
     int valid;
     float w2[3];
     float wab[9];          // w0[a] w1[b]
+    int pad;               // 96 bytes: six 16-byte loads per record
 };
 
 __global__ void k_rs_rows3(const RsTap<3>* __restrict__ taps, int64_t n, int K0, int K1, int K2,
@@ -266,13 +267,15 @@ __global__ void k_rs_rows3(const RsTap<3>* __restrict__ taps, int64_t n, int K0,
         }
     r.f2 = tp.f[2];
     r.valid = tp.valid;
+    r.pad = 0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) r.w2[c] = tp.w[2][c];
     out[t] = r;
 }
 
+template <int ES>   // floats per grid cell: 1 real grid, 2 complex (real part read)
 __global__ void __launch_bounds__(256)
-k_resample_rows3(const float* __restrict__ G, int es, int K2, const RsRow3* __restrict__ rows,
+k_resample_rows3(const float* __restrict__ G, int K2, const RsRow3* __restrict__ rows,
                  int64_t per_view, int v0, int nviews, int shift, float* __restrict__ vals,
                  const float* __restrict__ tscale, int n_t) {
     __shared__ float tile[32][33];
@@ -285,7 +288,12 @@ k_resample_rows3(const float* __restrict__ G, int es, int K2, const RsRow3* __re
         const int64_t t = t0 + tl;
         float out = 0.f;
         if (t < per_view) {
-            const RsRow3& rr = rows[t];
+            // the whole record through six 16-byte loads (same address in all lanes)
+            RsRow3 rr;
+            const uint4* src = reinterpret_cast<const uint4*>(rows + t);
+            uint4* dst = reinterpret_cast<uint4*>(&rr);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) dst[k] = __ldg(src + k);
             if (rr.valid && lane < nviews) {
                 int c0 = rr.f2 - pshift;
                 c0 += c0 < 0 ? K2 : 0;
@@ -294,13 +302,30 @@ k_resample_rows3(const float* __restrict__ G, int es, int K2, const RsRow3* __re
                 c2 -= c2 >= K2 ? K2 : 0;
                 const float w0 = rr.w2[0], w1 = rr.w2[1], w2 = rr.w2[2];
                 float acc = 0.f;
+                if constexpr (ES == 1) {
+                    // 32-bit cell index (grid < 2^32 cells): one add and one wide
+                    // multiply-add per tap address
+                    const unsigned u0 = c0, u1 = c1, u2 = c2;
 #pragma unroll
-                for (int ab = 0; ab < 9; ++ab) {
-                    const float* base = G + (size_t)es * rr.row[ab];   // es: floats per cell
-                    float r = w0 * __ldg(base + es * c0);
-                    r = fmaf(w1, __ldg(base + es * c1), r);
-                    r = fmaf(w2, __ldg(base + es * c2), r);
-                    acc = fmaf(rr.wab[ab], r, acc);
+                    for (int ab = 0; ab < 9; ++ab) {
+                        const unsigned b = rr.row[ab];
+                        float r = w0 * __ldg(G + (b + u0));
+                        r = fmaf(w1, __ldg(G + (b + u1)), r);
+                        r = fmaf(w2, __ldg(G + (b + u2)), r);
+                        acc = fmaf(rr.wab[ab], r, acc);
+                    }
+                } else {
+                    const float* g0 = G + (size_t)ES * c0;
+                    const float* g1 = G + (size_t)ES * c1;
+                    const float* g2 = G + (size_t)ES * c2;
+#pragma unroll
+                    for (int ab = 0; ab < 9; ++ab) {
+                        const size_t o = (size_t)ES * rr.row[ab];
+                        float r = w0 * __ldg(g0 + o);
+                        r = fmaf(w1, __ldg(g1 + o), r);
+                        r = fmaf(w2, __ldg(g2 + o), r);
+                        acc = fmaf(rr.wab[ab], r, acc);
+                    }
                 }
                 out = acc;   // Re(resample_apply): the real part of each cell
             }
@@ -1100,11 +1125,15 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
         UmbrellaTables& u = p->fumb;
         StageScope st(p->timer, "resample_gather", s);
         if constexpr (J == 3) {
-            const bool re = real_grid(p);
-            k_resample_rows3<<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
-                re ? p->grid_re : reinterpret_cast<const float*>(p->big.p), re ? 1 : 2, ax[0].K,
-                reinterpret_cast<const RsRow3*>(u.rows.p), per_view, v0, nb, shift, vals, tscale,
-                p->fumb.n_t);
+            const unsigned nblk = (unsigned)((per_view + 31) / 32);
+            const RsRow3* rows = reinterpret_cast<const RsRow3*>(u.rows.p);
+            if (real_grid(p))
+                k_resample_rows3<1><<<nblk, 256, 0, s>>>(p->grid_re, ax[0].K, rows, per_view, v0,
+                                                         nb, shift, vals, tscale, p->fumb.n_t);
+            else
+                k_resample_rows3<2><<<nblk, 256, 0, s>>>(reinterpret_cast<const float*>(p->big.p),
+                                                         ax[0].K, rows, per_view, v0, nb, shift,
+                                                         vals, tscale, p->fumb.n_t);
             CBN_LAUNCH_CHECK();
             return 0;
         }
