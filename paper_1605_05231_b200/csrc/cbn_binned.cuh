@@ -91,24 +91,32 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
     const SubProblem sp = subs[blockIdx.x];
     int o[3];
     bin_origin<D>(tg, sp.bin, o);
-    const int R0 = tg.R[0], R1 = D == 3 ? tg.R[1] : tg.P, R2 = D == 3 ? tg.R[2] : 1;
+    const int R0 = tg.R[0], R1 = D == 3 ? tg.R[1] : tg.P;
     const int P2 = D == 3 ? tg.P : 1;
+    const int R2 = D == 3 ? tg.R[2] : 1;
     const int nreg = R0 * R1 * P2;
+    // cell -> (r0, r1, r2) by multiply-shift division: exact while e * (mP P2 - 2^20)
+    // < 2^20 and e * mP < 2^32, true for the regions used (< 8K cells, P2 = 1 or >= 16)
+    const unsigned mP = ((1u << 20) + P2 - 1) / P2, mR = ((1u << 20) + R1 - 1) / R1;
+    unsigned negmask = 0;   // HALF: region columns r2 read as conj(G[-k])
+    if constexpr (D == 3 && HALF) {
+        const int lane = threadIdx.x & 31;
+        const bool neg = lane < R2 && wrapc(o[2] + lane, tg.K[2]) >= tg.K[2] / 2 + 1;
+        negmask = __ballot_sync(0xffffffffu, neg);
+    }
     for (int e = threadIdx.x; e < nreg; e += blockDim.x) {
-        const int r2 = e % P2, r01 = e / P2, r1 = r01 % R1, r0 = r01 / R1;
+        const int r01 = (int)(((unsigned)e * mP) >> 20), r2 = e - r01 * P2;
+        const int r0 = (int)(((unsigned)r01 * mR) >> 20), r1 = r01 - r0 * R1;
         if (r2 >= R2 || (D == 2 && r1 >= tg.R[1])) continue;
         size_t g;
         if constexpr (D == 3 && HALF) {
             int i0 = wrapc(o[0] + r0, tg.K[0]), i1 = wrapc(o[1] + r1, tg.K[1]);
             int i2 = wrapc(o[2] + r2, tg.K[2]);
             const int h2 = tg.K[2] / 2 + 1;
-            if (i2 >= h2) {
+            if ((negmask >> r2) & 1u) {   // conjugated after the copy
                 i0 = i0 ? tg.K[0] - i0 : 0;
                 i1 = i1 ? tg.K[1] - i1 : 0;
                 i2 = tg.K[2] - i2;
-                const float2 v = __ldg(grid + ((size_t)i0 * tg.K[1] + i1) * h2 + i2);
-                tile[e] = make_float2(v.x, -v.y);
-                continue;
             }
             g = ((size_t)i0 * tg.K[1] + i1) * h2 + i2;
         } else if constexpr (D == 3)
@@ -123,6 +131,14 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
                      "l"(grid + g));
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if constexpr (D == 3 && HALF) {
+        // each thread conjugates the mirrored cells it copied itself
+        if (negmask)
+            for (int e = threadIdx.x; e < nreg; e += blockDim.x) {
+                const int r01 = (int)(((unsigned)e * mP) >> 20), r2 = e - r01 * P2;
+                if (r2 < R2 && ((negmask >> r2) & 1u)) tile[e].y = -tile[e].y;
+            }
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
         const int64_t i = perm[sp.start + k];

@@ -881,6 +881,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         const BinPlan& bp = p->fspec_bins;
         const int s0 = (int)((int64_t)bp.nsubs * part / nparts);
         const int s1 = (int)((int64_t)bp.nsubs * (part + 1) / nparts);
+        CBN_REQUIRE(bp.tg.R[2] <= 32, "half-spectrum gather: region rows above 32 cells");
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             if (s1 > s0)
