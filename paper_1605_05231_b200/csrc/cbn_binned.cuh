@@ -95,9 +95,8 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
     const int P2 = D == 3 ? tg.P : 1;
     const int R2 = D == 3 ? tg.R[2] : 1;
     const int nreg = R0 * R1 * P2;
-    // cell -> (r0, r1, r2) by multiply-shift division: exact while e * (mP P2 - 2^20)
-    // < 2^20 and e * mP < 2^32, true for the regions used (< 8K cells, P2 = 1 or >= 16)
-    const unsigned mP = ((1u << 20) + P2 - 1) / P2, mR = ((1u << 20) + R1 - 1) / R1;
+    // cell -> (r0, r1, r2) by multiply-shift division (FastDiv)
+    const FastDiv dP(P2), dR(R1);
     unsigned negmask = 0;   // HALF: region columns r2 read as conj(G[-k])
     if constexpr (D == 3 && HALF) {
         const int lane = threadIdx.x & 31;
@@ -105,8 +104,8 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
         negmask = __ballot_sync(0xffffffffu, neg);
     }
     for (int e = threadIdx.x; e < nreg; e += blockDim.x) {
-        const int r01 = (int)(((unsigned)e * mP) >> 20), r2 = e - r01 * P2;
-        const int r0 = (int)(((unsigned)r01 * mR) >> 20), r1 = r01 - r0 * R1;
+        const int r01 = dP.div(e), r2 = e - r01 * P2;
+        const int r0 = dR.div(r01), r1 = r01 - r0 * R1;
         if (r2 >= R2 || (D == 2 && r1 >= tg.R[1])) continue;
         size_t g;
         if constexpr (D == 3 && HALF) {
@@ -135,7 +134,7 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
         // each thread conjugates the mirrored cells it copied itself
         if (negmask)
             for (int e = threadIdx.x; e < nreg; e += blockDim.x) {
-                const int r01 = (int)(((unsigned)e * mP) >> 20), r2 = e - r01 * P2;
+                const int r01 = dP.div(e), r2 = e - r01 * P2;
                 if (r2 < R2 && ((negmask >> r2) & 1u)) tile[e].y = -tile[e].y;
             }
     }
@@ -399,9 +398,11 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
         }
     }
     __syncthreads();
+    const FastDiv dP(P), dR1(R1);
     for (int e = threadIdx.x; e < nreg; e += NP) {
-        const int r2 = e % P, r01 = e / P, r1 = r01 % R1, r0 = r01 / R1;
+        const int r01 = dP.div(e), r2 = e - r01 * P;
         if (r2 >= R2) continue;
+        const int r0 = dR1.div(r01), r1 = r01 - r0 * R1;
         const float2 s = reg[e];
         if (s.x == 0.f && s.y == 0.f) continue;
         const size_t g = ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1])) *
@@ -491,9 +492,11 @@ k_spread_owned8(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
         }
     }
     __syncthreads();
+    const FastDiv dP(P), dR1(R1);
     for (int e = threadIdx.x; e < nreg; e += NP) {
-        const int r2 = e % P, r01 = e / P, r1 = r01 % R1, r0 = r01 / R1;
+        const int r01 = dP.div(e), r2 = e - r01 * P;
         if (r2 >= R2) continue;
+        const int r0 = dR1.div(r01), r1 = r01 - r0 * R1;
         const float2 sv = reg[e];
         if (sv.x == 0.f && sv.y == 0.f) continue;
         const size_t g = ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1])) *

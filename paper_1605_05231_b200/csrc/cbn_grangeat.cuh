@@ -386,9 +386,10 @@ k_gr_gather_binned(const float2* __restrict__ grids, size_t grid_stride, TileGeo
     bin_origin<2>(tg, sp.bin, o);
     const int R1 = tg.R[1];
     const int nreg = tg.R[0] * R1;
+    const FastDiv dreg(nreg), dR1(R1);
     for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
-        const int v = e / nreg, c = e % nreg;
-        const int r0 = c / R1, r1 = c % R1;
+        const int v = dreg.div(e), c = e - v * nreg;
+        const int r0 = dR1.div(c), r1 = c - r0 * R1;
         const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
                          (unsigned)__cvta_generic_to_shared(tile + e)),

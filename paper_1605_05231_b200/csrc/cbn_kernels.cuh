@@ -42,6 +42,16 @@ CBN_D int wrapc(int c, int K) {
     return c >= K ? c - K : c;
 }
 
+// e / d by multiply-shift for the small shared-memory region indices: exact
+// while e * (m d - 2^20) < 2^20 and e * m < 2^32 (regions of < 8K cells, d >= 16
+// or e < 4096)
+struct FastDiv {
+    unsigned m;
+    int d;
+    CBN_D explicit FastDiv(int d_) : m(((1u << 20) + (unsigned)d_ - 1) / (unsigned)d_), d(d_) {}
+    CBN_D int div(int e) const { return (int)(((unsigned)e * m) >> 20); }
+};
+
 // the nonzero taps of w and of its mirror wm are mirror images (mod K): same
 // count, and the mirror's lowest nonzero tap is minus the node's highest.  The
 // reference's exact support test can drop the edge tap on one side only
