@@ -195,6 +195,24 @@ int cbn_backproject_finish(cbn_projector* proj, void* lattice, int32_t part, int
                            void* grid, void* stream);
 int cbn_backproject_crop(cbn_projector* proj, void* grid, float* vol, void* stream);
 
+/* Phase 3 distributed by slabs of the slowest grid axis (x planes; SURVEY.md
+ * 8(e) adjoint steps 4-6: reduce-scatter of the grid by slab, slab IFFT,
+ * all-to-all transpose, column IFFT, crop).  Replaces cbn_backproject_crop
+ * when the summed grid is reduce-scattered instead of all-reduced.  With
+ * K = 2N and the balanced split y0_d = d * N / nparts:
+ * crop_slab: slab [device] = grid planes [x_lo, x_hi) (consumed): 2D inverse
+ *            FFT per plane, y/z crop + deapodisation; send [device]
+ *            (x_hi - x_lo) * N * N complex64 laid out [d][x][y - y0_d][z],
+ *            chunk d (contiguous) goes to the rank owning y range d.
+ * crop_cols: cols [device] [K][y_hi - y_lo][N] complex64 = the chunks
+ *            received from every slab in x order (consumed): inverse FFT
+ *            along x, x crop + deapodisation, Re, * bp_normalization;
+ *            vol_part [device] float32 [N][y_hi - y_lo][N]. */
+int cbn_backproject_crop_slab(cbn_projector* proj, void* slab, int32_t x_lo, int32_t x_hi,
+                              int32_t nparts, void* send, void* stream);
+int cbn_backproject_crop_cols(cbn_projector* proj, void* cols, int32_t y_lo, int32_t y_hi,
+                              float* vol_part, void* stream);
+
 /* Diagnostics: the forward plan's per-node Grangeat records in bin-sorted
  * order (56-byte records: int16 lu, lv; int32 col; float2 factor; float w[10])
  * and the sorted node ids [host]; *m in: capacity, out: node count. */

@@ -87,6 +87,8 @@ _SIGS = {
     "cbn_backproject_views": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "cbn_backproject_finish": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "cbn_backproject_crop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "cbn_backproject_crop_slab": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "cbn_backproject_crop_cols": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "cbn_projector_radial_lattice": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_projector_resample_views": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_projector_grangeat_reverse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_vp]),

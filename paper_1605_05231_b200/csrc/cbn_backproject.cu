@@ -674,22 +674,112 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
     });
 }
 
-// phase 3: grid (the summed spread) is consumed in place
-void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s) {
-    build_backward_plan(p, s);
-    CBN_REQUIRE(p->bspec_fit, "bp_crop before bp_finish");
+namespace {
+
+// sorted runs [a, b) of the (2N)-grid planes the crop reads along one axis
+std::vector<std::pair<int, int>> crop_plane_runs(int N, int K) {
+    std::vector<std::pair<int, int>> runs;
+    for (int k : pad_positions(N, K, false, false)) {
+        if (!runs.empty() && runs.back().second == k) runs.back().second = k + 1;
+        else runs.emplace_back(k, k + 1);
+    }
+    return runs;
+}
+
+// y/z crop + deapodisation of the 2D-transformed slab planes, written in the
+// all-to-all send layout [y block d][x][y - y0_d][z] (blocks: the balanced
+// split y0_d = d * ny / nparts), so each destination's chunk is contiguous and
+// the received chunks, concatenated in source-rank order, are [x][y][z].
+__global__ void k_crop_slab_yz(const float2* __restrict__ src, float2* __restrict__ dst,
+                               RemapAxis ay, RemapAxis az, int xc, int64_t plane, int nparts) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int ny = ay.n, nz = az.n;
+    if (q >= (int64_t)xc * ny * nz) return;
+    const int z = (int)(q % nz);
+    const int y = (int)((q / nz) % ny);
+    const int x = (int)(q / ((int64_t)nz * ny));
+    const int d = (int)(((int64_t)(y + 1) * nparts - 1) / ny);
+    const int y0 = (int)((int64_t)d * ny / nparts), y1 = (int)((int64_t)(d + 1) * ny / nparts);
+    const float sc = ay.scale[y] * az.scale[z];
+    const float2 g = src[(int64_t)x * plane + (int64_t)ay.idx[y] * ay.sstride + az.idx[z]];
+    dst[(int64_t)xc * y0 * nz + ((int64_t)x * (y1 - y0) + (y - y0)) * nz + z] =
+        make_float2(g.x * sc, g.y * sc);
+}
+
+// x crop + deapodisation + Re of the x-transformed columns [K0][yc][nz]
+__global__ void k_crop_cols_x(const float2* __restrict__ src, float* __restrict__ dst,
+                              RemapAxis ax, int64_t row, float gain) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (int64_t)ax.n * row) return;
+    const int x = (int)(q / row);
+    const int64_t r = q % row;
+    dst[q] = gain * ax.scale[x] * src[(int64_t)ax.idx[x] * row + r].x;
+}
+
+void crop_tables(cbn_projector_s* p, RemapAxis* cax, cudaStream_t s) {
     const AxisPlan* sax = p->bspec;
     const int n = p->n_vol;
-    long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
-    StageScope st_ff(p->timer, "bp_ifft_crop", s);
-    p->fft.exec(p->fft.get(3, k3d, 1), grid, grid, CUFFT_INVERSE, s);
-    RemapAxis cax[3];
     const int64_t cstr[3] = {(int64_t)sax[1].K * sax[2].K, sax[2].K, 1};
     p->s32.ensure(3 * (size_t)n);
     CBN_CUDA(cudaMemcpyAsync(p->s32.p, p->bspec_s32.p, sizeof(float) * 3 * n,
                              cudaMemcpyDeviceToDevice, s));
     projector_build_tables(p, kTabCrop, sax, n, s, cax, cstr);
+}
+
+}  // namespace
+
+// phase 3: grid (the summed spread) is consumed in place.  Inverse 3D FFT
+// pruned to the x planes the crop reads (1D along x, then 2D on N of 2N planes).
+void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s) {
+    build_backward_plan(p, s);
+    CBN_REQUIRE(p->bspec_fit, "bp_crop before bp_finish");
+    const AxisPlan* sax = p->bspec;
+    long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
+    StageScope st_ff(p->timer, "bp_ifft_crop", s);
+    fft3_pruned(p->fft, grid, k3d, 1, crop_plane_runs(sax[0].N, sax[0].K), CUFFT_INVERSE, s);
+    RemapAxis cax[3];
+    crop_tables(p, cax, s);
     launch_remap<float2, kStoreRe>(3, grid, vol, cax, (float)p->c.bp_normalization, s);
+    CBN_LAUNCH_CHECK();
+}
+
+// phase 3 distributed by slabs of the slowest grid axis (SURVEY.md 8(e),
+// adjoint steps 4-6).  slab: planes [x_lo, x_hi) of the summed grid (consumed);
+// send: (x_hi - x_lo) * N * N complex in the all-to-all layout above.
+void bp_crop_slab(cbn_projector_s* p, float2* slab, int x_lo, int x_hi, int nparts, float2* send,
+                  cudaStream_t s) {
+    build_backward_plan(p, s);
+    CBN_REQUIRE(p->bspec_fit, "bp_crop_slab before bp_finish");
+    const AxisPlan* sax = p->bspec;
+    CBN_REQUIRE(0 <= x_lo && x_lo < x_hi && x_hi <= sax[0].K, "slab out of range");
+    CBN_REQUIRE(nparts >= 1 && nparts <= sax[1].N, "bad part count");
+    StageScope st_ff(p->timer, "bp_ifft_crop", s);
+    const int xc = x_hi - x_lo;
+    const long long k2[2] = {sax[1].K, sax[2].K};
+    p->fft.exec(p->fft.get(2, k2, xc), slab, slab, CUFFT_INVERSE, s);
+    RemapAxis cax[3];
+    crop_tables(p, cax, s);
+    const int64_t cells = (int64_t)xc * cax[1].n * cax[2].n;
+    k_crop_slab_yz<<<blocks_for(cells, 256), 256, 0, s>>>(slab, send, cax[1], cax[2], xc,
+                                                         (int64_t)sax[1].K * sax[2].K, nparts);
+    CBN_LAUNCH_CHECK();
+}
+
+// cols: [2N][y_hi - y_lo][N] complex (the chunks received from every slab,
+// consumed); vol_part: [N][y_hi - y_lo][N] float32 (the volume's y range).
+void bp_crop_cols(cbn_projector_s* p, float2* cols, int y_lo, int y_hi, float* vol_part,
+                  cudaStream_t s) {
+    build_backward_plan(p, s);
+    CBN_REQUIRE(p->bspec_fit, "bp_crop_cols before bp_finish");
+    const AxisPlan* sax = p->bspec;
+    CBN_REQUIRE(0 <= y_lo && y_lo < y_hi && y_hi <= sax[1].N, "y range out of bounds");
+    StageScope st_ff(p->timer, "bp_ifft_crop", s);
+    const int64_t row = (int64_t)(y_hi - y_lo) * sax[2].N;
+    p->fft.exec(p->fft.get_strided(sax[0].K, row, row, 1), cols, cols, CUFFT_INVERSE, s);
+    RemapAxis cax[3];
+    crop_tables(p, cax, s);
+    k_crop_cols_x<<<blocks_for((int64_t)cax[0].n * row, 256), 256, 0, s>>>(
+        cols, vol_part, cax[0], row, (float)p->c.bp_normalization);
     CBN_LAUNCH_CHECK();
 }
 

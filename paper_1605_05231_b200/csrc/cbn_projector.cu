@@ -1470,6 +1470,10 @@ void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaS
 void bp_views(cbn_projector_s* p, const float* frames, int lo, int hi, float2* acc, cudaStream_t s);
 void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* grid, cudaStream_t s);
 void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s);
+void bp_crop_slab(cbn_projector_s* p, float2* slab, int x_lo, int x_hi, int nparts, float2* send,
+                  cudaStream_t s);
+void bp_crop_cols(cbn_projector_s* p, float2* cols, int y_lo, int y_hi, float* vol_part,
+                  cudaStream_t s);
 void bp_sizes(cbn_projector_s* p, int64_t* lattice, int64_t* grid, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
 void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
@@ -1697,6 +1701,32 @@ int cbn_backproject_crop(cbn_projector* p, void* grid, float* vol, void* stream)
         CBN_REQUIRE(p && grid && vol, "null argument");
         CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
         bp_crop(p, static_cast<float2*>(grid), vol, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject_crop_slab(cbn_projector* p, void* slab, int32_t x_lo, int32_t x_hi,
+                              int32_t nparts, void* send, void* stream) {
+    try {
+        CBN_REQUIRE(p && slab && send, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        bp_crop_slab(p, static_cast<float2*>(slab), x_lo, x_hi, nparts, static_cast<float2*>(send),
+                     static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_backproject_crop_cols(cbn_projector* p, void* cols, int32_t y_lo, int32_t y_hi,
+                              float* vol_part, void* stream) {
+    try {
+        CBN_REQUIRE(p && cols && vol_part, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        bp_crop_cols(p, static_cast<float2*>(cols), y_lo, y_hi, vol_part,
+                     static_cast<cudaStream_t>(stream));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

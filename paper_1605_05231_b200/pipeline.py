@@ -182,12 +182,18 @@ class Projector:
                    "nufft_forward_project")
         return out
 
-    def forward_sharded(self, vol, view_lo: int, view_hi: int, group=None):
-        """nufft_forward_project over a process group: 1/world of the radial nodes
-        (lattice summed with one NCCL all-reduce), then this rank's views."""
+    def forward_sharded(self, vol, view_lo: int, view_hi: int, group=None,
+                        broadcast: bool = True):
+        """nufft_forward_project over a process group: the volume (a torch tensor
+        on the group's device) broadcast from the group's first rank unless
+        `broadcast` is False, 1/world of the radial nodes (lattice summed with
+        one NCCL all-reduce), then this rank's views."""
         import torch.distributed as dist
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if world > 1 and broadcast:
+            dist.broadcast(vol, dist.get_global_rank(group, 0) if group is not None else 0,
+                           group=group)
         lat = self.forward_lattice(vol, rank, world)
         if world > 1:
             dist.all_reduce(lat, group=group)
@@ -234,9 +240,34 @@ class Projector:
                                                     self._s), "nufft_backproject")
         return out
 
+    def backproject_crop_slab(self, slab, x_lo: int, x_hi: int, nparts: int):
+        """Phase 3a (slab-distributed): planes [x_lo, x_hi) of the summed grid
+        (consumed) -> y/z-cropped planes in the all-to-all send layout
+        [y block d][x][y - y0_d][z] (y0_d = d * N // nparts)."""
+        t = _device.require_cuda()
+        send = t.empty((x_hi - x_lo) * self.n * self.n, dtype=t.complex64, device="cuda")
+        _lib.check(_lib.load().cbn_backproject_crop_slab(self._h, _device.ptr(slab), int(x_lo),
+                                                         int(x_hi), int(nparts),
+                                                         _device.ptr(send), self._s),
+                   "nufft_backproject")
+        return send
+
+    def backproject_crop_cols(self, cols, y_lo: int, y_hi: int):
+        """Phase 3b: the received columns [2N][y_hi - y_lo][N] (consumed) -> the
+        volume's y range, float32 (N, y_hi - y_lo, N)."""
+        t = _device.require_cuda()
+        out = t.empty((self.n, y_hi - y_lo, self.n), dtype=t.float32, device="cuda")
+        _lib.check(_lib.load().cbn_backproject_crop_cols(self._h, _device.ptr(cols), int(y_lo),
+                                                         int(y_hi), _device.ptr(out), self._s),
+                   "nufft_backproject")
+        return out
+
     def backproject_sharded(self, frames_local, view_lo: int, view_hi: int, group=None):
-        """nufft_backproject over a process group: this rank's views and 1/world of
-        the radial nodes, with the two sums as NCCL all-reduces."""
+        """nufft_backproject over a process group: this rank's
+        views (accumulators summed with an all-reduce), 1/world of the radial
+        nodes spread into a local (2N)^3 grid, the grids reduce-scattered by
+        slabs of x planes, slab IFFT + y/z crop, an all-to-all transpose to
+        y ranges, x IFFT + crop, and an all-gather of the volume."""
         import torch.distributed as dist
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -244,9 +275,9 @@ class Projector:
         if world > 1:
             dist.all_reduce(lat, group=group)
         grid = self.backproject_finish(lat, rank, world)
-        if world > 1:
-            dist.all_reduce(grid, group=group)
-        return self.backproject_crop(grid)
+        if world == 1:
+            return self.backproject_crop(grid)
+        return sharded_crop(self, grid, rank, world, group)
 
     # ---- stages
     def radial_lattice(self, vol):
@@ -286,6 +317,46 @@ class Projector:
         _lib.check(_lib.load().cbn_projector_grangeat_forward(self._h, _device.ptr(f),
                                                               _device.ptr(out), nb, self._s))
         return out
+
+
+def slab_ranges(extent: int, world: int) -> list[int]:
+    """Balanced split points of `extent` planes over `world` ranks."""
+    return [extent * r // world for r in range(world + 1)]
+
+
+def sharded_crop(proj, grid, rank: int, world: int, group=None):
+    """Slab-distributed phase 3 of the backprojector (adjoint
+    steps 4-6) for a rank's un-summed (K, K, K) grid, K = 2N:
+    reduce-scatter by x slab (all-reduce + slice when world does not divide K),
+    2D IFFT + y/z crop of the slab, all-to-all to y ranges, x IFFT + crop, and
+    an all-gather of the y ranges into the full N^3 volume on every rank."""
+    import torch
+    import torch.distributed as dist
+    n = proj.n
+    k = round(grid.numel() ** (1.0 / 3.0))
+    if k ** 3 != grid.numel() or k < n:
+        raise ValueError("grid is not a (2N)^3 cube")
+    plane = k * k
+    xs, ys = slab_ranges(k, world), slab_ranges(n, world)
+    if k % world == 0:
+        slab = torch.empty(plane * (k // world), dtype=grid.dtype, device=grid.device)
+        dist.reduce_scatter_tensor(slab, grid, group=group)
+    else:
+        dist.all_reduce(grid, group=group)
+        slab = grid[xs[rank] * plane: xs[rank + 1] * plane]
+    send = proj.backproject_crop_slab(slab, xs[rank], xs[rank + 1], world)
+    xc, yc = xs[rank + 1] - xs[rank], ys[rank + 1] - ys[rank]
+    in_splits = [xc * (ys[d + 1] - ys[d]) * n for d in range(world)]
+    out_splits = [(xs[q + 1] - xs[q]) * yc * n for q in range(world)]
+    cols = torch.empty(sum(out_splits), dtype=send.dtype, device=send.device)
+    dist.all_to_all_single(cols, send, out_splits, in_splits, group=group)
+    part = proj.backproject_crop_cols(cols, ys[rank], ys[rank + 1])
+    cap = max(ys[d + 1] - ys[d] for d in range(world))
+    buf = torch.zeros((n, cap, n), dtype=part.dtype, device=part.device)
+    buf[:, :yc] = part
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([parts[d][:, : ys[d + 1] - ys[d]] for d in range(world)], dim=1)
 
 
 def get_projector(geom, cfg, n, voxel_mm, direction):

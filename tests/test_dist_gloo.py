@@ -83,17 +83,18 @@ def test_gloo_sharded_forward_matches_single(tmp_path):
 
 class _FakeProjector:
     """CPU stand-in for the device phases: fixed random linear maps with the same
-    sharding contract (node parts summed over ranks, view ranges local)."""
+    sharding contract (node parts summed over ranks, view ranges local) and the
+    same separable crop structure (grid (K, K, K) -> volume (n, n, n))."""
 
-    def __init__(self, views=6, n_vox=5, m=9):
+    def __init__(self, views=6, n_vox=5, m=9, n=3, k=6):
         import torch
         g = torch.Generator().manual_seed(0)
-        self.views = views
+        self.views, self.n, self.k = views, n, k
         self.A = torch.randn(m, n_vox, generator=g, dtype=torch.float64)       # vol -> lattice
         self.B = torch.randn(views, m, generator=g, dtype=torch.float64)       # lattice -> views
         self.C = torch.randn(m, views, generator=g, dtype=torch.float64)       # views -> lattice
-        self.D = torch.randn(7, m, generator=g, dtype=torch.float64)           # lattice -> grid
-        self.E = torch.randn(n_vox, 7, generator=g, dtype=torch.float64)       # grid -> volume
+        self.D = torch.randn(k ** 3, m, generator=g, dtype=torch.float64)      # lattice -> grid
+        self.F = [torch.randn(n, k, generator=g, dtype=torch.float64) for _ in range(3)]
 
     @staticmethod
     def _rows(n, part, nparts):
@@ -115,10 +116,23 @@ class _FakeProjector:
         return (self.D * self._rows(self.D.shape[1], part, nparts)[:, 0]) @ lat
 
     def backproject_crop(self, grid):
-        return self.E @ grid
+        import torch
+        fx, fy, fz = self.F
+        return torch.einsum("xa,yb,zc,abc->xyz", fx, fy, fz, grid.view(self.k, self.k, self.k))
+
+    def backproject_crop_slab(self, slab, x_lo, x_hi, nparts):
+        import torch
+        _, fy, fz = self.F
+        t = torch.einsum("yb,zc,abc->ayz", fy, fz, slab.reshape(x_hi - x_lo, self.k, self.k))
+        ys = [self.n * d // nparts for d in range(nparts + 1)]
+        return torch.cat([t[:, ys[d]:ys[d + 1]].reshape(-1) for d in range(nparts)])
+
+    def backproject_crop_cols(self, cols, y_lo, y_hi):
+        import torch
+        return torch.einsum("xa,ayz->xyz", self.F[0], cols.view(self.k, y_hi - y_lo, self.n))
 
 
-def _sharded_worker(rank, world, port, result_path):
+def _sharded_worker(rank, world, port, result_path, k=6):
     import sys
     import torch
     import torch.distributed as dist
@@ -128,8 +142,8 @@ def _sharded_worker(rank, world, port, result_path):
     from paper_1605_05231_b200.pipeline import Projector
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    fake = _FakeProjector()
-    vol = torch.arange(5, dtype=torch.float64) + 1.0
+    fake = _FakeProjector(k=k)
+    vol = torch.arange(5, dtype=torch.float64) + 1.0 if rank == 0 else torch.zeros(5, dtype=torch.float64)
     frames = torch.linspace(-1.0, 2.0, fake.views, dtype=torch.float64)
     lo, hi = sharding.view_shard(fake.views, world, rank)
     fwd_local = Projector.forward_sharded(fake, vol, lo, hi)
@@ -141,15 +155,21 @@ def _sharded_worker(rank, world, port, result_path):
     dist.destroy_process_group()
 
 
-def test_gloo_sharded_phase_orchestration(tmp_path):
-    """Projector.forward_sharded / backproject_sharded over a gloo world of 2: the
-    node-part sums (all-reduce) and view ranges give the single-process maps."""
+@pytest.mark.parametrize("world,k", [(2, 6), (3, 6), (2, 5)])
+def test_gloo_sharded_phase_orchestration(tmp_path, world, k):
+    """Projector.forward_sharded / backproject_sharded over a gloo world: the
+    volume broadcast, node-part sums (all-reduce), view ranges and the
+    slab-distributed crop (reduce-scatter by x slab -- all-reduce + slice when
+    the world does not divide the grid -- all-to-all to y ranges, all-gather)
+    give the single-process maps."""
     out = str(tmp_path / "res.npz")
-    mp.spawn(_sharded_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out, k), nprocs=world, join=True)
     res = np.load(out)
-    f = _FakeProjector()
+    f = _FakeProjector(k=k)
     import torch
     vol = torch.arange(5, dtype=torch.float64) + 1.0
     frames = torch.linspace(-1.0, 2.0, f.views, dtype=torch.float64)
     assert np.allclose(res["fwd"], (f.B @ (f.A @ vol)).numpy(), rtol=1e-12)
-    assert np.allclose(res["bp"], (f.E @ (f.D @ (f.C @ frames))).numpy(), rtol=1e-12)
+    ref = f.backproject_crop(f.D @ (f.C @ frames)).numpy()
+    assert res["bp"].shape == ref.shape
+    assert np.allclose(res["bp"], ref, rtol=1e-12, atol=1e-12)

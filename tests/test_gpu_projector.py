@@ -205,6 +205,43 @@ def test_backprojector_phases_shard_exactly(pl, name):
 
 
 @pytest.mark.parametrize("name", ["pipeline_n16", "pipeline_n12_v24"])
+def test_backprojector_slab_crop_exact(pl, name):
+    """Slab-distributed phase 3 (what backproject_sharded runs under NCCL): the
+    summed grid cut into x slabs (reduce-scatter, even and uneven splits), each
+    slab's 2D IFFT + y/z crop written in the all-to-all send layout, the chunks
+    routed to y ranges here, then x IFFT + crop per range -- equals the
+    one-device crop of the whole grid."""
+    import torch
+    g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    proj = pl.Projector(geom, cfg, n, voxel, 2)
+    frames = torch.from_numpy(g["frames"].astype(np.float32)).cuda()
+    grid = proj.backproject_finish(proj.backproject_views(frames, 0, views))
+    one = proj.backproject_crop(grid.clone()).cpu().numpy()
+    assert rel_l2(one, proj.backproject(frames).cpu().numpy()) < 1e-6
+    k = round(grid.numel() ** (1 / 3))
+    plane = k * k
+    for world in (1, 2, 3, 4):
+        xs, ys = pl.slab_ranges(k, world), pl.slab_ranges(n, world)
+        sends = [proj.backproject_crop_slab(grid[xs[r] * plane: xs[r + 1] * plane].clone(),
+                                            xs[r], xs[r + 1], world) for r in range(world)]
+        parts = []
+        for d in range(world):
+            yc = ys[d + 1] - ys[d]
+            chunks = []
+            for r in range(world):
+                xc = xs[r + 1] - xs[r]
+                off = xc * ys[d] * n
+                chunks.append(sends[r][off: off + xc * yc * n])
+            parts.append(proj.backproject_crop_cols(torch.cat(chunks), ys[d], ys[d + 1]))
+        got = torch.cat(parts, dim=1).cpu().numpy()
+        assert rel_l2(got, one) < 1e-6, world
+    with pytest.raises(ValueError):
+        proj.backproject_crop_slab(grid[:plane].clone(), 0, k + 1, 1)
+
+
+@pytest.mark.parametrize("name", ["pipeline_n16", "pipeline_n12_v24"])
 def test_forward_phases_shard_exactly(pl, name):
     """Forward phases split over 'ranks' (radial-node parts summed, then view
     ranges) reproduce the one-call forward projection -- what the NCCL
