@@ -58,7 +58,7 @@ CBN_D int pad_src(int g, int N, int K) {
 // h = frame * w1 ; y = h * scaling placed at rolled positions (nufft.py:226-230)
 __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int Ku, int Kv,
                           double pu, double pv, double so, const float* __restrict__ s32, int smax,
-                          int64_t total, float2* __restrict__ grids) {
+                          int64_t total, float* __restrict__ grids) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= total) return;
     const int64_t per = (int64_t)Ku * Kv;
@@ -66,11 +66,11 @@ __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int 
     const int rem = (int)(e % per);
     const int gu = rem / Kv, gv = rem % Kv;
     const int nu_i = pad_src(gu, nu, Ku), nv_i = pad_src(gv, nv, Kv);
-    float2 out = make_float2(0.f, 0.f);
+    float out = 0.f;
     if (nu_i >= 0 && nv_i >= 0) {
         double h = (double)frames[((size_t)v * nu + nu_i) * nv + nv_i] *
                    w1_val(nu_i, nv_i, nu, nv, pu, pv, so);
-        out.x = (float)h * s32[nu_i] * s32[smax + nv_i];
+        out = (float)h * s32[nu_i] * s32[smax + nv_i];
     }
     grids[e] = out;
 }
@@ -253,19 +253,23 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     const int Ku = gp.ax[0].K, Kv = gp.ax[1].K;
     const int nu = p->g.nu, nv = p->g.nv;
     const int64_t per_view = (int64_t)u.n_mu * u.n_t;
-    B.grid.ensure((size_t)nb * Ku * Kv);
+    // the padded frame is real: real-to-complex 2D FFT to the half spectrum
+    // [Ku][Kv/2+1]; the gather reads the other half as conjugate mirrors
+    const int64_t hk = (int64_t)Ku * (Kv / 2 + 1);
+    B.grid.ensure((size_t)nb * hk);
+    B.tv.ensure(((size_t)nb * Ku * Kv + 1) / 2);
     B.t.ensure((size_t)nb * per_view);
+    float* padded = reinterpret_cast<float*>(B.tv.p);
     const int64_t gtot = (int64_t)nb * Ku * Kv;
     k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames, nu, nv, Ku, Kv, gp.pu, gp.pv,
-                                                    p->g.so_mm, gp.s32.p, gp.smax, gtot,
-                                                    B.grid.p);
+                                                    p->g.so_mm, gp.s32.p, gp.smax, gtot, padded);
     CBN_LAUNCH_CHECK();
     long long kd[2] = {Ku, Kv};
-    B.fft.exec(B.fft.get(2, kd, nb), B.grid.p, B.grid.p, CUFFT_FORWARD, s);
+    B.fft.exec_r2c3(B.fft.get_r2c2(kd, nb), padded, B.grid.p, s);
     const BinPlan& bb = gp.bins;
     dim3 grid(bb.nsubs, (nb + kGrVG - 1) / kGrVG);
-    k_gr_gather_binned<kGrJ, kGrVG><<<grid, 256, sizeof(float2) * kGrVG * bb.nreg, s>>>(
-        B.grid.p, (size_t)Ku * Kv, bb.geom<2>(), reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p),
+    k_gr_gather_binned<kGrJ, kGrVG, true><<<grid, 256, sizeof(float2) * kGrVG * bb.nreg, s>>>(
+        B.grid.p, (size_t)hk, bb.geom<2>(), reinterpret_cast<const GrPoint<kGrJ>*>(gp.pts.p),
         bb.subs.p, B.t.p, (size_t)per_view, nb);
     CBN_LAUNCH_CHECK();
     long long nt[1] = {u.n_t};

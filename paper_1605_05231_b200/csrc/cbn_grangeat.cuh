@@ -318,10 +318,47 @@ __global__ void k_gr_csr_fill(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts
 // cells are stored as one contiguous 256-byte row
 constexpr int kGrRows = 8;    // value rows in flight per warp (16: 10.1 ms, 8: 8.3 ms per step at cfg 2)
 
-static __global__ void __launch_bounds__(256)
+// sum of one cell's CSR entries with lanes = views (rows of the view-fastest
+// node-scaled t-spectra `tl` = tfv + lane): 32 entry records per coalesced
+// load, handed out by shuffles, kGrRows value rows in flight
+CBN_D float2 gr_cell_sum(int64_t c, const int* __restrict__ col_ptr,
+                         const GrEntry* __restrict__ ent, const float2* __restrict__ tl, int lane) {
+    float2 acc = make_float2(0.f, 0.f);
+    const int e1 = col_ptr[c + 1];
+    for (int base = col_ptr[c]; base < e1; base += 32) {
+        const int n = min(32, e1 - base);
+        GrEntry mine{0, 0.f};
+        if (lane < n) mine = ent[base + lane];
+        for (int j0 = 0; j0 < n; j0 += kGrRows) {
+            float2 y[kGrRows];
+            float w[kGrRows];
+#pragma unroll
+            for (int j = 0; j < kGrRows; ++j) {
+                const int src = j0 + j;               // < 32; entries past n have w = 0
+                const int id = __shfl_sync(0xffffffffu, mine.id, src);
+                w[j] = __shfl_sync(0xffffffffu, mine.w, src);
+                y[j] = __ldg(tl + (size_t)id * 32);
+            }
+#pragma unroll
+            for (int j = 0; j < kGrRows; ++j) {
+                acc.x = fmaf(w[j], y[j].x, acc.x);
+                acc.y = fmaf(w[j], y[j].y, acc.y);
+            }
+        }
+    }
+    return acc;
+}
+
+// One warp per cell, lanes = views; 32 cells per block, written view-major
+// through a shared-memory transpose.  HERM: cell c of the half plane
+// [Ku][Kv/2+1] holds the Hermitian part (G[k] + conj(G[-k])) / 2 of the full
+// grid G, whose complex-to-real inverse FFT is Re(IFFT(G)) -- the only part
+// the reverse Grangeat keeps (grangeat.py:166).  No atomics, no memset.
+template <bool HERM>
+__global__ void __launch_bounds__(256)
 k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
                   const int* __restrict__ col_ptr, const GrEntry* __restrict__ ent,
-                  const float2* __restrict__ tfv, int nviews) {
+                  const float2* __restrict__ tfv, int nviews, int Ku, int Kv) {
     __shared__ float2 tile[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c0 = (int64_t)blockIdx.x * 32;
@@ -332,29 +369,15 @@ k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
         const int64_t c = c0 + cl;
         float2 acc = make_float2(0.f, 0.f);
         if (c < ncell) {
-            const int e1 = col_ptr[c + 1];
-            // 32 entry records per coalesced load (one per lane), handed out by
-            // shuffles; kGrRows value rows in flight
-            for (int base = col_ptr[c]; base < e1; base += 32) {
-                const int n = min(32, e1 - base);
-                GrEntry mine{0, 0.f};
-                if (lane < n) mine = ent[base + lane];
-                for (int j0 = 0; j0 < n; j0 += kGrRows) {
-                    float2 y[kGrRows];
-                    float w[kGrRows];
-#pragma unroll
-                    for (int j = 0; j < kGrRows; ++j) {
-                        const int src = j0 + j;               // < 32; entries past n have w = 0
-                        const int id = __shfl_sync(0xffffffffu, mine.id, src);
-                        w[j] = __shfl_sync(0xffffffffu, mine.w, src);
-                        y[j] = __ldg(tl + (size_t)id * 32);
-                    }
-#pragma unroll
-                    for (int j = 0; j < kGrRows; ++j) {
-                        acc.x = fmaf(w[j], y[j].x, acc.x);
-                        acc.y = fmaf(w[j], y[j].y, acc.y);
-                    }
-                }
+            if constexpr (HERM) {
+                const int hv = Kv / 2 + 1;
+                const int u = (int)(c / hv), v = (int)(c - (int64_t)u * hv);
+                const float2 a = gr_cell_sum((int64_t)u * Kv + v, col_ptr, ent, tl, lane);
+                const int um = u ? Ku - u : 0, vm = v ? Kv - v : 0;
+                const float2 b = gr_cell_sum((int64_t)um * Kv + vm, col_ptr, ent, tl, lane);
+                acc = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+            } else {
+                acc = gr_cell_sum(c, col_ptr, ent, tl, lane);
             }
         }
         tile[cl][lane] = acc;
@@ -372,8 +395,11 @@ __global__ void k_views_nodes(const float2* __restrict__ in, int nb, int64_t nsp
                               const GrNode* __restrict__ tab, int64_t n,
                               float2* __restrict__ out);
 
-// forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv)
-template <int J, int VG>
+// forward: out[v][col] = fac * sum_taps w * grid_v   for views [v0, v0 + nv).
+// HALF: the grids are the [K0][K1/2+1] half spectra of real inputs (R2C);
+// cells with k1 > K1/2 are read as conj(G[-k]) (copied from the mirror
+// asynchronously, conjugated in place after the wait).
+template <int J, int VG, bool HALF = false>
 __global__ void __launch_bounds__(256)
 k_gr_gather_binned(const float2* __restrict__ grids, size_t grid_stride, TileGeom<2> tg,
                    const GrPoint<J>* __restrict__ pts, const SubProblem* __restrict__ subs,
@@ -387,15 +413,29 @@ k_gr_gather_binned(const float2* __restrict__ grids, size_t grid_stride, TileGeo
     const int R1 = tg.R[1];
     const int nreg = tg.R[0] * R1;
     const FastDiv dreg(nreg), dR1(R1);
+    const int K0 = tg.K[0], K1 = tg.K[1];
+    const int ld = HALF ? K1 / 2 + 1 : K1;
     for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
         const int v = dreg.div(e), c = e - v * nreg;
         const int r0 = dR1.div(c), r1 = c - r0 * R1;
-        const size_t gi = (size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] + wrapc(o[1] + r1, tg.K[1]);
+        int g0 = wrapc(o[0] + r0, K0), g1 = wrapc(o[1] + r1, K1);
+        if (HALF && g1 > K1 / 2) {
+            g0 = g0 ? K0 - g0 : 0;
+            g1 = K1 - g1;
+        }
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
                          (unsigned)__cvta_generic_to_shared(tile + e)),
-                     "l"(grids + (size_t)(v0 + v) * grid_stride + gi));
+                     "l"(grids + (size_t)(v0 + v) * grid_stride + (size_t)g0 * ld + g1));
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if constexpr (HALF) {
+        // conjugate the mirrored cells: those whose wrapped k1 exceeds K1/2
+        for (int e = threadIdx.x; e < nv * nreg; e += blockDim.x) {
+            const int c = e - dreg.div(e) * nreg;
+            const int r1 = c - dR1.div(c) * R1;
+            if (wrapc(o[1] + r1, K1) > K1 / 2) tile[e].y = -tile[e].y;
+        }
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < sp.count; k += blockDim.x) {
         const GrPoint<J> g = pts[sp.start + k];

@@ -477,17 +477,24 @@ struct GrPost {
     const float* s32;   // 2 x smax
 };
 
-CBN_D float gr_value(const float2* grid, const GrPost& p, int u, int v) {
+CBN_D float gr_re(const float2* g, size_t i) { return g[i].x; }
+CBN_D float gr_re(const float* g, size_t i) { return g[i]; }
+
+// detector pixel (u, v) of one view's inverse-transformed grid (complex: Re;
+// real: the complex-to-real output), [Ku][Kv]
+template <class T>
+CBN_D float gr_value(const T* grid, const GrPost& p, int u, int v) {
     int gu = (u - p.nu / 2 + p.Ku) % p.Ku;
     int gv = (v - p.nv / 2 + p.Kv) % p.Kv;
-    float re = grid[(size_t)gu * p.Kv + gv].x * p.s32[u] * p.s32[p.smax + v];
+    float re = gr_re(grid, (size_t)gu * p.Kv + gv) * p.s32[u] * p.s32[p.smax + v];
     return (float)((double)re / w1_at(u, v, p.nu, p.nv, p.pu, p.pv, p.so));
 }
 
 // mean of the outermost detector ring per view (grangeat.py:167-169)
-__global__ void k_gr_ring(const float2* __restrict__ grids, GrPost p, double* __restrict__ mean) {
+template <class T>
+__global__ void k_gr_ring(const T* __restrict__ grids, GrPost p, double* __restrict__ mean) {
     const int v = blockIdx.x;
-    const float2* grid = grids + (size_t)v * p.Ku * p.Kv;
+    const T* grid = grids + (size_t)v * p.Ku * p.Kv;
     const int nring = p.nu == 1 || p.nv == 1 ? p.nu * p.nv : 2 * p.nu + 2 * p.nv - 4;
     double acc = 0.0;
     for (int r = threadIdx.x; r < nring; r += blockDim.x) {
@@ -519,7 +526,8 @@ __global__ void k_gr_ring(const float2* __restrict__ grids, GrPost p, double* __
     }
 }
 
-__global__ void k_gr_frame(const float2* __restrict__ grids, GrPost p,
+template <class T>
+__global__ void k_gr_frame(const T* __restrict__ grids, GrPost p,
                            const double* __restrict__ mean, float norm, float* __restrict__ frames,
                            int64_t total, int* __restrict__ flag) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1269,13 +1277,16 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         }
         StageScope st(p->timer, "grangeat_spread", s);
         const int64_t nspec = (int64_t)u.n_mu * nh;
-        B.tv.ensure((size_t)gp.n_rows * 32);
+        B.tv.ensure(std::max((size_t)gp.n_rows * 32, ((size_t)nb * Ku * Kv + 1) / 2));
         k_views_nodes<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
             B.t.p, nb, nspec, gp.node_tab.p, gp.n_rows, B.tv.p);
         CBN_LAUNCH_CHECK();
-        k_gr_gather_cells<<<(unsigned)((ncell + 31) / 32), 256, 0, s>>>(
-            B.grid.p, (size_t)ncell, ncell, gp.cell_ptr.p,
-            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb);
+        // Hermitian half plane [Ku][Kv/2+1] of the grid (only Re of its
+        // inverse FFT is used), then a complex-to-real 2D FFT into tv
+        const int64_t nhalf = (int64_t)Ku * (Kv / 2 + 1);
+        k_gr_gather_cells<true><<<(unsigned)((nhalf + 31) / 32), 256, 0, s>>>(
+            B.grid.p, (size_t)nhalf, nhalf, gp.cell_ptr.p,
+            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb, Ku, Kv);
         CBN_LAUNCH_CHECK();
     } else {
         StageScope st(p->timer, "grangeat_spread", s);
@@ -1291,17 +1302,25 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     }
     long long kd[2] = {Ku, Kv};
     StageScope st(p->timer, "grangeat_ifft_post", s);
-    B.fft.exec(B.fft.get(2, kd, nb), B.grid.p, B.grid.p, CUFFT_INVERSE, s);
     GrPost q = gr_post(p, gp);
     B.red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
     double* mean = B.red.p + 2 * kRedBlocks + 64;
-    k_gr_ring<<<nb, 256, 0, s>>>(B.grid.p, q, mean);
-    CBN_LAUNCH_CHECK();
     const int64_t total = (int64_t)nb * p->g.nu * p->g.nv;
-    k_gr_frame<<<blocks_for(total, 256), 256, 0, s>>>(B.grid.p, q, mean,
-                                                      (float)p->c.normalization, frames, total,
-                                                      p->flag.p);
-    CBN_LAUNCH_CHECK();
+    auto post = [&](const auto* g) {
+        k_gr_ring<<<nb, 256, 0, s>>>(g, q, mean);
+        CBN_LAUNCH_CHECK();
+        k_gr_frame<<<blocks_for(total, 256), 256, 0, s>>>(g, q, mean, (float)p->c.normalization,
+                                                          frames, total, p->flag.p);
+        CBN_LAUNCH_CHECK();
+    };
+    if (cell_gather) {
+        float* re = reinterpret_cast<float*>(B.tv.p);
+        B.fft.exec_c2r(B.fft.get_c2r2(kd, nb), B.grid.p, re, s);
+        post(static_cast<const float*>(re));
+    } else {
+        B.fft.exec(B.fft.get(2, kd, nb), B.grid.p, B.grid.p, CUFFT_INVERSE, s);
+        post(static_cast<const float2*>(B.grid.p));
+    }
 }
 
 void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s) {

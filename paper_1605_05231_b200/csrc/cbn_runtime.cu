@@ -38,7 +38,7 @@ cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long st
         embed = emb;
     }
     cufftResult r;
-    if (type == CUFFT_R2C && rank == 3) {
+    if (type == CUFFT_R2C && rank >= 2) {
         r = cufftMakePlanMany64(h, rank, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_R2C, batch, &ws);
     } else if (type == CUFFT_C2R) {
         r = cufftMakePlanMany64(h, rank, n, nullptr, 1, 0, nullptr, 1, 0, CUFFT_C2R, batch, &ws);
@@ -104,6 +104,26 @@ cufftHandle FFTCache::get_c2r3(const long long* n) {
     if (it != plans_.end()) return it->second;
     long long dims[3] = {n[0], n[1], n[2]};
     cufftHandle h = make(3, dims, 1, 1, 0, CUFFT_C2R);
+    plans_[key] = h;
+    return h;
+}
+
+cufftHandle FFTCache::get_c2r2(const long long* n, long long batch) {
+    Key key{-5, n[0], n[1], 0, batch, 1, 0};
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return it->second;
+    long long dims[2] = {n[0], n[1]};
+    cufftHandle h = make(2, dims, batch, 1, 0, CUFFT_C2R);
+    plans_[key] = h;
+    return h;
+}
+
+cufftHandle FFTCache::get_r2c2(const long long* n, long long batch) {
+    Key key{-6, n[0], n[1], 0, batch, 1, 0};
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return it->second;
+    long long dims[2] = {n[0], n[1]};
+    cufftHandle h = make(2, dims, batch, 1, 0, CUFFT_R2C);
     plans_[key] = h;
     return h;
 }

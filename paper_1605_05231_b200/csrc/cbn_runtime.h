@@ -104,6 +104,12 @@ public:
     // complex-to-real 3D transform of a [n0][n1][n2/2+1] half spectrum to
     // [n0][n1][n2] real (out of place)
     cufftHandle get_c2r3(const long long* n);
+    // complex-to-real 2D transforms of `batch` [n0][n1/2+1] half spectra to
+    // [n0][n1] real (out of place, contiguous batches)
+    cufftHandle get_c2r2(const long long* n, long long batch);
+    // real-to-complex 2D transforms of `batch` [n0][n1] reals to [n0][n1/2+1]
+    // (out of place, contiguous batches; run with exec_r2c3)
+    cufftHandle get_r2c2(const long long* n, long long batch);
     // real-to-complex 3D transform [n0][n1][n2] -> [n0][n1][n2/2+1] (out of place)
     cufftHandle get_r2c3(const long long* n);
     void exec_r2c3(cufftHandle h, const float* in, void* out, cudaStream_t s);
