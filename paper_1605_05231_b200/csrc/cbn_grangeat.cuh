@@ -318,26 +318,26 @@ __global__ void k_gr_csr_fill(TileGeom<2> tg, const GrPoint<J>* __restrict__ pts
 // cells are stored as one contiguous 256-byte row
 constexpr int kGrRows = 8;    // value rows in flight per warp (16: 10.1 ms, 8: 8.3 ms per step at cfg 2)
 
-// sum of one cell's CSR entries with lanes = views (rows of the view-fastest
+// sum of CSR entries [e0, e1) with lanes = views (rows of the view-fastest
 // node-scaled t-spectra `tl` = tfv + lane): 32 entry records per coalesced
-// load, handed out by shuffles, kGrRows value rows in flight
-CBN_D float2 gr_cell_sum(int64_t c, const int* __restrict__ col_ptr,
-                         const GrEntry* __restrict__ ent, const float2* __restrict__ tl, int lane) {
+// load, staged in the warp's shared slots `sb` and read back as broadcasts
+// (one LDS per entry instead of two shuffles), kGrRows value rows in flight
+CBN_D float2 gr_range_sum(int e0, int e1, const GrEntry* __restrict__ ent,
+                          const float2* __restrict__ tl, int lane, GrEntry* sb) {
     float2 acc = make_float2(0.f, 0.f);
-    const int e1 = col_ptr[c + 1];
-    for (int base = col_ptr[c]; base < e1; base += 32) {
+    for (int base = e0; base < e1; base += 32) {
         const int n = min(32, e1 - base);
-        GrEntry mine{0, 0.f};
-        if (lane < n) mine = ent[base + lane];
+        __syncwarp();
+        sb[lane] = lane < n ? ent[base + lane] : GrEntry{0, 0.f};
+        __syncwarp();
         for (int j0 = 0; j0 < n; j0 += kGrRows) {
             float2 y[kGrRows];
             float w[kGrRows];
 #pragma unroll
             for (int j = 0; j < kGrRows; ++j) {
-                const int src = j0 + j;               // < 32; entries past n have w = 0
-                const int id = __shfl_sync(0xffffffffu, mine.id, src);
-                w[j] = __shfl_sync(0xffffffffu, mine.w, src);
-                y[j] = __ldg(tl + (size_t)id * 32);
+                const GrEntry e = sb[j0 + j];         // < 32; entries past n have w = 0
+                w[j] = e.w;
+                y[j] = __ldg(tl + (size_t)e.id * 32);
             }
 #pragma unroll
             for (int j = 0; j < kGrRows; ++j) {
@@ -349,43 +349,78 @@ CBN_D float2 gr_cell_sum(int64_t c, const int* __restrict__ col_ptr,
     return acc;
 }
 
-// One warp per cell, lanes = views; 32 cells per block, written view-major
-// through a shared-memory transpose.  HERM: cell c of the half plane
-// [Ku][Kv/2+1] holds the Hermitian part (G[k] + conj(G[-k])) / 2 of the full
-// grid G, whose complex-to-real inverse FFT is Re(IFFT(G)) -- the only part
-// the reverse Grangeat keeps (grangeat.py:166).  No atomics, no memset.
-template <bool HERM>
-__global__ void __launch_bounds__(256)
+// full-plane cell pair (k, -k) of half-plane cell c of [Ku][Kv/2+1]
+CBN_D void gr_half_cells(int64_t c, int Ku, int Kv, int64_t& k, int64_t& km) {
+    const int hv = Kv / 2 + 1;
+    const int u = (int)(c / hv), v = (int)(c - (int64_t)u * hv);
+    k = (int64_t)u * Kv + v;
+    km = (int64_t)(u ? Ku - u : 0) * Kv + (v ? Kv - v : 0);
+}
+
+// Cell gather onto the Hermitian half plane [Ku][Kv/2+1]: half-plane cell c
+// holds (G[k] + conj(G[-k])) / 2 of the full grid G, whose complex-to-real
+// inverse FFT is Re(IFFT(G)) -- the only part the reverse Grangeat keeps
+// (grangeat.py:166).  Lanes = views; no atomics, no memset.  Work items come
+// costliest first (plan-time order; node density peaks at the origin):
+//   item >= 0: 32 consecutive cells, 8 warps x 4 cells, results stored
+//              view-major through a shared-memory transpose (heavy cells
+//              skipped);
+//   item <  0: one heavy cell -(item + 1), its two entry lists split over the
+//              8 warps and reduced in shared memory.
+static __global__ void __launch_bounds__(256)
 k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
                   const int* __restrict__ col_ptr, const GrEntry* __restrict__ ent,
-                  const float2* __restrict__ tfv, int nviews, int Ku, int Kv) {
+                  const float2* __restrict__ tfv, int nviews, int Ku, int Kv,
+                  const int* __restrict__ order, const unsigned char* __restrict__ heavy) {
     __shared__ float2 tile[32][33];
+    __shared__ GrEntry slots[8][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t c0 = (int64_t)blockIdx.x * 32;
     const float2* tl = tfv + lane;
+    GrEntry* sb = slots[warp];
+    const int item = order[blockIdx.x];
+    if (item < 0) {
+        const int64_t c = -(int64_t)item - 1;
+        int64_t k, km;
+        gr_half_cells(c, Ku, Kv, k, km);
+        const int a0 = col_ptr[k], a1 = col_ptr[k + 1], b0 = col_ptr[km], b1 = col_ptr[km + 1];
+        const int la = a1 - a0, lb = b1 - b0;
+        const float2 a = gr_range_sum(a0 + (int)((int64_t)la * warp / 8),
+                                      a0 + (int)((int64_t)la * (warp + 1) / 8), ent, tl, lane, sb);
+        const float2 b = gr_range_sum(b0 + (int)((int64_t)lb * warp / 8),
+                                      b0 + (int)((int64_t)lb * (warp + 1) / 8), ent, tl, lane, sb);
+        tile[warp][lane] = make_float2(a.x + b.x, a.y - b.y);
+        __syncthreads();
+        if (warp == 0) {
+            float2 t = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                t.x += tile[w][lane].x;
+                t.y += tile[w][lane].y;
+            }
+            if (lane < nviews) grids[(size_t)lane * grid_stride + c] = make_float2(0.5f * t.x, 0.5f * t.y);
+        }
+        return;
+    }
+    const int64_t c0 = (int64_t)item * 32;
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
         const int cl = warp + 8 * q;
         const int64_t c = c0 + cl;
         float2 acc = make_float2(0.f, 0.f);
-        if (c < ncell) {
-            if constexpr (HERM) {
-                const int hv = Kv / 2 + 1;
-                const int u = (int)(c / hv), v = (int)(c - (int64_t)u * hv);
-                const float2 a = gr_cell_sum((int64_t)u * Kv + v, col_ptr, ent, tl, lane);
-                const int um = u ? Ku - u : 0, vm = v ? Kv - v : 0;
-                const float2 b = gr_cell_sum((int64_t)um * Kv + vm, col_ptr, ent, tl, lane);
-                acc = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
-            } else {
-                acc = gr_cell_sum(c, col_ptr, ent, tl, lane);
-            }
+        if (c < ncell && !heavy[c]) {
+            int64_t k, km;
+            gr_half_cells(c, Ku, Kv, k, km);
+            const float2 a = gr_range_sum(col_ptr[k], col_ptr[k + 1], ent, tl, lane, sb);
+            const float2 b = gr_range_sum(col_ptr[km], col_ptr[km + 1], ent, tl, lane, sb);
+            acc = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
         }
         tile[cl][lane] = acc;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
         const int v = e >> 5, cl = e & 31;
-        if (v < nviews && c0 + cl < ncell) grids[(size_t)v * grid_stride + c0 + cl] = tile[cl][v];
+        const int64_t c = c0 + cl;
+        if (v < nviews && c < ncell && !heavy[c]) grids[(size_t)v * grid_stride + c] = tile[cl][v];
     }
 }
 

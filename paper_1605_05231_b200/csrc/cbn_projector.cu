@@ -1212,6 +1212,46 @@ GrPost gr_post(const P* p, const GrangeatPlan& gp) {
     return q;
 }
 
+// Work items of k_gr_gather_cells from the host copy of the cell CSR offsets
+// h (full plane, Ku*Kv + 1): half-plane cells whose two entry lists exceed
+// kGrHeavy entries get a CTA of their own (8 warps split the lists); the rest
+// go in blocks of 32 cells.  Items are ordered by descending cost so the
+// dense cells near the origin (polar nodes crowd there) start first instead
+// of forming the tail.
+constexpr int64_t kGrHeavy = 1024;
+
+void gr_cell_schedule(GrangeatPlan& gp, const std::vector<int>& h, int Ku, int Kv,
+                      cudaStream_t s) {
+    const int hv = Kv / 2 + 1;
+    const int64_t nhalf = (int64_t)Ku * hv;
+    std::vector<unsigned char> heavy((size_t)nhalf, 0);
+    std::vector<std::pair<int64_t, int>> items;   // (cost, item)
+    const int64_t nblk = (nhalf + 31) / 32;
+    std::vector<int64_t> bcost((size_t)nblk, 0);
+    for (int64_t c = 0; c < nhalf; ++c) {
+        const int u = (int)(c / hv), v = (int)(c % hv);
+        const int64_t k = (int64_t)u * Kv + v;
+        const int64_t km = (int64_t)(u ? Ku - u : 0) * Kv + (v ? Kv - v : 0);
+        const int64_t cost = (int64_t)(h[k + 1] - h[k]) + (h[km + 1] - h[km]);
+        if (cost > kGrHeavy) {
+            heavy[(size_t)c] = 1;
+            items.emplace_back((cost + 7) / 8, (int)(-c - 1));
+        } else {
+            bcost[(size_t)(c / 32)] += cost;
+        }
+    }
+    // a block's 8 warps take 4 cells each: its time is about cost / 8
+    for (int64_t b = 0; b < nblk; ++b) items.emplace_back((bcost[(size_t)b] + 7) / 8, (int)b);
+    std::stable_sort(items.begin(), items.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<int> order(items.size());
+    for (size_t i = 0; i < items.size(); ++i) order[i] = items[i].second;
+    gp.n_items = (int)order.size();
+    gp.cell_order.upload(order.data(), order.size(), s);
+    gp.cell_heavy.upload(heavy.data(), heavy.size(), s);
+    CBN_CUDA(cudaStreamSynchronize(s));
+}
+
 // reverse_grangeat_view for nb views: vals (nb x n_mu x n_t) -> frames (nb x nu x nv)
 void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s,
                       GrBufs B) {
@@ -1273,6 +1313,7 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
                                                          mult.p, counts.p,
                                                          reinterpret_cast<GrEntry*>(gp.cell_ent.p));
             CBN_LAUNCH_CHECK();
+            gr_cell_schedule(gp, h, Ku, Kv, s);
             CBN_CUDA(cudaStreamSynchronize(s));
         }
         StageScope st(p->timer, "grangeat_spread", s);
@@ -1284,9 +1325,10 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         // Hermitian half plane [Ku][Kv/2+1] of the grid (only Re of its
         // inverse FFT is used), then a complex-to-real 2D FFT into tv
         const int64_t nhalf = (int64_t)Ku * (Kv / 2 + 1);
-        k_gr_gather_cells<true><<<(unsigned)((nhalf + 31) / 32), 256, 0, s>>>(
+        k_gr_gather_cells<<<(unsigned)gp.n_items, 256, 0, s>>>(
             B.grid.p, (size_t)nhalf, nhalf, gp.cell_ptr.p,
-            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb, Ku, Kv);
+            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb, Ku, Kv,
+            gp.cell_order.p, gp.cell_heavy.p);
         CBN_LAUNCH_CHECK();
     } else {
         StageScope st(p->timer, "grangeat_spread", s);

@@ -55,6 +55,10 @@ struct GrangeatPlan {
     bool pts_ready = false;
     DevBuf<int> cell_ptr;               // reverse: CSR of (node, weight) entries per grid cell
     DevBuf<char> cell_ent;              // GrEntry per (node, tap)
+    DevBuf<int> cell_order;             // work items of the half-plane cell gather, costliest
+                                        // first: >= 0 block of 32 cells, < 0 one heavy cell
+    DevBuf<unsigned char> cell_heavy;   // 1: half-plane cell handled by its own CTA
+    int n_items = 0;
     DevBuf<GrNode> node_tab;            // reverse: node-scaled t-spectrum rows
     int64_t n_rows = 0;                 // rows of node_tab (nspec + second nodes)
 };
