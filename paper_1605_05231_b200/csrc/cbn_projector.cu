@@ -433,6 +433,54 @@ __global__ void k_pad_lattice(const float2* __restrict__ src, int shift, float s
 }
 
 // ---- reverse Grangeat (grangeat.py:149-170)
+// k_views_nodes fused with the real-to-complex split: `z` holds the length-M
+// complex FFTs (M = n_t / 2) of the real t lines read as complex pairs
+// (z[n] = x[2n] + i x[2n+1]), [view][mu][M]; bin k of the real FFT is
+// E[k] + W^k O[k], W = exp(-2 pi i / n_t), with E / O the even / odd-sample
+// spectra (Z[k] +- conj Z[-k]) / (2, 2i).  Rows as k_views_nodes.
+__global__ void k_views_nodes_z(const float2* __restrict__ z, int nb, int n_mu, int M,
+                                const GrNode* __restrict__ tab, int64_t n,
+                                float2* __restrict__ out) {
+    __shared__ float2 tile[32][33];
+    __shared__ GrNode nd[32];
+    __shared__ int zk[32], zm[32];
+    __shared__ float2 tw[32];
+    const int64_t e0 = (int64_t)blockIdx.x * 32;
+    const int nh = M + 1;
+    if (threadIdx.x < 32 && e0 + threadIdx.x < n) {
+        const GrNode g = tab[e0 + threadIdx.x];
+        nd[threadIdx.x] = g;
+        const int mu = g.src / nh, k = g.src - mu * nh;
+        zk[threadIdx.x] = mu * M + (k == M ? 0 : k);
+        zm[threadIdx.x] = mu * M + (k == 0 ? 0 : M - k);
+        float sn, cs;
+        sincospif((float)k / (float)M, &sn, &cs);     // 2 pi k / n_t
+        tw[threadIdx.x] = make_float2(cs, -sn);
+    }
+    __syncthreads();
+    const int64_t per = (int64_t)n_mu * M;
+    for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
+        const int v = q >> 5, e = q & 31;
+        if (v < nb && e0 + e < n) {
+            const GrNode g = nd[e];
+            const float2 a = z[(size_t)v * per + zk[e]];
+            const float2 b = z[(size_t)v * per + zm[e]];   // conj taken below
+            // E = (a + conj b) / 2, O = (a - conj b) / (2i)
+            const float2 E = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+            const float2 O = make_float2(0.5f * (a.y + b.y), -0.5f * (a.x - b.x));
+            const float2 w = tw[e];
+            float2 x = make_float2(E.x + w.x * O.x - w.y * O.y, E.y + w.x * O.y + w.y * O.x);
+            if (g.conj) x.y = -x.y;
+            tile[v][e] = make_float2(g.fac.x * x.x - g.fac.y * x.y, g.fac.x * x.y + g.fac.y * x.x);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
+        const int e = q >> 5, v = q & 31;
+        if (v < nb && e0 + e < n) out[(size_t)(e0 + e) * 32 + v] = tile[v][e];
+    }
+}
+
 __global__ void k_views_nodes(const float2* __restrict__ in, int nb, int64_t nspec,
                               const GrNode* __restrict__ tab, int64_t n,
                               float2* __restrict__ out) {
@@ -1252,6 +1300,11 @@ void gr_cell_schedule(GrangeatPlan& gp, const std::vector<int>& h, int Ku, int K
     CBN_CUDA(cudaStreamSynchronize(s));
 }
 
+bool cell_gather_on() {
+    const char* spread_env = std::getenv("CBN_GR_SPREAD");
+    return !(spread_env && spread_env[0] == '1');
+}
+
 // reverse_grangeat_view for nb views: vals (nb x n_mu x n_t) -> frames (nb x nu x nv)
 void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream_t s,
                       GrBufs B) {
@@ -1268,9 +1321,17 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     (void)tl;
     // vals arrive already divided by w2 (folded into the resample store), so
     // the t lines go straight through a real-to-complex FFT
-    B.fft.exec_r2c(B.fft.get_r2c(u.n_t, (long long)nb * u.n_mu), vals, B.t.p, s);
-    const char* spread_env = std::getenv("CBN_GR_SPREAD");
-    const bool cell_gather = !(spread_env && spread_env[0] == '1');
+    // even n_t: complex FFTs of half length on the lines read as complex pairs;
+    // the real-to-complex split is fused into the node-row transpose below
+    const bool zsplit = u.n_t % 2 == 0 && cell_gather_on();
+    if (zsplit) {
+        long long m1[1] = {u.n_t / 2};
+        B.fft.exec(B.fft.get(1, m1, (long long)nb * u.n_mu), const_cast<float*>(vals), B.t.p,
+                   CUFFT_FORWARD, s);
+    } else {
+        B.fft.exec_r2c(B.fft.get_r2c(u.n_t, (long long)nb * u.n_mu), vals, B.t.p, s);
+    }
+    const bool cell_gather = cell_gather_on();
     if (!cell_gather) CBN_CUDA(cudaMemsetAsync(B.grid.p, 0, sizeof(float2) * nb * Ku * Kv, s));
     if (p->timer.on) p->timer.end(s);
     if (cell_gather) {
@@ -1319,8 +1380,12 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         StageScope st(p->timer, "grangeat_spread", s);
         const int64_t nspec = (int64_t)u.n_mu * nh;
         B.tv.ensure(std::max((size_t)gp.n_rows * 32, ((size_t)nb * Ku * Kv + 1) / 2));
-        k_views_nodes<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
-            B.t.p, nb, nspec, gp.node_tab.p, gp.n_rows, B.tv.p);
+        if (zsplit)
+            k_views_nodes_z<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
+                B.t.p, nb, u.n_mu, u.n_t / 2, gp.node_tab.p, gp.n_rows, B.tv.p);
+        else
+            k_views_nodes<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
+                B.t.p, nb, nspec, gp.node_tab.p, gp.n_rows, B.tv.p);
         CBN_LAUNCH_CHECK();
         // Hermitian half plane [Ku][Kv/2+1] of the grid (only Re of its
         // inverse FFT is used), then a complex-to-real 2D FFT into tv
