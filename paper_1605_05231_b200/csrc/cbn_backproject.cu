@@ -420,6 +420,12 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
         }
     };
+    // views-in-lanes: the transposed grid is real, [rho][theta][phi] (phi =
+    // rax[0]), stored after its half spectrum [rho][theta][phi/2+1]
+    const int64_t hphi = rax[0].K / 2 + 1;
+    const int64_t half_sz = (int64_t)rax[2].K * rax[1].K * hphi;
+    if (x.lanes) p->big.ensure((size_t)(half_sz + (x.kres + 1) / 2));
+    float* greal = x.lanes ? reinterpret_cast<float*>(p->big.p + half_sz) : nullptr;
     float* gn = reinterpret_cast<float*>(p->big.p);    // the transposed grid (real parts)
     // one group of batches sharing a scaling: inverse FFT of the summed
     // spreads, crop * scaling, accumulate into acc
@@ -441,6 +447,27 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             for (int d = 0; d < x.slow_axis; ++d) o += rax[d].N;
             p->bres_planes = index_runs(p->tab_idx.p + o, rax[x.slow_axis].N, false, s);
             p->bres_planes_slow = x.slow_axis;
+        }
+        if (x.lanes) {
+            // real grid: 2D R2C over the (theta, phi) planes, C2C along rho,
+            // then the crop reads IFFT = conj(FFT) from the half spectrum
+            {
+                StageScope st(p->timer, "transpose_ifft", s);
+                const long long k2[2] = {rax[1].K, rax[0].K};
+                p->fft.exec_r2c3(p->fft.get_r2c2(k2, rax[2].K), greal, p->big.p, s);
+                const long long plane = (long long)rax[1].K * hphi;
+                p->fft.exec(p->fft.get_strided(rax[2].K, plane, plane, 1), p->big.p, p->big.p,
+                            CUFFT_FORWARD, s);
+            }
+            StageScope st(p->timer, "transpose_crop", s);
+            ax[0].sstride = 1;
+            ax[1].sstride = hphi;
+            ax[2].sstride = (int64_t)rax[1].K * hphi;
+            dim3 grid((ax[2].n + 255) / 256, ax[1].n, ax[0].n);
+            k_remap_half_acc<<<grid, 256, 0, s>>>(p->big.p, acc, ax[0], ax[1], ax[2], rax[0].K,
+                                                  rax[1].K, rax[2].K);
+            CBN_LAUNCH_CHECK();
+            return;
         }
         {
             StageScope st(p->timer, "transpose_ifft", s);
@@ -501,8 +528,8 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 }
                 const unsigned ncol = (unsigned)(x.kd3[0] * x.kd3[1]);
                 const RsColEntry* ent = reinterpret_cast<const RsColEntry*>(p->bcol_ent.p);
-                float2* gnum = den_only ? nullptr : p->big.p;
-                float2* gden = den_only ? p->big.p : nullptr;
+                float* gnum = den_only ? nullptr : greal;
+                float* gden = den_only ? greal : nullptr;
                 const float* vt = den_only ? nullptr : p->values_t.p;
                 if (x.shift == 2) {
                     k_rs_gather_cols2<<<ncol, kRsPairThreads, 0, s>>>(

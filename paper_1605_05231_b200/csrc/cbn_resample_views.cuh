@@ -96,6 +96,32 @@ __global__ void k_rs_col_fill(const RsTap<J>* __restrict__ taps, int64_t n, int 
         }
 }
 
+// acc[e] += gain * prod_d scale_d[e_d] * IFFT(g)[k], k_d = idx_d[e_d], from
+// F = the forward 3D FFT of the real grid g kept as the half spectrum along
+// axis 0 (phi; [rho][theta][phi/2+1], strides a_d.sstride): IFFT(g)[k] is
+// conj(F[k]) for k_0 <= K_0/2 and F[-k] otherwise.  Grid as k_remap<3>.
+static __global__ void k_remap_half_acc(const float2* __restrict__ F, float2* __restrict__ acc,
+                                        RemapAxis a0, RemapAxis a1, RemapAxis a2, int K0, int K1,
+                                        int K2) {
+    const int e2 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e2 >= a2.n) return;
+    const int e0 = blockIdx.z, e1 = blockIdx.y;
+    int k0 = a0.idx[e0], k1 = a1.idx[e1], k2 = a2.idx[e2];
+    if (k0 < 0 || k1 < 0 || k2 < 0) return;
+    const float sc = a0.scale[e0] * a1.scale[e1] * a2.scale[e2];
+    float sg = -1.f;
+    if (k0 > K0 / 2) {
+        k0 = K0 - k0;
+        k1 = k1 ? K1 - k1 : 0;
+        k2 = k2 ? K2 - k2 : 0;
+        sg = 1.f;
+    }
+    const float2 f = F[k0 * a0.sstride + k1 * a1.sstride + k2 * a2.sstride];
+    float2* d = acc + ((size_t)e0 * a1.n + e1) * a2.n + e2;
+    const float2 o = *d;
+    *d = make_float2(o.x + sc * f.x, o.y + sg * sc * f.y);
+}
+
 // vals [nv][n] -> valsT [n][nv]
 static __global__ void k_transpose_vals(const float* __restrict__ in, int nv, int64_t n,
                                  float* __restrict__ out) {
@@ -114,12 +140,12 @@ static __global__ void k_transpose_vals(const float* __restrict__ in, int nv, in
 }
 
 // One CTA per grid column (rho, theta); threads over phi.  Views [vlo, vlo+nv)
-// of valsT [target][nv]; writes (num, 0) if gnum -- and (den, 0) if gden -- to
-// every cell of the column (den-only passes: gnum and valsT null).
+// of valsT [target][nv]; writes num if gnum -- and den if gden -- to every
+// cell of the column of the real grid (den-only passes: gnum and valsT null).
 constexpr int kRsColThreads = 256;
 
 static __global__ void __launch_bounds__(kRsColThreads)
-k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
+k_rs_gather_cols(float* __restrict__ gnum, float* __restrict__ gden, int K2,
                  const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
                  const float* __restrict__ valsT, int vlo, int nv, int shift) {
     const size_t col = blockIdx.x;
@@ -143,8 +169,8 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
                 }
             }
         }
-        if (gnum) gnum[col * K2 + phi] = make_float2(num, 0.f);
-        if (gden) gden[col * K2 + phi] = make_float2(den, 0.f);
+        if (gnum) gnum[col * K2 + phi] = num;
+        if (gden) gden[col * K2 + phi] = den;
     }
 }
 
@@ -157,7 +183,7 @@ k_rs_gather_cols(float2* __restrict__ gnum, float2* __restrict__ gden, int K2,
 constexpr int kRsPairThreads = 384;
 
 static __global__ void __launch_bounds__(kRsPairThreads)
-k_rs_gather_cols2(float2* __restrict__ gnum, float2* __restrict__ gden, int V,
+k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
                   const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
                   const float* __restrict__ valsT, int vlo, int nv) {
     const size_t col = blockIdx.x;
@@ -192,10 +218,8 @@ k_rs_gather_cols2(float2* __restrict__ gnum, float2* __restrict__ gden, int V,
                 de = fmaf(w1, u1, de);
             }
         }
-        if (gnum)
-            *(reinterpret_cast<float4*>(gnum + col * 2 * V) + i) = make_float4(ne, 0.f, no, 0.f);
-        if (gden)
-            *(reinterpret_cast<float4*>(gden + col * 2 * V) + i) = make_float4(de, 0.f, dn, 0.f);
+        if (gnum) *(reinterpret_cast<float2*>(gnum + col * 2 * V) + i) = make_float2(ne, no);
+        if (gden) *(reinterpret_cast<float2*>(gden + col * 2 * V) + i) = make_float2(de, dn);
     }
 }
 
