@@ -303,15 +303,27 @@ k_resample_rows3(const float* __restrict__ G, int K2, const RsRow3* __restrict__
                 const float w0 = rr.w2[0], w1 = rr.w2[1], w2 = rr.w2[2];
                 float acc = 0.f;
                 if constexpr (ES == 1) {
-                    // 32-bit cell index (grid < 2^32 cells): one add and one wide
-                    // multiply-add per tap address
-                    const unsigned u0 = c0, u1 = c1, u2 = c2;
+                    // 32-bit cell index (grid < 2^32 cells).  The three phi taps
+                    // c0..c0+2 lie in two aligned cell pairs (K2 even, so pairs
+                    // never straddle the row end): two 8-byte loads per row
+                    // instead of three 4-byte ones, and with the view shift of
+                    // 2 cells the warp's pairs are one contiguous 256-byte span
+                    (void)c1;
+                    (void)c2;
+                    const unsigned p0 = (unsigned)c0 & ~1u;
+                    const unsigned p1 = p0 + 2 == (unsigned)K2 ? 0u : p0 + 2;
+                    const bool odd = c0 & 1;
 #pragma unroll
                     for (int ab = 0; ab < 9; ++ab) {
                         const unsigned b = rr.row[ab];
-                        float r = w0 * __ldg(G + (b + u0));
-                        r = fmaf(w1, __ldg(G + (b + u1)), r);
-                        r = fmaf(w2, __ldg(G + (b + u2)), r);
+                        const float2 q0 = __ldg(reinterpret_cast<const float2*>(G + (b + p0)));
+                        const float2 q1 = __ldg(reinterpret_cast<const float2*>(G + (b + p1)));
+                        const float t0 = odd ? q0.y : q0.x;
+                        const float t1 = odd ? q1.x : q0.y;
+                        const float t2 = odd ? q1.y : q1.x;
+                        float r = w0 * t0;
+                        r = fmaf(w1, t1, r);
+                        r = fmaf(w2, t2, r);
                         acc = fmaf(rr.wab[ab], r, acc);
                     }
                 } else {
