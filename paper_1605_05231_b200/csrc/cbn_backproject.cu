@@ -30,6 +30,7 @@ void projector_build_tables(cbn_projector_s* p, int mode, const AxisPlan* ax, in
                             cudaStream_t s, RemapAxis* out, const int64_t* sstride);
 void projector_fit_grangeat(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
                             cudaStream_t s);
+void projector_gr_pix(const cbn_projector_s* p, GrangeatPlan& gp, bool reverse, cudaStream_t s);
 void projector_column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
                            double* partial, double* out, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s);
@@ -42,12 +43,6 @@ namespace {
 
 constexpr int kRed = 296;
 
-CBN_D double w1_val(int u, int v, int nu, int nv, double pu, double pv, double so) {
-    double uc = (((double)u - (double)nu / 2.0) + 0.5) * pu;
-    double vc = (((double)v - (double)nv / 2.0) + 0.5) * pv;
-    return so / sqrt(so * so + uc * uc + vc * vc);
-}
-
 CBN_D int pad_src(int g, int N, int K) {
     const int h = N / 2;
     if (g < N - h) return g + h;
@@ -57,8 +52,7 @@ CBN_D int pad_src(int g, int N, int K) {
 
 // h = frame * w1 ; y = h * scaling placed at rolled positions (nufft.py:226-230)
 __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int Ku, int Kv,
-                          double pu, double pv, double so, const float* __restrict__ s32, int smax,
-                          int64_t total, float* __restrict__ grids) {
+                          const float* __restrict__ pix, int64_t total, float* __restrict__ grids) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= total) return;
     const int64_t per = (int64_t)Ku * Kv;
@@ -68,9 +62,8 @@ __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int 
     const int nu_i = pad_src(gu, nu, Ku), nv_i = pad_src(gv, nv, Kv);
     float out = 0.f;
     if (nu_i >= 0 && nv_i >= 0) {
-        double h = (double)frames[((size_t)v * nu + nu_i) * nv + nv_i] *
-                   w1_val(nu_i, nv_i, nu, nv, pu, pv, so);
-        out = (float)h * s32[nu_i] * s32[smax + nv_i];
+        const size_t px = (size_t)nu_i * nv + nv_i;
+        out = frames[(size_t)v * nu * nv + px] * pix[px];
     }
     grids[e] = out;
 }
@@ -261,8 +254,9 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     B.t.ensure((size_t)nb * per_view);
     float* padded = reinterpret_cast<float*>(B.tv.p);
     const int64_t gtot = (int64_t)nb * Ku * Kv;
-    k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames, nu, nv, Ku, Kv, gp.pu, gp.pv,
-                                                    p->g.so_mm, gp.s32.p, gp.smax, gtot, padded);
+    projector_gr_pix(p, gp, false, s);
+    k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames, nu, nv, Ku, Kv, gp.pix.p, gtot,
+                                                    padded);
     CBN_LAUNCH_CHECK();
     long long kd[2] = {Ku, Kv};
     B.fft.exec_r2c3(B.fft.get_r2c2(kd, nb), padded, B.grid.p, s);

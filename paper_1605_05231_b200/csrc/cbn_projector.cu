@@ -532,9 +532,8 @@ CBN_D double w1_at(int u, int v, int nu, int nv, double pu, double pv, double so
 }
 
 struct GrPost {
-    int nu, nv, Ku, Kv, smax;
-    double pu, pv, so;
-    const float* s32;   // 2 x smax
+    int nu, nv, Ku, Kv;
+    const float* pix;   // [nu][nv] s_u s_v / w1
 };
 
 CBN_D float gr_re(const float2* g, size_t i) { return g[i].x; }
@@ -546,8 +545,30 @@ template <class T>
 CBN_D float gr_value(const T* grid, const GrPost& p, int u, int v) {
     int gu = (u - p.nu / 2 + p.Ku) % p.Ku;
     int gv = (v - p.nv / 2 + p.Kv) % p.Kv;
-    float re = gr_re(grid, (size_t)gu * p.Kv + gv) * p.s32[u] * p.s32[p.smax + v];
-    return (float)((double)re / w1_at(u, v, p.nu, p.nv, p.pu, p.pv, p.so));
+    return gr_re(grid, (size_t)gu * p.Kv + gv) * p.pix[(size_t)u * p.nv + v];
+}
+
+// per-pixel factor of the Grangeat post / pre step, once per plan in float64:
+// reverse: s_u s_v / w1 (grangeat.py:166, nufft.py:247); forward: w1 s_u s_v
+// (grangeat.py:139, nufft.py:226)
+__global__ void k_gr_pix(const float* __restrict__ s32, int smax, int nu, int nv, double pu,
+                         double pv, double so, int reverse, float* __restrict__ pix) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nu * nv) return;
+    const int u = e / nv, v = e % nv;
+    const double w1 = w1_at(u, v, nu, nv, pu, pv, so);
+    const double sc = (double)s32[u] * (double)s32[smax + v];
+    pix[e] = (float)(reverse ? sc / w1 : sc * w1);
+}
+
+void ensure_gr_pix(const cbn_projector_s* p, GrangeatPlan& gp, bool reverse, cudaStream_t s) {
+    if (gp.pix.p) return;
+    const int nu = p->g.nu, nv = p->g.nv;
+    gp.pix.alloc((size_t)nu * nv);
+    k_gr_pix<<<blocks_for((int64_t)nu * nv, 256), 256, 0, s>>>(gp.s32.p, gp.smax, nu, nv, gp.pu,
+                                                              gp.pv, p->g.so_mm, reverse ? 1 : 0,
+                                                              gp.pix.p);
+    CBN_LAUNCH_CHECK();
 }
 
 // mean of the outermost detector ring per view (grangeat.py:167-169)
@@ -1264,11 +1285,7 @@ GrPost gr_post(const P* p, const GrangeatPlan& gp) {
     q.nv = p->g.nv;
     q.Ku = gp.ax[0].K;
     q.Kv = gp.ax[1].K;
-    q.smax = gp.smax;
-    q.pu = gp.pu;
-    q.pv = gp.pv;
-    q.so = p->g.so_mm;
-    q.s32 = gp.s32.p;
+    q.pix = gp.pix.p;
     return q;
 }
 
@@ -1421,6 +1438,7 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     }
     long long kd[2] = {Ku, Kv};
     StageScope st(p->timer, "grangeat_ifft_post", s);
+    ensure_gr_pix(p, gp, true, s);
     GrPost q = gr_post(p, gp);
     B.red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
     double* mean = B.red.p + 2 * kRedBlocks + 64;
@@ -1643,6 +1661,9 @@ void projector_build_tables(cbn_projector_s* p, int mode, const AxisPlan* ax, in
 void projector_fit_grangeat(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
                             cudaStream_t s) {
     fit_grangeat(p, gp, u, s);
+}
+void projector_gr_pix(const cbn_projector_s* p, GrangeatPlan& gp, bool reverse, cudaStream_t s) {
+    ensure_gr_pix(p, gp, reverse, s);
 }
 void projector_column_mean(const float2* src, int64_t lines, int64_t ld, int col, double scale,
                            double* partial, double* out, cudaStream_t s) {

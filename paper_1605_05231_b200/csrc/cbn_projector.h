@@ -49,6 +49,8 @@ struct GrangeatPlan {
     int64_t m = 0;
     DevBuf<float> w2, fac_re, fac_im;   // per t: post-weight, reverse filter (complex)
     DevBuf<float> w2inv;                // per t: 1 / w2, folded into the resample store
+    DevBuf<float> pix;                  // per detector pixel [nu][nv]: reverse s_u s_v / w1,
+                                        // forward w1 s_u s_v (computed in float64 once)
     bool built = false;
     BinPlan bins;                       // polar nodes sorted by 2D tile
     DevBuf<char> pts;                   // GrPoint<5> per sorted node
