@@ -1138,8 +1138,30 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
             CBN_LAUNCH_CHECK();
         }
         StageScope st(p->timer, "resample_fft", s);
-        p->fft.exec_c2r(p->fft.get_c2r3(kd3), p->big.p,
-                        reinterpret_cast<float*>(p->big.p + half), s);
+        // pruned 3D C2R: the pad fills only the theta planes in pad_positions
+        // (and their mirrors), so the inverse C2C along rho (slowest axis,
+        // strided columns) runs on those theta ranges only; then a batched 2D
+        // C2R over the (theta, phi) planes
+        {
+            const long long hz = kd3[2] / 2 + 1, plane = kd3[1] * hz;
+            int a = -1, prev = -2;
+            auto run = [&](int lo, int hi) {
+                const long long nb = (long long)(hi - lo) * hz;
+                p->fft.exec(p->fft.get_strided(kd3[0], nb, plane, 1), p->big.p + (size_t)lo * hz,
+                            p->big.p + (size_t)lo * hz, CUFFT_INVERSE, s);
+            };
+            for (int k : pad_positions(ax[1].N, ax[1].K, true, false)) {
+                if (k != prev + 1) {
+                    if (a >= 0) run(a, prev + 1);
+                    a = k;
+                }
+                prev = k;
+            }
+            if (a >= 0) run(a, prev + 1);
+            const long long k2[2] = {kd3[1], kd3[2]};
+            p->fft.exec_c2r(p->fft.get_c2r2(k2, kd3[0]), p->big.p,
+                            reinterpret_cast<float*>(p->big.p + half), s);
+        }
         p->grid_re = reinterpret_cast<float*>(p->big.p + half);
         return;
     }
