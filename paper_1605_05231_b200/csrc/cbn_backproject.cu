@@ -435,6 +435,17 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             ax[d] = RemapAxis{p->tab_idx.p + off, p->tab_sc.p + off, rax[d].N, x.sstr[d]};
             off += rax[d].N;
         }
+        // theta cells the crop reads -- directly or as the mirror of a cell
+        // past the phi half -- in runs, for the real-grid path's rho pass
+        std::vector<std::pair<int, int>> bres_theta_runs;
+        if (x.lanes) {
+            for (int k : pad_positions(rax[1].N, rax[1].K, true, false)) {
+                if (!bres_theta_runs.empty() && bres_theta_runs.back().second == k)
+                    bres_theta_runs.back().second = k + 1;
+                else
+                    bres_theta_runs.emplace_back(k, k + 1);
+            }
+        }
         // the crop reads only some slowest-axis planes: inverse-FFT just those in 2D
         if (p->bres_planes.empty() || p->bres_planes_slow != x.slow_axis) {
             size_t o = 0;
@@ -449,9 +460,15 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 StageScope st(p->timer, "transpose_ifft", s);
                 const long long k2[2] = {rax[1].K, rax[0].K};
                 p->fft.exec_r2c3(p->fft.get_r2c2(k2, rax[2].K), greal, p->big.p, s);
+                // along rho only the theta columns the crop reads (the crop
+                // table's distinct theta cells, in runs)
                 const long long plane = (long long)rax[1].K * hphi;
-                p->fft.exec(p->fft.get_strided(rax[2].K, plane, plane, 1), p->big.p, p->big.p,
-                            CUFFT_FORWARD, s);
+                for (const auto& rn : bres_theta_runs) {
+                    float2* at = p->big.p + (size_t)rn.first * hphi;
+                    p->fft.exec(p->fft.get_strided(rax[2].K, (long long)(rn.second - rn.first) * hphi,
+                                                   plane, 1),
+                                at, at, CUFFT_FORWARD, s);
+                }
             }
             StageScope st(p->timer, "transpose_crop", s);
             ax[0].sstride = 1;
