@@ -438,14 +438,7 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
         // theta cells the crop reads -- directly or as the mirror of a cell
         // past the phi half -- in runs, for the real-grid path's rho pass
         std::vector<std::pair<int, int>> bres_theta_runs;
-        if (x.lanes) {
-            for (int k : pad_positions(rax[1].N, rax[1].K, true, false)) {
-                if (!bres_theta_runs.empty() && bres_theta_runs.back().second == k)
-                    bres_theta_runs.back().second = k + 1;
-                else
-                    bres_theta_runs.emplace_back(k, k + 1);
-            }
-        }
+        if (x.lanes) bres_theta_runs = pad_runs(rax[1].N, rax[1].K, true);
         // the crop reads only some slowest-axis planes: inverse-FFT just those in 2D
         if (p->bres_planes.empty() || p->bres_planes_slow != x.slow_axis) {
             size_t o = 0;
@@ -718,16 +711,6 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
 
 namespace {
 
-// sorted runs [a, b) of the (2N)-grid planes the crop reads along one axis
-std::vector<std::pair<int, int>> crop_plane_runs(int N, int K) {
-    std::vector<std::pair<int, int>> runs;
-    for (int k : pad_positions(N, K, false, false)) {
-        if (!runs.empty() && runs.back().second == k) runs.back().second = k + 1;
-        else runs.emplace_back(k, k + 1);
-    }
-    return runs;
-}
-
 // y/z crop + deapodisation of the 2D-transformed slab planes, written in the
 // all-to-all send layout [y block d][x][y - y0_d][z] (blocks: the balanced
 // split y0_d = d * ny / nparts), so each destination's chunk is contiguous and
@@ -778,7 +761,7 @@ void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s) {
     const AxisPlan* sax = p->bspec;
     long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
     StageScope st_ff(p->timer, "bp_ifft_crop", s);
-    fft3_pruned(p->fft, grid, k3d, 1, crop_plane_runs(sax[0].N, sax[0].K), CUFFT_INVERSE, s);
+    fft3_pruned(p->fft, grid, k3d, 1, pad_runs(sax[0].N, sax[0].K, false), CUFFT_INVERSE, s);
     RemapAxis cax[3];
     crop_tables(p, cax, s);
     launch_remap<float2, kStoreRe>(3, grid, vol, cax, (float)p->c.bp_normalization, s);

@@ -176,4 +176,13 @@ std::vector<int> pad_positions(int N, int K, bool mirror, bool half) {
     return out;
 }
 
+std::vector<std::pair<int, int>> pad_runs(int N, int K, bool mirror) {
+    std::vector<std::pair<int, int>> runs;
+    for (int k : pad_positions(N, K, mirror, false)) {
+        if (!runs.empty() && runs.back().second == k) runs.back().second = k + 1;
+        else runs.emplace_back(k, k + 1);
+    }
+    return runs;
+}
+
 }  // namespace cbn

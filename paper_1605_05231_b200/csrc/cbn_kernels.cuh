@@ -329,6 +329,8 @@ __global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __res
 // k = (n - N//2) mod K) can fill, with their mirrors -k when `mirror`, and
 // only k <= K/2 when `half` (host)
 std::vector<int> pad_positions(int N, int K, bool mirror, bool half);
+// pad_positions(N, K, mirror, false) as sorted runs [a, b)
+std::vector<std::pair<int, int>> pad_runs(int N, int K, bool mirror);
 
 // Table modes for k_build_table.
 enum TableMode {

@@ -917,9 +917,27 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         CBN_LAUNCH_CHECK();
     }
     {
+        // pruned 3D R2C: only the x planes the pad fills are non-zero, so the
+        // batched 2D R2C over (y, z) runs on those planes (the others' half
+        // planes are zeroed), then the C2C along x over every column
         StageScope st(p->timer, "spectrum_fft", s);
-        p->fft.exec_r2c3(p->fft.get_r2c3(kd), reinterpret_cast<const float*>(p->big.p),
-                         p->big.p + half_off, s);
+        const long long hz = kd[2] / 2 + 1, hplane = kd[1] * hz, rplane = kd[1] * kd[2];
+        const long long k2[2] = {kd[1], kd[2]};
+        float2* half = p->big.p + half_off;
+        const float* real = reinterpret_cast<const float*>(p->big.p);
+        int lo = 0;
+        for (const auto& rn : pad_runs(ax[0].N, ax[0].K, false)) {
+            if (rn.first > lo)
+                CBN_CUDA(cudaMemsetAsync(half + lo * hplane, 0,
+                                         sizeof(float2) * hplane * (rn.first - lo), s));
+            p->fft.exec_r2c3(p->fft.get_r2c2(k2, rn.second - rn.first), real + rn.first * rplane,
+                             half + rn.first * hplane, s);
+            lo = rn.second;
+        }
+        if (lo < kd[0])
+            CBN_CUDA(cudaMemsetAsync(half + lo * hplane, 0, sizeof(float2) * hplane * (kd[0] - lo),
+                                     s));
+        p->fft.exec(p->fft.get_strided(kd[0], hplane, hplane, 1), half, half, CUFFT_FORWARD, s);
     }
     const float2* spec_half = p->big.p + half_off;
     if (!lat) lat = p->lattice.p;
@@ -1144,20 +1162,12 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
         // C2R over the (theta, phi) planes
         {
             const long long hz = kd3[2] / 2 + 1, plane = kd3[1] * hz;
-            int a = -1, prev = -2;
-            auto run = [&](int lo, int hi) {
-                const long long nb = (long long)(hi - lo) * hz;
-                p->fft.exec(p->fft.get_strided(kd3[0], nb, plane, 1), p->big.p + (size_t)lo * hz,
-                            p->big.p + (size_t)lo * hz, CUFFT_INVERSE, s);
-            };
-            for (int k : pad_positions(ax[1].N, ax[1].K, true, false)) {
-                if (k != prev + 1) {
-                    if (a >= 0) run(a, prev + 1);
-                    a = k;
-                }
-                prev = k;
+            for (const auto& rn : pad_runs(ax[1].N, ax[1].K, true)) {
+                float2* at = p->big.p + (size_t)rn.first * hz;
+                p->fft.exec(p->fft.get_strided(kd3[0], (long long)(rn.second - rn.first) * hz,
+                                               plane, 1),
+                            at, at, CUFFT_INVERSE, s);
             }
-            if (a >= 0) run(a, prev + 1);
             const long long k2[2] = {kd3[1], kd3[2]};
             p->fft.exec_c2r(p->fft.get_c2r2(k2, kd3[0]), p->big.p,
                             reinterpret_cast<float*>(p->big.p + half), s);
