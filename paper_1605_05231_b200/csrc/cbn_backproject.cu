@@ -741,6 +741,21 @@ __global__ void k_crop_cols_x(const float2* __restrict__ src, float* __restrict_
     dst[q] = gain * ax.scale[x] * src[(int64_t)ax.idx[x] * row + r].x;
 }
 
+// Hermitian part of the spread grid on the z half: H[k] = (G[k] + conj G[-k]) / 2
+// over [K0][K1][K2/2+1].  Re(IFFT(G)) -- all the crop keeps (pipeline.py:212)
+// -- is the complex-to-real inverse FFT of H.
+__global__ void k_herm_half3(const float2* __restrict__ g, float2* __restrict__ h, int K0, int K1,
+                             int K2) {
+    const int hz = K2 / 2 + 1;
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    if (z >= hz) return;
+    const int y = blockIdx.y, x = blockIdx.z;
+    const int xm = x ? K0 - x : 0, ym = y ? K1 - y : 0, zm = z ? K2 - z : 0;
+    const float2 a = g[((size_t)x * K1 + y) * K2 + z];
+    const float2 b = g[((size_t)xm * K1 + ym) * K2 + zm];
+    h[((size_t)x * K1 + y) * hz + z] = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
+}
+
 void crop_tables(cbn_projector_s* p, RemapAxis* cax, cudaStream_t s) {
     const AxisPlan* sax = p->bspec;
     const int n = p->n_vol;
@@ -759,12 +774,24 @@ void bp_crop(cbn_projector_s* p, float2* grid, float* vol, cudaStream_t s) {
     build_backward_plan(p, s);
     CBN_REQUIRE(p->bspec_fit, "bp_crop before bp_finish");
     const AxisPlan* sax = p->bspec;
-    long long k3d[3] = {sax[0].K, sax[1].K, sax[2].K};
     StageScope st_ff(p->timer, "bp_ifft_crop", s);
-    fft3_pruned(p->fft, grid, k3d, 1, pad_runs(sax[0].N, sax[0].K, false), CUFFT_INVERSE, s);
+    // Hermitian half on z, inverse C2C along x, then batched 2D C2R of only
+    // the x planes the crop reads, into the (consumed) grid's memory as floats
+    const int K0 = sax[0].K, K1 = sax[1].K, K2 = sax[2].K;
+    const long long hz = K2 / 2 + 1, hplane = (long long)K1 * hz, rplane = (long long)K1 * K2;
+    p->bp_half.ensure((size_t)K0 * hplane);
+    float2* h = p->bp_half.p;
+    k_herm_half3<<<dim3((unsigned)((hz + 255) / 256), K1, K0), 256, 0, s>>>(grid, h, K0, K1, K2);
+    CBN_LAUNCH_CHECK();
+    p->fft.exec(p->fft.get_strided(K0, hplane, hplane, 1), h, h, CUFFT_INVERSE, s);
+    float* re = reinterpret_cast<float*>(grid);
+    const long long k2[2] = {K1, K2};
+    for (const auto& rn : pad_runs(sax[0].N, K0, false))
+        p->fft.exec_c2r(p->fft.get_c2r2(k2, rn.second - rn.first), h + rn.first * hplane,
+                        re + rn.first * rplane, s);
     RemapAxis cax[3];
     crop_tables(p, cax, s);
-    launch_remap<float2, kStoreRe>(3, grid, vol, cax, (float)p->c.bp_normalization, s);
+    launch_remap<float, kStoreRe>(3, re, vol, cax, (float)p->c.bp_normalization, s);
     CBN_LAUNCH_CHECK();
 }
 

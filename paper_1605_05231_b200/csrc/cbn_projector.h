@@ -157,6 +157,7 @@ struct cbn_projector_s {
     const float* grid_re = nullptr; // Re(resample grid) inside `big` (real_grid path)
     cbn::DevBuf<float2> lattice;    // radial lattice (raw IFFT layout)
     cbn::DevBuf<float2> padded;     // padded lattice and its FFT / transpose accumulators
+    cbn::DevBuf<float2> bp_half;    // backprojector crop: Hermitian half of the (2N)^3 grid
     cbn::DevBuf<float2> gr_t;       // Grangeat t-line buffers
     cbn::DevBuf<float2> gr_tv;      // reverse Grangeat t-spectra, view-fastest [mu][k][32 views]
     cbn::DevBuf<float2> gr_grid;    // Grangeat 2D grids
