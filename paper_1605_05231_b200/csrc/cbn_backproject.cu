@@ -536,8 +536,12 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 float* gden = den_only ? greal : nullptr;
                 const float* vt = den_only ? nullptr : p->values_t.p;
                 if (x.shift == 2) {
-                    k_rs_gather_cols2<<<ncol, kRsPairThreads, 0, s>>>(
-                        gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
+                    if (den_only)
+                        k_rs_gather_cols2<true><<<ncol, kRsPairThreads, 0, s>>>(
+                            gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
+                    else
+                        k_rs_gather_cols2<false><<<ncol, kRsPairThreads, 0, s>>>(
+                            gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
                 } else {
                     k_rs_gather_cols<<<ncol, kRsColThreads, 0, s>>>(
                         gnum, gden, (int)x.kd3[2], p->bcol_ptr.p, ent, vt, vlo, nvr, x.shift);

@@ -182,6 +182,7 @@ k_rs_gather_cols(float* __restrict__ gnum, float* __restrict__ gden, int K2,
 // so every entry costs two value loads and three FMAs per thread, no search.
 constexpr int kRsPairThreads = 384;
 
+template <bool DEN>   // false: values into gnum; true: validity mask into gden
 static __global__ void __launch_bounds__(kRsPairThreads)
 k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
                   const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
@@ -190,6 +191,7 @@ k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
     const int beg = col_ptr[col], end = col_ptr[col + 1];
     for (int i = threadIdx.x; i < V; i += kRsPairThreads) {
         float ne = 0.f, no = 0.f, de = 0.f, dn = 0.f;
+#pragma unroll 4
         for (int k = beg; k < end; ++k) {
             const RsColEntry e = ent[k];
             const int d = e.f2 - 2 * i;
@@ -202,8 +204,8 @@ k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
             r1 += r1 < 0 ? V : 0;
             const bool ok0 = r0 < nv, ok1 = r1 < nv;
             const float* vt = valsT + (size_t)e.t * nv;
-            const float x0 = (ok0 && valsT) ? __ldg(vt + r0) : 0.f;
-            const float x1 = (ok1 && valsT) ? __ldg(vt + r1) : 0.f;
+            const float x0 = (ok0 && !DEN) ? __ldg(vt + r0) : 0.f;
+            const float x1 = (ok1 && !DEN) ? __ldg(vt + r1) : 0.f;
             const float u0 = ok0 ? 1.f : 0.f, u1 = ok1 ? 1.f : 0.f;
             const float w0 = e.wab * e.w2[0], w1 = e.wab * e.w2[1], w2 = e.wab * e.w2[2];
             if ((d & 1) == 0) {
@@ -218,8 +220,8 @@ k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
                 de = fmaf(w1, u1, de);
             }
         }
-        if (gnum) *(reinterpret_cast<float2*>(gnum + col * 2 * V) + i) = make_float2(ne, no);
-        if (gden) *(reinterpret_cast<float2*>(gden + col * 2 * V) + i) = make_float2(de, dn);
+        if (!DEN) *(reinterpret_cast<float2*>(gnum + col * 2 * V) + i) = make_float2(ne, no);
+        else *(reinterpret_cast<float2*>(gden + col * 2 * V) + i) = make_float2(de, dn);
     }
 }
 
