@@ -1105,6 +1105,8 @@ bool real_grid(const P* p) {
     return views_in_lanes(p) && p->fres[0].J == 3 && p->c.method == 0;
 }
 
+void ensure_lane_taps(P* p, cudaStream_t s);
+
 void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool phi_fast = false) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fres;   // (phi, theta, rho)
@@ -1124,6 +1126,7 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
     if (phi_fast) std::swap(rax[0], rax[2]);
     const double size = (double)dr * r.n_theta * r.n_phi;
     if (real_grid(p)) {
+        ensure_lane_taps(p, s);   // the rho planes the gather reads
         // only Re(G) is read (real weights, Re of the result): pad straight to
         // the conjugated Hermitian half spectrum and complex-to-real FFT it,
         // into a float grid behind the half spectrum in `big`
@@ -1168,9 +1171,13 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
                                                plane, 1),
                             at, at, CUFFT_INVERSE, s);
             }
+            // then the 2D C2R only on the rho planes the umbrella taps read
             const long long k2[2] = {kd3[1], kd3[2]};
-            p->fft.exec_c2r(p->fft.get_c2r2(k2, kd3[0]), p->big.p,
-                            reinterpret_cast<float*>(p->big.p + half), s);
+            float* re = reinterpret_cast<float*>(p->big.p + half);
+            const long long rplane = kd3[1] * kd3[2];
+            for (const auto& rn : p->fres_rho_runs)
+                p->fft.exec_c2r(p->fft.get_c2r2(k2, rn.second - rn.first),
+                                p->big.p + (size_t)rn.first * plane, re + rn.first * rplane, s);
         }
         p->grid_re = reinterpret_cast<float*>(p->big.p + half);
         return;
@@ -1221,6 +1228,27 @@ void ensure_lane_taps(P* p, cudaStream_t s) {
         k_rs_taps<J><<<blocks_for(per_view, 256), 256, 0, s>>>(
             src, kb, per_view, reinterpret_cast<RsTap<J>*>(u.taps.p));
         CBN_LAUNCH_CHECK();
+        {
+            // rho planes the taps read: the grid's other planes are never
+            // inverse-transformed (build_resample_grid)
+            const int K0 = ax[2].K;
+            DevBuf<int> used((size_t)K0);
+            CBN_CUDA(cudaMemsetAsync(used.p, 0, sizeof(int) * K0, s));
+            k_rs_rho_used<J><<<blocks_for(per_view, 256), 256, 0, s>>>(
+                reinterpret_cast<const RsTap<J>*>(u.taps.p), per_view, K0, used.p);
+            CBN_LAUNCH_CHECK();
+            std::vector<int> h((size_t)K0);
+            CBN_CUDA(cudaMemcpyAsync(h.data(), used.p, sizeof(int) * K0, cudaMemcpyDeviceToHost, s));
+            CBN_CUDA(cudaStreamSynchronize(s));
+            p->fres_rho_runs.clear();
+            for (int k = 0; k < K0; ++k) {
+                if (!h[(size_t)k]) continue;
+                if (!p->fres_rho_runs.empty() && p->fres_rho_runs.back().second == k)
+                    p->fres_rho_runs.back().second = k + 1;
+                else
+                    p->fres_rho_runs.emplace_back(k, k + 1);
+            }
+        }
         if constexpr (J == 3) {
             CBN_REQUIRE((int64_t)ax[2].K * ax[1].K * ax[0].K < (1LL << 32),
                         "resample grid above 2^32 cells");

@@ -124,6 +124,8 @@ struct cbn_projector_s {
     cbn::DevBuf<int> fpairs;     // primary radial nodes (RadialPairSrc); mirrors by conjugation
     cbn::DevBuf<int> fspec_list, fres_list;   // compact pad positions per axis (see pad_positions)
     int fspec_nl[3] = {0, 0, 0}, fres_nl[3] = {0, 0, 0};
+    // rho planes of the (views-in-lanes) resample grid the umbrella taps read
+    std::vector<std::pair<int, int>> fres_rho_runs;
     int64_t fpairs_n = 0;
     bool fspec_fit = false;
     cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT

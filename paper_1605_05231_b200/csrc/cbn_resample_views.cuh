@@ -122,6 +122,20 @@ static __global__ void k_remap_half_acc(const float2* __restrict__ F, float2* __
     *d = make_float2(o.x + sc * f.x, o.y + sg * sc * f.y);
 }
 
+// used[k] = 1 for every axis-0 (rho) plane a valid target's taps touch
+template <int J>
+__global__ void k_rs_rho_used(const RsTap<J>* __restrict__ taps, int64_t n, int K0,
+                              int* __restrict__ used) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n || !taps[t].valid) return;
+    const int f = taps[t].f[0];
+#pragma unroll
+    for (int a = 0; a < J; ++a) {
+        const int k = f + a >= K0 ? f + a - K0 : f + a;
+        if (!used[k]) used[k] = 1;
+    }
+}
+
 // vals [nv][n] -> valsT [n][nv]
 static __global__ void k_transpose_vals(const float* __restrict__ in, int nv, int64_t n,
                                  float* __restrict__ out) {

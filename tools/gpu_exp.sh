@@ -1,4 +1,4 @@
-# A/B experiments: bp bench under spread-warp overrides
-for w in 1 2 4; do
-  CBN_SPREAD_W=$w python bench.py --direction back --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('W=$w', d['value'], d['stages_ms_per_step']['bp_spread'])"
+# A/B experiments: backprojector Grangeat gather views per CTA
+for vg in 4 8 16; do
+  CBN_GR_VG=$vg python bench.py --direction back --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('VG=$vg', d['value'], d['stages_ms_per_step']['grangeat_forward'])"
 done
