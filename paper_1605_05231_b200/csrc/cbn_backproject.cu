@@ -357,6 +357,22 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
             CBN_CUDA(cudaMemcpyAsync(h.data() + 1, counts.p, sizeof(int) * ncol,
                                      cudaMemcpyDeviceToHost, s));
             CBN_CUDA(cudaStreamSynchronize(s));
+            {
+                // rho planes (cols rho * K_theta + theta) that hold any entry
+                const int64_t kt = x.kd3[1];
+                std::vector<unsigned char> used((size_t)x.kd3[0], 0);
+                p->bres_rho_runs.clear();
+                for (int64_t rr = 0; rr < x.kd3[0]; ++rr) {
+                    for (int64_t t = 0; t < kt && !used[(size_t)rr]; ++t)
+                        used[(size_t)rr] = h[(size_t)(rr * kt + t) + 1] > 0;
+                    if (!used[(size_t)rr]) continue;
+                    if (!p->bres_rho_runs.empty() && p->bres_rho_runs.back().second == rr)
+                        p->bres_rho_runs.back().second = (int)rr + 1;
+                    else
+                        p->bres_rho_runs.emplace_back((int)rr, (int)rr + 1);
+                }
+                p->bres_rho_used.upload(used.data(), used.size(), s);
+            }
             std::partial_sum(h.begin(), h.end(), h.begin());
             p->bcol_ptr.upload(h.data(), h.size(), s);
             p->bcol_ent.alloc(sizeof(RsColEntry) * (size_t)std::max(h.back(), 1));
@@ -451,8 +467,23 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             // then the crop reads IFFT = conj(FFT) from the half spectrum
             {
                 StageScope st(p->timer, "transpose_ifft", s);
+                // 2D R2C only on the rho planes holding entries (the others'
+                // half planes are zeroed)
                 const long long k2[2] = {rax[1].K, rax[0].K};
-                p->fft.exec_r2c3(p->fft.get_r2c2(k2, rax[2].K), greal, p->big.p, s);
+                const long long hplane = (long long)rax[1].K * hphi;
+                const long long rplane = (long long)rax[1].K * rax[0].K;
+                int lo = 0;
+                for (const auto& rn : p->bres_rho_runs) {
+                    if (rn.first > lo)
+                        CBN_CUDA(cudaMemsetAsync(p->big.p + lo * hplane, 0,
+                                                 sizeof(float2) * hplane * (rn.first - lo), s));
+                    p->fft.exec_r2c3(p->fft.get_r2c2(k2, rn.second - rn.first),
+                                     greal + rn.first * rplane, p->big.p + rn.first * hplane, s);
+                    lo = rn.second;
+                }
+                if (lo < rax[2].K)
+                    CBN_CUDA(cudaMemsetAsync(p->big.p + lo * hplane, 0,
+                                             sizeof(float2) * hplane * (rax[2].K - lo), s));
                 // along rho only the theta columns the crop reads (the crop
                 // table's distinct theta cells, in runs)
                 const long long plane = (long long)rax[1].K * hphi;
@@ -536,12 +567,14 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 float* gden = den_only ? greal : nullptr;
                 const float* vt = den_only ? nullptr : p->values_t.p;
                 if (x.shift == 2) {
+                    const unsigned char* used = p->bres_rho_used.p;
+                    const int kt = (int)x.kd3[1];
                     if (den_only)
                         k_rs_gather_cols2<true><<<ncol, kRsPairThreads, 0, s>>>(
-                            gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
+                            gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr, used, kt);
                     else
                         k_rs_gather_cols2<false><<<ncol, kRsPairThreads, 0, s>>>(
-                            gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr);
+                            gnum, gden, p->g.n_views, p->bcol_ptr.p, ent, vt, vlo, nvr, used, kt);
                 } else {
                     k_rs_gather_cols<<<ncol, kRsColThreads, 0, s>>>(
                         gnum, gden, (int)x.kd3[2], p->bcol_ptr.p, ent, vt, vlo, nvr, x.shift);

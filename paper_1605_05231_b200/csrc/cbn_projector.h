@@ -126,6 +126,10 @@ struct cbn_projector_s {
     int fspec_nl[3] = {0, 0, 0}, fres_nl[3] = {0, 0, 0};
     // rho planes of the (views-in-lanes) resample grid the umbrella taps read
     std::vector<std::pair<int, int>> fres_rho_runs;
+    // backprojector: rho planes of the transposed grid with column entries, and
+    // a per-plane flag for the column gather
+    std::vector<std::pair<int, int>> bres_rho_runs;
+    cbn::DevBuf<unsigned char> bres_rho_used;
     int64_t fpairs_n = 0;
     bool fspec_fit = false;
     cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT

@@ -200,8 +200,10 @@ template <bool DEN>   // false: values into gnum; true: validity mask into gden
 static __global__ void __launch_bounds__(kRsPairThreads)
 k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
                   const int* __restrict__ col_ptr, const RsColEntry* __restrict__ ent,
-                  const float* __restrict__ valsT, int vlo, int nv) {
+                  const float* __restrict__ valsT, int vlo, int nv,
+                  const unsigned char* __restrict__ plane_used, int K1) {
     const size_t col = blockIdx.x;
+    if (!plane_used[col / K1]) return;   // rho plane never transformed
     const int beg = col_ptr[col], end = col_ptr[col + 1];
     for (int i = threadIdx.x; i < V; i += kRsPairThreads) {
         float ne = 0.f, no = 0.f, de = 0.f, dn = 0.f;
