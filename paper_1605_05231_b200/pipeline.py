@@ -340,7 +340,9 @@ def sharded_crop(proj, grid, rank: int, world: int, group=None):
     xs, ys = slab_ranges(k, world), slab_ranges(n, world)
     if k % world == 0:
         slab = torch.empty(plane * (k // world), dtype=grid.dtype, device=grid.device)
-        dist.reduce_scatter_tensor(slab, grid, group=group)
+        # reduce_scatter_tensor has no complex path: reduce the (re, im) view
+        real = torch.view_as_real if grid.is_complex() else (lambda t: t)
+        dist.reduce_scatter_tensor(real(slab), real(grid), group=group)
     else:
         dist.all_reduce(grid, group=group)
         slab = grid[xs[rank] * plane: xs[rank + 1] * plane]

@@ -86,7 +86,7 @@ class _FakeProjector:
     sharding contract (node parts summed over ranks, view ranges local) and the
     same separable crop structure (grid (K, K, K) -> volume (n, n, n))."""
 
-    def __init__(self, views=6, n_vox=5, m=9, n=3, k=6):
+    def __init__(self, views=6, n_vox=5, m=9, n=3, k=6, cplx=False):
         import torch
         g = torch.Generator().manual_seed(0)
         self.views, self.n, self.k = views, n, k
@@ -95,6 +95,10 @@ class _FakeProjector:
         self.C = torch.randn(m, views, generator=g, dtype=torch.float64)       # views -> lattice
         self.D = torch.randn(k ** 3, m, generator=g, dtype=torch.float64)      # lattice -> grid
         self.F = [torch.randn(n, k, generator=g, dtype=torch.float64) for _ in range(3)]
+        if cplx:   # complex grid and crop maps, as the device path's complex64 buffers
+            self.D = self.D + 1j * torch.randn(k ** 3, m, generator=g, dtype=torch.float64)
+            self.F = [f + 1j * torch.randn(n, k, generator=g, dtype=torch.float64) for f in self.F]
+            self.C = self.C.to(torch.complex128)
 
     @staticmethod
     def _rows(n, part, nparts):
@@ -132,7 +136,7 @@ class _FakeProjector:
         return torch.einsum("xa,ayz->xyz", self.F[0], cols.view(self.k, y_hi - y_lo, self.n))
 
 
-def _sharded_worker(rank, world, port, result_path, k=6):
+def _sharded_worker(rank, world, port, result_path, k=6, cplx=False):
     import sys
     import torch
     import torch.distributed as dist
@@ -142,34 +146,35 @@ def _sharded_worker(rank, world, port, result_path, k=6):
     from paper_1605_05231_b200.pipeline import Projector
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    fake = _FakeProjector(k=k)
+    fake = _FakeProjector(k=k, cplx=cplx)
     vol = torch.arange(5, dtype=torch.float64) + 1.0 if rank == 0 else torch.zeros(5, dtype=torch.float64)
     frames = torch.linspace(-1.0, 2.0, fake.views, dtype=torch.float64)
     lo, hi = sharding.view_shard(fake.views, world, rank)
     fwd_local = Projector.forward_sharded(fake, vol, lo, hi)
     fwd = sharding.gather_views(fwd_local, fake.views)
-    bp = Projector.backproject_sharded(fake, frames[lo:hi], lo, hi)
+    bp = Projector.backproject_sharded(fake, frames[lo:hi].to(fake.C.dtype), lo, hi)
     if rank == 0:
         np.savez(result_path, fwd=fwd.numpy(), bp=bp.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,k", [(2, 6), (3, 6), (2, 5)])
-def test_gloo_sharded_phase_orchestration(tmp_path, world, k):
+@pytest.mark.parametrize("world,k,cplx", [(2, 6, False), (3, 6, False), (2, 5, False),
+                                          (2, 6, True)])
+def test_gloo_sharded_phase_orchestration(tmp_path, world, k, cplx):
     """Projector.forward_sharded / backproject_sharded over a gloo world: the
     volume broadcast, node-part sums (all-reduce), view ranges and the
     slab-distributed crop (reduce-scatter by x slab -- all-reduce + slice when
     the world does not divide the grid -- all-to-all to y ranges, all-gather)
     give the single-process maps."""
     out = str(tmp_path / "res.npz")
-    mp.spawn(_sharded_worker, args=(world, _free_port(), out, k), nprocs=world, join=True)
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out, k, cplx), nprocs=world, join=True)
     res = np.load(out)
-    f = _FakeProjector(k=k)
+    f = _FakeProjector(k=k, cplx=cplx)
     import torch
     vol = torch.arange(5, dtype=torch.float64) + 1.0
     frames = torch.linspace(-1.0, 2.0, f.views, dtype=torch.float64)
     assert np.allclose(res["fwd"], (f.B @ (f.A @ vol)).numpy(), rtol=1e-12)
-    ref = f.backproject_crop(f.D @ (f.C @ frames)).numpy()
+    ref = f.backproject_crop(f.D @ (f.C @ frames.to(f.C.dtype))).numpy()
     assert res["bp"].shape == ref.shape
     assert np.allclose(res["bp"], ref, rtol=1e-12, atol=1e-12)

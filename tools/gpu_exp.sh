@@ -1,4 +1,5 @@
-# A/B experiments: backprojector Grangeat gather views per CTA
-for vg in 4 8 16; do
-  CBN_GR_VG=$vg python bench.py --direction back --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('VG=$vg', d['value'], d['stages_ms_per_step']['grangeat_forward'])"
+# A/B experiments: bp bench under spread-warp overrides
+python -m pytest tests -q -m gpu -x 2>&1 | tail -1
+for w in 2 4; do
+  CBN_SPREAD_W=$w python bench.py --direction back --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('W=$w', d['value'], d['stages_ms_per_step']['bp_spread'])"
 done
