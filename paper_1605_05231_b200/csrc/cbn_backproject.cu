@@ -52,30 +52,42 @@ CBN_D int pad_src(int g, int N, int K) {
 
 // h = frame * w1 ; y = h * scaling placed at rolled positions (nufft.py:226-230)
 __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int Ku, int Kv,
-                          const float* __restrict__ pix, int64_t total, float* __restrict__ grids) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= total) return;
-    const int64_t per = (int64_t)Ku * Kv;
-    const int v = (int)(e / per);
-    const int rem = (int)(e % per);
-    const int gu = rem / Kv, gv = rem % Kv;
+                          const float* __restrict__ pix, float* __restrict__ grids) {
+    // grid (Kv / 256, Ku, views): one padded row per (blockIdx.y, blockIdx.z)
+    const int gv = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gv >= Kv) return;
+    const int gu = blockIdx.y, v = blockIdx.z;
     const int nu_i = pad_src(gu, nu, Ku), nv_i = pad_src(gv, nv, Kv);
     float out = 0.f;
     if (nu_i >= 0 && nv_i >= 0) {
         const size_t px = (size_t)nu_i * nv + nv_i;
         out = frames[(size_t)v * nu * nv + px] * pix[px];
     }
-    grids[e] = out;
+    grids[((size_t)v * Ku + gu) * Kv + gv] = out;
 }
 
 // values = Re(fftshift(ifft)) / dt * w2   (grangeat.py:144-145)
 __global__ void k_grf_post(const float2* __restrict__ t, const float* __restrict__ w2, int n_t,
                            double inv, int64_t total, float* __restrict__ vals) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // two outputs (j, j + 1) per thread, j even; n_t % 4 == 0 so the two
+    // source bins (j - n_t/2 mod n_t) are one aligned 16-byte pair
+    const int64_t e = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (e >= total) return;
-    const int j = (int)(e % n_t);
     const int64_t row = e / n_t;
-    float re = t[row * n_t + (j - n_t / 2 + n_t) % n_t].x;
+    const int j = (int)(e - row * n_t);
+    const int src = j < n_t / 2 ? j + n_t / 2 : j - n_t / 2;
+    const float4 q = *reinterpret_cast<const float4*>(t + row * n_t + src);
+    *reinterpret_cast<float2*>(vals + e) =
+        make_float2((float)(q.x * inv) * w2[j], (float)(q.z * inv) * w2[j + 1]);
+}
+
+__global__ void k_grf_post1(const float2* __restrict__ t, const float* __restrict__ w2, int n_t,
+                            double inv, int64_t total, float* __restrict__ vals) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int64_t row = e / n_t;
+    const int j = (int)(e - row * n_t);
+    const float re = t[row * n_t + (j - n_t / 2 + n_t) % n_t].x;
     vals[e] = (float)(re * inv) * w2[j];
 }
 
@@ -255,8 +267,9 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     float* padded = reinterpret_cast<float*>(B.tv.p);
     const int64_t gtot = (int64_t)nb * Ku * Kv;
     projector_gr_pix(p, gp, false, s);
-    k_grf_pad<<<blocks_for(gtot, 256), 256, 0, s>>>(frames, nu, nv, Ku, Kv, gp.pix.p, gtot,
-                                                    padded);
+    k_grf_pad<<<dim3((unsigned)((Kv + 255) / 256), Ku, nb), 256, 0, s>>>(frames, nu, nv, Ku, Kv,
+                                                                      gp.pix.p, padded);
+    (void)gtot;
     CBN_LAUNCH_CHECK();
     long long kd[2] = {Ku, Kv};
     B.fft.exec_r2c3(B.fft.get_r2c2(kd, nb), padded, B.grid.p, s);
@@ -269,8 +282,11 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     long long nt[1] = {u.n_t};
     B.fft.exec(B.fft.get(1, nt, (long long)nb * u.n_mu), B.t.p, B.t.p, CUFFT_INVERSE, s);
     const int64_t vt = (int64_t)nb * per_view;
-    k_grf_post<<<blocks_for(vt, 256), 256, 0, s>>>(B.t.p, gp.w2.p, u.n_t,
-                                                  1.0 / ((double)u.n_t * u.dt), vt, values);
+    const double inv = 1.0 / ((double)u.n_t * u.dt);
+    if (u.n_t % 4 == 0)
+        k_grf_post<<<blocks_for(vt / 2, 256), 256, 0, s>>>(B.t.p, gp.w2.p, u.n_t, inv, vt, values);
+    else
+        k_grf_post1<<<blocks_for(vt, 256), 256, 0, s>>>(B.t.p, gp.w2.p, u.n_t, inv, vt, values);
     CBN_LAUNCH_CHECK();
 }
 

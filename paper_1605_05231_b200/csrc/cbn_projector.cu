@@ -610,17 +610,15 @@ __global__ void k_gr_ring(const T* __restrict__ grids, GrPost p, double* __restr
 template <class T>
 __global__ void k_gr_frame(const T* __restrict__ grids, GrPost p,
                            const double* __restrict__ mean, float norm, float* __restrict__ frames,
-                           int64_t total, int* __restrict__ flag) {
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= total) return;
-    const int64_t per = (int64_t)p.nu * p.nv;
-    const int v = (int)(e / per);
-    const int rem = (int)(e % per);
-    const int u = rem / p.nv, w = rem % p.nv;
+                           int* __restrict__ flag) {
+    // grid (nv / 256, nu, views): one detector row per (blockIdx.y, blockIdx.z)
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= p.nv) return;
+    const int u = blockIdx.y, v = blockIdx.z;
     float g = gr_value(grids + (size_t)v * p.Ku * p.Kv, p, u, w);
     float out = (float)((double)g - mean[v]) * norm;
     if (!isfinite(out)) atomicOr(flag, 1);
-    frames[e] = out;
+    frames[((size_t)v * p.nu + u) * p.nv + w] = out;
 }
 
 }  // namespace cbn
@@ -1502,12 +1500,11 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     GrPost q = gr_post(p, gp);
     B.red.ensure(2 * kRedBlocks + 64 + (size_t)nb);
     double* mean = B.red.p + 2 * kRedBlocks + 64;
-    const int64_t total = (int64_t)nb * p->g.nu * p->g.nv;
     auto post = [&](const auto* g) {
         k_gr_ring<<<nb, 256, 0, s>>>(g, q, mean);
         CBN_LAUNCH_CHECK();
-        k_gr_frame<<<blocks_for(total, 256), 256, 0, s>>>(g, q, mean, (float)p->c.normalization,
-                                                          frames, total, p->flag.p);
+        k_gr_frame<<<dim3((unsigned)((p->g.nv + 255) / 256), p->g.nu, nb), 256, 0, s>>>(
+            g, q, mean, (float)p->c.normalization, frames, p->flag.p);
         CBN_LAUNCH_CHECK();
     };
     if (cell_gather) {
