@@ -133,12 +133,11 @@ __global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict
 __global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __restrict__ dst,
                                    RemapAxis a0, RemapAxis a1, RemapAxis a2,
                                    const int* __restrict__ l0, const int* __restrict__ l1,
-                                   const int* __restrict__ l2, int n1l, int n2l, int64_t total,
-                                   float gain) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= total) return;
+                                   const int* __restrict__ l2, int n2l, float gain) {
+    const int q2 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q2 >= n2l) return;
     const int h2 = a2.n / 2 + 1;
-    const int e[3] = {l0[q / ((int64_t)n1l * n2l)], l1[(q / n2l) % n1l], l2[q % n2l]};
+    const int e[3] = {l0[blockIdx.z], l1[blockIdx.y], l2[q2]};
     const RemapAxis ax[3] = {a0, a1, a2};
     float2 v[2];
 #pragma unroll

@@ -292,16 +292,17 @@ __global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict
 
 // The same remaps restricted to the destination cells a pad table can make
 // non-zero (compact per-axis index lists `l`, lengths nl; the caller zeroes
-// the rest of the destination first): k_remap (3D, kStoreRe / kStoreC) and
+// the rest of the destination first; grid (nl2 / 256, nl1, nl0)): k_remap (3D, kStoreRe / kStoreC) and
 // k_remap_herm3 (list on the half axis limited to <= n2 / 2).
 template <class SrcT, int MODE>
 __global__ void k_remap_list3(const SrcT* __restrict__ src, void* __restrict__ dst, RemapAxis a0,
                               RemapAxis a1, RemapAxis a2, const int* __restrict__ l0,
-                              const int* __restrict__ l1, const int* __restrict__ l2, int n1l,
-                              int n2l, int64_t total, float gain) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= total) return;
-    const int e0 = l0[e / ((int64_t)n1l * n2l)], e1 = l1[(e / n2l) % n1l], e2 = l2[e % n2l];
+                              const int* __restrict__ l1, const int* __restrict__ l2, int n2l,
+                              float gain) {
+    // grid (n2l / 256, n1l, n0l)
+    const int q2 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q2 >= n2l) return;
+    const int e0 = l0[blockIdx.z], e1 = l1[blockIdx.y], e2 = l2[q2];
     const int id0 = a0.idx[e0], id1 = a1.idx[e1], id2 = a2.idx[e2];
     const size_t doff = ((size_t)e0 * a1.n + e1) * a2.n + e2;
     float2 v = make_float2(0.f, 0.f);
@@ -322,8 +323,7 @@ __global__ void k_remap_list3(const SrcT* __restrict__ src, void* __restrict__ d
 __global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __restrict__ dst,
                                    RemapAxis a0, RemapAxis a1, RemapAxis a2,
                                    const int* __restrict__ l0, const int* __restrict__ l1,
-                                   const int* __restrict__ l2, int n1l, int n2l, int64_t total,
-                                   float gain);
+                                   const int* __restrict__ l2, int n2l, float gain);
 
 // destination indices a pad table (kTabPad / kTabPadShift: source n, output
 // k = (n - N//2) mod K) can fill, with their mirrors -k when `mirror`, and

@@ -908,10 +908,10 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         StageScope st(p->timer, "spectrum_pad", s);
         CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float) * real_cells, s));
         const int* l = p->fspec_list.p;
-        const int64_t cells = (int64_t)p->fspec_nl[0] * p->fspec_nl[1] * p->fspec_nl[2];
-        k_remap_list3<float, kStoreRe><<<blocks_for(cells, 256), 256, 0, s>>>(
+        k_remap_list3<float, kStoreRe><<<dim3((unsigned)((p->fspec_nl[2] + 255) / 256),
+                                              p->fspec_nl[1], p->fspec_nl[0]), 256, 0, s>>>(
             vol, p->big.p, rax[0], rax[1], rax[2], l, l + p->fspec_nl[0],
-            l + p->fspec_nl[0] + p->fspec_nl[1], p->fspec_nl[1], p->fspec_nl[2], cells, 1.0f);
+            l + p->fspec_nl[0] + p->fspec_nl[1], p->fspec_nl[2], 1.0f);
         CBN_LAUNCH_CHECK();
     }
     {
@@ -1149,11 +1149,10 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
             StageScope st(p->timer, "resample_pad", s);
             CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * half, s));
             const int* l = p->fres_list.p;
-            const int64_t cells = (int64_t)p->fres_nl[0] * p->fres_nl[1] * p->fres_nl[2];
-            k_remap_herm3_list<<<blocks_for(cells, 256), 256, 0, s>>>(
+            k_remap_herm3_list<<<dim3((unsigned)((p->fres_nl[2] + 255) / 256), p->fres_nl[1],
+                                      p->fres_nl[0]), 256, 0, s>>>(
                 p->padded.p, p->big.p, rax[0], rax[1], rax[2], l, l + p->fres_nl[0],
-                l + p->fres_nl[0] + p->fres_nl[1], p->fres_nl[1], p->fres_nl[2], cells,
-                (float)(1.0 / size));
+                l + p->fres_nl[0] + p->fres_nl[1], p->fres_nl[2], (float)(1.0 / size));
             CBN_LAUNCH_CHECK();
         }
         StageScope st(p->timer, "resample_fft", s);
