@@ -34,11 +34,11 @@ PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 # dram__bytes_read.sum + dram__bytes_write.sum per config-2 step, summed over
 # the stage's launches, from the committed ncu launch lists
-# (profiles/r1d_launches_fwd.txt, profiles/r1d_launches_bp.txt); stages not
+# (profiles/r1h_launches_fwd.txt, profiles/r1h_launches_bp.txt); stages not
 # captured there report null
-TRAFFIC: dict = {"resample_gather": 2.338e9, "grangeat_spread": 3.716e9 + 1.707e9,
-                 "spectrum_gather": 0.953e9, "bp_spread": 1.025e9,
-                 "transpose_spread": 2.229e9 + 0.725e9}
+TRAFFIC: dict = {"resample_gather": 2.371e9, "grangeat_spread": 2.441e9 + 1.863e9,
+                 "spectrum_gather": 0.966e9, "bp_spread": 1.024e9,
+                 "transpose_spread": 0.839e9 + 0.725e9}
 
 
 def parse_args():
