@@ -56,6 +56,24 @@ def test_dot_test_fp32(nf, dims):
     assert abs(lhs - rhs) / abs(lhs) < 1e-5
 
 
+def test_dot_test_config2_radial(nf):
+    """Adjoint identity <A x, y> = <x, A^H y> at full config-2 sizes: the 33 M
+    radial nodes of the 512 x 180 x 360 lattice on a 256^3 grid, J = 6
+    (SURVEY 8(c) size-independent property; BASELINE config 1's dot check)."""
+    from paper_1605_05231_b200 import radon_fourier as rf
+    from paper_1605_05231_b200.geometry import RadialGridSpec
+    n = 256
+    spec = RadialGridSpec(512, 180, 360, 2.0)
+    nodes = rf._radial_direction_nodes(spec, 2.0 / n)
+    rng = np.random.default_rng(11)
+    plan = nf.plan_nufft((n, n, n), nodes, 2.0, 6)
+    x = (rng.standard_normal((n, n, n)) + 1j * rng.standard_normal((n, n, n))).astype(np.complex64)
+    y = (rng.standard_normal(len(nodes)) + 1j * rng.standard_normal(len(nodes))).astype(np.complex64)
+    lhs = np.vdot(y.astype(np.complex128), nf.nufft_forward(plan, x))
+    rhs = np.vdot(nf.nufft_adjoint(plan, y), x.astype(np.complex128))
+    assert abs(lhs - rhs) / abs(lhs) < 1e-5
+
+
 def test_wrap_is_bitwise_numpy(nf):
     """Device remainder (fma-based fmod) == numpy's mod(x + pi, 2 pi) - pi, bit for bit."""
     rng = np.random.default_rng(3)
