@@ -81,6 +81,33 @@ __global__ void k_grf_post(const float2* __restrict__ t, const float* __restrict
         make_float2((float)(q.x * inv) * w2[j], (float)(q.z * inv) * w2[j + 1]);
 }
 
+// k_grf_post writing target-major: valsT[target * ldT + voff + v] for the
+// block's views v < nb (<= 32); 32 targets x 32 views per CTA through shared
+// memory, so both the reads (along t) and the writes (along views) coalesce
+__global__ void k_grf_post_t(const float2* __restrict__ t, const float* __restrict__ w2, int n_t,
+                             double inv, int64_t per_view, int nb, float* __restrict__ valsT,
+                             int64_t ldT, int voff) {
+    __shared__ float tile[32][33];
+    const int64_t t0 = (int64_t)blockIdx.x * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t tt = t0 + lane;
+    if (tt < per_view) {
+        const int64_t line = tt / n_t;
+        const int j = (int)(tt - line * n_t);
+        const int src = j < n_t / 2 ? j + (n_t - n_t / 2) : j - n_t / 2;
+        const float w = w2[j];
+        for (int v = warp; v < nb; v += 8) {
+            const float re = t[((int64_t)v * (per_view / n_t) + line) * n_t + src].x;
+            tile[v][lane] = (float)(re * inv) * w;
+        }
+    }
+    __syncthreads();
+    for (int q = warp; q < 32; q += 8) {
+        const int64_t tq = t0 + q;
+        if (tq < per_view && lane < nb) valsT[tq * ldT + voff + lane] = tile[lane][q];
+    }
+}
+
 __global__ void k_grf_post1(const float2* __restrict__ t, const float* __restrict__ w2, int n_t,
                             double inv, int64_t total, float* __restrict__ vals) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -249,8 +276,10 @@ void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const Umb
 
 // forward_grangeat_view for nb (<= 32) views: frames (nb x nu x nv) -> values
 // (nb x n_mu x n_t), grangeat.py:131-146
+// values: [nb][n_mu][n_t]; or, with valsT, target-major valsT[target * ldT + voff + v]
 void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, float* values,
-                            cudaStream_t s, GrBufs B) {
+                            cudaStream_t s, GrBufs B, float* valsT = nullptr, int64_t ldT = 0,
+                            int voff = 0) {
     GrangeatPlan& gp = p->bgr;
     if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
     projector_prepare_gr_points(p, gp, p->bumb, false, s);
@@ -283,6 +312,12 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     B.fft.exec(B.fft.get(1, nt, (long long)nb * u.n_mu), B.t.p, B.t.p, CUFFT_INVERSE, s);
     const int64_t vt = (int64_t)nb * per_view;
     const double inv = 1.0 / ((double)u.n_t * u.dt);
+    if (valsT) {
+        k_grf_post_t<<<blocks_for(per_view, 32), 256, 0, s>>>(B.t.p, gp.w2.p, u.n_t, inv, per_view,
+                                                            nb, valsT, ldT, voff);
+        CBN_LAUNCH_CHECK();
+        return;
+    }
     if (u.n_t % 4 == 0)
         k_grf_post<<<blocks_for(vt / 2, 256), 256, 0, s>>>(B.t.p, gp.w2.p, u.n_t, inv, vt, values);
     else
@@ -421,7 +456,8 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
     CBN_CUDA(cudaMemsetAsync(acc, 0, sizeof(float2) * x.dsize, s));
     p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
     // blocks of 32 views alternate between the caller's stream and s1
-    auto forward_grangeat = [&](int v0, int nb, float* out) {
+    // out: [view][n_mu][n_t] values; or (outT) target-major [target][nb]
+    auto forward_grangeat = [&](int v0, int nb, float* out, float* outT = nullptr) {
         const bool dual = nb > 32 && lanes_allowed();
         if (dual) {
             // plan state both lanes read, then fork
@@ -438,8 +474,8 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             StageScope st(p->timer, "grangeat_forward", ls);
             const int n = std::min(32, nb - k);
             grangeat_forward_block(p, frames + (size_t)(v0 + k - lo) * nu * nv, n,
-                                   out + (size_t)k * per_view, ls,
-                                   l1 ? lane_bufs(p) : main_bufs(p));
+                                   outT ? nullptr : out + (size_t)k * per_view, ls,
+                                   l1 ? lane_bufs(p) : main_bufs(p), outT, nb, k);
         }
         if (dual) {
             CBN_CUDA(cudaEventRecord(p->ev_s1, p->s1));
@@ -566,17 +602,13 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             if (vlo >= vhi) continue;
             const int nvr = vhi - vlo;
             if (!den_only) {
-                p->values.ensure((size_t)per_view * nvr);
+                // the Grangeat post writes the values target-major for the
+                // column gather (no separate transpose)
                 p->values_t.ensure((size_t)per_view * nvr);
-                forward_grangeat(vlo, nvr, p->values.p);
+                forward_grangeat(vlo, nvr, nullptr, p->values_t.p);
             }
             {
                 StageScope st(p->timer, "transpose_spread", s);
-                if (!den_only) {
-                    dim3 tg((unsigned)((per_view + 31) / 32), (unsigned)((nvr + 31) / 32));
-                    k_transpose_vals<<<tg, 256, 0, s>>>(p->values.p, nvr, per_view, p->values_t.p);
-                    CBN_LAUNCH_CHECK();
-                }
                 const unsigned ncol = (unsigned)(x.kd3[0] * x.kd3[1]);
                 const RsColEntry* ent = reinterpret_cast<const RsColEntry*>(p->bcol_ent.p);
                 float* gnum = den_only ? nullptr : greal;
