@@ -130,6 +130,62 @@ __global__ void k_remap_herm3(const float2* __restrict__ src, float2* __restrict
         make_float2(0.5f * (v[0].x + v[1].x), 0.5f * (v[1].y - v[0].y));
 }
 
+// k_remap_herm3_list through 32 x 32 (axis 0 x axis 2) shared-memory tiles per
+// axis-1 cell, for sources whose axis 0 is the contiguous one (a0.sstride ==
+// 1): loads run along axis 0, stores along axis 2.  Grid (ceil(n2l / 32),
+// ceil(n0l / 32), n1l), block (32, 8).
+__global__ void k_remap_herm3_tile(const float2* __restrict__ src, float2* __restrict__ dst,
+                                   RemapAxis a0, RemapAxis a1, RemapAxis a2,
+                                   const int* __restrict__ l0, const int* __restrict__ l1,
+                                   const int* __restrict__ l2, int n0l, int n2l, float gain) {
+    __shared__ float2 tile[2][32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int q00 = blockIdx.y * 32, q20 = blockIdx.x * 32;
+    const int e1 = l1[blockIdx.z];
+    const int h2 = a2.n / 2 + 1;
+    const int e1m = e1 == 0 ? 0 : a1.n - e1;
+    const int id1[2] = {a1.idx[e1], a1.idx[e1m]};
+    const float sc1[2] = {gain * a1.scale[e1], gain * a1.scale[e1m]};
+    // load: tx along axis 0 (contiguous source), ty over axis-2 rows
+    const int q0 = q00 + tx;
+    int e0 = 0, k0[2] = {0, 0};
+    if (q0 < n0l) {
+        e0 = l0[q0];
+        k0[0] = e0;
+        k0[1] = e0 == 0 ? 0 : a0.n - e0;
+    }
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int q2 = q20 + r;
+        if (q0 >= n0l || q2 >= n2l) continue;
+        const int e2 = l2[q2];
+        const int k2[2] = {e2, e2 == 0 ? 0 : a2.n - e2};
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const int i0 = a0.idx[k0[side]], i2 = a2.idx[k2[side]];
+            float2 g = make_float2(0.f, 0.f);
+            if (i0 >= 0 && id1[side] >= 0 && i2 >= 0) {
+                const float sc = sc1[side] * a0.scale[k0[side]] * a2.scale[k2[side]];
+                const float2 x = src[(int64_t)i0 + (int64_t)id1[side] * a1.sstride +
+                                     (int64_t)i2 * a2.sstride];
+                g = make_float2(x.x * sc, x.y * sc);
+            }
+            tile[side][r][tx] = g;
+        }
+    }
+    __syncthreads();
+    // store: tx along axis 2, conj(P[e]) + P[-e], halved
+    const int q2 = q20 + tx;
+    if (q2 >= n2l) return;
+    const int e2 = l2[q2];
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int qq0 = q00 + r;
+        if (qq0 >= n0l) break;
+        const float2 v0 = tile[0][tx][r], v1 = tile[1][tx][r];
+        dst[((size_t)l0[qq0] * a1.n + e1) * h2 + e2] =
+            make_float2(0.5f * (v0.x + v1.x), 0.5f * (v1.y - v0.y));
+    }
+}
+
 __global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __restrict__ dst,
                                    RemapAxis a0, RemapAxis a1, RemapAxis a2,
                                    const int* __restrict__ l0, const int* __restrict__ l1,

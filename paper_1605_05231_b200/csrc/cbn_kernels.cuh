@@ -320,6 +320,10 @@ __global__ void k_remap_list3(const SrcT* __restrict__ src, void* __restrict__ d
     else static_cast<float2*>(dst)[doff] = v;
 }
 
+__global__ void k_remap_herm3_tile(const float2* __restrict__ src, float2* __restrict__ dst,
+                                   RemapAxis a0, RemapAxis a1, RemapAxis a2,
+                                   const int* __restrict__ l0, const int* __restrict__ l1,
+                                   const int* __restrict__ l2, int n0l, int n2l, float gain);
 __global__ void k_remap_herm3_list(const float2* __restrict__ src, float2* __restrict__ dst,
                                    RemapAxis a0, RemapAxis a1, RemapAxis a2,
                                    const int* __restrict__ l0, const int* __restrict__ l1,

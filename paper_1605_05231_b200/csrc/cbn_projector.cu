@@ -1149,7 +1149,15 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
             StageScope st(p->timer, "resample_pad", s);
             CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float2) * half, s));
             const int* l = p->fres_list.p;
-            k_remap_herm3_list<<<dim3((unsigned)((p->fres_nl[2] + 255) / 256), p->fres_nl[1],
+            if (rax[0].sstride == 1)   // phi-fast grid from the rho-fast padded lattice
+                k_remap_herm3_tile<<<dim3((unsigned)((p->fres_nl[2] + 31) / 32),
+                                          (unsigned)((p->fres_nl[0] + 31) / 32), p->fres_nl[1]),
+                                     dim3(32, 8), 0, s>>>(
+                    p->padded.p, p->big.p, rax[0], rax[1], rax[2], l, l + p->fres_nl[0],
+                    l + p->fres_nl[0] + p->fres_nl[1], p->fres_nl[0], p->fres_nl[2],
+                    (float)(1.0 / size));
+            else
+                k_remap_herm3_list<<<dim3((unsigned)((p->fres_nl[2] + 255) / 256), p->fres_nl[1],
                                       p->fres_nl[0]), 256, 0, s>>>(
                 p->padded.p, p->big.p, rax[0], rax[1], rax[2], l, l + p->fres_nl[0],
                 l + p->fres_nl[0] + p->fres_nl[1], p->fres_nl[2], (float)(1.0 / size));
