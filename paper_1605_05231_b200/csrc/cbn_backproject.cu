@@ -550,9 +550,9 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             ax[0].sstride = 1;
             ax[1].sstride = hphi;
             ax[2].sstride = (int64_t)rax[1].K * hphi;
-            dim3 grid((ax[2].n + 255) / 256, ax[1].n, ax[0].n);
-            k_remap_half_acc<<<grid, 256, 0, s>>>(p->big.p, acc, ax[0], ax[1], ax[2], rax[0].K,
-                                                  rax[1].K, rax[2].K);
+            dim3 grid((ax[2].n + 31) / 32, (ax[0].n + 31) / 32, ax[1].n);
+            k_remap_half_acc_tile<<<grid, dim3(32, 8), 0, s>>>(p->big.p, acc, ax[0], ax[1], ax[2],
+                                                             rax[0].K, rax[1].K, rax[2].K);
             CBN_LAUNCH_CHECK();
             return;
         }

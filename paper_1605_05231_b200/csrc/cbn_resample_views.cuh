@@ -99,40 +99,47 @@ __global__ void k_rs_col_fill(const RsTap<J>* __restrict__ taps, int64_t n, int 
 // acc[e] += gain * prod_d scale_d[e_d] * IFFT(g)[k], k_d = idx_d[e_d], from
 // F = the forward 3D FFT of the real grid g kept as the half spectrum along
 // axis 0 (phi; [rho][theta][phi/2+1], strides a_d.sstride): IFFT(g)[k] is
-// conj(F[k]) for k_0 <= K_0/2 and F[-k] otherwise.  Grid as k_remap<3>.
-static __global__ void k_remap_half_acc(const float2* __restrict__ F, float2* __restrict__ acc,
-                                        RemapAxis a0, RemapAxis a1, RemapAxis a2, int K0, int K1,
-                                        int K2) {
-    const int e2 = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e2 >= a2.n) return;
-    const int e0 = blockIdx.z, e1 = blockIdx.y;
-    int k0 = a0.idx[e0], k1 = a1.idx[e1], k2 = a2.idx[e2];
-    if (k0 < 0 || k1 < 0 || k2 < 0) return;
-    const float sc = a0.scale[e0] * a1.scale[e1] * a2.scale[e2];
-    float sg = -1.f;
-    if (k0 > K0 / 2) {
-        k0 = K0 - k0;
-        k1 = k1 ? K1 - k1 : 0;
-        k2 = k2 ? K2 - k2 : 0;
-        sg = 1.f;
+// conj(F[k]) for k_0 <= K_0/2 and F[-k] otherwise.  
+// Through 32 x 32 (axis 0 x axis 2) shared-memory tiles per axis-1 cell:
+// F's contiguous axis is 0 (phi), acc's is 2 (rho).  Grid
+// (ceil(a2.n / 32), ceil(a0.n / 32), a1.n), block (32, 8).
+static __global__ void k_remap_half_acc_tile(const float2* __restrict__ F, float2* __restrict__ acc,
+                                             RemapAxis a0, RemapAxis a1, RemapAxis a2, int K0,
+                                             int K1, int K2) {
+    __shared__ float2 tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int e00 = blockIdx.y * 32, e20 = blockIdx.x * 32, e1 = blockIdx.z;
+    const int k1c = a1.idx[e1];
+    const float s1 = a1.scale[e1];
+    const int e0 = e00 + tx;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int e2 = e20 + r;
+        if (e0 >= a0.n || e2 >= a2.n) continue;
+        int k0 = a0.idx[e0], k1 = k1c, k2 = a2.idx[e2];
+        float2 v = make_float2(0.f, 0.f);
+        if (k0 >= 0 && k1 >= 0 && k2 >= 0) {
+            const float sc = a0.scale[e0] * s1 * a2.scale[e2];
+            float sg = -1.f;
+            if (k0 > K0 / 2) {
+                k0 = K0 - k0;
+                k1 = k1 ? K1 - k1 : 0;
+                k2 = k2 ? K2 - k2 : 0;
+                sg = 1.f;
+            }
+            const float2 f = F[k0 * a0.sstride + k1 * a1.sstride + k2 * a2.sstride];
+            v = make_float2(sc * f.x, sg * sc * f.y);
+        }
+        tile[r][tx] = v;
     }
-    const float2 f = F[k0 * a0.sstride + k1 * a1.sstride + k2 * a2.sstride];
-    float2* d = acc + ((size_t)e0 * a1.n + e1) * a2.n + e2;
-    const float2 o = *d;
-    *d = make_float2(o.x + sc * f.x, o.y + sg * sc * f.y);
-}
-
-// used[k] = 1 for every axis-0 (rho) plane a valid target's taps touch
-template <int J>
-__global__ void k_rs_rho_used(const RsTap<J>* __restrict__ taps, int64_t n, int K0,
-                              int* __restrict__ used) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n || !taps[t].valid) return;
-    const int f = taps[t].f[0];
-#pragma unroll
-    for (int a = 0; a < J; ++a) {
-        const int k = f + a >= K0 ? f + a - K0 : f + a;
-        if (!used[k]) used[k] = 1;
+    __syncthreads();
+    const int e2 = e20 + tx;
+    if (e2 >= a2.n) return;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int ee0 = e00 + r;
+        if (ee0 >= a0.n) break;
+        float2* d = acc + ((size_t)ee0 * a1.n + e1) * a2.n + e2;
+        const float2 o = *d, v = tile[tx][r];
+        *d = make_float2(o.x + v.x, o.y + v.y);
     }
 }
 
