@@ -99,7 +99,7 @@ __global__ void k_rs_col_fill(const RsTap<J>* __restrict__ taps, int64_t n, int 
 // acc[e] += gain * prod_d scale_d[e_d] * IFFT(g)[k], k_d = idx_d[e_d], from
 // F = the forward 3D FFT of the real grid g kept as the half spectrum along
 // axis 0 (phi; [rho][theta][phi/2+1], strides a_d.sstride): IFFT(g)[k] is
-// conj(F[k]) for k_0 <= K_0/2 and F[-k] otherwise.  
+// conj(F[k]) for k_0 <= K_0/2 and F[-k] otherwise.
 // Through 32 x 32 (axis 0 x axis 2) shared-memory tiles per axis-1 cell:
 // F's contiguous axis is 0 (phi), acc's is 2 (rho).  Grid
 // (ceil(a2.n / 32), ceil(a0.n / 32), a1.n), block (32, 8).
@@ -140,6 +140,20 @@ static __global__ void k_remap_half_acc_tile(const float2* __restrict__ F, float
         float2* d = acc + ((size_t)ee0 * a1.n + e1) * a2.n + e2;
         const float2 o = *d, v = tile[tx][r];
         *d = make_float2(o.x + v.x, o.y + v.y);
+    }
+}
+
+// used[k] = 1 for every axis-0 (rho) plane a valid target's taps touch
+template <int J>
+__global__ void k_rs_rho_used(const RsTap<J>* __restrict__ taps, int64_t n, int K0,
+                              int* __restrict__ used) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n || !taps[t].valid) return;
+    const int f = taps[t].f[0];
+#pragma unroll
+    for (int a = 0; a < J; ++a) {
+        const int k = f + a >= K0 ? f + a - K0 : f + a;
+        if (!used[k]) used[k] = 1;
     }
 }
 
