@@ -23,6 +23,8 @@
 // the thread-per-point gather read 16 distinct bank pairs at every tap.
 #pragma once
 
+#include <type_traits>
+
 #include "cbn_kernels.cuh"
 
 namespace cbn {
@@ -79,6 +81,20 @@ __global__ void k_bin_keys(Src src, KBSet kb, TileGeom<D> tg, int64_t m, int* __
 
 __global__ void k_bin_scatter(const int* __restrict__ keys, int64_t m, int* __restrict__ cursor,
                               int* __restrict__ perm);
+
+// Sources that keep their coordinates in bin-sorted order expose
+// node_at(pos, i, ...) (pos = sorted position, i = original index); the binned
+// kernels prefer it, so coordinates stream instead of gathering by perm.
+template <class Src, class = void>
+struct has_node_at : std::false_type {};
+template <class Src>
+struct has_node_at<Src, std::void_t<decltype(&Src::node_at)>> : std::true_type {};
+
+template <class Src, int D>
+CBN_D void src_node(const Src& src, int64_t pos, int64_t i, double (&w)[D], typename Src::Aux& a) {
+    if constexpr (has_node_at<Src>::value) src.node_at(pos, i, w, a);
+    else src.node(i, w, a);
+}
 
 // ---------------------------------------------------------------- gather
 // HALF (3D): `grid` is the [K0][K1][K2/2+1] half spectrum of a real input
@@ -143,7 +159,7 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
         const int64_t i = perm[sp.start + k];
         double w[D];
         typename Src::Aux aux;
-        src.node(i, w, aux);
+        src_node(src, sp.start + k, i, w, aux);
         int first[D];
         float wt[D][J];
         tap_setup<D, J>(kb, w, first, wt);
@@ -224,7 +240,7 @@ k_spread_binned(float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src,
             const int64_t i = perm[sp.start + k];
             double w[D];
             typename Src::Aux aux;
-            src.node(i, w, aux);
+            src_node(src, sp.start + k, i, w, aux);
             v = src.value(i, w, aux);
             int first[D];
             float wt[D][J];
@@ -357,7 +373,7 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const int64_t i = perm[sp.start + k];
             double w[3];
             typename Src::Aux aux;
-            src.node(i, w, aux);
+            src_node(src, sp.start + k, i, w, aux);
             const float2 v = src.value(i, w, aux);
             int first[3];
             float wt[3][J];
@@ -447,7 +463,7 @@ k_spread_owned8(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const int64_t i = perm[sp.start + k];
             double w[3];
             typename Src::Aux aux;
-            src.node(i, w, aux);
+            src_node(src, sp.start + k, i, w, aux);
             const float2 v = src.value(i, w, aux);
             int first[3];
             float wt[3][J];

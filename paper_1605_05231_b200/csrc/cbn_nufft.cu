@@ -18,6 +18,7 @@ template <int D>
 struct ExplicitSrc {
     const double* nodes64;  // wrapped, m x D (or null)
     const float* nodes32;   // caller's float32 values, m x D, wrapped here (or null)
+    const float* sorted32 = nullptr;   // nodes32 in the plan's bin order (or null)
     struct Aux {};
     CBN_D void node(int64_t i, double (&w)[D], Aux&) const {
         if (nodes64) {
@@ -28,7 +29,25 @@ struct ExplicitSrc {
             for (int d = 0; d < D; ++d) w[d] = wrap_pi((double)nodes32[i * D + d]);
         }
     }
+    // binned kernels: sorted position pos of original node i
+    CBN_D void node_at(int64_t pos, int64_t i, double (&w)[D], Aux& a) const {
+        if (sorted32) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) w[d] = wrap_pi((double)sorted32[pos * D + d]);
+        } else {
+            node(i, w, a);
+        }
+    }
 };
+
+// sorted[pos] = nodes[perm[pos]] (D floats per node)
+__global__ void k_sort_nodes(const float* __restrict__ nodes, const int* __restrict__ perm,
+                             int64_t m, int D, float* __restrict__ sorted) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= m) return;
+    const int64_t i = perm[q];
+    for (int d = 0; d < D; ++d) sorted[q * D + d] = nodes[i * D + d];
+}
 
 // plan.phase = exp(-i w . (N//2))  (nufft.py:215-216), angle in float64
 template <int D>
@@ -96,6 +115,7 @@ struct cbn_nufft_s {
     KBSet kb{};
     DevBuf<double> nodes;      // wrapped float64 nodes, or
     DevBuf<float> nodes32;     // float32 nodes (wrapped on the fly)
+    DevBuf<float> sorted32;    // float32 nodes in bin order (2D / 3D float32 plans)
     DevBuf<float> s32;         // D x smax
     DevBuf<int> pad_idx, crop_idx;
     DevBuf<float> pad_sc, crop_sc;
@@ -108,7 +128,8 @@ struct cbn_nufft_s {
     double centre[kMaxDim] = {0, 0, 0};
     template <int D_>
     ExplicitSrc<D_> src() const {
-        return ExplicitSrc<D_>{nodes.p, nodes.p ? nullptr : nodes32.p};
+        return ExplicitSrc<D_>{nodes.p, nodes.p ? nullptr : nodes32.p,
+                               nodes.p ? nullptr : sorted32.p};
     }
 };
 
@@ -224,6 +245,14 @@ void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t
             build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true);
             return 0;
         });
+        if (!p->nodes.p) {
+            // float32 nodes: a bin-ordered copy, so the gather / spread stream
+            // their coordinates (the caller's order is kept for the rest)
+            p->sorted32.alloc((size_t)p->m * D);
+            k_sort_nodes<<<blocks_for(p->m, 256), 256, 0, s>>>(p->nodes32.p, p->bins.perm.p, p->m,
+                                                               D, p->sorted32.p);
+            CBN_LAUNCH_CHECK();
+        }
     }
     CBN_CUDA(cudaStreamSynchronize(s));   // rows / host scaling copy must outlive the launch
 }
