@@ -51,19 +51,29 @@ CBN_D int pad_src(int g, int N, int K) {
 }
 
 // h = frame * w1 ; y = h * scaling placed at rolled positions (nufft.py:226-230)
+template <int V>   // cells per thread: 4 (Kv % 4 == 0, one 16-byte store) or 1
 __global__ void k_grf_pad(const float* __restrict__ frames, int nu, int nv, int Ku, int Kv,
                           const float* __restrict__ pix, float* __restrict__ grids) {
-    // grid (Kv / 256, Ku, views): one padded row per (blockIdx.y, blockIdx.z)
-    const int gv = blockIdx.x * blockDim.x + threadIdx.x;
+    // grid (Kv / (256 V), Ku, views): one padded row per (blockIdx.y, blockIdx.z)
+    const int gv = V * (blockIdx.x * blockDim.x + threadIdx.x);
     if (gv >= Kv) return;
     const int gu = blockIdx.y, v = blockIdx.z;
-    const int nu_i = pad_src(gu, nu, Ku), nv_i = pad_src(gv, nv, Kv);
-    float out = 0.f;
-    if (nu_i >= 0 && nv_i >= 0) {
-        const size_t px = (size_t)nu_i * nv + nv_i;
-        out = frames[(size_t)v * nu * nv + px] * pix[px];
+    const int nu_i = pad_src(gu, nu, Ku);
+    float o[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) o[q] = 0.f;
+    if (nu_i >= 0) {
+        const float* fr = frames + ((size_t)v * nu + nu_i) * nv;
+        const float* px = pix + (size_t)nu_i * nv;
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const int nv_i = pad_src(gv + q, nv, Kv);
+            if (nv_i >= 0) o[q] = fr[nv_i] * px[nv_i];
+        }
     }
-    grids[((size_t)v * Ku + gu) * Kv + gv] = out;
+    float* dst = grids + ((size_t)v * Ku + gu) * Kv + gv;
+    if constexpr (V == 4) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+    else dst[0] = o[0];
 }
 
 // values = Re(fftshift(ifft)) / dt * w2   (grangeat.py:144-145)
@@ -296,8 +306,12 @@ void grangeat_forward_block(cbn_projector_s* p, const float* frames, int nb, flo
     float* padded = reinterpret_cast<float*>(B.tv.p);
     const int64_t gtot = (int64_t)nb * Ku * Kv;
     projector_gr_pix(p, gp, false, s);
-    k_grf_pad<<<dim3((unsigned)((Kv + 255) / 256), Ku, nb), 256, 0, s>>>(frames, nu, nv, Ku, Kv,
-                                                                      gp.pix.p, padded);
+    if (Kv % 4 == 0)
+        k_grf_pad<4><<<dim3((unsigned)((Kv / 4 + 255) / 256), Ku, nb), 256, 0, s>>>(
+            frames, nu, nv, Ku, Kv, gp.pix.p, padded);
+    else
+        k_grf_pad<1><<<dim3((unsigned)((Kv + 255) / 256), Ku, nb), 256, 0, s>>>(
+            frames, nu, nv, Ku, Kv, gp.pix.p, padded);
     (void)gtot;
     CBN_LAUNCH_CHECK();
     long long kd[2] = {Ku, Kv};
