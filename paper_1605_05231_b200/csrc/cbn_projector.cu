@@ -1097,6 +1097,11 @@ void ensure_batch_plan(P* p, BatchPlan& bp, const UmbrellaTables& u, const Radia
 bool views_in_lanes(const P* p);
 
 // the resample grid is kept as Re(G) only (C2R) on the views-in-lanes J = 3 path
+bool rho_lines_off() {   // CBN_RHO_LINES=0: the strided rho pass on the half spectrum (A/B)
+    const char* e = std::getenv("CBN_RHO_LINES");
+    return e && e[0] == '0';
+}
+
 bool real_grid(const P* p) {
     const char* off = std::getenv("CBN_COMPLEX_GRID");
     if (off && off[0] == '1') return false;
@@ -1104,6 +1109,63 @@ bool real_grid(const P* p) {
 }
 
 void ensure_lane_taps(P* p, cudaStream_t s);
+
+// Resample grid, rho lines first (phi-fast real grid): the padded, scaled
+// lattice spectrum v on the (theta, phi) pad positions with their mirrors as
+// contiguous rho lines [phi_i][theta_i][K_rho] (zero outside the rho pad) ...
+__global__ void k_rho_lines_pad(const float2* __restrict__ src, RemapAxis ar, RemapAxis at,
+                                RemapAxis ap, const int* __restrict__ lth,
+                                const int* __restrict__ lph, int nth, float gain,
+                                float2* __restrict__ lines) {
+    const int kr = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kr >= ar.n) return;
+    const int it = blockIdx.y, ip = blockIdx.z;
+    const int kt = lth[it], kp = lph[ip];
+    const int i0 = ar.idx[kr], i1 = at.idx[kt], i2 = ap.idx[kp];
+    float2 v = make_float2(0.f, 0.f);
+    if (i0 >= 0 && i1 >= 0 && i2 >= 0) {
+        const float sc = gain * ar.scale[kr] * at.scale[kt] * ap.scale[kp];
+        const float2 g = src[(int64_t)i0 * ar.sstride + (int64_t)i1 * at.sstride +
+                             (int64_t)i2 * ap.sstride];
+        v = make_float2(g.x * sc, g.y * sc);
+    }
+    lines[((size_t)ip * nth + it) * ar.n + kr] = v;
+}
+
+// ... forward FFT F along rho, then the half spectrum of the used rho planes x:
+// H[x][kt][kp] = (conj F(x, kt, kp) + F(x, -kt, -kp)) / 2, kp <= K_phi / 2
+// (= the inverse rho FFT of the Hermitian part), through 32 x 32 tiles per kt.
+// Grid (ceil(H / 32), ceil(nx / 32), K_theta), block (32, 8).
+__global__ void k_rho_lines_herm(const float2* __restrict__ F, const int* __restrict__ xs, int nx,
+                                 const int* __restrict__ thmap, const int* __restrict__ phmap,
+                                 int nth, int Kr, int Kt, int Kp, float2* __restrict__ dst) {
+    __shared__ float2 tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int qx0 = blockIdx.y * 32, kp0 = blockIdx.x * 32, kt = blockIdx.z;
+    const int hp = Kp / 2 + 1;
+    const int ktm = kt ? Kt - kt : 0;
+    const int ith = thmap[kt], ithm = thmap[ktm];
+    const int qx = qx0 + tx;
+    const int x = qx < nx ? xs[qx] : 0;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int kp = kp0 + r;
+        if (qx >= nx || kp >= hp) continue;
+        const int kpm = kp ? Kp - kp : 0;
+        const int iph = phmap[kp], iphm = phmap[kpm];
+        float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+        if (ith >= 0 && iph >= 0) a = F[((size_t)iph * nth + ith) * Kr + x];
+        if (ithm >= 0 && iphm >= 0) b = F[((size_t)iphm * nth + ithm) * Kr + x];
+        tile[r][tx] = make_float2(0.5f * (a.x + b.x), 0.5f * (b.y - a.y));
+    }
+    __syncthreads();
+    const int kp = kp0 + tx;
+    if (kp >= hp) return;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int q = qx0 + r;
+        if (q >= nx) break;
+        dst[((size_t)xs[q] * Kt + kt) * hp + kp] = tile[tx][r];
+    }
+}
 
 void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool phi_fast = false) {
     const RadialTables& r = p->frad;
@@ -1143,6 +1205,60 @@ void build_resample_grid(P* p, const float* s32b, int smax, cudaStream_t s, bool
             }
             p->fres_list.upload(all.data(), all.size(), s);
             CBN_CUDA(cudaStreamSynchronize(s));
+        }
+        if (rax[0].sstride == 1 && !rho_lines_off()) {
+            // rho lines first: contiguous forward FFTs along rho on the (theta,
+            // phi) pad positions, then the half spectrum of the used rho planes
+            if (!p->fres_lth.p) {
+                const std::vector<int> lth = pad_positions(ax[1].N, ax[1].K, true, false);
+                const AxisPlan& aph = phi_fast ? ax[0] : ax[2];
+                const std::vector<int> lph = pad_positions(aph.N, aph.K, true, false);
+                std::vector<int> thmap((size_t)ax[1].K, -1), phmap((size_t)aph.K, -1), xs;
+                for (size_t q = 0; q < lth.size(); ++q) thmap[(size_t)lth[q]] = (int)q;
+                for (size_t q = 0; q < lph.size(); ++q) phmap[(size_t)lph[q]] = (int)q;
+                for (const auto& rn : p->fres_rho_runs)
+                    for (int x = rn.first; x < rn.second; ++x) xs.push_back(x);
+                p->fres_nth = (int)lth.size();
+                p->fres_nph = (int)lph.size();
+                p->fres_nx = (int)xs.size();
+                p->fres_lth.upload(lth.data(), lth.size(), s);
+                p->fres_lph.upload(lph.data(), lph.size(), s);
+                p->fres_thmap.upload(thmap.data(), thmap.size(), s);
+                p->fres_phmap.upload(phmap.data(), phmap.size(), s);
+                p->fres_xs.upload(xs.data(), std::max<size_t>(xs.size(), 1), s);
+                CBN_CUDA(cudaStreamSynchronize(s));
+            }
+            const int Kr = (int)kd3[0], Kt = (int)kd3[1], Kp = (int)kd3[2];
+            const int64_t nlines = (int64_t)p->fres_nth * p->fres_nph;
+            p->rlines.ensure((size_t)nlines * Kr);
+            {
+                StageScope st(p->timer, "resample_pad", s);
+                k_rho_lines_pad<<<dim3((unsigned)((Kr + 255) / 256), p->fres_nth, p->fres_nph), 256,
+                                  0, s>>>(p->padded.p, rax[0], rax[1], rax[2], p->fres_lth.p,
+                                          p->fres_lph.p, p->fres_nth, (float)(1.0 / size),
+                                          p->rlines.p);
+                CBN_LAUNCH_CHECK();
+            }
+            StageScope st(p->timer, "resample_fft", s);
+            long long kr1[1] = {Kr};
+            p->fft.exec(p->fft.get(1, kr1, nlines), p->rlines.p, p->rlines.p, CUFFT_FORWARD, s);
+            const int hp = Kp / 2 + 1;
+            if (p->fres_nx > 0) {
+                k_rho_lines_herm<<<dim3((unsigned)((hp + 31) / 32),
+                                        (unsigned)((p->fres_nx + 31) / 32), Kt),
+                                   dim3(32, 8), 0, s>>>(p->rlines.p, p->fres_xs.p, p->fres_nx,
+                                                        p->fres_thmap.p, p->fres_phmap.p,
+                                                        p->fres_nth, Kr, Kt, Kp, p->big.p);
+                CBN_LAUNCH_CHECK();
+            }
+            const long long k2[2] = {Kt, Kp};
+            const long long plane = (long long)Kt * hp, rplane = (long long)Kt * Kp;
+            float* re = reinterpret_cast<float*>(p->big.p + half);
+            for (const auto& rn : p->fres_rho_runs)
+                p->fft.exec_c2r(p->fft.get_c2r2(k2, rn.second - rn.first),
+                                p->big.p + (size_t)rn.first * plane, re + rn.first * rplane, s);
+            p->grid_re = re;
+            return;
         }
         {
             // zero the half spectrum, then fill only the cells P or its mirror reaches

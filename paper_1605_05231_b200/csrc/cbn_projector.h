@@ -126,6 +126,11 @@ struct cbn_projector_s {
     int fspec_nl[3] = {0, 0, 0}, fres_nl[3] = {0, 0, 0};
     // rho planes of the (views-in-lanes) resample grid the umbrella taps read
     std::vector<std::pair<int, int>> fres_rho_runs;
+    // resample grid built rho-lines first: (theta, phi) pad positions with
+    // mirrors, their inverse maps, the used rho planes, the line buffer
+    cbn::DevBuf<int> fres_lth, fres_lph, fres_thmap, fres_phmap, fres_xs;
+    int fres_nth = 0, fres_nph = 0, fres_nx = 0;
+    cbn::DevBuf<float2> rlines;
     // backprojector: rho planes of the transposed grid with column entries, and
     // a per-plane flag for the column gather
     std::vector<std::pair<int, int>> bres_rho_runs;
