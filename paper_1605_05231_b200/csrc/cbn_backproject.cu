@@ -456,6 +456,11 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
     return x;
 }
 
+bool rho_lines_off_bp() {   // CBN_RHO_LINES=0: the strided rho pass (A/B)
+    const char* e = std::getenv("CBN_RHO_LINES");
+    return e && e[0] == '0';
+}
+
 // transposed resample of views [lo, hi) accumulated into acc (dsize complex,
 // zeroed here): the values of `frames` (views lo..hi-1), or -- den_only -- the
 // validity mask of the same views (resample_transpose(valid), pipeline.py:184)
@@ -550,17 +555,63 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 if (lo < rax[2].K)
                     CBN_CUDA(cudaMemsetAsync(p->big.p + lo * hplane, 0,
                                              sizeof(float2) * hplane * (rax[2].K - lo), s));
-                // along rho only the theta columns the crop reads (the crop
-                // table's distinct theta cells, in runs)
-                const long long plane = (long long)rax[1].K * hphi;
-                for (const auto& rn : bres_theta_runs) {
-                    float2* at = p->big.p + (size_t)rn.first * hphi;
-                    p->fft.exec(p->fft.get_strided(rax[2].K, (long long)(rn.second - rn.first) * hphi,
-                                                   plane, 1),
-                                at, at, CUFFT_FORWARD, s);
+                if (!rho_lines_off_bp()) {
+                    // the (theta, phi-half) columns the crop reads, as contiguous
+                    // rho lines; forward FFT along rho; the crop reads the lines
+                    if (!p->bres_lth.p) {
+                        const std::vector<int> lth = pad_positions(rax[1].N, rax[1].K, true, false);
+                        std::vector<char> onp((size_t)hphi, 0);
+                        for (int k : pad_positions(rax[0].N, rax[0].K, false, false))
+                            onp[(size_t)(k <= rax[0].K / 2 ? k : rax[0].K - k)] = 1;
+                        std::vector<int> lph, thmap((size_t)rax[1].K, 0), phmap((size_t)hphi, 0);
+                        for (int k = 0; k < (int)hphi; ++k)
+                            if (onp[(size_t)k]) {
+                                phmap[(size_t)k] = (int)lph.size();
+                                lph.push_back(k);
+                            }
+                        for (size_t q = 0; q < lth.size(); ++q) thmap[(size_t)lth[q]] = (int)q;
+                        p->bres_nth = (int)lth.size();
+                        p->bres_nph = (int)lph.size();
+                        p->bres_lth.upload(lth.data(), lth.size(), s);
+                        p->bres_lph.upload(lph.data(), lph.size(), s);
+                        p->bres_thmap.upload(thmap.data(), thmap.size(), s);
+                        p->bres_phmap.upload(phmap.data(), phmap.size(), s);
+                        CBN_CUDA(cudaStreamSynchronize(s));
+                    }
+                    const int Kr = rax[2].K;
+                    const int64_t nlines = (int64_t)p->bres_nth * p->bres_nph;
+                    p->brlines.ensure((size_t)nlines * Kr);
+                    k_lines_from_half<<<dim3((unsigned)((Kr + 31) / 32),
+                                             (unsigned)((p->bres_nph + 31) / 32), p->bres_nth),
+                                        dim3(32, 8), 0, s>>>(
+                        p->big.p, p->bres_rho_used.p, p->bres_lth.p, p->bres_lph.p, p->bres_nth,
+                        p->bres_nph, Kr, rax[1].K, (int)hphi, p->brlines.p);
+                    CBN_LAUNCH_CHECK();
+                    long long kr1[1] = {Kr};
+                    p->fft.exec(p->fft.get(1, kr1, nlines), p->brlines.p, p->brlines.p,
+                                CUFFT_FORWARD, s);
+                } else {
+                    // along rho only the theta columns the crop reads (the crop
+                    // table's distinct theta cells, in runs)
+                    const long long plane = (long long)rax[1].K * hphi;
+                    for (const auto& rn : bres_theta_runs) {
+                        float2* at = p->big.p + (size_t)rn.first * hphi;
+                        p->fft.exec(p->fft.get_strided(rax[2].K,
+                                                       (long long)(rn.second - rn.first) * hphi,
+                                                       plane, 1),
+                                    at, at, CUFFT_FORWARD, s);
+                    }
                 }
             }
             StageScope st(p->timer, "transpose_crop", s);
+            if (!rho_lines_off_bp()) {
+                k_crop_from_lines<<<dim3((unsigned)((ax[2].n + 255) / 256), ax[1].n, ax[0].n), 256, 0,
+                                    s>>>(p->brlines.p, ax[0], ax[1], ax[2], p->bres_thmap.p,
+                                         p->bres_phmap.p, p->bres_nth, rax[0].K, rax[1].K,
+                                         rax[2].K, acc);
+                CBN_LAUNCH_CHECK();
+                return;
+            }
             ax[0].sstride = 1;
             ax[1].sstride = hphi;
             ax[2].sstride = (int64_t)rax[1].K * hphi;

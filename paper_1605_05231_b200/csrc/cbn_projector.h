@@ -135,6 +135,11 @@ struct cbn_projector_s {
     // a per-plane flag for the column gather
     std::vector<std::pair<int, int>> bres_rho_runs;
     cbn::DevBuf<unsigned char> bres_rho_used;
+    // rho lines of the transposed grid's spectrum the crop reads: theta and
+    // phi-half positions, their inverse maps, the line buffer
+    cbn::DevBuf<int> bres_lth, bres_lph, bres_thmap, bres_phmap;
+    int bres_nth = 0, bres_nph = 0;
+    cbn::DevBuf<float2> brlines;
     int64_t fpairs_n = 0;
     bool fspec_fit = false;
     cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT

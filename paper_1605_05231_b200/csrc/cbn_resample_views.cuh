@@ -143,6 +143,63 @@ static __global__ void k_remap_half_acc_tile(const float2* __restrict__ F, float
     }
 }
 
+// rho lines from the half spectrum G [K_rho][K_theta][K_phi/2+1] of the used
+// rho planes (others read as zero): lines[(iph * nth + ith) * K_rho + x] =
+// G[x][lth[ith]][lph[iph]], through 32 x 32 tiles per ith.  Grid
+// (ceil(K_rho / 32), ceil(nph / 32), nth), block (32, 8).
+static __global__ void k_lines_from_half(const float2* __restrict__ G,
+                                         const unsigned char* __restrict__ used,
+                                         const int* __restrict__ lth, const int* __restrict__ lph,
+                                         int nth, int nph, int Kr, int Kt, int hp,
+                                         float2* __restrict__ lines) {
+    __shared__ float2 tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int x0 = blockIdx.x * 32, ip0 = blockIdx.y * 32, it = blockIdx.z;
+    const int kt = lth[it];
+    const int ip = ip0 + tx;
+    const int kp = ip < nph ? lph[ip] : 0;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int x = x0 + r;
+        if (x >= Kr || ip >= nph) continue;
+        tile[r][tx] = used[x] ? G[((size_t)x * Kt + kt) * hp + kp] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    const int x = x0 + tx;
+    if (x >= Kr) return;
+    for (int r = ty; r < 32; r += blockDim.y) {
+        const int q = ip0 + r;
+        if (q >= nph) break;
+        lines[((size_t)q * nth + it) * Kr + x] = tile[tx][r];
+    }
+}
+
+// the transposed-resample crop from the rho lines F (forward FFT along rho):
+// acc[e0][e1][e2] += s0 s1 s2 * IFFT(g)[k] with k_d = idx_d[e_d] (phi, theta,
+// rho), IFFT(g)[k] = conj F(k0, k1; k2) for k0 <= K0/2, else F(-k0, -k1; -k2).
+// Grid (ceil(a2.n / 256), a1.n, a0.n).
+static __global__ void k_crop_from_lines(const float2* __restrict__ F, RemapAxis a0, RemapAxis a1,
+                                         RemapAxis a2, const int* __restrict__ thmap,
+                                         const int* __restrict__ phmap, int nth, int K0, int K1,
+                                         int K2, float2* __restrict__ acc) {
+    const int e2 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e2 >= a2.n) return;
+    const int e0 = blockIdx.z, e1 = blockIdx.y;
+    int k0 = a0.idx[e0], k1 = a1.idx[e1], k2 = a2.idx[e2];
+    if (k0 < 0 || k1 < 0 || k2 < 0) return;
+    const float sc = a0.scale[e0] * a1.scale[e1] * a2.scale[e2];
+    float sg = -1.f;
+    if (k0 > K0 / 2) {
+        k0 = K0 - k0;
+        k1 = k1 ? K1 - k1 : 0;
+        k2 = k2 ? K2 - k2 : 0;
+        sg = 1.f;
+    }
+    const float2 f = F[((size_t)phmap[k0] * nth + thmap[k1]) * K2 + k2];
+    float2* d = acc + ((size_t)e0 * a1.n + e1) * a2.n + e2;
+    const float2 o = *d;
+    *d = make_float2(o.x + sc * f.x, o.y + sg * sc * f.y);
+}
+
 // used[k] = 1 for every axis-0 (rho) plane a valid target's taps touch
 template <int J>
 __global__ void k_rs_rho_used(const RsTap<J>* __restrict__ taps, int64_t n, int K0,
