@@ -543,16 +543,19 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                 const long long k2[2] = {rax[1].K, rax[0].K};
                 const long long hplane = (long long)rax[1].K * hphi;
                 const long long rplane = (long long)rax[1].K * rax[0].K;
+                // (the rho-lines extract reads unused planes as zero; the strided
+                // pass needs them zeroed)
+                const bool zero_unused = rho_lines_off_bp();
                 int lo = 0;
                 for (const auto& rn : p->bres_rho_runs) {
-                    if (rn.first > lo)
+                    if (rn.first > lo && zero_unused)
                         CBN_CUDA(cudaMemsetAsync(p->big.p + lo * hplane, 0,
                                                  sizeof(float2) * hplane * (rn.first - lo), s));
                     p->fft.exec_r2c3(p->fft.get_r2c2(k2, rn.second - rn.first),
                                      greal + rn.first * rplane, p->big.p + rn.first * hplane, s);
                     lo = rn.second;
                 }
-                if (lo < rax[2].K)
+                if (lo < rax[2].K && zero_unused)
                     CBN_CUDA(cudaMemsetAsync(p->big.p + lo * hplane, 0,
                                              sizeof(float2) * hplane * (rax[2].K - lo), s));
                 if (!rho_lines_off_bp()) {
