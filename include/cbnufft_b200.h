@@ -243,7 +243,9 @@ int cbn_projector_grangeat_forward(cbn_projector* proj, const float* frames, flo
                                    int32_t n_views_blk, void* stream);
 
 /* Per-stage CUDA-event timing: enable (1) / disable (0); when enabled every
- * operator call records events per stage.  stage_times synchronises and
+ * operator call records events per stage, and the operators run their view
+ * blocks on the caller's stream only (no second overlapping stream), so each
+ * stage's event time is its kernels' own time.  stage_times synchronises and
  * returns the accumulated milliseconds per stage since the last reset
  * (names: ';'-separated), then resets if `reset` is non-zero. */
 int cbn_projector_set_timing(cbn_projector* proj, int32_t on);

@@ -477,7 +477,7 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
     // blocks of 32 views alternate between the caller's stream and s1
     // out: [view][n_mu][n_t] values; or (outT) target-major [target][nb]
     auto forward_grangeat = [&](int v0, int nb, float* out, float* outT = nullptr) {
-        const bool dual = nb > 32 && lanes_allowed();
+        const bool dual = nb > 32 && lanes_allowed() && !p->timer.on;
         if (dual) {
             // plan state both lanes read, then fork
             GrangeatPlan& gp = p->bgr;

@@ -1674,7 +1674,7 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
     const bool lanes = views_in_lanes(p);
     // two lanes (the caller's stream and s1) alternate over view blocks so one
     // block's Grangeat FFTs overlap the next block's resample gather
-    const bool dual = lanes && !values_out && lanes_allowed();
+    const bool dual = lanes && !values_out && lanes_allowed() && !p->timer.on;
     if (dual) ensure_lane1(p);
     if (dual) {
         p->lane1.values.ensure((size_t)per_view * kViewBlock);
