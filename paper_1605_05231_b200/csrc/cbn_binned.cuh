@@ -390,6 +390,53 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
         }
         __syncthreads();
         const int npts = min(NP, sp.count - base);
+        if constexpr (J == 6 && W == 2) {
+            // J = 6, two warps, three rows each: lane = tap pair (b, c) =
+            // (lane / 6, lane % 6) of pq = lane < 32, fixed over the three
+            // rows, so wy * wz is formed once per point and each row costs
+            // one broadcast x weight; the 4 left-over pairs of each row
+            // (b = 5, c = 2..5) go to lanes 0..11 of a fourth pass
+            const int fb = lane / 6, fc = lane % 6;
+            const int f_off = fb * P + fc;
+            const int lr = lane >> 2, lc = 2 + (lane & 3);
+            const int l_off = lr * W * row_stride + 5 * P + lc;
+            for (int j = 0; j < npts; ++j) {
+                const float2 v = stv[j];
+                if (v.x == 0.f && v.y == 0.f) continue;     // uniform over the CTA
+                const int pl = stl[j];
+                const int l0 = pl >> 24;
+                const float* ws = stw + j * SW;
+                const int a0 = (warp - l0) & 1;
+                float2* base_row = reg + (pl & 0xffffff) + a0 * row_stride;
+                const float wyz = ws[J + fb] * ws[2 * J + fc];
+                float wl = 0.f;
+                if (lane < 12) wl = ws[a0 + lr * W] * ws[J + 5] * ws[2 * J + lc];
+                // the four cells are distinct: all loads issue before any store
+                float2* cell[4];
+                float2 cur[4];
+                float wk[4];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    cell[r] = base_row + r * W * row_stride + f_off;
+                    wk[r] = ws[a0 + r * W] * wyz;
+                }
+                cell[3] = base_row + l_off;
+                wk[3] = wl;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) cur[r] = *cell[r];
+                if (lane < 12) cur[3] = *cell[3];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    cur[r].x = fmaf(wk[r], v.x, cur[r].x);
+                    cur[r].y = fmaf(wk[r], v.y, cur[r].y);
+                }
+#pragma unroll
+                for (int r = 0; r < 3; ++r) *cell[r] = cur[r];
+                if (lane < 12) *cell[3] = cur[3];
+                __syncwarp();
+            }
+            continue;
+        }
         for (int j = 0; j < npts; ++j) {
             const float2 v = stv[j];
             if (v.x == 0.f && v.y == 0.f) continue;     // uniform over the CTA
