@@ -390,6 +390,40 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
         }
         __syncthreads();
         const int npts = min(NP, sp.count - base);
+        if constexpr (J == 8 && W == 4) {
+            // J = 8, four warps, two rows each: lane = tap pairs (b, c) and
+            // (b + 4, c), b = lane / 8, c = lane % 8, fixed over both rows, so
+            // wy * wz is formed once per point and each row costs one
+            // broadcast x weight; all four cell loads issue before the stores
+            const int fb = lane >> 3, fc = lane & 7;
+            const int off0 = fb * P + fc, off1 = (fb + 4) * P + fc;
+            for (int j = 0; j < npts; ++j) {
+                const float2 v = stv[j];
+                if (v.x == 0.f && v.y == 0.f) continue;     // uniform over the CTA
+                const int pl = stl[j];
+                const int l0 = pl >> 24;
+                const float* ws = stw + j * SW;
+                const int a0 = (warp - l0) & 3;
+                float2* row0 = reg + (pl & 0xffffff) + a0 * row_stride;
+                float2* row1 = row0 + W * row_stride;
+                const float wz = ws[2 * J + fc];
+                const float wyz0 = ws[J + fb] * wz, wyz1 = ws[J + fb + 4] * wz;
+                const float wx0 = ws[a0], wx1 = ws[a0 + W];
+                float2 cur[4] = {row0[off0], row0[off1], row1[off0], row1[off1]};
+                const float wk[4] = {wx0 * wyz0, wx0 * wyz1, wx1 * wyz0, wx1 * wyz1};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    cur[r].x = fmaf(wk[r], v.x, cur[r].x);
+                    cur[r].y = fmaf(wk[r], v.y, cur[r].y);
+                }
+                row0[off0] = cur[0];
+                row0[off1] = cur[1];
+                row1[off0] = cur[2];
+                row1[off1] = cur[3];
+                __syncwarp();
+            }
+            continue;
+        }
         if constexpr (J == 6 && W == 2) {
             // J = 6, two warps, three rows each: lane = tap pair (b, c) =
             // (lane / 6, lane % 6) of pq = lane < 32, fixed over the three
@@ -446,15 +480,22 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             int a0 = (W & (W - 1)) == 0 ? (warp - l0) & (W - 1) : ((warp - l0) % W + W) % W;
             const int nrows = J % W == 0 ? J / W : (a0 < J ? (J - 1 - a0) / W + 1 : 0);
             float2* base_row = reg + (pl & 0xffffff) + a0 * row_stride;
+            // a lane's cells are distinct: all loads issue before any store
+            float2 cur[ITERS];
+            float wk[ITERS];
 #pragma unroll
             for (int it = 0; it < ITERS; ++it) {
                 if (t_row[it] < nrows) {
-                    const float wk = ws[a0 + t_row[it] * W] * ws[t_wy[it]] * ws[t_wz[it]];
-                    float2* cell = base_row + t_off[it];
-                    float2 cur = *cell;
-                    cur.x = fmaf(wk, v.x, cur.x);
-                    cur.y = fmaf(wk, v.y, cur.y);
-                    *cell = cur;
+                    wk[it] = ws[a0 + t_row[it] * W] * ws[t_wy[it]] * ws[t_wz[it]];
+                    cur[it] = base_row[t_off[it]];
+                }
+            }
+#pragma unroll
+            for (int it = 0; it < ITERS; ++it) {
+                if (t_row[it] < nrows) {
+                    cur[it].x = fmaf(wk[it], v.x, cur[it].x);
+                    cur[it].y = fmaf(wk[it], v.y, cur[it].y);
+                    base_row[t_off[it]] = cur[it];
                 }
             }
             __syncwarp();
@@ -712,11 +753,12 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
 }
 
 // warps per CTA of the 3D owner-computes spread: rows per warp x J^2 taps
-// (measured on B200: J=8 -> 8 warps, 55 ms vs 64 ms at 4 on config 4; J=6 -> 2
-// warps, 10.4 ms vs 12.7 ms at 3 on the config-2 backprojection)
+// (measured on B200: J=8 -> 4 warps with fixed tap pairs per lane, 40.5 ms
+// of type 1 on config 4 against 41.6 ms for k_spread_owned8 (CBN_SPREAD_W=8);
+// J=6 -> 2 warps, 10.4 ms vs 12.7 ms at 3 on the config-2 backprojection)
 template <int J>
 constexpr int owned_warps() {
-    return J == 6 ? 2 : (J < 8 ? J : 8);
+    return J == 6 ? 2 : (J < 8 ? J : (J == 8 ? 4 : 8));
 }
 
 template <int J, int W, class Src>
@@ -740,7 +782,7 @@ void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src&
     CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
     if (s1 < 0) s1 = bb.nsubs;
     if constexpr (J == 8) {
-        if (spread_warps_override() == 0) {
+        if (spread_warps_override() == 8) {   // the one-row-per-warp kernel (A/B)
             const size_t smem = spread_owned8_smem_bytes(bb.nreg);
             CBN_CUDA(cudaFuncSetAttribute(k_spread_owned8<Src>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
