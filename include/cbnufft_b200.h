@@ -242,6 +242,37 @@ int cbn_projector_grangeat_reverse(cbn_projector* proj, const float* values, flo
 int cbn_projector_grangeat_forward(cbn_projector* proj, const float* frames, float* values,
                                    int32_t n_views_blk, void* stream);
 
+/* Stage parity of the backprojector (pipeline.py:174-184): the forward
+ * Grangeat step and the transposed resample of views [lo, hi) (frames [device]
+ * float32 (hi - lo) x nu x nv), summed over the range's view batches, after
+ * the lattice inverse FFT, the rho crop and the origin average
+ * (resampling.py:164-196): num [device] complex64 = sum of
+ * resample_transpose(values), den [device] float32 = sum of
+ * Re resample_transpose(valid); both in node order (n_phi, n_theta, n_rho)
+ * of the backprojector's radial spec.  Either output may be NULL.
+ * Synchronises. */
+int cbn_backproject_stage_transpose(cbn_projector* proj, const float* frames, int32_t lo,
+                                    int32_t hi, void* num, float* den, void* stream);
+
+/* Plan diagnostics (test/bench support; not on the operator path).
+ * first_indices: per-axis first-tap index mod K (nufft.py:171-179) of a node
+ * set exactly as the projector's kernels use it -- the reference's
+ * plan_nufft(...).interp.indices[:, 0] decoded per axis.  set: 0 forward
+ * radial lattice nodes (J = spectrum_j, radon_fourier.py:89-108); 1 forward
+ * umbrella targets of view batch `batch` (J = resample_j, (rho, theta, phi)
+ * order, resampling.py:79-103); 2 forward polar Grangeat nodes (J = 5,
+ * grangeat.py:93-128); 3-5 the same sets of the backprojector
+ * (pipeline.py:165-210).  out [host] int32 m x d, or NULL to query *m;
+ * *m in: capacity (rows), out: node count.  Synchronises. */
+int cbn_projector_first_indices(cbn_projector* proj, int32_t set, int32_t batch, int32_t* out,
+                                int64_t* m, void* stream);
+/* Plan statistics as ';'-separated names and int64 values (-1: that part of
+ * the plan is not built yet): primary nodes of the conjugate-pair gathers,
+ * resample rho planes used, invalid umbrella targets per view, batch scaling
+ * groups, reverse-Grangeat heavy cells, ...  Synchronises. */
+int cbn_projector_plan_stats(cbn_projector* proj, int64_t* vals, int32_t* count, char* names,
+                             int32_t names_len, void* stream);
+
 /* Per-stage CUDA-event timing: enable (1) / disable (0); when enabled every
  * operator call records events per stage, and the operators run their view
  * blocks on the caller's stream only (no second overlapping stream), so each

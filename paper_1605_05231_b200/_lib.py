@@ -96,6 +96,10 @@ _SIGS = {
     "cbn_projector_set_timing": (ctypes.c_int, [c_vp, c_i32]),
     "cbn_projector_stage_times": (ctypes.c_int, [c_vp, P_f64, P_i32, ctypes.c_char_p, c_i32,
                                                  c_i32]),
+    "cbn_backproject_stage_transpose": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                                       c_vp]),
+    "cbn_projector_first_indices": (ctypes.c_int, [c_vp, c_i32, c_i32, P_i32, P_i64, c_vp]),
+    "cbn_projector_plan_stats": (ctypes.c_int, [c_vp, P_i64, P_i32, ctypes.c_char_p, c_i32, c_vp]),
     "cbn_ct_project_linear": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i32, c_f64, c_vp,
                                              c_vp]),
     "cbn_launch_count": (ctypes.c_longlong, []),

@@ -412,6 +412,16 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
             DevBuf<RsTap<3>> taps((size_t)n);
             k_rs_taps<3><<<blocks_for(n, 256), 256, 0, s>>>(src0, kb, n, taps.p);
             CBN_LAUNCH_CHECK();
+            // pole targets are spread per view (k_rs_pole_spread), not from the CSR
+            std::vector<int> pole_f0;
+            build_poles<3>(p->bumb, src0, n, taps.p, s);
+            for (int q = 0; q < p->bumb.n_poles; ++q) {
+                int t = 0;
+                RsTap<3> tp;
+                CBN_CUDA(cudaMemcpy(&t, p->bumb.poles.p + q, sizeof(int), cudaMemcpyDeviceToHost));
+                CBN_CUDA(cudaMemcpy(&tp, taps.p + t, sizeof(tp), cudaMemcpyDeviceToHost));
+                pole_f0.push_back(tp.f[0]);
+            }
             const int64_t ncol = x.kd3[0] * x.kd3[1];
             DevBuf<int> counts((size_t)ncol);
             CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * ncol, s));
@@ -426,6 +436,8 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
                 // rho planes (cols rho * K_theta + theta) that hold any entry
                 const int64_t kt = x.kd3[1];
                 std::vector<unsigned char> used((size_t)x.kd3[0], 0);
+                for (int f0 : pole_f0)    // the pole targets' rho planes
+                    for (int a = 0; a < 3; ++a) used[(size_t)((f0 + a) % x.kd3[0])] = 1;
                 p->bres_rho_runs.clear();
                 for (int64_t rr = 0; rr < x.kd3[0]; ++rr) {
                     for (int64_t t = 0; t < kt && !used[(size_t)rr]; ++t)
@@ -483,6 +495,9 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             GrangeatPlan& gp = p->bgr;
             if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
             projector_prepare_gr_points(p, gp, p->bumb, false, s);
+            // gp.pix is built lazily by the first block; build it before the
+            // fork so lane 1's first pad kernel is ordered after it
+            projector_gr_pix(p, gp, false, s);
             ensure_lane1(p);
             CBN_CUDA(cudaEventRecord(p->ev_s0, s));
             CBN_CUDA(cudaStreamWaitEvent(p->s1, p->ev_s0, 0));
@@ -696,6 +711,18 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                         gnum, gden, (int)x.kd3[2], p->bcol_ptr.p, ent, vt, vlo, nvr, x.shift);
                 }
                 CBN_LAUNCH_CHECK();
+                if (p->bumb.n_poles) {
+                    // pole targets per view, after the column gather's stores
+                    UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, vlo, s);
+                    KBSet kb;   // grid order (rho, theta, phi)
+                    kb.ax[0] = rax[2].kb;
+                    kb.ax[1] = rax[1].kb;
+                    kb.ax[2] = rax[0].kb;
+                    const int nq = p->bumb.n_poles * nvr;
+                    k_rs_pole_spread<3><<<blocks_for(nq, 128), 128, 0, s>>>(
+                        greal, kb, src, p->bumb.poles.p, p->bumb.n_poles, per_view, nvr, vt);
+                    CBN_LAUNCH_CHECK();
+                }
             }
             flush(g);
         }
@@ -764,6 +791,51 @@ void bp_den(cbn_projector_s* p, const BpCtx& x, cudaStream_t s) {
     k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, p->den_max.p);
     CBN_LAUNCH_CHECK();
     p->den_cached = true;
+}
+
+// num (values) / den (mask) of nufft_backproject for a view range, after the
+// lattice-domain inverse FFT, rho crop and origin average: the sum over the
+// range's batches of resample_transpose (resampling.py:164-196,
+// pipeline.py:183-184), complex64 / float32 in node order [phi][theta][rho]
+__global__ void k_num_final(const float2* __restrict__ acc, int64_t lines, int dr, int pad, int n,
+                            double inv, const double* __restrict__ means, float2* __restrict__ num,
+                            float* __restrict__ re) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= lines * n) return;
+    const int j = (int)(e % n);
+    const int64_t line = e / n;
+    float2 v;
+    if (j == n / 2) {
+        v = make_float2((float)means[0], (float)means[1]);
+    } else {
+        const float2 a = acc[line * dr + pad + j];
+        v = make_float2((float)((double)a.x * inv), (float)((double)a.y * inv));
+    }
+    if (num) num[e] = v;
+    if (re) re[e] = v.x;
+}
+
+void bp_stage_transpose(cbn_projector_s* p, const float* frames, int lo, int hi, float2* num,
+                        float* den, cudaStream_t s) {
+    BpCtx x = bp_context(p, s);
+    const RadialTables& r = p->brad;
+    DevBuf<float2> acc((size_t)x.dsize);
+    p->red.ensure(2 * kRed + 64);
+    double* means = p->red.p + 2 * kRed;
+    const int64_t M = r.nodes();
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 0 && !num) continue;
+        if (pass == 1 && !den) continue;
+        bp_transpose(p, x, frames, lo, hi, acc.p, pass == 1, s);
+        const double inv = bp_lattice_ifft(p, x, acc.p, s);
+        projector_column_mean(acc.p, r.lines(), x.dr, p->bpad + r.n_rho / 2, inv, p->red.p, means,
+                              s);
+        k_num_final<<<blocks_for(M, 256), 256, 0, s>>>(acc.p, r.lines(), x.dr, p->bpad, r.n_rho,
+                                                        inv, means, pass == 0 ? num : nullptr,
+                                                        pass == 1 ? den : nullptr);
+        CBN_LAUNCH_CHECK();
+    }
+    CBN_CUDA(cudaStreamSynchronize(s));
 }
 
 // phase 1
@@ -988,6 +1060,9 @@ void bp_crop_cols(cbn_projector_s* p, float2* cols, int y_lo, int y_hi, float* v
     CBN_LAUNCH_CHECK();
 }
 
+// the backprojector's transposed-resample path: views in lanes (column gather)
+bool bp_uses_lanes(cbn_projector_s* p, cudaStream_t s) { return bp_context(p, s).lanes; }
+
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s) {
     BpCtx x = bp_context(p, s);
     bp_views(p, frames, 0, p->g.n_views, p->padded.p, s);
@@ -1003,6 +1078,20 @@ void bp_sizes(cbn_projector_s* p, int64_t* lattice, int64_t* grid, cudaStream_t 
 }
 
 }  // namespace cbn
+
+extern "C" int cbn_backproject_stage_transpose(cbn_projector* p, const float* frames, int32_t lo,
+                                               int32_t hi, void* num, float* den, void* stream) {
+    try {
+        CBN_REQUIRE(p && frames && (num || den), "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        cbn::bp_stage_transpose(p, frames, lo, hi, static_cast<float2*>(num), den,
+                                static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return cbn::fail(e);
+    }
+}
 
 extern "C" int cbn_projector_grangeat_forward(cbn_projector* p, const float* frames, float* values,
                                               int32_t nb, void* stream) {

@@ -1370,6 +1370,8 @@ void ensure_lane_taps(P* p, cudaStream_t s) {
                     p->fres_rho_runs.emplace_back(k, k + 1);
             }
         }
+        // pole targets leave the view-0 records (their planes are already counted)
+        build_poles<J>(u, src, per_view, reinterpret_cast<RsTap<J>*>(u.taps.p), s);
         if constexpr (J == 3) {
             CBN_REQUIRE((int64_t)ax[2].K * ax[1].K * ax[0].K < (1LL << 32),
                         "resample grid above 2^32 cells");
@@ -1395,23 +1397,40 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
         constexpr int J = decltype(jc)::value;
         UmbrellaTables& u = p->fumb;
         StageScope st(p->timer, "resample_gather", s);
+        const bool re = J == 3 && real_grid(p);
         if constexpr (J == 3) {
             const unsigned nblk = (unsigned)((per_view + 31) / 32);
             const RsRow3* rows = reinterpret_cast<const RsRow3*>(u.rows.p);
-            if (real_grid(p))
+            if (re)
                 k_resample_rows3<1><<<nblk, 256, 0, s>>>(p->grid_re, ax[0].K, rows, per_view, v0,
                                                          nb, shift, vals, tscale, p->fumb.n_t);
             else
                 k_resample_rows3<2><<<nblk, 256, 0, s>>>(reinterpret_cast<const float*>(p->big.p),
                                                          ax[0].K, rows, per_view, v0, nb, shift,
                                                          vals, tscale, p->fumb.n_t);
-            CBN_LAUNCH_CHECK();
-            return 0;
+        } else {
+            k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
+                p->big.p, ax[2].K, ax[1].K, ax[0].K, reinterpret_cast<const RsTap<J>*>(u.taps.p),
+                per_view, v0, nb, shift, vals, tscale, p->fumb.n_t);
         }
-        k_resample_views<J><<<(unsigned)((per_view + 31) / 32), 256, 0, s>>>(
-            p->big.p, ax[2].K, ax[1].K, ax[0].K, reinterpret_cast<const RsTap<J>*>(u.taps.p),
-            per_view, v0, nb, shift, vals, tscale, p->fumb.n_t);
         CBN_LAUNCH_CHECK();
+        if (u.n_poles) {
+            // pole targets per view (their records are not in the view-0 taps)
+            UmbrellaSrc src = cached_umbrella(p, u, p->frad, p->fpad, v0, s);
+            KBSet kb;   // grid order (rho, theta, phi)
+            kb.ax[0] = ax[2].kb;
+            kb.ax[1] = ax[1].kb;
+            kb.ax[2] = ax[0].kb;
+            const int nq = u.n_poles * nb;
+            if (re)
+                k_rs_pole_gather<J, 1><<<blocks_for(nq, 128), 128, 0, s>>>(
+                    p->grid_re, kb, src, u.poles.p, u.n_poles, per_view, nb, vals, tscale, u.n_t);
+            else
+                k_rs_pole_gather<J, 2><<<blocks_for(nq, 128), 128, 0, s>>>(
+                    reinterpret_cast<const float*>(p->big.p), kb, src, u.poles.p, u.n_poles,
+                    per_view, nb, vals, tscale, u.n_t);
+            CBN_LAUNCH_CHECK();
+        }
         return 0;
     });
 }
@@ -1682,6 +1701,9 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         ensure_lane_taps(p, s);
         if (!p->fgr.built) fit_grangeat(p, p->fgr, p->fumb, s);
         prepare_gr_points(p, p->fgr, p->fumb, true, s);
+        // the per-pixel factors lane 1's k_gr_frame reads (built lazily on
+        // first use): build them on s, before the first ev_s0 the lane waits on
+        ensure_gr_pix(p, p->fgr, true, s);
     }
     int lane = 0;
     bool s1_used = false, s1_stale = true;   // s1 has not yet waited for the current grid
@@ -1812,6 +1834,9 @@ void bp_crop_cols(cbn_projector_s* p, float2* cols, int y_lo, int y_hi, float* v
                   cudaStream_t s);
 void bp_sizes(cbn_projector_s* p, int64_t* lattice, int64_t* grid, cudaStream_t s);
 void build_backward_plan(cbn_projector_s* p, cudaStream_t s) { build_backward(p, s); }
+void build_forward_plan(cbn_projector_s* p, cudaStream_t s) { build_forward(p, s); }
+bool projector_views_in_lanes(const cbn_projector_s* p) { return views_in_lanes(p); }
+bool projector_real_grid(const cbn_projector_s* p) { return real_grid(p); }
 void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
                                  bool reverse, cudaStream_t s) {
     prepare_gr_points(p, gp, u, reverse, s);

@@ -36,6 +36,8 @@ struct UmbrellaTables {
     DevBuf<char> taps;      // view-0 resample taps (RsTap) for the views-in-lanes gather
     bool taps_ready = false;
     DevBuf<char> rows;      // J = 3: the same taps as grid-row offsets + weight products (RsRow3)
+    DevBuf<int> poles;      // pole targets (theta == 0), handled per view (cbn_resample_views.cuh)
+    int n_poles = 0;
     void build(const cbn_geometry& g, int n_mu, int n_t, double dt, cudaStream_t s);
 };
 

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "cbn_kernels.cuh"
+#include "cbn_projector.h"
 #include "cbn_sources.cuh"
 
 namespace cbn {
@@ -198,6 +199,107 @@ static __global__ void k_crop_from_lines(const float2* __restrict__ F, RemapAxis
     float2* d = acc + ((size_t)e0 * a1.n + e1) * a2.n + e2;
     const float2 o = *d;
     *d = make_float2(o.x + sc * f.x, o.y + sg * sc * f.y);
+}
+
+// ----------------------------------------------------------------------
+// Pole targets (theta == 0; see UmbrellaSrc): the reference sets their phi
+// per view from signed zeros, so view 0's taps shifted by whole phi cells do
+// not apply.  They are listed once per plan, dropped from the view-0 tap
+// records (valid = 0, after the rho-plane scan), and handled per view by
+// k_rs_pole_gather (forward) / k_rs_pole_spread (transpose) -- one or two
+// targets per view.
+constexpr int kMaxPoles = 4096;
+
+template <int J>
+__global__ void k_rs_poles(UmbrellaSrc src0, int64_t n, RsTap<J>* __restrict__ taps,
+                           int* __restrict__ list, int* __restrict__ count) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double wd[3];
+    UmbrellaSrc::Aux aux;
+    src0.node(t, wd, aux);
+    if (!aux.pole) return;
+    taps[t].valid = 0;
+    const int k = atomicAdd(count, 1);
+    if (k < kMaxPoles) list[k] = (int)t;
+}
+
+// lists the poles into u.poles / u.n_poles and clears their tap records
+template <int J>
+void build_poles(UmbrellaTables& u, const UmbrellaSrc& src0, int64_t n, RsTap<J>* taps,
+                 cudaStream_t s) {
+    DevBuf<int> cnt(1);
+    CBN_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), s));
+    u.poles.alloc(kMaxPoles);
+    k_rs_poles<J><<<blocks_for(n, 256), 256, 0, s>>>(src0, n, taps, u.poles.p, cnt.p);
+    CBN_LAUNCH_CHECK();
+    int h = 0;
+    CBN_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    CBN_REQUIRE(h <= kMaxPoles, "too many pole targets");
+    u.n_poles = h;
+}
+
+// Re(resample_apply) at the pole targets of views [v0, v0 + nb): the grid is
+// phi-fast [rho][theta][phi] (ES floats per cell, the real part read); kb in
+// grid order (rho, theta, phi); src.view0 = v0
+template <int J, int ES>
+__global__ void k_rs_pole_gather(const float* __restrict__ G, KBSet kb, UmbrellaSrc src,
+                                 const int* __restrict__ poles, int npoles, int64_t per_view, int nb,
+                                 float* __restrict__ vals, const float* __restrict__ tscale,
+                                 int n_t) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= npoles * nb) return;
+    const int v = q / npoles;
+    const int64_t t = poles[q % npoles];
+    double wd[3];
+    UmbrellaSrc::Aux aux;
+    src.node((int64_t)v * per_view + t, wd, aux);
+    const double w[3] = {wd[2], wd[1], wd[0]};
+    int first[3];
+    float wt[3][J];
+    tap_setup<3, J>(kb, w, first, wt);
+    const int K0 = kb.ax[0].K, K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+    float acc = 0.f;
+    for (int a = 0; a < J; ++a)
+        for (int b = 0; b < J; ++b) {
+            const size_t row = ((size_t)wrapc(first[0] + a, K0) * K1 + wrapc(first[1] + b, K1)) * K2;
+            float r = 0.f;
+            for (int c = 0; c < J; ++c)
+                r = fmaf(wt[2][c], __ldg(G + ES * (row + wrapc(first[2] + c, K2))), r);
+            acc = fmaf(wt[0][a] * wt[1][b], r, acc);
+        }
+    if (!aux.valid) acc = 0.f;
+    vals[(size_t)v * per_view + t] = tscale ? acc * tscale[t % n_t] : acc;
+}
+
+// transposed resample at the pole targets of views [v0, v0 + nb) into the
+// real phi-fast grid G (after the column gather wrote it): values from valsT
+// [target][nb] (null: the validity mask, den)
+template <int J>
+__global__ void k_rs_pole_spread(float* __restrict__ G, KBSet kb, UmbrellaSrc src,
+                                 const int* __restrict__ poles, int npoles, int64_t per_view, int nb,
+                                 const float* __restrict__ valsT) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= npoles * nb) return;
+    const int v = q / npoles;
+    const int64_t t = poles[q % npoles];
+    double wd[3];
+    UmbrellaSrc::Aux aux;
+    src.node((int64_t)v * per_view + t, wd, aux);
+    if (!aux.valid) return;
+    const double w[3] = {wd[2], wd[1], wd[0]};
+    int first[3];
+    float wt[3][J];
+    tap_setup<3, J>(kb, w, first, wt);
+    const float x = valsT ? valsT[(size_t)t * nb + v] : 1.f;
+    const int K0 = kb.ax[0].K, K1 = kb.ax[1].K, K2 = kb.ax[2].K;
+    for (int a = 0; a < J; ++a)
+        for (int b = 0; b < J; ++b) {
+            const size_t row = ((size_t)wrapc(first[0] + a, K0) * K1 + wrapc(first[1] + b, K1)) * K2;
+            const float wab = wt[0][a] * wt[1][b] * x;
+            for (int c = 0; c < J; ++c) atomicAdd(G + row + wrapc(first[2] + c, K2), wab * wt[2][c]);
+        }
 }
 
 // used[k] = 1 for every axis-0 (rho) plane a valid target's taps touch

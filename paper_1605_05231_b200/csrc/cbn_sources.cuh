@@ -143,9 +143,17 @@ struct UmbrellaSrc {
     // plane normal about z, leaving rho and theta unchanged and adding
     // k n_phi / V to the phi index (mod n_phi), so view k's targets follow
     // from view 0's without the per-target trigonometry.
+    //
+    // The pole (theta exactly 0: the mu = pi/2, t = 0 plane of every view) is
+    // the exception: the reference's canonical wrap sets its phi from the
+    // signs of zero components (0 or pi per view, geometry.py:143-159), not
+    // by the rotation, so pole targets are always computed directly.  (The
+    // lattice rows at theta = 0 coincide for every phi, so the two choices
+    // differ only at the level of the J = 3 interpolation error.)
     const double4* cache = nullptr;
     struct Aux {
         bool valid;
+        bool pole;     // valid target at theta == 0 (phi from the view's own geometry)
     };
     CBN_D void cached_position(int64_t i, double (&pos)[3], bool& valid) const {
         const int64_t per_view = (int64_t)g.n_mu * g.n_t;
@@ -161,7 +169,7 @@ struct UmbrellaSrc {
     CBN_D void position(int64_t i, double (&pos)[3], bool& valid) const {
         if (cache) {
             cached_position(i, pos, valid);
-            return;
+            if (!(valid && pos[1] == 0.0)) return;
         }
         const int64_t per_view = (int64_t)g.n_mu * g.n_t;
         const int v = view0 + (int)(i / per_view);
@@ -219,6 +227,7 @@ struct UmbrellaSrc {
     CBN_D void node(int64_t i, double (&w)[3], Aux& a) const {
         double pos[3];
         position(i, pos, a.valid);
+        a.pole = a.valid && pos[1] == 0.0;
         const double m2pi = -kTwoPi;
         // device axis order: (phi, theta, rho)
         w[0] = wrap_pi(ddiv(dmul(m2pi, pos[2]), g.padded[2]));

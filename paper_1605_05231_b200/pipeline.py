@@ -309,6 +309,55 @@ class Projector:
                                                               _device.ptr(out), nb, self._s))
         return out
 
+    def backproject_stage_transpose(self, frames, view_lo: int, view_hi: int):
+        """(num, den) of the backprojector for views [view_lo, view_hi): the summed
+        resample_transpose of the forward-Grangeat values and of the validity
+        mask (pipeline.py:174-184), after the lattice IFFT, rho crop and origin
+        average -- complex64 / float32 in node order (n_phi, n_theta, n_rho)."""
+        t = _device.require_cuda()
+        f = _device.to_device(frames, t.float32)
+        if tuple(f.shape) != (view_hi - view_lo, self.geom.nu, self.geom.nv):
+            raise ValueError("frames must be (view_hi - view_lo, nu, nv)")
+        n_rho = 2 * int(np.ceil(1.5 * self.n / 2.0))
+        shape = (self.cfg.radial_spec.n_phi, self.cfg.radial_spec.n_theta, n_rho)
+        num = t.empty(shape, dtype=t.complex64, device="cuda")
+        den = t.empty(shape, dtype=t.float32, device="cuda")
+        _lib.check(_lib.load().cbn_backproject_stage_transpose(
+            self._h, _device.ptr(f), int(view_lo), int(view_hi), _device.ptr(num),
+            _device.ptr(den), self._s), "nufft_backproject")
+        return num, den
+
+    # ---- plan diagnostics
+    _SETS = {("forward", "radial"): 0, ("forward", "umbrella"): 1, ("forward", "polar"): 2,
+             ("back", "radial"): 3, ("back", "umbrella"): 4, ("back", "polar"): 5}
+
+    def first_indices(self, direction: str, node_set: str, batch: int = 0) -> np.ndarray:
+        """(m, d) int32 first-tap index mod K per axis of one of the projector's
+        node sets (reference axis order), as its kernels use it -- comparable to
+        plan_nufft(...).interp.indices[:, 0] of the reference (nufft.py:171-179)."""
+        s = self._SETS[(direction, node_set)]
+        lib = _lib.load()
+        m = ctypes.c_int64(0)
+        _lib.check(lib.cbn_projector_first_indices(self._h, s, int(batch), None, ctypes.byref(m),
+                                                   self._s))
+        d = 2 if node_set == "polar" else 3
+        out = np.empty((m.value, d), dtype=np.int32)
+        _lib.check(lib.cbn_projector_first_indices(self._h, s, int(batch),
+                                                   out.ctypes.data_as(_lib.P_i32),
+                                                   ctypes.byref(m), self._s))
+        return out
+
+    def plan_stats(self) -> dict:
+        """Plan statistics (cbn_projector_plan_stats); -1 = not built yet."""
+        lib = _lib.load()
+        cnt = ctypes.c_int32(64)
+        vals = (ctypes.c_int64 * 64)()
+        names = ctypes.create_string_buffer(4096)
+        _lib.check(lib.cbn_projector_plan_stats(self._h, vals, ctypes.byref(cnt), names, 4096,
+                                                self._s))
+        keys = names.value.decode().split(";")[:cnt.value]
+        return {k: int(vals[i]) for i, k in enumerate(keys)}
+
     def grangeat_forward(self, frames):
         t = _device.require_cuda()
         f = _device.to_device(frames, t.float32)

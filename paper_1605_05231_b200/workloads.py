@@ -62,3 +62,42 @@ def config4_inputs(n_points: int = 100_000_000, grid: int = 256):
     rng = np.random.default_rng(5)
     pts = rng.uniform(-np.pi, np.pi, (n_points, 3)).astype(np.float32)
     return x, pts
+
+
+def analytic_projections(geom: ConeGeometry, table, views=None, extent_mm: float = 2.0) -> np.ndarray:
+    """Exact cone-beam line integrals of an ellipsoid table (input generation).
+
+    ``table`` is ``phantom.random_ellipsoids(...)``: (centre, semi_axes, rotation,
+    density) in the phantom's unit cube [-1, 1]^3, scaled to ``extent_mm``.
+    Rays run from the source of view k to the centre of every detector pixel
+    (u, v) (the detector layout of pipeline.calibrate_normalization,
+    pipeline.py:225-240).  float64 numpy, so the same frames are produced on
+    any host -- the backprojector parity fixtures use them as input.
+    Returns float64 (n_views, nu, nv), frames indexed [u, v].
+    """
+    views = range(geom.n_views) if views is None else views
+    half = extent_mm / 2.0
+    pu, pv = geom.pixel_mm
+    u = (np.arange(geom.nu) - geom.nu / 2.0 + 0.5) * pu
+    v = (np.arange(geom.nv) - geom.nv / 2.0 + 0.5) * pv
+    uu, vv = np.meshgrid(u, v, indexing="ij")
+    out = np.zeros((len(views), geom.nu, geom.nv))
+    for i, k in enumerate(views):
+        a = 2.0 * np.pi * k / geom.n_views
+        s_hat = np.array([np.cos(a), np.sin(a), 0.0])
+        u_hat = np.array([-np.sin(a), np.cos(a), 0.0])
+        src = geom.so_mm * s_hat
+        pts = (src - geom.sd_mm * s_hat)[None, None, :] + uu[..., None] * u_hat \
+            + vv[..., None] * np.array([0.0, 0.0, 1.0])
+        d = pts - src
+        d /= np.linalg.norm(d, axis=-1, keepdims=True)
+        for centre, axes, rot, density in table:
+            # body coordinates b(t) = b0 + t b1 of the ray p(t) = src + t d
+            p0 = src / half - centre
+            b0 = (p0 @ rot) / axes
+            b1 = (d @ rot) / (axes * half)
+            qa = np.sum(b1 * b1, axis=-1)
+            qb = b1 @ b0
+            disc = qb * qb - qa * (b0 @ b0 - 1.0)
+            out[i] += density * 2.0 * np.sqrt(np.maximum(disc, 0.0)) / qa
+    return out

@@ -45,3 +45,13 @@ def golden_n16():
 @pytest.fixture(scope="session")
 def golden_n12():
     return dict(np.load(os.path.join(GOLDEN, "pipeline_n12_dirac.npz")))
+
+
+def unpack_int(z, key):
+    """Decode an (m, d) integer fixture written by make_golden_r2.pack_int
+    (row deltas, axis-major, zlib) -> int64 (m, d)."""
+    import zlib
+    shape = tuple(int(s) for s in z[key + "__shape"])
+    d = np.frombuffer(zlib.decompress(z[key + "__z"].tobytes()), np.int16)
+    d = d.reshape(shape[1], shape[0]).T.astype(np.int64)
+    return np.cumsum(d, axis=0)

@@ -1,0 +1,121 @@
+"""Reference-pinned parity at BASELINE config 2 (the benchmarked workload):
+256^3 30-ellipsoid phantom (seed 2), 512 x 180 x 360 radial lattice (33.2M
+nodes: 16 chunked sub-plans in the reference, each with its own scaling),
+360 views of 256^2.  Fixtures from the reference itself (make_golden_r2.py):
+
+  config2_fwd.npz       _radial_lattice (200k sampled entries) and
+                        nufft_forward_project frames of views 0-3, 120, 241
+                        (single-view batches here, pipeline.py:105-110);
+  config2_bp_stage.npz  the first backprojector batch (views 0-3): forward
+                        Grangeat values and the batch's resample_transpose of
+                        the values and of the mask, sampled; one 2^21-node
+                        nufft_adjoint sub-plan of the backprojector nodes;
+  config2_bp.npz        nufft_backproject of all 360 views: slices + 4^3 block
+                        means.
+Backprojector inputs are analytic ellipsoid projections
+(workloads.analytic_projections, float64 numpy, identical on any host).
+Contract: relative L2 <= 1e-4 (fp32); the observed error is each message.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, rel_l2
+from _cases import config_setup
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def c2():
+    geom, voxel, spec, cfg = config_setup(2)
+    return geom, voxel, spec, cfg
+
+
+@pytest.fixture(scope="module")
+def c2_vol():
+    from paper_1605_05231_b200.phantom import random_ellipsoid_phantom
+    return random_ellipsoid_phantom(256, 30, 2)
+
+
+def test_config2_radial_lattice(c2, c2_vol):
+    from paper_1605_05231_b200.pipeline import Projector
+    geom, voxel, spec, cfg = c2
+    z = np.load(os.path.join(GOLDEN, "config2_fwd.npz"))
+    lat = Projector(geom, cfg, 256, voxel, 1).radial_lattice(c2_vol)
+    r, t, p = (np.asarray(a, dtype=np.int64) for a in z["lat_idx"].T)
+    import torch
+    idx = torch.from_numpy((p * spec.n_theta + t) * spec.n_rho + r).cuda()
+    got = lat.reshape(-1)[idx].cpu().numpy()
+    err = rel_l2(got, z["lat_val"])
+    assert err < TOL, err
+
+
+def test_config2_forward_views(c2, c2_vol):
+    from paper_1605_05231_b200 import pipeline as pl
+    from paper_1605_05231_b200.phantom import Volume3D
+    geom, voxel, spec, cfg = c2
+    z = np.load(os.path.join(GOLDEN, "config2_fwd.npz"))
+    frames = pl.nufft_forward_project(Volume3D(c2_vol, voxel), geom, cfg)
+    got = np.stack([frames[int(k)].data for k in z["views"]])
+    errs = [rel_l2(got[i], z["frames"][i]) for i in range(got.shape[0])]
+    assert max(errs) < TOL, errs
+
+
+def test_config2_backprojector_batch_stage(c2):
+    """Forward Grangeat + resample_transpose of the first 4-view batch."""
+    from paper_1605_05231_b200.phantom import random_ellipsoids
+    from paper_1605_05231_b200.pipeline import Projector
+    from paper_1605_05231_b200.workloads import analytic_projections
+    geom, voxel, spec, cfg = c2
+    z = np.load(os.path.join(GOLDEN, "config2_bp_stage.npz"))
+    lo, hi = (int(v) for v in z["views"])
+    frames = analytic_projections(geom, random_ellipsoids(30, 2), views=range(lo, hi))
+    proj = Projector(geom, cfg, 256, voxel, 2)
+    vals = proj.grangeat_forward(frames.astype(np.float32)).cpu().numpy().ravel()
+    e_gr = rel_l2(vals[z["gr_idx"]], z["gr_values"])
+    num, den = proj.backproject_stage_transpose(frames.astype(np.float32), lo, hi)
+    r, t, p = (np.asarray(a, dtype=np.int64) for a in z["idx"].T)
+    e_num = rel_l2(num.cpu().numpy()[p, t, r], z["num"])
+    e_den = rel_l2(den.cpu().numpy()[p, t, r], z["den"])
+    assert max(e_gr, e_num, e_den) < TOL, (e_gr, e_num, e_den)
+
+
+def test_config2_backprojector_adjoint_subplan(c2):
+    """nufft_adjoint of the first 2^21-node sub-plan of the backprojector's
+    node set (pipeline.py:202-210, nufft.py:268-282) onto 256^3."""
+    import cbn_oracle as orc
+    from paper_1605_05231_b200 import nufft
+    from paper_1605_05231_b200.geometry import RadialGridSpec
+    geom, voxel, spec, cfg = c2
+    z = np.load(os.path.join(GOLDEN, "config2_bp_stage.npz"))
+    bspec = RadialGridSpec(384, spec.n_theta, spec.n_phi, 256 * voxel * np.sqrt(3.0) / 2.0)
+    nodes = orc.wrap(orc.radial_direction_nodes(bspec, voxel))[: 1 << 21]
+    yr = np.random.default_rng(204)
+    y = yr.standard_normal(nodes.shape[0]) + 1j * yr.standard_normal(nodes.shape[0])
+    plan = nufft.plan_nufft((256,) * 3, nodes, 2.0, 6)
+    x = nufft.nufft_adjoint(plan, y)
+    errs = (rel_l2(x[128], z["adj_x"]), rel_l2(x[:, 128], z["adj_y_slice"]),
+            rel_l2(x[:, :, 128], z["adj_z"]))
+    norm = abs(np.linalg.norm(x) / float(z["adj_norm"]) - 1.0)
+    assert max(errs) < TOL and norm < TOL, (errs, norm)
+
+
+def test_config2_backproject_all_views(c2):
+    from paper_1605_05231_b200 import pipeline as pl
+    from paper_1605_05231_b200.grangeat import DetectorFrame
+    from paper_1605_05231_b200.phantom import random_ellipsoids
+    from paper_1605_05231_b200.workloads import analytic_projections
+    geom, voxel, spec, cfg = c2
+    z = np.load(os.path.join(GOLDEN, "config2_bp.npz"))
+    frames = analytic_projections(geom, random_ellipsoids(30, 2))
+    vol = pl.nufft_backproject([DetectorFrame(k, frames[k], geom.pixel_mm)
+                                for k in range(geom.n_views)], geom, cfg, 256, voxel).data
+    blocks = vol.reshape(64, 4, 64, 4, 64, 4).mean(axis=(1, 3, 5))
+    errs = dict(x=rel_l2(vol[128], z["x"]), y=rel_l2(vol[:, 128], z["y"]),
+                z=rel_l2(vol[:, :, 128], z["z"]), blocks=rel_l2(blocks, z["blocks"]),
+                norm=abs(np.linalg.norm(vol) / float(z["norm"]) - 1.0))
+    assert max(errs.values()) < TOL, errs
