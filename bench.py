@@ -1,23 +1,31 @@
 #!/usr/bin/env python
-"""Benchmark: NUFFT cone-beam forward projector, BASELINE.json config 2.
+"""Benchmark of the NUFFT cone-beam projector pair and the NUFFT (BASELINE.json).
 
-One step = one full forward projection (``nufft_forward_project``) of the
-seeded 256^3 30-ellipsoid phantom onto 360 cone-beam views (256^2 detector),
-with the reference's view batching and per-batch resample scalings.
+Default run (``python bench.py``, N = 1): ONE JSON line whose headline is the
+config-2 forward projector (``nufft_forward_project``: 256^3 30-ellipsoid
+phantom -> 360 cone-beam views of 256^2, the reference's view batching and
+per-batch resample scalings) in views/s, with two sub-objects carrying the
+rest of BASELINE's metric ("views/s and Msamples/s, fwd+adj"):
+  * "adjoint": the config-2 backprojector (``nufft_backproject``), views/s;
+  * "nufft4":  config 4, type-2 + type-1 of 100M unstructured points, Msamples/s
+               (with and without the per-step bin sort).
+Each carries ``roofline``, ``e2e`` (through the drop-in API with host numpy
+buffers) and ``cpu_baseline`` (the oracle port on this host's cores).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config 2] [--direction forward|back]
+                  [--config 2|3|4] [--direction forward|back] [--only]
 
-Under torchrun (N > 1) the views are sharded across ranks (strong scaling:
-360 views in total); every rank computes the radial lattice itself.
-``--impl reference`` times the CPU oracle port (oracle/cbn_oracle.py, the
-reference algorithm in numpy/scipy) on a bounded, extrapolated sample.
-Prints ONE JSON line on rank 0.
+``--only`` measures just the selected config/direction.  Under torchrun
+(N > 1) views and radial nodes are sharded across ranks (strong scaling);
+timings are the max over ranks.  ``--impl reference`` times the CPU oracle
+port (oracle/cbn_oracle.py) on bounded, extrapolated samples.
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
+import gc
 import json
 import os
 import subprocess
@@ -31,14 +39,13 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
-FALLBACK_HBM_GBS = 6650.0
-# dram__bytes_read.sum + dram__bytes_write.sum per config-2 step, summed over
-# the stage's launches, from the committed ncu launch lists
-# (profiles/r1j_launches_fwd.txt, profiles/r1j_launches_bp.txt); stages not
-# captured there report null
-TRAFFIC: dict = {"resample_gather": 2.373e9, "grangeat_spread": 2.441e9 + 1.858e9,
-                 "spectrum_gather": 0.966e9, "bp_spread": 1.024e9,
-                 "transpose_spread": 0.839e9 + 0.725e9}
+FALLBACK_HBM_GBS = 6650.0       # B200_PROFILING.md fallback when no measured peak exists
+SMEM_TBS = 148 * 128 * 1.965e9 / 1e12   # nominal shared-memory bandwidth
+# dram__bytes_read.sum + dram__bytes_write.sum per config-2 step of the
+# dominant kernels, from the committed ncu captures (profiles/)
+TRAFFIC = {"forward": {"resample_gather": 2.373e9, "spectrum_gather": 0.966e9,
+                       "grangeat_spread": 2.441e9},
+           "back": {"bp_spread": 1.024e9, "transpose_spread": 0.839e9}}
 
 
 def parse_args():
@@ -49,6 +56,7 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--direction", choices=["forward", "back"], default="forward")
+    ap.add_argument("--only", action="store_true", help="skip the sub-object measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -57,9 +65,36 @@ def parse_args():
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback"
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    def init(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(self.local)
+        if self.world > 1 and not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, vals):
+        import torch
+        t = torch.tensor(list(vals), dtype=torch.float64, device="cuda")
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t.tolist()]
 
 
 # ----------------------------------------------------------------- clocks
@@ -83,6 +118,7 @@ class ClockSampler:
             self.thread.start()
         except Exception:
             self.proc = None
+        return self
 
     def _read(self):
         for line in self.proc.stdout:
@@ -115,267 +151,253 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------- roofline helpers
-def stage_bytes(stage: str, w, views: int):
-    """Algorithmic bytes of one step's stage: (compulsory HBM bytes, on-chip tap
-    bytes).  DESIGN.md section 4 derives each; nodes/targets generated from
-    index tables stream no coordinates (c = 0 in SURVEY 8(d))."""
-    spec, cfg = w.spec, w.cfg
-    n = w.n
-    K3 = (2 * n) ** 3
-    M = spec.n_rho * spec.n_theta * spec.n_phi
-    dr = spec.n_rho + 2 * cfg.rho_pad
-    D = dr * spec.n_theta * spec.n_phi
-    Kr = 8 * D
-    tpv = cfg.n_mu * cfg.n_t                  # umbrella targets per view
-    grid2 = 4 * w.geom.nu * w.geom.nv          # oversampled detector cells per view
-    J, Jr, Jg = 6, 3, 5
-    if stage == "spectrum_gather":             # read K^3 grid once, write M lattice values
-        return 8.0 * K3 + 8.0 * M, 8.0 * J ** 3 * M
-    if stage == "resample_gather":             # read the resample grid once, write f32 values
-        return 8.0 * Kr + 4.0 * tpv * views + 32.0 * tpv, 8.0 * Jr ** 3 * tpv * views
-    if stage == "grangeat_spread":             # read t-spectra, RED the 2D grids once
-        return 8.0 * tpv * views + 8.0 * grid2 * views + 56.0 * tpv, 16.0 * Jg ** 2 * tpv * views
-    if stage == "bp_spread":                   # read M lattice values, write K^3 grid once
-        return 8.0 * M + 8.0 * K3, 16.0 * J ** 3 * M
-    if stage == "transpose_spread":            # transpose + gather: values 3x, grid once
-        return 3 * 4.0 * tpv * views + 8.0 * Kr, 4.0 * Jr ** 3 * tpv * views
-    if stage == "spectrum_pad":
-        return 4.0 * n ** 3 + 8.0 * K3, 0.0
-    if stage == "resample_pad":
-        return 8.0 * D + 8.0 * Kr, 0.0
-    return None
-
-
-def run_ours(args):
+def timed(fn, steps, d: Dist, stream):
+    """K steps between a barrier + synchronize on both sides, CUDA events on
+    the launching stream; returns the max-over-ranks milliseconds."""
     import torch
-    import torch.distributed as dist
+    torch.cuda.synchronize()
+    d.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    d.barrier()
+    return d.max([e0.elapsed_time(e1)])[0]
+
+
+def roofline_from_stages(lib, handle, steps, peak, peak_kind, traffic):
+    """Per-stage rooflines from the projector's stage events and its own
+    algorithmic-byte accounting (cbn_projector_stage_bytes)."""
+    cnt = ctypes.c_int32(64)
+    ms = (ctypes.c_double * 64)()
+    names = ctypes.create_string_buffer(4096)
+    lib.cbn_projector_stage_times(handle, ms, ctypes.byref(cnt), names, 4096, 1)
+    stages = {nm: ms[i] / steps for i, nm in enumerate(names.value.decode().split(";")[:cnt.value])}
+    cnt = ctypes.c_int32(64)
+    hb = (ctypes.c_double * 64)()
+    cb = (ctypes.c_double * 64)()
+    names = ctypes.create_string_buffer(4096)
+    lib.cbn_projector_stage_bytes(handle, hb, cb, ctypes.byref(cnt), names, 4096, 1)
+    kernels = {}
+    for i, nm in enumerate(names.value.decode().split(";")[:cnt.value]):
+        t = stages.get(nm, 0.0)
+        if t <= 0:
+            continue
+        hbm, chip = hb[i] / steps, cb[i] / steps
+        ach = hbm / (t / 1e3) / 1e9
+        kernels[nm] = {"ms_per_step": round(t, 3), "hbm_bytes": hbm, "achieved_gbs": round(ach, 1),
+                       "hbm_frac": round(ach / peak, 4), "onchip_bytes": chip,
+                       "onchip_tbs": round(chip / (t / 1e3) / 1e12, 2),
+                       "onchip_frac": round(chip / (t / 1e3) / 1e12 / SMEM_TBS, 3)}
+    roofline = None
+    if kernels:
+        st = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+        kk = kernels[st]
+        tr = traffic.get(st)
+        roofline = {"kernel": st, "bound": "hbm", "achieved": kk["achieved_gbs"], "peak": peak,
+                    "unit": "GB/s", "frac": kk["hbm_frac"],
+                    "traffic": tr, "peak_kind": peak_kind,
+                    "algorithmic_bytes_per_step": kk["hbm_bytes"],
+                    "note": "achieved = the stage's algorithmic (compulsory) HBM bytes per step / its "
+                            "CUDA-event time in a serialised pass; traffic = ncu DRAM bytes per step "
+                            "(profiles/); onchip_* = shared-memory/L1 tap bytes (the binding "
+                            "resource of the J >= 3 gathers/spreads)",
+                    "onchip_tbs": kk["onchip_tbs"], "onchip_frac": kk["onchip_frac"]}
+    return stages, kernels, roofline
+
+
+# ------------------------------------------------------ projector (configs 0-3)
+def measure_projector(args, d: Dist, config: int, direction: str):
+    import torch
     from paper_1605_05231_b200 import _lib
-    from paper_1605_05231_b200.pipeline import Projector
+    from paper_1605_05231_b200 import pipeline as pl
+    from paper_1605_05231_b200 import sharding
+    from paper_1605_05231_b200.grangeat import DetectorFrame
+    from paper_1605_05231_b200.phantom import Volume3D
     from paper_1605_05231_b200.workloads import workload
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1605_05231_b200 import pipeline as _pl
-    from paper_1605_05231_b200 import sharding
-    w = workload(args.config)
+    w = workload(config)
     V = w.geom.n_views
     per_view = w.cfg.n_mu * w.cfg.n_t
-    lo, hi = sharding.view_shard(V, world, rank,
-                                 sharding.view_batches(V, per_view, _pl._TARGET_BATCH))
+    lo, hi = sharding.view_shard(V, d.world, d.rank,
+                                 sharding.view_batches(V, per_view, pl._TARGET_BATCH))
+    fwd = direction == "forward"
     vol_host = w.volume()
     lib = _lib.load()
-    direction = 1 if args.direction == "forward" else 2
-    proj = Projector(w.geom, w.cfg, w.n, w.voxel, direction)
     stream = torch.cuda.current_stream()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    if direction == 1:
+    proj = pl.Projector(w.geom, w.cfg, w.n, w.voxel, 1 if fwd else 2)
+    if fwd:
         x_dev = torch.from_numpy(vol_host).cuda()
-        if world > 1:
-            # radial nodes and views sharded; the lattice summed with one NCCL all-reduce
+        if d.world > 1:
             def step():
                 return proj.forward_sharded(x_dev, lo, hi)
         else:
             def step():
                 return proj.forward(x_dev, lo, hi)
     else:
-        frames_dev = Projector(w.geom, w.cfg, w.n, w.voxel, 1).forward(torch.from_numpy(vol_host).cuda())
-        x_dev = frames_dev
-        if world > 1:
-            # views and radial nodes sharded; lattice and grid summed with NCCL
-            x_loc = x_dev[lo:hi].contiguous()
-
+        fp = pl.Projector(w.geom, w.cfg, w.n, w.voxel, 1)
+        x_dev = fp.forward(torch.from_numpy(vol_host).cuda())
+        del fp
+        gc.collect()
+        x_loc = x_dev[lo:hi].contiguous()
+        if d.world > 1:
             def step():
                 return proj.backproject_sharded(x_loc, lo, hi)
         else:
             def step():
                 return proj.backproject(x_dev)
 
+    t_plan = time.perf_counter()
+    step()                                   # builds the plan (not timed)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t_plan
     for _ in range(max(args.warmup, 3)):
         step()
-    torch.cuda.synchronize()
-    barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks = ClockSampler(d.local).start()
     n0 = lib.cbn_launch_count()
-    torch.cuda.synchronize()
-    barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
-        step()
-    t1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms = timed(step, args.steps, d, stream)
     launches = lib.cbn_launch_count() - n0
-    ms = t0.elapsed_time(t1)
     clk = clocks.stop()
-    # per-stage kernel times: a separate pass of the same steps with stage
-    # events on, during which the operators keep every view block on one
-    # stream (no overlap), so each stage's event time is its own kernels'
-    # time and the shares agree with the serialised ncu launch list
+    value = V * args.steps / (ms / 1e3)
+
+    # serialised pass with stage events + algorithmic bytes (per-kernel rooflines)
     lib.cbn_projector_set_timing(proj._h, 1)
     for _ in range(args.steps):
         step()
     torch.cuda.synchronize()
-    import ctypes
-    cnt = ctypes.c_int32(64)
-    stage_ms = (ctypes.c_double * 64)()
-    names = ctypes.create_string_buffer(4096)
-    lib.cbn_projector_stage_times(proj._h, stage_ms, ctypes.byref(cnt), names, 4096, 1)
-    lib.cbn_projector_set_timing(proj._h, 0)
-    stages = {nm: stage_ms[i] / args.steps
-              for i, nm in enumerate(names.value.decode().split(";")[:cnt.value])}
-    ms_t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    units = V if direction == 1 else V        # views per step across all ranks
-    value = units * args.steps / (ms_max / 1e3)
-
-    # ---- end to end through the public API path: pinned host in, host out
-    e2e = None
-    if not args.no_e2e:
-        if direction == 1:
-            host_in = torch.from_numpy(vol_host).pin_memory()
-            host_out = torch.empty((hi - lo, w.geom.nu, w.geom.nv), dtype=torch.float32).pin_memory()
-        else:
-            host_in = x_dev.cpu().pin_memory()
-            host_out = torch.empty((w.n,) * 3, dtype=torch.float32).pin_memory()
-
-        def run(dev):
-            if direction == 1:
-                return proj.forward_sharded(dev, lo, hi) if world > 1 else proj.forward(dev, lo, hi)
-            if world > 1:
-                return proj.backproject_sharded(dev[lo:hi].contiguous(), lo, hi)
-            return proj.backproject(dev)
-
-        # Pipelined through the public API: a copy stream brings step k+1's input
-        # in while step k computes and takes step k-1's result out, so every
-        # step's H2D and D2H are inside the timed region but overlap the compute
-        copy_s = torch.cuda.Stream()
-        dev_in = [torch.empty(host_in.shape, dtype=host_in.dtype, device="cuda") for _ in range(2)]
-        host_outs = [host_out, torch.empty_like(host_out).pin_memory()]
-        in_ready = [torch.cuda.Event() for _ in range(2)]
-        out_ready = [torch.cuda.Event() for _ in range(2)]
-
-        def pipeline(nsteps, start_event=None):
-            with torch.cuda.stream(copy_s):
-                if start_event is not None:
-                    copy_s.wait_event(start_event)
-                dev_in[0].copy_(host_in, non_blocking=True)
-                in_ready[0].record(copy_s)
-            for k in range(nsteps):
-                slot = k % 2
-                if k + 1 < nsteps:               # next input, once step k-1 released its slot
-                    with torch.cuda.stream(copy_s):
-                        if k >= 1:
-                            copy_s.wait_event(out_ready[1 - slot])
-                        dev_in[1 - slot].copy_(host_in, non_blocking=True)
-                        in_ready[1 - slot].record(copy_s)
-                stream.wait_event(in_ready[slot])
-                out = run(dev_in[slot])
-                out_ready[slot].record(stream)
-                with torch.cuda.stream(copy_s):
-                    copy_s.wait_event(out_ready[slot])
-                    host_outs[slot].copy_(out, non_blocking=True)
-                out.record_stream(copy_s)
-
-        pipeline(2)
-        torch.cuda.synchronize()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        wall0 = time.perf_counter()
-        e0.record(stream)
-        pipeline(args.steps, e0)
-        e1.record(copy_s)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - wall0
-        barrier()
-        et = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item())
-        e2e = {"value": units * args.steps / (e_ms / 1e3), "unit": "views/s",
-               "h2d_bytes_per_step": int(host_in.numel() * 4),
-               "d2h_bytes_per_step": int(host_out.numel() * 4),
-               "wall_s": wall, "api": "Projector.forward/backproject with pinned host tensors, "
-                                      "copies on a second stream overlapping the previous/next step"}
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
     peak, peak_kind = hbm_peak()
-    # per-kernel rooflines for the stages that are a single kernel of ours
-    kernels = {}
-    for st, t_ms in stages.items():
-        sb = stage_bytes(st, w, hi - lo)
-        if sb is None or t_ms <= 0:
-            continue
-        hbm_b, chip_b = sb
-        ach = hbm_b / (t_ms / 1e3) / 1e9
-        kernels[st] = {"ms_per_step": round(t_ms, 3), "hbm_bytes": hbm_b,
-                       "achieved_gbs": round(ach, 1), "hbm_frac": round(ach / peak, 4),
-                       "onchip_tap_bytes": chip_b,
-                       "onchip_tbs": round(chip_b / (t_ms / 1e3) / 1e12, 2)}
-    roofline = None
-    if kernels:
-        st = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
-        kk = kernels[st]
-        roofline = {"kernel": st, "bound": "hbm", "achieved": kk["achieved_gbs"], "peak": peak,
-                    "unit": "GB/s", "frac": kk["hbm_frac"], "traffic": TRAFFIC.get(st),
-                    "peak_kind": peak_kind,
-                    "note": "achieved = compulsory bytes / CUDA-event stage time (serialised stage pass); these "
-                            "gathers/spreads are bound on chip (tap traffic, onchip_tbs)",
-                    "onchip_tbs": kk["onchip_tbs"]}
+    stages, kernels, roofline = roofline_from_stages(lib, proj._h, args.steps, peak, peak_kind,
+                                                     TRAFFIC[direction])
+    lib.cbn_projector_set_timing(proj._h, 0)
+    stats = proj.plan_stats()
+
+    e2e = e2e_proj = None
+    if not args.no_e2e:
+        if d.world == 1:
+            # the drop-in API itself: host float64 numpy in, float64 results out
+            # (nufft_forward_project -> list[DetectorFrame]; nufft_backproject -> Volume3D)
+            if fwd:
+                vol_api = Volume3D(vol_host, w.voxel)
+
+                def api():
+                    return pl.nufft_forward_project(vol_api, w.geom, w.cfg)
+                h2d, d2h = vol_host.size * 4, V * w.geom.nu * w.geom.nv * 4
+            else:
+                fr = x_dev.cpu().numpy().astype(np.float64)
+                frames_api = [DetectorFrame(k, fr[k], w.geom.pixel_mm) for k in range(V)]
+
+                def api():
+                    return pl.nufft_backproject(frames_api, w.geom, w.cfg, w.n, w.voxel)
+                h2d, d2h = V * w.geom.nu * w.geom.nv * 4, w.n ** 3 * 4
+            api()
+            api()
+            w0 = time.perf_counter()
+            e_ms = timed(api, args.steps, d, stream)
+            wall = time.perf_counter() - w0
+            e2e = {"value": round(V * args.steps / (e_ms / 1e3), 3), "unit": "views/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "ms_per_step": round(e_ms / args.steps, 3), "wall_s": round(wall, 3),
+                   "api": ("pipeline.nufft_forward_project(Volume3D float64) -> list[DetectorFrame] "
+                           "float64" if fwd else
+                           "pipeline.nufft_backproject(list[DetectorFrame] float64) -> Volume3D "
+                           "float64") + "; host conversions on threads via pinned staging"}
+        e2e_proj = e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d, stream)
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(w, direction, n_samples=1)
-    out = {
-        "metric": "cone-beam views/s (NUFFT forward projector)" if direction == 1
-        else "cone-beam views/s (NUFFT backprojector)",
-        "value": round(value, 3),
-        "unit": "views/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": max(args.warmup, 3),
-        "ms_per_step": round(ms_max / args.steps, 3),
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
+    if d.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_forward(w) if fwd else cpu_backward(w)
+    del proj
+    gc.collect()
+    torch.cuda.empty_cache()
+    return {
+        "metric": "cone-beam views/s (NUFFT " + ("forward projector)" if fwd else "backprojector)"),
+        "value": round(value, 3), "unit": "views/s", "n_gpus": d.world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c64/f32 (fp64 index math)",
         "data": f"synthetic: seeded random-ellipsoid phantom (BASELINE {w.name})",
-        "config": {"workload": f"{w.name} {args.direction}: {w.n}^3 volume, "
+        "config": {"workload": f"{w.name} {direction}: {w.n}^3 volume, "
                                f"{w.spec.n_rho}x{w.spec.n_theta}x{w.spec.n_phi} radial lattice, "
                                f"{V} views of {w.geom.nu}^2, KB J=6 sigma=2, resample J=3",
                    "views": V, "views_per_rank": hi - lo,
-                   "parallelism": f"views sharded x{world}" + (
-                       "" if world == 1 else ", radial nodes sharded, NCCL all-reduce of the "
-                       + ("lattice" if direction == 1 else "lattice + grid")),
-                   "l2": "working set > L2 (resample grid 2.4 GB per view batch)"},
-        "e2e": e2e,
-        "gpu_launches": int(launches),
-        "gpu_launches_per_step": int(launches) // max(args.steps, 1),
-        "clocks": clk,
-        "roofline": roofline,
-        "kernels": kernels,
+                   "parallelism": f"views sharded x{d.world}" + (
+                       "" if d.world == 1 else ", radial nodes sharded, NCCL collectives"),
+                   "l2": "inputs in HBM; working set > L2 every step (resample grid "
+                         f"{stats.get('fwd_resample_cells', stats.get('bp_resample_cells', 0)) * 4 / 1e9:.1f}"
+                         " GB), no flush needed",
+                   "plan_s": round(plan_s, 3)},
+        "e2e": e2e, "e2e_projector": e2e_proj,
+        "gpu_launches": int(launches), "gpu_launches_per_step": int(launches) // max(args.steps, 1),
+        "clocks": clk, "roofline": roofline, "kernels": kernels,
         "stages_ms_per_step": {k: round(v, 3) for k, v in stages.items()},
-        "cpu_baseline": cpu,
+        "plan_stats": stats, "cpu_baseline": cpu,
     }
-    print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+
+
+def e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d: Dist, stream):
+    """Projector API with pinned host tensors, copies on a second stream
+    overlapping the previous/next step (a serving loop)."""
+    import torch
+    if fwd:
+        host_in = torch.from_numpy(vol_host).pin_memory()
+        host_out = torch.empty((hi - lo, w.geom.nu, w.geom.nv), dtype=torch.float32).pin_memory()
+    else:
+        host_in = x_dev.cpu().pin_memory()
+        host_out = torch.empty((w.n,) * 3, dtype=torch.float32).pin_memory()
+
+    def run(dev):
+        if fwd:
+            return proj.forward_sharded(dev, lo, hi) if d.world > 1 else proj.forward(dev, lo, hi)
+        if d.world > 1:
+            return proj.backproject_sharded(dev[lo:hi].contiguous(), lo, hi)
+        return proj.backproject(dev)
+
+    copy_s = torch.cuda.Stream()
+    dev_in = [torch.empty(host_in.shape, dtype=host_in.dtype, device="cuda") for _ in range(2)]
+    host_outs = [host_out, torch.empty_like(host_out).pin_memory()]
+    in_ready = [torch.cuda.Event() for _ in range(2)]
+    out_ready = [torch.cuda.Event() for _ in range(2)]
+
+    def pipeline(nsteps, start_event=None):
+        with torch.cuda.stream(copy_s):
+            if start_event is not None:
+                copy_s.wait_event(start_event)
+            dev_in[0].copy_(host_in, non_blocking=True)
+            in_ready[0].record(copy_s)
+        for k in range(nsteps):
+            slot = k % 2
+            if k + 1 < nsteps:
+                with torch.cuda.stream(copy_s):
+                    if k >= 1:
+                        copy_s.wait_event(out_ready[1 - slot])
+                    dev_in[1 - slot].copy_(host_in, non_blocking=True)
+                    in_ready[1 - slot].record(copy_s)
+            stream.wait_event(in_ready[slot])
+            out = run(dev_in[slot])
+            out_ready[slot].record(stream)
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(out_ready[slot])
+                host_outs[slot].copy_(out, non_blocking=True)
+            out.record_stream(copy_s)
+
+    pipeline(2)
+    torch.cuda.synchronize()
+    d.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    pipeline(args.steps, e0)
+    e1.record(copy_s)
+    torch.cuda.synchronize()
+    d.barrier()
+    e_ms = d.max([e0.elapsed_time(e1)])[0]
+    return {"value": round(w.geom.n_views * args.steps / (e_ms / 1e3), 3), "unit": "views/s",
+            "h2d_bytes_per_step": int(host_in.numel() * 4),
+            "d2h_bytes_per_step": int(host_out.numel() * 4),
+            "api": "Projector.forward/backproject on pinned float32 tensors, H2D/D2H on a copy "
+                   "stream overlapping the neighbouring steps"}
 
 
 # ------------------------------------------- config 4: NUFFT stress microbench
@@ -384,46 +406,39 @@ C4_GRID = 256
 C4_J = 8
 
 
-def run_nufft4(args):
+def measure_nufft4(args, d: Dist):
     """BASELINE config 4: type-2 gather + type-1 spread of 100M float32 points
     (i.i.d. uniform in [-pi, pi)^3) against a 256^3 CN(0,1) grid, KB J=8,
-    sigma 2.  One step = one type-2 and one type-1 over every point; the
-    metric counts points per second through that pair.  Under torchrun the
-    points are split evenly across ranks; type-2 needs no exchange (x is
-    replicated), type-1's 256^3 outputs are summed and scattered by z-slab
-    with one NCCL reduce-scatter (linear, so reducing after the crop moves
-    1/8 of the oversampled grid's bytes)."""
+    sigma 2.  One step = one type-2 and one type-1 over every point.  The
+    headline excludes the plan (bin sort + LS fit, once per node set, as the
+    reference's plan_nufft is); ``value_with_sort`` re-sorts the points every
+    step ("sort + gather", "sort + spread").  Under torchrun the
+    points are split evenly across ranks; type-1's 256^3 outputs are summed
+    and scattered by z-slab with one NCCL reduce-scatter."""
     import torch
     import torch.distributed as dist
     from paper_1605_05231_b200 import _lib, nufft
     from paper_1605_05231_b200.workloads import config4_inputs
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     m_total = int(os.environ.get("CBN_C4_POINTS", C4_POINTS))
     x_host, pts = config4_inputs(n_points=m_total, grid=C4_GRID)
-    lo = m_total * rank // world
-    hi = m_total * (rank + 1) // world
+    lo = m_total * d.rank // d.world
+    hi = m_total * (d.rank + 1) // d.world
     pts = np.ascontiguousarray(pts[lo:hi])
     m = hi - lo
     lib = _lib.load()
+    stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
     tp = time.perf_counter()
     plan = nufft.plan_nufft((C4_GRID,) * 3, pts, 2.0, C4_J)
     torch.cuda.synchronize()
     plan_s = time.perf_counter() - tp
-    stream = torch.cuda.current_stream()
-    import ctypes
     sp = ctypes.c_void_p(stream.cuda_stream)
     x = torch.from_numpy(x_host).cuda()
     y = torch.empty(m, dtype=torch.complex64, device="cuda")
     xa = torch.empty((C4_GRID,) * 3, dtype=torch.complex64, device="cuda")
-    slab = torch.empty((C4_GRID // world, C4_GRID, C4_GRID), dtype=torch.complex64, device="cuda") \
-        if world > 1 else None
+    slab = torch.empty((C4_GRID // d.world, C4_GRID, C4_GRID), dtype=torch.complex64,
+                       device="cuda") if d.world > 1 else None
 
     def type2():
         _lib.check(lib.cbn_nufft_type2(plan.handle, ctypes.c_void_p(x.data_ptr()),
@@ -432,24 +447,22 @@ def run_nufft4(args):
     def type1():
         _lib.check(lib.cbn_nufft_type1(plan.handle, ctypes.c_void_p(y.data_ptr()),
                                        ctypes.c_void_p(xa.data_ptr()), sp))
-        if world > 1:
-            dist.reduce_scatter_tensor(slab, xa)
+        if d.world > 1:
+            dist.reduce_scatter_tensor(torch.view_as_real(slab), torch.view_as_real(xa))
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    def resort():
+        _lib.check(lib.cbn_nufft_resort(plan.handle, sp))
 
     for _ in range(max(args.warmup, 3)):
         type2()
         type1()
     torch.cuda.synchronize()
-    barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    d.barrier()
+    clocks = ClockSampler(d.local).start()
     n0 = lib.cbn_launch_count()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
     torch.cuda.synchronize()
-    barrier()
+    d.barrier()
     ev[0].record(stream)
     for k in range(args.steps):
         type2()
@@ -457,111 +470,287 @@ def run_nufft4(args):
         type1()
         ev[2 * k + 2].record(stream)
     torch.cuda.synchronize()
-    barrier()
+    d.barrier()
     launches = lib.cbn_launch_count() - n0
     clk = clocks.stop()
     t2 = sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps)) / args.steps
     t1 = sum(ev[2 * k + 1].elapsed_time(ev[2 * k + 2]) for k in range(args.steps)) / args.steps
     ms = ev[0].elapsed_time(ev[-1])
-    tt = torch.tensor([ms, t2, t1], device="cuda")
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms_max, t2, t1 = (float(v) for v in tt.tolist())
-    value = m_total * args.steps / (ms_max / 1e3) / 1e6
+    ms, t2, t1 = d.max([ms, t2, t1])
+    value = m_total * args.steps / (ms / 1e3) / 1e6
+
+    # the same steps with the device bin sort redone every step
+    def step_sorted():
+        resort()
+        type2()
+        type1()
+    step_sorted()
+    ms_sorted = timed(step_sorted, args.steps, d, stream)
+    ts = timed(resort, args.steps, d, stream) / args.steps
+    value_sorted = m_total * args.steps / (ms_sorted / 1e3) / 1e6
 
     e2e = None
-    if not args.no_e2e:
-        # public API with pinned host buffers: x and the node values in, results out
-        hx = torch.from_numpy(x_host).pin_memory()
-        hy = torch.from_numpy(np.zeros(m, np.complex64)).pin_memory()
-        hxa = torch.empty((C4_GRID,) * 3, dtype=torch.complex64).pin_memory()
+    if not args.no_e2e and d.world == 1:
+        # the drop-in API with host numpy buffers: nufft_forward(plan, x) ->
+        # complex128 node values; nufft_adjoint(plan, y) -> complex128 grid
+        x128 = x_host.astype(np.complex128)
+        y128 = np.zeros(m, np.complex128)
 
-        def e2e_step():
-            xd = nufft.nufft_forward(plan, hx.to("cuda", non_blocking=True))
-            hy.copy_(xd, non_blocking=True)
-            yd = hy.to("cuda", non_blocking=True)
-            hxa.copy_(nufft.nufft_adjoint(plan, yd), non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        et = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_ms = float(et.item())
-        e2e = {"value": round(m_total * args.steps / (e_ms / 1e3) / 1e6, 3), "unit": "Msamples/s",
-               "h2d_bytes_per_step": int(hx.numel() * 8 + hy.numel() * 8),
-               "d2h_bytes_per_step": int(hy.numel() * 8 + hxa.numel() * 8),
-               "api": "nufft_forward / nufft_adjoint on pinned host-staged tensors"}
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+        def api():
+            nufft.nufft_forward(plan, x128)
+            nufft.nufft_adjoint(plan, y128)
+        api()
+        e_ms = timed(api, max(2, args.steps // 4), d, stream)
+        nst = max(2, args.steps // 4)
+        e2e = {"value": round(m_total * nst / (e_ms / 1e3) / 1e6, 3), "unit": "Msamples/s",
+               "h2d_bytes_per_step": int(x128.size * 16 + y128.size * 16),
+               "d2h_bytes_per_step": int(m * 16 + x128.size * 16),
+               "steps": nst,
+               "api": "nufft.nufft_forward / nufft_adjoint with host complex128 numpy in and out "
+                      "(the reference's types)"}
     peak, peak_kind = hbm_peak()
     K3 = (2 * C4_GRID) ** 3
-    # compulsory bytes: gather reads the oversampled grid once + 12 B nodes +
-    # 8 B output per point; spread reads 12 B nodes + 8 B values and writes
-    # the grid once
-    gb = {"type2_step": 8.0 * K3 + 20.0 * m, "type1_step": 8.0 * K3 + 20.0 * m}
+    # compulsory bytes: the oversampled grid once (8 B/cell), 12 B float32
+    # coordinates + 8 B value per point; the FFT/pad/crop passes not counted
+    gbytes = 8.0 * K3 + 20.0 * m
     taps = C4_J ** 3
+    # serialised pass with the plan's stage events: kernel times + bytes
+    lib.cbn_nufft_set_timing(plan.handle, 1)
+    for _ in range(args.steps):
+        resort()
+        type2()
+        type1()
+    torch.cuda.synchronize()
+    st_t = stage_times_nufft(lib, plan, args.steps)
+    lib.cbn_nufft_set_timing(plan.handle, 0)
     kernels = {
-        "type2": {"ms_per_step": round(t2, 3), "achieved_gbs": round(gb["type2_step"] / t2 / 1e6, 1),
-                  "onchip_tap_bytes": 8.0 * taps * m,
-                  "onchip_tbs": round(8.0 * taps * m / t2 / 1e9, 2),
+        "type2": {"ms_per_step": round(t2, 3), "hbm_bytes": gbytes,
+                  "achieved_gbs": round(gbytes / t2 / 1e6, 1),
+                  "onchip_bytes": 8.0 * taps * m, "onchip_tbs": round(8.0 * taps * m / t2 / 1e9, 2),
                   "msamples_s": round(m / t2 / 1e3, 2)},
-        "type1": {"ms_per_step": round(t1, 3), "achieved_gbs": round(gb["type1_step"] / t1 / 1e6, 1),
-                  "onchip_tap_bytes": 16.0 * taps * m,          # shared-memory read + write per tap
+        "type1": {"ms_per_step": round(t1, 3), "hbm_bytes": gbytes,
+                  "achieved_gbs": round(gbytes / t1 / 1e6, 1),
+                  "onchip_bytes": 16.0 * taps * m,
                   "onchip_tbs": round(16.0 * taps * m / t1 / 1e9, 2),
                   "msamples_s": round(m / t1 / 1e3, 2)},
+        "sort": {"ms_per_step": round(ts, 3)},
     }
-    st = "type1" if t1 >= t2 else "type2"
-    roofline = {"kernel": st + " (whole transform incl. FFT)", "bound": "hbm",
-                "achieved": kernels[st]["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                "frac": round(kernels[st]["achieved_gbs"] / peak, 4), "traffic": None,
-                "peak_kind": peak_kind, "onchip_tbs": kernels[st]["onchip_tbs"]}
+    kernels.update(st_t)
+    dom = "gather" if st_t.get("gather", {}).get("ms_per_step", 0) >= \
+        st_t.get("spread", {}).get("ms_per_step", 0) else "spread"
+    roofline = None
+    if dom in st_t:
+        kk = st_t[dom]
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": kk["achieved_gbs"], "peak": peak,
+                    "unit": "GB/s", "frac": kk["hbm_frac"], "traffic": None,
+                    "peak_kind": peak_kind, "algorithmic_bytes_per_step": kk["hbm_bytes"],
+                    "onchip_tbs": kk["onchip_tbs"], "onchip_frac": kk["onchip_frac"]}
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample_nufft4()
-    out = {
+    if d.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_nufft4()
+    del plan
+    gc.collect()
+    torch.cuda.empty_cache()
+    return {
         "metric": "NUFFT nonuniform Msamples/s (fwd+adj)",
-        "value": round(value, 3), "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max / args.steps, 3),
+        "value": round(value, 3), "value_with_sort": round(value_sorted, 3),
+        "unit": "Msamples/s", "n_gpus": d.world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms / args.steps, 3),
+        "ms_per_step_with_sort": round(ms_sorted / args.steps, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c64/f32 (fp64 index math)",
         "data": "synthetic: 256^3 CN(0,1) grid (seed 4), float32 points U[-pi,pi)^3 (seed 5)",
         "config": {"workload": f"config4: {m_total} points, {C4_GRID}^3 grid, KB J={C4_J}, sigma 2, "
                                "one type-2 + one type-1 per step",
-                   "points_per_rank": m, "parallelism": f"points sharded x{world}",
+                   "points_per_rank": m, "parallelism": f"points sharded x{d.world}",
                    "plan_s": round(plan_s, 3),
-                   "l2": "working set > L2 (1.07 GB oversampled grid, 1.2 GB nodes)"},
+                   "l2": "working set > L2 (1.07 GB oversampled grid, 1.2 GB coordinates)"},
         "e2e": e2e, "gpu_launches": int(launches),
         "gpu_launches_per_step": int(launches) // max(args.steps, 1),
         "clocks": clk, "roofline": roofline, "kernels": kernels,
-        "stages_ms_per_step": {"type2": round(t2, 3), "type1": round(t1, 3)},
+        "stages_ms_per_step": {"type2": round(t2, 3), "type1": round(t1, 3), "sort": round(ts, 3)},
         "cpu_baseline": cpu,
     }
-    print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
-def cpu_sample_nufft4(n_sample: int = 1 << 17):
-    """Oracle port on a 2^17-point sample of config 4 (plan excluded, like the
-    GPU value): per-point type-2 + type-1 cost, plus one 512^3 FFT per
-    transform, extrapolated to 100M points."""
+def stage_times_nufft(lib, plan, steps):
+    """Sort / gather / spread kernel times per step from the plan's own stage
+    events (cbn_nufft_stage_times), with their algorithmic bytes."""
+    peak, _ = hbm_peak()
+    cnt = ctypes.c_int32(16)
+    ms = (ctypes.c_double * 16)()
+    hb = (ctypes.c_double * 16)()
+    cb = (ctypes.c_double * 16)()
+    names = ctypes.create_string_buffer(1024)
+    if lib.cbn_nufft_stage_times(plan.handle, ms, hb, cb, ctypes.byref(cnt), names, 1024) != 0:
+        return {}
+    out = {}
+    for i, nm in enumerate(names.value.decode().split(";")[:cnt.value]):
+        t, hbm, chip = ms[i] / steps, hb[i] / steps, cb[i] / steps
+        if t <= 0:
+            continue
+        ach = hbm / (t / 1e3) / 1e9
+        out[nm] = {"ms_per_step": round(t, 3), "hbm_bytes": hbm, "achieved_gbs": round(ach, 1),
+                   "hbm_frac": round(ach / peak, 4), "onchip_bytes": chip,
+                   "onchip_tbs": round(chip / (t / 1e3) / 1e12, 2),
+                   "onchip_frac": round(chip / (t / 1e3) / 1e12 / SMEM_TBS, 3)}
+    return out
+
+
+# --------------------------------------------------------- CPU (oracle) legs
+def _oracle():
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import cbn_oracle as orc
+    orc.WORKERS = os.cpu_count() or 1
+    return orc
+
+
+SPEC_PIECE = 1 << 19     # nodes of one spectrum sub-plan timed per sample (of 2^21)
+
+
+def cpu_forward_pieces(w, k: int, orc, state):
+    """Piece k of the config's forward projector on the oracle port:
+    even k: plan + gather of SPEC_PIECE nodes of one spectrum sub-plan
+    (per-node cost); odd k: one view's umbrella targets, resample plan + apply
+    and reverse Grangeat (per-view cost).  Fixed per-call costs -- the sub-plan
+    pad + 512^3 FFT and the Grangeat plan -- are timed once in `state`."""
+    spec, cfg, geom = w.spec, w.cfg, w.geom
+    M = spec.n_rho * spec.n_theta * spec.n_phi
+    if "nodes" not in state:
+        state["nodes"] = orc.wrap(orc.radial_direction_nodes(spec, w.voxel))
+        state["vol"] = w.volume(np.float64).astype(np.complex128)
+        t = time.perf_counter()
+        g = np.zeros((2 * w.n,) * 3, np.complex128)
+        orc.sfft.fftn(g, overwrite_x=True, workers=orc.WORKERS)
+        state["t_fft"] = time.perf_counter() - t
+        t = time.perf_counter()
+        state["gp"] = orc.make_grangeat(geom, cfg.n_mu, cfg.n_t, t_pitch_mm=cfg.t_pitch_mm,
+                                        t_taper=cfg.t_taper)
+        state["t_gp"] = time.perf_counter() - t
+        rng = np.random.default_rng(0)
+        state["lattice"] = (rng.standard_normal((spec.n_rho, spec.n_theta, spec.n_phi))
+                            + 1j * rng.standard_normal((spec.n_rho, spec.n_theta, spec.n_phi)))
+        state["node"], state["view"] = [], []
+    t = time.perf_counter()
+    if k % 2 == 0:
+        chunk = (k // 2) % max(1, -(-M // orc.PLAN_CHUNK))
+        lo = chunk * orc.PLAN_CHUNK
+        hi = min(lo + SPEC_PIECE, M)
+        plan = orc.make_plan((w.n,) * 3, state["nodes"][lo:hi], 2.0, 6)
+        orc.type2(plan, state["vol"])
+        # per-node part: plan + gather (the sub-plan's pad + FFT is the fixed t_fft)
+        dt = max(time.perf_counter() - t - state["t_fft"], 1e-9)
+        state["node"].append(dt / (hi - lo))
+    else:
+        # one reference view batch (one view at configs 2/3): per-batch resample
+        # plan + apply, then reverse Grangeat of each of its views
+        per_view = cfg.n_mu * cfg.n_t
+        batches = orc.view_batches(geom.n_views, per_view)
+        batch = batches[(k // 2 * 37) % len(batches)]
+        targets, valid = orc.umbrella_targets(geom, spec, batch, cfg.n_mu, cfg.n_t, cfg.t_pitch_mm)
+        rs = orc.make_resampler(spec, targets, cfg.rho_pad, cfg.resample_j)
+        vals = np.real(orc.resample_forward(rs, state["lattice"]))
+        vals[~valid] = 0.0
+        for i in range(len(batch)):
+            orc.grangeat_reverse(vals[i * per_view:(i + 1) * per_view].reshape(cfg.n_mu, cfg.n_t),
+                                 state["gp"])
+        state["view"].append((time.perf_counter() - t) / len(batch))
+    return time.perf_counter() - t
+
+
+def cpu_forward_value(w, orc, state):
+    M = w.spec.n_rho * w.spec.n_theta * w.spec.n_phi
+    n_chunks = -(-M // orc.PLAN_CHUNK)
+    per_node = float(np.mean(state["node"])) if state["node"] else 0.0
+    per_view = float(np.mean(state["view"])) if state["view"] else 0.0
+    total = n_chunks * state["t_fft"] + M * per_node + state["t_gp"] + w.geom.n_views * per_view
+    return w.geom.n_views / total, total, per_node, per_view, n_chunks
+
+
+def cpu_forward(w, pieces: int = 2):
+    orc = _oracle()
+    state = {}
+    t0 = time.perf_counter()
+    for k in range(pieces):
+        cpu_forward_pieces(w, k, orc, state)
+    value, total, per_node, per_view, n_chunks = cpu_forward_value(w, orc, state)
+    return {"value": round(value, 6), "unit": "views/s", "cores": os.cpu_count() or 1,
+            "kind": "port",
+            "sample": f"oracle port (reference algorithm, numpy/scipy): {n_chunks} spectrum "
+                      f"sub-plans x (pad + {2 * w.n}^3 FFT {state['t_fft']:.2f}s) + "
+                      f"{M_str(w)} nodes x {per_node * 1e6:.2f}us (plan + gather, sampled on "
+                      f"{SPEC_PIECE} nodes) + Grangeat plan {state['t_gp']:.2f}s once + "
+                      f"{w.geom.n_views} views x {per_view:.2f}s (targets, resample plan + apply, "
+                      f"reverse Grangeat; sampled on {len(state['view'])} view batch(es)); extrapolated "
+                      f"= {total:.0f}s per step; scipy.fft on all cores, numpy gather one core",
+            "extrapolated": True, "sample_wall_s": round(time.perf_counter() - t0, 1)}
+
+
+def M_str(w):
+    return str(w.spec.n_rho * w.spec.n_theta * w.spec.n_phi)
+
+
+def cpu_backward(w):
+    """Oracle port of the config's backprojector on bounded samples: one view
+    batch (forward Grangeat of its views, targets, resample plan, transposed
+    resample of values and mask) and the plan + spread of SPEC_PIECE nodes of
+    one 3D adjoint sub-plan, plus the per-sub-plan (2N)^3 inverse FFT;
+    extrapolated to every batch and sub-plan."""
+    from paper_1605_05231_b200.geometry import RadialGridSpec
+    orc = _oracle()
+    cfg, geom = w.cfg, w.geom
+    t0 = time.perf_counter()
+    n = w.n
+    bspec = RadialGridSpec(2 * int(np.ceil(1.5 * n / 2.0)), w.spec.n_theta, w.spec.n_phi,
+                           n * w.voxel * np.sqrt(3.0) / 2.0)
+    n_t = 2 * geom.nu
+    pad = min(bspec.n_rho // 8, 32)
+    t = time.perf_counter()
+    gp = orc.make_grangeat(geom, cfg.n_mu, n_t, t_pitch_mm=None)
+    t_gp = time.perf_counter() - t
+    batches = orc.view_batches(geom.n_views, cfg.n_mu * n_t)
+    batch = batches[0]
+    rng = np.random.default_rng(1)
+    frames = rng.standard_normal((len(batch), geom.nu, geom.nv))
+    t = time.perf_counter()
+    vals = np.concatenate([orc.grangeat_forward(frames[i], gp).ravel() for i in range(len(batch))])
+    targets, valid = orc.umbrella_targets(geom, bspec, batch, cfg.n_mu, n_t, gp.dt)
+    rs = orc.make_resampler(bspec, targets, pad, cfg.resample_j, cfg.oversample_factor)
+    orc.resample_adjoint(rs, np.where(valid, vals, 0.0).astype(np.complex128))
+    orc.resample_adjoint(rs, valid.astype(np.complex128))
+    t_batch = time.perf_counter() - t
+    del rs
+    M = bspec.n_rho * bspec.n_theta * bspec.n_phi
+    nodes = orc.wrap(orc.radial_direction_nodes(bspec, w.voxel))[:SPEC_PIECE]
+    y = np.ones(nodes.shape[0], np.complex128)
+    t = time.perf_counter()
+    g = np.zeros((2 * n,) * 3, np.complex128)
+    orc.sfft.ifftn(g, overwrite_x=True, workers=orc.WORKERS)
+    t_fft = time.perf_counter() - t
+    t = time.perf_counter()
+    plan = orc.make_plan((n,) * 3, nodes, 2.0, 6)
+    orc.type1(plan, y)
+    per_node = max(time.perf_counter() - t - t_fft, 1e-9) / nodes.shape[0]
+    n_chunks = -(-M // orc.PLAN_CHUNK)
+    total = t_gp + len(batches) * t_batch + n_chunks * t_fft + M * per_node
+    return {"value": round(geom.n_views / total, 6), "unit": "views/s", "cores": os.cpu_count() or 1,
+            "kind": "port",
+            "sample": f"oracle port: Grangeat plan {t_gp:.2f}s once + {len(batches)} view batches x "
+                      f"{t_batch:.2f}s (batch 0 of {len(batch)} views: forward Grangeat, targets, "
+                      f"resample plan, transposed resample of values and mask) + {n_chunks} "
+                      f"adjoint sub-plans x {2 * n}^3 IFFT {t_fft:.2f}s + {M} nodes x "
+                      f"{per_node * 1e6:.2f}us (plan + spread, sampled on {SPEC_PIECE} nodes); "
+                      f"extrapolated = {total:.0f}s per step",
+            "extrapolated": True, "sample_wall_s": round(time.perf_counter() - t0, 1)}
+
+
+def cpu_nufft4(n_sample: int = 1 << 17):
+    """Oracle port on a 2^17-point sample of config 4 (plan excluded, like the
+    GPU headline): per-point type-2 + type-1 cost plus one 512^3 FFT per
+    transform, extrapolated to 100M points."""
     from paper_1605_05231_b200.workloads import config4_inputs
-    cores = os.cpu_count() or 1
-    orc.WORKERS = cores
+    orc = _oracle()
+    t0 = time.perf_counter()
     x, pts = config4_inputs(n_points=n_sample, grid=C4_GRID)
     x = x.astype(np.complex128)
     plan = orc.make_plan((C4_GRID,) * 3, pts.astype(np.float64), 2.0, C4_J)
@@ -572,107 +761,74 @@ def cpu_sample_nufft4(n_sample: int = 1 << 17):
     t = time.perf_counter()
     orc.type1(plan, y)
     t1 = time.perf_counter() - t
-    # separate the FFT (fixed per transform) from the per-point part
     g = np.zeros((2 * C4_GRID,) * 3, np.complex128)
     t = time.perf_counter()
     orc.sfft.fftn(g, overwrite_x=True, workers=orc.WORKERS)
     tf = time.perf_counter() - t
     per_point = max(t2 + t1 - 2 * tf, 1e-12) / n_sample
     total = per_point * C4_POINTS + 2 * tf
-    return {"value": round(C4_POINTS / total / 1e6, 6), "unit": "Msamples/s", "cores": cores,
-            "kind": "port",
+    return {"value": round(C4_POINTS / total / 1e6, 6), "unit": "Msamples/s",
+            "cores": os.cpu_count() or 1, "kind": "port",
             "sample": f"oracle port: type-2 {t2:.2f}s + type-1 {t1:.2f}s on {n_sample} points "
                       f"(512^3 FFT {tf:.2f}s each), per-point part extrapolated to {C4_POINTS}",
-            "extrapolated": True}
+            "extrapolated": True, "sample_wall_s": round(time.perf_counter() - t0, 1)}
 
 
-# --------------------------------------------------------- CPU (oracle) leg
-def cpu_sample(w, direction: int, n_samples: int = 1):
-    """Time the oracle port on a bounded sample and extrapolate to the full
-    workload: one 2^21-node spectrum sub-plan (of ceil(M / 2^21)) and the
-    resample + reverse Grangeat of one view (of V)."""
-    sys.path.insert(0, os.path.join(REPO, "oracle"))
-    import cbn_oracle as orc
-    cores = os.cpu_count() or 1
-    orc.WORKERS = cores
-    spec, cfg, geom = w.spec, w.cfg, w.geom
-    M = spec.n_rho * spec.n_theta * spec.n_phi
-    n_chunks = -(-M // orc.PLAN_CHUNK)
-    vol = w.volume(np.float64)
-    nodes_all = None
-    t_chunk, t_view = [], []
-    rng = np.random.default_rng(0)
-    for s in range(n_samples):
-        if direction != 1:
-            break
-        # spectrum sub-plan sample
-        t = time.perf_counter()
-        if nodes_all is None:
-            nodes_all = orc.wrap(orc.radial_direction_nodes(spec, w.voxel))
-        lo = (s % n_chunks) * orc.PLAN_CHUNK
-        hi = min(lo + orc.PLAN_CHUNK, M)
-        plan = orc.make_plan((w.n,) * 3, nodes_all[lo:hi], 2.0, 6)
-        orc.type2(plan, vol.astype(np.complex128))
-        t_chunk.append(time.perf_counter() - t)
-        del plan
-        # one view: umbrella targets, per-batch resample plan + apply, reverse Grangeat
-        t = time.perf_counter()
-        lattice = (rng.standard_normal((spec.n_rho, spec.n_theta, spec.n_phi))
-                   + 1j * rng.standard_normal((spec.n_rho, spec.n_theta, spec.n_phi)))
-        t_lat = time.perf_counter() - t
-        t = time.perf_counter()
-        per_view = cfg.n_mu * cfg.n_t
-        batch = orc.view_batches(geom.n_views, per_view)[s % geom.n_views]
-        targets, valid = orc.umbrella_targets(geom, spec, batch, cfg.n_mu, cfg.n_t, cfg.t_pitch_mm)
-        rs = orc.make_resampler(spec, targets, cfg.rho_pad, cfg.resample_j)
-        vals = np.real(orc.resample_forward(rs, lattice))
-        gp = orc.make_grangeat(geom, cfg.n_mu, cfg.n_t, t_pitch_mm=cfg.t_pitch_mm,
-                               t_taper=cfg.t_taper)
-        for i in range(len(batch)):
-            orc.grangeat_reverse(vals[i * per_view:(i + 1) * per_view].reshape(cfg.n_mu, cfg.n_t), gp)
-        t_view.append((time.perf_counter() - t) / len(batch))
-        del lattice, rs
-    if direction != 1:
-        return None
-    tc, tv = float(np.mean(t_chunk)), float(np.mean(t_view))
-    total = n_chunks * tc + geom.n_views * tv
-    return {"value": round(geom.n_views / total, 6), "unit": "views/s", "cores": cores,
-            "kind": "port",
-            "sample": f"oracle port: {len(t_chunk)} of {n_chunks} spectrum sub-plans (2^21 nodes) "
-                      f"+ {len(t_view)} view(s) of {geom.n_views} (resample plan+apply, reverse "
-                      f"Grangeat); extrapolated linearly; sub-plan {tc:.2f}s, view {tv:.2f}s; "
-                      "scipy.fft uses all cores, the numpy gather/bincount one",
-            "extrapolated": True}
-
-
+# ------------------------------------------------------------ reference arm
 def run_reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The reference algorithm on the host cores (oracle port; the reference
+    package cannot travel to the GPU box).  Each of the K steps times one
+    bounded piece of the config's forward projector (alternately a spectrum
+    sub-plan sample and one view), and the views/s value extrapolates the
+    measured per-node / per-view costs to the whole workload.  ms_per_step is
+    the real time of a step (one piece); the extrapolated time of one full
+    projection is extrapolated_ms_per_projection."""
+    d = Dist()
+    if d.rank != 0:
         return
     from paper_1605_05231_b200.workloads import workload
-    w = workload(args.config)
-    direction = 1 if args.direction == "forward" else 2
-    t0 = time.perf_counter()
-    # each step is one bounded CPU sample (~17 s at config 2); no warm-up is
-    # needed on the CPU and at most 3 samples are taken so the arm stays
-    # within a few minutes for any --steps
-    vals = [cpu_sample(w, direction, 1) for _ in range(max(1, min(args.steps, 3)))]
-    timed = [v for v in vals if v is not None]
-    wall = time.perf_counter() - t0
-    if not timed:
-        print(json.dumps({"impl": "reference", "unavailable": "backprojector CPU sample not implemented"}))
+    if args.config == 4:
+        t0 = time.perf_counter()
+        vals = [cpu_nufft4() for _ in range(max(1, min(args.steps, 3)))]
+        value = float(np.mean([v["value"] for v in vals]))
+        cpu = dict(vals[-1])
+        cpu["value"] = round(value, 6)
+        wall = time.perf_counter() - t0
+        print(json.dumps({
+            "impl": "reference", "metric": "NUFFT nonuniform Msamples/s (fwd+adj)",
+            "value": round(value, 6), "unit": "Msamples/s", "n_gpus": d.world,
+            "steps": len(vals), "warmup": 0, "ms_per_step": round(1e3 * wall / len(vals), 1),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64/c128", "data": "synthetic: config 4 inputs",
+            "config": {"workload": "config4 (CPU oracle port, extrapolated)"}, "cpu_baseline": cpu,
+            "e2e": {"value": round(value, 6), "unit": "Msamples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}, "wall_s": round(wall, 1)}), flush=True)
         return
-    value = float(np.mean([v["value"] for v in timed]))
-    cpu = dict(timed[-1])
-    cpu["value"] = round(value, 6)
+    w = workload(args.config)
+    orc = _oracle()
+    state = {}
+    t0 = time.perf_counter()
+    cpu_forward_pieces(w, 0, orc, state)      # warm-up piece (not counted)
+    state["node"].clear()
+    steps = max(2, args.steps)
+    piece_s = [cpu_forward_pieces(w, k, orc, state) for k in range(steps)]
+    value, total, per_node, per_view, n_chunks = cpu_forward_value(w, orc, state)
+    wall = time.perf_counter() - t0
+    cpu = {"value": round(value, 6), "unit": "views/s", "cores": os.cpu_count() or 1,
+           "kind": "port",
+           "sample": f"oracle port: {steps} pieces (spectrum sub-plan samples of {SPEC_PIECE} "
+                     f"nodes and single views, alternating); per node {per_node * 1e6:.2f}us, "
+                     f"per view {per_view:.2f}s, {n_chunks} x sub-plan FFT {state['t_fft']:.2f}s, "
+                     f"Grangeat plan {state['t_gp']:.2f}s; extrapolated {total:.0f}s per projection",
+           "extrapolated": True}
     out = {"impl": "reference",
            "metric": "cone-beam views/s (NUFFT forward projector)",
-           "value": round(value, 6), "unit": "views/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(1e3 * w.geom.n_views / value, 1),
+           "value": round(value, 6), "unit": "views/s", "n_gpus": d.world, "steps": steps,
+           "warmup": 1, "ms_per_step": round(1e3 * float(np.mean(piece_s)), 1),
+           "extrapolated_ms_per_projection": round(1e3 * total, 1),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "f64/c128", "data": f"synthetic: seeded random-ellipsoid phantom (BASELINE {w.name})",
-           "config": {"workload": f"{w.name} {args.direction} (CPU oracle port, extrapolated)"},
+           "config": {"workload": f"{w.name} forward (CPU oracle port, bounded pieces, extrapolated)"},
            "cpu_baseline": cpu,
            "e2e": {"value": round(value, 6), "unit": "views/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
@@ -680,39 +836,25 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-def run_reference_nufft4(args):
-    if int(os.environ.get("RANK", "0")) != 0:
-        return
-    t0 = time.perf_counter()
-    vals = [cpu_sample_nufft4() for _ in range(max(1, min(args.steps, 3)))]   # <= 3 samples
-    timed = vals
-    value = float(np.mean([v["value"] for v in timed]))
-    cpu = dict(timed[-1])
-    cpu["value"] = round(value, 6)
-    print(json.dumps({
-        "impl": "reference", "metric": "NUFFT nonuniform Msamples/s (fwd+adj)",
-        "value": round(value, 6), "unit": "Msamples/s",
-        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(1e3 * C4_POINTS / (value * 1e6), 1),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/c128",
-        "data": "synthetic: config 4 inputs",
-        "config": {"workload": "config4 (CPU oracle port, extrapolated)"}, "cpu_baseline": cpu,
-        "e2e": {"value": round(value, 6), "unit": "Msamples/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-        "wall_s": round(time.perf_counter() - t0, 1)}), flush=True)
-
-
 def main():
     args = parse_args()
-    if args.config == 4:
-        if args.impl == "reference":
-            run_reference_nufft4(args)
-        else:
-            run_nufft4(args)
-    elif args.impl == "reference":
+    if args.impl == "reference":
         run_reference(args)
+        return
+    d = Dist()
+    d.init()
+    if args.config == 4:
+        out = measure_nufft4(args, d)
     else:
-        run_ours(args)
+        out = measure_projector(args, d, args.config, args.direction)
+        if not args.only and args.config == 2 and args.direction == "forward":
+            out["adjoint"] = measure_projector(args, d, 2, "back")
+            out["nufft4"] = measure_nufft4(args, d)
+    if d.rank == 0:
+        print(json.dumps(out), flush=True)
+    if d.world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

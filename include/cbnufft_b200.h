@@ -79,6 +79,18 @@ int cbn_nufft_type1(cbn_nufft* plan, const void* y, void* x, void* stream);
  * exactly (resampling.py:147-148, SURVEY finding 9) */
 int cbn_nufft_set_phase(cbn_nufft* plan, int32_t on);
 
+/* Re-run the plan's bin sort of its nodes on the device (keys, CUB scans,
+ * scatter, subproblem list, bank interleave; no host round trip) -- the
+ * "sort" of SURVEY 8(d)'s Msamples/s, timed per step by the bench.  2D/3D. */
+int cbn_nufft_resort(cbn_nufft* plan, void* stream);
+/* Stage events + algorithmic bytes (bench): set_timing(1) resets and turns
+ * them on; stage_times returns per-stage ms, compulsory HBM bytes and
+ * on-chip tap bytes since then (names ';'-separated: sort, gather, spread),
+ * synchronises, and resets. */
+int cbn_nufft_set_timing(cbn_nufft* plan, int32_t on);
+int cbn_nufft_stage_times(cbn_nufft* plan, double* ms, double* hbm, double* chip, int32_t* count,
+                          char* names, int32_t names_len);
+
 /* ------------------------------------------------------------ resampling
  * plan_resample / resample_apply / resample_transpose, methods A and B
  * (resampling.py:79-103,136-161,164-196).  targets [host] m x 3 float64
@@ -281,6 +293,13 @@ int cbn_projector_plan_stats(cbn_projector* proj, int64_t* vals, int32_t* count,
  * (names: ';'-separated), then resets if `reset` is non-zero. */
 int cbn_projector_set_timing(cbn_projector* proj, int32_t on);
 int cbn_projector_stage_times(cbn_projector* proj, double* ms, int32_t* count,
+                              char* names, int32_t names_len, int32_t reset);
+
+/* Algorithmic bytes per stage accumulated while timing is on (the bench's
+ * roofline): compulsory HBM bytes and on-chip tap bytes of the work each
+ * stage's kernels did; names ';'-separated; clears the
+ * totals if `reset` is non-zero. */
+int cbn_projector_stage_bytes(cbn_projector* proj, double* hbm, double* chip, int32_t* count,
                               char* names, int32_t names_len, int32_t reset);
 
 /* ------------------------------------------------------------ baseline

@@ -62,6 +62,10 @@ _SIGS = {
     "cbn_nufft_type2": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_nufft_type1": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_nufft_set_phase": (ctypes.c_int, [c_vp, c_i32]),
+    "cbn_nufft_resort": (ctypes.c_int, [c_vp, c_vp]),
+    "cbn_nufft_set_timing": (ctypes.c_int, [c_vp, c_i32]),
+    "cbn_nufft_stage_times": (ctypes.c_int, [c_vp, P_f64, P_f64, P_f64, P_i32, ctypes.c_char_p,
+                                             c_i32]),
     "cbn_resample_create": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, c_i32, P_i32,
                                            c_f64, P_f64, c_i64, P_i64, c_i64, c_vp]),
     "cbn_resample_create_b": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, c_i32,
@@ -100,6 +104,8 @@ _SIGS = {
                                                        c_vp]),
     "cbn_projector_first_indices": (ctypes.c_int, [c_vp, c_i32, c_i32, P_i32, P_i64, c_vp]),
     "cbn_projector_plan_stats": (ctypes.c_int, [c_vp, P_i64, P_i32, ctypes.c_char_p, c_i32, c_vp]),
+    "cbn_projector_stage_bytes": (ctypes.c_int, [c_vp, P_f64, P_f64, P_i32, ctypes.c_char_p, c_i32,
+                                                 c_i32]),
     "cbn_ct_project_linear": (ctypes.c_int, [ctypes.POINTER(Geometry), c_vp, c_i32, c_f64, c_vp,
                                              c_vp]),
     "cbn_launch_count": (ctypes.c_longlong, []),

@@ -453,6 +453,7 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
             std::partial_sum(h.begin(), h.end(), h.begin());
             p->bcol_ptr.upload(h.data(), h.size(), s);
             p->bcol_ent.alloc(sizeof(RsColEntry) * (size_t)std::max(h.back(), 1));
+            p->bcol_n = h.back();
             CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncol, cudaMemcpyHostToDevice,
                                      s));
             k_rs_col_fill<3><<<blocks_for(n, 256), 256, 0, s>>>(
@@ -693,6 +694,18 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             {
                 StageScope st(p->timer, "transpose_spread", s);
                 const unsigned ncol = (unsigned)(x.kd3[0] * x.kd3[1]);
+                {
+                    // values (once), column entries (once), the real grid of
+                    // the used rho planes written once; on chip: entries x
+                    // views (two value loads + weights per entry per cell pair)
+                    double planes = 0;
+                    for (const auto& rn : p->bres_rho_runs) planes += rn.second - rn.first;
+                    p->timer.add_bytes("transpose_spread",
+                                       (den_only ? 0.0 : 4.0 * per_view * nvr) +
+                                           (double)sizeof(RsColEntry) * p->bcol_n +
+                                           4.0 * planes * x.kd3[1] * x.kd3[2],
+                                       (double)sizeof(RsColEntry) * p->bcol_n * (x.kd3[2] / 2));
+                }
                 const RsColEntry* ent = reinterpret_cast<const RsColEntry*>(p->bcol_ent.p);
                 float* gnum = den_only ? nullptr : greal;
                 float* gden = den_only ? greal : nullptr;
@@ -924,6 +937,13 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
     bsrc.tri = c.basis == 0;
     StageScope st_sp(p->timer, "bp_spread", s);
     CBN_CUDA(cudaMemsetAsync(grid, 0, sizeof(float2) * x.k3, s));
+    {
+        // lattice read once, the (2N)^3 grid written once (this part's share);
+        // on chip: J^3 shared-memory read + write per primary node
+        const double f = (double)1.0 / nparts;
+        const double J = sax[0].J;
+        p->timer.add_bytes("bp_spread", f * 8.0 * M + 8.0 * x.k3, f * 16.0 * J * J * J * p->bpairs_n);
+    }
     // this part's share of the bin subproblems (each node belongs to one)
     const BinPlan& bb = p->bspec_bins;
     const int s0 = (int)((int64_t)bb.nsubs * part / nparts);

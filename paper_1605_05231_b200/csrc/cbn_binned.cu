@@ -5,6 +5,8 @@
 
 #include <cstdlib>
 
+#include <cub/device/device_scan.cuh>
+
 namespace cbn {
 
 int spread_warps_override() {
@@ -46,6 +48,53 @@ void finish_bins(BinPlan& bp, DevBuf<int>& keys, DevBuf<int>& counts, int64_t nb
     CBN_CUDA(cudaMemcpyAsync(bp.subs.p, subs.data(), sizeof(SubProblem) * subs.size(),
                              cudaMemcpyHostToDevice, s));
     CBN_CUDA(cudaStreamSynchronize(s));
+    bp.ready = true;
+}
+
+__global__ void k_sub_counts(const int* __restrict__ counts, int64_t nbins, int max_sub,
+                             int* __restrict__ nsub) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nbins) nsub[b] = (counts[b] + max_sub - 1) / max_sub;
+}
+
+__global__ void k_fill_subs(const int* __restrict__ counts, const int* __restrict__ offs,
+                            const int* __restrict__ suboff, int64_t nbins, int max_sub,
+                            SubProblem* __restrict__ subs) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbins) return;
+    const int c = counts[b];
+    int q = suboff[b];
+    for (int st = 0; st < c; st += max_sub)
+        subs[q++] = SubProblem{(int)b, offs[b] + st, min(max_sub, c - st), 0};
+}
+
+void device_bins_finish(BinPlan& bp, DeviceSortScratch& sc, int64_t nbins, int max_sub,
+                        cudaStream_t s) {
+    CBN_REQUIRE(nbins < (1LL << 31) && bp.m < (1LL << 31), "device sort: too many bins or points");
+    const int64_t cap = nbins + (bp.m + max_sub - 1) / max_sub;
+    sc.offs.ensure((size_t)nbins);
+    sc.nsub.ensure((size_t)nbins);
+    sc.suboff.ensure((size_t)nbins);
+    size_t need = 0;
+    CBN_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, sc.counts.p, sc.offs.p, (int)nbins, s));
+    if (need > sc.temp_bytes) {
+        sc.temp.alloc(need);
+        sc.temp_bytes = need;
+    }
+    const unsigned nb = (unsigned)((nbins + 255) / 256);
+    k_sub_counts<<<nb, 256, 0, s>>>(sc.counts.p, nbins, max_sub, sc.nsub.p);
+    CBN_LAUNCH_CHECK();
+    CBN_CUDA(cub::DeviceScan::ExclusiveSum(sc.temp.p, need, sc.counts.p, sc.offs.p, (int)nbins, s));
+    CBN_CUDA(cub::DeviceScan::ExclusiveSum(sc.temp.p, need, sc.nsub.p, sc.suboff.p, (int)nbins, s));
+    if (bp.subs.n < (size_t)cap) bp.subs.alloc((size_t)cap);
+    CBN_CUDA(cudaMemsetAsync(bp.subs.p, 0, sizeof(SubProblem) * cap, s));
+    k_fill_subs<<<nb, 256, 0, s>>>(sc.counts.p, sc.offs.p, sc.suboff.p, nbins, max_sub, bp.subs.p);
+    CBN_LAUNCH_CHECK();
+    if (bp.perm.n < (size_t)bp.m) bp.perm.alloc((size_t)bp.m);
+    // the scatter advances offs as cursors (k_fill_subs has read them)
+    k_bin_scatter<<<(unsigned)((bp.m + 255) / 256), 256, 0, s>>>(sc.keys.p, bp.m, sc.offs.p, bp.perm.p);
+    CBN_LAUNCH_CHECK();
+    bp.nsubs = (int)cap;
     bp.ready = true;
 }
 

@@ -100,11 +100,12 @@ CBN_D void src_node(const Src& src, int64_t pos, int64_t i, double (&w)[D], type
 // HALF (3D): `grid` is the [K0][K1][K2/2+1] half spectrum of a real input
 // (R2C); cells with k2 > K2/2 are read as conj(G[-k]).
 template <int D, int J, class Src, class Epi, bool HALF = false>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)   // <= 80 registers: 3 CTAs per SM
 k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src, Epi epi,
                 const int* __restrict__ perm, const SubProblem* __restrict__ subs) {
     extern __shared__ float2 tile[];
     const SubProblem sp = subs[blockIdx.x];
+    if (sp.count == 0) return;   // unused slot of a device-sorted plan
     int o[3];
     bin_origin<D>(tg, sp.bin, o);
     const int R0 = tg.R[0], R1 = D == 3 ? tg.R[1] : tg.P;
@@ -221,6 +222,7 @@ k_spread_binned(float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src,
     static_assert(D == 2, "3D spreads use k_spread_owned");
     extern __shared__ float2 smem[];
     const SubProblem sp = subs[blockIdx.x];
+    if (sp.count == 0) return;   // unused slot of a device-sorted plan
     int o[3];
     bin_origin<D>(tg, sp.bin, o);
     const int R0 = tg.R[0], R1 = tg.R[1], R2 = D == 3 ? tg.R[2] : 1;
@@ -344,6 +346,7 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
     constexpr int ITERS = (ROWS * JJ + 31) / 32;
     extern __shared__ float4 smem4[];
     const SubProblem sp = subs[blockIdx.x];
+    if (sp.count == 0) return;   // unused slot of a device-sorted plan
     int o[3];
     bin_origin<3>(tg, sp.bin, o);
     const int R0 = tg.R[0], R1 = tg.R[1], R2 = tg.R[2], P = tg.P;
@@ -532,6 +535,7 @@ k_spread_owned8(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
     constexpr int J = 8, NP = 256, SW = kOwned8Stride;
     extern __shared__ float4 smem4[];
     const SubProblem sp = subs[blockIdx.x];
+    if (sp.count == 0) return;   // unused slot of a device-sorted plan
     int o[3];
     bin_origin<3>(tg, sp.bin, o);
     const int R0 = tg.R[0], R1 = tg.R[1], R2 = tg.R[2], P = tg.P;
@@ -625,6 +629,7 @@ k_bin_interleave(Src src, KBSet kb, TileGeom<D> tg, int* __restrict__ perm,
     __shared__ int wcnt[8][16];
     __shared__ int cnt[16];
     const SubProblem sp = subs[blockIdx.x];
+    if (sp.count == 0) return;   // unused slot of a device-sorted plan
     int o[3];
     bin_origin<D>(tg, sp.bin, o);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -714,11 +719,25 @@ struct BinPlan {
 void finish_bins(BinPlan& bp, DevBuf<int>& keys, DevBuf<int>& counts, int64_t nbins, int max_sub,
                  cudaStream_t s);
 
+// Device-only counting sort (no host round trip, graph-capturable): bin keys
+// and counts -> exclusive scans (CUB) of the counts and of the per-bin
+// subproblem counts -> subproblem list, written into a list of fixed capacity
+// nbins + ceil(m / max_sub) whose unused entries have count 0 (the binned
+// kernels return at once for those) -> scatter.  Scratch is kept for re-sorts.
+struct DeviceSortScratch {
+    DevBuf<int> keys, counts, offs, nsub, suboff;
+    DevBuf<char> temp;
+    size_t temp_bytes = 0;
+};
+void device_bins_finish(BinPlan& bp, DeviceSortScratch& sc, int64_t nbins, int max_sub,
+                        cudaStream_t s);
+
 // pitch_pad: store the last region axis with pitch = J (mod 16) (required by
 // k_spread_owned; harmless for the gather)
 template <int D, int J, class Src>
 void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const int* tile,
-                int max_sub, cudaStream_t s, bool pitch_pad = false) {
+                int max_sub, cudaStream_t s, bool pitch_pad = false,
+                DeviceSortScratch* dev = nullptr) {
     CBN_REQUIRE(max_sub <= kInterleaveMax, "subproblem size above the interleave limit");
     bp.D = D;
     bp.J = J;
@@ -740,6 +759,20 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
     bp.tg.P = bp.tg.R[D - 1];
     if (D == 3 && pitch_pad) bp.tg.P += (((J - bp.tg.P) % 16) + 16) % 16;
     bp.nreg = bp.nreg / bp.tg.R[D - 1] * bp.tg.P;
+    if (dev) {
+        DeviceSortScratch& sc = *dev;
+        sc.keys.ensure((size_t)m);
+        sc.counts.ensure((size_t)nbins);
+        CBN_CUDA(cudaMemsetAsync(sc.counts.p, 0, sizeof(int) * nbins, s));
+        k_bin_keys<D, J, Src><<<(unsigned)((m + 255) / 256), 256, 0, s>>>(src, kb, bp.geom<D>(), m,
+                                                                        sc.keys.p, sc.counts.p);
+        CBN_LAUNCH_CHECK();
+        device_bins_finish(bp, sc, nbins, max_sub, s);
+        k_bin_interleave<D, J, Src><<<bp.nsubs, 256, 0, s>>>(src, kb, bp.geom<D>(), bp.perm.p,
+                                                             bp.subs.p);
+        CBN_LAUNCH_CHECK();
+        return;
+    }
     DevBuf<int> keys((size_t)m), counts((size_t)nbins);
     CBN_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int) * nbins, s));
     TileGeom<D> tg = bp.geom<D>();

@@ -7,6 +7,7 @@
 // weights are recomputed inside the gather/spread kernels instead of being
 // stored (the reference stores J^d per node).
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "cbn_binned.cuh"
@@ -121,6 +122,8 @@ struct cbn_nufft_s {
     DevBuf<float> pad_sc, crop_sc;
     DevBuf<float2> grid;
     BinPlan bins;              // 2D / 3D: bin-sorted order and subproblems
+    DeviceSortScratch sort;    // device-only counting sort (plan and re-sorts)
+    StageTimer timer;          // per-stage events + algorithmic bytes (bench)
     std::vector<double> s64_host;
     int smax = 0;
     int64_t ktot = 1, ntot = 1;
@@ -159,6 +162,13 @@ void run_type2(cbn_nufft* p, const float2* x, float2* y, cudaStream_t s) {
     epi.y = y;
     for (int d = 0; d < D; ++d) epi.c[d] = p->centre[d];
     ExplicitSrc<D> src = p->src<D>();
+    // grid read once, coordinates (float32: 4 B, float64: 8 B per axis) and
+    // values once; on chip: J^D tap reads of 8 B per node
+    const double cb = (p->nodes.p ? 8.0 : 4.0) * D;
+    double taps = 1;
+    for (int d = 0; d < D; ++d) taps *= p->J;
+    p->timer.add_bytes("gather", 8.0 * p->ktot + (cb + 8.0) * p->m, 8.0 * taps * p->m);
+    StageScope st(p->timer, "gather", s);
     dispatch_j(p->J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         if constexpr (D >= 2) {
@@ -175,11 +185,20 @@ void run_type2(cbn_nufft* p, const float2* x, float2* y, cudaStream_t s) {
 
 template <int D>
 void run_type1(cbn_nufft* p, const float2* y, float2* x, cudaStream_t s) {
-    CBN_CUDA(cudaMemsetAsync(p->grid.p, 0, p->grid.bytes(), s));
     PhaseIn<D> src;
     static_cast<ExplicitSrc<D>&>(src) = p->src<D>();
     src.yin = y;
     for (int d = 0; d < D; ++d) src.c[d] = p->centre[d];
+    {
+        // the grid written once (memset + flushes), coordinates and values
+        // read once; on chip: J^D shared-memory read + write of 8 B per node
+        const double cb = (p->nodes.p ? 8.0 : 4.0) * D;
+        double taps = 1;
+        for (int d = 0; d < D; ++d) taps *= p->J;
+        p->timer.add_bytes("spread", 8.0 * p->ktot + (cb + 8.0) * p->m, 16.0 * taps * p->m);
+    }
+    StageScope st_sp(p->timer, "spread", s);
+    CBN_CUDA(cudaMemsetAsync(p->grid.p, 0, p->grid.bytes(), s));
     dispatch_j(p->J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         if constexpr (D == 3) {
@@ -217,6 +236,34 @@ void run_type1(cbn_nufft* p, const float2* y, float2* x, cudaStream_t s) {
     CBN_LAUNCH_CHECK();
 }
 
+// bin-sorted order for the shared-memory gather/spread, entirely on the
+// device (build_bins with DeviceSortScratch): 3D tiles 8 x 8 x 16 cells (the
+// pitch-padded region holds 16 + J - 1 along z at no extra shared memory for
+// J = 6, 8), 2D 16 x 16.  float32 nodes also get a bin-ordered copy, so the
+// gather / spread stream their coordinates.
+template <int D>
+void sort_plan(cbn_nufft* p, cudaStream_t s) {
+    ExplicitSrc<D> src{p->nodes.p, p->nodes.p ? nullptr : p->nodes32.p, nullptr};
+    const int tile[3] = {D == 3 ? 8 : 16, D == 3 ? 8 : 16, 16};
+    {
+        // coordinates read twice (keys, interleave), keys written + read,
+        // the permutation written; float32: the sorted copy (read + write)
+        const double cb = (p->nodes.p ? 8.0 : 4.0) * D;
+        p->timer.add_bytes("sort", p->m * (2.0 * cb + 8.0 + 8.0 + (p->nodes.p ? 0.0 : 2.0 * cb)), 0.0);
+    }
+    StageScope st(p->timer, "sort", s);
+    dispatch_j(p->J, [&](auto jc) {
+        build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true, &p->sort);
+        return 0;
+    });
+    if (!p->nodes.p) {
+        p->sorted32.ensure((size_t)p->m * D);
+        k_sort_nodes<<<blocks_for(p->m, 256), 256, 0, s>>>(p->nodes32.p, p->bins.perm.p, p->m, D,
+                                                           p->sorted32.p);
+        CBN_LAUNCH_CHECK();
+    }
+}
+
 template <int D>
 void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t s) {
     DevBuf<int64_t> rows;
@@ -240,19 +287,7 @@ void fit_plan(cbn_nufft* p, const int64_t* rows_host, int64_t n_ls, cudaStream_t
         // bin-sorted order for the shared-memory gather/spread (one-time plan step)
         // 3D: 8 x 8 x 16 cells (the pitch-padded region holds 16 + J - 1 along z
         // at no extra shared memory for J = 6, 8); 2D: 16 x 16
-        const int tile[3] = {D == 3 ? 8 : 16, D == 3 ? 8 : 16, 16};
-        dispatch_j(p->J, [&](auto jc) {
-            build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true);
-            return 0;
-        });
-        if (!p->nodes.p) {
-            // float32 nodes: a bin-ordered copy, so the gather / spread stream
-            // their coordinates (the caller's order is kept for the rest)
-            p->sorted32.alloc((size_t)p->m * D);
-            k_sort_nodes<<<blocks_for(p->m, 256), 256, 0, s>>>(p->nodes32.p, p->bins.perm.p, p->m,
-                                                               D, p->sorted32.p);
-            CBN_LAUNCH_CHECK();
-        }
+        sort_plan<D>(p, s);
     }
     CBN_CUDA(cudaStreamSynchronize(s));   // rows / host scaling copy must outlive the launch
 }
@@ -412,6 +447,68 @@ int cbn_nufft_first_indices(const cbn_nufft* p, int32_t* out, void* stream) {
         CBN_LAUNCH_CHECK();
         CBN_CUDA(cudaMemcpyAsync(out, dev.p, sizeof(int32_t) * p->m * p->D, cudaMemcpyDeviceToHost, s));
         CBN_CUDA(cudaStreamSynchronize(s));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_resort(cbn_nufft* p, void* stream) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        CBN_REQUIRE(p->D >= 2, "1D plans are not bin-sorted");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        dispatch_d(p->D, [&](auto dc) {
+            constexpr int D = decltype(dc)::value;
+            if constexpr (D >= 2) sort_plan<D>(p, s);
+            return 0;
+        });
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_set_timing(cbn_nufft* p, int32_t on) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        p->timer.reset();
+        p->timer.on = on != 0;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_nufft_stage_times(cbn_nufft* p, double* ms, double* hbm, double* chip, int32_t* count,
+                          char* names, int32_t names_len) {
+    try {
+        CBN_REQUIRE(p && count, "null argument");
+        p->timer.collect();
+        const int cap = *count;
+        *count = (int32_t)p->timer.totals.size();
+        std::string joined;
+        for (int i = 0; i < *count; ++i) {
+            const std::string& nm = p->timer.totals[i].first;
+            if (i < cap) {
+                if (ms) ms[i] = p->timer.totals[i].second;
+                double h = 0, c = 0;
+                for (const auto& kv : p->timer.bytes)
+                    if (kv.first == nm) {
+                        h = kv.second.hbm;
+                        c = kv.second.chip;
+                    }
+                if (hbm) hbm[i] = h;
+                if (chip) chip[i] = c;
+            }
+            if (i) joined += ";";
+            joined += nm;
+        }
+        if (names && names_len > 0) {
+            std::strncpy(names, joined.c_str(), (size_t)names_len - 1);
+            names[names_len - 1] = 0;
+        }
+        p->timer.reset();
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

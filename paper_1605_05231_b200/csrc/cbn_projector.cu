@@ -294,7 +294,7 @@ k_resample_rows3(const float* __restrict__ G, int K2, const RsRow3* __restrict__
             uint4* dst = reinterpret_cast<uint4*>(&rr);
 #pragma unroll
             for (int k = 0; k < 6; ++k) dst[k] = __ldg(src + k);
-            if (rr.valid && lane < nviews) {
+            if (rr.valid == 1 && lane < nviews) {
                 int c0 = rr.f2 - pshift;
                 c0 += c0 < 0 ? K2 : 0;
                 int c1 = c0 + 1, c2 = c0 + 2;
@@ -351,6 +351,187 @@ k_resample_rows3(const float* __restrict__ G, int K2, const RsRow3* __restrict__
             const float x = tile[v][tt];
             vals[(size_t)v * per_view + t0 + tt] = tscale ? x * tscale[(t0 + tt) % n_t] : x;
         }
+    }
+}
+
+// Windowed view-chunk gather (J = 3, real phi-fast grid).  View v of a target
+// reads the three phi cells c0(v) = f2 - shift v (+0, 1, 2) of each of its nine
+// (rho, theta) rows, and c0 does not depend on the row.  So per target the
+// row-weighted sum R(c) = sum_ab wab[ab] G_ab[c] is formed once over the phi
+// window the chunk's views reach (length shift (nv - 1) + 3, in aligned float4
+// slots, coalesced 16-byte loads), kept in shared memory, and every view is
+// then three shared-memory reads and three FMAs: 9 x 4 B per window cell
+// instead of 27 x 4 B per view (views overlap 1-2 cells at shift 2), and the
+// row reads are contiguous spans instead of 64-lane scatters.
+//   CTA = 8 warps x 4 targets = 32 consecutive targets; each warp owns a
+//   window buffer (K2 + 4 floats); the [view][32 targets] output tile goes out
+//   in 128-byte rows.  Pole targets (valid == 2) read their per-view phi cell
+//   from `pole_f2` ([pole][V]); invalid targets (valid == 0) are zero.
+// chunk of 120 views: at shift 2 the window is <= 61 float4 slots, two passes of
+// the warp (360 = 3 x 120 at config 2)
+constexpr int kWinWarps = 8, kWinTargets = 4, kWinChunk = 120;
+
+__host__ __device__ constexpr int win_buf_floats(int K2) { return ((K2 + 4 + 3) / 4) * 4; }
+
+__global__ void __launch_bounds__(kWinWarps * 32)
+k_resample_window(const float* __restrict__ G, int K2, const RsRow3* __restrict__ rows,
+                  int64_t per_view, int v0, int nv, int shift, const int* __restrict__ pole_f2,
+                  int n_views, float* __restrict__ vals, const float* __restrict__ tscale, int n_t) {
+    extern __shared__ float4 smem4[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bufn = win_buf_floats(K2);
+    float* buf = reinterpret_cast<float*>(smem4) + warp * bufn;
+    float* tile = reinterpret_cast<float*>(smem4) + kWinWarps * bufn;   // [nv][33] (padded)
+    const int64_t t0 = (int64_t)blockIdx.x * (kWinWarps * kWinTargets);
+    const int K4 = K2 >> 2;
+    const float4* G4 = reinterpret_cast<const float4*>(G);
+    const int L = shift * (nv - 1) + 3;           // window cells the chunk's views reach
+    const bool full = L > K2 - 4;
+    // shift * view offsets mod K2 (32-bit: shift * n_views < 2^31)
+    const int sh_last = (int)(((int64_t)shift * (v0 + nv - 1)) % K2);
+    const int sh_lane = (int)(((int64_t)shift * (v0 + lane)) % K2);
+    const int step32 = (32 * shift) % K2;
+#pragma unroll 1
+    for (int q = 0; q < kWinTargets; ++q) {
+        const int tl = warp * kWinTargets + q;
+        const int64_t t = t0 + tl;
+        if (t >= per_view) break;
+        RsRow3 rr;
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(rows + t);
+            uint4* dst = reinterpret_cast<uint4*>(&rr);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) dst[k] = __ldg(src + k);
+        }
+        if (rr.valid == 0) {
+            for (int v = lane; v < nv; v += 32) tile[v * 33 + tl] = 0.f;
+            continue;
+        }
+        if (rr.valid == 2) {
+            // pole target: its phi cell follows each view's own geometry
+            for (int v = lane; v < nv; v += 32) {
+                const int c0 = pole_f2[(int64_t)rr.pad * n_views + v0 + v];
+                const int c1 = c0 + 1 >= K2 ? c0 + 1 - K2 : c0 + 1;
+                const int c2 = c0 + 2 >= K2 ? c0 + 2 - K2 : c0 + 2;
+                float acc = 0.f;
+#pragma unroll
+                for (int ab = 0; ab < 9; ++ab) {
+                    const float* g = G + rr.row[ab];
+                    float r = rr.w2[0] * __ldg(g + c0);
+                    r = fmaf(rr.w2[1], __ldg(g + c1), r);
+                    r = fmaf(rr.w2[2], __ldg(g + c2), r);
+                    acc = fmaf(rr.wab[ab], r, acc);
+                }
+                tile[v * 33 + tl] = acc;
+            }
+            continue;
+        }
+        // window start cell (the last view's c0) and its float4 slots
+        int cs = rr.f2 - sh_last;
+        cs += cs < 0 ? K2 : 0;
+        const int s4 = full ? 0 : (cs >> 2);
+        const int n4 = full ? K4 : (((cs & 3) + L + 3) >> 2);
+        for (int j = lane; j < n4; j += 32) {
+            int g4 = s4 + j;
+            g4 -= g4 >= K4 ? K4 : 0;
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 x[9];
+#pragma unroll
+            for (int ab = 0; ab < 9; ++ab) x[ab] = __ldg(G4 + (rr.row[ab] >> 2) + g4);
+#pragma unroll
+            for (int ab = 0; ab < 9; ++ab) {
+                const float w = rr.wab[ab];
+                a.x = fmaf(w, x[ab].x, a.x);
+                a.y = fmaf(w, x[ab].y, a.y);
+                a.z = fmaf(w, x[ab].z, a.z);
+                a.w = fmaf(w, x[ab].w, a.w);
+            }
+            reinterpret_cast<float4*>(buf)[j] = a;
+        }
+        __syncwarp();
+        if (full && lane < 2) buf[K2 + lane] = buf[lane];   // circular tail
+        __syncwarp();
+        const int base = full ? 0 : 4 * s4;
+        // o(v) = f2 - shift (v0 + v) - base (mod K2), stepped by 32 views
+        int o = rr.f2 - sh_lane - base;
+        o += o < 0 ? K2 : 0;
+        o += o < 0 ? K2 : 0;
+        for (int v = lane; v < nv; v += 32, o -= step32, o += o < 0 ? K2 : 0) {
+            // the three cells as one aligned pair + one cell (an even shift keeps
+            // the lanes' pairs on distinct banks: 2 wavefronts per read)
+            float b0, b1, b2;
+            if (o & 1) {
+                b0 = buf[o];
+                const float2 q = *reinterpret_cast<const float2*>(buf + o + 1);
+                b1 = q.x;
+                b2 = q.y;
+            } else {
+                const float2 q = *reinterpret_cast<const float2*>(buf + o);
+                b0 = q.x;
+                b1 = q.y;
+                b2 = buf[o + 2];
+            }
+            float r = rr.w2[0] * b0;
+            r = fmaf(rr.w2[1], b1, r);
+            r = fmaf(rr.w2[2], b2, r);
+            tile[v * 33 + tl] = r;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // [view][32 targets] tile -> vals[v][t0 + tt] (128-byte rows)
+    {
+        // each thread keeps one target column (256 threads = 8 view rows x 32)
+        const int tt = threadIdx.x & 31;
+        const int64_t t = t0 + tt;
+        if (t < per_view) {
+            const float sc = tscale ? tscale[(int)(t % n_t)] : 1.f;
+            float* dst = vals + t;
+            for (int v = threadIdx.x >> 5; v < nv; v += kWinWarps)
+                dst[(size_t)v * per_view] = tile[v * 33 + tt] * sc;
+        }
+    }
+}
+
+inline size_t win_smem_bytes(int K2, int nv) {
+    return sizeof(float) * ((size_t)kWinWarps * win_buf_floats(K2) + (size_t)nv * 33);
+}
+
+// pole rows: valid = 2, pad = pole index; per-view phi cells of every pole
+__global__ void k_pole_rows(const int* __restrict__ poles, int npoles, RsRow3* __restrict__ rows) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= npoles) return;
+    rows[poles[q]].valid = 2;
+    rows[poles[q]].pad = q;
+}
+
+__global__ void k_pole_table(UmbrellaSrc src0, KBSet kb, const int* __restrict__ poles, int npoles,
+                             int n_views, int f0_ref_check, int* __restrict__ table,
+                             int* __restrict__ mismatch) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= npoles * n_views) return;
+    const int q = e / n_views, v = e % n_views;
+    UmbrellaSrc sv = src0;
+    sv.view0 = v;
+    double wd[3];
+    UmbrellaSrc::Aux aux;
+    sv.node(poles[q], wd, aux);
+    const double w[3] = {wd[2], wd[1], wd[0]};
+    int first[3];
+    float wt[3][3];
+    tap_setup<3, 3>(kb, w, first, wt);
+    table[e] = wrapc(first[2], kb.ax[2].K);
+    // the pole's rho / theta taps must be view 0's (theta == 0, rho snapped)
+    if (f0_ref_check) {
+        UmbrellaSrc s0 = src0;
+        s0.view0 = 0;
+        double w0d[3];
+        s0.node(poles[q], w0d, aux);
+        const double ww[3] = {w0d[2], w0d[1], w0d[0]};
+        int f0[3];
+        float wt0[3][3];
+        tap_setup<3, 3>(kb, ww, f0, wt0);
+        if (f0[0] != first[0] || f0[1] != first[1]) atomicAdd(mismatch, 1);
     }
 }
 
@@ -907,6 +1088,8 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         // zero the grid, then fill only the cells the pad reaches (1/8 of them)
         StageScope st(p->timer, "spectrum_pad", s);
         CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float) * real_cells, s));
+        // zero the real grid, read the volume, write its N^3 cells
+        p->timer.add_bytes("spectrum_pad", 4.0 * real_cells + 8.0 * (double)n * n * n, 0.0);
         const int* l = p->fspec_list.p;
         k_remap_list3<float, kStoreRe><<<dim3((unsigned)((p->fspec_nl[2] + 255) / 256),
                                               p->fspec_nl[1], p->fspec_nl[0]), 256, 0, s>>>(
@@ -987,6 +1170,14 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         const int s0 = (int)((int64_t)bp.nsubs * part / nparts);
         const int s1 = (int)((int64_t)bp.nsubs * (part + 1) / nparts);
         CBN_REQUIRE(bp.tg.R[2] <= 32, "half-spectrum gather: region rows above 32 cells");
+        {
+            // half spectrum read once, every lattice node written (mirrors by
+            // conjugation), J^3 shared-memory tap reads per primary node
+            const double f = bp.nsubs ? (double)(s1 - s0) / bp.nsubs : 0.0;
+            const double J = ax[0].J;
+            p->timer.add_bytes("spectrum_gather", f * (8.0 * half_cells + 8.0 * M),
+                               f * 8.0 * J * J * J * (double)Mh);
+        }
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             if (s1 > s0)
@@ -1106,6 +1297,14 @@ bool real_grid(const P* p) {
     const char* off = std::getenv("CBN_COMPLEX_GRID");
     if (off && off[0] == '1') return false;
     return views_in_lanes(p) && p->fres[0].J == 3 && p->c.method == 0;
+}
+
+// the windowed view-chunk gather (k_resample_window) on the real grid; off
+// with CBN_WINDOW_GATHER=0 (A/B against the 32-view k_resample_rows3)
+bool window_gather(const P* p) {
+    const char* e = std::getenv("CBN_WINDOW_GATHER");
+    if (e && e[0] == '0') return false;
+    return real_grid(p) && p->fres[0].K % 4 == 0;
 }
 
 void ensure_lane_taps(P* p, cudaStream_t s);
@@ -1380,17 +1579,46 @@ void ensure_lane_taps(P* p, cudaStream_t s) {
                 reinterpret_cast<const RsTap<3>*>(u.taps.p), per_view, ax[2].K, ax[1].K,
                 ax[0].K, reinterpret_cast<RsRow3*>(u.rows.p));
             CBN_LAUNCH_CHECK();
+            if (u.n_poles) {
+                // pole records (valid = 2) and their per-view phi taps
+                k_pole_rows<<<blocks_for(u.n_poles, 128), 128, 0, s>>>(
+                    u.poles.p, u.n_poles, reinterpret_cast<RsRow3*>(u.rows.p));
+                CBN_LAUNCH_CHECK();
+                const int V = p->g.n_views;
+                u.pole_f2.alloc((size_t)u.n_poles * V);
+                DevBuf<int> bad(1);
+                CBN_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+                KBSet kbg;   // grid order (rho, theta, phi)
+                kbg.ax[0] = ax[2].kb;
+                kbg.ax[1] = ax[1].kb;
+                kbg.ax[2] = ax[0].kb;
+                k_pole_table<<<blocks_for((int64_t)u.n_poles * V, 128), 128, 0, s>>>(
+                    src, kbg, u.poles.p, u.n_poles, V, 1, u.pole_f2.p, bad.p);
+                CBN_LAUNCH_CHECK();
+                int h_bad = 0;
+                CBN_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CBN_CUDA(cudaStreamSynchronize(s));
+                CBN_REQUIRE(h_bad == 0, "pole target with view-dependent rho/theta taps");
+            }
         }
         return 0;
     });
     u.taps_ready = true;
 }
 
-// Re(resample_apply) for nb <= 32 consecutive views [v0, v0 + nb) from a phi-fast grid
+// Re(resample_apply) for consecutive views [v0, v0 + nb) from a phi-fast grid:
+// up to kWinChunk views per launch with the window gather, else 32 per launch
 void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
                         const float* tscale = nullptr) {
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
+    const int per_launch = ax[0].J == 3 && window_gather(p) ? kWinChunk : 32;
+    if (nb > per_launch) {
+        for (int k = 0; k < nb; k += per_launch)
+            gather_views_lanes(p, v0 + k, std::min(per_launch, nb - k), vals + (size_t)k * per_view,
+                               s, tscale);
+        return;
+    }
     const int shift = (int)(2LL * p->frad.n_phi / p->g.n_views);
     ensure_lane_taps(p, s);
     dispatch_j(ax[0].J, [&](auto jc) {
@@ -1398,6 +1626,26 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
         UmbrellaTables& u = p->fumb;
         StageScope st(p->timer, "resample_gather", s);
         const bool re = J == 3 && real_grid(p);
+        if (J == 3 && re && window_gather(p)) {
+            // chunk of up to kWinChunk views: one window sum per target
+            const RsRow3* rows = reinterpret_cast<const RsRow3*>(u.rows.p);
+            const int K2 = ax[0].K;
+            const size_t smem = win_smem_bytes(K2, nb);
+            CBN_CUDA(cudaFuncSetAttribute(k_resample_window,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const unsigned nblk = (unsigned)((per_view + kWinWarps * kWinTargets - 1) /
+                                             (kWinWarps * kWinTargets));
+            k_resample_window<<<nblk, kWinWarps * 32, smem, s>>>(
+                p->grid_re, K2, rows, per_view, v0, nb, shift, u.pole_f2.p, p->g.n_views, vals,
+                tscale, u.n_t);
+            CBN_LAUNCH_CHECK();
+            // outputs + records once; on chip: 9 rows x the window's float4
+            // slots per target, 3 reads per view
+            const double win = std::min<double>(shift * (nb - 1) + 3 + 3, ax[0].K);
+            p->timer.add_bytes("resample_gather", 4.0 * nb * per_view + 96.0 * per_view,
+                               (double)per_view * (9.0 * 4.0 * win + 12.0 * nb));
+            return 0;
+        }
         if constexpr (J == 3) {
             const unsigned nblk = (unsigned)((per_view + 31) / 32);
             const RsRow3* rows = reinterpret_cast<const RsRow3*>(u.rows.p);
@@ -1414,6 +1662,11 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
                 per_view, v0, nb, shift, vals, tscale, p->fumb.n_t);
         }
         CBN_LAUNCH_CHECK();
+        // outputs + one read of the tap records per launch; on chip: J^2 rows
+        // per target and view (rows3: two 8-byte cell pairs per row)
+        p->timer.add_bytes("resample_gather",
+                           4.0 * nb * per_view + (J == 3 ? 96.0 : (double)sizeof(RsTap<J>)) * per_view,
+                           (double)nb * per_view * (J == 3 ? 9.0 * 16.0 : 4.0 * (re ? 1 : 2) * J * J * J));
         if (u.n_poles) {
             // pole targets per view (their records are not in the view-0 taps)
             UmbrellaSrc src = cached_umbrella(p, u, p->frad, p->fpad, v0, s);
@@ -1446,6 +1699,8 @@ void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s,
     KBSet kb;
     for (int d = 0; d < 3; ++d) kb.ax[d] = ax[d].kb;
     StageScope st(p->timer, "resample_gather", s);
+    p->timer.add_bytes("resample_gather", 4.0 * m,
+                       8.0 * m * ax[0].J * ax[1].J * ax[2].J);
     dispatch_j(ax[0].J, [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         k_gather<3, J><<<blocks_for(m, 256), 256, 0, s>>>(p->big.p, kb, src,
@@ -1597,6 +1852,7 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
             for (size_t q = 1; q < h.size(); ++q) h[q] += h[q - 1];
             gp.cell_ptr.upload(h.data(), h.size(), s);
             gp.cell_ent.alloc(sizeof(GrEntry) * (size_t)std::max(h.back(), 1));
+            gp.n_entries = h.back();
             CBN_CUDA(cudaMemcpyAsync(counts.p, h.data(), sizeof(int) * ncell, cudaMemcpyHostToDevice,
                                      s));
             k_gr_csr_fill<kGrJ><<<bb.nsubs, 256, 0, s>>>(bb.geom<2>(), pts, bb.subs.p, node_id.p,
@@ -1619,6 +1875,12 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         // Hermitian half plane [Ku][Kv/2+1] of the grid (only Re of its
         // inverse FFT is used), then a complex-to-real 2D FFT into tv
         const int64_t nhalf = (int64_t)Ku * (Kv / 2 + 1);
+        // node rows of the block once, CSR entries once, the half-plane grids
+        // written once; on chip: one row value per entry and view
+        p->timer.add_bytes("grangeat_spread",
+                           8.0 * nb * gp.n_rows + (double)sizeof(GrEntry) * gp.n_entries +
+                               8.0 * nb * nhalf,
+                           8.0 * nb * (double)gp.n_entries);
         k_gr_gather_cells<<<(unsigned)gp.n_items, 256, 0, s>>>(
             B.grid.p, (size_t)nhalf, nhalf, gp.cell_ptr.p,
             reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb, Ku, Kv,
@@ -1663,7 +1925,12 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
     grangeat_reverse(p, vals, frames, nb, s, main_bufs(p));
 }
 
-constexpr int kViewBlock = 32;
+constexpr int kViewBlock = 32;   // views per reverse-Grangeat block
+
+// views per resample-gather chunk of the forward view loop
+int gather_chunk(const P* p) {
+    return views_in_lanes(p) && p->fres[0].J == 3 && window_gather(p) ? kWinChunk : kViewBlock;
+}
 
 // Views [lo, hi): one resample grid per run of batches with equal scalings,
 // gather at the umbrella targets, then reverse Grangeat in blocks of up to
@@ -1689,14 +1956,17 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
     ensure_batch_plan(p, bp, p->fumb, p->frad, p->fpad, p->fres, s);
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
     const size_t frame_sz = (size_t)p->g.nu * p->g.nv;
-    if (!values_out) p->values.ensure((size_t)per_view * kViewBlock);
     const bool lanes = views_in_lanes(p);
+    // views per gather chunk (the window gather takes up to kWinChunk at once);
+    // the reverse Grangeat runs on 32-view blocks of each chunk
+    const int chunk = lanes ? gather_chunk(p) : kViewBlock;
+    if (!values_out) p->values.ensure((size_t)per_view * chunk);
     // two lanes (the caller's stream and s1) alternate over view blocks so one
     // block's Grangeat FFTs overlap the next block's resample gather
     const bool dual = lanes && !values_out && lanes_allowed() && !p->timer.on;
     if (dual) ensure_lane1(p);
     if (dual) {
-        p->lane1.values.ensure((size_t)per_view * kViewBlock);
+        p->lane1.values.ensure((size_t)per_view * chunk);
         // everything s1 reads besides the grid exists before the first grid event
         ensure_lane_taps(p, s);
         if (!p->fgr.built) fit_grangeat(p, p->fgr, p->fumb, s);
@@ -1723,9 +1993,12 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
     auto flush = [&]() {
         if (!blk_n) return;
         const cudaStream_t ls = lane_stream();
-        grangeat_reverse(p, lane ? p->lane1.values.p : p->values.p,
-                         frames + (size_t)(blk_lo - lo) * frame_sz, blk_n, ls,
-                         lane ? lane_bufs(p) : main_bufs(p));
+        const float* vb = lane ? p->lane1.values.p : p->values.p;
+        for (int k = 0; k < blk_n; k += kViewBlock)
+            grangeat_reverse(p, vb + (size_t)k * per_view,
+                             frames + (size_t)(blk_lo + k - lo) * frame_sz,
+                             std::min(kViewBlock, blk_n - k), ls,
+                             lane ? lane_bufs(p) : main_bufs(p));
         lane_done();
         blk_lo += blk_n;
         blk_n = 0;
@@ -1739,9 +2012,7 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
             return;
         }
         const cudaStream_t ls = values_out ? s : lane_stream();
-        for (int k = 0; k < n; k += 32)
-            gather_views_lanes(p, v + k, std::min(32, n - k), out + (size_t)k * per_view, ls,
-                               tscale);
+        gather_views_lanes(p, v, n, out, ls, tscale);
         if (!values_out) lane_done();
     };
     // runs of consecutive batches (clipped to [lo, hi)) sharing one scaling group
@@ -1764,6 +2035,19 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
             // the previous grid may still be read on s1
             if (s1_used) CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
             build_resample_grid(p, bp.s32.p + (size_t)g * 3 * bp.smax, bp.smax, s, lanes);
+            {
+                // the gathers read the built grid once: the rho planes the
+                // taps reach (views-in-lanes: real grid of those planes only)
+                const AxisPlan* ax = p->fres;
+                const double plane = (double)ax[0].K * ax[1].K;
+                double planes = ax[2].K;
+                if (lanes && !p->fres_rho_runs.empty()) {
+                    planes = 0;
+                    for (const auto& rn : p->fres_rho_runs) planes += rn.second - rn.first;
+                }
+                const double es = lanes && real_grid(p) ? 4.0 : 8.0;
+                p->timer.add_bytes("resample_gather", es * plane * planes, 0.0);
+            }
             if (dual) {
                 CBN_CUDA(cudaEventRecord(p->ev_s0, s));
                 s1_stale = true;
@@ -1772,16 +2056,16 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         }
         for (int v = vlo; v < vhi;) {
             if (values_out) {
-                const int take = std::min(vhi - v, kViewBlock);
+                const int take = std::min(vhi - v, chunk);
                 gather(v, take, values_out + (size_t)(v - lo) * per_view);
                 v += take;
                 continue;
             }
-            const int take = std::min(vhi - v, kViewBlock - blk_n);
+            const int take = std::min(vhi - v, chunk - blk_n);
             gather(v, take, (lane ? p->lane1.values.p : p->values.p) + (size_t)blk_n * per_view);
             blk_n += take;
             v += take;
-            if (blk_n == kViewBlock) flush();
+            if (blk_n == chunk) flush();
         }
         b = e;
     }
@@ -2199,6 +2483,32 @@ int cbn_projector_set_timing(cbn_projector* p, int32_t on) {
         CBN_REQUIRE(p, "null argument");
         p->timer.reset();
         p->timer.on = on != 0;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_stage_bytes(cbn_projector* p, double* hbm, double* chip, int32_t* count,
+                              char* names, int32_t names_len, int32_t reset) {
+    try {
+        CBN_REQUIRE(p && count, "null argument");
+        const int cap = *count;
+        *count = (int32_t)p->timer.bytes.size();
+        std::string joined;
+        for (int i = 0; i < *count; ++i) {
+            if (i < cap) {
+                if (hbm) hbm[i] = p->timer.bytes[i].second.hbm;
+                if (chip) chip[i] = p->timer.bytes[i].second.chip;
+            }
+            if (i) joined += ";";
+            joined += p->timer.bytes[i].first;
+        }
+        if (names && names_len > 0) {
+            std::strncpy(names, joined.c_str(), (size_t)names_len - 1);
+            names[names_len - 1] = 0;
+        }
+        if (reset) p->timer.bytes.clear();
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

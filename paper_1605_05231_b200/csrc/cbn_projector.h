@@ -38,6 +38,7 @@ struct UmbrellaTables {
     DevBuf<char> rows;      // J = 3: the same taps as grid-row offsets + weight products (RsRow3)
     DevBuf<int> poles;      // pole targets (theta == 0), handled per view (cbn_resample_views.cuh)
     int n_poles = 0;
+    DevBuf<int> pole_f2;    // [pole][view] first phi tap of each pole target (k_resample_window)
     void build(const cbn_geometry& g, int n_mu, int n_t, double dt, cudaStream_t s);
 };
 
@@ -65,6 +66,7 @@ struct GrangeatPlan {
     int n_items = 0;
     DevBuf<GrNode> node_tab;            // reverse: node-scaled t-spectrum rows
     int64_t n_rows = 0;                 // rows of node_tab (nspec + second nodes)
+    int64_t n_entries = 0;              // reverse: CSR entries (node, tap) over all cells
 };
 
 constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)
@@ -159,6 +161,7 @@ struct cbn_projector_s {
     int bres_planes_slow = -1;
     cbn::DevBuf<int> bcol_ptr;      // transposed-resample CSR: column -> entries (views in lanes)
     cbn::DevBuf<char> bcol_ent;     // RsColEntry per (target, rho tap, theta tap)
+    int64_t bcol_n = 0;             // entries of the column CSR
     cbn::DevBuf<float> values_t;    // umbrella values of a view run, target-major
     cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
     cbn::DevBuf<int> bpairs;     // primary radial nodes of the 3D adjoint (conjugate pairs)

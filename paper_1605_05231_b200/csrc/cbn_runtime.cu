@@ -254,6 +254,21 @@ void StageTimer::collect() {
 void StageTimer::reset() {
     collect();
     totals.clear();
+    bytes.clear();
+}
+
+void StageTimer::add_bytes(const char* name, double hbm, double chip) {
+    if (!on) return;
+    for (auto& kv : bytes)
+        if (kv.first == name) {
+            kv.second.hbm += hbm;
+            kv.second.chip += chip;
+            return;
+        }
+    Bytes b;
+    b.hbm = hbm;
+    b.chip = chip;
+    bytes.emplace_back(name, b);
 }
 
 }  // namespace cbn

@@ -148,6 +148,12 @@ public:
     void collect();
     void reset();
     std::vector<std::pair<std::string, double>> totals;   // name -> ms
+    // algorithmic bytes per stage (roofline of the bench): compulsory HBM
+    // bytes and on-chip tap bytes of the work the stage's kernels did,
+    // accumulated while timing is on (DESIGN.md section 4 gives each formula)
+    void add_bytes(const char* name, double hbm, double chip);
+    struct Bytes { double hbm = 0, chip = 0; };
+    std::vector<std::pair<std::string, Bytes>> bytes;
 private:
     struct Rec { std::string name; cudaEvent_t a, b; };
     std::vector<Rec> recs_;

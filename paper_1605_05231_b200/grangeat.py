@@ -42,6 +42,15 @@ class DetectorFrame:
         if not np.all(np.isfinite(self.data)):
             raise ValueError("detector data contains non-finite values")
 
+    @classmethod
+    def _checked(cls, view_index: int, data: np.ndarray, pixel_mm):
+        """A frame whose data the device already checked for non-finite values
+        (cbn_forward_project returns CBN_ENONFINITE -> FloatingPointError,
+        pipeline.py:144-145), so the per-frame host scan is skipped."""
+        f = object.__new__(cls)
+        f.view_index, f.data, f.pixel_mm = view_index, data, pixel_mm
+        return f
+
 
 def detector_axes_virtual(geom):
     pu, pv = geom.virtual_pixel_mm

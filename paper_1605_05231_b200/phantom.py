@@ -34,6 +34,14 @@ class Volume3D:
         if not self.voxel_mm > 0:
             raise ValueError("voxel_mm must be positive")
 
+    @classmethod
+    def _checked(cls, data: np.ndarray, voxel_mm: float):
+        """A float64 cubic volume already checked for non-finite values on
+        the device (nufft_backproject), so the host scan is skipped."""
+        v = object.__new__(cls)
+        v.data, v.voxel_mm = data, float(voxel_mm)
+        return v
+
     @property
     def n(self) -> int:
         return self.data.shape[0]

@@ -21,7 +21,7 @@ from collections import OrderedDict
 
 import numpy as np
 
-from . import _device, _lib
+from . import _device, _hostio, _lib
 from .config import ProjectorConfig, make_projector_config  # noqa: F401  (API re-export)
 from .geometry import ConeGeometry, RadialGridSpec  # noqa: F401
 from .grangeat import DetectorFrame, UmbrellaView  # noqa: F401
@@ -114,6 +114,7 @@ class Projector:
                                             ctypes.byref(self._c), self.n, self.voxel,
                                             direction), "projector")
         self._h = h
+        self.stage = _hostio.Staging()
         cnt = ctypes.c_int32(64)
         sizes = (ctypes.c_int64 * 64)()
         _lib.check(lib.cbn_projector_ls_sizes(h, sizes, ctypes.byref(cnt)))
@@ -429,20 +430,43 @@ def clear_plan_cache() -> None:
 
 
 def nufft_forward_project(vol: Volume3D, geom, cfg) -> list[DetectorFrame]:
-    """NUFFT cone-beam forward projection of all views (pipeline.py:122-147)."""
-    proj = get_projector(geom, cfg, vol.data.shape[0], vol.voxel_mm, _FORWARD)
-    frames = proj.forward(vol.data).cpu().numpy().astype(np.float64)
-    return [DetectorFrame(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
+    """NUFFT cone-beam forward projection of all views (pipeline.py:122-147).
+
+    Host float64 volume in, ``list[DetectorFrame]`` (float64) out, like the
+    reference.  The conversions run on host threads through the plan's pinned
+    staging buffers (_hostio); non-finite projections raise FloatingPointError
+    from the device check."""
+    import torch
+    data = np.asarray(vol.data)
+    proj = get_projector(geom, cfg, data.shape[0], vol.voxel_mm, _FORWARD)
+    v = _hostio.upload(proj.stage, "vol", data, torch.float32)
+    frames = _hostio.download(proj.stage, "frames", proj.forward(v))
+    return [DetectorFrame._checked(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
 
 
 def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volume3D:
-    """Direct NUFFT backprojection (pipeline.py:150-212)."""
+    """Direct NUFFT backprojection (pipeline.py:150-212): list of frames in,
+    float64 ``Volume3D`` out (ValueError on non-finite values, as the
+    reference's Volume3D raises)."""
+    import torch
     if len(frames) != geom.n_views:
         raise ValueError("frame count does not match the geometry")
-    data = np.stack([np.asarray(f.data, dtype=np.float32) for f in frames])
     proj = get_projector(geom, cfg, out_size, voxel_mm, _BACK)
-    vol = proj.backproject(data).cpu().numpy().astype(np.float64)
-    return Volume3D(vol, voxel_mm)
+    shape = (geom.n_views, geom.nu, geom.nv)
+    pin = proj.stage.get("frames", shape, torch.float32)
+    host = pin.numpy()
+    for k, f in enumerate(frames):
+        if np.shape(f.data) != shape[1:]:
+            raise ValueError("frames must be (n_views, nu, nv)")
+    _hostio.pool()
+    futs = [_hostio.pool().submit(np.copyto, host[k], frames[k].data, casting="unsafe")
+            for k in range(geom.n_views)]
+    for fu in futs:
+        fu.result()
+    vol = proj.backproject(pin.to("cuda", non_blocking=True))
+    if not bool(torch.isfinite(vol).all()):
+        raise ValueError("volume contains non-finite values")
+    return Volume3D._checked(_hostio.download(proj.stage, "vol", vol), voxel_mm)
 
 
 def calibrate_normalization(geom, n: int, cfg, voxel_mm: float) -> float:
