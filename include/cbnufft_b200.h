@@ -173,6 +173,20 @@ int cbn_projector_scratch_bytes(const cbn_projector* proj, int64_t* bytes);
  * projection value is non-finite (checked on device, synchronises). */
 int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
                         int32_t view_lo, int32_t view_hi, void* stream);
+/* cbn_forward_project without the final synchronisation, for a host that
+ * copies frames out while later views are still computing: the call enqueues
+ * every kernel and returns; the frames of each reverse-Grangeat block (views
+ * [view_lo[k], view_hi[k]) relative to lo, from cbn_projector_blocks) are
+ * complete once cbn_projector_block_sync(k) returns (host wait on that
+ * block's event); cbn_forward_finish synchronises `stream` and returns
+ * CBN_ENONFINITE if any projection value of the call was non-finite
+ * (pipeline.py:144-145). */
+int cbn_forward_project_async(cbn_projector* proj, const float* vol, float* frames, int32_t view_lo,
+                              int32_t view_hi, void* stream);
+int cbn_projector_blocks(cbn_projector* proj, int32_t* view_lo, int32_t* view_hi, int32_t* count);
+int cbn_projector_block_sync(cbn_projector* proj, int32_t k);
+int cbn_forward_finish(cbn_projector* proj, void* stream);
+
 /* nufft_forward_project in two phases, for sharding the radial nodes and the
  * views across devices; cbn_forward_project == lattice(0 of 1)
  * + views.  lattice [device] complex64 x lattice_elems, caller-owned:

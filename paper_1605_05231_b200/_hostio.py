@@ -14,6 +14,8 @@ conversion of the previous chunk.
 from __future__ import annotations
 
 import os
+import sys
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -45,10 +47,31 @@ def copy(dst: np.ndarray, src: np.ndarray, min_chunk: int = 1 << 18) -> None:
 
 
 class Staging:
-    """Pinned host buffers of one projector plan, keyed by (tag, shape, dtype)."""
+    """Pinned host buffers of one projector plan, keyed by (tag, shape, dtype),
+    and its result arrays: a result whose previous instance nobody holds any
+    more (the caller dropped every frame / volume that viewed it) is reused,
+    which saves the first-touch page faults of a fresh 100+ MB array; while
+    the caller holds it, a new one is allocated."""
 
     def __init__(self):
         self._bufs = {}
+        self._results = {}
+
+    def result(self, tag: str, shape, dtype):
+        key = (tag, tuple(shape), np.dtype(dtype).str)
+        arr = self._results.get(key)
+        # references: this dict, `arr`, getrefcount's argument
+        if arr is not None and sys.getrefcount(arr) <= 3:
+            return arr
+        arr = np.empty(tuple(shape), dtype=dtype)
+        self._results[key] = arr
+        return arr
+
+    def copy_stream(self):
+        import torch
+        if getattr(self, "_cs", None) is None:
+            self._cs = torch.cuda.Stream()
+        return self._cs
 
     def get(self, tag: str, shape, dtype):
         import torch
@@ -60,13 +83,67 @@ class Staging:
         return b
 
 
-def upload(stage: Staging, tag: str, host: np.ndarray, dtype):
+def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int = 4):
     """numpy (any real dtype) -> new CUDA tensor of `dtype`, through a pinned
-    buffer filled by the thread pool."""
+    buffer filled by the thread pool; chunk k's DMA overlaps the conversion of
+    chunk k + 1 (all copies on the current stream)."""
     import torch
     pin = stage.get(tag, host.shape, dtype)
-    copy(pin.numpy(), host)
-    return pin.to("cuda", non_blocking=True)
+    dev = torch.empty(tuple(host.shape), dtype=dtype, device="cuda")
+    n = host.shape[0]
+    chunks = max(1, min(chunks, n))
+    bounds = [n * i // chunks for i in range(chunks + 1)]
+    hp = pin.numpy()
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        copy(hp[a:b], host[a:b])
+        dev[a:b].copy_(pin[a:b], non_blocking=True)
+    return dev
+
+
+def download_blocks(stage: Staging, tag: str, dev, blocks, wait, out_dtype=np.float64):
+    """CUDA tensor -> numpy array while it is still being produced: for each
+    block (lo, hi) of axis 0, in order, `wait(k)` returns once block k is
+    complete on the device; its rows are then copied to a pinned buffer on a
+    copy stream, and a converter thread turns each landed block into the
+    result dtype on the pool while later blocks still compute."""
+    import queue
+    import torch
+    pin = stage.get(tag, dev.shape, dev.dtype)
+    host = pin.numpy()
+    out = stage.result(tag, tuple(dev.shape), out_dtype)
+    cs = stage.copy_stream()
+    q: "queue.Queue" = queue.Queue()
+    futs = []
+
+    def converter():
+        while True:
+            item = q.get()
+            if item is None:
+                return
+            ev, a, b = item
+            ev.synchronize()
+            parts = max(1, min(_THREADS, b - a))
+            cuts = [a + (b - a) * i // parts for i in range(parts + 1)]
+            for x, y in zip(cuts[:-1], cuts[1:]):
+                if y > x:
+                    futs.append(pool().submit(np.copyto, out[x:y], host[x:y], casting="unsafe"))
+
+    th = threading.Thread(target=converter, daemon=True)
+    th.start()
+    try:
+        for k, (a, b) in enumerate(blocks):
+            wait(k)
+            with torch.cuda.stream(cs):
+                pin[a:b].copy_(dev[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            q.put((ev, a, b))
+    finally:
+        q.put(None)
+        th.join()
+    for f in futs:
+        f.result()
+    return out
 
 
 def download(stage: Staging, tag: str, dev, out_dtype=np.float64, chunks: int = 4) -> np.ndarray:
@@ -74,7 +151,7 @@ def download(stage: Staging, tag: str, dev, out_dtype=np.float64, chunks: int = 
     a pinned buffer, each chunk converted while the next one is in flight."""
     import torch
     pin = stage.get(tag, dev.shape, dev.dtype)
-    out = np.empty(tuple(dev.shape), dtype=out_dtype)
+    out = stage.result(tag, tuple(dev.shape), out_dtype)
     n = dev.shape[0]
     chunks = max(1, min(chunks, n))
     bounds = [n * i // chunks for i in range(chunks + 1)]

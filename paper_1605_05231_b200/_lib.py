@@ -83,6 +83,10 @@ _SIGS = {
     "cbn_projector_set_ls_rows": (ctypes.c_int, [c_vp, c_i64, P_i64, c_i64]),
     "cbn_projector_scratch_bytes": (ctypes.c_int, [c_vp, P_i64]),
     "cbn_forward_project": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "cbn_forward_project_async": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "cbn_projector_blocks": (ctypes.c_int, [c_vp, P_i32, P_i32, P_i32]),
+    "cbn_projector_block_sync": (ctypes.c_int, [c_vp, c_i32]),
+    "cbn_forward_finish": (ctypes.c_int, [c_vp, c_vp]),
     "cbn_forward_lattice_size": (ctypes.c_int, [c_vp, P_i64, c_vp]),
     "cbn_forward_lattice": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "cbn_forward_views": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),

@@ -1949,6 +1949,7 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
             }
             gather_views_b(p, v, nb, p->values.p, s, p->fgr.w2inv.p);
             grangeat_reverse(p, p->values.p, frames + (size_t)(v - lo) * p->g.nu * p->g.nv, nb, s);
+            p->block_done(v - lo, v - lo + nb, s);
         }
         return;
     }
@@ -1994,11 +1995,13 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
         if (!blk_n) return;
         const cudaStream_t ls = lane_stream();
         const float* vb = lane ? p->lane1.values.p : p->values.p;
-        for (int k = 0; k < blk_n; k += kViewBlock)
+        for (int k = 0; k < blk_n; k += kViewBlock) {
+            const int nk = std::min(kViewBlock, blk_n - k);
             grangeat_reverse(p, vb + (size_t)k * per_view,
-                             frames + (size_t)(blk_lo + k - lo) * frame_sz,
-                             std::min(kViewBlock, blk_n - k), ls,
+                             frames + (size_t)(blk_lo + k - lo) * frame_sz, nk, ls,
                              lane ? lane_bufs(p) : main_bufs(p));
+            p->block_done(blk_lo + k - lo, blk_lo + k - lo + nk, ls);
+        }
         lane_done();
         blk_lo += blk_n;
         blk_n = 0;
@@ -2074,16 +2077,22 @@ void resample_and_reverse(P* p, int lo, int hi, float* frames, cudaStream_t s,
 }
 
 // views [lo, hi) from a radial lattice (after the radial IFFT) -> frames
-void project_views(P* p, const float2* lat, float* frames, int lo, int hi, cudaStream_t s) {
+// raises CBN_ENONFINITE if any projection of the call was non-finite (syncs s)
+void check_flag(P* p, cudaStream_t s) {
+    int flag = 0;
+    CBN_CUDA(cudaMemcpyAsync(&flag, p->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    if (flag) throw Error(CBN_ENONFINITE, "non-finite projection values");
+}
+
+void project_views(P* p, const float2* lat, float* frames, int lo, int hi, cudaStream_t s,
+                   bool check = true) {
     p->flag.ensure(1);
     CBN_CUDA(cudaMemsetAsync(p->flag.p, 0, sizeof(int), s));
     const RadialTables& r = p->frad;
     lattice_spectrum(p, lat, r.n_rho - r.n_rho / 2, (float)(1.0 / (r.n_rho * r.d_rho)), s);
     resample_and_reverse(p, lo, hi, frames, s);
-    int flag = 0;
-    CBN_CUDA(cudaMemcpyAsync(&flag, p->flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CBN_CUDA(cudaStreamSynchronize(s));
-    if (flag) throw Error(CBN_ENONFINITE, "non-finite projection values");
+    if (check) check_flag(p, s);
 }
 
 // sharded forward, phase 2: the summed pre-IFFT lattice (consumed) -> views
@@ -2098,10 +2107,11 @@ void fwd_views(P* p, float2* lat, float* frames, int lo, int hi, cudaStream_t s)
     project_views(p, lat, frames, lo, hi, s);
 }
 
-void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s) {
+void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s,
+                     bool check = true) {
     build_forward(p, s);
     radial_lattice_raw(p, vol, s);
-    project_views(p, p->lattice.p, frames, lo, hi, s);
+    project_views(p, p->lattice.p, frames, lo, hi, s, check);
 }
 
 }  // namespace
@@ -2247,6 +2257,62 @@ int cbn_forward_project(cbn_projector* p, const float* vol, float* frames, int32
         CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
         CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
         forward_project(p, vol, frames, lo, hi, static_cast<cudaStream_t>(stream));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_project_async(cbn_projector* p, const float* vol, float* frames, int32_t lo,
+                              int32_t hi, void* stream) {
+    try {
+        CBN_REQUIRE(p && vol && frames, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        p->track_blocks = true;
+        p->blk_count = 0;
+        try {
+            forward_project(p, vol, frames, lo, hi, static_cast<cudaStream_t>(stream), false);
+        } catch (...) {
+            p->track_blocks = false;
+            throw;
+        }
+        p->track_blocks = false;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_blocks(cbn_projector* p, int32_t* view_lo, int32_t* view_hi, int32_t* count) {
+    try {
+        CBN_REQUIRE(p && count, "null argument");
+        const int cap = *count;
+        *count = p->blk_count;
+        for (int k = 0; k < std::min(cap, p->blk_count); ++k) {
+            if (view_lo) view_lo[k] = p->blk_lo[(size_t)k];
+            if (view_hi) view_hi[k] = p->blk_hi[(size_t)k];
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_block_sync(cbn_projector* p, int32_t k) {
+    try {
+        CBN_REQUIRE(p && k >= 0 && k < p->blk_count, "block out of range");
+        CBN_CUDA(cudaEventSynchronize(p->blk_ev[(size_t)k]));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_finish(cbn_projector* p, void* stream) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        check_flag(p, static_cast<cudaStream_t>(stream));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

@@ -199,11 +199,35 @@ struct cbn_projector_s {
         cbn::DevBuf<double> red;
     };
     Lane lane1;
+    // progress of an asynchronous forward projection: one event per reverse-
+    // Grangeat block, recorded on the stream that wrote the block's frames
+    // (cbn_forward_project_async / cbn_projector_block_sync)
+    bool track_blocks = false;
+    std::vector<cudaEvent_t> blk_ev;
+    std::vector<int> blk_lo, blk_hi;
+    int blk_count = 0;
+    void block_done(int v_lo, int v_hi, cudaStream_t s) {
+        if (!track_blocks) return;
+        if (blk_count == (int)blk_ev.size()) {
+            cudaEvent_t e;
+            CBN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            blk_ev.push_back(e);
+        }
+        CBN_CUDA(cudaEventRecord(blk_ev[(size_t)blk_count], s));
+        if ((int)blk_lo.size() <= blk_count) {
+            blk_lo.resize((size_t)blk_count + 1);
+            blk_hi.resize((size_t)blk_count + 1);
+        }
+        blk_lo[(size_t)blk_count] = v_lo;
+        blk_hi[(size_t)blk_count] = v_hi;
+        ++blk_count;
+    }
     cudaStream_t s1 = nullptr;
     cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
 
     ~cbn_projector_s() {
         for (auto& kv : ls_rows) delete kv.second;
+        for (auto e : blk_ev) cudaEventDestroy(e);
         if (ev_s0) cudaEventDestroy(ev_s0);
         if (ev_s1) cudaEventDestroy(ev_s1);
         if (s1) cudaStreamDestroy(s1);

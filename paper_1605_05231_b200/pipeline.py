@@ -124,8 +124,9 @@ class Projector:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value and _lib._lib is not None:
-            _lib._lib.cbn_projector_destroy(h)
+        lib = getattr(_lib, "_lib", None) if _lib is not None else None
+        if h and h.value and lib is not None:
+            lib.cbn_projector_destroy(h)
             self._h = ctypes.c_void_p()
 
     @property
@@ -155,6 +156,17 @@ class Projector:
         _lib.check(_lib.load().cbn_backproject(self._h, _device.ptr(f), _device.ptr(out), self._s),
                    "nufft_backproject")
         return out
+
+    def blocks(self):
+        """View blocks [(lo, hi), ...] of the last cbn_forward_project_async,
+        in completion-event order (cbn_projector_blocks)."""
+        lib = _lib.load()
+        cnt = ctypes.c_int32(0)
+        _lib.check(lib.cbn_projector_blocks(self._h, None, None, ctypes.byref(cnt)))
+        lo = (ctypes.c_int32 * max(1, cnt.value))()
+        hi = (ctypes.c_int32 * max(1, cnt.value))()
+        _lib.check(lib.cbn_projector_blocks(self._h, lo, hi, ctypes.byref(cnt)))
+        return [(int(lo[k]), int(hi[k])) for k in range(cnt.value)]
 
     # ---- forward phases (node / view sharding, SURVEY.md 8(e))
     def forward_lattice(self, vol, part: int = 0, nparts: int = 1, out=None):
@@ -439,8 +451,21 @@ def nufft_forward_project(vol: Volume3D, geom, cfg) -> list[DetectorFrame]:
     import torch
     data = np.asarray(vol.data)
     proj = get_projector(geom, cfg, data.shape[0], vol.voxel_mm, _FORWARD)
+    if data.shape != (proj.n,) * 3:
+        raise ValueError(f"volume must be ({proj.n},)*3")
+    lib = _lib.load()
     v = _hostio.upload(proj.stage, "vol", data, torch.float32)
-    frames = _hostio.download(proj.stage, "frames", proj.forward(v))
+    out = torch.empty((geom.n_views, geom.nu, geom.nv), dtype=torch.float32, device="cuda")
+    s = proj._s
+    # every kernel is enqueued at once; the frames of each reverse-Grangeat
+    # block are copied out and converted while later blocks still compute
+    _lib.check(lib.cbn_forward_project_async(proj._h, _device.ptr(v), _device.ptr(out), 0,
+                                             geom.n_views, s), "nufft_forward_project")
+    blocks = proj.blocks()
+    frames = _hostio.download_blocks(
+        proj.stage, "frames", out, blocks,
+        lambda k: _lib.check(lib.cbn_projector_block_sync(proj._h, k), "nufft_forward_project"))
+    _lib.check(lib.cbn_forward_finish(proj._h, s), "nufft_forward_project")
     return [DetectorFrame._checked(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
 
 
@@ -458,12 +483,18 @@ def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volu
     for k, f in enumerate(frames):
         if np.shape(f.data) != shape[1:]:
             raise ValueError("frames must be (n_views, nu, nv)")
-    _hostio.pool()
-    futs = [_hostio.pool().submit(np.copyto, host[k], frames[k].data, casting="unsafe")
-            for k in range(geom.n_views)]
-    for fu in futs:
-        fu.result()
-    vol = proj.backproject(pin.to("cuda", non_blocking=True))
+    dev = torch.empty(shape, dtype=torch.float32, device="cuda")
+    V = geom.n_views
+    bounds = [V * i // 4 for i in range(5)]
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        # frames of this quarter converted on the pool, then their DMA overlaps
+        # the next quarter's conversion
+        futs = [_hostio.pool().submit(np.copyto, host[k], frames[k].data, casting="unsafe")
+                for k in range(a, b)]
+        for fu in futs:
+            fu.result()
+        dev[a:b].copy_(pin[a:b], non_blocking=True)
+    vol = proj.backproject(dev)
     if not bool(torch.isfinite(vol).all()):
         raise ValueError("volume contains non-finite values")
     return Volume3D._checked(_hostio.download(proj.stage, "vol", vol), voxel_mm)
