@@ -106,3 +106,54 @@ def test_validation_errors(nf):
         nf.nufft_forward(plan, np.zeros(7))
     with pytest.raises(ValueError):
         nf.nufft_adjoint(plan, np.zeros(5))
+
+
+def test_chunked_forward_matches_nudft(monkeypatch):
+    """nufft_forward_chunked with 64-node sub-plans, each fitting its own
+    scaling (the reference's test_nufft.py:80-92, _PLAN_CHUNK patched)."""
+    import cbn_oracle as orc
+    from paper_1605_05231_b200 import nufft
+    monkeypatch.setattr(nufft, "_PLAN_CHUNK", 64)
+    rng = np.random.default_rng(11)
+    dims = (8, 8, 8)
+    nodes = rng.uniform(-np.pi, np.pi, (200, 3))
+    x = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
+    ref = orc.nudft(dims, nodes, x)
+    got = nufft.nufft_forward_chunked(dims, nodes, x, 2.0, 6)
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 2e-5
+    # the sub-plans are separate plans: chunk k equals a plan of its own nodes
+    k = nufft.nufft_forward(nufft.plan_nufft(dims, nodes[64:128], 2.0, 6), x)
+    assert np.array_equal(got[64:128], k)
+
+
+def test_chunked_adjoint_is_adjoint_of_chunked_forward(monkeypatch):
+    """(reference test_nufft.py:95-105) at fp32: dot test <= 1e-6."""
+    from paper_1605_05231_b200 import nufft
+    monkeypatch.setattr(nufft, "_PLAN_CHUNK", 64)
+    rng = np.random.default_rng(12)
+    dims = (8, 8, 8)
+    nodes = rng.uniform(-np.pi, np.pi, (200, 3))
+    x = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
+    y = rng.standard_normal(200) + 1j * rng.standard_normal(200)
+    lhs = np.vdot(y, nufft.nufft_forward_chunked(dims, nodes, x, 2.0, 3))
+    rhs = np.vdot(nufft.nufft_adjoint_chunked(dims, nodes, y, 2.0, 3), x)
+    assert abs(lhs - rhs) / abs(lhs) < 1e-6
+
+
+def test_chunked_matches_oracle_per_chunk_scaling(monkeypatch):
+    """Chunked forward/adjoint against the oracle's chunked restatement
+    (oracle type2_chunked / type1_chunked, per-chunk LS scaling) at 1e-5."""
+    import cbn_oracle as orc
+    from paper_1605_05231_b200 import nufft
+    monkeypatch.setattr(nufft, "_PLAN_CHUNK", 3000)
+    rng = np.random.default_rng(13)
+    dims = (16, 12, 10)
+    nodes = rng.uniform(-np.pi, np.pi, (10000, 3))
+    x = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
+    y = rng.standard_normal(10000) + 1j * rng.standard_normal(10000)
+    got = nufft.nufft_forward_chunked(dims, nodes, x, 2.0, 6)
+    ref = orc.type2_chunked(dims, nodes, x, 2.0, 6, chunk=3000)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
+    got = nufft.nufft_adjoint_chunked(dims, nodes, y, 2.0, 6)
+    ref = orc.type1_chunked(dims, nodes, y, 2.0, 6, chunk=3000)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5

@@ -64,3 +64,19 @@ def test_cli_validation_exit_code(tmp_path):
     from paper_1605_05231_b200.cli import main
     assert main(["project", "--method", "nufft-a", "--volume", str(tmp_path / "x.raw"),
                  "--out", str(tmp_path / "o.raw")]) == 2
+
+
+def test_cli_numerical_failure_exit_code(tmp_path, monkeypatch):
+    """Exit code 3 on a non-finite result (the reference's test_cli.py:118-131
+    contract, with its monkeypatch of cli.ct_project_linear)."""
+    from paper_1605_05231_b200 import cli
+
+    def bad_project(vol, geom):
+        class F:   # a frame the projector failed on (bypasses the frame validator)
+            data = np.full((geom.nu, geom.nv), np.nan)
+        return [F() for _ in range(geom.n_views)]
+    monkeypatch.setattr(cli, "ct_project_linear", bad_project)
+    code = cli.main(["project", "--method", "linear", "--volume", os.path.join(IO, "vol.raw"),
+                     "--geometry", os.path.join(IO, "geom.json"),
+                     "--out", str(tmp_path / "o.raw")])
+    assert code == 3

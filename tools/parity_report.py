@@ -53,6 +53,63 @@ def main():
     bp = pl.nufft_backproject(frames, geom, cfg, 64, voxel).data
     print(f"{'config0 fwd / config1 bp (64^3, 90v)':34s} {rel_l2(fr, z['frames']):15.2e} {worst:11.2e} "
           f"{rel_l2(bp, z['bp']):12.2e}")
+    # round-2 fixtures: CLI default geometry, config 2, bins at config 0/1
+    from conftest import unpack_int
+    from paper_1605_05231_b200.config import make_projector_config
+    from paper_1605_05231_b200.geometry import ConeGeometry
+    from paper_1605_05231_b200.phantom import random_ellipsoid_phantom, random_ellipsoids
+    from paper_1605_05231_b200.workloads import analytic_projections
+    z = dict(np.load(os.path.join(GOLDEN, "cli_default.npz")))
+    g = z["geom"]
+    geom = ConeGeometry(float(g[0]), float(g[1]), float(g[2]), float(g[3]), int(g[4]),
+                        int(g[5]), int(g[6]), float(g[7]))
+    n, voxel = int(z["n"]), float(z["voxel"])
+    cfg = make_projector_config(geom, n, "a")
+    fr = np.stack([f.data for f in pl.nufft_forward_project(Volume3D(z["vol"], voxel), geom, cfg)])
+    bp = pl.nufft_backproject([DetectorFrame(k, z["frames"][k].astype(np.float64), geom.pixel_mm)
+                               for k in range(geom.n_views)], geom, cfg, n, voxel).data
+    st = pl.get_projector(geom, cfg, n, voxel, pl._FORWARD).plan_stats()
+    print(f"{'CLI default geometry (N=16, 12v)':34s} {rel_l2(fr, z['frames']):15.2e} "
+          f"{max(rel_l2(fr[k], z['frames'][k]) for k in range(geom.n_views)):11.2e} "
+          f"{rel_l2(bp, z['bp']):12.2e}   invalid targets {int(z['invalid_fwd'])}, "
+          f"heavy cells {st['fwd_gr_heavy_cells']}")
+    geom, voxel, spec, cfg = config_setup(2)
+    vol = random_ellipsoid_phantom(256, 30, 2)
+    z = np.load(os.path.join(GOLDEN, "config2_fwd.npz"))
+    proj = pl.Projector(geom, cfg, 256, voxel, 1)
+    lat = proj.radial_lattice(vol).cpu().numpy()
+    r, t, p = (np.asarray(a, dtype=np.int64) for a in z["lat_idx"].T)
+    e_lat = rel_l2(lat[p, t, r], z["lat_val"])
+    del lat
+    frs = pl.nufft_forward_project(Volume3D(vol, voxel), geom, cfg)
+    errs = [rel_l2(frs[int(k)].data, z["frames"][i]) for i, k in enumerate(z["views"])]
+    zb = np.load(os.path.join(GOLDEN, "config2_bp.npz"))
+    af = analytic_projections(geom, random_ellipsoids(30, 2))
+    vb = pl.nufft_backproject([DetectorFrame(k, af[k], geom.pixel_mm) for k in range(360)],
+                              geom, cfg, 256, voxel).data
+    blocks = vb.reshape(64, 4, 64, 4, 64, 4).mean(axis=(1, 3, 5))
+    e_bp = max(rel_l2(vb[128], zb["x"]), rel_l2(vb[:, 128], zb["y"]), rel_l2(vb[:, :, 128], zb["z"]))
+    print(f"{'config 2 (256^3, 360v)':34s} {'lattice':>7s} {e_lat:.2e}  views "
+          + " ".join(f"{e:.2e}" for e in errs)
+          + f"  bp slices {e_bp:.2e} blocks {rel_l2(blocks, zb['blocks']):.2e}")
+    print()
+    zb = np.load(os.path.join(GOLDEN, "bins_config0.npz"))
+    geom, voxel, spec, cfg = config_setup(0)
+    proj = pl.Projector(geom, cfg, 64, voxel, 3)
+    total = bad = 0
+    for key in [k[:-3] for k in zb.files if k.endswith("__z")]:
+        direction = "back" if key.endswith("_bp") or key.startswith("umb_bp") else "forward"
+        node_set = "radial" if key.startswith("radial") else ("polar" if key.startswith("polar")
+                                                             else "umbrella")
+        batch = int(key.rsplit("_", 1)[1]) if node_set == "umbrella" else 0
+        ref = unpack_int(zb, key)
+        got = proj.first_indices(direction, node_set, batch).astype(np.int64)
+        nb = int(np.any(got != ref, axis=1).sum())
+        total += ref.shape[0]
+        bad += nb
+        print(f"bins {key:14s} {ref.shape[0]:9d} nodes  mismatches {nb}")
+    print(f"bins total {total} nodes, mismatches {bad}")
+    print()
     # config 4 shapes: 256^3 grid, 1M float32 points, J=8, against the direct DFT
     import cbn_oracle as orc
     from paper_1605_05231_b200.workloads import config4_inputs
