@@ -166,7 +166,10 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
         tap_setup<D, J>(kb, w, first, wt);
         int l[3] = {0, 0, 0};
 #pragma unroll
-        for (int d = 0; d < D; ++d) l[d] = wrapc(first[d], tg.K[d]) - o[d];
+        for (int d = 0; d < D; ++d) {
+            l[d] = wrapc(first[d], tg.K[d]) - o[d];
+            CBN_DCHECK(l[d] >= 0 && l[d] < tg.T[d], "gather: point outside its bin tile");
+        }
         float2 acc = make_float2(0.f, 0.f);
         if constexpr (D == 3) {
 #pragma unroll
@@ -250,6 +253,9 @@ k_spread_binned(float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src,
             l0 = wrapc(first[0], tg.K[0]) - o[0];
             l1 = wrapc(first[1], tg.K[1]) - o[1];
             if constexpr (D == 3) l2 = wrapc(first[2], tg.K[2]) - o[2];
+            CBN_DCHECK(l0 >= 0 && l0 < tg.T[0] && l1 >= 0 && l1 < tg.T[1] && l2 >= 0 &&
+                           (D == 2 || l2 < tg.T[2]),
+                       "spread: point outside its bin tile");
 #pragma unroll
             for (int d = 0; d < D; ++d)
 #pragma unroll
@@ -384,6 +390,9 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const int l0 = wrapc(first[0], tg.K[0]) - o[0];
             const int l1 = wrapc(first[1], tg.K[1]) - o[1];
             const int l2 = wrapc(first[2], tg.K[2]) - o[2];
+            CBN_DCHECK(l0 >= 0 && l0 < tg.T[0] && l1 >= 0 && l1 < tg.T[1] && l2 >= 0 &&
+                           l2 < tg.T[2],
+                       "owned spread: point outside its bin tile");
             stl[threadIdx.x] = (l0 << 24) | ((l0 * R1 + l1) * P + l2);
             stv[threadIdx.x] = v;
 #pragma unroll
@@ -563,6 +572,9 @@ k_spread_owned8(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const int l0 = wrapc(first[0], tg.K[0]) - o[0];
             const int l1 = wrapc(first[1], tg.K[1]) - o[1];
             const int l2 = wrapc(first[2], tg.K[2]) - o[2];
+            CBN_DCHECK(l0 >= 0 && l0 < tg.T[0] && l1 >= 0 && l1 < tg.T[1] && l2 >= 0 &&
+                           l2 < tg.T[2],
+                       "owned spread: point outside its bin tile");
             hdr[threadIdx.x] = make_float4(v.x, v.y, __int_as_float((l0 << 24) | ((l0 * R1 + l1) * P + l2)),
                                            0.f);
             float* ws = stw + threadIdx.x * SW;

@@ -15,6 +15,28 @@
 #define CBN_HD __host__ __device__ __forceinline__
 #define CBN_D __device__ __forceinline__
 
+// Device-side checks of the check build (make check -> libcbnufft_b200_check.so,
+// -DCBN_BOUNDS_CHECK): every binned kernel asserts that a point's first tap
+// lies in its bin's tile (so all J^d taps stay inside the shared-memory
+// region), the window gather asserts its buffer indices, the cell gather its
+// row ids.  compute-sanitizer is not available on this GPU pool; this build
+// plus the parity tests is the memory check.  Off (no code) otherwise.
+#ifdef CBN_BOUNDS_CHECK
+#include <cstdio>
+#define CBN_DCHECK(cond, what)                                                            \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("CBN_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                          \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define CBN_DCHECK(cond, what) \
+    do {                       \
+    } while (0)
+#endif
+
 namespace cbn {
 
 // numpy's float64 pi and 2*pi (exact doubles)

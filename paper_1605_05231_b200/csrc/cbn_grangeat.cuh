@@ -53,6 +53,8 @@ __global__ void k_gr_points(KBSet kb, TileGeom<2> tg, PolarSrc src, GrFactor f,
         GrPoint<J> g;
         g.lu = (short)(wrapc(first[0], tg.K[0]) - o[0]);
         g.lv = (short)(wrapc(first[1], tg.K[1]) - o[1]);
+        CBN_DCHECK(g.lu >= 0 && g.lu < tg.T[0] && g.lv >= 0 && g.lv < tg.T[1],
+                   "grangeat: point outside its bin tile");
         const int im = i / f.n_t;
         const int kr = (aux.jt - f.n_t / 2 + f.n_t) % f.n_t;   // fftshift of the t FFT
         g.col = im * f.n_t + kr;

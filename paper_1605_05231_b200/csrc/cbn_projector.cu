@@ -411,6 +411,7 @@ k_resample_window(const float* __restrict__ G, int K2, const RsRow3* __restrict_
             // pole target: its phi cell follows each view's own geometry
             for (int v = lane; v < nv; v += 32) {
                 const int c0 = pole_f2[(int64_t)rr.pad * n_views + v0 + v];
+                CBN_DCHECK(c0 >= 0 && c0 < K2, "window gather: pole cell out of range");
                 const int c1 = c0 + 1 >= K2 ? c0 + 1 - K2 : c0 + 1;
                 const int c2 = c0 + 2 >= K2 ? c0 + 2 - K2 : c0 + 2;
                 float acc = 0.f;
@@ -459,6 +460,7 @@ k_resample_window(const float* __restrict__ G, int K2, const RsRow3* __restrict_
         for (int v = lane; v < nv; v += 32, o -= step32, o += o < 0 ? K2 : 0) {
             // the three cells as one aligned pair + one cell (an even shift keeps
             // the lanes' pairs on distinct banks: 2 wavefronts per read)
+            CBN_DCHECK(o >= 0 && o + 2 < (full ? K2 + 2 : 4 * n4), "window gather: cell outside window");
             float b0, b1, b2;
             if (o & 1) {
                 b0 = buf[o];

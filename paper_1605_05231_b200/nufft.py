@@ -105,8 +105,9 @@ class NufftPlan:
 
     def __del__(self):
         h, self._handle = self._handle, 0
-        if h and _lib._lib is not None:
-            _lib._lib.cbn_nufft_destroy(ctypes.c_void_p(h))
+        lib = getattr(_lib, "_lib", None) if _lib is not None else None
+        if h and lib is not None:
+            lib.cbn_nufft_destroy(ctypes.c_void_p(h))
 
     @property
     def handle(self):
