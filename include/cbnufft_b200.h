@@ -118,6 +118,24 @@ int cbn_resample_transpose(cbn_resample* plan, const void* values, void* lattice
 int cbn_radial_fft(void* data, int64_t n, int64_t lines, int32_t inverse, double scale,
                    void* stream);
 
+/* per-rho complex weights (spectral_rho_derivative radon_fourier.py:111-114,
+ * ramp_filter_radial 160-164, the fbp2d_nufft ramp 206-207): complex64 data
+ * [device] viewed as [outer][n][inner], element (o, k, i) *= w[k]; w is host
+ * float64 (re, im) pairs, n of them */
+int cbn_line_weight(void* data, int64_t outer, int64_t n, int64_t inner, const double* w,
+                    void* stream);
+
+/* _center_phase (radon_fourier.py:52-56) applied in place: values[i] (complex64,
+ * device) *= exp(+-i nodes[i] . shift) (minus when conj != 0), times w[i / w_inner]
+ * when w (host float64) is given; nodes are host float64 m x d, d <= 3 */
+int cbn_node_phase(void* values, const double* nodes, int64_t m, int32_t d, const double* shift,
+                   int32_t conj, const double* w, int64_t w_inner, void* stream);
+
+/* trilinear_transfer (radon_fourier.py:75-86): prod_d sinc^2(node_d / 2 pi) at the
+ * unwrapped radial nodes, written float64 [phi][theta][rho] (node order) [device] */
+int cbn_trilinear_transfer(int32_t n_rho, int32_t n_theta, int32_t n_phi, double delta_rho,
+                           double voxel_mm, double* out, void* stream);
+
 /* -------------------------------------------------------------- projector
  * Replaces ConeGeometry / ProjectorConfig / nufft_forward_project /
  * nufft_backproject (geometry.py:21-64, pipeline.py:31-212).

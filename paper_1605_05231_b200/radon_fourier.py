@@ -1,9 +1,11 @@
 """Fourier-slice transforms (drop-in for ``cbnufft/radon_fourier.py``).
 
-Device paths: ``image_to_radial_spectrum`` (3D type-2 NUFFT onto the radial
-lines through the projector plan), ``radial_fft`` / ``radial_ifft`` (centred
-cuFFT along rho), the 2D helpers (device NUFFT plans).  The remaining
-functions are O(size) elementwise weights kept on the host for API parity.
+Every data pass runs on the device: ``image_to_radial_spectrum`` (3D type-2
+NUFFT onto the radial lines through the projector plan), ``radial_fft`` /
+``radial_ifft`` (centred cuFFT along rho), the per-rho weights of
+``spectral_rho_derivative`` / ``ramp_filter_radial`` and the sinc^2 transfer
+(``csrc/cbn_lines.cu``), and the 2D helpers (device NUFFT plans plus the
+node-phase kernel).  Only O(n_rho) weight vectors are formed on the host.
 Layouts follow the reference: lattices are (n_rho, n_theta, n_phi).
 """
 
@@ -76,9 +78,29 @@ def _to_lattice(node_order: np.ndarray, spec) -> np.ndarray:
 
 
 def trilinear_transfer(spec, voxel_mm: float) -> np.ndarray:
-    """sinc^2 transfer of the trilinear voxel basis (radon_fourier.py:75-86)."""
-    nodes = _radial_direction_nodes(spec, voxel_mm)
-    return _to_lattice(np.prod(np.sinc(nodes / (2.0 * np.pi)), axis=-1) ** 2, spec)
+    """sinc^2 transfer of the trilinear voxel basis (radon_fourier.py:75-86), device kernel."""
+    t = _device.require_cuda()
+    n_r, n_t, n_p, _ = spec_tuple(spec)
+    out = t.empty((n_p, n_t, n_r), dtype=t.float64, device="cuda")
+    _lib.check(_lib.load().cbn_trilinear_transfer(n_r, n_t, n_p, float(spec.delta_rho),
+                                                  float(voxel_mm), _device.ptr(out),
+                                                  ctypes.c_void_p(_device.stream_ptr())),
+               "trilinear_transfer")
+    return _to_lattice(out.cpu().numpy().reshape(-1), spec)
+
+
+def _rho_weighted(data, w: np.ndarray) -> np.ndarray:
+    """data (n_rho, ...) complex times w[rho] (complex), on the device."""
+    t = _device.require_cuda()
+    arr = np.asarray(data)
+    x = _device.to_device(arr, t.complex64).contiguous()
+    n = arr.shape[0]
+    inner = int(np.prod(arr.shape[1:])) if arr.ndim > 1 else 1
+    wc = np.ascontiguousarray(np.stack([np.real(w), np.imag(w)], axis=-1), dtype=np.float64)
+    _lib.check(_lib.load().cbn_line_weight(_device.ptr(x), 1, n, inner,
+                                           wc.ctypes.data_as(_lib.P_f64),
+                                           ctypes.c_void_p(_device.stream_ptr())), "line weight")
+    return x.cpu().numpy().astype(np.complex128)
 
 
 def _spectrum_projector(n: int, voxel_mm: float, spec, j, oversample_factor):
@@ -103,7 +125,8 @@ def image_to_radial_spectrum(vol, spec, j=6, oversample_factor: float = 2.0) -> 
 
 
 def spectral_rho_derivative(s: RadialSpectrum3D) -> RadialSpectrum3D:
-    return RadialSpectrum3D(s.spec, s.data * (1j * radial_omega(s.spec))[:, None, None])
+    """x i*omega_rho along rho (radon_fourier.py:111-114), device kernel."""
+    return RadialSpectrum3D(s.spec, _rho_weighted(s.data, 1j * radial_omega(s.spec)))
 
 
 def _radial_transform(data, spec, inverse: bool, scale: float) -> np.ndarray:
@@ -145,9 +168,10 @@ def ramp_weights(n_rho: int, delta_rho: float, n_theta: int, dimension: int,
 
 
 def ramp_filter_radial(s: RadialSpectrum3D, dimension: int) -> RadialSpectrum3D:
+    """Ramp weights along rho (radon_fourier.py:160-164), device kernel."""
     w = ramp_weights(int(s.spec.n_rho), s.spec.delta_rho, int(s.spec.n_theta), dimension,
                      int(s.spec.n_phi))
-    return RadialSpectrum3D(s.spec, s.data * w[:, None, None])
+    return RadialSpectrum3D(s.spec, _rho_weighted(s.data, w.astype(np.complex128)))
 
 
 def _polar_nodes_2d(n: int, n_rho: int, n_theta: int):
@@ -158,29 +182,53 @@ def _polar_nodes_2d(n: int, n_rho: int, n_theta: int):
     return np.stack([(ww * np.cos(tt)).ravel(), (ww * np.sin(tt)).ravel()], axis=-1), delta_rho
 
 
+def _phase_on_device(values, nodes: np.ndarray, n: int, conj: bool, w=None, w_inner: int = 1):
+    """values (device complex64) *= exp(+-i nodes . shift) [* w[i // w_inner]] in place."""
+    shift = np.array([n / 2.0 - 0.5, n / 2.0 - 0.5], dtype=np.float64)
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    wp = None
+    if w is not None:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        wp = w.ctypes.data_as(_lib.P_f64)
+    _lib.check(_lib.load().cbn_node_phase(_device.ptr(values), nodes.ctypes.data_as(_lib.P_f64),
+                                          nodes.shape[0], nodes.shape[1],
+                                          shift.ctypes.data_as(_lib.P_f64), 1 if conj else 0, wp,
+                                          int(w_inner), ctypes.c_void_p(_device.stream_ptr())),
+               "center phase")
+    return values
+
+
 def image_to_radial_spectrum_2d(image, n_rho: int, n_theta: int, j=6,
                                 oversample_factor: float = 2.0) -> np.ndarray:
-    """2D NUFFT onto radial lines (radon_fourier.py:168-188), device NUFFT."""
+    """2D NUFFT onto radial lines (radon_fourier.py:168-188), device NUFFT + phase."""
     from .nufft import nufft_forward, plan_nufft
+    t = _device.require_cuda()
     image = np.asarray(image)
     if image.ndim != 2 or image.shape[0] != image.shape[1]:
         raise ValueError("image must be square")
     n = image.shape[0]
     nodes, _ = _polar_nodes_2d(n, n_rho, n_theta)
     values = nufft_forward(plan_nufft((n, n), nodes, oversample_factor, j),
-                           image.astype(np.complex128))
-    return (values * _center_phase(nodes, (n, n))).reshape(n_rho, n_theta)
+                           _device.to_device(image, t.complex64))
+    _phase_on_device(values, nodes, n, conj=False)
+    return values.cpu().numpy().astype(np.complex128).reshape(n_rho, n_theta)
 
 
 def fbp2d_nufft(spectrum, out_size: int, j=6, oversample_factor: float = 2.0):
-    """2D NUFFT filtered backprojection (radon_fourier.py:191-213), device NUFFT."""
+    """2D NUFFT filtered backprojection (radon_fourier.py:191-213), device NUFFT + ramp."""
     from .nufft import nufft_adjoint, plan_nufft
-    spectrum = np.asarray(spectrum, dtype=np.complex128)
+    t = _device.require_cuda()
+    spectrum = np.asarray(spectrum)
+    if spectrum.ndim != 2:
+        raise ValueError("spectrum must be (n_rho, n_theta)")
     n_rho, n_theta = spectrum.shape
     n = int(out_size)
     nodes, delta_rho = _polar_nodes_2d(n, n_rho, n_theta)
     w = ramp_weights(n_rho, delta_rho, n_theta, 2)
-    y = (spectrum * w[:, None]).ravel() * np.conj(_center_phase(nodes, (n, n)))
+    y = _device.to_device(spectrum.reshape(-1), t.complex64)
+    _phase_on_device(y, nodes, n, conj=True, w=w, w_inner=n_theta)
     grid = nufft_adjoint(plan_nufft((n, n), nodes, oversample_factor, j), y)
-    real_norm = np.linalg.norm(grid.real)
-    return grid.real.copy(), np.linalg.norm(grid.imag) / max(real_norm, 1e-300)
+    g = grid.cpu().numpy()
+    re = g.real.astype(np.float64)
+    real_norm = float(np.linalg.norm(re))
+    return re, float(np.linalg.norm(g.imag.astype(np.float64))) / max(real_norm, 1e-300)
