@@ -221,6 +221,17 @@ int cbn_forward_views(cbn_projector* proj, void* lattice, float* frames, int32_t
  * -> vol [device] float32 N^3 */
 int cbn_backproject(cbn_projector* proj, const float* frames, float* vol, void* stream);
 
+/* Upload-overlapped nufft_backproject: the forward Grangeat step of views
+ * [lo, hi) runs as soon as their frames are on the device (frames [device]
+ * float32 (hi - lo) x nu x nv, the views themselves), while the host still
+ * converts and copies later views; the next cbn_backproject on the same
+ * stream consumes the staged views once all n_views have been staged (and
+ * drops a partial staging).  Views arrive in order, blocks start on 32-view
+ * bounds.  CBN_EUNSUPPORTED (nothing staged) where the plan has more than one
+ * resample scaling group or uses method B: call cbn_backproject alone. */
+int cbn_backproject_stage_views(cbn_projector* proj, const float* frames, int32_t lo, int32_t hi,
+                                void* stream);
+
 /* nufft_backproject in three phases, for sharding views and nodes across
  * devices; cbn_backproject == views(all) + finish(0 of 1) +
  * crop.  Buffers [device] complex64, caller-owned:
@@ -314,6 +325,11 @@ int cbn_projector_first_indices(cbn_projector* proj, int32_t set, int32_t batch,
  * the plan is not built yet): primary nodes of the conjugate-pair gathers,
  * resample rho planes used, invalid umbrella targets per view, batch scaling
  * groups, reverse-Grangeat heavy cells, ...  Synchronises. */
+/* Diagnostics: copy the named plan buffer (den_cache, den_max, bspec_s32,
+ * ramp_q, bpairs, bspec_perm, bspec_subs, bbatch_s32, fspec_s32, values_t, lattice) to
+ * host memory `out` (null: only report its size in *bytes) */
+int cbn_projector_debug_buffer(cbn_projector* proj, const char* name, void* out, int64_t* bytes,
+                               void* stream);
 int cbn_projector_plan_stats(cbn_projector* proj, int64_t* vals, int32_t* count, char* names,
                              int32_t names_len, void* stream);
 

@@ -76,6 +76,8 @@ _SIGS = {
     "cbn_resample_apply": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_resample_transpose": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_radial_fft": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i32, c_f64, c_vp]),
+    "cbn_projector_debug_buffer": (ctypes.c_int, [c_vp, ctypes.c_char_p, c_vp, P_i64, c_vp]),
+    "cbn_backproject_stage_views": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_line_weight": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, P_f64, c_vp]),
     "cbn_node_phase": (ctypes.c_int, [c_vp, P_f64, c_i64, c_i32, P_f64, c_i32, P_f64, c_i64, c_vp]),
     "cbn_trilinear_transfer": (ctypes.c_int, [c_i32, c_i32, c_i32, c_f64, c_f64, c_vp, c_vp]),

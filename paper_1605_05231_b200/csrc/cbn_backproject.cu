@@ -179,6 +179,27 @@ __global__ void k_den_final(const float2* __restrict__ acc_den, int64_t lines, i
     den[e] = (j == n / 2) ? (float)means[0] : (float)((double)acc_den[line * dr + pad + j].x * inv);
 }
 
+// den over each phi orbit {c, c + s, ...} (node order [phi][theta][rho]):
+// the float64 mean written back to every member
+__global__ void k_den_orbit_mean(float* __restrict__ den, int n_rho, int n_theta, int n_phi,
+                                 int sft) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t plane = (int64_t)n_rho * n_theta;
+    if (e >= plane * sft) return;
+    const int c = (int)(e / plane);
+    const int64_t rt = e - (int64_t)c * plane;
+    double sum = 0.0;
+    int cnt = 0;
+    for (int f = c; f < n_phi; f += sft, ++cnt) sum += (double)den[(int64_t)f * plane + rt];
+    const float m = (float)(sum / cnt);
+    for (int f = c; f < n_phi; f += sft) den[(int64_t)f * plane + rt] = m;
+}
+
+bool den_orbit_off() {   // CBN_DEN_ORBIT=0: per-entry den (A/B)
+    const char* e = std::getenv("CBN_DEN_ORBIT");
+    return e && e[0] == '0';
+}
+
 __global__ void k_max_partial(const float* __restrict__ x, int64_t total, double* __restrict__ partial) {
     double mx = -1e308;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -460,6 +481,9 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
                 taps.p, n, (int)x.kd3[0], (int)x.kd3[1], counts.p,
                 reinterpret_cast<RsColEntry*>(p->bcol_ent.p));
             CBN_LAUNCH_CHECK();
+            k_rs_col_sort<<<blocks_for(ncol, 128), 128, 0, s>>>(
+                p->bcol_ptr.p, ncol, reinterpret_cast<RsColEntry*>(p->bcol_ent.p));
+            CBN_LAUNCH_CHECK();
             CBN_CUDA(cudaStreamSynchronize(s));
         }
     }
@@ -472,6 +496,42 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
 bool rho_lines_off_bp() {   // CBN_RHO_LINES=0: the strided rho pass (A/B)
     const char* e = std::getenv("CBN_RHO_LINES");
     return e && e[0] == '0';
+}
+
+// forward Grangeat of n views (frames: the first of them) into values
+// ([view][n_mu][n_t]) or target-major outT columns k0 .. k0 + n - 1 of row
+// length nb_total; blocks of 32 views alternate between the caller's stream
+// and s1 when there are more than 32
+void bp_grangeat_views(cbn_projector_s* p, const float* frames, int n, float* out, float* outT,
+                       int nb_total, int k0, cudaStream_t s) {
+    const int nu = p->g.nu, nv = p->g.nv;
+    const int64_t per_view = (int64_t)p->bumb.n_mu * p->bumb.n_t;
+    const bool dual = n > 32 && lanes_allowed() && !p->timer.on;
+    if (dual) {
+        // plan state both lanes read, then fork
+        GrangeatPlan& gp = p->bgr;
+        if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
+        projector_prepare_gr_points(p, gp, p->bumb, false, s);
+        // gp.pix is built lazily by the first block; build it before the
+        // fork so lane 1's first pad kernel is ordered after it
+        projector_gr_pix(p, gp, false, s);
+        ensure_lane1(p);
+        CBN_CUDA(cudaEventRecord(p->ev_s0, s));
+        CBN_CUDA(cudaStreamWaitEvent(p->s1, p->ev_s0, 0));
+    }
+    for (int k = 0; k < n; k += 32) {
+        const bool l1 = dual && ((k / 32) & 1);
+        const cudaStream_t ls = l1 ? p->s1 : s;
+        StageScope st(p->timer, "grangeat_forward", ls);
+        const int m = std::min(32, n - k);
+        grangeat_forward_block(p, frames + (size_t)k * nu * nv, m,
+                               outT ? nullptr : out + (size_t)k * per_view, ls,
+                               l1 ? lane_bufs(p) : main_bufs(p), outT, nb_total, k0 + k);
+    }
+    if (dual) {
+        CBN_CUDA(cudaEventRecord(p->ev_s1, p->s1));
+        CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
+    }
 }
 
 // transposed resample of views [lo, hi) accumulated into acc (dsize complex,
@@ -487,35 +547,9 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
     const int nu = p->g.nu, nv = p->g.nv;
     CBN_CUDA(cudaMemsetAsync(acc, 0, sizeof(float2) * x.dsize, s));
     p->s32.ensure(3 * (size_t)std::max(bp.smax, p->n_vol));
-    // blocks of 32 views alternate between the caller's stream and s1
     // out: [view][n_mu][n_t] values; or (outT) target-major [target][nb]
     auto forward_grangeat = [&](int v0, int nb, float* out, float* outT = nullptr) {
-        const bool dual = nb > 32 && lanes_allowed() && !p->timer.on;
-        if (dual) {
-            // plan state both lanes read, then fork
-            GrangeatPlan& gp = p->bgr;
-            if (!gp.built) projector_fit_grangeat(p, gp, p->bumb, s);
-            projector_prepare_gr_points(p, gp, p->bumb, false, s);
-            // gp.pix is built lazily by the first block; build it before the
-            // fork so lane 1's first pad kernel is ordered after it
-            projector_gr_pix(p, gp, false, s);
-            ensure_lane1(p);
-            CBN_CUDA(cudaEventRecord(p->ev_s0, s));
-            CBN_CUDA(cudaStreamWaitEvent(p->s1, p->ev_s0, 0));
-        }
-        for (int k = 0; k < nb; k += 32) {
-            const bool l1 = dual && ((k / 32) & 1);
-            const cudaStream_t ls = l1 ? p->s1 : s;
-            StageScope st(p->timer, "grangeat_forward", ls);
-            const int n = std::min(32, nb - k);
-            grangeat_forward_block(p, frames + (size_t)(v0 + k - lo) * nu * nv, n,
-                                   outT ? nullptr : out + (size_t)k * per_view, ls,
-                                   l1 ? lane_bufs(p) : main_bufs(p), outT, nb, k);
-        }
-        if (dual) {
-            CBN_CUDA(cudaEventRecord(p->ev_s1, p->s1));
-            CBN_CUDA(cudaStreamWaitEvent(s, p->ev_s1, 0));
-        }
+        bp_grangeat_views(p, frames + (size_t)(v0 - lo) * nu * nv, nb, out, outT, nb, 0, s);
     };
     // views-in-lanes: the transposed grid is real, [rho][theta][phi] (phi =
     // rax[0]), stored after its half spectrum [rho][theta][phi/2+1]
@@ -687,9 +721,13 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
             const int nvr = vhi - vlo;
             if (!den_only) {
                 // the Grangeat post writes the values target-major for the
-                // column gather (no separate transpose)
-                p->values_t.ensure((size_t)per_view * nvr);
-                forward_grangeat(vlo, nvr, nullptr, p->values_t.p);
+                // column gather (no separate transpose); a staged call
+                // (cbn_backproject_stage_views) has done it view block by
+                // view block while the frames were still being uploaded
+                if (!(p->bp_staged == p->g.n_views && vlo == 0 && vhi == p->g.n_views)) {
+                    p->values_t.ensure((size_t)per_view * nvr);
+                    forward_grangeat(vlo, nvr, nullptr, p->values_t.p);
+                }
             }
             {
                 StageScope st(p->timer, "transpose_spread", s);
@@ -799,6 +837,23 @@ void bp_den(cbn_projector_s* p, const BpCtx& x, cudaStream_t s) {
     k_den_final<<<blocks_for(M, 256), 256, 0, s>>>(acc_den, r.lines(), x.dr, p->bpad, r.n_rho, inv,
                                                     means + 2, p->den_cache.p);
     CBN_LAUNCH_CHECK();
+    // Rotation-aligned views (each view's targets are view 0's rotated by a
+    // whole number s of lattice phi cells, one resample scaling group): the
+    // transposed resample is phi-shift equivariant, so den is exactly
+    // invariant under phi -> phi + s.  The reference's den (float64) is then
+    // uniform over each phi orbit up to 1e-15, and its keep decision
+    // den > den_tol * max(den) (pipeline.py:187-188) takes or drops a whole
+    // orbit.  The float32 evaluations of one orbit scatter by ~1e-5 of the
+    // threshold, enough to split an orbit that sits that close to it; the
+    // orbit mean (in float64) restores the all-or-nothing decision and
+    // averages the rounding of its V / (n_phi / s) evaluations.
+    if (x.lanes && p->bbatch.groups() == 1 && r.n_phi % p->g.n_views == 0 && !den_orbit_off()) {
+        const int sft = r.n_phi / p->g.n_views;
+        const int64_t orbits = (int64_t)r.n_rho * r.n_theta * sft;
+        k_den_orbit_mean<<<blocks_for(orbits, 256), 256, 0, s>>>(p->den_cache.p, r.n_rho,
+                                                                 r.n_theta, r.n_phi, sft);
+        CBN_LAUNCH_CHECK();
+    }
     k_max_partial<<<kRed, 256, 0, s>>>(p->den_cache.p, M, p->red.p);
     CBN_LAUNCH_CHECK();
     k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, p->den_max.p);
@@ -1085,10 +1140,33 @@ bool bp_uses_lanes(cbn_projector_s* p, cudaStream_t s) { return bp_context(p, s)
 
 void backproject_impl(cbn_projector_s* p, const float* frames, float* vol, cudaStream_t s) {
     BpCtx x = bp_context(p, s);
+    struct Reset {   // a staged run is consumed (or abandoned) by this call
+        cbn_projector_s* p;
+        ~Reset() { p->bp_staged = 0; }
+    } reset{p};
     bp_views(p, frames, 0, p->g.n_views, p->padded.p, s);
     bp_finish(p, p->padded.p, 0, 1, p->big.p, s);
     bp_crop(p, p->big.p, vol, s);
     (void)x;
+}
+
+// forward Grangeat of views [lo, hi) ahead of cbn_backproject (views-in-lanes
+// path with one scaling group: the target-major values of every view feed one
+// column gather); views must arrive in order, lo = the views staged so far
+int bp_stage_views(cbn_projector_s* p, const float* frames, int lo, int hi, cudaStream_t s) {
+    BpCtx x = bp_context(p, s);
+    const BatchPlan& bp = p->bbatch;
+    const bool one_group = !bp.group.empty() && bp.groups() == 1 && bp.batches.front().first == 0 &&
+                           bp.batches.back().second == p->g.n_views;
+    if (!x.lanes || x.method_b || !one_group) return CBN_EUNSUPPORTED;
+    CBN_REQUIRE(lo == p->bp_staged, "staged views must arrive in order");
+    CBN_REQUIRE(lo % 32 == 0 || hi == p->g.n_views, "staged view blocks must start on 32-view bounds");
+    bp_den(p, x, s);   // geometry only; computed before the first view
+    const int64_t per_view = (int64_t)p->bumb.n_mu * p->bumb.n_t;
+    p->values_t.ensure((size_t)per_view * p->g.n_views);
+    bp_grangeat_views(p, frames, hi - lo, nullptr, p->values_t.p, p->g.n_views, lo, s);
+    p->bp_staged = hi;
+    return CBN_OK;
 }
 
 void bp_sizes(cbn_projector_s* p, int64_t* lattice, int64_t* grid, cudaStream_t s) {
@@ -1109,6 +1187,21 @@ extern "C" int cbn_backproject_stage_transpose(cbn_projector* p, const float* fr
                                 static_cast<cudaStream_t>(stream));
         return CBN_OK;
     } catch (const std::exception& e) {
+        return cbn::fail(e);
+    }
+}
+
+extern "C" int cbn_backproject_stage_views(cbn_projector* p, const float* frames, int32_t lo,
+                                           int32_t hi, void* stream) {
+    try {
+        CBN_REQUIRE(p && frames, "null argument");
+        CBN_REQUIRE(p->direction & 2, "projector was not created for the back direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        cbn::build_backward_plan(p, s);
+        return cbn::bp_stage_views(p, frames, lo, hi, s);
+    } catch (const std::exception& e) {
+        p->bp_staged = 0;
         return cbn::fail(e);
     }
 }

@@ -195,6 +195,44 @@ int cbn_projector_first_indices(cbn_projector* p, int32_t set, int32_t batch, in
 
 // Plan statistics as (name, value) pairs; -1 where that part of the plan has
 // not been built yet (most are built by the first operator call).
+// Diagnostics: copy a named plan buffer to the host (bytes = its size; out may
+// be null to query it): den_cache, den_max, bspec_s32, ramp_q, bpairs, bspec_perm,
+// bspec_subs, bbatch_s32, fspec_s32, values_t, lattice.
+int cbn_projector_debug_buffer(cbn_projector* p, const char* name, void* out, int64_t* bytes,
+                               void* stream) {
+    try {
+        CBN_REQUIRE(p && name && bytes, "null argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const std::string n(name);
+        const void* src = nullptr;
+        size_t len = 0;
+        auto pick = [&](const auto& buf) {
+            src = buf.p;
+            len = buf.bytes();
+        };
+        if (n == "den_cache") pick(p->den_cache);
+        else if (n == "den_max") pick(p->den_max);
+        else if (n == "bspec_s32") pick(p->bspec_s32);
+        else if (n == "ramp_q") pick(p->ramp_q);
+        else if (n == "bpairs") pick(p->bpairs);
+        else if (n == "bspec_perm") pick(p->bspec_bins.perm);
+        else if (n == "bspec_subs") pick(p->bspec_bins.subs);
+        else if (n == "bbatch_s32") pick(p->bbatch.s32);
+        else if (n == "fspec_s32") pick(p->fspec_s32);
+        else if (n == "values_t") pick(p->values_t);
+        else if (n == "lattice") pick(p->lattice);
+        else throw Error(CBN_EINVAL, "unknown buffer " + n);
+        *bytes = (int64_t)len;
+        if (out && src && len) {
+            CBN_CUDA(cudaMemcpyAsync(out, src, len, cudaMemcpyDeviceToHost, s));
+            CBN_CUDA(cudaStreamSynchronize(s));
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int cbn_projector_plan_stats(cbn_projector* p, int64_t* vals, int32_t* count, char* names,
                              int32_t names_len, void* stream) {
     try {

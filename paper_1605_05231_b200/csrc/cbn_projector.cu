@@ -17,6 +17,7 @@
 #include "cbn_projector.h"
 #include "cbn_resample_views.cuh"
 #include "cbn_dirichlet.cuh"
+#include "cbn_specgather.cuh"
 
 using namespace cbn;
 
@@ -162,6 +163,56 @@ struct SpecOut {
             out[line * n_rho + (n_rho - a.ir + n_rho - n_rho / 2) % n_rho] = make_float2(val.x, -val.y);
     }
 };
+
+// per-plan records of k_spec_gather (cbn_specgather.cuh), one per sorted
+// primary node: the KB argument y and edge-tap decision per axis exactly as
+// kb_weights forms them from tap_setup, the tap origin in its bin tile, the
+// SpecOut epilogue factor in float64 and the lattice indices
+template <int J>
+__global__ void k_spec_records(RadialSrc src, KBSet kb, TileGeom<3> tg,
+                               const int* __restrict__ perm, int64_t m,
+                               const float* __restrict__ om_phys, int n_vol, int tri,
+                               float4* __restrict__ rec, float2* __restrict__ fac,
+                               int2* __restrict__ out) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= m) return;
+    const int f = perm[pos];
+    double w[3];
+    RadialSrc::Aux a;
+    src.node(f >= 0 ? f : ~f, w, a);
+    unsigned bits = 0;
+    float y[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        int first;
+        const double u = axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, first);
+        const double fr = dsub(u, (double)first);
+        y[d] = (float)(2.0 * (fr - (0.5 * J - 1.0)) - 1.0);
+        const bool drop = fr >= 0.5 * J * (1.0 - 1e-12) && !kb_inside(fr, J);
+        bits |= (unsigned)(wrapc(first, kb.ax[d].K) % tg.T[d]) << (5 * d);
+        if (drop) bits |= 1u << (15 + d);
+    }
+    rec[pos] = make_float4(y[0], y[1], y[2], __uint_as_float(bits));
+    const int N3[3] = {n_vol, n_vol, n_vol};
+    double sn, cs;
+    sincos(centre_plan_angle<3>(a.wc, w, N3), &sn, &cs);
+    double t = 1.0;
+    if (tri) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double x = a.raw[d] * (1.0 / kTwoPi);
+            const double sc = x == 0.0 ? 1.0 : sinpi(x) / (kPi * x);
+            t *= sc * sc;
+        }
+    }
+    // val = i * omega * t * e^{i ang} * v
+    const double g = t * (double)om_phys[a.ir];
+    fac[pos] = make_float2((float)(-sn * g), (float)(cs * g));
+    const int n_rho = src.n_rho;
+    const int line = (f >= 0 ? f : ~f) / n_rho;
+    out[pos] = make_int2(line * n_rho + (a.ir + n_rho - n_rho / 2) % n_rho,
+                         f >= 0 ? line * n_rho + (n_rho - a.ir + n_rho - n_rho / 2) % n_rho : -1);
+}
 
 struct UmbOut {
     float* vals;
@@ -1040,6 +1091,11 @@ int64_t ktot(const AxisPlan* ax) { return (int64_t)ax[0].K * ax[1].K * ax[2].K; 
 // p->lattice) followed by the radial IFFT.  nparts > 1: only the nodes of
 // bin-subproblem share `part` (lat zeroed first); raw_only: stop before the
 // IFFT (the sharded caller sums the shares, then fwd_views runs it)
+bool spec_records_off() {   // CBN_SPEC_RECORDS=0: node generation per step (A/B)
+    const char* e = std::getenv("CBN_SPEC_RECORDS");
+    return e && e[0] == '0';
+}
+
 void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum = nullptr,
                         int part = 0, int nparts = 1, float2* lat = nullptr,
                         bool raw_only = false) {
@@ -1180,9 +1236,29 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
             p->timer.add_bytes("spectrum_gather", f * (8.0 * half_cells + 8.0 * M),
                                f * 8.0 * J * J * J * (double)Mh);
         }
+        // lattice values (not the API spectrum): the record-driven gather
+        const bool recs = !epi.spectrum_only && !spec_records_off();
+        if (recs && !p->fspec_rec.p) {
+            p->fspec_rec.alloc((size_t)Mh);
+            p->fspec_fac.alloc((size_t)Mh);
+            p->fspec_out.alloc((size_t)Mh);
+            dispatch_j(ax[0].J, [&](auto jc) {
+                k_spec_records<decltype(jc)::value><<<blocks_for(Mh, 256), 256, 0, s>>>(
+                    r.src(), kb, bp.geom<3>(), bp.perm.p, Mh, r.om_phys.p, n, epi.tri,
+                    p->fspec_rec.p, p->fspec_fac.p, p->fspec_out.p);
+                return 0;
+            });
+            CBN_LAUNCH_CHECK();
+        }
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
-            if (s1 > s0)
+            if (s1 <= s0) return 0;
+            if (recs)
+                k_spec_gather<J><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
+                    spec_half, kb, bp.geom<3>(),
+                    SpecRec{p->fspec_rec.p, p->fspec_fac.p, p->fspec_out.p}, epi.out,
+                    bp.subs.p + s0);
+            else
                 k_gather_binned<3, J, RadialPackedSrc, SpecOut, true><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
                     spec_half, kb, bp.geom<3>(), RadialPackedSrc{r.src()}, epi, bp.perm.p,
                     bp.subs.p + s0);

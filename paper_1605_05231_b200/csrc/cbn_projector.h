@@ -126,6 +126,9 @@ struct cbn_projector_s {
     int fres_planes_slow = -1;
     cbn::BinPlan fspec_bins;     // radial nodes sorted by spectrum-grid tile
     cbn::DevBuf<int> fpairs;     // primary radial nodes (RadialPairSrc); mirrors by conjugation
+    cbn::DevBuf<float4> fspec_rec;   // per sorted primary node: KB arguments + tile offsets
+    cbn::DevBuf<float2> fspec_fac;   // ... epilogue factor (i omega transfer phase)
+    cbn::DevBuf<int2> fspec_out;     // ... lattice index and its conjugate mirror's
     cbn::DevBuf<int> fspec_list, fres_list;   // compact pad positions per axis (see pad_positions)
     int fspec_nl[3] = {0, 0, 0}, fres_nl[3] = {0, 0, 0};
     // rho planes of the (views-in-lanes) resample grid the umbrella taps read
@@ -163,6 +166,8 @@ struct cbn_projector_s {
     cbn::DevBuf<char> bcol_ent;     // RsColEntry per (target, rho tap, theta tap)
     int64_t bcol_n = 0;             // entries of the column CSR
     cbn::DevBuf<float> values_t;    // umbrella values of a view run, target-major
+    int bp_staged = 0;              // views [0, bp_staged) of the next backprojection already
+                                    // forward-Grangeat'ed into values_t (cbn_backproject_stage_views)
     cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
     cbn::DevBuf<int> bpairs;     // primary radial nodes of the 3D adjoint (conjugate pairs)
     int64_t bpairs_n = 0;

@@ -97,6 +97,26 @@ __global__ void k_rs_col_fill(const RsTap<J>* __restrict__ taps, int64_t n, int 
         }
 }
 
+// the fill's atomic cursors leave each column's entries in arrival order;
+// sorting them by target makes every column sum (and so the transposed
+// resample, den included) independent of the plan build: one thread per
+// column, insertion sort (a few to a few hundred entries per column)
+static __global__ void k_rs_col_sort(const int* __restrict__ col_ptr, int64_t ncol,
+                                     RsColEntry* __restrict__ ent) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncol) return;
+    const int lo = col_ptr[c], hi = col_ptr[c + 1];
+    for (int i = lo + 1; i < hi; ++i) {
+        const RsColEntry e = ent[i];
+        int j = i - 1;
+        while (j >= lo && ent[j].t > e.t) {
+            ent[j + 1] = ent[j];
+            --j;
+        }
+        ent[j + 1] = e;
+    }
+}
+
 // acc[e] += gain * prod_d scale_d[e_d] * IFFT(g)[k], k_d = idx_d[e_d], from
 // F = the forward 3D FFT of the real grid g kept as the half spectrum along
 // axis 0 (phi; [rho][theta][phi/2+1], strides a_d.sstride): IFFT(g)[k] is

@@ -1,3 +1,5 @@
+#include <cstdlib>
+
 #include "cbn_runtime.h"
 
 #include <algorithm>
@@ -29,7 +31,11 @@ cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long st
                            cufftType type) {
     cufftHandle h;
     CBN_CUFFT(cufftCreate(&h));
-    CBN_CUFFT(cufftSetAutoAllocation(h, 0));
+    static const bool auto_ws = [] {
+        const char* e = std::getenv("CBN_FFT_AUTOALLOC");
+        return e && e[0] == '1';
+    }();
+    if (!auto_ws) CBN_CUFFT(cufftSetAutoAllocation(h, 0));
     size_t ws = 0;
     long long* embed = nullptr;
     long long emb[3];
@@ -54,6 +60,7 @@ cufftHandle FFTCache::make(int rank, long long* n, long long batch, long long st
         throw Error(r == CUFFT_ALLOC_FAILED ? CBN_ENOMEM : CBN_ECUDA,
                     "cufftMakePlanMany64 failed: " + std::to_string((int)r));
     }
+    if (auto_ws) return h;
     if (ws > work_.n) {
         work_.alloc(ws);
         for (auto& kv : plans_) CBN_CUFFT(cufftSetWorkArea(kv.second, work_.p));

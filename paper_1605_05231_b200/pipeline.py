@@ -469,6 +469,9 @@ def nufft_forward_project(vol: Volume3D, geom, cfg) -> list[DetectorFrame]:
     return [DetectorFrame._checked(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
 
 
+_BP_STAGE_VIEWS = 64   # views per upload block of the drop-in backprojector
+
+
 def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volume3D:
     """Direct NUFFT backprojection (pipeline.py:150-212): list of frames in,
     float64 ``Volume3D`` out (ValueError on non-finite values, as the
@@ -485,15 +488,25 @@ def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volu
             raise ValueError("frames must be (n_views, nu, nv)")
     dev = torch.empty(shape, dtype=torch.float32, device="cuda")
     V = geom.n_views
-    bounds = [V * i // 4 for i in range(5)]
+    lib = _lib.load()
+    s = proj._s
+    # blocks of 64 views: converted on the pool, copied on the device stream and
+    # (where the plan allows) forward-Grangeat'ed at once, so the device works
+    # on block k while the host converts block k + 1
+    bounds = list(range(0, V, _BP_STAGE_VIEWS)) + [V]
+    staged = True
     for a, b in zip(bounds[:-1], bounds[1:]):
-        # frames of this quarter converted on the pool, then their DMA overlaps
-        # the next quarter's conversion
         futs = [_hostio.pool().submit(np.copyto, host[k], frames[k].data, casting="unsafe")
                 for k in range(a, b)]
         for fu in futs:
             fu.result()
         dev[a:b].copy_(pin[a:b], non_blocking=True)
+        if staged:
+            rc = lib.cbn_backproject_stage_views(proj._h, _device.ptr(dev[a]), a, b, s)
+            if rc == _lib.CBN_EUNSUPPORTED:
+                staged = False
+            else:
+                _lib.check(rc, "nufft_backproject")
     vol = proj.backproject(dev)
     if not bool(torch.isfinite(vol).all()):
         raise ValueError("volume contains non-finite values")

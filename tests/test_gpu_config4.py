@@ -109,3 +109,30 @@ def test_2d_binned_paths(nf):
     y = rng.standard_normal(30000) + 1j * rng.standard_normal(30000)
     assert rel_l2(nf.nufft_forward(plan, x), orc.type2(ref, x)) < 1e-5
     assert rel_l2(nf.nufft_adjoint(plan, y), orc.type1(ref, y)) < 1e-5
+
+
+def test_config4_full_size_10k_direct_dft(nf):
+    """BASELINE config 4 at full size: all 100M float32 points (seed 5) on the
+    256^3 CN(0,1) grid (seed 4), KB J=8, sigma 2.  Type 2 at 10,000 points
+    drawn from the whole set against the separable direct DFT (<= 1e-5, the
+    tolerance BASELINE.json states); type 1 through the dot test over all
+    100M points.  Inputs and outputs stay on the device."""
+    import torch
+    from paper_1605_05231_b200.workloads import config4_inputs
+    x, pts = config4_inputs()
+    assert pts.shape == (100_000_000, 3)
+    plan = nf.plan_nufft(x.shape, pts, 2.0, 8)
+    xd = torch.from_numpy(x).cuda()
+    y = nf.nufft_forward(plan, xd)
+    sel = np.sort(np.random.default_rng(9).choice(pts.shape[0], 10_000, replace=False))
+    got = y[torch.from_numpy(sel).cuda()].cpu().numpy()
+    ref = orc.separable_dft(x.astype(np.complex128), orc.wrap(pts[sel].astype(np.float64)))
+    err = rel_l2(got, ref)
+    assert err < 1e-5, err
+    g = torch.Generator(device="cuda").manual_seed(10)
+    yr = torch.complex(torch.randn(pts.shape[0], generator=g, device="cuda"),
+                       torch.randn(pts.shape[0], generator=g, device="cuda")) / np.sqrt(2)
+    xa = nf.nufft_adjoint(plan, yr)
+    lhs = torch.vdot(yr.to(torch.complex128), y.to(torch.complex128)).item()
+    rhs = torch.vdot(xa.to(torch.complex128).ravel(), xd.to(torch.complex128).ravel()).item()
+    assert abs(lhs - rhs) / abs(lhs) < 1e-5

@@ -282,3 +282,60 @@ def test_radial_lattice_conjugate_pairs_at_wrap_ties(pl):
     got = proj.radial_lattice(torch.from_numpy(vol.data.astype(np.float32)).cuda())
     got = got.cpu().numpy().transpose(2, 1, 0)
     assert rel_l2(got, ref) < 1e-5
+
+
+def test_backproject_staged_upload(pl, monkeypatch):
+    """The drop-in backprojector stages the forward Grangeat step block by block
+    while later frames upload (cbn_backproject_stage_views): 32-view blocks on
+    the 48-view rotation-aligned geometry (one scaling group) give the one-call
+    result and the reference's; a plan with several scaling groups refuses the
+    staging (CBN_EUNSUPPORTED) and the call falls back."""
+    import torch
+    from paper_1605_05231_b200 import _device, _lib
+    from paper_1605_05231_b200.grangeat import DetectorFrame
+    g = dict(np.load(os.path.join(GOLDEN, "pipeline_n12_v48.npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    fr = [DetectorFrame(k, g["frames"][k], geom.pixel_mm) for k in range(views)]
+    monkeypatch.setattr(pl, "_BP_STAGE_VIEWS", 32)
+    staged = pl.nufft_backproject(fr, geom, cfg, n, voxel).data
+    proj = pl.get_projector(geom, cfg, n, voxel, pl._BACK)
+    one = proj.backproject(torch.from_numpy(g["frames"].astype(np.float32)).cuda()).cpu().numpy()
+    assert rel_l2(staged, one) < 1e-6
+    assert rel_l2(staged, g["bp"]) < TOL
+    # out-of-order staging is an argument error and leaves nothing staged
+    dev = torch.from_numpy(g["frames"].astype(np.float32)).cuda()
+    rc = _lib.load().cbn_backproject_stage_views(proj._h, _device.ptr(dev[32]), 32, 48, proj._s)
+    assert rc == _lib.CBN_EINVAL
+    assert rel_l2(proj.backproject(dev).cpu().numpy(), one) < 1e-6
+    # 4096-target batches: several batches, still one scaling group here
+    monkeypatch.setattr(pl, "_TARGET_BATCH", 4096)
+    err = rel_l2(pl.nufft_backproject(fr, geom, cfg, n, voxel).data, g["bp_b4"])
+    assert err < TOL, err
+    # method B has no views-in-lanes column gather: refused, the call falls back
+    gb = dict(np.load(os.path.join(GOLDEN, "pipeline_n12_b.npz")))
+    nb_, vb = int(gb["n"]), int(gb["views"])
+    geom_b, voxel_b, _, cfg_b = small_setup(nb_, vb)
+    cfg_b.method = "b"
+    proj_b = pl.get_projector(geom_b, cfg_b, nb_, voxel_b, pl._BACK)
+    devb = torch.from_numpy(gb["frames"].astype(np.float32)).cuda()
+    rc = _lib.load().cbn_backproject_stage_views(proj_b._h, _device.ptr(devb), 0, vb, proj_b._s)
+    assert rc == _lib.CBN_EUNSUPPORTED
+    frb = [DetectorFrame(k, gb["frames"][k], geom_b.pixel_mm) for k in range(vb)]
+    err = rel_l2(pl.nufft_backproject(frb, geom_b, cfg_b, nb_, voxel_b).data, gb["bp"])
+    assert err < TOL, err
+
+
+def test_spectrum_records_match_node_generation(pl, golden_n16, monkeypatch):
+    """The record-driven spectrum gather (k_spec_gather: per-plan KB arguments,
+    tile offsets, epilogue factors) and the per-step node generation path
+    (CBN_SPEC_RECORDS=0, k_gather_binned) give the same lattice, and both the
+    reference's."""
+    g = golden_n16
+    geom, voxel, spec, cfg = small_setup()
+    proj = pl.Projector(geom, cfg, 16, voxel, 1)
+    rec = proj.radial_lattice(g["vol"]).cpu().numpy()
+    monkeypatch.setenv("CBN_SPEC_RECORDS", "0")
+    gen = proj.radial_lattice(g["vol"]).cpu().numpy()
+    assert rel_l2(rec, gen) < 1e-6
+    assert rel_l2(rec, to_nodes(g["lattice"])) < TOL
