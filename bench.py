@@ -59,6 +59,9 @@ def parse_args():
     ap.add_argument("--only", action="store_true", help="skip the sub-object measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--comm", choices=["capi", "torch"], default="capi",
+                    help="multi-GPU collectives: NCCL behind the C ABI (libcbnufft_b200_comm) "
+                         "or torch.distributed around the projector phases")
     return ap.parse_args()
 
 
@@ -229,9 +232,16 @@ def measure_projector(args, d: Dist, config: int, direction: str):
     lib = _lib.load()
     stream = torch.cuda.current_stream()
     proj = pl.Projector(w.geom, w.cfg, w.n, w.voxel, 1 if fwd else 2)
+    cm = None
+    if d.world > 1 and args.comm == "capi":
+        from paper_1605_05231_b200.comm import NcclComm
+        cm = NcclComm.from_group()
     if fwd:
         x_dev = torch.from_numpy(vol_host).cuda()
-        if d.world > 1:
+        if cm is not None:
+            def step():
+                return cm.forward_project(proj, x_dev, lo, hi)
+        elif d.world > 1:
             def step():
                 return proj.forward_sharded(x_dev, lo, hi)
         else:
@@ -243,7 +253,10 @@ def measure_projector(args, d: Dist, config: int, direction: str):
         del fp
         gc.collect()
         x_loc = x_dev[lo:hi].contiguous()
-        if d.world > 1:
+        if cm is not None:
+            def step():
+                return cm.backproject(proj, x_loc, lo, hi)
+        elif d.world > 1:
             def step():
                 return proj.backproject_sharded(x_loc, lo, hi)
         else:
@@ -304,7 +317,7 @@ def measure_projector(args, d: Dist, config: int, direction: str):
                            "float64" if fwd else
                            "pipeline.nufft_backproject(list[DetectorFrame] float64) -> Volume3D "
                            "float64") + "; host conversions on threads via pinned staging"}
-        e2e_proj = e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d, stream)
+        e2e_proj = e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d, stream, cm)
     cpu = None
     if d.world == 1 and not args.no_cpu_baseline:
         cpu = cpu_forward(w) if fwd else cpu_backward(w)
@@ -323,7 +336,9 @@ def measure_projector(args, d: Dist, config: int, direction: str):
                                f"{V} views of {w.geom.nu}^2, KB J=6 sigma=2, resample J=3",
                    "views": V, "views_per_rank": hi - lo,
                    "parallelism": f"views sharded x{d.world}" + (
-                       "" if d.world == 1 else ", radial nodes sharded, NCCL collectives"),
+                       "" if d.world == 1 else ", radial nodes sharded, NCCL collectives ("
+                       + ("C ABI, libcbnufft_b200_comm" if cm is not None else "torch.distributed")
+                       + ")"),
                    "l2": "inputs in HBM; working set > L2 every step (resample grid "
                          f"{stats.get('fwd_resample_cells', stats.get('bp_resample_cells', 0)) * 4 / 1e9:.1f}"
                          " GB), no flush needed",
@@ -336,7 +351,7 @@ def measure_projector(args, d: Dist, config: int, direction: str):
     }
 
 
-def e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d: Dist, stream):
+def e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d: Dist, stream, cm=None):
     """Projector API with pinned host tensors, copies on a second stream
     overlapping the previous/next step (a serving loop)."""
     import torch
@@ -348,6 +363,9 @@ def e2e_projector(proj, fwd, vol_host, x_dev, w, lo, hi, args, d: Dist, stream):
         host_out = torch.empty((w.n,) * 3, dtype=torch.float32).pin_memory()
 
     def run(dev):
+        if cm is not None:
+            return (cm.forward_project(proj, dev, lo, hi) if fwd
+                    else cm.backproject(proj, dev[lo:hi].contiguous(), lo, hi))
         if fwd:
             return proj.forward_sharded(dev, lo, hi) if d.world > 1 else proj.forward(dev, lo, hi)
         if d.world > 1:

@@ -136,6 +136,14 @@ int cbn_node_phase(void* values, const double* nodes, int64_t m, int32_t d, cons
 int cbn_trilinear_transfer(int32_t n_rho, int32_t n_theta, int32_t n_phi, double delta_rho,
                            double voxel_mm, double* out, void* stream);
 
+/* Host dtype conversion of the drop-in operators (float64 numpy <-> float32
+ * staging), threaded outside the caller's interpreter lock; threads <= 0: all
+ * cores.  gather: dst[k * elems + i] = (float)src[k][i] for n_src arrays. */
+int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t elems, float* dst,
+                               int32_t threads);
+int cbn_host_f64_to_f32(const double* src, float* dst, int64_t n, int32_t threads);
+int cbn_host_f32_to_f64(const float* src, double* dst, int64_t n, int32_t threads);
+
 /* -------------------------------------------------------------- projector
  * Replaces ConeGeometry / ProjectorConfig / nufft_forward_project /
  * nufft_backproject (geometry.py:21-64, pipeline.py:31-212).
@@ -183,6 +191,10 @@ int cbn_projector_destroy(cbn_projector* proj);
 int cbn_projector_ls_sizes(const cbn_projector* proj, int64_t* sizes, int32_t* count);
 int cbn_projector_set_ls_rows(cbn_projector* proj, int64_t m, const int64_t* rows, int64_t n);
 /* bytes of device scratch the plan will hold once built */
+/* volume edge N, view count and detector size of a plan (for hosts that
+ * size buffers from the plan alone, e.g. cbnufft_b200_comm.h) */
+int cbn_projector_info(const cbn_projector* proj, int32_t* n_vol, int32_t* n_views, int32_t* nu,
+                       int32_t* nv);
 int cbn_projector_scratch_bytes(const cbn_projector* proj, int64_t* bytes);
 
 /* nufft_forward_project (pipeline.py:122-147): vol [device] float32 N^3 [ix,iy,iz]

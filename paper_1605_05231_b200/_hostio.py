@@ -5,9 +5,11 @@ The reference API is numpy in / numpy out with float64 results
 (``DetectorFrame``/``Volume3D`` store float64).  The device
 path computes in float32, so every call converts on the host: float64 volume
 -> float32 upload, float32 frames -> float64 results (and the reverse for the
-backprojector).  Those conversions are split over a thread pool (numpy
-releases the GIL inside ``copyto``) and go through pinned staging buffers that
-each projector plan keeps, so the copies run at DMA speed and overlap the
+backprojector).  float64 <-> float32 conversions of contiguous arrays run in
+the library's OpenMP threads (cbn_host_*, csrc/cbn_hostio.cu) outside the
+interpreter lock; anything else is split over a Python thread pool (numpy
+releases the GIL inside ``copyto``).  They go through pinned staging buffers
+that each projector plan keeps, so the copies run at DMA speed and overlap the
 conversion of the previous chunk.
 """
 
@@ -31,8 +33,45 @@ def pool() -> ThreadPoolExecutor:
     return _POOL
 
 
+def _native_convert(dst: np.ndarray, src: np.ndarray) -> bool:
+    """float64 <-> float32 conversion of contiguous arrays in the library's
+    OpenMP threads (cbn_host_*), outside the interpreter lock."""
+    if dst.shape != src.shape or not (dst.flags.c_contiguous and src.flags.c_contiguous):
+        return False
+    from . import _lib
+    lib = _lib.load()
+    if dst.dtype == np.float32 and src.dtype == np.float64:
+        fn = lib.cbn_host_f64_to_f32
+    elif dst.dtype == np.float64 and src.dtype == np.float32:
+        fn = lib.cbn_host_f32_to_f64
+    else:
+        return False
+    _lib.check(fn(src.ctypes.data, dst.ctypes.data, src.size, 0), "host conversion")
+    return True
+
+
+def gather_frames(dst: np.ndarray, arrays) -> None:
+    """dst[k] = arrays[k] (float64 -> float32) for a list of equally shaped
+    frames, in one native threaded call when they are contiguous float64."""
+    import ctypes
+    from . import _lib
+    arrs = [np.asarray(a) for a in arrays]
+    if (dst.dtype == np.float32 and dst.flags.c_contiguous and len(arrs) == dst.shape[0]
+            and all(a.dtype == np.float64 and a.flags.c_contiguous and a.shape == dst.shape[1:]
+                    for a in arrs)):
+        ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        _lib.check(_lib.load().cbn_host_gather_f64_to_f32(ptrs, len(arrs), int(dst[0].size),
+                                                          dst.ctypes.data, 0), "host conversion")
+        return
+    futs = [pool().submit(np.copyto, dst[k], a, casting="unsafe") for k, a in enumerate(arrs)]
+    for f in futs:
+        f.result()
+
+
 def copy(dst: np.ndarray, src: np.ndarray, min_chunk: int = 1 << 18) -> None:
     """dst[...] = src (with dtype conversion), split along axis 0 over threads."""
+    if _native_convert(dst, src):
+        return
     n = dst.shape[0]
     per = max(1, min_chunk // max(1, dst[0].size if dst.ndim > 1 else 1))
     parts = max(1, min(_THREADS, -(-n // per)))
@@ -122,6 +161,8 @@ def download_blocks(stage: Staging, tag: str, dev, blocks, wait, out_dtype=np.fl
                 return
             ev, a, b = item
             ev.synchronize()
+            if _native_convert(out[a:b], host[a:b]):
+                continue
             parts = max(1, min(_THREADS, b - a))
             cuts = [a + (b - a) * i // parts for i in range(parts + 1)]
             for x, y in zip(cuts[:-1], cuts[1:]):

@@ -300,6 +300,102 @@ struct BpPairSrc : BpSrc {
     }
 };
 
+// BpPairSrc from per-plan records (sorted order): KB arguments and bin-local
+// first taps as k_spec_records forms them, the two lattice samples a primary
+// node reads (its own and, for a pair, its mirror's) and their factors
+// -i * q * sin(theta) * sinc^2 transfer * conj(centre * plan phase), so the
+// spread's staging reads 40 bytes and two lattice values per point
+struct BpRecSrc {
+    using is_record_src = void;
+    using Aux = RadialSrc::Aux;
+    const float4* rec;    // y0, y1, y2, bits (l0 | l1 << 5 | l2 << 10 | edge drops << 15)
+    const float4* g;      // factor of X[i1] (x, y), factor of X[i2] (z, w)
+    const int2* idx;      // i1, i2 (-1: no mirror)
+    const float2* X;      // ramp-filtered lattice, node order
+    template <int J>
+    CBN_D void stage(const KBSet& kb, int64_t pos, float2& v, int (&l)[3], float (&wt)[3][J]) const {
+        const float4 q = rec[pos];
+        const unsigned bits = __float_as_uint(q.w);
+        l[0] = bits & 31;
+        l[1] = (bits >> 5) & 31;
+        l[2] = (bits >> 10) & 31;
+        kb_weights_y<J>(kb.ax[0], q.x, (bits >> 15) & 1, wt[0]);
+        kb_weights_y<J>(kb.ax[1], q.y, (bits >> 16) & 1, wt[1]);
+        kb_weights_y<J>(kb.ax[2], q.z, (bits >> 17) & 1, wt[2]);
+        const float4 f = g[pos];
+        const int2 ix = idx[pos];
+        v = cmul(X[ix.x], make_float2(f.x, f.y));
+        if (ix.y >= 0) {
+            const float2 m = cmul(X[ix.y], make_float2(f.z, f.w));
+            v.x += m.x;
+            v.y -= m.y;
+        }
+    }
+};
+
+template <int J>
+__global__ void k_bp_records(BpSrc src, KBSet kb, TileGeom<3> tg, const int* __restrict__ perm,
+                             int64_t m, float4* __restrict__ rec, float4* __restrict__ g,
+                             int2* __restrict__ idx) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= m) return;
+    const int e = perm[pos];
+    const int f = e >= 0 ? e : ~e;
+    double w[3];
+    RadialSrc::Aux a;
+    src.RadialSrc::node(f, w, a);
+    unsigned bits = 0;
+    float y[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        int first;
+        const double u = axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, first);
+        const double fr = dsub(u, (double)first);
+        y[d] = (float)(2.0 * (fr - (0.5 * J - 1.0)) - 1.0);
+        const bool drop = fr >= 0.5 * J * (1.0 - 1e-12) && !kb_inside(fr, J);
+        bits |= (unsigned)(wrapc(first, kb.ax[d].K) % tg.T[d]) << (5 * d);
+        if (drop) bits |= 1u << (15 + d);
+    }
+    rec[pos] = make_float4(y[0], y[1], y[2], __uint_as_float(bits));
+    const int n_rho = src.n_rho;
+    // factor of BpSrc::value at node f: x * (-i qq t) * e^{-i ang}
+    auto factor = [&](const double (&wn)[3], const RadialSrc::Aux& an) {
+        double t = 1.0;
+        if (src.tri) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double x = an.raw[d] * (1.0 / kTwoPi);
+                const double sc = x == 0.0 ? 1.0 : sinpi(x) / (kPi * x);
+                t *= sc * sc;
+            }
+        }
+        const double gq = (double)src.q[an.ir] * (double)src.sin_th[an.it] * t;
+        double sn, cs;
+        sincos(-centre_plan_angle<3>(an.wc, wn, src.N), &sn, &cs);
+        return make_float2((float)(sn * gq), (float)(-cs * gq));
+    };
+    const int line = f / n_rho;
+    const float2 g1 = factor(w, a);
+    const int i1 = line * n_rho + (a.ir - n_rho / 2 + n_rho) % n_rho;
+    float2 g2 = make_float2(0.f, 0.f);
+    int i2 = -1;
+    if (e >= 0) {
+        const int fm = line * n_rho + (n_rho - a.ir);
+        double wm[3];
+        RadialSrc::Aux am;
+        src.RadialSrc::node(fm, wm, am);
+        g2 = factor(wm, am);
+        i2 = line * n_rho + (am.ir - n_rho / 2 + n_rho) % n_rho;
+    }
+    g[pos] = make_float4(g1.x, g1.y, g2.x, g2.y);
+    idx[pos] = make_int2(i1, i2);
+}
+
+bool bp_records_off() {   // CBN_BP_RECORDS=0: node generation per step (A/B)
+    const char* e = std::getenv("CBN_BP_RECORDS");
+    return e && e[0] == '0';
+}
+
 }  // namespace
 
 void projector_prepare_gr_points(cbn_projector_s* p, GrangeatPlan& gp, const UmbrellaTables& u,
@@ -1003,6 +1099,27 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
     const BinPlan& bb = p->bspec_bins;
     const int s0 = (int)((int64_t)bb.nsubs * part / nparts);
     const int s1 = (int)((int64_t)bb.nsubs * (part + 1) / nparts);
+    if (!bp_records_off()) {
+        if (!p->bspec_rec.p) {
+            const int64_t m = p->bpairs_n;
+            p->bspec_rec.alloc((size_t)m);
+            p->bspec_g.alloc((size_t)m);
+            p->bspec_idx.alloc((size_t)m);
+            dispatch_j(sax[0].J, [&](auto jc) {
+                k_bp_records<decltype(jc)::value><<<blocks_for(m, 256), 256, 0, s>>>(
+                    bsrc, kbs, bb.geom<3>(), bb.perm.p, m, p->bspec_rec.p, p->bspec_g.p,
+                    p->bspec_idx.p);
+                return 0;
+            });
+            CBN_LAUNCH_CHECK();
+        }
+        const BpRecSrc rsrc{p->bspec_rec.p, p->bspec_g.p, p->bspec_idx.p, p->lattice.p};
+        dispatch_j(sax[0].J, [&](auto jc) {
+            launch_spread3<decltype(jc)::value>(grid, kbs, bb, rsrc, s, s0, s1);
+            return 0;
+        });
+        return;
+    }
     dispatch_j(sax[0].J, [&](auto jc) {
         launch_spread3<decltype(jc)::value>(grid, kbs, bb, bsrc, s, s0, s1);
         return 0;

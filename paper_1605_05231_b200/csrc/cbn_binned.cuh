@@ -90,6 +90,14 @@ struct has_node_at : std::false_type {};
 template <class Src>
 struct has_node_at<Src, std::void_t<decltype(&Src::node_at)>> : std::true_type {};
 
+// Sources that carry per-plan point records (sorted order) expose
+// stage<J>(kb, pos, v, l, wt): value, bin-local first taps and KB weights of
+// the point at sorted position pos, with no node generation per step.
+template <class Src, class = void>
+struct has_stage : std::false_type {};
+template <class Src>
+struct has_stage<Src, std::void_t<typename Src::is_record_src>> : std::true_type {};
+
 template <class Src, int D>
 CBN_D void src_node(const Src& src, int64_t pos, int64_t i, double (&w)[D], typename Src::Aux& a) {
     if constexpr (has_node_at<Src>::value) src.node_at(pos, i, w, a);
@@ -379,17 +387,27 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
         __syncthreads();   // region zeroed / previous round's points consumed
         const int k = base + threadIdx.x;
         if (k < sp.count) {
-            const int64_t i = perm[sp.start + k];
-            double w[3];
-            typename Src::Aux aux;
-            src_node(src, sp.start + k, i, w, aux);
-            const float2 v = src.value(i, w, aux);
-            int first[3];
+            float2 v;
             float wt[3][J];
-            tap_setup<3, J>(kb, w, first, wt);
-            const int l0 = wrapc(first[0], tg.K[0]) - o[0];
-            const int l1 = wrapc(first[1], tg.K[1]) - o[1];
-            const int l2 = wrapc(first[2], tg.K[2]) - o[2];
+            int l0, l1, l2;
+            if constexpr (has_stage<Src>::value) {
+                int l[3];
+                src.template stage<J>(kb, (int64_t)sp.start + k, v, l, wt);
+                l0 = l[0];
+                l1 = l[1];
+                l2 = l[2];
+            } else {
+                const int64_t i = perm[sp.start + k];
+                double w[3];
+                typename Src::Aux aux;
+                src_node(src, sp.start + k, i, w, aux);
+                v = src.value(i, w, aux);
+                int first[3];
+                tap_setup<3, J>(kb, w, first, wt);
+                l0 = wrapc(first[0], tg.K[0]) - o[0];
+                l1 = wrapc(first[1], tg.K[1]) - o[1];
+                l2 = wrapc(first[2], tg.K[2]) - o[2];
+            }
             CBN_DCHECK(l0 >= 0 && l0 < tg.T[0] && l1 >= 0 && l1 < tg.T[1] && l2 >= 0 &&
                            l2 < tg.T[2],
                        "owned spread: point outside its bin tile");
@@ -826,7 +844,7 @@ void launch_spread3(float2* grid, const KBSet& kb, const BinPlan& bb, const Src&
                     int s0 = 0, int s1 = -1) {
     CBN_REQUIRE(bb.D == 3 && bb.tg.P % 16 == J % 16, "3D spread needs a pitch-padded bin plan");
     if (s1 < 0) s1 = bb.nsubs;
-    if constexpr (J == 8) {
+    if constexpr (J == 8 && !has_stage<Src>::value) {
         if (spread_warps_override() == 8) {   // the one-row-per-warp kernel (A/B)
             const size_t smem = spread_owned8_smem_bytes(bb.nreg);
             CBN_CUDA(cudaFuncSetAttribute(k_spread_owned8<Src>,

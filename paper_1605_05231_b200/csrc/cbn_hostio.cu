@@ -1,0 +1,68 @@
+// Host-side dtype conversion for the drop-in operators (plumbing, no numerics):
+// the reference API is float64 numpy in and out, the device computes in
+// float32, so every call converts on the host between the caller's arrays and
+// the plan's pinned staging buffers.  Done here with OpenMP threads (outside the
+// Python interpreter lock) at memory bandwidth: per-frame numpy calls from a
+// Python thread pool spent most of their time in task dispatch.
+#include <omp.h>
+
+#include <cstdint>
+
+#include "cbn_runtime.h"
+
+namespace {
+
+int team(int32_t threads) { return threads > 0 ? threads : omp_get_max_threads(); }
+
+}  // namespace
+
+extern "C" {
+
+// dst[k * elems + i] = (float)src[k][i] for the n_src arrays src[0..n_src)
+int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t elems, float* dst,
+                               int32_t threads) {
+    try {
+        CBN_REQUIRE(src && dst && n_src >= 0 && elems >= 0, "bad argument");
+        for (int64_t k = 0; k < n_src; ++k) CBN_REQUIRE(src[k], "null source array");
+        // blocks of 64 Ki elements across all arrays, so a few large frames
+        // and many small ones both spread over the team
+        constexpr int64_t B = 1 << 16;
+        const int64_t per = (elems + B - 1) / B;
+        const int64_t tasks = n_src * per;
+#pragma omp parallel for schedule(static) num_threads(team(threads))
+        for (int64_t t = 0; t < tasks; ++t) {
+            const int64_t k = t / per, b = t - k * per;
+            const int64_t lo = b * B, hi = lo + B < elems ? lo + B : elems;
+            const double* s = src[k];
+            float* d = dst + k * elems;
+            for (int64_t i = lo; i < hi; ++i) d[i] = (float)s[i];
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return cbn::fail(e);
+    }
+}
+
+// dst[i] = (double)src[i]  (float32 result -> float64 numpy)
+int cbn_host_f32_to_f64(const float* src, double* dst, int64_t n, int32_t threads) {
+    try {
+        CBN_REQUIRE(src && dst && n >= 0, "bad argument");
+        constexpr int64_t B = 1 << 16;
+        const int64_t tasks = (n + B - 1) / B;
+#pragma omp parallel for schedule(static) num_threads(team(threads))
+        for (int64_t t = 0; t < tasks; ++t) {
+            const int64_t lo = t * B, hi = lo + B < n ? lo + B : n;
+            for (int64_t i = lo; i < hi; ++i) dst[i] = (double)src[i];
+        }
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return cbn::fail(e);
+    }
+}
+
+// dst[i] = (float)src[i]  (float64 numpy -> float32 staging)
+int cbn_host_f64_to_f32(const double* src, float* dst, int64_t n, int32_t threads) {
+    return cbn_host_gather_f64_to_f32(&src, 1, n, dst, threads);
+}
+
+}  // extern "C"

@@ -37,6 +37,20 @@ CBN_D void tap_setup(const KBSet& kb, const double (&w)[D], int (&first)[D], flo
     }
 }
 
+// kb_weights from a precomputed polynomial argument y and edge-tap decision
+// (point records of the projector's radial node sets)
+template <int J>
+CBN_D void kb_weights_y(const KBAxis& kb, float y, bool drop0, float (&w)[J]) {
+#pragma unroll
+    for (int p = 0; p < J; ++p) w[p] = kb.pp[p][kPPDeg];
+#pragma unroll
+    for (int k = kPPDeg - 1; k >= 0; --k)
+#pragma unroll
+        for (int p = 0; p < J; ++p) w[p] = fmaf(w[p], y, kb.pp[p][k]);
+    if (drop0) w[0] = 0.0f;
+}
+
+
 CBN_D int wrapc(int c, int K) {
     c = c < 0 ? c + K : c;
     return c >= K ? c - K : c;

@@ -2317,6 +2317,20 @@ int cbn_projector_set_ls_rows(cbn_projector* p, int64_t m, const int64_t* rows, 
     }
 }
 
+int cbn_projector_info(const cbn_projector* p, int32_t* n_vol, int32_t* n_views, int32_t* nu,
+                       int32_t* nv) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        if (n_vol) *n_vol = p->n_vol;
+        if (n_views) *n_views = p->g.n_views;
+        if (nu) *nu = p->g.nu;
+        if (nv) *nv = p->g.nv;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 int cbn_projector_scratch_bytes(const cbn_projector* p, int64_t* bytes) {
     try {
         CBN_REQUIRE(p && bytes, "null argument");

@@ -170,6 +170,9 @@ struct cbn_projector_s {
                                     // forward-Grangeat'ed into values_t (cbn_backproject_stage_views)
     cbn::BinPlan bspec_bins;     // backprojector radial nodes sorted by grid tile
     cbn::DevBuf<int> bpairs;     // primary radial nodes of the 3D adjoint (conjugate pairs)
+    cbn::DevBuf<float4> bspec_rec;   // per sorted primary node: KB arguments + tile offsets
+    cbn::DevBuf<float4> bspec_g;     // ... factors of its lattice sample and its mirror's
+    cbn::DevBuf<int2> bspec_idx;     // ... those two lattice indices
     int64_t bpairs_n = 0;
     bool bspec_fit = false;
     cbn::DevBuf<float> bspec_s32;   // cached first-sub-plan scaling of the 3D adjoint

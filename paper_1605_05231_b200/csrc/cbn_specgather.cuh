@@ -29,17 +29,6 @@ struct SpecRec {
 };
 
 template <int J>
-CBN_D void kb_weights_y(const KBAxis& kb, float y, bool drop0, float (&w)[J]) {
-#pragma unroll
-    for (int p = 0; p < J; ++p) w[p] = kb.pp[p][kPPDeg];
-#pragma unroll
-    for (int k = kPPDeg - 1; k >= 0; --k)
-#pragma unroll
-        for (int p = 0; p < J; ++p) w[p] = fmaf(w[p], y, kb.pp[p][k]);
-    if (drop0) w[0] = 0.0f;
-}
-
-template <int J>
 __global__ void __launch_bounds__(256, 3)
 k_spec_gather(const float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, SpecRec r,
               float2* __restrict__ lat, const SubProblem* __restrict__ subs) {

@@ -496,10 +496,7 @@ def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volu
     bounds = list(range(0, V, _BP_STAGE_VIEWS)) + [V]
     staged = True
     for a, b in zip(bounds[:-1], bounds[1:]):
-        futs = [_hostio.pool().submit(np.copyto, host[k], frames[k].data, casting="unsafe")
-                for k in range(a, b)]
-        for fu in futs:
-            fu.result()
+        _hostio.gather_frames(host[a:b], [frames[k].data for k in range(a, b)])
         dev[a:b].copy_(pin[a:b], non_blocking=True)
         if staged:
             rc = lib.cbn_backproject_stage_views(proj._h, _device.ptr(dev[a]), a, b, s)

@@ -86,3 +86,21 @@ def test_operators_fail_loudly_without_gpu():
     from paper_1605_05231_b200 import nufft
     with pytest.raises(RuntimeError):
         nufft.plan_nufft((8,), np.zeros((4, 1)), 2.0, 6)
+
+
+def test_comm_library_exports_header_symbols():
+    """libcbnufft_b200_comm.so (NCCL collectives behind the C ABI) loads without
+    a GPU and exports every symbol include/cbnufft_b200_comm.h declares; the
+    NCCL unique id is host-only."""
+    from paper_1605_05231_b200 import comm
+    text = open(os.path.join(REPO, "include", "cbnufft_b200_comm.h")).read()
+    syms = sorted(set(re.findall(r"\b(cbn_[a-z0-9_]+)\s*\(", text)))
+    lib = comm.load()
+    assert not [s for s in syms if not hasattr(lib, s)]
+    assert set(syms) == set(comm.EXPORTED), set(syms) ^ set(comm.EXPORTED)
+    assert not lib.cbn_missing_symbols
+    uid = comm.unique_id()
+    assert len(uid) == comm.ID_BYTES and uid != comm.unique_id()
+    h = ctypes.c_void_p()
+    assert lib.cbn_comm_init(ctypes.byref(h), None, 1, 0) == 1   # CBN_EINVAL
+    assert lib.cbn_comm_init(ctypes.byref(h), ctypes.create_string_buffer(uid, 128), 2, 2) == 1

@@ -339,3 +339,20 @@ def test_spectrum_records_match_node_generation(pl, golden_n16, monkeypatch):
     gen = proj.radial_lattice(g["vol"]).cpu().numpy()
     assert rel_l2(rec, gen) < 1e-6
     assert rel_l2(rec, to_nodes(g["lattice"])) < TOL
+
+
+def test_backprojector_records_match_node_generation(pl, golden_n16, monkeypatch):
+    """The record-driven 3D spread (BpRecSrc: per-plan KB arguments, tile
+    offsets, lattice indices and factors of each primary node and its mirror)
+    and the per-step node generation path (CBN_BP_RECORDS=0) agree, and both
+    match the reference's backprojection."""
+    import torch
+    g = golden_n16
+    geom, voxel, spec, cfg = small_setup()
+    frames = torch.from_numpy(g["frames"].astype(np.float32)).cuda()
+    proj = pl.Projector(geom, cfg, 16, voxel, 2)
+    rec = proj.backproject(frames).cpu().numpy()
+    monkeypatch.setenv("CBN_BP_RECORDS", "0")
+    gen = proj.backproject(frames).cpu().numpy()
+    assert rel_l2(rec, gen) < 1e-5
+    assert rel_l2(rec, g["bp"]) < TOL
