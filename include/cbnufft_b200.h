@@ -338,7 +338,8 @@ int cbn_projector_first_indices(cbn_projector* proj, int32_t set, int32_t batch,
  * resample rho planes used, invalid umbrella targets per view, batch scaling
  * groups, reverse-Grangeat heavy cells, ...  Synchronises. */
 /* Diagnostics: copy the named plan buffer (den_cache, den_max, bspec_s32,
- * ramp_q, bpairs, bspec_perm, bspec_subs, bbatch_s32, fspec_s32, values_t, lattice) to
+ * ramp_q, bpairs, bspec_perm, bspec_subs, bbatch_s32, fspec_s32, values_t, lattice,
+ * den_keep) to
  * host memory `out` (null: only report its size in *bytes) */
 int cbn_projector_debug_buffer(cbn_projector* proj, const char* name, void* out, int64_t* bytes,
                                void* stream);

@@ -179,10 +179,18 @@ __global__ void k_den_final(const float2* __restrict__ acc_den, int64_t lines, i
     den[e] = (j == n / 2) ? (float)means[0] : (float)((double)acc_den[line * dr + pad + j].x * inv);
 }
 
-// den over each phi orbit {c, c + s, ...} (node order [phi][theta][rho]):
-// the float64 mean written back to every member
-__global__ void k_den_orbit_mean(float* __restrict__ den, int n_rho, int n_theta, int n_phi,
-                                 int sft) {
+// keep = den > tol * max(den) (pipeline.py:187-188) decided per phi orbit
+// {c, c + s, ...} from the orbit's float64 mean, for rotation-aligned views:
+// each view's targets are view 0's rotated by s whole lattice phi cells, so
+// the transposed resample is phi-shift equivariant and the reference's den is
+// uniform over an orbit (to ~1e-8 of the threshold away from the poles, whose
+// targets take per-view phi).  The float32 den of one orbit scatters by ~1e-5
+// of the threshold, enough to split an orbit that sits that close to it, which
+// the reference never does; the mean decides for the whole orbit, while every
+// entry is still divided by its own den.  Node order [phi][theta][rho].
+__global__ void k_den_keep_orbit(const float* __restrict__ den, int n_rho, int n_theta, int n_phi,
+                                 int sft, const double* __restrict__ dmax, double tol,
+                                 unsigned char* __restrict__ keep) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t plane = (int64_t)n_rho * n_theta;
     if (e >= plane * sft) return;
@@ -191,11 +199,11 @@ __global__ void k_den_orbit_mean(float* __restrict__ den, int n_rho, int n_theta
     double sum = 0.0;
     int cnt = 0;
     for (int f = c; f < n_phi; f += sft, ++cnt) sum += (double)den[(int64_t)f * plane + rt];
-    const float m = (float)(sum / cnt);
-    for (int f = c; f < n_phi; f += sft) den[(int64_t)f * plane + rt] = m;
+    const unsigned char k = sum / cnt > tol * dmax[0] ? 1 : 0;
+    for (int f = c; f < n_phi; f += sft) keep[(int64_t)f * plane + rt] = k;
 }
 
-bool den_orbit_off() {   // CBN_DEN_ORBIT=0: per-entry den (A/B)
+bool den_orbit_off() {   // CBN_DEN_ORBIT=0: per-entry keep decision (A/B)
     const char* e = std::getenv("CBN_DEN_ORBIT");
     return e && e[0] == '0';
 }
@@ -228,7 +236,8 @@ __global__ void k_max_final(const double* __restrict__ partial, int n, double* _
 __global__ void k_bp_div(const float2* __restrict__ acc_num, const float* __restrict__ den,
                          int64_t lines, int dr, int pad, int n, double inv,
                          const double* __restrict__ means, const double* __restrict__ dmax,
-                         double tol, float2* __restrict__ out) {
+                         double tol, const unsigned char* __restrict__ keep,
+                         float2* __restrict__ out) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= lines * n) return;
     const int j = (int)(e % n);
@@ -244,7 +253,7 @@ __global__ void k_bp_div(const float2* __restrict__ acc_num, const float* __rest
     }
     const double d = den[e];
     float2 v = make_float2(0.f, 0.f);
-    if (d > tol * dmax[0]) v = make_float2((float)(nr / d), (float)(ni / d));
+    if (keep ? keep[e] != 0 : d > tol * dmax[0]) v = make_float2((float)(nr / d), (float)(ni / d));
     out[line * n + (j - n / 2 + n) % n] = v;
 }
 
@@ -933,27 +942,20 @@ void bp_den(cbn_projector_s* p, const BpCtx& x, cudaStream_t s) {
     k_den_final<<<blocks_for(M, 256), 256, 0, s>>>(acc_den, r.lines(), x.dr, p->bpad, r.n_rho, inv,
                                                     means + 2, p->den_cache.p);
     CBN_LAUNCH_CHECK();
-    // Rotation-aligned views (each view's targets are view 0's rotated by a
-    // whole number s of lattice phi cells, one resample scaling group): the
-    // transposed resample is phi-shift equivariant, so den is exactly
-    // invariant under phi -> phi + s.  The reference's den (float64) is then
-    // uniform over each phi orbit up to 1e-15, and its keep decision
-    // den > den_tol * max(den) (pipeline.py:187-188) takes or drops a whole
-    // orbit.  The float32 evaluations of one orbit scatter by ~1e-5 of the
-    // threshold, enough to split an orbit that sits that close to it; the
-    // orbit mean (in float64) restores the all-or-nothing decision and
-    // averages the rounding of its V / (n_phi / s) evaluations.
-    if (x.lanes && p->bbatch.groups() == 1 && r.n_phi % p->g.n_views == 0 && !den_orbit_off()) {
-        const int sft = r.n_phi / p->g.n_views;
-        const int64_t orbits = (int64_t)r.n_rho * r.n_theta * sft;
-        k_den_orbit_mean<<<blocks_for(orbits, 256), 256, 0, s>>>(p->den_cache.p, r.n_rho,
-                                                                 r.n_theta, r.n_phi, sft);
-        CBN_LAUNCH_CHECK();
-    }
     k_max_partial<<<kRed, 256, 0, s>>>(p->den_cache.p, M, p->red.p);
     CBN_LAUNCH_CHECK();
     k_max_final<<<1, 32, 0, s>>>(p->red.p, kRed, p->den_max.p);
     CBN_LAUNCH_CHECK();
+    p->den_keep.release();
+    if (x.lanes && p->bbatch.groups() == 1 && r.n_phi % p->g.n_views == 0 && !den_orbit_off()) {
+        const int sft = r.n_phi / p->g.n_views;
+        const int64_t orbits = (int64_t)r.n_rho * r.n_theta * sft;
+        p->den_keep.alloc((size_t)M);
+        k_den_keep_orbit<<<blocks_for(orbits, 256), 256, 0, s>>>(p->den_cache.p, r.n_rho, r.n_theta,
+                                                                 r.n_phi, sft, p->den_max.p,
+                                                                 p->c.den_tol, p->den_keep.p);
+        CBN_LAUNCH_CHECK();
+    }
     p->den_cached = true;
 }
 
@@ -1026,7 +1028,7 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
     p->lattice.ensure((size_t)M);
     k_bp_div<<<blocks_for(M, 256), 256, 0, s>>>(acc, p->den_cache.p, r.lines(), x.dr, p->bpad,
                                                  r.n_rho, inv, means, p->den_max.p, c.den_tol,
-                                                 p->lattice.p);
+                                                 p->den_keep.p, p->lattice.p);
     CBN_LAUNCH_CHECK();
     long long nr1[1] = {r.n_rho};
     p->fft.exec(p->fft.get(1, nr1, r.lines()), p->lattice.p, p->lattice.p, CUFFT_FORWARD, s);

@@ -197,7 +197,7 @@ int cbn_projector_first_indices(cbn_projector* p, int32_t set, int32_t batch, in
 // not been built yet (most are built by the first operator call).
 // Diagnostics: copy a named plan buffer to the host (bytes = its size; out may
 // be null to query it): den_cache, den_max, bspec_s32, ramp_q, bpairs, bspec_perm,
-// bspec_subs, bbatch_s32, fspec_s32, values_t, lattice.
+// bspec_subs, bbatch_s32, fspec_s32, values_t, lattice, den_keep.
 int cbn_projector_debug_buffer(cbn_projector* p, const char* name, void* out, int64_t* bytes,
                                void* stream) {
     try {
@@ -221,6 +221,7 @@ int cbn_projector_debug_buffer(cbn_projector* p, const char* name, void* out, in
         else if (n == "fspec_s32") pick(p->fspec_s32);
         else if (n == "values_t") pick(p->values_t);
         else if (n == "lattice") pick(p->lattice);
+        else if (n == "den_keep") pick(p->den_keep);
         else throw Error(CBN_EINVAL, "unknown buffer " + n);
         *bytes = (int64_t)len;
         if (out && src && len) {

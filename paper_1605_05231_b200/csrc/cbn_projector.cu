@@ -1940,16 +1940,24 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
             gr_cell_schedule(gp, h, Ku, Kv, s);
             CBN_CUDA(cudaStreamSynchronize(s));
         }
-        StageScope st(p->timer, "grangeat_spread", s);
         const int64_t nspec = (int64_t)u.n_mu * nh;
         B.tv.ensure(std::max((size_t)gp.n_rows * 32, ((size_t)nb * Ku * Kv + 1) / 2));
-        if (zsplit)
-            k_views_nodes_z<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
-                B.t.p, nb, u.n_mu, u.n_t / 2, gp.node_tab.p, gp.n_rows, B.tv.p);
-        else
-            k_views_nodes<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
-                B.t.p, nb, nspec, gp.node_tab.p, gp.n_rows, B.tv.p);
-        CBN_LAUNCH_CHECK();
+        {
+            // t-spectra of the block read once, view-fastest node rows written once
+            StageScope st(p->timer, "grangeat_rows", s);
+            p->timer.add_bytes("grangeat_rows",
+                               8.0 * nb * (double)u.n_mu * (zsplit ? u.n_t / 2 : nh) +
+                                   8.0 * nb * gp.n_rows,
+                               0.0);
+            if (zsplit)
+                k_views_nodes_z<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
+                    B.t.p, nb, u.n_mu, u.n_t / 2, gp.node_tab.p, gp.n_rows, B.tv.p);
+            else
+                k_views_nodes<<<(unsigned)((gp.n_rows + 31) / 32), 256, 0, s>>>(
+                    B.t.p, nb, nspec, gp.node_tab.p, gp.n_rows, B.tv.p);
+            CBN_LAUNCH_CHECK();
+        }
+        StageScope st(p->timer, "grangeat_spread", s);
         // Hermitian half plane [Ku][Kv/2+1] of the grid (only Re of its
         // inverse FFT is used), then a complex-to-real 2D FFT into tv
         const int64_t nhalf = (int64_t)Ku * (Kv / 2 + 1);

@@ -179,6 +179,7 @@ struct cbn_projector_s {
     bool den_cached = false;
     cbn::DevBuf<float> den_cache;   // final den lattice (incl. origin average), node order
     cbn::DevBuf<double> den_max;
+    cbn::DevBuf<unsigned char> den_keep;   // per-orbit keep decision (rotation-aligned views), or empty
     cbn::DevBuf<float> ramp_q;      // backprojector ramp per rho bin
 
     // ---- scratch (shared by both directions, sized on demand)

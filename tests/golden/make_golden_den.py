@@ -3,11 +3,13 @@
 and its margin to the keep threshold den > den_tol * max(den).
 
     python tests/golden/make_golden_den.py      # ~30 min on 8 cores
+    python tests/golden/make_golden_den.py --from-cache   # re-summarise /tmp/config2_den_ref.npy
 
 Writes tests/golden/config2_den.npz with, for every (rho, theta) ring of the
 lattice (the den of a rotation-aligned view set is phi-invariant up to
 rounding), the ring's min and max over phi of den / (den_tol * max(den)) for
-the rings within 1e-2 of the threshold, the threshold itself and den's max.
+the rings within 1e-2 of the threshold, the threshold itself, den's max and
+the phi = 0 plane of den (float32, (n_rho, n_theta)).
 """
 
 from __future__ import annotations
@@ -45,6 +47,9 @@ def main():
     cfg = replace(cfg, n_t=2 * geom.nu, t_pitch_mm=None, radial_spec=bp_spec,
                   rho_pad=min(bp_spec.n_rho // 8, 32))
     spec = cfg.radial_spec
+    cache = "/tmp/config2_den_ref.npy"
+    if "--from-cache" in sys.argv and os.path.exists(cache):
+        return summarise(np.load(cache), cfg.den_tol)
     den = np.zeros((spec.n_rho, spec.n_theta, spec.n_phi))
     t0 = time.time()
     batches = list(rpipe._view_batches(geom, cfg))
@@ -56,8 +61,12 @@ def main():
         del rplan
         if i % 10 == 0:
             print(f"batch {i}/{len(batches)} {time.time() - t0:.0f}s", flush=True)
-    thr = cfg.den_tol * den.max()
-    np.save("/tmp/config2_den_ref.npy", den)
+    np.save(cache, den)
+    summarise(den, cfg.den_tol)
+
+
+def summarise(den, den_tol):
+    thr = den_tol * den.max()
     r = den / thr
     lo, hi = r.min(axis=2), r.max(axis=2)
     near = np.argwhere((np.abs(lo - 1.0) < 1e-2) | (np.abs(hi - 1.0) < 1e-2))
@@ -65,7 +74,8 @@ def main():
                         ring_min=lo[near[:, 0], near[:, 1]], ring_max=hi[near[:, 0], near[:, 1]],
                         thr=np.float64(thr), dmax=np.float64(den.max()),
                         kept=np.int64((den > thr).sum()),
-                        phi_spread=np.float64(np.max((hi - lo) * thr / den.max())))
+                        phi_spread=np.float64(np.max((hi - lo) * thr / den.max())),
+                        plane0=den[:, :, 0].astype(np.float32))
     print("rings near threshold", len(near), "kept", int((den > thr).sum()), "thr", thr,
           "max phi spread / max", np.max((hi - lo) * thr / den.max()))
 

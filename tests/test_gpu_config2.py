@@ -119,3 +119,52 @@ def test_config2_backproject_all_views(c2):
                 z=rel_l2(vol[:, :, 128], z["z"]), blocks=rel_l2(blocks, z["blocks"]),
                 norm=abs(np.linalg.norm(vol) / float(z["norm"]) - 1.0))
     assert max(errs.values()) < TOL, errs
+
+
+def test_config2_den_and_keep_decisions(c2):
+    """The backprojector's den (pipeline.py:171-188: transposed resample of the
+    validity masks) against the reference's own float64 den at config 2
+    (tests/golden/make_golden_den.py).  keep = den > den_tol * max(den) is a
+    hard threshold: 14 (rho, theta) rings of 360 entries lie within 1e-3 of it,
+    the closest at 4.5e-5, while the float32 den of one ring scatters by ~1e-5.
+    The keep decision is taken per phi orbit from the orbit mean (the den of
+    rotation-aligned views is phi-invariant), so every ring is kept or dropped
+    whole, as the reference does; the den itself is deterministic (sorted
+    column entries), so this holds for every plan built."""
+    import ctypes
+    from paper_1605_05231_b200 import _lib
+    from paper_1605_05231_b200 import pipeline as pl
+    geom, voxel, spec, cfg = c2
+    z = dict(np.load(os.path.join(GOLDEN, "config2_den.npz")))
+    proj = pl.Projector(geom, cfg, 256, voxel, 2)
+    import torch
+    proj.backproject(torch.zeros((geom.n_views, geom.nu, geom.nv), dtype=torch.float32,
+                                 device="cuda"))
+    lib = _lib.load()
+
+    def buf(name, dt):
+        n = ctypes.c_int64()
+        _lib.check(lib.cbn_projector_debug_buffer(proj._h, name.encode(), None, ctypes.byref(n),
+                                                  proj._s))
+        out = np.empty(n.value, np.uint8)
+        _lib.check(lib.cbn_projector_debug_buffer(proj._h, name.encode(), out.ctypes.data,
+                                                  ctypes.byref(n), proj._s))
+        return out.view(dt)
+
+    ref0 = z["plane0"].astype(np.float64)                    # (n_rho, n_theta) at phi = 0
+    n_rho, n_theta = ref0.shape
+    den = buf("den_cache", np.float32).reshape(-1, n_theta, n_rho).astype(np.float64)
+    dmax = float(buf("den_max", np.float64)[0])
+    assert abs(dmax / float(z["dmax"]) - 1.0) < 1e-6
+    ours0 = den[0].T
+    kept = ref0 > float(z["thr"])
+    err = np.abs(ours0 - ref0)[kept] / ref0[kept]
+    assert np.median(err) < 1e-6 and err.max() < 1e-3, (np.median(err), err.max())
+    # the keep decision (k_den_keep_orbit: per phi orbit, rotation-aligned views)
+    keep = buf("den_keep", np.uint8).reshape(-1, n_theta, n_rho)
+    assert keep.size == den.size
+    assert int(keep.sum()) == int(z["kept"])
+    for (a, b), lo, hi in zip(z["rings"], z["ring_min"], z["ring_max"]):
+        if (lo > 1.0) != (hi > 1.0):
+            continue                                          # the reference splits this ring
+        assert np.all(keep[:, b, a] == (1 if lo > 1.0 else 0)), ((a, b), lo)
