@@ -225,6 +225,16 @@ int cbn_forward_finish(cbn_projector* proj, void* stream);
  * views:   consumes the summed lattice; views [lo, hi) into frames [device]
  *          float32 (hi - lo) x nu x nv; CBN_ENONFINITE as cbn_forward_project */
 int cbn_forward_lattice_size(cbn_projector* proj, int64_t* lattice_elems, void* stream);
+/* Node-sharded forward plan: the spectrum plan (conjugate pairs, bins,
+ * records) of a forward-only projector covers only the radial lines of share
+ * `part` of `nparts` (contiguous in node order), and cbn_forward_lattice(part,
+ * nparts) then writes only the lattice entries [*node_lo, *node_hi) -- equal
+ * blocks in rank order, so the shares are assembled with an in-place
+ * all-gather (SURVEY.md 8(e) forward step 4) instead of an all-reduce of the
+ * whole zero-padded lattice.  CBN_EUNSUPPORTED when nparts does not divide the
+ * line count; a sharded plan refuses every other forward entry point. */
+int cbn_projector_set_node_shard(cbn_projector* proj, int32_t part, int32_t nparts,
+                                 int64_t* node_lo, int64_t* node_hi, void* stream);
 int cbn_forward_lattice(cbn_projector* proj, const float* vol, int32_t part, int32_t nparts,
                         void* lattice, void* stream);
 int cbn_forward_views(cbn_projector* proj, void* lattice, float* frames, int32_t lo, int32_t hi,

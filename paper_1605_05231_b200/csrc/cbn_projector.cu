@@ -90,12 +90,12 @@ void UmbrellaTables::build(const cbn_geometry& g, int nmu, int nt, double pitch,
 // rho position of its line (image_to_radial_spectrum + trilinear_transfer +
 // spectral_rho_derivative + the input shift of _centered_ifft).
 __global__ void k_radial_pairs(RadialSrc r, KBSet kb, int J, int64_t lines, int* __restrict__ idx,
-                               int* __restrict__ extra, int64_t base_count) {
+                               int* __restrict__ extra, int64_t base_count, int64_t line0) {
     const int n = r.n_rho, nh = n / 2 + 1;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= lines * nh) return;
     const int k = (int)(e % nh);
-    const int64_t line = e / nh;
+    const int64_t line = line0 + e / nh;
     const int64_t f = line * n + k;
     if (k == 0 || k == n / 2) {
         idx[e] = ~(int)f;
@@ -1180,7 +1180,16 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     }
     const float2* spec_half = p->big.p + half_off;
     if (!lat) lat = p->lattice.p;
-    if (nparts > 1) CBN_CUDA(cudaMemsetAsync(lat, 0, sizeof(float2) * M, s));
+    // a node-sharded plan (cbn_projector_set_node_shard) holds only its own
+    // lines and writes only their lattice entries (gathered across ranks);
+    // otherwise a share of the bin subproblems over all lines, summed across ranks
+    const bool compact = p->fshard_nparts > 1;
+    CBN_REQUIRE(!compact || (spectrum == nullptr && raw_only && part == p->fshard_part &&
+                             nparts == p->fshard_nparts),
+                "node-sharded plan: only its own cbn_forward_lattice share can run");
+    const int64_t line_lo = compact ? r.lines() * part / nparts : 0;
+    const int64_t line_hi = compact ? r.lines() * (part + 1) / nparts : r.lines();
+    if (nparts > 1 && !compact) CBN_CUDA(cudaMemsetAsync(lat, 0, sizeof(float2) * M, s));
     SpecOut epi;
     epi.out = spectrum ? spectrum : lat;
     epi.om_phys = r.om_phys.p;
@@ -1191,14 +1200,16 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     // half the nodes: rho indices 0..n_rho/2 of every line, mirrors by conjugation
     if (!p->fpairs_n) {
         // plan step: the primary nodes (about half: conjugate pairs along each line)
-        const int64_t base_n = r.lines() * (r.n_rho / 2 + 1);
-        p->fpairs.alloc((size_t)base_n + (size_t)r.lines() * (r.n_rho / 2));
+        const int64_t nl = line_hi - line_lo;
+        const int64_t base_n = nl * (r.n_rho / 2 + 1);
+        p->fpairs.alloc((size_t)base_n + (size_t)nl * (r.n_rho / 2));
         DevBuf<int> extra(1);
         CBN_CUDA(cudaMemsetAsync(extra.p, 0, sizeof(int), s));
         KBSet kbp;
         for (int d = 0; d < 3; ++d) kbp.ax[d] = ax[d].kb;
-        k_radial_pairs<<<blocks_for(base_n, 256), 256, 0, s>>>(r.src(), kbp, ax[0].J, r.lines(),
-                                                               p->fpairs.p, extra.p, base_n);
+        k_radial_pairs<<<blocks_for(base_n, 256), 256, 0, s>>>(r.src(), kbp, ax[0].J, nl,
+                                                               p->fpairs.p, extra.p, base_n,
+                                                               line_lo);
         CBN_LAUNCH_CHECK();
         int h_extra = 0;
         CBN_CUDA(cudaMemcpyAsync(&h_extra, extra.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1225,8 +1236,8 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     {
         StageScope st(p->timer, "spectrum_gather", s);
         const BinPlan& bp = p->fspec_bins;
-        const int s0 = (int)((int64_t)bp.nsubs * part / nparts);
-        const int s1 = (int)((int64_t)bp.nsubs * (part + 1) / nparts);
+        const int s0 = compact ? 0 : (int)((int64_t)bp.nsubs * part / nparts);
+        const int s1 = compact ? bp.nsubs : (int)((int64_t)bp.nsubs * (part + 1) / nparts);
         CBN_REQUIRE(bp.tg.R[2] <= 32, "half-spectrum gather: region rows above 32 cells");
         {
             // half spectrum read once, every lattice node written (mirrors by
@@ -1237,7 +1248,8 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
                                f * 8.0 * J * J * J * (double)Mh);
         }
         // lattice values (not the API spectrum): the record-driven gather
-        const bool recs = !epi.spectrum_only && !spec_records_off();
+        const bool recs = !epi.spectrum_only && !spec_records_off() &&
+                          bp.tg.R[0] * bp.tg.R[1] <= kSpecMaxRows;
         if (recs && !p->fspec_rec.p) {
             p->fspec_rec.alloc((size_t)Mh);
             p->fspec_fac.alloc((size_t)Mh);
@@ -1253,12 +1265,15 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         dispatch_j(ax[0].J, [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             if (s1 <= s0) return 0;
-            if (recs)
+            if (recs) {
+                CBN_CUDA(cudaFuncSetAttribute(k_spec_gather<J>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)(sizeof(float2) * bp.nreg)));
                 k_spec_gather<J><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
                     spec_half, kb, bp.geom<3>(),
                     SpecRec{p->fspec_rec.p, p->fspec_fac.p, p->fspec_out.p}, epi.out,
                     bp.subs.p + s0);
-            else
+            } else
                 k_gather_binned<3, J, RadialPackedSrc, SpecOut, true><<<s1 - s0, 256, sizeof(float2) * bp.nreg, s>>>(
                     spec_half, kb, bp.geom<3>(), RadialPackedSrc{r.src()}, epi, bp.perm.p,
                     bp.subs.p + s0);
@@ -2436,6 +2451,39 @@ int cbn_forward_lattice_size(cbn_projector* p, int64_t* lattice_elems, void* str
         CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
         build_forward(p, static_cast<cudaStream_t>(stream));
         *lattice_elems = p->frad.nodes();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_projector_set_node_shard(cbn_projector* p, int32_t part, int32_t nparts, int64_t* node_lo,
+                                 int64_t* node_hi, void* stream) {
+    try {
+        CBN_REQUIRE(p, "null argument");
+        CBN_REQUIRE(p->direction == 1, "node shards need a forward-only projector");
+        CBN_REQUIRE(nparts >= 1 && 0 <= part && part < nparts, "bad part");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        const int64_t lines = p->frad.lines(), n_rho = p->frad.n_rho;
+        if (nparts > 1 && lines % nparts != 0)
+            throw Error(CBN_EUNSUPPORTED, "radial lines do not split evenly over the parts");
+        if (p->fshard_part != part || p->fshard_nparts != nparts) {
+            // the spectrum plan (pairs, bins, records) is rebuilt for the new share
+            CBN_CUDA(cudaStreamSynchronize(s));
+            p->fpairs_n = 0;
+            p->fspec_bins.ready = false;
+            p->fspec_bins.perm.release();
+            p->fspec_bins.subs.release();
+            p->fspec_bins.nsubs = 0;
+            p->fspec_rec.release();
+            p->fspec_fac.release();
+            p->fspec_out.release();
+            p->fshard_part = nparts > 1 ? part : 0;
+            p->fshard_nparts = nparts;
+        }
+        if (node_lo) *node_lo = lines * part / nparts * n_rho;
+        if (node_hi) *node_hi = lines * (part + 1) / nparts * n_rho;
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

@@ -148,6 +148,8 @@ struct cbn_projector_s {
     int bres_nth = 0, bres_nph = 0;
     cbn::DevBuf<float2> brlines;
     int64_t fpairs_n = 0;
+    int fshard_part = 0, fshard_nparts = 1;   // forward node shard (cbn_projector_set_node_shard):
+                                              // the spectrum plan covers lines of this share only
     bool fspec_fit = false;
     cbn::DevBuf<float> fspec_s32;   // cached first-sub-plan scaling of the spectrum NUFFT
 

@@ -82,7 +82,8 @@ struct RadialPackedSrc {
 // lower-half node whose mirror is not exactly its negation is entered
 // without mirroring and its mirror is appended (counter `extra`)
 __global__ void k_radial_pairs(RadialSrc r, KBSet kb, int J, int64_t lines, int* __restrict__ idx,
-                               int* __restrict__ extra, int64_t base_count);
+                               int* __restrict__ extra, int64_t base_count,
+                               int64_t line0 = 0);
 // perm[k] = idx[perm[k]] (in place): a bin order over RadialPairSrc -> packed entries
 __global__ void k_gather_index(const int* __restrict__ idx, int64_t n, int* __restrict__ perm);
 

@@ -28,11 +28,15 @@ struct SpecRec {
     const int2* out;     // lattice index, conjugate-mirror index (-1: none)
 };
 
+constexpr int kSpecMaxRows = 512;   // region rows R0 x R1 (13 x 21 at J = 6)
+
 template <int J>
 __global__ void __launch_bounds__(256, 3)
 k_spec_gather(const float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, SpecRec r,
               float2* __restrict__ lat, const SubProblem* __restrict__ subs) {
     extern __shared__ float2 tile[];
+    // grid offsets of the region rows, direct and conjugate-mirrored
+    __shared__ long long rowoff[2][kSpecMaxRows];
     const SubProblem sp = subs[blockIdx.x];
     if (sp.count == 0) return;
     int o[3];
@@ -41,24 +45,26 @@ k_spec_gather(const float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, SpecRec
     const int rows = tg.R[0] * R1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int K0 = tg.K[0], K1 = tg.K[1], K2 = tg.K[2], h2 = K2 / 2 + 1;
+    for (int row = threadIdx.x; row < rows; row += blockDim.x) {
+        const int r0 = row / R1, r1 = row - r0 * R1;
+        const int i0 = wrapc(o[0] + r0, K0), i1 = wrapc(o[1] + r1, K1);
+        rowoff[0][row] = ((long long)i0 * K1 + i1) * h2;
+        rowoff[1][row] = ((long long)(i0 ? K0 - i0 : 0) * K1 + (i1 ? K1 - i1 : 0)) * h2;
+    }
     // this lane's column of every region row
     const bool col = lane < R2;
     int i2 = wrapc(o[2] + lane, K2);
     const bool mir = col && i2 >= h2;   // read as conj(G[-k])
     if (mir) i2 = K2 - i2;
+    __syncthreads();
     if (col) {
-        for (int row = warp; row < rows; row += 8) {
-            const int r0 = row / R1, r1 = row - r0 * R1;
-            int i0 = wrapc(o[0] + r0, K0), i1 = wrapc(o[1] + r1, K1);
-            if (mir) {
-                i0 = i0 ? K0 - i0 : 0;
-                i1 = i1 ? K1 - i1 : 0;
-            }
-            const float2* src = grid + ((size_t)i0 * K1 + i1) * h2 + i2;
-            CBN_DCHECK(((size_t)i0 * K1 + i1) * h2 + i2 < (size_t)K0 * K1 * h2, "spec fill: cell");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
-                             (unsigned)__cvta_generic_to_shared(tile + row * P2 + lane)),
-                         "l"(src));
+        const long long* ro = rowoff[mir ? 1 : 0];
+        const float2* src = grid + i2;
+        unsigned dst = (unsigned)__cvta_generic_to_shared(tile + warp * P2 + lane);
+        const unsigned dstep = 8u * (unsigned)P2 * sizeof(float2);
+        for (int row = warp; row < rows; row += 8, dst += dstep) {
+            CBN_DCHECK(ro[row] + i2 < (long long)K0 * K1 * h2, "spec fill: cell");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src + ro[row]));
         }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");

@@ -161,13 +161,23 @@ int cbn_forward_project_sharded(cbn_projector* p, cbn_comm* c, float* vol, float
         const size_t nvox = (size_t)n * n * n;
         // 1. the volume from rank 0 (SURVEY.md 8(e) forward step 1)
         if (c->nranks > 1) COMM_NCCL(ncclBroadcast(vol, vol, nvox, ncclFloat, 0, c->nccl, s));
-        // 2-4. this rank's share of the radial nodes, lattice summed over ranks
+        // 2-4. this rank's share of the radial nodes: with a forward-only plan
+        //      whose lines split evenly, a node-sharded plan writes just its
+        //      lattice block and an in-place all-gather assembles the lattice;
+        //      otherwise a share of the bin subproblems, summed by all-reduce
         int64_t m = 0;
         COMM_PHASE(cbn_forward_lattice_size(p, &m, stream));
-        void* lat = c->lattice.get(sizeof(float) * 2 * (size_t)m);
+        auto* lat = static_cast<float*>(c->lattice.get(sizeof(float) * 2 * (size_t)m));
+        int64_t nlo = 0, nhi = 0;
+        const int st = c->nranks > 1
+                           ? cbn_projector_set_node_shard(p, c->rank, c->nranks, &nlo, &nhi, stream)
+                           : CBN_EUNSUPPORTED;
         COMM_PHASE(cbn_forward_lattice(p, vol, c->rank, c->nranks, lat, stream));
-        if (c->nranks > 1)
+        if (st == CBN_OK) {
+            COMM_NCCL(ncclAllGather(lat + 2 * nlo, lat, 2 * (size_t)(nhi - nlo), ncclFloat, c->nccl, s));
+        } else if (c->nranks > 1) {
             COMM_NCCL(ncclAllReduce(lat, lat, 2 * (size_t)m, ncclFloat, ncclSum, c->nccl, s));
+        }
         // 5. this rank's views
         if (hi > lo) COMM_PHASE(cbn_forward_views(p, lat, frames, lo, hi, stream));
         return CBN_OK;

@@ -184,6 +184,17 @@ class Projector:
                    "nufft_forward_project")
         return out
 
+    def set_node_shard(self, part: int, nparts: int):
+        """Restrict this forward-only plan's spectrum plan to the radial lines of
+        share `part` of `nparts`; returns its lattice block (node_lo, node_hi)
+        (cbn_projector_set_node_shard).  NotImplementedError when the lines do
+        not split evenly."""
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.load().cbn_projector_set_node_shard(self._h, int(part), int(nparts),
+                                                            ctypes.byref(lo), ctypes.byref(hi),
+                                                            self._s), "set_node_shard")
+        return int(lo.value), int(hi.value)
+
     def forward_views(self, lattice, view_lo: int = 0, view_hi: int | None = None):
         """Phase 2: from the summed lattice (consumed), views [view_lo, view_hi)."""
         t = _device.require_cuda()

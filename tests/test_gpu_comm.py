@@ -47,3 +47,35 @@ def test_single_rank_sharded_operators(comm):
     assert rel_l2(bp, g["bp"]) < TOL
     with pytest.raises(ValueError):
         comm.forward_project(proj, vol, 0, views + 1)
+
+
+def test_node_sharded_lattice_blocks_assemble_the_lattice():
+    """Node-sharded forward plans (cbn_projector_set_node_shard): each share
+    writes only its contiguous lattice block; the blocks in rank order (what
+    the in-place NCCL all-gather of cbn_forward_project_sharded assembles) are
+    the unsharded lattice, and a sharded plan refuses the other entry points."""
+    import torch
+    from paper_1605_05231_b200 import pipeline as pl
+    g = dict(np.load(os.path.join(GOLDEN, "pipeline_n12_v24.npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    vol = torch.from_numpy(g["vol"].astype(np.float32)).cuda().contiguous()
+    full = pl.Projector(geom, cfg, n, voxel, 1).forward_lattice(vol).cpu().numpy()
+    lines = spec.n_theta * spec.n_phi
+    for nparts in (2, 3, 4):
+        if lines % nparts:
+            continue
+        blocks = []
+        for part in range(nparts):
+            proj = pl.Projector(geom, cfg, n, voxel, 1)
+            lo, hi = proj.set_node_shard(part, nparts)
+            assert hi - lo == full.size // nparts and lo == part * (hi - lo)
+            lat = proj.forward_lattice(vol, part, nparts).cpu().numpy()
+            blocks.append(lat[lo:hi])
+            with pytest.raises(ValueError):
+                proj.forward(vol)
+        got = np.concatenate(blocks)
+        assert np.max(np.abs(got - full)) <= 1e-6 * np.max(np.abs(full))
+    proj = pl.Projector(geom, cfg, n, voxel, 1)
+    with pytest.raises(NotImplementedError):
+        proj.set_node_shard(0, lines + 1)
