@@ -38,6 +38,10 @@ def _native_convert(dst: np.ndarray, src: np.ndarray) -> bool:
     OpenMP threads (cbn_host_*), outside the interpreter lock."""
     if dst.shape != src.shape or not (dst.flags.c_contiguous and src.flags.c_contiguous):
         return False
+    if dst.dtype == np.complex64 and src.dtype == np.complex128:
+        dst, src = dst.view(np.float32), src.view(np.float64)
+    elif dst.dtype == np.complex128 and src.dtype == np.complex64:
+        dst, src = dst.view(np.float64), src.view(np.float32)
     from . import _lib
     lib = _lib.load()
     if dst.dtype == np.float32 and src.dtype == np.float64:
@@ -92,12 +96,16 @@ class Staging:
     which saves the first-touch page faults of a fresh 100+ MB array; while
     the caller holds it, a new one is allocated."""
 
-    def __init__(self):
+    def __init__(self, single_shape: bool = False):
         self._bufs = {}
         self._results = {}
+        self.single_shape = single_shape
 
     def result(self, tag: str, shape, dtype):
         key = (tag, tuple(shape), np.dtype(dtype).str)
+        if self.single_shape:
+            for k in [k for k in self._results if k[0] == tag and k != key]:
+                del self._results[k]
         arr = self._results.get(key)
         # references: this dict, `arr`, getrefcount's argument
         if arr is not None and sys.getrefcount(arr) <= 3:
@@ -115,6 +123,10 @@ class Staging:
     def get(self, tag: str, shape, dtype):
         import torch
         key = (tag, tuple(shape), dtype)
+        if self.single_shape:
+            # one pinned buffer per tag: a new shape releases the old one
+            for k in [k for k in self._bufs if k[0] == tag and k != key]:
+                del self._bufs[k]
         b = self._bufs.get(key)
         if b is None:
             b = torch.empty(tuple(shape), dtype=dtype, pin_memory=True)

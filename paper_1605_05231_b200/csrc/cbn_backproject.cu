@@ -1095,7 +1095,10 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
         // on chip: J^3 shared-memory read + write per primary node
         const double f = (double)1.0 / nparts;
         const double J = sax[0].J;
-        p->timer.add_bytes("bp_spread", f * 8.0 * M + 8.0 * x.k3, f * 16.0 * J * J * J * p->bpairs_n);
+        // + the 40-byte point records of the record-driven spread
+        const double rec = bp_records_off() ? 0.0 : 40.0 * p->bpairs_n;
+        p->timer.add_bytes("bp_spread", f * (8.0 * M + rec) + 8.0 * x.k3,
+                           f * 16.0 * J * J * J * p->bpairs_n);
     }
     // this part's share of the bin subproblems (each node belongs to one)
     const BinPlan& bb = p->bspec_bins;

@@ -1244,7 +1244,9 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
             // conjugation), J^3 shared-memory tap reads per primary node
             const double f = bp.nsubs ? (double)(s1 - s0) / bp.nsubs : 0.0;
             const double J = ax[0].J;
-            p->timer.add_bytes("spectrum_gather", f * (8.0 * half_cells + 8.0 * M),
+            // + the 32-byte point records of the record-driven gather
+            const double rec = (!epi.spectrum_only && !spec_records_off()) ? 32.0 * Mh : 0.0;
+            p->timer.add_bytes("spectrum_gather", f * (8.0 * half_cells + 8.0 * M + rec),
                                f * 8.0 * J * J * J * (double)Mh);
         }
         // lattice values (not the API spectrum): the record-driven gather

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _device, _lib
+from . import _device, _hostio, _lib
 
 _CHUNK = 1 << 19        # kept for API parity (the device path has no row chunks)
 _PLAN_CHUNK = 1 << 21   # nodes per sub-plan in the *_chunked variants (nufft.py:24)
@@ -195,8 +195,29 @@ def plan_nufft(dims, nodes, oversample_factor: float = 2.0, j=6) -> NufftPlan:
     return NufftPlan(dims, k_dims, tuple(int(t) for t in taps), betas, m, h.value)
 
 
+# pinned staging of the host-array calls (complex128 numpy in and out, like
+# the reference): native threaded conversions, chunked DMA (_hostio)
+_STAGE = _hostio.Staging(single_shape=True)
+
+
+def _input(x, dtype):
+    """The device copy of an operator input: torch tensors as they are, numpy
+    through the pinned staging."""
+    t = _device.require_cuda()
+    if isinstance(x, t.Tensor):
+        return _device.to_device(x, dtype)
+    arr = np.ascontiguousarray(np.asarray(x))
+    if arr.ndim == 0 or arr.size == 0:
+        return _device.to_device(arr, dtype)
+    return _hostio.upload(_STAGE, "in", arr, dtype)
+
+
 def _as_result(out, host: bool):
-    return out.cpu().numpy().astype(np.complex128) if host else out
+    if not host:
+        return out
+    if out.numel() == 0 or out.dim() == 0:
+        return out.cpu().numpy().astype(np.complex128)
+    return _hostio.download(_STAGE, "out", out, np.complex128)
 
 
 def nufft_forward(plan: NufftPlan, x):
@@ -206,7 +227,7 @@ def nufft_forward(plan: NufftPlan, x):
     shape = tuple(x.shape)
     if shape != plan.dims:
         raise ValueError(f"input shape {shape} does not match plan dims {plan.dims}")
-    xd = _device.to_device(x, t.complex64)
+    xd = _input(x, t.complex64)
     y = t.empty(plan.n_nodes, dtype=t.complex64, device="cuda")
     _lib.check(_lib.load().cbn_nufft_type2(plan.handle, _device.ptr(xd), _device.ptr(y),
                                            ctypes.c_void_p(_device.stream_ptr())), "nufft_forward")
@@ -219,7 +240,7 @@ def nufft_adjoint(plan: NufftPlan, y):
     host = not isinstance(y, t.Tensor)
     if tuple(y.shape) != (plan.n_nodes,):
         raise ValueError(f"expected {plan.n_nodes} node values, got {tuple(y.shape)}")
-    yd = _device.to_device(y, t.complex64)
+    yd = _input(y, t.complex64)
     x = t.empty(plan.dims, dtype=t.complex64, device="cuda")
     _lib.check(_lib.load().cbn_nufft_type1(plan.handle, _device.ptr(yd), _device.ptr(x),
                                            ctypes.c_void_p(_device.stream_ptr())), "nufft_adjoint")
