@@ -72,7 +72,7 @@ __global__ void k_bin_keys(Src src, KBSet kb, TileGeom<D> tg, int64_t m, int* __
 #pragma unroll
     for (int d = 0; d < D; ++d) {
         int f;
-        axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, f);
+        axis_coord(w[d], kb.ax[d].K, 0.5 * (double)kb.ax[d].J, f);
         key = key * tg.nb[d] + wrapc(f, kb.ax[d].K) / tg.T[d];
     }
     keys[i] = key;
@@ -676,7 +676,7 @@ k_bin_interleave(Src src, KBSet kb, TileGeom<D> tg, int* __restrict__ perm,
 #pragma unroll
             for (int d = 0; d < D; ++d) {
                 int f;
-                axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, f);
+                axis_coord(w[d], kb.ax[d].K, 0.5 * (double)kb.ax[d].J, f);
                 l[d] = wrapc(f, kb.ax[d].K) - o[d];
             }
             const int off = D == 3 ? (l[0] * tg.R[1] + l[1]) * tg.P + l[2] : l[0] * tg.P + l[1];

@@ -141,17 +141,22 @@ CBN_D bool kb_inside(double x, int J) {
 // compile-time offsets into the kernel-parameter bank).  Only tap 0 can reach
 // the support edge (x = J/2 when u - J/2 is an integer); there the reference's
 // exact float64 support test decides (nufft.py:39-41).
+// J (the template) is the plan's largest per-axis tap count: an axis with
+// fewer taps (kb.J < J, nufft.py:137 takes per-axis j) has zero polynomials
+// for taps kb.J..J-1 (fit_kb_pieces), so those weights vanish; the
+// polynomial argument and the support test use the axis's own tap count.
 template <int J>
 CBN_D void kb_weights(const KBAxis& kb, double u, int first, float (&w)[J]) {
     const double fr = dsub(u, (double)first);
-    const float y = (float)(2.0 * (fr - (0.5 * J - 1.0)) - 1.0);
+    const int Ja = kb.J;
+    const float y = (float)(2.0 * (fr - (0.5 * Ja - 1.0)) - 1.0);
 #pragma unroll
     for (int p = 0; p < J; ++p) w[p] = kb.pp[p][kPPDeg];
 #pragma unroll
     for (int k = kPPDeg - 1; k >= 0; --k)
 #pragma unroll
         for (int p = 0; p < J; ++p) w[p] = fmaf(w[p], y, kb.pp[p][k]);
-    if (fr >= 0.5 * J * (1.0 - 1e-12) && !kb_inside(fr, J)) w[0] = 0.0f;
+    if (fr >= 0.5 * Ja * (1.0 - 1e-12) && !kb_inside(fr, Ja)) w[0] = 0.0f;
 }
 
 // float64 I0 by its (all-positive) power series; |z| <= ~25 here.

@@ -32,7 +32,7 @@ template <int D, int J>
 CBN_D void tap_setup(const KBSet& kb, const double (&w)[D], int (&first)[D], float (&wt)[D][J]) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-        double u = axis_coord(w[d], kb.ax[d].K, 0.5 * (double)J, first[d]);
+        double u = axis_coord(w[d], kb.ax[d].K, 0.5 * (double)kb.ax[d].J, first[d]);
         kb_weights<J>(kb.ax[d], u, first[d], wt[d]);
     }
 }

@@ -314,13 +314,13 @@ int create_plan(cbn_nufft** out, int ndim, const int64_t* dims, const int32_t* t
     for (int d = 0; d < ndim; ++d) {
         CBN_REQUIRE(dims[d] >= 1, "dims must be >= 1");
         CBN_REQUIRE(taps[d] >= 1, "tap counts must be >= 1");
-        CBN_REQUIRE(taps[d] == taps[0], "per-axis tap counts must be equal on the device path");
     }
     for (int64_t r = 0; r < n_ls; ++r) CBN_REQUIRE(ls_rows[r] >= 0 && ls_rows[r] < m, "bad scaling-fit row");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     auto p = std::make_unique<cbn_nufft_s>();
     p->D = ndim;
-    p->J = taps[0];
+    p->J = taps[0];   // the largest per-axis tap count sizes the kernels' tap loops
+    for (int d = 1; d < ndim; ++d) p->J = std::max(p->J, (int)taps[d]);
     p->m = m;
     for (int d = 0; d < ndim; ++d) {
         p->ax[d] = make_axis((int)dims[d], taps[d], oversample_factor);
