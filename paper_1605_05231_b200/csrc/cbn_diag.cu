@@ -282,6 +282,21 @@ int cbn_projector_plan_stats(cbn_projector* p, int64_t* vals, int32_t* count, ch
             st.emplace_back("fwd_batch_groups", p->fbatch.ready ? p->fbatch.groups() : -1);
             st.emplace_back("fwd_gr_cell_items", p->fgr.cell_order.p ? p->fgr.n_items : -1);
             st.emplace_back("fwd_gr_heavy_cells", heavy(p->fgr));
+            {
+                const GrangeatPlan& gp = p->fgr;
+                int64_t hs = -1;
+                if (gp.strip_order.p) {
+                    std::vector<int> h((size_t)gp.n_strip_items);
+                    CBN_CUDA(cudaMemcpy(h.data(), gp.strip_order.p, sizeof(int) * h.size(),
+                                        cudaMemcpyDeviceToHost));
+                    hs = 0;
+                    for (int v : h) hs += v < 0;
+                }
+                st.emplace_back("fwd_gr_strip_items", gp.strip_order.p ? gp.n_strip_items : -1);
+                st.emplace_back("fwd_gr_heavy_strips", hs);
+                st.emplace_back("fwd_gr_strip_entries", gp.strip_order.p ? gp.n_strip_entries : -1);
+                st.emplace_back("fwd_gr_cell_entries", gp.cell_ptr.p ? gp.n_entries : -1);
+            }
         }
         if (p->direction & 2) {
             build_backward_plan(p, s);

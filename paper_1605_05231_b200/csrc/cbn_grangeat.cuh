@@ -426,6 +426,115 @@ k_gr_gather_cells(float2* __restrict__ grids, size_t grid_stride, int64_t ncell,
     }
 }
 
+// ----------------------------------------------------------------------
+// Strip form of the reverse-Grangeat cell gather.  A node's 5 x 5 taps reach
+// 5 consecutive cells along v in each of 5 rows, so the cell CSR lists every
+// node row ~25 times and the gather reads each 256-byte row (32 views) once
+// per cell: the kernel is bound by L1 wavefronts.  Grouping the half plane
+// into strips of kGrStrip cells along v and merging a strip's cell lists by
+// node (plan time, host) reads each row once per strip and applies it to the
+// strip's cells with per-cell weights: half-plane cell i of the strip is
+//   (G[k_i] + conj G[-k_i]) / 2 = sum_nodes (p_i Re y, q_i Im y)
+// with p_i = (w_i + m_i) / 2 and q_i = (w_i - m_i) / 2, where w_i / m_i are
+// the node's weights in the direct / mirrored cell lists (real weights).
+constexpr int kGrStrip = 4;
+
+CBN_D void gr_strip_sum(int e0, int e1, const int* __restrict__ sid, const float4* __restrict__ sp,
+                        const float4* __restrict__ sq, const float2* __restrict__ tl, int lane,
+                        int* s_id, float4* s_p, float4* s_q, float2 (&acc)[kGrStrip]) {
+    for (int base = e0; base < e1; base += 32) {
+        const int n = min(32, e1 - base);
+        __syncwarp();
+        if (lane < n) {
+            s_id[lane] = sid[base + lane];
+            s_p[lane] = sp[base + lane];
+            s_q[lane] = sq[base + lane];
+        } else {
+            s_id[lane] = 0;
+            s_p[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+            s_q[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        for (int j0 = 0; j0 < n; j0 += kGrRows) {
+            float2 y[kGrRows];
+#pragma unroll
+            for (int j = 0; j < kGrRows; ++j) y[j] = __ldg(tl + (size_t)s_id[j0 + j] * 32);
+#pragma unroll
+            for (int j = 0; j < kGrRows; ++j) {
+                const float4 p = s_p[j0 + j], q = s_q[j0 + j];
+                acc[0].x = fmaf(p.x, y[j].x, acc[0].x);
+                acc[0].y = fmaf(q.x, y[j].y, acc[0].y);
+                acc[1].x = fmaf(p.y, y[j].x, acc[1].x);
+                acc[1].y = fmaf(q.y, y[j].y, acc[1].y);
+                acc[2].x = fmaf(p.z, y[j].x, acc[2].x);
+                acc[2].y = fmaf(q.z, y[j].y, acc[2].y);
+                acc[3].x = fmaf(p.w, y[j].x, acc[3].x);
+                acc[3].y = fmaf(q.w, y[j].y, acc[3].y);
+            }
+        }
+    }
+}
+
+// Work items (plan-time order, costliest first):
+//   item >= 0: row u = item / ngrp, strips 8 g .. 8 g + 7 (g = item % ngrp),
+//              one per warp, = half-plane cells 32 g .. 32 g + 31 of the row,
+//              stored view-major through a shared-memory transpose (heavy
+//              strips skipped);
+//   item <  0: one heavy strip -(item + 1), its entries split over 8 warps.
+static __global__ void __launch_bounds__(256)
+k_gr_gather_strips(float2* __restrict__ grids, size_t grid_stride, int hv, int nsx, int ngrp,
+                   const int* __restrict__ sptr, const int* __restrict__ sid,
+                   const float4* __restrict__ sp, const float4* __restrict__ sq,
+                   const float2* __restrict__ tfv, int nviews, const int* __restrict__ order,
+                   const unsigned char* __restrict__ heavy) {
+    __shared__ float2 tile[32][33];
+    __shared__ int s_id[8][32];
+    __shared__ float4 s_p[8][32], s_q[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float2* tl = tfv + lane;
+    const int item = order[blockIdx.x];
+    float2 acc[kGrStrip];
+#pragma unroll
+    for (int i = 0; i < kGrStrip; ++i) acc[i] = make_float2(0.f, 0.f);
+    if (item < 0) {
+        const int64_t st = -(int64_t)item - 1;
+        const int a0 = sptr[st], a1 = sptr[st + 1], la = a1 - a0;
+        gr_strip_sum(a0 + (int)((int64_t)la * warp / 8), a0 + (int)((int64_t)la * (warp + 1) / 8),
+                     sid, sp, sq, tl, lane, s_id[warp], s_p[warp], s_q[warp], acc);
+#pragma unroll
+        for (int i = 0; i < kGrStrip; ++i) tile[warp * kGrStrip + i][lane] = acc[i];
+        __syncthreads();
+        if (warp < kGrStrip) {
+            float2 t = make_float2(0.f, 0.f);
+            for (int w = 0; w < 8; ++w) {
+                t.x += tile[w * kGrStrip + warp][lane].x;
+                t.y += tile[w * kGrStrip + warp][lane].y;
+            }
+            const int u = (int)(st / nsx), v = (int)(st % nsx) * kGrStrip + warp;
+            if (v < hv && lane < nviews) grids[(size_t)lane * grid_stride + (size_t)u * hv + v] = t;
+        }
+        return;
+    }
+    const int u = item / ngrp, g = item % ngrp;
+    const int sx = g * 8 + warp;
+    if (sx < nsx) {
+        const int64_t st = (int64_t)u * nsx + sx;
+        if (!heavy[st])
+            gr_strip_sum(sptr[st], sptr[st + 1], sid, sp, sq, tl, lane, s_id[warp], s_p[warp],
+                         s_q[warp], acc);
+    }
+#pragma unroll
+    for (int i = 0; i < kGrStrip; ++i) tile[warp * kGrStrip + i][lane] = acc[i];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int v = e >> 5, cl = e & 31;
+        const int cv = g * 32 + cl;                       // cell along v in the row
+        const int csx = cv / kGrStrip;
+        if (v < nviews && cv < hv && !heavy[(int64_t)u * nsx + csx])
+            grids[(size_t)v * grid_stride + (size_t)u * hv + cv] = tile[cl][v];
+    }
+}
+
 // node-scaled t-spectra: out[id][v] = fac_id * (conj?) in[v][src_id] for
 // ids [0, n), views v < nb (views >= nb unwritten; the readers mask them)
 __global__ void k_views_nodes(const float2* __restrict__ in, int nb, int64_t nspec,

@@ -1879,6 +1879,135 @@ void gr_cell_schedule(GrangeatPlan& gp, const std::vector<int>& h, int Ku, int K
     CBN_CUDA(cudaStreamSynchronize(s));
 }
 
+// Strip form of the cell CSR (k_gr_gather_strips), built once per plan on the
+// host from the device cell CSR: per half-plane strip the entries of its
+// kGrStrip direct cells and of their mirrors, merged by node row (sorted, so
+// the strip sums are deterministic), and the work schedule.
+static int64_t gr_heavy_strip() {   // strips above this many entries get a CTA of their own
+    const char* e = std::getenv("CBN_GR_HEAVY_STRIP");
+    return e ? std::atoll(e) : 640;
+}
+
+void gr_build_strips(GrangeatPlan& gp, int Ku, int Kv, cudaStream_t s) {
+    const int hv = Kv / 2 + 1;
+    const int nsx = (hv + kGrStrip - 1) / kGrStrip;
+    const int ngrp = (nsx + 7) / 8;
+    const int64_t ncell = (int64_t)Ku * Kv, nstrips = (int64_t)Ku * nsx;
+    std::vector<int> ptr((size_t)ncell + 1);
+    std::vector<GrEntry> ent((size_t)gp.n_entries);
+    CBN_CUDA(cudaMemcpyAsync(ptr.data(), gp.cell_ptr.p, sizeof(int) * ptr.size(),
+                             cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaMemcpyAsync(ent.data(), gp.cell_ent.p, sizeof(GrEntry) * ent.size(),
+                             cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    struct Rec {
+        int id;
+        float p[kGrStrip], q[kGrStrip];
+    };
+    std::vector<std::vector<Rec>> rows((size_t)Ku);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int u = 0; u < Ku; ++u) {
+        std::vector<std::pair<int, int>> items;   // (node, slot: cell i, mirror flag)
+        std::vector<float> wts;
+        std::vector<Rec>& out = rows[(size_t)u];
+        for (int sx = 0; sx < nsx; ++sx) {
+            items.clear();
+            wts.clear();
+            for (int i = 0; i < kGrStrip; ++i) {
+                const int v = sx * kGrStrip + i;
+                if (v >= hv) break;
+                const int64_t k = (int64_t)u * Kv + v;
+                const int64_t km = (int64_t)(u ? Ku - u : 0) * Kv + (v ? Kv - v : 0);
+                for (int e = ptr[(size_t)k]; e < ptr[(size_t)k + 1]; ++e) {
+                    items.emplace_back(ent[(size_t)e].id, 2 * i);
+                    wts.push_back(ent[(size_t)e].w);
+                }
+                for (int e = ptr[(size_t)km]; e < ptr[(size_t)km + 1]; ++e) {
+                    items.emplace_back(ent[(size_t)e].id, 2 * i + 1);
+                    wts.push_back(ent[(size_t)e].w);
+                }
+            }
+            std::vector<int> ord(items.size());
+            for (size_t q = 0; q < ord.size(); ++q) ord[q] = (int)q;
+            std::sort(ord.begin(), ord.end(), [&](int a, int b) {
+                return items[(size_t)a] < items[(size_t)b];
+            });
+            // a strip record per node; double sums over the node's taps
+            size_t q = 0;
+            const size_t start = out.size();
+            while (q < ord.size()) {
+                const int id = items[(size_t)ord[q]].first;
+                double w[kGrStrip] = {0}, m[kGrStrip] = {0};
+                for (; q < ord.size() && items[(size_t)ord[q]].first == id; ++q) {
+                    const int slot = items[(size_t)ord[q]].second;
+                    (slot & 1 ? m : w)[slot >> 1] += wts[(size_t)ord[q]];
+                }
+                Rec r;
+                r.id = id;
+                for (int i = 0; i < kGrStrip; ++i) {
+                    r.p[i] = (float)(0.5 * (w[i] + m[i]));
+                    r.q[i] = (float)(0.5 * (w[i] - m[i]));
+                }
+                out.push_back(r);
+            }
+            // strip boundary marker: the count goes into a separate pass below
+            out.push_back(Rec{-1 - (int)(out.size() - start), {0}, {0}});
+        }
+    }
+    // flatten: strip_ptr, ids, p, q (the markers hold each strip's count)
+    std::vector<int> sptr((size_t)nstrips + 1, 0), sid;
+    std::vector<float4> sp, sq;
+    std::vector<unsigned char> heavy((size_t)nstrips, 0);
+    std::vector<std::pair<int64_t, int>> work;
+    const int64_t heavy_at = gr_heavy_strip();
+    int64_t st = 0;
+    for (int u = 0; u < Ku; ++u) {
+        const auto& out = rows[(size_t)u];
+        size_t q = 0;
+        std::vector<int64_t> gcost((size_t)ngrp, 0);
+        for (int sx = 0; sx < nsx; ++sx, ++st) {
+            for (; out[q].id >= 0; ++q) {
+                sid.push_back(out[q].id);
+                sp.push_back(make_float4(out[q].p[0], out[q].p[1], out[q].p[2], out[q].p[3]));
+                sq.push_back(make_float4(out[q].q[0], out[q].q[1], out[q].q[2], out[q].q[3]));
+            }
+            const int cnt = -1 - out[q].id;
+            ++q;
+            sptr[(size_t)st + 1] = sptr[(size_t)st] + cnt;
+            if (cnt > heavy_at) {
+                heavy[(size_t)st] = 1;
+                work.emplace_back((cnt + 7) / 8, (int)(-st - 1));
+            } else {
+                gcost[(size_t)(sx / 8)] += cnt;
+            }
+        }
+        for (int g = 0; g < ngrp; ++g) work.emplace_back((gcost[(size_t)g] + 7) / 8, u * ngrp + g);
+    }
+    std::stable_sort(work.begin(), work.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<int> order(work.size());
+    for (size_t i = 0; i < work.size(); ++i) order[i] = work[i].second;
+    gp.n_strip_entries = (int64_t)sid.size();
+    if (sid.empty()) {
+        sid.push_back(0);
+        sp.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
+        sq.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    gp.n_strip_items = (int)order.size();
+    gp.strip_ptr.upload(sptr.data(), sptr.size(), s);
+    gp.strip_id.upload(sid.data(), sid.size(), s);
+    gp.strip_p.upload(sp.data(), sp.size(), s);
+    gp.strip_q.upload(sq.data(), sq.size(), s);
+    gp.strip_order.upload(order.data(), order.size(), s);
+    gp.strip_heavy.upload(heavy.data(), heavy.size(), s);
+    CBN_CUDA(cudaStreamSynchronize(s));
+}
+
+bool gr_strips_on() {   // CBN_GR_STRIPS=0: the per-cell gather (A/B)
+    const char* e = std::getenv("CBN_GR_STRIPS");
+    return !(e && e[0] == '0');
+}
+
 bool cell_gather_on() {
     const char* spread_env = std::getenv("CBN_GR_SPREAD");
     return !(spread_env && spread_env[0] == '1');
@@ -1956,6 +2085,7 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
             CBN_LAUNCH_CHECK();
             gr_cell_schedule(gp, h, Ku, Kv, s);
             CBN_CUDA(cudaStreamSynchronize(s));
+            if (gr_strips_on()) gr_build_strips(gp, Ku, Kv, s);
         }
         const int64_t nspec = (int64_t)u.n_mu * nh;
         B.tv.ensure(std::max((size_t)gp.n_rows * 32, ((size_t)nb * Ku * Kv + 1) / 2));
@@ -1980,14 +2110,28 @@ void grangeat_reverse(P* p, const float* vals, float* frames, int nb, cudaStream
         const int64_t nhalf = (int64_t)Ku * (Kv / 2 + 1);
         // node rows of the block once, CSR entries once, the half-plane grids
         // written once; on chip: one row value per entry and view
-        p->timer.add_bytes("grangeat_spread",
-                           8.0 * nb * gp.n_rows + (double)sizeof(GrEntry) * gp.n_entries +
-                               8.0 * nb * nhalf,
-                           8.0 * nb * (double)gp.n_entries);
-        k_gr_gather_cells<<<(unsigned)gp.n_items, 256, 0, s>>>(
-            B.grid.p, (size_t)nhalf, nhalf, gp.cell_ptr.p,
-            reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb, Ku, Kv,
-            gp.cell_order.p, gp.cell_heavy.p);
+        if (gr_strips_on() && gp.strip_ptr.p) {
+            // node rows once, strip records (4 + 32 B) once, the half planes
+            // written once; on chip: one row value per strip entry and view
+            const int hv = Kv / 2 + 1;
+            const int nsx = (hv + kGrStrip - 1) / kGrStrip;
+            p->timer.add_bytes("grangeat_spread",
+                               8.0 * nb * gp.n_rows + 36.0 * gp.n_strip_entries +
+                                   8.0 * nb * nhalf,
+                               8.0 * nb * (double)gp.n_strip_entries);
+            k_gr_gather_strips<<<(unsigned)gp.n_strip_items, 256, 0, s>>>(
+                B.grid.p, (size_t)nhalf, hv, nsx, (nsx + 7) / 8, gp.strip_ptr.p, gp.strip_id.p,
+                gp.strip_p.p, gp.strip_q.p, B.tv.p, nb, gp.strip_order.p, gp.strip_heavy.p);
+        } else {
+            p->timer.add_bytes("grangeat_spread",
+                               8.0 * nb * gp.n_rows + (double)sizeof(GrEntry) * gp.n_entries +
+                                   8.0 * nb * nhalf,
+                               8.0 * nb * (double)gp.n_entries);
+            k_gr_gather_cells<<<(unsigned)gp.n_items, 256, 0, s>>>(
+                B.grid.p, (size_t)nhalf, nhalf, gp.cell_ptr.p,
+                reinterpret_cast<const GrEntry*>(gp.cell_ent.p), B.tv.p, nb, Ku, Kv,
+                gp.cell_order.p, gp.cell_heavy.p);
+        }
         CBN_LAUNCH_CHECK();
     } else {
         StageScope st(p->timer, "grangeat_spread", s);

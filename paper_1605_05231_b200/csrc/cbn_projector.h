@@ -67,6 +67,14 @@ struct GrangeatPlan {
     DevBuf<GrNode> node_tab;            // reverse: node-scaled t-spectrum rows
     int64_t n_rows = 0;                 // rows of node_tab (nspec + second nodes)
     int64_t n_entries = 0;              // reverse: CSR entries (node, tap) over all cells
+    // reverse, strip form of the cell CSR (k_gr_gather_strips): per half-plane
+    // strip of kGrStrip cells along v, one entry per node with the strip's
+    // per-cell weights of the node value (p) and of its conjugate's sign (q)
+    DevBuf<int> strip_ptr, strip_id, strip_order;
+    DevBuf<float4> strip_p, strip_q;
+    DevBuf<unsigned char> strip_heavy;
+    int n_strip_items = 0;
+    int64_t n_strip_entries = 0;
 };
 
 constexpr int kGrJ = 5;        // plan_grangeat j=(5, 5) (grangeat.py:94)

@@ -79,3 +79,14 @@ def test_cli_geometry_reverse_grangeat_heavy_cells(case):
     assert err < TOL, err
     st = proj.plan_stats()
     assert st["fwd_gr_heavy_cells"] > 0 and st["fwd_gr_cell_items"] > 0, st
+    # the strip form (k_gr_gather_strips, the default) ran, heavy strips included,
+    # and the per-cell gather it replaced (CBN_GR_STRIPS=0) gives the same frames
+    assert st["fwd_gr_heavy_strips"] > 0 and st["fwd_gr_strip_items"] > 0, st
+    assert 0 < st["fwd_gr_strip_entries"] < st["fwd_gr_cell_entries"], st
+    import os
+    os.environ["CBN_GR_STRIPS"] = "0"
+    try:
+        cells = proj.grangeat_reverse(z["gr_values"]).cpu().numpy()
+    finally:
+        del os.environ["CBN_GR_STRIPS"]
+    assert rel_l2(cells, out) < 1e-6
