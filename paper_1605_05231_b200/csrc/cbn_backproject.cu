@@ -489,6 +489,106 @@ struct BpCtx {
     KBSet kbr{};
 };
 
+bool rs_strips_on() {   // CBN_RS_STRIPS=0: the per-column transposed gather (A/B)
+    const char* e = std::getenv("CBN_RS_STRIPS");
+    return !(e && e[0] == '0');
+}
+
+// Strip form of the transposed-resample column CSR (k_rs_gather_strips):
+// per rho plane, strips of kRsStrip theta columns, their (sorted) column lists
+// merged by target on the host once per plan.
+void bp_build_col_strips(cbn_projector_s* p, int64_t K0, int64_t K1, cudaStream_t s) {
+    const int64_t ncol = K0 * K1;
+    const int nsx = (int)((K1 + kRsStrip - 1) / kRsStrip);
+    const int64_t nstrips = K0 * nsx;
+    std::vector<int> ptr((size_t)ncol + 1);
+    std::vector<RsColEntry> ent((size_t)p->bcol_n);
+    CBN_CUDA(cudaMemcpyAsync(ptr.data(), p->bcol_ptr.p, sizeof(int) * ptr.size(),
+                             cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaMemcpyAsync(ent.data(), p->bcol_ent.p, sizeof(RsColEntry) * ent.size(),
+                             cudaMemcpyDeviceToHost, s));
+    CBN_CUDA(cudaStreamSynchronize(s));
+    struct Rec {
+        int t, f2;
+        float w2[3];
+        float wab[kRsStrip];
+    };
+    std::vector<std::vector<Rec>> planes((size_t)K0);
+    std::vector<std::vector<int>> counts((size_t)K0, std::vector<int>((size_t)nsx, 0));
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t r = 0; r < K0; ++r) {
+        std::vector<std::pair<int, int>> items;   // (target, entry index)
+        auto& out = planes[(size_t)r];
+        for (int sx = 0; sx < nsx; ++sx) {
+            items.clear();
+            for (int c = 0; c < kRsStrip; ++c) {
+                const int64_t th = (int64_t)sx * kRsStrip + c;
+                if (th >= K1) break;
+                const int64_t col = r * K1 + th;
+                for (int e = ptr[(size_t)col]; e < ptr[(size_t)col + 1]; ++e)
+                    items.emplace_back(ent[(size_t)e].t, e);
+            }
+            std::sort(items.begin(), items.end());
+            size_t q = 0;
+            int cnt = 0;
+            while (q < items.size()) {
+                const int t = items[q].first;
+                Rec rec{};
+                const RsColEntry& e0 = ent[(size_t)items[q].second];
+                rec.t = t;
+                rec.f2 = e0.f2;
+                for (int k = 0; k < 3; ++k) rec.w2[k] = e0.w2[k];
+                for (; q < items.size() && items[q].first == t; ++q) {
+                    const int e = items[q].second;
+                    int col_in = 0;   // which of the strip's columns holds entry e
+                    for (int c = 0; c < kRsStrip; ++c) {
+                        const int64_t col = r * K1 + (int64_t)sx * kRsStrip + c;
+                        if ((int64_t)sx * kRsStrip + c < K1 && e >= ptr[(size_t)col] &&
+                            e < ptr[(size_t)col + 1])
+                            col_in = c;
+                    }
+                    rec.wab[col_in] += ent[(size_t)e].wab;
+                }
+                out.push_back(rec);
+                ++cnt;
+            }
+            counts[(size_t)r][(size_t)sx] = cnt;
+        }
+    }
+    std::vector<int> sptr((size_t)nstrips + 1, 0);
+    std::vector<RsStripEnt> se;
+    std::vector<float4> w2, wab;
+    int64_t st = 0;
+    for (int64_t r = 0; r < K0; ++r) {
+        const auto& out = planes[(size_t)r];
+        size_t q = 0;
+        for (int sx = 0; sx < nsx; ++sx, ++st) {
+            const int cnt = counts[(size_t)r][(size_t)sx];
+            for (int k = 0; k < cnt; ++k, ++q) {
+                const Rec& rc = out[q];
+                se.push_back(RsStripEnt{rc.t, rc.f2});
+                w2.push_back(make_float4(rc.w2[0], rc.w2[1], rc.w2[2], 0.f));
+                wab.push_back(make_float4(rc.wab[0], rc.wab[1], rc.wab[2], rc.wab[3]));
+            }
+            sptr[(size_t)st + 1] = sptr[(size_t)st] + cnt;
+        }
+    }
+    p->bstrip_n = (int64_t)se.size();
+    if (se.empty()) {
+        se.push_back(RsStripEnt{0, 0});
+        w2.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
+        wab.push_back(make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    p->bstrip_nsx = nsx;
+    p->bstrip_ptr.upload(sptr.data(), sptr.size(), s);
+    p->bstrip_ent.alloc(sizeof(RsStripEnt) * se.size());
+    CBN_CUDA(cudaMemcpyAsync(p->bstrip_ent.p, se.data(), sizeof(RsStripEnt) * se.size(),
+                             cudaMemcpyHostToDevice, s));
+    p->bstrip_w2.upload(w2.data(), w2.size(), s);
+    p->bstrip_wab.upload(wab.data(), wab.size(), s);
+    CBN_CUDA(cudaStreamSynchronize(s));
+}
+
 BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
     build_backward_plan(p, s);
     const cbn_projector_config& c = p->c;
@@ -589,6 +689,7 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
             k_rs_col_sort<<<blocks_for(ncol, 128), 128, 0, s>>>(
                 p->bcol_ptr.p, ncol, reinterpret_cast<RsColEntry*>(p->bcol_ent.p));
             CBN_LAUNCH_CHECK();
+            if (rs_strips_on() && rax[0].J == 3) bp_build_col_strips(p, x.kd3[0], x.kd3[1], s);
             CBN_CUDA(cudaStreamSynchronize(s));
         }
     }
@@ -843,17 +944,32 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
                     // views (two value loads + weights per entry per cell pair)
                     double planes = 0;
                     for (const auto& rn : p->bres_rho_runs) planes += rn.second - rn.first;
+                    const bool strips = x.shift == 2 && rs_strips_on() && p->bstrip_ptr.p;
+                    const double ents = strips ? 40.0 * p->bstrip_n
+                                               : (double)sizeof(RsColEntry) * p->bcol_n;
                     p->timer.add_bytes("transpose_spread",
-                                       (den_only ? 0.0 : 4.0 * per_view * nvr) +
-                                           (double)sizeof(RsColEntry) * p->bcol_n +
+                                       (den_only ? 0.0 : 4.0 * per_view * nvr) + ents +
                                            4.0 * planes * x.kd3[1] * x.kd3[2],
-                                       (double)sizeof(RsColEntry) * p->bcol_n * (x.kd3[2] / 2));
+                                       ents * (x.kd3[2] / 2));
                 }
                 const RsColEntry* ent = reinterpret_cast<const RsColEntry*>(p->bcol_ent.p);
                 float* gnum = den_only ? nullptr : greal;
                 float* gden = den_only ? greal : nullptr;
                 const float* vt = den_only ? nullptr : p->values_t.p;
-                if (x.shift == 2) {
+                if (x.shift == 2 && rs_strips_on() && p->bstrip_ptr.p) {
+                    const unsigned char* used = p->bres_rho_used.p;
+                    const int kt = (int)x.kd3[1];
+                    const unsigned nst = (unsigned)(x.kd3[0] * p->bstrip_nsx);
+                    const RsStripEnt* se = reinterpret_cast<const RsStripEnt*>(p->bstrip_ent.p);
+                    if (den_only)
+                        k_rs_gather_strips<true><<<nst, kRsPairThreads, 0, s>>>(
+                            gnum, gden, p->g.n_views, p->bstrip_ptr.p, se, p->bstrip_w2.p,
+                            p->bstrip_wab.p, vt, vlo, nvr, used, kt, p->bstrip_nsx);
+                    else
+                        k_rs_gather_strips<false><<<nst, kRsPairThreads, 0, s>>>(
+                            gnum, gden, p->g.n_views, p->bstrip_ptr.p, se, p->bstrip_w2.p,
+                            p->bstrip_wab.p, vt, vlo, nvr, used, kt, p->bstrip_nsx);
+                } else if (x.shift == 2) {
                     const unsigned char* used = p->bres_rho_used.p;
                     const int kt = (int)x.kd3[1];
                     if (den_only)

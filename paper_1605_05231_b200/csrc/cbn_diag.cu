@@ -304,6 +304,8 @@ int cbn_projector_plan_stats(cbn_projector* p, int64_t* vals, int32_t* count, ch
             st.emplace_back("bp_primary_nodes", p->bpairs.p ? p->bpairs_n : -1);
             st.emplace_back("bp_rho_planes", p->bres[2].K);
             st.emplace_back("bp_rho_planes_used", runs_sum(p->bres_rho_runs));
+            st.emplace_back("bp_column_entries", p->bcol_ent.p ? p->bcol_n : -1);
+            st.emplace_back("bp_strip_entries", p->bstrip_ptr.p ? p->bstrip_n : -1);
             st.emplace_back("bp_resample_cells", (int64_t)p->bres[0].K * p->bres[1].K * p->bres[2].K);
             st.emplace_back("bp_umbrella_targets_per_view", (int64_t)p->bumb.n_mu * p->bumb.n_t);
             st.emplace_back("bp_umbrella_invalid_per_view", invalid_per_view(p->bumb, p->brad, p->bpad));

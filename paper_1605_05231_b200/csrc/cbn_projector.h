@@ -175,6 +175,11 @@ struct cbn_projector_s {
     cbn::DevBuf<int> bcol_ptr;      // transposed-resample CSR: column -> entries (views in lanes)
     cbn::DevBuf<char> bcol_ent;     // RsColEntry per (target, rho tap, theta tap)
     int64_t bcol_n = 0;             // entries of the column CSR
+    cbn::DevBuf<int> bstrip_ptr;    // strip form of the column CSR (k_rs_gather_strips)
+    cbn::DevBuf<char> bstrip_ent;   // RsStripEnt per (target, strip)
+    cbn::DevBuf<float4> bstrip_w2, bstrip_wab;   // phi weights; per-column rho-theta weights
+    int64_t bstrip_n = 0;
+    int bstrip_nsx = 0;
     cbn::DevBuf<float> values_t;    // umbrella values of a view run, target-major
     int bp_staged = 0;              // views [0, bp_staged) of the next backprojection already
                                     // forward-Grangeat'ed into values_t (cbn_backproject_stage_views)

@@ -441,4 +441,74 @@ k_rs_gather_cols2(float* __restrict__ gnum, float* __restrict__ gden, int V,
     }
 }
 
+// Strip form of the column gather: a target's 3 x 3 (rho, theta) taps put
+// the same 2 value loads and phi weights into 9 columns; strips of kRsStrip
+// consecutive theta columns of one rho plane, with a strip's column lists
+// merged by target at plan time (host, sorted by target), load each value
+// pair once per strip and apply it to every column the target reaches there
+// (per-column rho-theta weight wab[c], zero elsewhere).
+constexpr int kRsStrip = 4;
+
+struct RsStripEnt {
+    int t;          // view-0 target
+    int f2;         // first phi tap of view 0
+};
+
+template <bool DEN>
+static __global__ void __launch_bounds__(kRsPairThreads)
+k_rs_gather_strips(float* __restrict__ gnum, float* __restrict__ gden, int V,
+                   const int* __restrict__ sptr, const RsStripEnt* __restrict__ ent,
+                   const float4* __restrict__ w2s, const float4* __restrict__ wabs,
+                   const float* __restrict__ valsT, int vlo, int nv,
+                   const unsigned char* __restrict__ plane_used, int K1, int nsx) {
+    const int strip = blockIdx.x;
+    const int rho = strip / nsx, c0 = (strip - rho * nsx) * kRsStrip;
+    if (!plane_used[rho]) return;   // rho plane never transformed
+    const int beg = sptr[strip], end = sptr[strip + 1];
+    for (int i = threadIdx.x; i < V; i += kRsPairThreads) {
+        float ev[kRsStrip], od[kRsStrip];
+#pragma unroll
+        for (int c = 0; c < kRsStrip; ++c) ev[c] = od[c] = 0.f;
+#pragma unroll 2
+        for (int k = beg; k < end; ++k) {
+            const RsStripEnt e = ent[k];
+            const float4 w2 = w2s[k], wab = wabs[k];
+            const int d = e.f2 - 2 * i;
+            int b0 = d >> 1;                       // floor(d / 2)
+            b0 += b0 < 0 ? V : 0;
+            int b1 = b0 + 1;
+            b1 -= b1 >= V ? V : 0;
+            int r0 = b0 - vlo, r1 = b1 - vlo;
+            r0 += r0 < 0 ? V : 0;
+            r1 += r1 < 0 ? V : 0;
+            const bool ok0 = r0 < nv, ok1 = r1 < nv;
+            float x0, x1;
+            if constexpr (DEN) {
+                x0 = ok0 ? 1.f : 0.f;
+                x1 = ok1 ? 1.f : 0.f;
+            } else {
+                const float* vt = valsT + (size_t)e.t * nv;
+                x0 = ok0 ? __ldg(vt + r0) : 0.f;
+                x1 = ok1 ? __ldg(vt + r1) : 0.f;
+            }
+            // the target's contribution to the even / odd phi cell of the pair
+            const float a = fmaf(w2.x, x0, w2.z * x1);
+            const float b = (d & 1) == 0 ? w2.y * x0 : w2.y * x1;
+            const float ae = (d & 1) == 0 ? a : b, ao = (d & 1) == 0 ? b : a;
+            const float wc[4] = {wab.x, wab.y, wab.z, wab.w};
+#pragma unroll
+            for (int c = 0; c < kRsStrip; ++c) {
+                ev[c] = fmaf(wc[c], ae, ev[c]);
+                od[c] = fmaf(wc[c], ao, od[c]);
+            }
+        }
+        float* g = DEN ? gden : gnum;
+#pragma unroll
+        for (int c = 0; c < kRsStrip; ++c)
+            if (c0 + c < K1)
+                *(reinterpret_cast<float2*>(g + ((size_t)rho * K1 + c0 + c) * 2 * V) + i) =
+                    make_float2(ev[c], od[c]);
+    }
+}
+
 }  // namespace cbn

@@ -356,3 +356,20 @@ def test_backprojector_records_match_node_generation(pl, golden_n16, monkeypatch
     gen = proj.backproject(frames).cpu().numpy()
     assert rel_l2(rec, gen) < 1e-5
     assert rel_l2(rec, g["bp"]) < TOL
+
+
+def test_transposed_resample_strips_match_columns(pl, monkeypatch):
+    """The strip form of the backprojector's transposed-resample gather
+    (k_rs_gather_strips: per rho plane, 4 theta columns merged by target) and
+    the per-column gather (CBN_RS_STRIPS=0) give the same backprojection, on a
+    geometry with the 2-cell view shift of configs 2/3 (k_rs_gather_cols2)."""
+    import torch
+    g = dict(np.load(os.path.join(GOLDEN, "pipeline_n12_v24.npz")))
+    n, views = int(g["n"]), int(g["views"])
+    geom, voxel, spec, cfg = small_setup(n, views)
+    frames = torch.from_numpy(g["frames"].astype(np.float32)).cuda()
+    strips = pl.Projector(geom, cfg, n, voxel, 2).backproject(frames).cpu().numpy()
+    monkeypatch.setenv("CBN_RS_STRIPS", "0")
+    cols = pl.Projector(geom, cfg, n, voxel, 2).backproject(frames).cpu().numpy()
+    assert rel_l2(strips, cols) < 1e-5
+    assert rel_l2(strips, g["bp"]) < TOL
