@@ -43,9 +43,10 @@ FALLBACK_HBM_GBS = 6650.0       # B200_PROFILING.md fallback when no measured pe
 SMEM_TBS = 148 * 128 * 1.965e9 / 1e12   # nominal shared-memory bandwidth
 # dram__bytes_read.sum + dram__bytes_write.sum per config-2 step of the
 # dominant kernels, from the committed ncu captures (profiles/)
-TRAFFIC = {"forward": {"resample_gather": 1.736e9, "spectrum_gather": 1.467e9,
-                       "grangeat_spread": 2.442e9, "grangeat_rows": 1.862e9},
-           "back": {"bp_spread": 1.025e9, "transpose_spread": 0.838e9}}
+TRAFFIC = {"forward": {"resample_gather": 1.736e9, "spectrum_gather": 1.470e9,
+                       "grangeat_spread": 3.284e9, "grangeat_rows": 1.865e9},
+           "back": {"bp_spread": 1.512e9, "transpose_spread": 0.828e9,
+                    "grangeat_forward": 0.718e9}}
 
 
 def parse_args():

@@ -321,6 +321,7 @@ struct BpRecSrc {
     const float4* g;      // factor of X[i1] (x, y), factor of X[i2] (z, w)
     const int2* idx;      // i1, i2 (-1: no mirror)
     const float2* X;      // ramp-filtered lattice, node order
+    const float2* vals;   // or: the values already formed in sorted order (k_bp_values)
     template <int J>
     CBN_D void stage(const KBSet& kb, int64_t pos, float2& v, int (&l)[3], float (&wt)[3][J]) const {
         const float4 q = rec[pos];
@@ -331,6 +332,10 @@ struct BpRecSrc {
         kb_weights_y<J>(kb.ax[0], q.x, (bits >> 15) & 1, wt[0]);
         kb_weights_y<J>(kb.ax[1], q.y, (bits >> 16) & 1, wt[1]);
         kb_weights_y<J>(kb.ax[2], q.z, (bits >> 17) & 1, wt[2]);
+        if (vals) {
+            v = vals[pos];
+            return;
+        }
         const float4 f = g[pos];
         const int2 ix = idx[pos];
         v = cmul(X[ix.x], make_float2(f.x, f.y));
@@ -341,6 +346,29 @@ struct BpRecSrc {
         }
     }
 };
+
+// the spread's point values in sorted order, one streaming pass ahead of the
+// spread so its staging reads them sequentially instead of gathering two
+// lattice samples per point behind each round's barrier
+__global__ void k_bp_values(const float4* __restrict__ g, const int2* __restrict__ idx,
+                            const float2* __restrict__ X, int64_t m, float2* __restrict__ vals) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= m) return;
+    const float4 f = g[pos];
+    const int2 ix = idx[pos];
+    float2 v = cmul(X[ix.x], make_float2(f.x, f.y));
+    if (ix.y >= 0) {
+        const float2 q = cmul(X[ix.y], make_float2(f.z, f.w));
+        v.x += q.x;
+        v.y -= q.y;
+    }
+    vals[pos] = v;
+}
+
+bool bp_values_pass_on() {   // CBN_BP_VALUES=0: values gathered inside the spread (A/B)
+    const char* e = std::getenv("CBN_BP_VALUES");
+    return !(e && e[0] == '0');
+}
 
 template <int J>
 __global__ void k_bp_records(BpSrc src, KBSet kb, TileGeom<3> tg, const int* __restrict__ perm,
@@ -1234,7 +1262,16 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
             });
             CBN_LAUNCH_CHECK();
         }
-        const BpRecSrc rsrc{p->bspec_rec.p, p->bspec_g.p, p->bspec_idx.p, p->lattice.p};
+        const float2* vals = nullptr;
+        if (bp_values_pass_on()) {
+            // the part's subproblems cover sorted positions [sub s0 start, sub s1 end)
+            p->bspec_vals.ensure((size_t)p->bpairs_n);
+            k_bp_values<<<blocks_for(p->bpairs_n, 256), 256, 0, s>>>(
+                p->bspec_g.p, p->bspec_idx.p, p->lattice.p, p->bpairs_n, p->bspec_vals.p);
+            CBN_LAUNCH_CHECK();
+            vals = p->bspec_vals.p;
+        }
+        const BpRecSrc rsrc{p->bspec_rec.p, p->bspec_g.p, p->bspec_idx.p, p->lattice.p, vals};
         dispatch_j(sax[0].J, [&](auto jc) {
             launch_spread3<decltype(jc)::value>(grid, kbs, bb, rsrc, s, s0, s1);
             return 0;

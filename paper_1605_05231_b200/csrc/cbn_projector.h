@@ -188,6 +188,7 @@ struct cbn_projector_s {
     cbn::DevBuf<float4> bspec_rec;   // per sorted primary node: KB arguments + tile offsets
     cbn::DevBuf<float4> bspec_g;     // ... factors of its lattice sample and its mirror's
     cbn::DevBuf<int2> bspec_idx;     // ... those two lattice indices
+    cbn::DevBuf<float2> bspec_vals;  // ... the values of a step (k_bp_values)
     int64_t bpairs_n = 0;
     bool bspec_fit = false;
     cbn::DevBuf<float> bspec_s32;   // cached first-sub-plan scaling of the 3D adjoint

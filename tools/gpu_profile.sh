@@ -12,6 +12,6 @@ python tools/profile_step.py > $OUT/plain.log 2>&1 && \
 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches_fwd.csv python tools/profile_step.py > $OUT/ncu_launch_fwd.log 2>&1
 python tools/profile_step.py --direction back > $OUT/plainb.log 2>&1 && \
 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches_bp.csv python tools/profile_step.py --direction back > $OUT/ncu_launch_bp.log 2>&1
-ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_gr_gather_cells|k_spec_gather|k_resample_window" -c 3 -o $OUT/full_fwd python tools/profile_step.py > $OUT/ncu_full_fwd.log 2>&1
-ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_spread_owned" -c 1 -o $OUT/full_bp python tools/profile_step.py --direction back > $OUT/ncu_full_bp.log 2>&1
+ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_gr_gather_strips|k_spec_gather|k_resample_window" -c 3 -o $OUT/full_fwd python tools/profile_step.py > $OUT/ncu_full_fwd.log 2>&1
+ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"k_spread_owned|k_rs_gather_strips" -c 2 -o $OUT/full_bp python tools/profile_step.py --direction back > $OUT/ncu_full_bp.log 2>&1
 ls -la $OUT
