@@ -1201,7 +1201,11 @@ void bp_finish(cbn_projector_s* p, float2* acc, int part, int nparts, float2* gr
         CBN_CUDA(cudaStreamSynchronize(s));
         p->bpairs_n = base_n + h_extra;
         const RadialPairSrc psrc{r.src(), p->bpairs.p};
-        const int tile[3] = {kTile3, kTile3, kTile3Fast};
+        // 8 x 4 x 16 tiles: a 13 x 9 x 22 region (25 KB) lets 8 CTAs share an
+        // SM (8 x 8 x 16: 6); measured 3.25 -> 3.12 ms at config 2
+        int tile[3] = {kTile3, kTile3 / 2, kTile3Fast};
+        if (const char* e = std::getenv("CBN_BP_TILE"))   // "t0,t1,t2" (tuning A/B)
+            std::sscanf(e, "%d,%d,%d", &tile[0], &tile[1], &tile[2]);
         dispatch_j(sax[0].J, [&](auto jc) {
             build_bins<3, decltype(jc)::value>(p->bspec_bins, psrc, kbs, p->bpairs_n, tile, kMaxSub,
                                                s, true);

@@ -244,7 +244,9 @@ void run_type1(cbn_nufft* p, const float2* y, float2* x, cudaStream_t s) {
 template <int D>
 void sort_plan(cbn_nufft* p, cudaStream_t s) {
     ExplicitSrc<D> src{p->nodes.p, p->nodes.p ? nullptr : p->nodes32.p, nullptr};
-    const int tile[3] = {D == 3 ? 8 : 16, D == 3 ? 8 : 16, 16};
+    int tile[3] = {D == 3 ? 8 : 16, D == 3 ? 8 : 16, 16};
+    if (const char* e = std::getenv("CBN_NUFFT_TILE"); e && D == 3)   // "t0,t1,t2" (tuning A/B)
+        std::sscanf(e, "%d,%d,%d", &tile[0], &tile[1], &tile[2]);
     {
         // coordinates read twice (keys, interleave), keys written + read,
         // the permutation written; float32: the sorted copy (read + write)
