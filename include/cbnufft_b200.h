@@ -144,6 +144,17 @@ int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t 
 int cbn_host_f64_to_f32(const double* src, float* dst, int64_t n, int32_t threads);
 int cbn_host_f32_to_f64(const float* src, double* dst, int64_t n, int32_t threads);
 
+/* Elementwise pieces of the general Grangeat transforms (grangeat.py:131-170,
+ * any plan_grangeat j / oversample): real lines in [outer][n] -> complex64
+ * out = in * w[k] (w host float64, n of them); complex64 lines ->
+ * float32 out = Re(in) * w[k]; and g -= mean of the frame's outermost ring
+ * (grangeat.py:167-169), all on device buffers. */
+int cbn_lines_real_in(const float* in, int64_t outer, int64_t n, const double* w, void* out,
+                      void* stream);
+int cbn_lines_real_out(const void* in, int64_t outer, int64_t n, const double* w, float* out,
+                       void* stream);
+int cbn_frame_ring_center(float* g, int32_t nu, int32_t nv, void* stream);
+
 /* -------------------------------------------------------------- projector
  * Replaces ConeGeometry / ProjectorConfig / nufft_forward_project /
  * nufft_backproject (geometry.py:21-64, pipeline.py:31-212).

@@ -76,6 +76,9 @@ _SIGS = {
     "cbn_resample_apply": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_resample_transpose": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "cbn_radial_fft": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i32, c_f64, c_vp]),
+    "cbn_lines_real_in": (ctypes.c_int, [c_vp, c_i64, c_i64, P_f64, c_vp, c_vp]),
+    "cbn_lines_real_out": (ctypes.c_int, [c_vp, c_i64, c_i64, P_f64, c_vp, c_vp]),
+    "cbn_frame_ring_center": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
     "cbn_projector_set_node_shard": (ctypes.c_int, [c_vp, c_i32, c_i32, P_i64, P_i64, c_vp]),
     "cbn_host_gather_f64_to_f32": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_i32]),
     "cbn_host_f64_to_f32": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32]),

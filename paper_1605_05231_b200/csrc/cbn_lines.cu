@@ -78,6 +78,62 @@ __global__ void k_trilinear_transfer(double* __restrict__ out, int n_rho, int n_
     }
 }
 
+// out[o][k] = (in[o][k] * w[k], 0)  (real lines -> complex, per-column weight)
+__global__ void k_lines_real_in(const float* __restrict__ in, int64_t total, int64_t n,
+                                const double* __restrict__ w, float2* __restrict__ out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = make_float2((float)((double)in[e] * w[e % n]), 0.f);
+}
+
+// out[o][k] = Re(in[o][k]) * w[k]
+__global__ void k_lines_real_out(const float2* __restrict__ in, int64_t total, int64_t n,
+                                 const double* __restrict__ w, float* __restrict__ out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = (float)((double)in[e].x * w[e % n]);
+}
+
+// g -= mean of the outermost ring of an nu x nv frame (grangeat.py:167-169):
+// one block sums the ring in float64, then every element is shifted
+__global__ void k_ring_mean(const float* __restrict__ g, int nu, int nv, double* __restrict__ mean) {
+    const int nring = (nu == 1 || nv == 1) ? nu * nv : 2 * nu + 2 * nv - 4;
+    double acc = 0.0;
+    for (int r = threadIdx.x; r < nring; r += blockDim.x) {
+        int u, v;
+        if (nu == 1 || nv == 1) {
+            u = r / nv;
+            v = r % nv;
+        } else if (r < nv) {
+            u = 0;
+            v = r;
+        } else if (r < 2 * nv) {
+            u = nu - 1;
+            v = r - nv;
+        } else {
+            const int k = r - 2 * nv;
+            u = 1 + k / 2;
+            v = (k & 1) ? nv - 1 : 0;
+        }
+        acc += (double)g[(int64_t)u * nv + v];
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+        mean[0] = t / nring;
+    }
+}
+
+__global__ void k_sub_mean(float* __restrict__ g, int64_t n, const double* __restrict__ mean) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        g[e] = (float)((double)g[e] - mean[0]);
+}
+
 static unsigned stream_grid(int64_t total) {
     const int64_t b = (total + 255) / 256;
     return (unsigned)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -138,6 +194,58 @@ int cbn_trilinear_transfer(int32_t n_rho, int32_t n_theta, int32_t n_phi, double
         k_trilinear_transfer<<<stream_grid(total), 256, 0, s>>>(out, n_rho, n_theta, n_phi,
                                                                 delta_rho, voxel_mm);
         CBN_LAUNCH_CHECK();
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_lines_real_in(const float* in, int64_t outer, int64_t n, const double* w, void* out,
+                      void* stream) {
+    try {
+        CBN_REQUIRE(in && w && out && outer >= 1 && n >= 1, "bad argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevBuf<double> wd;
+        wd.upload(w, (size_t)n, s);
+        const int64_t total = outer * n;
+        k_lines_real_in<<<stream_grid(total), 256, 0, s>>>(in, total, n, wd.p,
+                                                          static_cast<float2*>(out));
+        CBN_LAUNCH_CHECK();
+        CBN_CUDA(cudaStreamSynchronize(s));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_lines_real_out(const void* in, int64_t outer, int64_t n, const double* w, float* out,
+                       void* stream) {
+    try {
+        CBN_REQUIRE(in && w && out && outer >= 1 && n >= 1, "bad argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevBuf<double> wd;
+        wd.upload(w, (size_t)n, s);
+        const int64_t total = outer * n;
+        k_lines_real_out<<<stream_grid(total), 256, 0, s>>>(static_cast<const float2*>(in), total,
+                                                           n, wd.p, out);
+        CBN_LAUNCH_CHECK();
+        CBN_CUDA(cudaStreamSynchronize(s));
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_frame_ring_center(float* g, int32_t nu, int32_t nv, void* stream) {
+    try {
+        CBN_REQUIRE(g && nu >= 1 && nv >= 1, "bad argument");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DevBuf<double> mean(1);
+        k_ring_mean<<<1, 256, 0, s>>>(g, nu, nv, mean.p);
+        CBN_LAUNCH_CHECK();
+        k_sub_mean<<<stream_grid((int64_t)nu * nv), 256, 0, s>>>(g, (int64_t)nu * nv, mean.p);
+        CBN_LAUNCH_CHECK();
+        CBN_CUDA(cudaStreamSynchronize(s));
         return CBN_OK;
     } catch (const std::exception& e) {
         return fail(e);

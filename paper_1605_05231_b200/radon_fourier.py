@@ -182,9 +182,11 @@ def _polar_nodes_2d(n: int, n_rho: int, n_theta: int):
     return np.stack([(ww * np.cos(tt)).ravel(), (ww * np.sin(tt)).ravel()], axis=-1), delta_rho
 
 
-def _phase_on_device(values, nodes: np.ndarray, n: int, conj: bool, w=None, w_inner: int = 1):
-    """values (device complex64) *= exp(+-i nodes . shift) [* w[i // w_inner]] in place."""
-    shift = np.array([n / 2.0 - 0.5, n / 2.0 - 0.5], dtype=np.float64)
+def _phase_on_device(values, nodes: np.ndarray, n, conj: bool, w=None, w_inner: int = 1):
+    """values (device complex64) *= exp(+-i nodes . shift) [* w[i // w_inner]] in place;
+    shift = dims / 2 - 1/2 (_center_phase), n an edge or the dims."""
+    dims = (n, n) if np.isscalar(n) else tuple(n)
+    shift = np.array([d / 2.0 - 0.5 for d in dims], dtype=np.float64)
     nodes = np.ascontiguousarray(nodes, dtype=np.float64)
     wp = None
     if w is not None:
