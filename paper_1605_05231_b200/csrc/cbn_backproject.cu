@@ -640,7 +640,7 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
     // (k_rs_gather_cols) instead of the atomic scatter
     const char* no_lanes = std::getenv("CBN_NO_VIEW_LANES");
     x.method_b = c.method == 1;
-    x.lanes = !x.method_b && !(no_lanes && no_lanes[0] == '1') && rax[0].J == 3 &&
+    x.lanes = !x.method_b && !(no_lanes && no_lanes[0] == '1') && res_j3(rax) &&
               (2LL * r.n_phi) % p->g.n_views == 0 && rax[0].K == 2 * r.n_phi;
     x.shift = (int)(2LL * r.n_phi / p->g.n_views);
     x.kd3[0] = rax[0].K;
@@ -717,7 +717,7 @@ BpCtx bp_context(cbn_projector_s* p, cudaStream_t s) {
             k_rs_col_sort<<<blocks_for(ncol, 128), 128, 0, s>>>(
                 p->bcol_ptr.p, ncol, reinterpret_cast<RsColEntry*>(p->bcol_ent.p));
             CBN_LAUNCH_CHECK();
-            if (rs_strips_on() && rax[0].J == 3) bp_build_col_strips(p, x.kd3[0], x.kd3[1], s);
+            if (rs_strips_on() && res_j3(rax)) bp_build_col_strips(p, x.kd3[0], x.kd3[1], s);
             CBN_CUDA(cudaStreamSynchronize(s));
         }
     }
@@ -1046,7 +1046,7 @@ void bp_transpose(cbn_projector_s* p, const BpCtx& x, const float* frames, int l
         }
         UmbrellaSrc src = projector_cached_umbrella(p, p->bumb, r, p->bpad, bl, s);
         StageScope st_sp(p->timer, "transpose_spread", s);
-        dispatch_j(rax[0].J, [&](auto jc) {
+        dispatch_j(res_jmax(rax), [&](auto jc) {
             constexpr int J = decltype(jc)::value;
             k_rs_spread2<J><<<blocks_for(mb, 256), 256, 0, s>>>(
                 den_only ? nullptr : gn, den_only ? gn : nullptr, x.kbr, src,

@@ -894,10 +894,13 @@ void add_needed(P* p, int64_t m) {
 
 int rho_pad_of(int cfg_pad, int n_rho) { return cfg_pad < 0 ? n_rho / 2 : cfg_pad; }
 
-void require_uniform(const int32_t* j, const char* what) {
-    if (!(j[0] == j[1] && j[1] == j[2]))
-        throw Error(CBN_EUNSUPPORTED, std::string(what) + ": per-axis tap counts must be equal");
-}
+// resample_j may differ per axis (ProjectorConfig, resampling.py:79): the
+// generic resample kernels loop the largest count (shorter axes carry zero
+// weights, kb_weights); the views-in-lanes kernels need J = 3 on every axis
+}  // namespace
+int cbn::res_jmax(const AxisPlan* ax) { return std::max(ax[0].J, std::max(ax[1].J, ax[2].J)); }
+bool cbn::res_j3(const AxisPlan* ax) { return ax[0].J == 3 && ax[1].J == 3 && ax[2].J == 3; }
+namespace {
 
 UmbrellaGeom umb_geom(const P* p, const UmbrellaTables& u, const RadialTables& r, int pad) {
     UmbrellaGeom g;
@@ -998,7 +1001,6 @@ void build_forward(P* p, cudaStream_t s) {
     CBN_REQUIRE(c.method == 0 || (c.side_lobes >= 0 && c.side_lobes + 1 <= kMaxDirTaps),
                 "side_lobes must be 0..7");
     CBN_REQUIRE(c.spectrum_j >= 2 && c.spectrum_j <= 8, "spectrum_j must be 2..8");
-    require_uniform(c.resample_j, "resample_j");
     p->frad.build(c.spec.n_rho, c.spec.n_theta, c.spec.n_phi, c.spec.rho_max, p->voxel, s);
     const double dt = c.t_pitch_mm > 0 ? c.t_pitch_mm : p->pu;
     p->fumb.build(p->g, c.n_mu, c.n_t, dt, s);
@@ -1018,7 +1020,6 @@ void build_backward(P* p, cudaStream_t s) {
     CBN_REQUIRE(c.method == 0 || c.method == 1, "method must be 0 ('a') or 1 ('b')");
     CBN_REQUIRE(c.method == 0 || (c.side_lobes >= 0 && c.side_lobes + 1 <= kMaxDirTaps),
                 "side_lobes must be 0..7");
-    require_uniform(c.resample_j, "resample_j");
     const int out = p->n_vol;
     const double extent = out * p->voxel;
     const int n_rho = 2 * (int)std::ceil(1.5 * out / 2.0);                 // pipeline.py:165
@@ -1391,7 +1392,7 @@ bool rho_lines_off() {   // CBN_RHO_LINES=0: the strided rho pass on the half sp
 bool real_grid(const P* p) {
     const char* off = std::getenv("CBN_COMPLEX_GRID");
     if (off && off[0] == '1') return false;
-    return views_in_lanes(p) && p->fres[0].J == 3 && p->c.method == 0;
+    return views_in_lanes(p) && res_j3(p->fres) && p->c.method == 0;
 }
 
 // the windowed view-chunk gather (k_resample_window) on the real grid; off
@@ -1632,7 +1633,7 @@ void ensure_lane_taps(P* p, cudaStream_t s) {
     if (u.taps_ready) return;
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)u.n_mu * u.n_t;
-    dispatch_j(ax[0].J, [&](auto jc) {
+    dispatch_j(res_jmax(ax), [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         UmbrellaSrc src = cached_umbrella(p, u, p->frad, p->fpad, 0, s);
         KBSet kb;
@@ -1707,7 +1708,7 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
                         const float* tscale = nullptr) {
     const AxisPlan* ax = p->fres;
     const int64_t per_view = (int64_t)p->fumb.n_mu * p->fumb.n_t;
-    const int per_launch = ax[0].J == 3 && window_gather(p) ? kWinChunk : 32;
+    const int per_launch = res_j3(ax) && window_gather(p) ? kWinChunk : 32;
     if (nb > per_launch) {
         for (int k = 0; k < nb; k += per_launch)
             gather_views_lanes(p, v0 + k, std::min(per_launch, nb - k), vals + (size_t)k * per_view,
@@ -1716,7 +1717,7 @@ void gather_views_lanes(P* p, int v0, int nb, float* vals, cudaStream_t s,
     }
     const int shift = (int)(2LL * p->frad.n_phi / p->g.n_views);
     ensure_lane_taps(p, s);
-    dispatch_j(ax[0].J, [&](auto jc) {
+    dispatch_j(res_jmax(ax), [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         UmbrellaTables& u = p->fumb;
         StageScope st(p->timer, "resample_gather", s);
@@ -1796,7 +1797,7 @@ void gather_views(P* p, int lo, int hi, float* vals, cudaStream_t s,
     StageScope st(p->timer, "resample_gather", s);
     p->timer.add_bytes("resample_gather", 4.0 * m,
                        8.0 * m * ax[0].J * ax[1].J * ax[2].J);
-    dispatch_j(ax[0].J, [&](auto jc) {
+    dispatch_j(res_jmax(ax), [&](auto jc) {
         constexpr int J = decltype(jc)::value;
         k_gather<3, J><<<blocks_for(m, 256), 256, 0, s>>>(p->big.p, kb, src,
                                                          UmbOut{vals, tscale, p->fumb.n_t}, m);
@@ -2176,7 +2177,7 @@ constexpr int kViewBlock = 32;   // views per reverse-Grangeat block
 
 // views per resample-gather chunk of the forward view loop
 int gather_chunk(const P* p) {
-    return views_in_lanes(p) && p->fres[0].J == 3 && window_gather(p) ? kWinChunk : kViewBlock;
+    return views_in_lanes(p) && res_j3(p->fres) && window_gather(p) ? kWinChunk : kViewBlock;
 }
 
 // Views [lo, hi): one resample grid per run of batches with equal scalings,

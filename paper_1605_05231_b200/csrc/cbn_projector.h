@@ -263,6 +263,9 @@ namespace cbn {
 
 // per-lane Grangeat scratch: the projector's own buffers (lane 0, caller's
 // stream) or lane1's (stream s1)
+int res_jmax(const AxisPlan* ax);
+bool res_j3(const AxisPlan* ax);
+
 struct GrBufs {
     FFTCache& fft;
     DevBuf<float2>& t;
