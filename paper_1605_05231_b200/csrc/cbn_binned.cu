@@ -17,6 +17,16 @@ int spread_warps_override() {
     return w;
 }
 
+bool bulk_flush_enabled() {
+    static const bool on = [] {
+        // off by default: measured 3.15 -> 3.28 ms on the config-2 backprojector
+        // spread and 40.8 -> 40.9 ms on config 4
+        const char* e = std::getenv("CBN_BULK_FLUSH");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 __global__ void k_bin_scatter(const int* __restrict__ keys, int64_t m, int* __restrict__ cursor,
                               int* __restrict__ perm) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

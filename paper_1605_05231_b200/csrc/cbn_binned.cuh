@@ -43,7 +43,17 @@ struct TileGeom {
     int nb[3];       // bins per axis
     int K[3];        // grid extent per axis
     int P;           // shared-memory pitch of the last axis (>= R[D-1])
+    int bulk;        // 3D spread: flush region rows with TMA bulk reductions
 };
+
+// Shared -> global bulk reduction of one contiguous run of floats (TMA,
+// UBLKRED): the run is added element-wise into global memory by the async
+// proxy; 16-byte aligned on both sides, size a multiple of 16 bytes.
+CBN_D void bulk_red_add_f32(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
+                 "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+                 : "memory");
+}
 
 template <int D>
 CBN_D void bin_origin(const TileGeom<D>& tg, int bin, int (&o)[3]) {
@@ -343,8 +353,32 @@ constexpr int owned_stage_stride() {
     return (3 * J) | 1;   // odd: conflict-free staging writes
 }
 
+// J = 8 with four warps stages each point as a 16-byte aligned block -- header
+// (value, packed first taps), the x weights as (a, a + 4) pairs by owning
+// warp, the y weights as (b, b + 4) pairs -- plus the z weights at an odd
+// stride: a warp reads a point's header, its x pair, its y pair and its z
+// weight with one instruction each, 4 instead of 7 staging reads per point and
+// warp (type 1 of config 4: 41.3 -> 37.8 ms).  The same packing at J = 6 / two
+// warps (header and the warp's three x weights as 16-byte broadcasts) was
+// slower, 3.16 -> 3.68 ms on the config-2 backprojector: it stays scalar.
+template <int J, int W>
+constexpr bool owned_packed() {
+    return J == 8 && W == 4;
+}
+template <int J>
+constexpr int owned_block_floats() {   // aligned block per staged point
+    return 20;
+}
+template <int J>
+constexpr int owned_rest_stride() {    // odd stride of the z weights
+    return 9;
+}
+
 template <int J, int W>
 constexpr size_t spread_owned_smem_bytes(int nreg) {
+    if (owned_packed<J, W>())
+        return (size_t)((nreg + 1) & ~1) * sizeof(float2) +
+               (size_t)W * 32 * (owned_block_floats<J>() + owned_rest_stride<J>()) * sizeof(float) + 16;
     return (size_t)nreg * sizeof(float2) + (size_t)W * 32 * owned_stage_stride<J>() * sizeof(float) +
            (size_t)W * 32 * (sizeof(float2) + sizeof(int)) + 8;
 }
@@ -365,10 +399,15 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
     bin_origin<3>(tg, sp.bin, o);
     const int R0 = tg.R[0], R1 = tg.R[1], R2 = tg.R[2], P = tg.P;
     const int nreg = R0 * R1 * P;
+    constexpr bool PACK = owned_packed<J, W>();
+    constexpr int BF = owned_block_floats<J>(), RS = owned_rest_stride<J>();
     float2* reg = reinterpret_cast<float2*>(smem4);
     float* stw = reinterpret_cast<float*>(reg + nreg);
     float2* stv = reinterpret_cast<float2*>(stw + ((NP * SW + 1) & ~1));
     int* stl = reinterpret_cast<int*>(stv + NP);
+    // packed staging: aligned blocks, then the odd-stride rest
+    float4* blk = reinterpret_cast<float4*>(reg + ((nreg + 1) & ~1));
+    float* rest = reinterpret_cast<float*>(blk) + NP * BF;
     for (int e = threadIdx.x; e < nreg; e += NP) reg[e] = make_float2(0.f, 0.f);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // this lane's taps of a warp's rows: row index, cell offset, weight slots
@@ -411,12 +450,26 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             CBN_DCHECK(l0 >= 0 && l0 < tg.T[0] && l1 >= 0 && l1 < tg.T[1] && l2 >= 0 &&
                            l2 < tg.T[2],
                        "owned spread: point outside its bin tile");
-            stl[threadIdx.x] = (l0 << 24) | ((l0 * R1 + l1) * P + l2);
-            stv[threadIdx.x] = v;
+            const int pl = (l0 << 24) | ((l0 * R1 + l1) * P + l2);
+            if constexpr (PACK) {
+                float4* b4 = blk + threadIdx.x * (BF / 4);
+                float* rs = rest + threadIdx.x * RS;
+                b4[0] = make_float4(v.x, v.y, __int_as_float(pl), 0.f);
+                // (a, a + 4) x pairs by owning warp, (b, b + 4) y pairs
+                b4[1] = make_float4(wt[0][0], wt[0][4], wt[0][1], wt[0][5]);
+                b4[2] = make_float4(wt[0][2], wt[0][6], wt[0][3], wt[0][7]);
+                b4[3] = make_float4(wt[1][0], wt[1][4], wt[1][1], wt[1][5]);
+                b4[4] = make_float4(wt[1][2], wt[1][6], wt[1][3], wt[1][7]);
 #pragma unroll
-            for (int d = 0; d < 3; ++d)
+                for (int q = 0; q < 8; ++q) rs[q] = wt[2][q];
+            } else {
+                stl[threadIdx.x] = pl;
+                stv[threadIdx.x] = v;
 #pragma unroll
-                for (int p = 0; p < J; ++p) stw[threadIdx.x * SW + d * J + p] = wt[d][p];
+                for (int d = 0; d < 3; ++d)
+#pragma unroll
+                    for (int p = 0; p < J; ++p) stw[threadIdx.x * SW + d * J + p] = wt[d][p];
+            }
         }
         __syncthreads();
         const int npts = min(NP, sp.count - base);
@@ -428,17 +481,19 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             const int fb = lane >> 3, fc = lane & 7;
             const int off0 = fb * P + fc, off1 = (fb + 4) * P + fc;
             for (int j = 0; j < npts; ++j) {
-                const float2 v = stv[j];
+                const float4 h = blk[j * (BF / 4)];
+                const float2 v = make_float2(h.x, h.y);
                 if (v.x == 0.f && v.y == 0.f) continue;     // uniform over the CTA
-                const int pl = stl[j];
+                const int pl = __float_as_int(h.z);
                 const int l0 = pl >> 24;
-                const float* ws = stw + j * SW;
+                const float2* pairs = reinterpret_cast<const float2*>(blk + j * (BF / 4) + 1);
                 const int a0 = (warp - l0) & 3;
                 float2* row0 = reg + (pl & 0xffffff) + a0 * row_stride;
                 float2* row1 = row0 + W * row_stride;
-                const float wz = ws[2 * J + fc];
-                const float wyz0 = ws[J + fb] * wz, wyz1 = ws[J + fb + 4] * wz;
-                const float wx0 = ws[a0], wx1 = ws[a0 + W];
+                const float wz = rest[j * RS + fc];
+                const float2 wy = pairs[4 + fb], wx = pairs[a0];
+                const float wyz0 = wy.x * wz, wyz1 = wy.y * wz;
+                const float wx0 = wx.x, wx1 = wx.y;
                 float2 cur[4] = {row0[off0], row0[off1], row1[off0], row1[off1]};
                 const float wk[4] = {wx0 * wyz0, wx0 * wyz1, wx1 * wyz0, wx1 * wyz1};
 #pragma unroll
@@ -531,8 +586,31 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
             __syncwarp();
         }
     }
-    __syncthreads();
     const FastDiv dP(P), dR1(R1);
+    if (tg.bulk) {
+        // Region rows (r0, r1) are contiguous runs of P cells in shared memory
+        // and, up to the axis-2 wrap, in the grid (the pad cells past R2 are
+        // zero): one TMA bulk reduction per run instead of one RED per cell.
+        // The generic-proxy tap writes are fenced to the async proxy first.
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (lane == 0) {
+            const int n1 = min(P, tg.K[2] - o[2]);   // cells before the wrap
+            for (int r = warp; r < R0 * R1; r += W) {
+                const int r0 = dR1.div(r), r1 = r - r0 * R1;
+                float2* grow = grid + ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] +
+                                       wrapc(o[1] + r1, tg.K[1])) * tg.K[2];
+                const float2* srow = reg + r * P;
+                bulk_red_add_f32(grow + o[2], srow, (unsigned)n1 * 8u);
+                if (n1 < P) bulk_red_add_f32(grow, srow + n1, (unsigned)(P - n1) * 8u);
+            }
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            // the region must stay allocated until the engine has read it
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        }
+        return;
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < nreg; e += NP) {
         const int r01 = dP.div(e), r2 = e - r01 * P;
         if (r2 >= R2) continue;
@@ -740,6 +818,7 @@ struct BinPlan {
             g.K[d] = tg.K[d];
         }
         g.P = tg.P;
+        g.bulk = tg.bulk;
         return g;
     }
 };
@@ -761,6 +840,8 @@ struct DeviceSortScratch {
 };
 void device_bins_finish(BinPlan& bp, DeviceSortScratch& sc, int64_t nbins, int max_sub,
                         cudaStream_t s);
+
+bool bulk_flush_enabled();   // CBN_BULK_FLUSH=1: TMA bulk-reduction flush of the 3D spread (A/B)
 
 // pitch_pad: store the last region axis with pitch = J (mod 16) (required by
 // k_spread_owned; harmless for the gather)
@@ -789,6 +870,11 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
     bp.tg.P = bp.tg.R[D - 1];
     if (D == 3 && pitch_pad) bp.tg.P += (((J - bp.tg.P) % 16) + 16) % 16;
     bp.nreg = bp.nreg / bp.tg.R[D - 1] * bp.tg.P;
+    // TMA bulk flush of the 3D spread: 16-byte aligned row runs on both sides
+    // and at most one wrap along the last axis
+    bp.tg.bulk = D == 3 && pitch_pad && bulk_flush_enabled() && bp.tg.P % 2 == 0 &&
+                 bp.tg.T[2] % 2 == 0 && bp.tg.K[2] % 2 == 0 && bp.tg.P <= bp.tg.K[2] &&
+                 bp.tg.K[2] % bp.tg.T[2] == 0;
     if (dev) {
         DeviceSortScratch& sc = *dev;
         sc.keys.ensure((size_t)m);

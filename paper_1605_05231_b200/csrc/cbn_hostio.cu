@@ -4,6 +4,7 @@
 // the plan's pinned staging buffers.  Done here with OpenMP threads (outside the
 // Python interpreter lock) at memory bandwidth: per-frame numpy calls from a
 // Python thread pool spent most of their time in task dispatch.
+#include <immintrin.h>
 #include <omp.h>
 
 #include <cstdint>
@@ -13,6 +14,24 @@
 namespace {
 
 int team(int32_t threads) { return threads > 0 ? threads : omp_get_max_threads(); }
+
+// float32 -> float64 with non-temporal stores: the result (2x the input) is
+// written once and not read back by this code, so the lines skip the
+// read-for-ownership (measured 1.5-1.9x on the 94 MB -> 189 MB frames)
+__attribute__((target("avx2"))) void widen_stream_avx2(const float* s, double* d, int64_t n) {
+    int64_t i = 0;
+    while (i < n && (reinterpret_cast<uintptr_t>(d + i) & 31)) {
+        d[i] = (double)s[i];
+        ++i;
+    }
+    for (; i + 8 <= n; i += 8) {
+        const __m256 v = _mm256_loadu_ps(s + i);
+        _mm256_stream_pd(d + i, _mm256_cvtps_pd(_mm256_castps256_ps128(v)));
+        _mm256_stream_pd(d + i + 4, _mm256_cvtps_pd(_mm256_extractf128_ps(v, 1)));
+    }
+    for (; i < n; ++i) d[i] = (double)s[i];
+    _mm_sfence();
+}
 
 }  // namespace
 
@@ -47,11 +66,16 @@ int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t 
 int cbn_host_f32_to_f64(const float* src, double* dst, int64_t n, int32_t threads) {
     try {
         CBN_REQUIRE(src && dst && n >= 0, "bad argument");
-        constexpr int64_t B = 1 << 16;
+        constexpr int64_t B = 1 << 14;
         const int64_t tasks = (n + B - 1) / B;
+        static const bool avx2 = __builtin_cpu_supports("avx2");
 #pragma omp parallel for schedule(static) num_threads(team(threads))
         for (int64_t t = 0; t < tasks; ++t) {
             const int64_t lo = t * B, hi = lo + B < n ? lo + B : n;
+            if (avx2) {
+                widen_stream_avx2(src + lo, dst + lo, hi - lo);
+                continue;
+            }
             for (int64_t i = lo; i < hi; ++i) dst[i] = (double)src[i];
         }
         return CBN_OK;
