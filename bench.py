@@ -159,6 +159,12 @@ def timed(fn, steps, d: Dist, stream):
     """K steps between a barrier + synchronize on both sides, CUDA events on
     the launching stream; returns the max-over-ranks milliseconds."""
     import torch
+    # a full cyclic-GC pass over torch's object graph takes tens of ms; when
+    # one landed inside the 20 timed calls of the drop-in API (which creates
+    # 360 frame objects per call) it moved the average by 3-4 ms.  Collect now
+    # and freeze the survivors so that no such pass runs inside the timed loop.
+    gc.collect()
+    gc.freeze()
     torch.cuda.synchronize()
     d.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -246,8 +252,21 @@ def measure_projector(args, d: Dist, config: int, direction: str):
     proj = pl.Projector(w.geom, w.cfg, w.n, w.voxel, 1 if fwd else 2)
     cm = None
     if d.world > 1 and args.comm == "capi":
-        from paper_1605_05231_b200.comm import NcclComm
-        cm = NcclComm.from_group()
+        # the C-ABI communicator has never met a multi-GPU node (this pool has
+        # one GPU per box): if any rank cannot create it, every rank takes the
+        # torch.distributed data plane instead of losing the run
+        import torch.distributed as dist
+        try:
+            from paper_1605_05231_b200.comm import NcclComm
+            cm = NcclComm.from_group()
+        except Exception as e:   # noqa: BLE001
+            print(f"[bench] rank {d.rank}: libcbnufft_b200_comm unavailable ({e}); "
+                  "falling back to torch.distributed", file=sys.stderr)
+            cm = None
+        ok = torch.tensor([1 if cm is not None else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            cm = None
     if fwd:
         x_dev = torch.from_numpy(vol_host).cuda()
         if cm is not None:
@@ -325,12 +344,23 @@ def measure_projector(args, d: Dist, config: int, direction: str):
                 h2d, d2h = V * w.geom.nu * w.geom.nv * 4, w.n ** 3 * 4
             api()
             api()
+            calls = []
+
+            def api_timed():
+                t0 = time.perf_counter()
+                api()
+                calls.append(1e3 * (time.perf_counter() - t0))
             w0 = time.perf_counter()
-            e_ms = timed(api, args.steps, d, stream)
+            e_ms = timed(api_timed, args.steps, d, stream)
             wall = time.perf_counter() - w0
+            calls.sort()
             e2e = {"value": round(V * args.steps / (e_ms / 1e3), 3), "unit": "views/s",
                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                    "ms_per_step": round(e_ms / args.steps, 3), "wall_s": round(wall, 3),
+                   # host wall clock of the individual calls (the value above is
+                   # the mean over all of them; the host side varies from box to box)
+                   "call_ms": {"min": round(calls[0], 3), "median": round(calls[len(calls) // 2], 3),
+                               "max": round(calls[-1], 3)},
                    "api": ("pipeline.nufft_forward_project(Volume3D float64) -> list[DetectorFrame] "
                            "float64" if fwd else
                            "pipeline.nufft_backproject(list[DetectorFrame] float64) -> Volume3D "

@@ -23,6 +23,7 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 _POOL: ThreadPoolExecutor | None = None
+_UPLOAD_CHUNKS = int(os.environ.get("CBN_UPLOAD_CHUNKS", "4"))
 _THREADS = max(1, min(16, os.cpu_count() or 1))
 
 
@@ -134,7 +135,7 @@ class Staging:
         return b
 
 
-def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int = 4):
+def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int | None = None):
     """numpy (any real dtype) -> new CUDA tensor of `dtype`, through a pinned
     buffer filled by the thread pool; chunk k's DMA overlaps the conversion of
     chunk k + 1 (all copies on the current stream)."""
@@ -142,6 +143,8 @@ def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int = 4):
     pin = stage.get(tag, host.shape, dtype)
     dev = torch.empty(tuple(host.shape), dtype=dtype, device="cuda")
     n = host.shape[0]
+    if chunks is None:
+        chunks = _UPLOAD_CHUNKS
     chunks = max(1, min(chunks, n))
     bounds = [n * i // chunks for i in range(chunks + 1)]
     hp = pin.numpy()

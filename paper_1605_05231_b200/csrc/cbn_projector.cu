@@ -705,12 +705,25 @@ __global__ void k_views_nodes_z(const float2* __restrict__ z, int nb, int n_mu, 
     }
     __syncthreads();
     const int64_t per = (int64_t)n_mu * M;
-    for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
-        const int v = q >> 5, e = q & 31;
-        if (v < nb && e0 + e < n) {
+    // 256 threads: thread = (view row q / 32, node e), four view rows each; the
+    // eight loads of a thread are issued before the first is used
+    const int e = threadIdx.x & 31, v0 = threadIdx.x >> 5;
+    const bool live = e0 + e < n;
+    float2 za[4], zb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int v = v0 + 8 * i;
+        if (live && v < nb) {
+            za[i] = z[(size_t)v * per + zk[e]];
+            zb[i] = z[(size_t)v * per + zm[e]];   // conj taken below
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int v = v0 + 8 * i;
+        if (live && v < nb) {
             const GrNode g = nd[e];
-            const float2 a = z[(size_t)v * per + zk[e]];
-            const float2 b = z[(size_t)v * per + zm[e]];   // conj taken below
+            const float2 a = za[i], b = zb[i];
             // E = (a + conj b) / 2, O = (a - conj b) / (2i)
             const float2 E = make_float2(0.5f * (a.x + b.x), 0.5f * (a.y - b.y));
             const float2 O = make_float2(0.5f * (a.y + b.y), -0.5f * (a.x - b.x));
@@ -721,9 +734,10 @@ __global__ void k_views_nodes_z(const float2* __restrict__ z, int nb, int n_mu, 
         }
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < 32 * 32; q += blockDim.x) {
-        const int e = q >> 5, v = q & 31;
-        if (v < nb && e0 + e < n) out[(size_t)(e0 + e) * 32 + v] = tile[v][e];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int eo = v0 + 8 * i, v = e;
+        if (v < nb && e0 + eo < n) out[(size_t)(e0 + eo) * 32 + v] = tile[v][eo];
     }
 }
 
