@@ -146,7 +146,12 @@ def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int | None
     if chunks is None:
         chunks = _UPLOAD_CHUNKS
     chunks = max(1, min(chunks, n))
-    bounds = [n * i // chunks for i in range(chunks + 1)]
+    if chunks == 4 and n >= 16:
+        # the DMA outruns the conversion, so only the last chunk's copy is
+        # exposed: shrinking chunks (40 / 30 / 20 / 10 %) leave a short one
+        bounds = [0, n * 4 // 10, n * 7 // 10, n * 9 // 10, n]
+    else:
+        bounds = [n * i // chunks for i in range(chunks + 1)]
     hp = pin.numpy()
     for a, b in zip(bounds[:-1], bounds[1:]):
         copy(hp[a:b], host[a:b])
