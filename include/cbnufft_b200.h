@@ -224,6 +224,21 @@ int cbn_forward_project(cbn_projector* proj, const float* vol, float* frames,
  * (pipeline.py:144-145). */
 int cbn_forward_project_async(cbn_projector* proj, const float* vol, float* frames, int32_t view_lo,
                               int32_t view_hi, void* stream);
+/* Upload-overlapped input of nufft_forward_project (pipeline.py:122-147; the
+ * spectrum NUFFT's input side, nufft.py:226-231): a host that converts and
+ * copies the volume in chunks of its slowest axis calls cbn_forward_stage_volume
+ * for rows [row_lo, row_hi) of `vol` (the full device volume; ascending
+ * contiguous chunks starting at row 0, all on `stream`) as soon as the chunk
+ * is enqueued: its rows are deapodised, padded and 2D-transformed while the
+ * host converts the next chunk.  cbn_forward_project_staged_async then runs
+ * the rest of the projection on the staged volume (CBN_EINVAL unless every
+ * row has been staged; otherwise as cbn_forward_project_async).  Any other
+ * forward call discards staged rows.  CBN_EUNSUPPORTED for node-sharded plans:
+ * the caller falls back to cbn_forward_project_async. */
+int cbn_forward_stage_volume(cbn_projector* proj, const float* vol, int32_t row_lo, int32_t row_hi,
+                             void* stream);
+int cbn_forward_project_staged_async(cbn_projector* proj, float* frames, int32_t view_lo,
+                                     int32_t view_hi, void* stream);
 int cbn_projector_blocks(cbn_projector* proj, int32_t* view_lo, int32_t* view_hi, int32_t* count);
 int cbn_projector_block_sync(cbn_projector* proj, int32_t k);
 int cbn_forward_finish(cbn_projector* proj, void* stream);

@@ -73,6 +73,32 @@ def gather_frames(dst: np.ndarray, arrays) -> None:
         f.result()
 
 
+def frame_pointers(arrays, shape):
+    """ctypes pointer table of a list of equally shaped contiguous float64
+    frames (one pass over the list), or None when any frame needs the general
+    route; `gather_block` then converts ranges of it natively."""
+    import ctypes
+    arrs = [np.asarray(a) for a in arrays]
+    shape = tuple(shape)
+    for a in arrs:
+        if a.dtype != np.float64 or not a.flags.c_contiguous or a.shape != shape:
+            return None
+    table = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    table._keep = arrs      # the arrays stay alive with the table
+    return table
+
+
+def gather_block(dst: np.ndarray, table, lo: int, hi: int) -> None:
+    """dst[k - lo] = float32(frame k) for lo <= k < hi, frames given by a
+    `frame_pointers` table; dst is a contiguous float32 block."""
+    import ctypes
+    from . import _lib
+    elems = int(dst[0].size) if hi > lo else 0
+    ptr = ctypes.c_void_p(ctypes.addressof(table) + lo * ctypes.sizeof(ctypes.c_void_p))
+    _lib.check(_lib.load().cbn_host_gather_f64_to_f32(ptr, hi - lo, elems, dst.ctypes.data, 0),
+               "host conversion")
+
+
 def copy(dst: np.ndarray, src: np.ndarray, min_chunk: int = 1 << 18) -> None:
     """dst[...] = src (with dtype conversion), split along axis 0 over threads."""
     if _native_convert(dst, src):
@@ -135,10 +161,13 @@ class Staging:
         return b
 
 
-def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int | None = None):
+def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int | None = None,
+           on_chunk=None):
     """numpy (any real dtype) -> new CUDA tensor of `dtype`, through a pinned
     buffer filled by the thread pool; chunk k's DMA overlaps the conversion of
-    chunk k + 1 (all copies on the current stream)."""
+    chunk k + 1 (all copies on the current stream).  `on_chunk(dev, a, b)` runs
+    after rows [a, b) have been enqueued (device work on them can follow on the
+    same stream while the host converts the next chunk)."""
     import torch
     pin = stage.get(tag, host.shape, dtype)
     dev = torch.empty(tuple(host.shape), dtype=dtype, device="cuda")
@@ -156,6 +185,8 @@ def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int | None
     for a, b in zip(bounds[:-1], bounds[1:]):
         copy(hp[a:b], host[a:b])
         dev[a:b].copy_(pin[a:b], non_blocking=True)
+        if on_chunk is not None:
+            on_chunk(dev, a, b)
     return dev
 
 
@@ -215,7 +246,11 @@ def download(stage: Staging, tag: str, dev, out_dtype=np.float64, chunks: int = 
     out = stage.result(tag, tuple(dev.shape), out_dtype)
     n = dev.shape[0]
     chunks = max(1, min(chunks, n))
-    bounds = [n * i // chunks for i in range(chunks + 1)]
+    if chunks == 4 and n >= 16:
+        # only the last chunk's conversion is exposed: shrinking chunks
+        bounds = [0, n * 4 // 10, n * 7 // 10, n * 9 // 10, n]
+    else:
+        bounds = [n * i // chunks for i in range(chunks + 1)]
     s = torch.cuda.current_stream()
     events = []
     for a, b in zip(bounds[:-1], bounds[1:]):

@@ -99,6 +99,8 @@ _SIGS = {
     "cbn_projector_scratch_bytes": (ctypes.c_int, [c_vp, P_i64]),
     "cbn_forward_project": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_forward_project_async": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "cbn_forward_stage_volume": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "cbn_forward_project_staged_async": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
     "cbn_projector_blocks": (ctypes.c_int, [c_vp, P_i32, P_i32, P_i32]),
     "cbn_projector_block_sync": (ctypes.c_int, [c_vp, c_i32]),
     "cbn_forward_finish": (ctypes.c_int, [c_vp, c_vp]),

@@ -1111,9 +1111,9 @@ bool spec_records_off() {   // CBN_SPEC_RECORDS=0: node generation per step (A/B
     return e && e[0] == '0';
 }
 
-void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum = nullptr,
-                        int part = 0, int nparts = 1, float2* lat = nullptr,
-                        bool raw_only = false) {
+// buffers, cached scaling, pad tables and the compact pad lists of the spectrum
+// NUFFT's input side (everything ahead of the pad kernel)
+void spectrum_setup(P* p, cudaStream_t s, RemapAxis (&rax)[3]) {
     const RadialTables& r = p->frad;
     const AxisPlan* ax = p->fspec;
     const int64_t M = r.nodes();
@@ -1123,7 +1123,6 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     p->lattice.ensure((size_t)M);
     const int smax = n;
     p->s32.ensure(3 * (size_t)smax);
-    RemapAxis rax[3];
     {
         StageScope st(p->timer, "spectrum_fit", s);
         if (!p->fspec_fit) {
@@ -1142,7 +1141,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     // the deapodised, padded volume is real: R2C to the half spectrum (the
     // gather reads k2 > K2/2 as conj(G[-k])); real grid at the front of `big`,
     // half spectrum behind it
-    long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    const long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
     const int64_t real_cells = (int64_t)kd[0] * kd[1] * kd[2];
     const int64_t half_off = (real_cells + 1) / 2;                // float2 units
     const int64_t half_cells = (int64_t)kd[0] * kd[1] * (kd[2] / 2 + 1);
@@ -1157,6 +1156,79 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         p->fspec_list.upload(all.data(), all.size(), s);
         CBN_CUDA(cudaStreamSynchronize(s));
     }
+}
+
+// Staged input of the drop-in forward call (cbn_forward_stage_volume): the
+// host converts and uploads the volume in chunks of its slowest axis, and each
+// chunk's rows are deapodised, padded and 2D-transformed as soon as they are
+// on the device, so only the last chunk's share of that work (and the pass
+// along the slowest axis) is left when the upload ends.  Rows map to grid
+// planes k = (n - N/2) mod K (pad_positions): rows >= N/2 to planes from 0,
+// rows < N/2 to the planes below K; the compact list is sorted by plane.
+void spectrum_stage_rows(P* p, const float* vol, int n_lo, int n_hi, cudaStream_t s) {
+    const AxisPlan* ax = p->fspec;
+    const int N = ax[0].N, K = ax[0].K, h = N / 2;
+    CBN_REQUIRE(K >= N && p->fspec_nl[0] == N, "staged input needs one grid plane per volume row");
+    const long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    const int64_t real_cells = (int64_t)kd[0] * kd[1] * kd[2];
+    const int64_t half_off = (real_cells + 1) / 2;
+    const long long hz = kd[2] / 2 + 1, hplane = kd[1] * hz, rplane = kd[1] * kd[2];
+    const long long k2[2] = {kd[1], kd[2]};
+    float2* half = p->big.p + half_off;
+    const float* real = reinterpret_cast<const float*>(p->big.p);
+    const int* l = p->fspec_list.p;
+    // (list index, first plane, count) of the rows below and from N/2
+    const int part[2][2] = {{std::max(n_lo, h), std::max(n_hi, h)}, {std::min(n_lo, h), std::min(n_hi, h)}};
+    for (int q = 0; q < 2; ++q) {
+        const int a = part[q][0], b = part[q][1];
+        if (b <= a) continue;
+        const int li = q == 0 ? a - h : (N - h) + a;
+        const int k0 = q == 0 ? a - h : K - h + a;
+        k_remap_list3<float, kStoreRe><<<dim3((unsigned)((p->fspec_nl[2] + 255) / 256),
+                                              p->fspec_nl[1], b - a), 256, 0, s>>>(
+            vol, p->big.p, p->fspec_rax[0], p->fspec_rax[1], p->fspec_rax[2], l + li,
+            l + p->fspec_nl[0], l + p->fspec_nl[0] + p->fspec_nl[1], p->fspec_nl[2], 1.0f);
+        CBN_LAUNCH_CHECK();
+        p->fft.exec_r2c3(p->fft.get_r2c2(k2, b - a), real + (long long)k0 * rplane,
+                         half + (long long)k0 * hplane, s);
+    }
+}
+
+void spectrum_stage_begin(P* p, cudaStream_t s) {
+    spectrum_setup(p, s, p->fspec_rax);
+    const AxisPlan* ax = p->fspec;
+    const long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    const int64_t real_cells = (int64_t)kd[0] * kd[1] * kd[2];
+    const int64_t half_off = (real_cells + 1) / 2;
+    const long long hplane = kd[1] * (kd[2] / 2 + 1);
+    float2* half = p->big.p + half_off;
+    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float) * real_cells, s));
+    int lo = 0;
+    for (const auto& rn : pad_runs(ax[0].N, ax[0].K, false)) {
+        if (rn.first > lo)
+            CBN_CUDA(cudaMemsetAsync(half + lo * hplane, 0, sizeof(float2) * hplane * (rn.first - lo), s));
+        lo = rn.second;
+    }
+    if (lo < kd[0])
+        CBN_CUDA(cudaMemsetAsync(half + lo * hplane, 0, sizeof(float2) * hplane * (kd[0] - lo), s));
+}
+
+void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum = nullptr,
+                        int part = 0, int nparts = 1, float2* lat = nullptr,
+                        bool raw_only = false, bool staged = false) {
+    const RadialTables& r = p->frad;
+    const AxisPlan* ax = p->fspec;
+    const int64_t M = r.nodes();
+    const int n = p->n_vol;
+    RemapAxis rax[3];
+    if (!staged) spectrum_setup(p, s, rax);
+    p->fspec_staged = 0;            // staged rows are consumed (or discarded) here
+    p->fspec_staged_vol = nullptr;
+    long long kd[3] = {ax[0].K, ax[1].K, ax[2].K};
+    const int64_t real_cells = (int64_t)kd[0] * kd[1] * kd[2];
+    const int64_t half_off = (real_cells + 1) / 2;                // float2 units
+    const int64_t half_cells = (int64_t)kd[0] * kd[1] * (kd[2] / 2 + 1);
+    if (!staged)
     {
         // zero the grid, then fill only the cells the pad reaches (1/8 of them)
         StageScope st(p->timer, "spectrum_pad", s);
@@ -1180,7 +1252,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
         float2* half = p->big.p + half_off;
         const float* real = reinterpret_cast<const float*>(p->big.p);
         int lo = 0;
-        for (const auto& rn : pad_runs(ax[0].N, ax[0].K, false)) {
+        for (const auto& rn : staged ? std::vector<std::pair<int, int>>() : pad_runs(ax[0].N, ax[0].K, false)) {
             if (rn.first > lo)
                 CBN_CUDA(cudaMemsetAsync(half + lo * hplane, 0,
                                          sizeof(float2) * hplane * (rn.first - lo), s));
@@ -1188,7 +1260,7 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
                              half + rn.first * hplane, s);
             lo = rn.second;
         }
-        if (lo < kd[0])
+        if (!staged && lo < kd[0])
             CBN_CUDA(cudaMemsetAsync(half + lo * hplane, 0, sizeof(float2) * hplane * (kd[0] - lo),
                                      s));
         p->fft.exec(p->fft.get_strided(kd[0], hplane, hplane, 1), half, half, CUFFT_FORWARD, s);
@@ -2370,9 +2442,9 @@ void fwd_views(P* p, float2* lat, float* frames, int lo, int hi, cudaStream_t s)
 }
 
 void forward_project(P* p, const float* vol, float* frames, int lo, int hi, cudaStream_t s,
-                     bool check = true) {
+                     bool check = true, bool staged = false) {
     build_forward(p, s);
-    radial_lattice_raw(p, vol, s);
+    radial_lattice_raw(p, vol, s, nullptr, 0, 1, nullptr, false, staged);
     project_views(p, p->lattice.p, frames, lo, hi, s, check);
 }
 
@@ -2551,6 +2623,57 @@ int cbn_forward_project_async(cbn_projector* p, const float* vol, float* frames,
             forward_project(p, vol, frames, lo, hi, static_cast<cudaStream_t>(stream), false);
         } catch (...) {
             p->track_blocks = false;
+            throw;
+        }
+        p->track_blocks = false;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int cbn_forward_stage_volume(cbn_projector* p, const float* vol, int32_t row_lo, int32_t row_hi,
+                             void* stream) {
+    try {
+        CBN_REQUIRE(p && vol, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(0 <= row_lo && row_lo < row_hi && row_hi <= p->n_vol, "row range out of bounds");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        build_forward(p, s);
+        if (p->fshard_nparts > 1 || p->fspec[0].K < p->fspec[0].N)
+            throw Error(CBN_EUNSUPPORTED, "staged volume input: plan shape not supported");
+        if (row_lo == 0) {
+            spectrum_stage_begin(p, s);
+            p->fspec_staged = 0;
+            p->fspec_staged_vol = vol;
+        }
+        CBN_REQUIRE(row_lo == p->fspec_staged && vol == p->fspec_staged_vol,
+                    "volume rows must be staged in ascending contiguous chunks from row 0");
+        spectrum_stage_rows(p, vol, row_lo, row_hi, s);
+        p->fspec_staged = row_hi;
+        return CBN_OK;
+    } catch (const std::exception& e) {
+        if (p) p->fspec_staged = 0;
+        return fail(e);
+    }
+}
+
+int cbn_forward_project_staged_async(cbn_projector* p, float* frames, int32_t lo, int32_t hi,
+                                     void* stream) {
+    try {
+        CBN_REQUIRE(p && frames, "null argument");
+        CBN_REQUIRE(p->direction & 1, "projector was not created for the forward direction");
+        CBN_REQUIRE(0 <= lo && lo < hi && hi <= p->g.n_views, "view range out of bounds");
+        CBN_REQUIRE(p->fspec_staged == p->n_vol && p->fspec_staged_vol,
+                    "the whole volume must be staged first (cbn_forward_stage_volume)");
+        p->track_blocks = true;
+        p->blk_count = 0;
+        try {
+            forward_project(p, p->fspec_staged_vol, frames, lo, hi, static_cast<cudaStream_t>(stream),
+                            false, true);
+        } catch (...) {
+            p->track_blocks = false;
+            p->fspec_staged = 0;
             throw;
         }
         p->track_blocks = false;

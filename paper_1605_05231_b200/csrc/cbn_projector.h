@@ -139,6 +139,11 @@ struct cbn_projector_s {
     cbn::DevBuf<int2> fspec_out;     // ... lattice index and its conjugate mirror's
     cbn::DevBuf<int> fspec_list, fres_list;   // compact pad positions per axis (see pad_positions)
     int fspec_nl[3] = {0, 0, 0}, fres_nl[3] = {0, 0, 0};
+    // staged spectrum input (cbn_forward_stage_volume): rows [0, fspec_staged)
+    // of fspec_staged_vol are padded and 2D-transformed already
+    cbn::RemapAxis fspec_rax[3];
+    int fspec_staged = 0;
+    const float* fspec_staged_vol = nullptr;
     // rho planes of the (views-in-lanes) resample grid the umbrella taps read
     std::vector<std::pair<int, int>> fres_rho_runs;
     // resample grid built rho-lines first: (theta, phi) pad positions with

@@ -17,6 +17,7 @@ runs in one C-ABI call per operator (``cbn_forward_project`` /
 from __future__ import annotations
 
 import ctypes
+import os
 from collections import OrderedDict
 
 import numpy as np
@@ -30,6 +31,9 @@ from .phantom import Volume3D
 _TARGET_BATCH = 1 << 20   # umbrella targets per resampling plan (pipeline.py:28)
 
 _FORWARD, _BACK = 1, 2
+# the drop-in forward call pads and 2D-transforms each uploaded chunk of the
+# volume at once (cbn_forward_stage_volume); CBN_STAGE_VOLUME=0: plain call
+_STAGE_VOLUME = os.environ.get("CBN_STAGE_VOLUME", "1") != "0"
 _CACHE: "OrderedDict[tuple, Projector]" = OrderedDict()
 _CACHE_SIZE = 2
 
@@ -465,13 +469,29 @@ def nufft_forward_project(vol: Volume3D, geom, cfg) -> list[DetectorFrame]:
     if data.shape != (proj.n,) * 3:
         raise ValueError(f"volume must be ({proj.n},)*3")
     lib = _lib.load()
-    v = _hostio.upload(proj.stage, "vol", data, torch.float32)
-    out = torch.empty((geom.n_views, geom.nu, geom.nv), dtype=torch.float32, device="cuda")
     s = proj._s
+    staged = [_STAGE_VOLUME]
+
+    def stage_rows(dev, a, b):
+        # rows [a, b) are on their way: pad and 2D-transform them while the host
+        # converts the next chunk (plans that cannot stage take the plain call)
+        if staged[0]:
+            rc = lib.cbn_forward_stage_volume(proj._h, _device.ptr(dev), a, b, s)
+            if rc == _lib.CBN_EUNSUPPORTED:
+                staged[0] = False
+            else:
+                _lib.check(rc, "nufft_forward_project")
+
+    v = _hostio.upload(proj.stage, "vol", data, torch.float32, on_chunk=stage_rows)
+    out = torch.empty((geom.n_views, geom.nu, geom.nv), dtype=torch.float32, device="cuda")
     # every kernel is enqueued at once; the frames of each reverse-Grangeat
     # block are copied out and converted while later blocks still compute
-    _lib.check(lib.cbn_forward_project_async(proj._h, _device.ptr(v), _device.ptr(out), 0,
-                                             geom.n_views, s), "nufft_forward_project")
+    if staged[0]:
+        _lib.check(lib.cbn_forward_project_staged_async(proj._h, _device.ptr(out), 0, geom.n_views,
+                                                        s), "nufft_forward_project")
+    else:
+        _lib.check(lib.cbn_forward_project_async(proj._h, _device.ptr(v), _device.ptr(out), 0,
+                                                 geom.n_views, s), "nufft_forward_project")
     blocks = proj.blocks()
     frames = _hostio.download_blocks(
         proj.stage, "frames", out, blocks,
@@ -506,8 +526,12 @@ def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volu
     # on block k while the host converts block k + 1
     bounds = list(range(0, V, _BP_STAGE_VIEWS)) + [V]
     staged = True
+    table = _hostio.frame_pointers([f.data for f in frames], shape[1:])
     for a, b in zip(bounds[:-1], bounds[1:]):
-        _hostio.gather_frames(host[a:b], [frames[k].data for k in range(a, b)])
+        if table is not None:
+            _hostio.gather_block(host[a:b], table, a, b)
+        else:
+            _hostio.gather_frames(host[a:b], [frames[k].data for k in range(a, b)])
         dev[a:b].copy_(pin[a:b], non_blocking=True)
         if staged:
             rc = lib.cbn_backproject_stage_views(proj._h, _device.ptr(dev[a]), a, b, s)
@@ -516,9 +540,11 @@ def nufft_backproject(frames, geom, cfg, out_size: int, voxel_mm: float) -> Volu
             else:
                 _lib.check(rc, "nufft_backproject")
     vol = proj.backproject(dev)
-    if not bool(torch.isfinite(vol).all()):
+    finite = torch.isfinite(vol).all()      # read after the download is under way
+    out = _hostio.download(proj.stage, "vol", vol)
+    if not bool(finite):
         raise ValueError("volume contains non-finite values")
-    return Volume3D._checked(_hostio.download(proj.stage, "vol", vol), voxel_mm)
+    return Volume3D._checked(out, voxel_mm)
 
 
 def calibrate_normalization(geom, n: int, cfg, voxel_mm: float) -> float:

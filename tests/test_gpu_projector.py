@@ -172,6 +172,39 @@ def test_repeated_calls_use_cached_plan_data(pl, golden_n16):
     assert rel_l2(b2, b1) < 1e-6 and rel_l2(b2, g["bp"]) < TOL
 
 
+def test_staged_volume_upload_matches_plain_call(pl, golden_n16, golden_n12, monkeypatch):
+    """The drop-in forward pads and 2D-transforms each uploaded chunk of the
+    volume at once (cbn_forward_stage_volume + cbn_forward_project_staged_async);
+    the frames equal those of the plain call, for even and odd chunk splits, and
+    the staged entry point refuses a volume that was not staged in full."""
+    import torch
+    from paper_1605_05231_b200 import _device, _hostio, _lib
+    from paper_1605_05231_b200.phantom import Volume3D
+    for g, basis in ((golden_n16, "trilinear"), (golden_n12, "dirac")):
+        n, views = int(g["n"]), int(g["views"])
+        geom, voxel, spec, cfg = small_setup(n, views, basis)
+        vol = Volume3D(g["vol"], voxel)
+        monkeypatch.setattr(pl, "_STAGE_VOLUME", False)
+        plain = np.stack([f.data for f in pl.nufft_forward_project(vol, geom, cfg)])
+        monkeypatch.setattr(pl, "_STAGE_VOLUME", True)
+        for chunks in (4, 3, 1):
+            monkeypatch.setattr(_hostio, "_UPLOAD_CHUNKS", chunks)
+            staged = np.stack([f.data for f in pl.nufft_forward_project(vol, geom, cfg)])
+            assert rel_l2(staged, plain) < 1e-6, (n, chunks)
+            assert rel_l2(staged, g["frames"]) < TOL
+    # misuse: rows staged out of order / not in full
+    geom, voxel, spec, cfg = small_setup()
+    proj = pl.get_projector(geom, cfg, 16, voxel, pl._FORWARD)
+    lib = _lib.load()
+    v = torch.zeros((16, 16, 16), dtype=torch.float32, device="cuda")
+    out = torch.empty((geom.n_views, geom.nu, geom.nv), dtype=torch.float32, device="cuda")
+    assert lib.cbn_forward_stage_volume(proj._h, _device.ptr(v), 4, 8, proj._s) == _lib.CBN_EINVAL
+    assert lib.cbn_forward_stage_volume(proj._h, _device.ptr(v), 0, 8, proj._s) == _lib.CBN_OK
+    assert lib.cbn_forward_project_staged_async(proj._h, _device.ptr(out), 0, geom.n_views,
+                                                proj._s) == _lib.CBN_EINVAL
+    torch.cuda.synchronize()
+
+
 def test_view_range_matches_full(pl, golden_n16):
     """Sharded view ranges (multi-GPU path) reproduce the full projection."""
     g = golden_n16

@@ -32,3 +32,34 @@ def test_copy_widen_and_narrow():
     out = np.empty(6, np.float32)
     _hostio.copy(out, special)
     assert np.array_equal(out, special.astype(np.float32), equal_nan=True)
+
+
+def test_frame_pointer_table_blocks():
+    """The backprojector's pointer table: ranges of it convert like numpy's
+    cast; a frame of another dtype, shape or layout sends the caller to the
+    general route."""
+    rng = np.random.default_rng(2)
+    frames = [rng.standard_normal((19, 23)) for _ in range(11)]
+    table = _hostio.frame_pointers(frames, (19, 23))
+    assert table is not None
+    dst = np.zeros((11, 19, 23), np.float32)
+    _hostio.gather_block(dst[0:4], table, 0, 4)
+    _hostio.gather_block(dst[4:11], table, 4, 11)
+    assert np.array_equal(dst, np.stack(frames).astype(np.float32))
+    assert _hostio.frame_pointers(frames[:3] + [frames[3].astype(np.float32)], (19, 23)) is None
+    assert _hostio.frame_pointers([f[:, ::2] for f in frames], (19, 12)) is None
+    assert _hostio.frame_pointers(frames, (19, 24)) is None
+
+
+def test_widen_unaligned_and_odd_lengths():
+    """The streaming-store widening handles any destination alignment and tail."""
+    rng = np.random.default_rng(3)
+    base_src = rng.standard_normal(100_003).astype(np.float32)
+    base_dst = np.empty(100_010, np.float64)
+    for off in range(5):
+        for n in (0, 1, 7, 8, 9, 16_385, 99_990):
+            src = base_src[off:off + n]
+            dst = base_dst[off:off + n]
+            dst[...] = -1.0
+            _hostio.copy(dst, src)
+            assert np.array_equal(dst, src.astype(np.float64))

@@ -16,18 +16,25 @@ for _ in range(3):
     pl.nufft_forward_project(vol, geom, cfg)
 lib = _lib.load()
 T = time.perf_counter
-for rep in range(4):
+for rep in range(6):
+    stage = rep % 2 == 1          # odd reps: chunks staged as they are uploaded
     marks = []
     t0 = T()
     data = np.asarray(vol.data)
     proj = pl.get_projector(geom, cfg, data.shape[0], vol.voxel_mm, pl._FORWARD)
+    s = proj._s
     marks.append(("plan lookup", T()))
-    v = _hostio.upload(proj.stage, "vol", data, torch.float32)
+
+    def on_chunk(dev, a, b):
+        _lib.check(lib.cbn_forward_stage_volume(proj._h, _device.ptr(dev), a, b, s), "x")
+    v = _hostio.upload(proj.stage, "vol", data, torch.float32, on_chunk=on_chunk if stage else None)
     marks.append(("upload enqueued", T()))
     out = torch.empty((geom.n_views, geom.nu, geom.nv), dtype=torch.float32, device="cuda")
-    s = proj._s
-    _lib.check(lib.cbn_forward_project_async(proj._h, _device.ptr(v), _device.ptr(out), 0, geom.n_views, s), "x")
-    marks.append(("project enqueued", T()))
+    if stage:
+        _lib.check(lib.cbn_forward_project_staged_async(proj._h, _device.ptr(out), 0, geom.n_views, s), "x")
+    else:
+        _lib.check(lib.cbn_forward_project_async(proj._h, _device.ptr(v), _device.ptr(out), 0, geom.n_views, s), "x")
+    marks.append(("project enqueued (staged)" if stage else "project enqueued", T()))
     blocks = proj.blocks()
     waits = []
     def wait(k):
