@@ -27,6 +27,14 @@ bool bulk_flush_enabled() {
     return on;
 }
 
+bool bulk_fill_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CBN_BULK_FILL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
 __global__ void k_bin_scatter(const int* __restrict__ keys, int64_t m, int* __restrict__ cursor,
                               int* __restrict__ perm) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

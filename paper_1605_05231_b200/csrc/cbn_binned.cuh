@@ -43,7 +43,8 @@ struct TileGeom {
     int nb[3];       // bins per axis
     int K[3];        // grid extent per axis
     int P;           // shared-memory pitch of the last axis (>= R[D-1])
-    int bulk;        // 3D spread: flush region rows with TMA bulk reductions
+    int bulk;        // 3D: bit 0 = spread flushes region rows with TMA bulk reductions,
+                     // bit 1 = gather fills its tile with TMA bulk copies
 };
 
 // Shared -> global bulk reduction of one contiguous run of floats (TMA,
@@ -53,6 +54,35 @@ CBN_D void bulk_red_add_f32(void* gdst, const void* ssrc, unsigned bytes) {
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
                  "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes)
                  : "memory");
+}
+
+// Global -> shared bulk copy (TMA, UBLKCP) completing on an mbarrier: 16-byte
+// aligned on both sides, size a multiple of 16 bytes.
+CBN_D void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+CBN_D void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)), "r"(bytes)
+                 : "memory");
+}
+CBN_D void bulk_copy_g2s(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(gsrc), "r"(bytes),
+        "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+CBN_D void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+        "r"(phase)
+        : "memory");
 }
 
 template <int D>
@@ -121,7 +151,8 @@ template <int D, int J, class Src, class Epi, bool HALF = false>
 __global__ void __launch_bounds__(256, 3)   // <= 80 registers: 3 CTAs per SM
 k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src src, Epi epi,
                 const int* __restrict__ perm, const SubProblem* __restrict__ subs) {
-    extern __shared__ float2 tile[];
+    extern __shared__ float4 smem4[];   // 16-byte aligned: the bulk copies need it
+    float2* tile = reinterpret_cast<float2*>(smem4);
     const SubProblem sp = subs[blockIdx.x];
     if (sp.count == 0) return;   // unused slot of a device-sorted plan
     int o[3];
@@ -138,7 +169,34 @@ k_gather_binned(const float2* __restrict__ grid, KBSet kb, TileGeom<D> tg, Src s
         const bool neg = lane < R2 && wrapc(o[2] + lane, tg.K[2]) >= tg.K[2] / 2 + 1;
         negmask = __ballot_sync(0xffffffffu, neg);
     }
-    for (int e = threadIdx.x; e < nreg; e += blockDim.x) {
+    bool filled = false;
+    if constexpr (D == 3 && !HALF) {
+        if (tg.bulk & 2) {
+            // Tile rows (r0, r1) are contiguous runs of P2 cells in shared memory
+            // and, up to the wrap of the last axis, in the grid: one TMA bulk copy
+            // per run (two at the wrap) completing on an mbarrier, instead of one
+            // 8-byte cp.async per cell with its index arithmetic.
+            __shared__ unsigned long long fill_bar;
+            const int rows = R0 * R1;
+            if (threadIdx.x == 0) {
+                mbar_init(&fill_bar, 1);
+                mbar_expect_tx(&fill_bar, (unsigned)rows * (unsigned)P2 * 8u);
+            }
+            __syncthreads();
+            const int n1 = min(P2, tg.K[2] - o[2]);   // cells before the wrap
+            for (int row = threadIdx.x; row < rows; row += blockDim.x) {
+                const int r0 = dR.div(row), r1 = row - r0 * R1;
+                const float2* grow = grid + ((size_t)wrapc(o[0] + r0, tg.K[0]) * tg.K[1] +
+                                             wrapc(o[1] + r1, tg.K[1])) * tg.K[2];
+                float2* srow = tile + row * P2;
+                bulk_copy_g2s(srow, grow + o[2], (unsigned)n1 * 8u, &fill_bar);
+                if (n1 < P2) bulk_copy_g2s(srow + n1, grow, (unsigned)(P2 - n1) * 8u, &fill_bar);
+            }
+            mbar_wait(&fill_bar, 0);
+            filled = true;
+        }
+    }
+    for (int e = threadIdx.x; e < (filled ? 0 : nreg); e += blockDim.x) {
         const int r01 = dP.div(e), r2 = e - r01 * P2;
         const int r0 = dR.div(r01), r1 = r01 - r0 * R1;
         if (r2 >= R2 || (D == 2 && r1 >= tg.R[1])) continue;
@@ -587,7 +645,7 @@ k_spread_owned(float2* __restrict__ grid, KBSet kb, TileGeom<3> tg, Src src,
         }
     }
     const FastDiv dP(P), dR1(R1);
-    if (tg.bulk) {
+    if (tg.bulk & 1) {
         // Region rows (r0, r1) are contiguous runs of P cells in shared memory
         // and, up to the axis-2 wrap, in the grid (the pad cells past R2 are
         // zero): one TMA bulk reduction per run instead of one RED per cell.
@@ -842,6 +900,7 @@ void device_bins_finish(BinPlan& bp, DeviceSortScratch& sc, int64_t nbins, int m
                         cudaStream_t s);
 
 bool bulk_flush_enabled();   // CBN_BULK_FLUSH=1: TMA bulk-reduction flush of the 3D spread (A/B)
+bool bulk_fill_enabled();    // CBN_BULK_FILL=0: cp.async tile fill of the 3D gather instead of TMA bulk copies
 
 // pitch_pad: store the last region axis with pitch = J (mod 16) (required by
 // k_spread_owned; harmless for the gather)
@@ -872,9 +931,9 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
     bp.nreg = bp.nreg / bp.tg.R[D - 1] * bp.tg.P;
     // TMA bulk flush of the 3D spread: 16-byte aligned row runs on both sides
     // and at most one wrap along the last axis
-    bp.tg.bulk = D == 3 && pitch_pad && bulk_flush_enabled() && bp.tg.P % 2 == 0 &&
-                 bp.tg.T[2] % 2 == 0 && bp.tg.K[2] % 2 == 0 && bp.tg.P <= bp.tg.K[2] &&
-                 bp.tg.K[2] % bp.tg.T[2] == 0;
+    const bool bulk_ok = D == 3 && pitch_pad && bp.tg.P % 2 == 0 && bp.tg.T[2] % 2 == 0 &&
+                         bp.tg.K[2] % 2 == 0 && bp.tg.P <= bp.tg.K[2] && bp.tg.K[2] % bp.tg.T[2] == 0;
+    bp.tg.bulk = bulk_ok ? (bulk_flush_enabled() ? 1 : 0) | (bulk_fill_enabled() ? 2 : 0) : 0;
     if (dev) {
         DeviceSortScratch& sc = *dev;
         sc.keys.ensure((size_t)m);
