@@ -788,7 +788,8 @@ constexpr int kInterleaveMax = 4096;
 template <int D, int J, class Src>
 __global__ void __launch_bounds__(256)
 k_bin_interleave(Src src, KBSet kb, TileGeom<D> tg, int* __restrict__ perm,
-                 const SubProblem* __restrict__ subs) {
+                 const SubProblem* __restrict__ subs, const float* __restrict__ raw32 = nullptr,
+                 float* __restrict__ sorted32 = nullptr) {
     __shared__ int ids[kInterleaveMax];
     __shared__ short rank[kInterleaveMax];
     __shared__ unsigned char res[kInterleaveMax];
@@ -847,6 +848,14 @@ k_bin_interleave(Src src, KBSet kb, TileGeom<D> tg, int* __restrict__ perm,
 #pragma unroll
         for (int rr = 0; rr < 16; ++rr) pos += min(cnt[rr], q) + (rr < r && cnt[rr] > q ? 1 : 0);
         perm[sp.start + pos] = ids[k];
+        // float32 node sets keep a bin-ordered copy of the coordinates: written
+        // here, while the subproblem's nodes (read above) are still in L1 / L2,
+        // instead of by a separate pass of random reads
+        if (sorted32) {
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                sorted32[(size_t)(sp.start + pos) * D + d] = __ldg(raw32 + (size_t)ids[k] * D + d);
+        }
     }
 }
 
@@ -907,7 +916,8 @@ bool bulk_fill_enabled();    // CBN_BULK_FILL=0: cp.async tile fill of the 3D ga
 template <int D, int J, class Src>
 void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const int* tile,
                 int max_sub, cudaStream_t s, bool pitch_pad = false,
-                DeviceSortScratch* dev = nullptr) {
+                DeviceSortScratch* dev = nullptr, const float* raw32 = nullptr,
+                float* sorted32 = nullptr) {
     CBN_REQUIRE(max_sub <= kInterleaveMax, "subproblem size above the interleave limit");
     bp.D = D;
     bp.J = J;
@@ -944,7 +954,7 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
         CBN_LAUNCH_CHECK();
         device_bins_finish(bp, sc, nbins, max_sub, s);
         k_bin_interleave<D, J, Src><<<bp.nsubs, 256, 0, s>>>(src, kb, bp.geom<D>(), bp.perm.p,
-                                                             bp.subs.p);
+                                                             bp.subs.p, raw32, sorted32);
         CBN_LAUNCH_CHECK();
         return;
     }
@@ -955,7 +965,8 @@ void build_bins(BinPlan& bp, const Src& src, const KBSet& kb, int64_t m, const i
     CBN_LAUNCH_CHECK();
     finish_bins(bp, keys, counts, nbins, max_sub, s);
     if (bp.nsubs > 0) {
-        k_bin_interleave<D, J, Src><<<bp.nsubs, 256, 0, s>>>(src, kb, bp.geom<D>(), bp.perm.p, bp.subs.p);
+        k_bin_interleave<D, J, Src><<<bp.nsubs, 256, 0, s>>>(src, kb, bp.geom<D>(), bp.perm.p, bp.subs.p,
+                                                             raw32, sorted32);
         CBN_LAUNCH_CHECK();
     }
 }

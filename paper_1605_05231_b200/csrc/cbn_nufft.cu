@@ -41,15 +41,6 @@ struct ExplicitSrc {
     }
 };
 
-// sorted[pos] = nodes[perm[pos]] (D floats per node)
-__global__ void k_sort_nodes(const float* __restrict__ nodes, const int* __restrict__ perm,
-                             int64_t m, int D, float* __restrict__ sorted) {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= m) return;
-    const int64_t i = perm[q];
-    for (int d = 0; d < D; ++d) sorted[q * D + d] = nodes[i * D + d];
-}
-
 // plan.phase = exp(-i w . (N//2))  (nufft.py:215-216), angle in float64
 template <int D>
 struct PhaseOut {
@@ -254,16 +245,15 @@ void sort_plan(cbn_nufft* p, cudaStream_t s) {
         p->timer.add_bytes("sort", p->m * (2.0 * cb + 8.0 + 8.0 + (p->nodes.p ? 0.0 : 2.0 * cb)), 0.0);
     }
     StageScope st(p->timer, "sort", s);
+    // float32 node sets: the interleave pass also writes the bin-ordered copy
+    // of the coordinates (sorted32[pos] = nodes32[perm[pos]])
+    if (!p->nodes.p) p->sorted32.ensure((size_t)p->m * D);
     dispatch_j(p->J, [&](auto jc) {
-        build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true, &p->sort);
+        build_bins<D, decltype(jc)::value>(p->bins, src, p->kb, p->m, tile, 1024, s, true, &p->sort,
+                                           p->nodes.p ? nullptr : p->nodes32.p,
+                                           p->nodes.p ? nullptr : p->sorted32.p);
         return 0;
     });
-    if (!p->nodes.p) {
-        p->sorted32.ensure((size_t)p->m * D);
-        k_sort_nodes<<<blocks_for(p->m, 256), 256, 0, s>>>(p->nodes32.p, p->bins.perm.p, p->m, D,
-                                                           p->sorted32.p);
-        CBN_LAUNCH_CHECK();
-    }
 }
 
 template <int D>
