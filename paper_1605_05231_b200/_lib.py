@@ -15,9 +15,11 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# CBN_LIB=check loads the bounds-checked build (csrc/Makefile target `check`)
-LIB_PATH = os.path.join(_HERE, "libcbnufft_b200_check.so" if os.environ.get("CBN_LIB") == "check"
-                        else "libcbnufft_b200.so")
+# CBN_LIB=check loads the bounds-checked build (csrc/Makefile target `check`);
+# CBN_LIB=<name>.so another build of the library in this directory (A/B variants)
+_ALT = os.environ.get("CBN_LIB", "")
+LIB_PATH = os.path.join(_HERE, "libcbnufft_b200_check.so" if _ALT == "check"
+                        else _ALT if _ALT.endswith(".so") else "libcbnufft_b200.so")
 
 CBN_OK, CBN_EINVAL, CBN_ECUDA, CBN_ENOMEM, CBN_ENONFINITE, CBN_ENCCL, CBN_EUNSUPPORTED = range(7)
 
