@@ -608,7 +608,13 @@ def measure_nufft4(args, d: Dist):
     if dom in st_t:
         kk = st_t[dom]
         roofline = {"kernel": dom, "bound": "hbm", "achieved": kk["achieved_gbs"], "peak": peak,
-                    "unit": "GB/s", "frac": kk["hbm_frac"], "traffic": None,
+                    "unit": "GB/s", "frac": kk["hbm_frac"],
+                    # ncu dram bytes of the 100 M-point launch (profiles/r2z_c4_*): the
+                    # excess over the algorithmic bytes is the caller-order value /
+                    # result access (4.72e9 / 3.98e9 with bin-ordered points,
+                    # profiles/r2y_c4_presort_traffic.txt)
+                    "traffic": ({"spread": 17.38e9, "gather": 9.93e9}[dom]
+                                if m == 100_000_000 else None),
                     "peak_kind": peak_kind, "algorithmic_bytes_per_step": kk["hbm_bytes"],
                     "onchip_tbs": kk["onchip_tbs"], "onchip_frac": kk["onchip_frac"]}
     cpu = None
