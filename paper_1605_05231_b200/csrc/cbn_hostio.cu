@@ -13,7 +13,21 @@
 
 namespace {
 
-int team(int32_t threads) { return threads > 0 ? threads : omp_get_max_threads(); }
+// Conversion team: all cores but two by default.  The calling thread spins on
+// CUDA events, a second host thread feeds the copies, and the driver has its
+// own threads; with one conversion thread per core, a descheduled team member
+// stalled whole calls (20 drop-in forward calls at config 2 on 16 cores:
+// median 13.3 ms, worst 17-31 ms with 16 threads; median 12.8-13.0 ms, worst
+// 13.2 ms with 14).  OMP_NUM_THREADS below that still wins.
+int team(int32_t threads) {
+    if (threads > 0) return threads;
+    static const int n = [] {
+        const int hw = omp_get_num_procs(), m = omp_get_max_threads();
+        const int want = hw > 4 ? hw - 2 : hw;
+        return m < want ? (m > 0 ? m : 1) : want;
+    }();
+    return n;
+}
 
 // float32 -> float64 with non-temporal stores: the result (2x the input) is
 // written once and not read back by this code, so the lines skip the
