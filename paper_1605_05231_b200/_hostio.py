@@ -190,17 +190,20 @@ def upload(stage: Staging, tag: str, host: np.ndarray, dtype, chunks: int | None
     return dev
 
 
-def download_blocks(stage: Staging, tag: str, dev, blocks, wait, out_dtype=np.float64):
+def download_blocks(stage: Staging, tag: str, dev, blocks, wait, out_dtype=np.float64, out=None):
     """CUDA tensor -> numpy array while it is still being produced: for each
     block (lo, hi) of axis 0, in order, `wait(k)` returns once block k is
     complete on the device; its rows are then copied to a pinned buffer on a
     copy stream, and a converter thread turns each landed block into the
-    result dtype on the pool while later blocks still compute."""
+    result dtype on the pool while later blocks still compute.  `out`: the
+    result array, when the caller took it from `stage.result` beforehand (to
+    build its views while the device is still busy)."""
     import queue
     import torch
     pin = stage.get(tag, dev.shape, dev.dtype)
     host = pin.numpy()
-    out = stage.result(tag, tuple(dev.shape), out_dtype)
+    if out is None:
+        out = stage.result(tag, tuple(dev.shape), out_dtype)
     cs = stage.copy_stream()
     q: "queue.Queue" = queue.Queue()
     futs = []

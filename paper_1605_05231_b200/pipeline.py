@@ -493,11 +493,16 @@ def nufft_forward_project(vol: Volume3D, geom, cfg) -> list[DetectorFrame]:
         _lib.check(lib.cbn_forward_project_async(proj._h, _device.ptr(v), _device.ptr(out), 0,
                                                  geom.n_views, s), "nufft_forward_project")
     blocks = proj.blocks()
-    frames = _hostio.download_blocks(
+    # the result array and its per-view wrappers are made while the device is
+    # still working towards the first view block
+    frames = proj.stage.result("frames", tuple(out.shape), np.float64)
+    result = [DetectorFrame._checked(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
+    _hostio.download_blocks(
         proj.stage, "frames", out, blocks,
-        lambda k: _lib.check(lib.cbn_projector_block_sync(proj._h, k), "nufft_forward_project"))
+        lambda k: _lib.check(lib.cbn_projector_block_sync(proj._h, k), "nufft_forward_project"),
+        out=frames)
     _lib.check(lib.cbn_forward_finish(proj._h, s), "nufft_forward_project")
-    return [DetectorFrame._checked(k, frames[k], geom.pixel_mm) for k in range(geom.n_views)]
+    return result
 
 
 _BP_STAGE_VIEWS = 64   # views per upload block of the drop-in backprojector

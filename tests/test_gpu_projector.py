@@ -172,6 +172,28 @@ def test_repeated_calls_use_cached_plan_data(pl, golden_n16):
     assert rel_l2(b2, b1) < 1e-6 and rel_l2(b2, g["bp"]) < TOL
 
 
+def test_results_held_by_the_caller_are_not_reused(pl, golden_n16):
+    """The plan recycles its float64 result array only when the caller has
+    dropped every frame of the previous call."""
+    from paper_1605_05231_b200.phantom import Volume3D
+    g = golden_n16
+    geom, voxel, spec, cfg = small_setup()
+    held = pl.nufft_forward_project(Volume3D(g["vol"], voxel), geom, cfg)
+    snap = np.stack([f.data for f in held]).copy()
+    other = pl.nufft_forward_project(Volume3D(2.0 * g["vol"], voxel), geom, cfg)
+    assert not np.shares_memory(other[0].data, held[0].data)
+    assert np.array_equal(np.stack([f.data for f in held]), snap)
+    assert rel_l2(np.stack([f.data for f in other]), 2.0 * snap) < 1e-6
+    del held, other
+    a = pl.nufft_forward_project(Volume3D(g["vol"], voxel), geom, cfg)
+    addr = a[0].data.__array_interface__["data"][0]
+    assert np.array_equal(np.stack([f.data for f in a]), snap)
+    del a
+    b = pl.nufft_forward_project(Volume3D(g["vol"], voxel), geom, cfg)   # released -> recycled
+    assert b[0].data.__array_interface__["data"][0] == addr
+    assert np.array_equal(np.stack([f.data for f in b]), snap)
+
+
 def test_staged_volume_upload_matches_plain_call(pl, golden_n16, golden_n12, monkeypatch):
     """The drop-in forward pads and 2D-transforms each uploaded chunk of the
     volume at once (cbn_forward_stage_volume + cbn_forward_project_staged_async);
