@@ -8,6 +8,7 @@
 #include <omp.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "cbn_runtime.h"
 
@@ -47,6 +48,33 @@ __attribute__((target("avx2"))) void widen_stream_avx2(const float* s, double* d
     _mm_sfence();
 }
 
+// float64 -> float32 with non-temporal stores (the pinned staging buffer is
+// written once and read by the DMA engine, not by this code)
+__attribute__((target("avx2"))) void narrow_stream_avx2(const double* s, float* d, int64_t n) {
+    int64_t i = 0;
+    while (i < n && (reinterpret_cast<uintptr_t>(d + i) & 31)) {
+        d[i] = (float)s[i];
+        ++i;
+    }
+    for (; i + 8 <= n; i += 8) {
+        const __m128 a = _mm256_cvtpd_ps(_mm256_loadu_pd(s + i));
+        const __m128 b = _mm256_cvtpd_ps(_mm256_loadu_pd(s + i + 4));
+        _mm256_stream_ps(d + i, _mm256_set_m128(b, a));
+    }
+    for (; i < n; ++i) d[i] = (float)s[i];
+    _mm_sfence();
+}
+
+bool narrow_stream_on() {
+    static const bool on = [] {
+        // on by default (drop-in forward call 12.76 / 12.94 -> 12.46 / 12.43 ms on
+        // the GPU box's 16 cores); CBN_NT_NARROW=0 keeps the plain loop
+        const char* e = std::getenv("CBN_NT_NARROW");
+        return !(e && e[0] == '0') && __builtin_cpu_supports("avx2");
+    }();
+    return on;
+}
+
 }  // namespace
 
 extern "C" {
@@ -68,6 +96,10 @@ int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t 
             const int64_t lo = b * B, hi = lo + B < elems ? lo + B : elems;
             const double* s = src[k];
             float* d = dst + k * elems;
+            if (narrow_stream_on()) {
+                narrow_stream_avx2(s + lo, d + lo, hi - lo);
+                continue;
+            }
             for (int64_t i = lo; i < hi; ++i) d[i] = (float)s[i];
         }
         return CBN_OK;
