@@ -85,9 +85,9 @@ int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t 
     try {
         CBN_REQUIRE(src && dst && n_src >= 0 && elems >= 0, "bad argument");
         for (int64_t k = 0; k < n_src; ++k) CBN_REQUIRE(src[k], "null source array");
-        // blocks of 64 Ki elements across all arrays, so a few large frames
-        // and many small ones both spread over the team
-        constexpr int64_t B = 1 << 16;
+        // blocks of 16 Ki elements across all arrays, so a few large frames
+        // and many small ones both spread evenly over the team
+        constexpr int64_t B = 1 << 14;
         const int64_t per = (elems + B - 1) / B;
         const int64_t tasks = n_src * per;
 #pragma omp parallel for schedule(static) num_threads(team(threads))
