@@ -87,10 +87,12 @@ int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t 
         for (int64_t k = 0; k < n_src; ++k) CBN_REQUIRE(src[k], "null source array");
         // blocks of 16 Ki elements across all arrays, so a few large frames
         // and many small ones both spread evenly over the team
+        // (dynamic schedule: a thread that loses its core for a moment holds
+        // back one 16 Ki task, not a fixed share of the array)
         constexpr int64_t B = 1 << 14;
         const int64_t per = (elems + B - 1) / B;
         const int64_t tasks = n_src * per;
-#pragma omp parallel for schedule(static) num_threads(team(threads))
+#pragma omp parallel for schedule(dynamic, 1) num_threads(team(threads))
         for (int64_t t = 0; t < tasks; ++t) {
             const int64_t k = t / per, b = t - k * per;
             const int64_t lo = b * B, hi = lo + B < elems ? lo + B : elems;
@@ -115,7 +117,7 @@ int cbn_host_f32_to_f64(const float* src, double* dst, int64_t n, int32_t thread
         constexpr int64_t B = 1 << 14;
         const int64_t tasks = (n + B - 1) / B;
         static const bool avx2 = __builtin_cpu_supports("avx2");
-#pragma omp parallel for schedule(static) num_threads(team(threads))
+#pragma omp parallel for schedule(dynamic, 1) num_threads(team(threads))
         for (int64_t t = 0; t < tasks; ++t) {
             const int64_t lo = t * B, hi = lo + B < n ? lo + B : n;
             if (avx2) {
