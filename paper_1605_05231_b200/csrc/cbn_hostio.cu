@@ -75,6 +75,26 @@ bool narrow_stream_on() {
     return on;
 }
 
+// tasks 0..tasks-1 over the team.  Calls of a few million elements (the
+// chunks and view blocks of the projector calls, ~1 ms each) take tasks
+// dynamically: a thread that loses its core for a moment then holds back one
+// 16 Ki task, not a fixed share of the array (it removed the stalled calls of
+// the drop-in operators).  Large arrays (config 4's 10^8 values) keep the
+// static split, whose long contiguous runs per thread stream faster (800-830
+// against 630 Msamples/s through the numpy API).
+constexpr int64_t kDynamicBelowTasks = 2048;   // 32 Mi elements
+
+template <class Body>
+void for_tasks(int64_t tasks, int32_t threads, Body body) {
+    if (tasks < kDynamicBelowTasks) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(team(threads))
+        for (int64_t t = 0; t < tasks; ++t) body(t);
+    } else {
+#pragma omp parallel for schedule(static) num_threads(team(threads))
+        for (int64_t t = 0; t < tasks; ++t) body(t);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -87,23 +107,21 @@ int cbn_host_gather_f64_to_f32(const double* const* src, int64_t n_src, int64_t 
         for (int64_t k = 0; k < n_src; ++k) CBN_REQUIRE(src[k], "null source array");
         // blocks of 16 Ki elements across all arrays, so a few large frames
         // and many small ones both spread evenly over the team
-        // (dynamic schedule: a thread that loses its core for a moment holds
-        // back one 16 Ki task, not a fixed share of the array)
         constexpr int64_t B = 1 << 14;
         const int64_t per = (elems + B - 1) / B;
         const int64_t tasks = n_src * per;
-#pragma omp parallel for schedule(dynamic, 1) num_threads(team(threads))
-        for (int64_t t = 0; t < tasks; ++t) {
+        const bool stream = narrow_stream_on();
+        for_tasks(tasks, threads, [=](int64_t t) {
             const int64_t k = t / per, b = t - k * per;
             const int64_t lo = b * B, hi = lo + B < elems ? lo + B : elems;
             const double* s = src[k];
             float* d = dst + k * elems;
-            if (narrow_stream_on()) {
+            if (stream) {
                 narrow_stream_avx2(s + lo, d + lo, hi - lo);
-                continue;
+                return;
             }
             for (int64_t i = lo; i < hi; ++i) d[i] = (float)s[i];
-        }
+        });
         return CBN_OK;
     } catch (const std::exception& e) {
         return cbn::fail(e);
@@ -117,15 +135,14 @@ int cbn_host_f32_to_f64(const float* src, double* dst, int64_t n, int32_t thread
         constexpr int64_t B = 1 << 14;
         const int64_t tasks = (n + B - 1) / B;
         static const bool avx2 = __builtin_cpu_supports("avx2");
-#pragma omp parallel for schedule(dynamic, 1) num_threads(team(threads))
-        for (int64_t t = 0; t < tasks; ++t) {
+        for_tasks(tasks, threads, [=](int64_t t) {
             const int64_t lo = t * B, hi = lo + B < n ? lo + B : n;
             if (avx2) {
                 widen_stream_avx2(src + lo, dst + lo, hi - lo);
-                continue;
+                return;
             }
             for (int64_t i = lo; i < hi; ++i) dst[i] = (double)src[i];
-        }
+        });
         return CBN_OK;
     } catch (const std::exception& e) {
         return cbn::fail(e);
