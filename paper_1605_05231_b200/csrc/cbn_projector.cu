@@ -1202,7 +1202,10 @@ void spectrum_stage_begin(P* p, cudaStream_t s) {
     const int64_t half_off = (real_cells + 1) / 2;
     const long long hplane = kd[1] * (kd[2] / 2 + 1);
     float2* half = p->big.p + half_off;
-    CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float) * real_cells, s));
+    // only the x planes the pad reaches are transformed: zero those
+    for (const auto& rn : pad_runs(ax[0].N, ax[0].K, false))
+        CBN_CUDA(cudaMemsetAsync(reinterpret_cast<float*>(p->big.p) + rn.first * kd[1] * kd[2], 0,
+                                 sizeof(float) * kd[1] * kd[2] * (rn.second - rn.first), s));
     int lo = 0;
     for (const auto& rn : pad_runs(ax[0].N, ax[0].K, false)) {
         if (rn.first > lo)
@@ -1232,9 +1235,15 @@ void radial_lattice_raw(P* p, const float* vol, cudaStream_t s, float2* spectrum
     {
         // zero the grid, then fill only the cells the pad reaches (1/8 of them)
         StageScope st(p->timer, "spectrum_pad", s);
-        CBN_CUDA(cudaMemsetAsync(p->big.p, 0, sizeof(float) * real_cells, s));
-        // zero the real grid, read the volume, write its N^3 cells
-        p->timer.add_bytes("spectrum_pad", 4.0 * real_cells + 8.0 * (double)n * n * n, 0.0);
+        // only the x planes the pad reaches are transformed: zero those
+        double zeroed = 0.0;
+        for (const auto& rn : pad_runs(ax[0].N, ax[0].K, false)) {
+            CBN_CUDA(cudaMemsetAsync(reinterpret_cast<float*>(p->big.p) + rn.first * kd[1] * kd[2], 0,
+                                     sizeof(float) * kd[1] * kd[2] * (rn.second - rn.first), s));
+            zeroed += (double)kd[1] * kd[2] * (rn.second - rn.first);
+        }
+        // zero those planes, read the volume, write its N^3 cells
+        p->timer.add_bytes("spectrum_pad", 4.0 * zeroed + 8.0 * (double)n * n * n, 0.0);
         const int* l = p->fspec_list.p;
         k_remap_list3<float, kStoreRe><<<dim3((unsigned)((p->fspec_nl[2] + 255) / 256),
                                               p->fspec_nl[1], p->fspec_nl[0]), 256, 0, s>>>(
